@@ -1,0 +1,183 @@
+/*
+ * fxg.h -- C ABI of the B200-native featurex hot path (libfxg.so).
+ *
+ * Drop-in boundary for the reference's featurize path (featurex, /root/reference/proj):
+ * plain pointers and sizes only, no C++ or torch types.  Each entry point names
+ * the reference interface it replaces (paths relative to /root/reference/proj).
+ * The C++ host layer (include/featurex_gpu/engine.hpp) re-exposes the
+ * reference's engine.hpp signatures on top of these calls.
+ *
+ * Conventions
+ *  - Return value: FX_OK (0) or an fx_status code; fx_last_error() returns a
+ *    thread-local message for the last failure on the calling thread.
+ *  - Error codes map 1:1 onto the reference exception types
+ *    (include/featurex/errors.hpp:8-58) plus device-side failures.
+ *  - The caller owns every buffer.  The library never returns memory to free;
+ *    device scratch belongs to the fx_ctx.
+ *  - A fx_ctx is not thread-safe; distinct contexts on distinct host threads are.
+ *  - There is no CPU fallback: every fx_featurize* call runs sm_100a kernels and
+ *    fails with FX_E_CUDA when no usable device/kernel image is present.
+ */
+#ifndef FXG_H
+#define FXG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FXG_ABI_VERSION 1
+
+typedef enum fx_status {
+    FX_OK = 0,
+    FX_E_CONFIG = 1,          /* featurex::ConfigError    (errors.hpp:56-58) */
+    FX_E_UNKNOWN_PROFILE = 2, /* featurex::UnknownProfile (errors.hpp:48-50) */
+    FX_E_PAIRING = 3,         /* featurex::PairingError   (errors.hpp:16-18) */
+    FX_E_IO = 4,              /* featurex::IoError        (errors.hpp:8-10)  */
+    FX_E_FORMAT = 5,          /* featurex::FormatError    (errors.hpp:12-14) */
+    FX_E_ZERO_MASS = 6,       /* featurex::ZeroMassError  (errors.hpp:24-26) */
+    FX_E_CUDA = 7,            /* CUDA runtime / launch failure, no device     */
+    FX_E_OOM = 8,             /* device or pinned allocation failed           */
+    FX_E_NCCL = 9,            /* collective failure (sharded entry points)    */
+    FX_E_CAPACITY = 10,       /* caller's output buffer too small             */
+    FX_E_ARG = 11,            /* invalid argument (null pointer, bad size)    */
+    FX_E_INTERNAL = 12
+} fx_status;
+
+typedef enum fx_mem_kind { FX_MEM_HOST = 0, FX_MEM_DEVICE = 1 } fx_mem_kind;
+
+/* Feature group bits, canonical order of engine.cpp:22-23. */
+#define FX_GROUP_INTENSITY 0x01u
+#define FX_GROUP_SHAPE 0x02u
+#define FX_GROUP_MOMENTS 0x04u
+#define FX_GROUP_GLCM 0x08u
+#define FX_GROUP_GLRLM 0x10u
+#define FX_GROUP_GLSZM 0x20u
+#define FX_GROUP_NGTDM 0x40u
+#define FX_GROUP_ALL 0x7Fu
+/* Groups with device kernels in this build (others return FX_E_CONFIG). */
+#define FX_GROUP_DEVICE (FX_GROUP_INTENSITY | FX_GROUP_MOMENTS | FX_GROUP_GLCM)
+
+/* TextureParams (engine.hpp:14-17) + GlcmParams (texture.hpp:30-35). */
+typedef struct fx_texture_params {
+    int ng;             /* grey levels; >= 2 (discretize, texture.cpp:30)       */
+    int offset;         /* pixel distance d                                     */
+    int n_angles;       /* number of entries used in angles[] (1..8)            */
+    int angles[8];      /* each in {0,45,90,135}; columns use sorted order      */
+    int symmetric;      /* count (b,a) with (a,b)                               */
+    int histogram_bins; /* intensity entropy/uniformity bins, max(2, bins)      */
+} fx_texture_params;
+
+/* One image pair: row-major uint16 rasters.  pitch is in elements (>= width).
+ * origin_x/origin_y are the global coordinates of pixel (0,0); raw moments and
+ * weighted centroids are reported in global coordinates (a band shard or a
+ * rasterized PixelCloud passes its offset here).  mem_kind says where the two
+ * rasters live; outputs of fx_featurize live in the same kind of memory. */
+typedef struct fx_image {
+    const uint16_t* intensity;
+    const uint16_t* labels;
+    int width;
+    int height;
+    size_t pitch;
+    int origin_x;
+    int origin_y;
+    int mem_kind;
+} fx_image;
+
+int fx_abi_version(void);
+const char* fx_last_error(void);
+
+/* ---- pure host helpers (no device) ------------------------------------- */
+
+/* resolve_profile (engine.hpp:22, engine.cpp:71-86): "default",
+ * "performance", "ibsi-like"; FX_E_UNKNOWN_PROFILE otherwise. */
+int fx_resolve_profile(const char* name, fx_texture_params* out);
+
+/* resolve_feature_groups (engine.hpp:60, engine.cpp:88-105): names
+ * (incl. "*ALL*") -> canonical group bit mask; FX_E_CONFIG on empty/unknown. */
+int fx_resolve_groups(const char* const* names, int n_names, unsigned* out_mask);
+
+/* feature_columns (engine.hpp:64-65, engine.cpp:107-136): '\n'-joined names
+ * into buf (may be NULL for a size query); *need = bytes incl. NUL. */
+int fx_columns(unsigned groups, const fx_texture_params* params, char* buf, size_t cap,
+               size_t* need, int* n_cols);
+
+/* ---- device context ------------------------------------------------------ */
+
+typedef struct fx_ctx fx_ctx;
+
+int fx_ctx_create(int device, fx_ctx** out);
+int fx_ctx_destroy(fx_ctx* ctx);
+/* Launch on a caller-owned cudaStream_t (NULL restores the ctx's own stream). */
+int fx_ctx_set_stream(fx_ctx* ctx, void* cuda_stream);
+/* Kernel launches issued by this ctx since creation (evidence counter). */
+uint64_t fx_ctx_launch_count(const fx_ctx* ctx);
+/* Optional per-kernel CUDA-event timing on the launching stream. */
+int fx_ctx_enable_timing(fx_ctx* ctx, int enable);
+/* names: '\n'-joined kernel names; ms[i]: accumulated device ms; count[i]:
+ * launches.  Returns the number of kernels in *n. */
+int fx_ctx_kernel_times(fx_ctx* ctx, char* names, size_t names_cap, double* ms,
+                        uint64_t* counts, int cap, int* n);
+int fx_ctx_reset_kernel_times(fx_ctx* ctx);
+
+/* ---- the hot path ---------------------------------------------------------- */
+
+/* Replaces the per-pair body of featurex::run (engine.cpp:300-336):
+ * RoiRegistry::accumulate (roi.cpp:76-110) + compute_roi_features
+ * (engine.cpp:138-209) for every label.  Writes labels ascending into
+ * out_labels[0..*n_rois) and the feature table row-major
+ * [*n_rois x n_cols] in feature_columns order into out_values.  When the
+ * table does not fit (cap_rois), *n_rois is set and FX_E_CAPACITY returned. */
+int fx_featurize(fx_ctx* ctx, const fx_image* image, unsigned groups,
+                 const fx_texture_params* params, uint32_t* out_labels, double* out_values,
+                 size_t cap_rois, size_t* n_rois);
+
+/* Convenience form of fx_featurize with origin (0,0). */
+int fx_featurize_u16(fx_ctx* ctx, const uint16_t* intensity, const uint16_t* labels, int width,
+                     int height, size_t pitch, int mem_kind, unsigned groups,
+                     const fx_texture_params* params, uint32_t* out_labels,
+                     double* out_values, size_t cap_rois, size_t* n_rois);
+
+/* The per-ROI operator compute_roi_features(PixelCloud, groups, params)
+ * (engine.hpp:68-70): host arrays of pixel x, y, intensity (no duplicates).
+ * The cloud is rasterized into its bbox window and run through the same
+ * device kernels (a batch of one).  out receives n_cols values. */
+int fx_roi_features(fx_ctx* ctx, const uint32_t* xs, const uint32_t* ys,
+                    const uint16_t* intensities, size_t n, unsigned groups,
+                    const fx_texture_params* params, double* out, size_t cap);
+
+/* Label scan only (RoiRegistry::accumulate + labels(), roi.cpp:76-117):
+ * ascending labels, pixel counts and inclusive bboxes [xmin,ymin,xmax,ymax]
+ * in image coordinates (origin added).  Host output buffers. */
+int fx_roi_table(fx_ctx* ctx, const fx_image* image, uint32_t* out_labels, uint64_t* out_count,
+                 uint32_t* out_bbox, size_t cap, size_t* n_rois);
+
+/* Introspection of one ROI's integer intermediates, for the bit-exact tests:
+ *  hist      : intensity histogram counts over max(2,bins) bins
+ *              (intensity_features.cpp:156-167)                 [nb]
+ *  edge_xy   : edge pixel set used by the edge_* columns, interleaved x,y in
+ *              row-major order (== trace_contour's visited set)  [2*cap_edge]
+ *  glcm      : raw co-occurrence counts per sorted angle, dense [A][ng][ng]
+ *              (texture.cpp:58-80) and pair counts [A]
+ * Any output pointer may be NULL.  All host buffers. */
+int fx_debug_roi(fx_ctx* ctx, const fx_image* image, uint32_t label,
+                 const fx_texture_params* params, uint64_t* hist, int32_t* edge_xy,
+                 size_t cap_edge, size_t* n_edge, uint32_t* glcm_counts, uint64_t* glcm_pairs);
+
+/* ---- synthetic inputs (the reference's synth.hpp generators) --------------- */
+
+/* blob_mask_grid (synth.hpp:22-26): disk-with-ears blobs on a grid, labels
+ * 1..roi_count; FX_E_CONFIG (PackingError) when it cannot pack. */
+int fx_synth_blob_mask_grid(int image_size, int roi_size, int roi_count, uint64_t seed,
+                            uint16_t* out);
+/* siemens_star (synth.hpp:18-20) */
+int fx_synth_siemens_star(int size, int spokes, uint16_t* out);
+/* uniform uint16: std::mt19937_64(seed)() & 0xffff in row-major order */
+int fx_synth_uniform_u16(uint64_t seed, size_t n, uint16_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FXG_H */

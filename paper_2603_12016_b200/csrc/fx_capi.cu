@@ -1,0 +1,738 @@
+// Device context + orchestration of the featurize pipeline (C ABI, fxg.h).
+//
+//   H2D (host inputs only) -> k_label_scan -> k_compact_count -> k_compact_emit
+//   -> k_roi_s<S1> / k_roi_s<S2> (TMA-staged windows, warp per ROI)
+//   -> k_roi_l (large windows + S overflow, global slabs) -> D2H table
+//
+// The only host synchronisation before the table readback is a small
+// side-stream copy of the compaction counters (L-path slab sizing), which
+// overlaps the S kernels.
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "fx_dev.cuh"
+#include "fx_host.hpp"
+#include "fx_roi.cuh"
+#include "fxg.h"
+
+namespace fxg {
+__global__ void k_label_scan(const uint16_t* L, int W, int H, size_t pitch, int vec_ok,
+                             LabelTable t);
+__global__ void k_compact_count(LabelTable t, Control* ctl);
+__global__ void k_compact_emit(LabelTable t, Control* ctl, RoiList r);
+cudaError_t roi_kernels_setup(int* occ_s1, int* occ_s2);
+void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap, DevImage img,
+                  RoiList rl, Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg,
+                  int use_tma);
+void launch_roi_l(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
+                  double* out, const DebugOut* dbg, uint8_t* scratch, const Layout& L);
+}  // namespace fxg
+
+using namespace fxg;
+
+#define CK(x)                                                                        \
+    do {                                                                             \
+        cudaError_t e_ = (x);                                                        \
+        if (e_ != cudaSuccess)                                                       \
+            return set_error(e_ == cudaErrorMemoryAllocation ? FX_E_OOM : FX_E_CUDA, \
+                             std::string(#x) + ": " + cudaGetErrorString(e_));      \
+    } while (0)
+
+struct KTime {
+    double ms = 0;
+    uint64_t count = 0;
+};
+
+struct fx_ctx {
+    int device = 0;
+    int sm_count = 0;
+    cudaStream_t own_stream = nullptr, stream = nullptr, side = nullptr;
+    cudaEvent_t ev_compact = nullptr, ev_stats = nullptr;
+    // label table + control
+    unsigned long long* d_cnt = nullptr;
+    uint32_t* d_bb = nullptr;  // xmin | ymin | xmax | ymax, 65536 each
+    Control* d_ctl = nullptr;
+    Control* h_ctl = nullptr;  // pinned
+    // ROI list
+    uint32_t* d_roi32 = nullptr;  // label,x0,y0,w,h + 3 class lists + overflow: 9 x 65536
+    unsigned long long* d_roin = nullptr;
+    // staging for host inputs / outputs
+    uint16_t* d_img = nullptr;  // intensity then labels, pitched
+    size_t img_pitch = 0, img_rows_cap = 0;
+    double* d_out = nullptr;
+    size_t out_cap = 0;  // doubles
+    // L-path slabs
+    uint8_t* d_lscratch = nullptr;
+    size_t lscratch_bytes = 0;
+    // debug capture
+    DebugOut* d_dbg = nullptr;
+    // accounting
+    uint64_t launches = 0;
+    bool timing = false;
+    std::map<std::string, KTime> ktimes;
+    std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+    std::vector<cudaEvent_t> ev_pool;
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    int occ_s1 = 1, occ_s2 = 1;
+    bool sync_debug = false;
+    bool no_tma = false;
+};
+
+namespace {
+
+RoiList roi_list(fx_ctx* c) {
+    RoiList r;
+    uint32_t* b = c->d_roi32;
+    r.label = b;
+    r.x0 = b + 1 * kMaxLabels;
+    r.y0 = b + 2 * kMaxLabels;
+    r.w = b + 3 * kMaxLabels;
+    r.h = b + 4 * kMaxLabels;
+    r.cls_list[0] = b + 5 * kMaxLabels;
+    r.cls_list[1] = b + 6 * kMaxLabels;
+    r.cls_list[2] = b + 7 * kMaxLabels;
+    r.overflow = b + 8 * kMaxLabels;
+    r.n = c->d_roin;
+    return r;
+}
+
+LabelTable label_table(fx_ctx* c) {
+    LabelTable t;
+    t.cnt = c->d_cnt;
+    t.xmin = c->d_bb;
+    t.ymin = c->d_bb + kMaxLabels;
+    t.xmax = c->d_bb + 2 * kMaxLabels;
+    t.ymax = c->d_bb + 3 * kMaxLabels;
+    return t;
+}
+
+cudaEvent_t get_event(fx_ctx* c) {
+    if (!c->ev_pool.empty()) {
+        cudaEvent_t e = c->ev_pool.back();
+        c->ev_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+}
+
+// Launch bracket: counts launches; with timing on, records events on the stream.
+struct Launch {
+    fx_ctx* c;
+    const char* name;
+    cudaEvent_t a = nullptr, b = nullptr;
+    Launch(fx_ctx* c_, const char* n) : c(c_), name(n) {
+        c->launches++;
+        if (c->timing) {
+            a = get_event(c);
+            b = get_event(c);
+            cudaEventRecord(a, c->stream);
+        }
+    }
+    ~Launch() {
+        if (c->timing) {
+            cudaEventRecord(b, c->stream);
+            c->pending.push_back({name, {a, b}});
+        }
+        if (c->sync_debug) {  // FXG_SYNC_DEBUG=1: attribute device faults to a kernel
+            cudaError_t e = cudaStreamSynchronize(c->stream);
+            if (e != cudaSuccess) fprintf(stderr, "[fxg] %s: %s\n", name, cudaGetErrorString(e));
+        }
+    }
+};
+
+void collect_times(fx_ctx* c) {
+    for (auto& p : c->pending) {
+        float ms = 0;
+        cudaEventSynchronize(p.second.second);
+        cudaEventElapsedTime(&ms, p.second.first, p.second.second);
+        auto& k = c->ktimes[p.first];
+        k.ms += ms;
+        k.count++;
+        c->ev_pool.push_back(p.second.first);
+        c->ev_pool.push_back(p.second.second);
+    }
+    c->pending.clear();
+}
+
+int validate_texture(unsigned groups, const fx_texture_params& p) {
+    if (!(groups & FX_GROUP_GLCM)) return FX_OK;
+    if (p.ng < 2) return set_error(FX_E_CONFIG, "grey level count must be >= 2");
+    if (p.ng > 256)
+        return set_error(FX_E_CONFIG, "device GLCM supports ng <= 256 in this build");
+    if (p.n_angles < 1 || p.n_angles > 8) return set_error(FX_E_CONFIG, "1..8 angles supported");
+    for (int i = 0; i < p.n_angles; ++i) {
+        const int a = p.angles[i];
+        if (a != 0 && a != 45 && a != 90 && a != 135)
+            return set_error(FX_E_CONFIG, "unsupported angle " + std::to_string(a));
+    }
+    return FX_OK;
+}
+
+FeatCfg make_cfg(unsigned groups, const fx_texture_params& p) {
+    FeatCfg f{};
+    f.groups = groups;
+    int col = 0;
+    f.col_int = f.col_mom = f.col_glcm = -1;
+    if (groups & FX_GROUP_INTENSITY) {
+        f.col_int = col;
+        col += 39;
+    }
+    if (groups & FX_GROUP_MOMENTS) {
+        f.col_mom = col;
+        col += 104;
+    }
+    if (groups & FX_GROUP_GLCM) {
+        f.col_glcm = col;
+        col += 29 * (p.n_angles + 1);
+    }
+    f.ncols = col;
+    f.bins = std::max(2, p.histogram_bins);
+    f.ng = p.ng;
+    f.symmetric = p.symmetric;
+    const std::vector<int> a = sorted_angles(p);
+    f.n_angles = (int)a.size();
+    for (int i = 0; i < f.n_angles; ++i) {
+        f.angle[i] = a[i];
+        const int d = p.offset;
+        switch (a[i]) {  // angle_offset, texture.cpp:15-23 (y points down)
+            case 0: f.dx[i] = d; f.dy[i] = 0; break;
+            case 45: f.dx[i] = d; f.dy[i] = -d; break;
+            case 90: f.dx[i] = 0; f.dy[i] = -d; break;
+            default: f.dx[i] = -d; f.dy[i] = -d; break;
+        }
+    }
+    return f;
+}
+
+int ensure_out(fx_ctx* c, size_t doubles) {
+    if (doubles <= c->out_cap) return FX_OK;
+    if (c->d_out) cudaFree(c->d_out);
+    c->d_out = nullptr;
+    c->out_cap = 0;
+    CK(cudaMalloc(&c->d_out, doubles * sizeof(double)));
+    c->out_cap = doubles;
+    return FX_OK;
+}
+
+int ensure_lscratch(fx_ctx* c, size_t bytes) {
+    if (bytes <= c->lscratch_bytes) return FX_OK;
+    if (c->d_lscratch) {
+        cudaStreamSynchronize(c->stream);
+        cudaFree(c->d_lscratch);
+    }
+    c->d_lscratch = nullptr;
+    c->lscratch_bytes = 0;
+    CK(cudaMalloc(&c->d_lscratch, bytes));
+    c->lscratch_bytes = bytes;
+    return FX_OK;
+}
+
+int ensure_img(fx_ctx* c, int w, int h) {
+    const size_t pitch = ((size_t)w + 63) / 64 * 64;  // elements; 128 B rows for TMA
+    if (pitch <= c->img_pitch && (size_t)h <= c->img_rows_cap) return FX_OK;
+    if (c->d_img) cudaFree(c->d_img);
+    c->d_img = nullptr;
+    c->img_pitch = c->img_rows_cap = 0;
+    CK(cudaMalloc(&c->d_img, pitch * (size_t)h * 2 * sizeof(uint16_t)));
+    c->img_pitch = pitch;
+    c->img_rows_cap = (size_t)h;
+    return FX_OK;
+}
+
+bool make_tmap(fx_ctx* c, const DevImage& img, CUtensorMap* m) {
+    if (!c->encode) return false;
+    if ((reinterpret_cast<uintptr_t>(img.L) & 15u) || ((img.pitch * 2) & 15u)) return false;
+    if (img.w < kStageW || img.h < 8) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)img.w, (cuuint64_t)img.h};
+    cuuint64_t strides[1] = {(cuuint64_t)img.pitch * 2};
+    cuuint32_t box[2] = {(cuuint32_t)kStageW, 8};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = c->encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (void*)img.L, dims, strides, box,
+                           estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+Layout l_layout(const Control& h) {
+    const uint32_t H = std::max<uint32_t>(h.l_max_h, kSH);
+    const uint32_t WPR = std::max<uint32_t>(h.l_max_wpr, 1);
+    const uint32_t NMAX = (uint32_t)std::max<unsigned long long>(h.l_max_n, kS2N);
+    const unsigned long long cells = std::max<unsigned long long>(h.l_max_cells, (unsigned long long)kSW * kSH);
+    const uint32_t RUNMAX =
+        (uint32_t)std::min<unsigned long long>(cells / 2 + H + 64, 16ull << 20);
+    return make_layout(H, WPR, NMAX, RUNMAX, 4, 0);
+}
+
+struct DebugHost {
+    uint32_t label = 0;
+    int nb = 0;
+    unsigned long long* hist = nullptr;  // device
+    int32_t* edge = nullptr;
+    uint32_t cap_edge = 0;
+    uint32_t* n_edge = nullptr;
+    uint32_t* glcm = nullptr;
+    unsigned long long* pairs = nullptr;
+};
+
+// Core pipeline on a device-resident image.  out_dev: [cap_rois x ncols] device.
+int run_pipeline(fx_ctx* c, const DevImage& img, unsigned groups, const fx_texture_params& p,
+                 double* out_dev, size_t cap_rois, size_t* n_rois, const DebugOut* dbg_dev) {
+    const FeatCfg cfg = make_cfg(groups, p);
+    const int vrc = validate_texture(groups, p);
+    LabelTable t = label_table(c);
+    RoiList rl = roi_list(c);
+    cudaStream_t s = c->stream;
+    CK(cudaMemsetAsync(c->d_cnt, 0, kMaxLabels * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(c->d_bb, 0xff, 2 * kMaxLabels * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(c->d_bb + 2 * kMaxLabels, 0, 2 * kMaxLabels * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(c->d_ctl, 0, sizeof(Control), s));
+    {
+        const int vec_ok = ((reinterpret_cast<uintptr_t>(img.L) & 15u) == 0) && (img.pitch % 8 == 0);
+        const int tiles = ((img.w + 255) / 256) * ((img.h + 63) / 64);
+        const int grid = std::max(1, std::min(tiles, c->sm_count * 6));
+        Launch l(c, "k_label_scan");
+        k_label_scan<<<grid, 256, 0, s>>>(img.L, img.w, img.h, img.pitch, vec_ok, t);
+    }
+    {
+        Launch l(c, "k_compact_count");
+        k_compact_count<<<64, 1024, 0, s>>>(t, c->d_ctl);
+    }
+    {
+        Launch l(c, "k_compact_emit");
+        k_compact_emit<<<64, 1024, 0, s>>>(t, c->d_ctl, rl);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev_compact, s));
+    CK(cudaStreamWaitEvent(c->side, c->ev_compact, 0));
+    CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, c->side));
+    CK(cudaEventRecord(c->ev_stats, c->side));
+
+    if (vrc != FX_OK) {  // texture parameters are only an error when a ROI exists
+        CK(cudaEventSynchronize(c->ev_stats));
+        *n_rois = c->h_ctl->n_rois;
+        return c->h_ctl->n_rois ? vrc : FX_OK;
+    }
+    CUtensorMap tmap;
+    std::memset(&tmap, 0, sizeof tmap);
+    int use_tma = (!c->no_tma && make_tmap(c, img, &tmap)) ? 1 : 0;
+    if (use_tma && getenv("FXG_TMA_DIAG")) use_tma = atoi(getenv("FXG_TMA_DIAG"));
+    {
+        Launch l(c, "k_roi_s1");
+        launch_roi_s(kClassS1, c->sm_count * c->occ_s1, s, tmap, img, rl, c->d_ctl, cfg, out_dev,
+                     dbg_dev, use_tma);
+    }
+    {
+        Launch l(c, "k_roi_s2");
+        launch_roi_s(kClassS2, c->sm_count * c->occ_s2, s, tmap, img, rl, c->d_ctl, cfg, out_dev,
+                     dbg_dev, use_tma);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventSynchronize(c->ev_stats));
+    const Control hc = *c->h_ctl;
+    *n_rois = hc.n_rois;
+    if (hc.n_rois > cap_rois) {
+        cudaStreamSynchronize(s);
+        return set_error(FX_E_CAPACITY, "output capacity " + std::to_string(cap_rois) +
+                                            " < " + std::to_string(hc.n_rois) + " ROIs");
+    }
+    {
+        const Layout L = l_layout(hc);
+        const uint32_t nl = hc.class_count[kClassL];
+        const uint32_t grid = (uint32_t)std::min<uint64_t>(
+            (uint64_t)c->sm_count * 2,
+            std::max<uint64_t>(std::max<uint64_t>(nl, 1),
+                               hc.class_count[kClassS1] + hc.class_count[kClassS2] > 0 ? 16 : 1));
+        size_t bytes = (size_t)L.bytes * grid;
+        int rc = ensure_lscratch(c, bytes);
+        if (rc) return rc;
+        Launch l(c, "k_roi_l");
+        launch_roi_l((int)grid, s, img, rl, c->d_ctl, cfg, out_dev, dbg_dev, c->d_lscratch, L);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+    return FX_OK;
+}
+
+int finish(fx_ctx* c) {
+    CK(cudaStreamSynchronize(c->stream));
+    if (c->timing) collect_times(c);
+    if (c->h_ctl->error & kErrCapacity)
+        return set_error(FX_E_CAPACITY, "a large ROI exceeded the L-path slab");
+    if (c->h_ctl->error & kErrRuns)
+        return set_error(FX_E_CAPACITY, "a large ROI exceeded the run-list capacity");
+    return FX_OK;
+}
+
+DevImage to_dev(const fx_image& im) {
+    DevImage d;
+    d.I = im.intensity;
+    d.L = im.labels;
+    d.w = im.width;
+    d.h = im.height;
+    d.pitch = im.pitch ? im.pitch : (size_t)im.width;
+    d.ox = im.origin_x;
+    d.oy = im.origin_y;
+    return d;
+}
+
+int check_groups(unsigned groups) {
+    if (groups == 0) return set_error(FX_E_CONFIG, "feature list is empty");
+    if (groups & ~FX_GROUP_ALL) return set_error(FX_E_CONFIG, "unknown feature group bit");
+    const unsigned missing = groups & ~FX_GROUP_DEVICE;
+    if (missing) {
+        std::string names;
+        for (int i = 0; i < 7; ++i)
+            if (missing & (1u << i)) names += (names.empty() ? "" : ",") + all_group_names()[i];
+        return set_error(FX_E_CONFIG, "feature group(s) '" + names +
+                                          "' have no device kernel in this build (no CPU fallback)");
+    }
+    return FX_OK;
+}
+
+// Device image from the caller's image; host rasters are staged into pitched buffers.
+int stage_image(fx_ctx* c, const fx_image* im, DevImage* d) {
+    *d = to_dev(*im);
+    if (im->mem_kind == FX_MEM_DEVICE) return FX_OK;
+    int rc = ensure_img(c, im->width, im->height);
+    if (rc) return rc;
+    uint16_t* dI = c->d_img;
+    uint16_t* dL = c->d_img + c->img_pitch * c->img_rows_cap;
+    const size_t sp = (im->pitch ? im->pitch : (size_t)im->width) * 2;
+    CK(cudaMemcpy2DAsync(dI, c->img_pitch * 2, im->intensity, sp, (size_t)im->width * 2,
+                         (size_t)im->height, cudaMemcpyHostToDevice, c->stream));
+    CK(cudaMemcpy2DAsync(dL, c->img_pitch * 2, im->labels, sp, (size_t)im->width * 2,
+                         (size_t)im->height, cudaMemcpyHostToDevice, c->stream));
+    d->I = dI;
+    d->L = dL;
+    d->pitch = c->img_pitch;
+    return FX_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int fx_ctx_create(int device, fx_ctx** out) {
+    if (!out) return set_error(FX_E_ARG, "null argument");
+    *out = nullptr;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return set_error(FX_E_CUDA, "no CUDA device visible (the device path has no CPU fallback)");
+    if (device < 0 || device >= ndev) return set_error(FX_E_ARG, "bad device index");
+    fx_ctx* c = new fx_ctx();
+    c->device = device;
+    auto fail = [&](int rc) {
+        fx_ctx_destroy(c);
+        return rc;
+    };
+#define CKC(x)                                                                     \
+    do {                                                                           \
+        cudaError_t e_ = (x);                                                      \
+        if (e_ != cudaSuccess)                                                     \
+            return fail(set_error(e_ == cudaErrorMemoryAllocation ? FX_E_OOM : FX_E_CUDA, \
+                                  std::string(#x) + ": " + cudaGetErrorString(e_))); \
+    } while (0)
+    CKC(cudaSetDevice(device));
+    cudaDeviceProp prop;
+    CKC(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10)
+        return fail(set_error(FX_E_CUDA, "libfxg is built for sm_100a (B200); device is sm_" +
+                                             std::to_string(prop.major * 10 + prop.minor)));
+    c->sm_count = prop.multiProcessorCount;
+    if (const char* e = getenv("FXG_SYNC_DEBUG")) c->sync_debug = atoi(e) != 0;
+    if (const char* e = getenv("FXG_NO_TMA")) c->no_tma = atoi(e) != 0;
+    CKC(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    c->stream = c->own_stream;
+    CKC(cudaEventCreateWithFlags(&c->ev_compact, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
+    CKC(cudaMalloc(&c->d_cnt, kMaxLabels * sizeof(unsigned long long)));
+    CKC(cudaMalloc(&c->d_bb, 4 * kMaxLabels * sizeof(uint32_t)));
+    CKC(cudaMalloc(&c->d_ctl, sizeof(Control)));
+    CKC(cudaMallocHost(&c->h_ctl, sizeof(Control)));
+    CKC(cudaMalloc(&c->d_roi32, 9 * kMaxLabels * sizeof(uint32_t)));
+    CKC(cudaMalloc(&c->d_roin, kMaxLabels * sizeof(unsigned long long)));
+    CKC(cudaMalloc(&c->d_dbg, sizeof(DebugOut)));
+    CKC(roi_kernels_setup(&c->occ_s1, &c->occ_s2));
+    c->occ_s1 = std::max(1, c->occ_s1);
+    c->occ_s2 = std::max(1, c->occ_s2);
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+        c->encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+#undef CKC
+    *out = c;
+    return FX_OK;
+}
+
+int fx_ctx_destroy(fx_ctx* c) {
+    if (!c) return FX_OK;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    cudaFree(c->d_cnt);
+    cudaFree(c->d_bb);
+    cudaFree(c->d_ctl);
+    if (c->h_ctl) cudaFreeHost(c->h_ctl);
+    cudaFree(c->d_roi32);
+    cudaFree(c->d_roin);
+    cudaFree(c->d_img);
+    cudaFree(c->d_out);
+    cudaFree(c->d_lscratch);
+    cudaFree(c->d_dbg);
+    for (auto& p : c->pending) {
+        cudaEventDestroy(p.second.first);
+        cudaEventDestroy(p.second.second);
+    }
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    if (c->ev_compact) cudaEventDestroy(c->ev_compact);
+    if (c->ev_stats) cudaEventDestroy(c->ev_stats);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+    return FX_OK;
+}
+
+int fx_ctx_set_stream(fx_ctx* c, void* stream) {
+    if (!c) return set_error(FX_E_ARG, "null ctx");
+    c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    return FX_OK;
+}
+
+uint64_t fx_ctx_launch_count(const fx_ctx* c) { return c ? c->launches : 0; }
+
+int fx_ctx_enable_timing(fx_ctx* c, int enable) {
+    if (!c) return set_error(FX_E_ARG, "null ctx");
+    c->timing = enable != 0;
+    return FX_OK;
+}
+
+int fx_ctx_kernel_times(fx_ctx* c, char* names, size_t names_cap, double* ms, uint64_t* counts,
+                        int cap, int* n) {
+    if (!c || !n) return set_error(FX_E_ARG, "null argument");
+    collect_times(c);
+    std::string joined;
+    int i = 0;
+    for (auto& kv : c->ktimes) {
+        if (i < cap) {
+            if (ms) ms[i] = kv.second.ms;
+            if (counts) counts[i] = kv.second.count;
+        }
+        if (i) joined += '\n';
+        joined += kv.first;
+        ++i;
+    }
+    *n = i;
+    if (names) {
+        if (names_cap < joined.size() + 1) return set_error(FX_E_CAPACITY, "names buffer too small");
+        std::memcpy(names, joined.c_str(), joined.size() + 1);
+    }
+    return FX_OK;
+}
+
+int fx_ctx_reset_kernel_times(fx_ctx* c) {
+    if (!c) return set_error(FX_E_ARG, "null ctx");
+    collect_times(c);
+    c->ktimes.clear();
+    return FX_OK;
+}
+
+int fx_featurize(fx_ctx* c, const fx_image* im, unsigned groups, const fx_texture_params* p,
+                 uint32_t* out_labels, double* out_values, size_t cap_rois, size_t* n_rois) {
+    if (!c || !im || !p || !n_rois) return set_error(FX_E_ARG, "null argument");
+    if (!im->intensity || !im->labels) return set_error(FX_E_ARG, "null raster");
+    if (im->width < 1 || im->height < 1) return set_error(FX_E_PAIRING, "empty raster");
+    if (im->pitch && im->pitch < (size_t)im->width) return set_error(FX_E_ARG, "pitch < width");
+    *n_rois = 0;
+    int rc = check_groups(groups);
+    if (rc) return rc;
+    CK(cudaSetDevice(c->device));
+    DevImage d;
+    rc = stage_image(c, im, &d);
+    if (rc) return rc;
+    const FeatCfg cfg = make_cfg(groups, *p);
+    double* out_dev = out_values;
+    if (im->mem_kind == FX_MEM_HOST) {
+        rc = ensure_out(c, std::max<size_t>(1, cap_rois) * (size_t)cfg.ncols);
+        if (rc) return rc;
+        out_dev = c->d_out;
+    }
+    rc = run_pipeline(c, d, groups, *p, out_dev, cap_rois, n_rois, nullptr);
+    if (rc) {
+        cudaStreamSynchronize(c->stream);
+        return rc;
+    }
+    const size_t nr = *n_rois;
+    if (im->mem_kind == FX_MEM_HOST) {
+        if (nr) {
+            CK(cudaMemcpyAsync(out_values, out_dev, nr * cfg.ncols * sizeof(double),
+                               cudaMemcpyDeviceToHost, c->stream));
+            CK(cudaMemcpyAsync(out_labels, roi_list(c).label, nr * sizeof(uint32_t),
+                               cudaMemcpyDeviceToHost, c->stream));
+        }
+    } else if (nr) {
+        CK(cudaMemcpyAsync(out_labels, roi_list(c).label, nr * sizeof(uint32_t),
+                           cudaMemcpyDeviceToDevice, c->stream));
+    }
+    return finish(c);
+}
+
+int fx_featurize_u16(fx_ctx* c, const uint16_t* intensity, const uint16_t* labels, int width,
+                     int height, size_t pitch, int mem_kind, unsigned groups,
+                     const fx_texture_params* p, uint32_t* out_labels, double* out_values,
+                     size_t cap_rois, size_t* n_rois) {
+    fx_image im{intensity, labels, width, height, pitch, 0, 0, mem_kind};
+    return fx_featurize(c, &im, groups, p, out_labels, out_values, cap_rois, n_rois);
+}
+
+int fx_roi_features(fx_ctx* c, const uint32_t* xs, const uint32_t* ys, const uint16_t* is,
+                    size_t n, unsigned groups, const fx_texture_params* p, double* out,
+                    size_t cap) {
+    if (!c || !p || !out || (n && (!xs || !ys || !is))) return set_error(FX_E_ARG, "null argument");
+    int rc = check_groups(groups);
+    if (rc) return rc;
+    const FeatCfg cfg = make_cfg(groups, *p);
+    if (cap < (size_t)cfg.ncols) return set_error(FX_E_CAPACITY, "output buffer too small");
+    if (n == 0) {  // empty cloud: every group reports zeros (engine.cpp:138-209)
+        std::fill(out, out + cfg.ncols, 0.0);
+        return FX_OK;
+    }
+    uint32_t x0 = xs[0], x1 = xs[0], y0 = ys[0], y1 = ys[0];
+    for (size_t i = 0; i < n; ++i) {
+        x0 = std::min(x0, xs[i]);
+        x1 = std::max(x1, xs[i]);
+        y0 = std::min(y0, ys[i]);
+        y1 = std::max(y1, ys[i]);
+    }
+    const int w = (int)(x1 - x0 + 1), h = (int)(y1 - y0 + 1);
+    std::vector<uint16_t> I((size_t)w * h, 0), L((size_t)w * h, 0);
+    for (size_t i = 0; i < n; ++i) {
+        const size_t k = (size_t)(ys[i] - y0) * w + (xs[i] - x0);
+        I[k] = is[i];
+        L[k] = 1;
+    }
+    fx_image im{I.data(), L.data(), w, h, (size_t)w, (int)x0, (int)y0, FX_MEM_HOST};
+    uint32_t lab = 0;
+    size_t nr = 0;
+    rc = fx_featurize(c, &im, groups, p, &lab, out, 1, &nr);
+    if (rc) return rc;
+    if (nr != 1) return set_error(FX_E_INTERNAL, "rasterized cloud did not yield one ROI");
+    return FX_OK;
+}
+
+int fx_roi_table(fx_ctx* c, const fx_image* im, uint32_t* out_labels, uint64_t* out_count,
+                 uint32_t* out_bbox, size_t cap, size_t* n_rois) {
+    if (!c || !im || !n_rois) return set_error(FX_E_ARG, "null argument");
+    CK(cudaSetDevice(c->device));
+    DevImage d;
+    int rc = stage_image(c, im, &d);
+    if (rc) return rc;
+    LabelTable t = label_table(c);
+    RoiList rl = roi_list(c);
+    cudaStream_t s = c->stream;
+    CK(cudaMemsetAsync(c->d_cnt, 0, kMaxLabels * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(c->d_bb, 0xff, 2 * kMaxLabels * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(c->d_bb + 2 * kMaxLabels, 0, 2 * kMaxLabels * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(c->d_ctl, 0, sizeof(Control), s));
+    const int vec_ok = ((reinterpret_cast<uintptr_t>(d.L) & 15u) == 0) && (d.pitch % 8 == 0);
+    const int tiles = ((d.w + 255) / 256) * ((d.h + 63) / 64);
+    {
+        Launch l(c, "k_label_scan");
+        k_label_scan<<<std::max(1, std::min(tiles, c->sm_count * 6)), 256, 0, s>>>(d.L, d.w, d.h,
+                                                                                 d.pitch, vec_ok, t);
+    }
+    {
+        Launch l(c, "k_compact_count");
+        k_compact_count<<<64, 1024, 0, s>>>(t, c->d_ctl);
+    }
+    {
+        Launch l(c, "k_compact_emit");
+        k_compact_emit<<<64, 1024, 0, s>>>(t, c->d_ctl, rl);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const size_t nr = c->h_ctl->n_rois;
+    *n_rois = nr;
+    if (nr > cap) return set_error(FX_E_CAPACITY, "output capacity too small");
+    if (!nr) return finish(c);
+    std::vector<uint32_t> x0(nr), y0(nr), w(nr), h(nr);
+    std::vector<unsigned long long> cnt(nr);
+    CK(cudaMemcpy(out_labels, rl.label, nr * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(x0.data(), rl.x0, nr * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(y0.data(), rl.y0, nr * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(w.data(), rl.w, nr * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(h.data(), rl.h, nr * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(cnt.data(), rl.n, nr * 8, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < nr; ++i) {
+        out_count[i] = cnt[i];
+        out_bbox[4 * i + 0] = x0[i] + im->origin_x;
+        out_bbox[4 * i + 1] = y0[i] + im->origin_y;
+        out_bbox[4 * i + 2] = x0[i] + w[i] - 1 + im->origin_x;
+        out_bbox[4 * i + 3] = y0[i] + h[i] - 1 + im->origin_y;
+    }
+    return finish(c);
+}
+
+int fx_debug_roi(fx_ctx* c, const fx_image* im, uint32_t label, const fx_texture_params* p,
+                 uint64_t* hist, int32_t* edge_xy, size_t cap_edge, size_t* n_edge,
+                 uint32_t* glcm_counts, uint64_t* glcm_pairs) {
+    if (!c || !im || !p) return set_error(FX_E_ARG, "null argument");
+    CK(cudaSetDevice(c->device));
+    unsigned groups = FX_GROUP_INTENSITY | FX_GROUP_GLCM;
+    const FeatCfg cfg = make_cfg(groups, *p);
+    int rc = validate_texture(groups, *p);
+    if (rc) return rc;
+    DevImage d;
+    rc = stage_image(c, im, &d);
+    if (rc) return rc;
+    const int nb = cfg.bins, A = cfg.n_angles, ng = cfg.ng;
+    DebugOut h{};
+    h.label = label;
+    h.nb = nb;
+    h.cap_edge = (uint32_t)std::min<size_t>(cap_edge, 1u << 26);
+    void* buf = nullptr;
+    const size_t bytes = (size_t)nb * 8 + (size_t)h.cap_edge * 8 + 8 + (size_t)A * ng * ng * 4 + A * 8 + 64;
+    CK(cudaMalloc(&buf, bytes));
+    CK(cudaMemsetAsync(buf, 0, bytes, c->stream));
+    uint8_t* b = (uint8_t*)buf;
+    h.hist = (unsigned long long*)b;
+    b += (size_t)nb * 8;
+    h.pairs = (unsigned long long*)b;
+    b += (size_t)A * 8;
+    h.n_edge = (uint32_t*)b;
+    b += 8;
+    h.edge_xy = (int32_t*)b;
+    b += (size_t)h.cap_edge * 8;
+    h.glcm = (uint32_t*)b;
+    CK(cudaMemcpyAsync(c->d_dbg, &h, sizeof h, cudaMemcpyHostToDevice, c->stream));
+    rc = ensure_out(c, (size_t)kMaxLabels * cfg.ncols);
+    size_t nr = 0;
+    if (!rc) rc = run_pipeline(c, d, groups, *p, c->d_out, kMaxLabels, &nr, c->d_dbg);
+    if (!rc) rc = finish(c);
+    if (!rc) {
+        uint32_t ne = 0;
+        cudaMemcpy(&ne, h.n_edge, 4, cudaMemcpyDeviceToHost);
+        if (n_edge) *n_edge = ne;
+        if (hist) cudaMemcpy(hist, h.hist, (size_t)nb * 8, cudaMemcpyDeviceToHost);
+        if (edge_xy) cudaMemcpy(edge_xy, h.edge_xy, (size_t)std::min<uint32_t>(ne, h.cap_edge) * 8,
+                                cudaMemcpyDeviceToHost);
+        if (glcm_counts) cudaMemcpy(glcm_counts, h.glcm, (size_t)A * ng * ng * 4, cudaMemcpyDeviceToHost);
+        if (glcm_pairs) cudaMemcpy(glcm_pairs, h.pairs, (size_t)A * 8, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(buf);
+    return rc;
+}
+
+}  // extern "C"

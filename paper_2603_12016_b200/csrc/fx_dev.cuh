@@ -1,0 +1,133 @@
+// Shared device-side definitions for libfxg (sm_100a).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace fxg {
+
+constexpr int kMaxLabels = 65536;  // uint16 labels (reference image.hpp:24)
+constexpr unsigned kFull = 0xffffffffu;
+
+// Per-label accumulators of the label scan, direct-mapped by label value
+// (replaces RoiRegistry's std::map<label, Entry>, roi.cpp:76-110).
+struct LabelTable {
+    unsigned long long* cnt;  // [65536] pixel count
+    uint32_t* xmin;           // [65536] inclusive bbox, image-local
+    uint32_t* ymin;
+    uint32_t* xmax;
+    uint32_t* ymax;
+};
+
+// ROI classes by window (bbox) size; each is consumed by its own persistent kernel.
+enum RoiClass { kClassS1 = 0, kClassS2 = 1, kClassL = 2, kNumClasses = 3 };
+
+// S-class limits: window fits a 64x64 TMA staging tile, one u64 mask word per row.
+constexpr int kSW = 64, kSH = 64;
+// TMA staging tile: box x origin must be 16 B aligned (multiple of 8 u16) on
+// sm_100a (an unaligned innermost coordinate raises "illegal instruction"),
+// so the box starts at x0 & ~7 and is 72 wide to cover any 64-wide window.
+constexpr int kStageW = 72;
+constexpr int kS1N = 1024;  // max ROI pixels for S1
+constexpr int kS2N = 4096;  // = kSW*kSH
+constexpr int kS1Runs = 512;
+constexpr int kS2Runs = 2176;  // >= worst case (33 free runs x 64 rows + 64)
+
+// Device-side control block, zeroed per featurize call.
+struct Control {
+    uint32_t n_rois;
+    uint32_t class_count[kNumClasses];
+    uint32_t class_next[kNumClasses];
+    uint32_t overflow_count;  // S ROIs re-queued to the L path (run capacity)
+    uint32_t overflow_next;
+    uint32_t error;           // bit flags, see kErr*
+    uint32_t l_max_h;         // max window height among L ROIs
+    uint32_t l_max_wpr;       // max 64-bit words per row among L ROIs
+    unsigned long long l_max_n;      // max pixel count among L ROIs
+    unsigned long long l_max_cells;  // max window cells among L ROIs
+    uint32_t block_sum[64];   // compaction: present labels per 1024-label block
+};
+
+constexpr uint32_t kErrCapacity = 1u;  // L slab too small for a ROI
+constexpr uint32_t kErrRuns = 2u;      // L run capacity exceeded
+
+// Compacted ROI list: rank r == output row r (labels ascending).
+struct RoiList {
+    uint32_t* label;
+    uint32_t* x0;
+    uint32_t* y0;
+    uint32_t* w;
+    uint32_t* h;
+    unsigned long long* n;
+    uint32_t* cls_list[kNumClasses];  // ranks per class, [65536] each
+    uint32_t* overflow;               // ranks re-queued from S to L
+};
+
+struct DevImage {
+    const uint16_t* I;
+    const uint16_t* L;
+    int w, h;
+    size_t pitch;  // elements
+    int ox, oy;    // global origin
+};
+
+// Feature configuration for the per-ROI kernels (resolved on the host).
+struct FeatCfg {
+    uint32_t groups;
+    int ncols;
+    int col_int, col_mom, col_glcm;  // column offsets, -1 if absent
+    int bins;                        // max(2, histogram_bins)
+    int ng, symmetric, n_angles;
+    int angle[8];                    // sorted (engine.cpp:36-40)
+    int dx[8], dy[8];                // angle_offset (texture.cpp:15-23)
+};
+
+__device__ __forceinline__ unsigned lane_id() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ unsigned lanemask_lt() {
+    unsigned r;
+    asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_min(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        T u = __shfl_xor_sync(kFull, v, o);
+        v = u < v ? u : v;
+    }
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T warp_max(T v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        T u = __shfl_xor_sync(kFull, v, o);
+        v = u > v ? u : v;
+    }
+    return v;
+}
+// inclusive prefix sum across the warp
+template <typename T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+    const unsigned lane = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T u = __shfl_up_sync(kFull, v, o);
+        if (lane >= (unsigned)o) v += u;
+    }
+    return v;
+}
+
+}  // namespace fxg

@@ -1,0 +1,108 @@
+"""Parity comparator for feature tables.
+
+* Bit-exact columns must be identical (==): labels and the 24 intensity columns
+  derived from exact integer sums / the sorted multiset.
+* Every other column must satisfy  |g - r| <= tol * (max(|g|, |r|) + s)
+  with tol = 1e-9 for intensity and moments, 1e-6 for Haralick (north star),
+  and s a per-feature natural scale:
+    - central moments mu_pq: s = sum w |x-cx|^p |y-cy|^q  (computed here from the
+      pixels; the reference's own fp64 binomial shift misses a pure relative
+      bound by up to 2.4e-8 on mu33)
+    - eta_pq: s_mu / m00^(1+(p+q)/2);  Hu: s2, s2^2, s3^2, s3^2, s3^4, s2*s3^2, s3^4
+      with s2 = |e20|+|e02|+2|e11|, s3 = |e30|+3|e12|+3|e21|+|e03| of the reference
+    - skewness / hyperskewness, and Haralick clushade / corr / infomeas1: s = 1
+    - everything else: s = 1e-300 (pure relative)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+EXACT_INTENSITY = ["mean", "median", "mode", "min", "max", "range", "median_ad", "iqr", "p1",
+                   "p10", "p25", "p75", "p90", "p99", "energy", "rms", "qcod",
+                   "integrated_intensity", "edge_mean", "edge_min", "edge_max",
+                   "edge_integrated", "weighted_centroid_x", "weighted_centroid_y"]
+EXACT = {"intensity_" + n for n in EXACT_INTENSITY}
+UNIT_FLOOR = {"intensity_skewness", "intensity_hyperskewness"}
+HARALICK_UNIT = ("clushade", "corr", "infomeas1")
+
+
+def _moment_scales(intensity, labels, roi_labels):
+    """s_pq = sum w |x-cx|^p |y-cy|^q per ROI, for binary and weighted."""
+    ys, xs = np.nonzero(labels)
+    lab = labels[ys, xs]
+    val = intensity[ys, xs].astype(np.float64)
+    order = np.argsort(lab, kind="stable")
+    lab, xs, ys, val = lab[order], xs[order].astype(np.float64), ys[order].astype(np.float64), val[order]
+    bounds = np.searchsorted(lab, roi_labels), np.searchsorted(lab, roi_labels, side="right")
+    out = np.zeros((len(roi_labels), 2, 4, 4))
+    for k, (a, b) in enumerate(zip(*bounds)):
+        x, y, v = xs[a:b], ys[a:b], val[a:b]
+        for g, w in enumerate((np.ones_like(v), v)):
+            m = w.sum()
+            if m <= 0:
+                continue
+            ax = np.abs(x - (w * x).sum() / m)
+            ay = np.abs(y - (w * y).sum() / m)
+            for p in range(4):
+                for q in range(4):
+                    out[k, g, p, q] = (w * ax ** p * ay ** q).sum()
+    return out
+
+
+def floors(columns, ref_table, intensity=None, labels=None, roi_labels=None):
+    """Per-cell floor s (same shape as the table)."""
+    s = np.full(ref_table.shape, 1e-300)
+    col = {c: i for i, c in enumerate(columns)}
+    for c, i in col.items():
+        if c in UNIT_FLOOR:
+            s[:, i] = 1.0
+        if c.startswith("glcm_") and any(c.startswith("glcm_" + h + "_") for h in HARALICK_UNIT):
+            s[:, i] = 1.0
+    if "moments_mu00" in col and intensity is not None:
+        ms = _moment_scales(intensity, labels, roi_labels)
+        for g, pre in enumerate(("", "w")):
+            m00 = ref_table[:, col[f"moments_{pre}m00"]]
+            with np.errstate(divide="ignore", invalid="ignore"):
+                for p in range(4):
+                    for q in range(4):
+                        s[:, col[f"moments_{pre}mu{p}{q}"]] = np.maximum(ms[:, g, p, q], 1e-300)
+                        if p + q >= 2:
+                            se = ms[:, g, p, q] / np.power(m00, 1.0 + (p + q) / 2.0)
+                            s[:, col[f"moments_{pre}eta{p}{q}"]] = np.where(np.isfinite(se), se, 1.0)
+                e = {f"{p}{q}": np.abs(ref_table[:, col[f"moments_{pre}eta{p}{q}"]])
+                     for p in range(4) for q in range(4) if p + q >= 2}
+                s2 = e["20"] + e["02"] + 2 * e["11"]
+                s3 = e["30"] + 3 * e["12"] + 3 * e["21"] + e["03"]
+                hs = [s2, s2 ** 2, s3 ** 2, s3 ** 2, s3 ** 4, s2 * s3 ** 2, s3 ** 4]
+                for k in range(7):
+                    s[:, col[f"moments_{pre}hu{k + 1}"]] = np.maximum(hs[k], 1e-300)
+    return s
+
+
+def compare(columns, gpu, ref, s, tol_int=1e-9, tol_glcm=1e-6):
+    """Returns a list of (column, worst ratio, n_bad) for violating columns."""
+    bad = []
+    g, r = np.asarray(gpu), np.asarray(ref)
+    for i, c in enumerate(columns):
+        a, b = g[:, i], r[:, i]
+        if c in EXACT:
+            nb = int(np.count_nonzero(~((a == b) | (np.isnan(a) & np.isnan(b)))))
+            if nb:
+                bad.append((c, float("inf"), nb))
+            continue
+        tol = tol_glcm if c.startswith("glcm_") else tol_int
+        bound = tol * (np.maximum(np.abs(a), np.abs(b)) + s[:, i])
+        err = np.abs(a - b)
+        ok = (err <= bound) | (a == b)
+        if not ok.all():
+            ratio = float(np.max(np.where(ok, 0, err / np.maximum(bound, 1e-300))))
+            bad.append((c, ratio, int((~ok).sum())))
+    return bad
+
+
+def assert_parity(columns, gpu_labels, gpu, ref_labels, ref, intensity=None, labels=None):
+    assert np.array_equal(np.asarray(gpu_labels), np.asarray(ref_labels)), "label list differs"
+    assert gpu.shape == ref.shape, (gpu.shape, ref.shape)
+    s = floors(columns, ref, intensity, labels, np.asarray(ref_labels))
+    bad = compare(columns, gpu, ref, s)
+    assert not bad, "parity violations: " + "; ".join(f"{c} (x{r:.3g}, {n} rows)" for c, r, n in bad[:12])

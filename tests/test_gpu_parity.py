@@ -1,0 +1,162 @@
+"""GPU parity: the sm_100a path through the C ABI vs the oracle.
+
+The oracle is the C restatement (oracle/fx_oracle.c), itself pinned bit-for-bit
+against the compiled reference in test_oracle_pin.py; where the compiled
+reference (oracle/_ref) is present it is checked directly as well.
+"""
+import numpy as np
+import pytest
+
+import inputs
+from parity import assert_parity
+
+import paper_2603_12016_b200 as fx
+from oracle import make_params as oparams
+
+pytestmark = pytest.mark.gpu
+
+GROUPS = ["intensity", "moments", "glcm"]
+
+
+def both_params(profile="default", **over):
+    return fx.make_params(profile, **over), oparams(profile, **over)
+
+
+def check(ctx, oracle, I, L, groups, profile="default", **over):
+    gp, op = both_params(profile, **over)
+    cols = fx.feature_columns(groups, gp)
+    gl, gv = ctx.featurize(I, L, groups, gp)
+    ol, ov = oracle.featurize(I, L, groups, op)
+    assert_parity(cols, gl, gv, ol, ov, I, L)
+    return gl, gv
+
+
+@pytest.mark.parametrize("profile", ["default", "performance", "ibsi-like"])
+def test_c1_blob_grid_all_groups(ctx, oracle, profile):
+    L = fx.blob_mask_grid(1024, 421, 500, 1)
+    I = fx.uniform_u16(L.shape, 0)
+    gl, _ = check(ctx, oracle, I, L, GROUPS, profile)
+    assert len(gl) == 500
+
+
+@pytest.mark.parametrize("groups", [["intensity"], ["moments"], ["glcm"], ["intensity", "glcm"]])
+def test_group_subsets(ctx, oracle, groups):
+    L = fx.blob_mask_grid(512, 300, 100, 7)
+    I = fx.siemens_star(512)
+    check(ctx, oracle, I, L, groups)
+
+
+def test_tertiary_intensities(ctx, oracle):
+    L, _ = fx.packed_blob_mask_grid(768, 600, 250, 3)
+    I = inputs.per_roi_levels(L, 5)
+    check(ctx, oracle, I, L, GROUPS)
+
+
+@pytest.mark.parametrize("name", sorted(inputs.adversarial_masks()))
+def test_adversarial_masks(ctx, oracle, name):
+    L = inputs.adversarial_masks()[name]
+    for seed, I in enumerate([inputs.uniform(L.shape, 1), np.full(L.shape, 77, np.uint16),
+                              np.zeros(L.shape, np.uint16),
+                              np.full(L.shape, 65535, np.uint16)]):
+        check(ctx, oracle, I, L, GROUPS)
+        check(ctx, oracle, I, L, GROUPS, "performance")
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_random_blobs(ctx, oracle, seed):
+    L = inputs.random_blobs((96, 130), 40, seed=seed)
+    I = inputs.uniform(L.shape, seed)
+    check(ctx, oracle, I, L, GROUPS)
+
+
+@pytest.mark.parametrize("shape,n", [((20, 20), 6), ((64, 64), 9), ((150, 97), 5)])
+def test_random_label_masks_large_windows(ctx, oracle, shape, n):
+    """labels scattered over the whole image: windows exceed the S tile -> L path"""
+    L = inputs.random_labels(shape, n, seed=11)
+    I = inputs.uniform(shape, 2)
+    check(ctx, oracle, I, L, GROUPS)
+
+
+def test_large_roi_l_path(ctx, oracle):
+    yy, xx = np.mgrid[0:300, 0:260]
+    L = np.zeros((300, 260), np.uint16)
+    L[(xx - 130) ** 2 / 110.0 ** 2 + (yy - 150) ** 2 / 140.0 ** 2 <= 1] = 3
+    L[20:40, 10:200] = 9
+    I = inputs.uniform(L.shape, 9)
+    check(ctx, oracle, I, L, GROUPS)
+
+
+def test_odd_width_no_tma(ctx, oracle):
+    L = fx.blob_mask_grid(331, 200, 40, 2)[:, :329].copy()
+    I = inputs.uniform(L.shape, 4)
+    check(ctx, oracle, I, L, GROUPS)
+
+
+def test_histogram_bins_and_offsets(ctx, oracle):
+    L = fx.blob_mask_grid(256, 220, 25, 5)
+    I = inputs.uniform(L.shape, 6)
+    for over in [dict(histogram_bins=2), dict(histogram_bins=1000), dict(offset=2),
+                 dict(ng=2), dict(ng=7, symmetric=False, angles=(135, 0, 45)),
+                 dict(angles=(90, 90))]:
+        check(ctx, oracle, I, L, GROUPS, **over)
+
+
+def test_empty_mask(ctx):
+    L = np.zeros((64, 64), np.uint16)
+    I = inputs.uniform(L.shape, 0)
+    gl, gv = ctx.featurize(I, L, GROUPS)
+    assert len(gl) == 0 and gv.shape[0] == 0
+
+
+def test_label_scan_bit_exact(ctx, oracle):
+    for L in [fx.blob_mask_grid(1024, 421, 500, 1), inputs.random_labels((77, 1003), 300, 3),
+              inputs.random_blobs((257, 513), 200, seed=4,
+                                  label_values=np.array([1, 2, 65535, 40000, 17]))]:
+        gl, gc, gb = ctx.roi_table(np.zeros_like(L), L)
+        ol, oc, ob = oracle.roi_table(L)
+        assert np.array_equal(gl, ol) and np.array_equal(gc, oc) and np.array_equal(gb, ob)
+
+
+def test_debug_histogram_edges_glcm_bit_exact(ctx, oracle):
+    masks = inputs.adversarial_masks()
+    masks["blobs"] = fx.blob_mask_grid(256, 220, 25, 5)
+    p = fx.make_params("default", histogram_bins=16)
+    for name, L in masks.items():
+        I = inputs.uniform(L.shape, 3)
+        for lab in np.unique(L[L > 0])[:6]:
+            ys, xs = np.nonzero(L == lab)
+            vs = I[ys, xs]
+            hist, edge, glcm, pairs = ctx.debug_roi(I, L, int(lab), p)
+            assert np.array_equal(hist, oracle.intensity_hist(vs, 16)), name
+            pts = oracle.trace_contour(xs, ys)
+            assert set(map(tuple, edge.tolist())) == set(map(tuple, pts.tolist())), (name, lab)
+            for a, ang in enumerate(sorted(p.angles[: p.n_angles])):
+                cnt, pc = oracle.glcm_counts(xs, ys, vs, p.ng, p.offset, ang, p.symmetric)
+                assert pairs[a] == pc, (name, lab, ang)
+                assert np.array_equal(glcm[a].astype(np.uint64), cnt), (name, lab, ang)
+
+
+def test_per_roi_operator(ctx, oracle):
+    rng = np.random.default_rng(3)
+    for trial in range(10):
+        L = inputs.random_blobs((40, 40), 3, seed=trial, label_values=np.array([1]))
+        ys, xs = np.nonzero(L)
+        if len(xs) == 0:
+            continue
+        xs = xs + 1000 * trial
+        ys = ys + 37
+        vs = rng.integers(0, 4000, len(xs)).astype(np.uint16)
+        gp, op = both_params("default")
+        g = ctx.roi_features(xs, ys, vs, GROUPS, gp)
+        o = oracle.roi_features(xs, ys, vs, GROUPS, op)
+        assert_parity(fx.feature_columns(GROUPS, gp), [1], g[None], [1], o[None])
+
+
+def test_vs_compiled_reference(ctx, reference):
+    L = fx.blob_mask_grid(512, 300, 100, 7)
+    I = fx.uniform_u16(L.shape, 0)
+    gp, op = both_params("default")
+    cols = fx.feature_columns(GROUPS, gp)
+    gl, gv = ctx.featurize(I, L, GROUPS, gp)
+    rl, rv = reference.featurize(I, L, GROUPS, op)
+    assert_parity(cols, gl, gv, rl, rv, I, L)
