@@ -1,0 +1,317 @@
+#!/usr/bin/env python3
+"""Benchmark of the per-ROI featurization hot path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1], "C2"): one 8192x8192 uint16 intensity image
+(uniform, std::mt19937_64(seed)() & 0xffff) + uint16 label mask of ~50k
+disk-with-ears blobs (blob_mask_grid, seed 1, roi_size shrunk by 10% until it
+packs), feature groups intensity + moments (default profile).
+
+One step = one fx_featurize call over the whole image:
+  value : device-resident inputs (HBM) -> feature table in HBM; CUDA events on the
+          launching stream, K steps, max over ranks.  268 MB of rasters > 126 MB L2,
+          so no explicit flush is needed between steps.
+  e2e   : the same call through the C ABI with pinned HOST rasters and a HOST table
+          (H2D of both rasters + D2H of labels/table inside the timed region).
+N>1: one process per GPU (torchrun), each rank featurizes its own image (file
+sharding, no data-path collective) -> weak scaling; value = all ranks' MP / max time.
+
+--impl reference: the reference's own CPU implementation (oracle/_ref, compiled
+from /root/reference sources) on all host cores, rank 0 only.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+IMAGE = 8192
+ROI_COUNT = 50000
+ROI_SIZE0 = 400
+GROUPS = ["intensity", "moments"]
+PROFILE = "default"
+METRIC = "megapixels/s"
+UNIT = "MP/s"
+
+
+def workload(seed_intensity: int):
+    import paper_2603_12016_b200 as fx
+    labels, roi_size = fx.packed_blob_mask_grid(IMAGE, ROI_SIZE0, ROI_COUNT, 1)
+    intensity = fx.uniform_u16(labels.shape, seed_intensity)
+    return intensity, labels, roi_size
+
+
+def config_dict(roi_size, n_rois, fg_frac, n):
+    return {"workload": f"C2: {IMAGE}x{IMAGE} uint16 intensity + uint16 labels, "
+                        f"{n_rois} blob ROIs (roi_size {roi_size}, {fg_frac:.1%} fg), "
+                        f"groups {'+'.join(GROUPS)}, profile {PROFILE}",
+            "image": [IMAGE, IMAGE], "rois_per_image": int(n_rois), "groups": GROUPS,
+            "profile": PROFILE, "images_per_step": n, "sharding": "one image per GPU",
+            "l2": "inputs (268 MB) larger than L2 (126 MB); no flush"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled while the timed region runs."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.proc = index, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+            time.sleep(0.15)
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            time.sleep(0.1)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[0]))
+                mx = float(r[1])
+                for k, nm in enumerate(names):
+                    if r[3 + k].lower().startswith("active"):
+                        reasons.add(nm)
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def cpu_reference(intensity, labels, steps, warmup, threads=None):
+    """Reference CPU path (oracle/_ref): accumulate + OpenMP compute_roi_features."""
+    from oracle import Reference, make_params
+    ref = Reference()
+    threads = threads or ref.max_threads()
+    p = make_params(PROFILE)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        rl, rv = ref.featurize(intensity, labels, GROUPS, p, threads=threads)
+        dt = time.perf_counter() - t0
+        if i >= warmup:
+            times.append(dt)
+    return times, threads, len(rl)
+
+
+def run_reference_arm(args, rank, world):
+    if rank != 0:
+        return
+    intensity, labels, roi_size = workload(0)
+    n_rois = int(np.count_nonzero(np.bincount(labels.ravel(), minlength=65536)[1:]))
+    steps, warmup = max(1, min(args.steps, 3)), min(args.warmup, 1)
+    times, threads, nr = cpu_reference(intensity, labels, steps, warmup)
+    t = float(np.sum(times))
+    mp = IMAGE * IMAGE / 1e6
+    value = mp * len(times) / t
+    line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
+            "n_gpus": world, "steps": len(times), "warmup": warmup,
+            "ms_per_step": round(1e3 * t / len(times), 3), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": config_dict(roi_size, n_rois, float((labels > 0).mean()), 1),
+            "rois_per_s": round(nr * len(times) / t, 1),
+            "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads,
+                             "kind": "reference",
+                             "sample": f"full C2 image per step ({len(times)} steps, "
+                                       f"OpenMP over ROIs, {threads} threads)"},
+            "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(3, args.warmup)
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        run_reference_arm(args, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+
+    import paper_2603_12016_b200 as fx
+    intensity, labels, roi_size = workload(rank)  # each rank: its own image (file shard)
+    h, w = labels.shape
+    n_rois = int(np.count_nonzero(np.bincount(labels.ravel(), minlength=65536)[1:]))
+    params = fx.resolve_profile(PROFILE)
+    gmask = fx.resolve_groups(GROUPS)
+    ncols = len(fx.feature_columns(gmask, params))
+
+    ctx = fx.Context(local_rank)
+    stream = torch.cuda.current_stream()
+    ctx.set_stream(stream.cuda_stream)
+
+    # device-resident rasters and outputs
+    d_img = torch.from_numpy(intensity.view(np.int16).reshape(-1)).cuda()
+    d_lab = torch.from_numpy(labels.view(np.int16).reshape(-1)).cuda()
+    d_out = torch.empty((n_rois, ncols), dtype=torch.float64, device="cuda")
+    d_ol = torch.empty((n_rois,), dtype=torch.int32, device="cuda")
+
+    def step_device():
+        return ctx.featurize_device(d_img.data_ptr(), d_lab.data_ptr(), w, h, w, gmask, params,
+                                    d_ol.data_ptr(), d_out.data_ptr(), n_rois)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if dist is None:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        assert step_device() == n_rois
+    barrier()
+    ctx.enable_timing(True)
+    ctx.reset_kernel_times()
+    l0 = ctx.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local_rank) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step_device()
+        e1.record(stream)
+        barrier()
+    launches = ctx.launch_count() - l0
+    ktimes = ctx.kernel_times()
+    ctx.enable_timing(False)
+    t_dev = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+
+    # end-to-end through the C ABI with pinned host buffers
+    h_img = torch.from_numpy(intensity.view(np.int16)).pin_memory()
+    h_lab = torch.from_numpy(labels.view(np.int16)).pin_memory()
+    h_out = torch.empty((n_rois, ncols), dtype=torch.float64).pin_memory()
+    h_ol = torch.empty((n_rois,), dtype=torch.int32).pin_memory()
+
+    def step_e2e():
+        return ctx.featurize_host_ptrs(h_img.data_ptr(), h_lab.data_ptr(), w, h, gmask, params,
+                                       h_ol.data_ptr(), h_out.data_ptr(), n_rois)
+
+    for _ in range(2):
+        step_e2e()
+    e2e_steps = max(3, min(args.steps, 20))
+    barrier()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        step_e2e()
+    e1.record(stream)
+    barrier()
+    t_e2e = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    assert int(h_ol[0]) >= 1
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+
+    mp_step = h * w / 1e6
+    value = world * mp_step * args.steps / t_dev
+    e2e_value = world * mp_step * e2e_steps / t_e2e
+
+    # roofline of the dominant kernel (largest share of device time)
+    hbm, peak_src = peaks()
+    dom = max(ktimes.items(), key=lambda kv: kv[1][0])
+    dom_name, (dom_ms, dom_cnt) = dom[0], dom[1]
+    fg = int(np.count_nonzero(labels))
+    algo_bytes = {  # per launch, SURVEY.md 8(d) per-unit figures
+        "k_label_scan": h * w * 2,                      # label raster read once
+        "k_roi_s1": fg * 4 + n_rois * ncols * 8,        # ROI pixels (label+intensity) + table
+        "k_roi_s2": fg * 4 + n_rois * ncols * 8,
+    }
+    per_launch_s = dom_ms / 1e3 / max(1, dom_cnt)
+    achieved = algo_bytes.get(dom_name, h * w * 4 + n_rois * ncols * 8) / per_launch_s / 1e9
+    call_bytes = h * w * 4 + n_rois * ncols * 8
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(1e3 * t_dev / args.steps, 4), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": config_dict(roi_size, n_rois, fg / (h * w), world),
+        "rois_per_s": round(world * n_rois * args.steps / t_dev, 1),
+        "featurize_hbm_gbs": round(call_bytes / (t_dev / args.steps) / 1e9, 1),
+        "e2e": {"value": round(e2e_value, 2), "unit": UNIT,
+                "h2d_bytes_per_step": int(2 * h * w * 2),
+                "d2h_bytes_per_step": int(n_rois * ncols * 8 + n_rois * 4),
+                "steps": e2e_steps},
+        "gpu_launches": int(launches),
+        "kernels_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in ktimes.items()},
+        "roofline": {"kernel": dom_name, "bound": "hbm", "achieved": round(achieved, 1),
+                     "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
+                     "traffic": None, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": int(algo_bytes.get(dom_name, call_bytes))},
+        "clocks": clk.summary(),
+    }
+    if not args.no_cpu_baseline and world == 1:
+        times, threads, _ = cpu_reference(intensity, labels, 1, 0)
+        line["cpu_baseline"] = {"value": round(mp_step / times[0], 3), "unit": UNIT,
+                                "cores": threads, "kind": "reference",
+                                "sample": "one full C2 image (in-memory accumulate + OpenMP "
+                                          "compute_roi_features, oracle/_ref)"}
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -201,7 +201,7 @@ __device__ void union_rows(int h, int ext, Slab& S) {
 // ---- the pipeline ---------------------------------------------------------
 
 template <int WMAX, typename XY, bool TMA>
-__device__ void process_roi(const Job& J, Slab& S, const DevImage& img, const FeatCfg& cfg,
+__device__ __forceinline__ void process_roi(const Job& J, Slab& S, const DevImage& img, const FeatCfg& cfg,
                             double* __restrict__ out, const CUtensorMap* tmapL, uint64_t* mbar,
                             uint32_t& mbar_phase, Control* ctl, RoiList rl, int rank,
                             bool allow_overflow, const DebugOut* dbg) {
@@ -1005,10 +1005,10 @@ __device__ void process_roi(const Job& J, Slab& S, const DevImage& img, const Fe
 
 constexpr uint32_t kSmemSlack = 128 + 16;  // base alignment + mbarrier
 
-template <int CLS>
+template <int CLS, bool USE_TMA>
 __global__ void __launch_bounds__(32)
     k_roi_s(const __grid_constant__ CUtensorMap tmapL, DevImage img, RoiList rl, Control* ctl,
-            FeatCfg cfg, double* out, const DebugOut* dbg, int use_tma) {
+            FeatCfg cfg, double* out, const DebugOut* dbg) {
     extern __shared__ __align__(128) uint8_t smem_raw[];
     constexpr Layout L = CLS == kClassS1 ? kLayoutS1 : kLayoutS2;
     // TMA destinations need 128 B alignment; the dynamic base is only 16 B aligned
@@ -1027,7 +1027,7 @@ __global__ void __launch_bounds__(32)
         if (idx >= count) break;
         const uint32_t r = rl.cls_list[CLS][idx];
         Job J{rl.label[r], rl.x0[r], rl.y0[r], rl.w[r], rl.h[r], r, rl.n[r]};
-        if (use_tma) {
+        if constexpr (USE_TMA) {
             // TMA: the 72-wide x 8-row label boxes covering the window land in the
             // slab's staging tile and complete on the warp's mbarrier.  Issued in
             // the kernel body (inside process_roi ptxas emitted a faulting sequence).
@@ -1042,9 +1042,10 @@ __global__ void __launch_bounds__(32)
             __syncwarp();
             process_roi<1, uint16_t, true>(J, S, img, cfg, out, &tmapL, &mbar, phase, ctl, rl,
                                            (int)r, true, dbg);
-        } else
+        } else {
             process_roi<1, uint16_t, false>(J, S, img, cfg, out, &tmapL, &mbar, phase, ctl, rl,
                                             (int)r, true, dbg);
+        }
     }
 }
 
@@ -1077,26 +1078,34 @@ __global__ void __launch_bounds__(32)
 
 // ---- host-side launch helpers (keep template instantiation in this TU) ----
 
+template <int CLS, bool T>
+static cudaError_t setup_one(int* occ) {
+    constexpr uint32_t bytes = (CLS == kClassS1 ? kLayoutS1.bytes : kLayoutS2.bytes) + kSmemSlack;
+    cudaError_t e = cudaFuncSetAttribute(k_roi_s<CLS, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_roi_s<CLS, T>, 32, bytes);
+}
+
 cudaError_t roi_kernels_setup(int* occ_s1, int* occ_s2) {
-    cudaError_t e = cudaFuncSetAttribute(k_roi_s<kClassS1>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (kLayoutS1.bytes + kSmemSlack));
-    if (e != cudaSuccess) return e;
-    e = cudaFuncSetAttribute(k_roi_s<kClassS2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (kLayoutS2.bytes + kSmemSlack));
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ_s1, k_roi_s<kClassS1>, 32, (kLayoutS1.bytes + kSmemSlack));
-    if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ_s2, k_roi_s<kClassS2>, 32,
-                                                         (kLayoutS2.bytes + kSmemSlack));
+    int o = 0;
+    cudaError_t e = setup_one<kClassS1, true>(occ_s1);
+    if (e == cudaSuccess) e = setup_one<kClassS1, false>(&o);
+    if (e == cudaSuccess) e = setup_one<kClassS2, true>(occ_s2);
+    if (e == cudaSuccess) e = setup_one<kClassS2, false>(&o);
+    return e;
 }
 
 void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap, DevImage img,
                   RoiList rl, Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg,
                   int use_tma) {
-    if (cls == kClassS1)
-        k_roi_s<kClassS1><<<grid, 32, (kLayoutS1.bytes + kSmemSlack), s>>>(tmap, img, rl, ctl, cfg, out, dbg, use_tma);
-    else
-        k_roi_s<kClassS2><<<grid, 32, (kLayoutS2.bytes + kSmemSlack), s>>>(tmap, img, rl, ctl, cfg, out, dbg, use_tma);
+    const uint32_t b1 = kLayoutS1.bytes + kSmemSlack, b2 = kLayoutS2.bytes + kSmemSlack;
+    if (cls == kClassS1) {
+        if (use_tma) k_roi_s<kClassS1, true><<<grid, 32, b1, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
+        else k_roi_s<kClassS1, false><<<grid, 32, b1, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
+    } else {
+        if (use_tma) k_roi_s<kClassS2, true><<<grid, 32, b2, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
+        else k_roi_s<kClassS2, false><<<grid, 32, b2, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
+    }
 }
 
 void launch_roi_l(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
