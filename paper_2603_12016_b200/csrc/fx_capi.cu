@@ -28,10 +28,10 @@ __global__ void k_label_scan(const uint16_t* L, int W, int H, size_t pitch, int 
                              LabelTable t);
 __global__ void k_compact_count(LabelTable t, Control* ctl);
 __global__ void k_compact_emit(LabelTable t, Control* ctl, RoiList r);
-cudaError_t roi_kernels_setup(int* occ_s1, int* occ_s2);
-void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap, DevImage img,
-                  RoiList rl, Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg,
-                  int use_tma);
+cudaError_t roi_s2_setup(int* occ_s1, int* occ_s2);
+void launch_roi_s2(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap, DevImage img,
+                   RoiList rl, Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg,
+                   int use_tma);
 void launch_roi_l(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                   double* out, const DebugOut* dbg, uint8_t* scratch, const Layout& L);
 }  // namespace fxg
@@ -328,13 +328,13 @@ int run_pipeline(fx_ctx* c, const DevImage& img, unsigned groups, const fx_textu
     if (use_tma && getenv("FXG_TMA_DIAG")) use_tma = atoi(getenv("FXG_TMA_DIAG"));
     {
         Launch l(c, "k_roi_s1");
-        launch_roi_s(kClassS1, c->sm_count * c->occ_s1, s, tmap, img, rl, c->d_ctl, cfg, out_dev,
-                     dbg_dev, use_tma);
+        launch_roi_s2(kClassS1, c->sm_count * c->occ_s1, s, tmap, img, rl, c->d_ctl, cfg, out_dev,
+                      dbg_dev, use_tma);
     }
     {
         Launch l(c, "k_roi_s2");
-        launch_roi_s(kClassS2, c->sm_count * c->occ_s2, s, tmap, img, rl, c->d_ctl, cfg, out_dev,
-                     dbg_dev, use_tma);
+        launch_roi_s2(kClassS2, c->sm_count * c->occ_s2, s, tmap, img, rl, c->d_ctl, cfg, out_dev,
+                      dbg_dev, use_tma);
     }
     CK(cudaGetLastError());
     CK(cudaEventSynchronize(c->ev_stats));
@@ -463,7 +463,7 @@ int fx_ctx_create(int device, fx_ctx** out) {
     CKC(cudaMalloc(&c->d_roi32, 9 * kMaxLabels * sizeof(uint32_t)));
     CKC(cudaMalloc(&c->d_roin, kMaxLabels * sizeof(unsigned long long)));
     CKC(cudaMalloc(&c->d_dbg, sizeof(DebugOut)));
-    CKC(roi_kernels_setup(&c->occ_s1, &c->occ_s2));
+    CKC(roi_s2_setup(&c->occ_s1, &c->occ_s2));
     c->occ_s1 = std::max(1, c->occ_s1);
     c->occ_s2 = std::max(1, c->occ_s2);
     void* fn = nullptr;

@@ -1005,50 +1005,6 @@ __device__ __forceinline__ void process_roi(const Job& J, Slab& S, const DevImag
 
 constexpr uint32_t kSmemSlack = 128 + 16;  // base alignment + mbarrier
 
-template <int CLS, bool USE_TMA>
-__global__ void __launch_bounds__(32)
-    k_roi_s(const __grid_constant__ CUtensorMap tmapL, DevImage img, RoiList rl, Control* ctl,
-            FeatCfg cfg, double* out, const DebugOut* dbg) {
-    extern __shared__ __align__(128) uint8_t smem_raw[];
-    constexpr Layout L = CLS == kClassS1 ? kLayoutS1 : kLayoutS2;
-    // TMA destinations need 128 B alignment; the dynamic base is only 16 B aligned
-    uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
-    uint64_t& mbar = *reinterpret_cast<uint64_t*>(smem + L.bytes);
-    const unsigned lane = lane_id();
-    if (lane == 0) mbar_init(&mbar, 1);
-    __syncwarp();
-    uint32_t phase = 0;
-    Slab S = slab_at(smem, L);
-    const uint32_t count = ctl->class_count[CLS];
-    for (;;) {
-        uint32_t idx = 0;
-        if (lane == 0) idx = atomicAdd(&ctl->class_next[CLS], 1u);
-        idx = __shfl_sync(kFull, idx, 0);
-        if (idx >= count) break;
-        const uint32_t r = rl.cls_list[CLS][idx];
-        Job J{rl.label[r], rl.x0[r], rl.y0[r], rl.w[r], rl.h[r], r, rl.n[r]};
-        if constexpr (USE_TMA) {
-            // TMA: the 72-wide x 8-row label boxes covering the window land in the
-            // slab's staging tile and complete on the warp's mbarrier.  Issued in
-            // the kernel body (inside process_roi ptxas emitted a faulting sequence).
-            const int nbox = ((int)J.h + 7) >> 3;
-            if (lane == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(&mbar, (uint32_t)nbox * (uint32_t)(kStageW * 8 * 2));
-                for (int b = 0; b < nbox; ++b)
-                    tma_load_2d(S.stage + b * 8 * kStageW, &tmapL, &mbar, (int)(J.x0 & ~7u),
-                                (int)J.y0 + b * 8);
-            }
-            __syncwarp();
-            process_roi<1, uint16_t, true>(J, S, img, cfg, out, &tmapL, &mbar, phase, ctl, rl,
-                                           (int)r, true, dbg);
-        } else {
-            process_roi<1, uint16_t, false>(J, S, img, cfg, out, &tmapL, &mbar, phase, ctl, rl,
-                                            (int)r, true, dbg);
-        }
-    }
-}
-
 // L path: one warp per CTA, slab in global scratch, plain loads.  Consumes the
 // L class list, then the overflow list re-queued by the S kernels.
 __global__ void __launch_bounds__(32)
@@ -1077,36 +1033,6 @@ __global__ void __launch_bounds__(32)
 }
 
 // ---- host-side launch helpers (keep template instantiation in this TU) ----
-
-template <int CLS, bool T>
-static cudaError_t setup_one(int* occ) {
-    constexpr uint32_t bytes = (CLS == kClassS1 ? kLayoutS1.bytes : kLayoutS2.bytes) + kSmemSlack;
-    cudaError_t e = cudaFuncSetAttribute(k_roi_s<CLS, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-    if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_roi_s<CLS, T>, 32, bytes);
-}
-
-cudaError_t roi_kernels_setup(int* occ_s1, int* occ_s2) {
-    int o = 0;
-    cudaError_t e = setup_one<kClassS1, true>(occ_s1);
-    if (e == cudaSuccess) e = setup_one<kClassS1, false>(&o);
-    if (e == cudaSuccess) e = setup_one<kClassS2, true>(occ_s2);
-    if (e == cudaSuccess) e = setup_one<kClassS2, false>(&o);
-    return e;
-}
-
-void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap, DevImage img,
-                  RoiList rl, Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg,
-                  int use_tma) {
-    const uint32_t b1 = kLayoutS1.bytes + kSmemSlack, b2 = kLayoutS2.bytes + kSmemSlack;
-    if (cls == kClassS1) {
-        if (use_tma) k_roi_s<kClassS1, true><<<grid, 32, b1, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
-        else k_roi_s<kClassS1, false><<<grid, 32, b1, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
-    } else {
-        if (use_tma) k_roi_s<kClassS2, true><<<grid, 32, b2, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
-        else k_roi_s<kClassS2, false><<<grid, 32, b2, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
-    }
-}
 
 void launch_roi_l(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                   double* out, const DebugOut* dbg, uint8_t* scratch, const Layout& L) {

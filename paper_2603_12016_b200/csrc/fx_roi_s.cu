@@ -1,0 +1,1255 @@
+// S-class per-ROI kernels (window <= 64 x 64): one warp per ROI, lanes = window
+// rows.  Bit-parallel over u64 row masks wherever the reference works per
+// pixel.  See fx_roi.cuh for the reference mapping; the general (multi-word)
+// pipeline in fx_roi.cu serves the L class and the S slow paths.
+//
+// Phases (warp-synchronous, shared-memory slab per warp):
+//   load    TMA label boxes (72x8, x origin 16 B aligned) -> row masks via 16 B
+//           LDS; row offsets by warp scan; pixel coordinates; coalesced gather of
+//           member intensities; exact integer sums (order-free, bit-exact).
+//   sort    stable 2 x 8-bit LSD radix sort of the u16 values (one warp).
+//   stats   order statistics from the sorted multiset (bit-exact class), fp64
+//           central moments in a fixed order, histogram/mode by run detection.
+//   edge    trace_contour visited set (definition B): bit-parallel 4-connected
+//           exterior flood + 8-connected Euler number; when the ROI is one
+//           component without holes the edge set is K & dilate4(exterior);
+//           otherwise the run union-find slow path computes K and E.
+//   moments separable row sums about integer anchors, fp64, fixed-order
+//           reduce-scatter; binomial shift to the centroid and the origin.
+//   glcm    integer discretisation; canonical pair keys; radix sort; run-length
+//           counts; Haralick statistics from integer marginals.
+#include <math.h>
+
+#include "fx_roi.cuh"
+
+namespace fxg {
+
+namespace {
+
+constexpr int kTW = kStageW;  // staging tile row stride (u16)
+
+// ---- slab layout for S windows ---------------------------------------------
+struct SLayout {
+    uint32_t rowmask, rowoff, vals, xy;        // region A
+    uint32_t stage;                            // B: load
+    uint32_t tmp, sorted, cnt;                 // B: sort / stats
+    uint32_t kmask, emask, runoff, rs, re, parent, rsize;  // B: edge slow path
+    uint32_t lvl, keys, keys2, gcnt, marg;     // B: glcm
+    uint32_t bytes;
+};
+
+__host__ __device__ constexpr SLayout make_slayout(uint32_t NMAX, uint32_t RUNMAX) {
+    SLayout L{};
+    uint32_t o = 0;
+    L.rowmask = o;
+    o += kSH * 8;
+    L.rowoff = o;
+    o = al(o + (kSH + 1) * 4, 16);
+    L.vals = o;
+    o = al(o + NMAX * 2, 16);
+    L.xy = o;
+    o = al(o + NMAX * 2, 128);
+    const uint32_t B = o;
+    L.stage = B;
+    const uint32_t e_load = B + kTW * kSH * 2;
+    L.tmp = B;
+    L.sorted = al(L.tmp + NMAX * 2, 16);
+    L.cnt = al(L.sorted + NMAX * 2, 16);
+    const uint32_t e_sort = L.cnt + 512 * 4;
+    L.kmask = B;
+    L.emask = L.kmask + kSH * 8;
+    L.runoff = L.emask + kSH * 8;
+    L.rs = al(L.runoff + (kSH + 1) * 4, 16);
+    L.re = al(L.rs + RUNMAX * 2, 16);
+    L.parent = al(L.re + RUNMAX * 2, 16);
+    L.rsize = al(L.parent + RUNMAX * 4, 16);
+    const uint32_t e_edge = L.rsize + RUNMAX * 4;
+    L.lvl = B;
+    L.keys = al(L.lvl + NMAX, 16);
+    L.keys2 = al(L.keys + NMAX * 2, 16);
+    L.gcnt = al(L.keys2 + NMAX * 2, 16);
+    L.marg = L.gcnt + 512 * 4;
+    const uint32_t e_glcm = L.marg + 1280 * 4;
+    L.bytes = al(mx(mx(e_load, e_sort), mx(e_edge, e_glcm)), 128) + 128;  // + mbarrier
+    return L;
+}
+
+constexpr SLayout kSL1 = make_slayout(kS1N, 512);
+constexpr SLayout kSL2 = make_slayout(kS2N, 1024);
+constexpr uint32_t kSlack = 128;  // dynamic smem base alignment
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tWAIT%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra WAIT%=;\n\t}" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+
+// all lanes get sum_j v[k] over lanes for k < 8 (reduce-scatter + broadcast)
+__device__ __forceinline__ void warp_sum8(double (&v)[8]) {
+    const unsigned lane = lane_id();
+#pragma unroll
+    for (int s = 16, half = 4; s >= 4; s >>= 1, half >>= 1) {
+        const bool up = (lane & s) != 0;
+#pragma unroll
+        for (int j = 0; j < half; ++j) {
+            const double send = up ? v[j] : v[j + half];
+            const double recv = __shfl_xor_sync(kFull, send, s);
+            v[j] = (up ? v[j + half] : v[j]) + recv;
+        }
+    }
+    double t = v[0];
+    t += __shfl_xor_sync(kFull, t, 2);
+    t += __shfl_xor_sync(kFull, t, 1);
+    // lane L holds index ((L>>4)&1)<<2 | ((L>>3)&1)<<1 | ((L>>2)&1)
+#pragma unroll
+    for (int k = 0; k < 8; ++k) v[k] = __shfl_sync(kFull, t, ((k >> 2) << 4) | (((k >> 1) & 1) << 3) | ((k & 1) << 2));
+}
+
+// fill seeds s along the runs of f (both directions), Kogge-Stone
+__device__ __forceinline__ uint64_t run_fill(uint64_t f, uint64_t s) {
+    uint64_t g = s & f, p = f;
+    g |= p & (g << 1); p &= p << 1;
+    g |= p & (g << 2); p &= p << 2;
+    g |= p & (g << 4); p &= p << 4;
+    g |= p & (g << 8); p &= p << 8;
+    g |= p & (g << 16); p &= p << 16;
+    g |= p & (g << 32);
+    p = f;
+    g |= p & (g >> 1); p &= p >> 1;
+    g |= p & (g >> 2); p &= p >> 2;
+    g |= p & (g >> 4); p &= p >> 4;
+    g |= p & (g >> 8); p &= p >> 8;
+    g |= p & (g >> 16); p &= p >> 16;
+    g |= p & (g >> 32);
+    return g;
+}
+
+struct SJob {
+    uint32_t label, x0, y0, w, h, row;
+};
+
+// ---------------------------------------------------------------------------
+// Edge-set slow path (multiple 8-components or holes): run union-find for K,
+// then for the 4-connected exterior E.  Returns false on run-capacity overflow.
+// Writes K rows to km[] and E rows to em[] (lane-per-row layout).
+__device__ __noinline__ bool edge_sets_slow(const uint64_t* rowmask, int h, int w, uint64_t* km,
+                                            uint64_t* em, uint32_t* runoff, uint16_t* rs,
+                                            uint16_t* re, uint32_t* parent, uint32_t* rsize,
+                                            uint32_t runmax) {
+    const unsigned lane = lane_id();
+    auto build = [&](const uint64_t* m) -> uint32_t {
+        uint32_t total = 0;
+        for (int yb = 0; yb < h; yb += 32) {
+            const int y = yb + lane;
+            uint64_t r = (y < h) ? m[y] : 0ull;
+            const uint32_t c = __popcll(r & ~(r << 1));
+            const uint32_t incl = warp_incl_scan(c);
+            if (y < h) runoff[y] = total + incl - c;
+            total += __shfl_sync(kFull, incl, 31);
+        }
+        if (lane == 0) runoff[h] = total;
+        __syncwarp();
+        if (total > runmax) return ~0u;
+        for (int y = lane; y < h; y += 32) {
+            const uint64_t r = m[y];
+            uint64_t st = r & ~(r << 1), en = r & ~(r >> 1);
+            uint32_t j = runoff[y];
+            while (st) {
+                rs[j] = (uint16_t)(__ffsll((long long)st) - 1);
+                re[j] = (uint16_t)(__ffsll((long long)en) - 1);
+                st &= st - 1;
+                en &= en - 1;
+                ++j;
+            }
+        }
+        for (uint32_t r = lane; r < total; r += 32) parent[r] = r;
+        __syncwarp();
+        return total;
+    };
+    auto unite = [&](int ext) {
+        for (int y = 1 + lane; y < h; y += 32) {
+            uint32_t i = runoff[y], ie = runoff[y + 1], j = runoff[y - 1], je = runoff[y];
+            while (i < ie && j < je) {
+                const int as = rs[i], ae = re[i], bs = rs[j], be = re[j];
+                if (be + ext < as) ++j;
+                else if (ae + ext < bs) ++i;
+                else {
+                    uf_union(parent, i, j);
+                    if (ae < be) ++i;
+                    else ++j;
+                }
+            }
+        }
+        __syncwarp();
+        for (uint32_t r = lane; r < runoff[h]; r += 32) parent[r] = uf_find(parent, r);
+        __syncwarp();
+    };
+    const uint32_t nr = build(rowmask);
+    if (nr == ~0u) return false;
+    unite(1);
+    for (uint32_t r = lane; r < nr; r += 32) rsize[r] = 0;
+    __syncwarp();
+    for (uint32_t r = lane; r < nr; r += 32) atomicAdd(&rsize[parent[r]], (uint32_t)(re[r] - rs[r] + 1));
+    __syncwarp();
+    unsigned long long best = 0;
+    for (uint32_t r = lane; r < nr; r += 32)
+        if (parent[r] == r) {
+            const unsigned long long k = ((unsigned long long)rsize[r] << 32) | (0xffffffffu - r);
+            best = k > best ? k : best;
+        }
+    best = warp_max(best);
+    const uint32_t broot = 0xffffffffu - (uint32_t)(best & 0xffffffffu);
+    const uint64_t wm = (w >= 64) ? ~0ull : ((1ull << w) - 1ull);
+    for (int y = lane; y < h; y += 32) {
+        uint64_t k = 0;
+        for (uint32_t r = runoff[y]; r < runoff[y + 1]; ++r)
+            if (parent[r] == broot) k |= bits_between(rs[r], re[r]);
+        km[y] = k;
+        em[y] = ~k & wm;
+    }
+    __syncwarp();
+    const uint32_t nf = build(em);
+    if (nf == ~0u) return false;
+    unite(0);
+    for (uint32_t r = lane; r < nf; r += 32) rsize[r] = 0;
+    __syncwarp();
+    for (int y = lane; y < h; y += 32)
+        for (uint32_t r = runoff[y]; r < runoff[y + 1]; ++r)
+            if (y == 0 || y == h - 1 || rs[r] == 0 || re[r] == w - 1) rsize[parent[r]] = 1u;
+    __syncwarp();
+    for (int y = lane; y < h; y += 32) {
+        uint64_t e = 0;
+        for (uint32_t r = runoff[y]; r < runoff[y + 1]; ++r)
+            if (rsize[parent[r]]) e |= bits_between(rs[r], re[r]);
+        em[y] = e;
+    }
+    __syncwarp();
+    return true;
+}
+
+
+// scatter pass of a stable LSD radix sort; cnt[] holds exclusive digit offsets
+__device__ __forceinline__ void radix_scatter(const uint16_t* src, uint16_t* dst, uint32_t n,
+                                              int shift, uint32_t* cnt) {
+    const unsigned lane = lane_id();
+    for (uint32_t b0 = 0; b0 < n; b0 += 32) {
+        const uint32_t i = b0 + lane;
+        const bool ok = i < n;
+        const uint16_t key = ok ? src[i] : 0;
+        const uint32_t d = ok ? ((uint32_t)key >> shift) & 0xffu : 256u + lane;
+        const unsigned peers = __match_any_sync(kFull, d);
+        if (ok) dst[cnt[d] + __popc(peers & lanemask_lt())] = key;
+        __syncwarp();
+        if (ok && lane == (unsigned)(31 - __clz(peers))) cnt[d] += __popc(peers);
+        __syncwarp();
+    }
+}
+
+// Stable 16-bit LSD radix sort by one warp: both digit histograms in one pass,
+// the high-digit pass skipped when every key shares its high byte.  Returns the
+// buffer holding the sorted keys (tmp or dst).  cnt: 512 u32.
+__device__ __noinline__ const uint16_t* radix_sort16(const uint16_t* src, uint16_t* tmp,
+                                                     uint16_t* dst, uint32_t n, uint32_t* cnt) {
+    const unsigned lane = lane_id();
+    for (int i = lane; i < 512; i += 32) cnt[i] = 0;
+    __syncwarp();
+    for (uint32_t b0 = 0; b0 < n; b0 += 32) {
+        const uint32_t i = b0 + lane;
+        const bool ok = i < n;
+        const uint32_t key = ok ? src[i] : 0u;
+        const uint32_t d0 = ok ? key & 0xffu : 256u + lane, d1 = ok ? key >> 8 : 256u + lane;
+        const unsigned p0 = __match_any_sync(kFull, d0), p1 = __match_any_sync(kFull, d1);
+        if (ok && lane == (unsigned)(__ffs(p0) - 1)) cnt[d0] += __popc(p0);
+        if (ok && lane == (unsigned)(__ffs(p1) - 1)) cnt[256 + d1] += __popc(p1);
+        __syncwarp();
+    }
+    const bool one_high = n == 0 || cnt[256 + (src[0] >> 8)] == n;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+        uint32_t c[8], t = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            c[k] = cnt[h * 256 + lane * 8 + k];
+            t += c[k];
+        }
+        const uint32_t incl = warp_incl_scan(t);
+        uint32_t run = incl - t;
+        __syncwarp();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+            cnt[h * 256 + lane * 8 + k] = run;
+            run += c[k];
+        }
+    }
+    __syncwarp();
+    radix_scatter(src, tmp, n, 0, cnt);
+    if (one_high) return tmp;
+    radix_scatter(tmp, dst, n, 8, cnt + 256);
+    return dst;
+}
+
+
+__device__ __noinline__ double nlog2(double x) { return log2(x); }
+
+// log2 of small integers (run lengths / counts), filled once per process
+constexpr int kLog2Tab = 4096;
+__device__ double g_log2_tab[kLog2Tab + 1];
+__device__ __forceinline__ double log2_int(uint32_t c) {
+    return c <= (uint32_t)kLog2Tab ? __ldg(&g_log2_tab[c]) : nlog2((double)c);
+}
+__global__ void k_init_log2_tab() {
+    for (int i = threadIdx.x + blockIdx.x * blockDim.x; i <= kLog2Tab; i += blockDim.x * gridDim.x)
+        g_log2_tab[i] = i ? log2((double)i) : 0.0;
+}
+
+// k-th smallest (0-based) of |2 s[i] - M2| over sorted s by the whole warp:
+// 32-ary searches for the V split and the merge split of the two sorted halves.
+__device__ __noinline__ uint32_t kth_dev2_warp(const uint16_t* s, uint32_t n, uint32_t M2, uint32_t k) {
+    const unsigned lane = lane_id();
+    // m = first index with 2 s[i] >= M2 (in [0, n])
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+        const uint32_t step = (hi - lo + 31) / 32;
+        const uint32_t t = lo + lane * step;
+        const bool pr = t < hi && 2u * s[t] >= M2;
+        const unsigned b = __ballot_sync(kFull, pr);
+        if (b == 0) {
+            lo = lo + 31 * step + 1;
+            if (lo > hi) lo = hi;
+        } else {
+            const uint32_t f = __ffs(b) - 1;  // first lane whose probe is true
+            hi = lo + f * step;
+            lo = f ? lo + (f - 1) * step + 1 : lo;
+        }
+    }
+    const uint32_t m = lo, na = m, nb = n - m;
+    // smallest i in [ilo, ihi] with (i == ihi) or A[i] >= B[k-i]
+    uint32_t ilo = (k + 1 > nb) ? k + 1 - nb : 0, ihi = (k + 1 < na) ? k + 1 : na;
+    while (ilo < ihi) {
+        const uint32_t step = (ihi - ilo + 31) / 32;
+        const uint32_t i = ilo + lane * step;
+        bool pr = true;
+        if (i < ihi) {
+            const uint32_t Ai = M2 - 2u * s[m - 1 - i];
+            const uint32_t Bj1 = 2u * s[m + (k - i)] - M2;  // B[j-1], j = k+1-i
+            pr = !(Ai < Bj1);
+        }
+        const unsigned b = __ballot_sync(kFull, pr);
+        const uint32_t f = __ffs(b) - 1;
+        const uint32_t cand = ilo + f * step;
+        const uint32_t nhi = cand < ihi ? cand : ihi;
+        ilo = f ? ilo + (f - 1) * step + 1 : ilo;
+        ihi = nhi;
+    }
+    const uint32_t i = ilo, j = k + 1 - i;
+    uint32_t best = 0;
+    if (i > 0) best = M2 - 2u * s[m - i];
+    if (j > 0) {
+        const uint32_t b = 2u * s[m + j - 1] - M2;
+        if (i == 0 || b > best) best = b;
+    }
+    return best;
+}
+
+
+// GLCM group for an S window (ng <= 256): discretize (texture.cpp:45-53, exact
+// integer floor), pair keys per sorted angle (texture.cpp:58-80), radix sort,
+// run-length counts, Haralick statistics from integer marginals
+// (texture.cpp:87-217; hxy1 == hxy2 == hx + hy).
+__device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64_t* rowmask,
+                                          const uint32_t* rowoff, const uint16_t* vals,
+                                          uint8_t* lvl, uint16_t* keys, uint16_t* keys2,
+                                          uint32_t* gcnt, uint32_t* marg, uint32_t vmin,
+                                          uint32_t vmax, const FeatCfg& cfg, double* og,
+                                          const DebugOut* dbg) {
+    const unsigned lane = lane_id();
+    const int ng = cfg.ng, A = cfg.n_angles;
+    const uint32_t span = vmax - vmin + 1u;
+    for (uint32_t i = lane; i < n; i += 32) {
+        uint32_t lv = 0;
+        if (vmax > vmin) lv = min((uint32_t)(ng - 1), ((uint32_t)ng * (vals[i] - vmin)) / span);
+        lvl[i] = (uint8_t)lv;
+    }
+    __syncwarp();
+    const bool sym = cfg.symmetric != 0;
+    double sacc = 0;
+    for (int a = 0; a < A; ++a) {
+        const int ddx = cfg.dx[a], ddy = cfg.dy[a];
+        // pair keys, lane-per-row: bits x with (x,y) and (x+dx,y+dy) both in the ROI
+        uint64_t pm[2] = {0, 0};
+        uint32_t npr = 0;
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+            const int y = lane + 32 * hf, ny = y + ddy;
+            if (y < h && ny >= 0 && ny < h && ddx > -64 && ddx < 64) {
+                const uint64_t r = rowmask[ny];
+                const uint64_t sh = ddx >= 0 ? (r >> ddx) : (r << (-ddx));
+                pm[hf] = rowmask[y] & sh;
+            }
+            npr += __popcll(pm[hf]);
+        }
+        const uint32_t incl = warp_incl_scan(npr);
+        const uint32_t np = __shfl_sync(kFull, incl, 31);
+        uint32_t j = incl - npr;
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+            const int y = lane + 32 * hf, ny = y + ddy;
+            uint64_t m = pm[hf];
+            while (m) {
+                const int x = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                const uint32_t la = lvl[rowoff[y] + __popcll(rowmask[y] & ((1ull << x) - 1ull))];
+                const int nx = x + ddx;
+                const uint32_t lb = lvl[rowoff[ny] + __popcll(rowmask[ny] & ((1ull << nx) - 1ull))];
+                keys[j++] = (uint16_t)(sym ? min(la, lb) * (uint32_t)ng + max(la, lb)
+                                           : la * (uint32_t)ng + lb);
+            }
+        }
+        for (int k = lane; k < 1280; k += 32) marg[k] = 0;
+        __syncwarp();
+        double st[29];
+#pragma unroll
+        for (int k = 0; k < 29; ++k) st[k] = 0;
+        if (dbg && dbg->pairs && lane == 0) dbg->pairs[a] = np;
+        if (np > 0) {
+            const uint16_t* sk = radix_sort16(keys, keys2, keys, np, gcnt);
+            __syncwarp();
+            const double T = sym ? 2.0 * (double)np : (double)np;
+            const double logT = nlog2(T);
+            double asm_ = 0, ent = 0, acor = 0, jmax = 0;
+            uint32_t carry = 0;
+            for (uint32_t b0 = 0; b0 < np; b0 += 32) {
+                const uint32_t i = b0 + lane;
+                const bool ok = i < np;
+                const uint32_t k = ok ? sk[i] : 0u;
+                const bool st_ = ok && (i == 0 || sk[i - 1] != k);
+                const bool en_ = ok && (i + 1 == np || sk[i + 1] != k);
+                const unsigned sb = __ballot_sync(kFull, st_);
+                const unsigned le = lanemask_lt() | (1u << lane);
+                const uint32_t s0 = (sb & le) ? b0 + 31 - __clz(sb & le) : carry;
+                if (en_) {
+                    const uint32_t c = i - s0 + 1;
+                    const uint32_t ga = k / (uint32_t)ng, gb = k % (uint32_t)ng;
+                    const double gi = ga + 1.0, gj = gb + 1.0;
+                    const bool off = sym && ga != gb;
+                    const uint32_t cc = (sym && !off) ? 2u * c : c;
+                    const double p = (double)cc / T, mult = off ? 2.0 : 1.0;
+                    asm_ += mult * p * p;
+                    ent += mult * p * (logT - log2_int(cc));
+                    acor += mult * gi * gj * p;
+                    jmax = fmax(jmax, p);
+                    atomicAdd(&marg[ga], cc);
+                    atomicAdd(&marg[256 + gb], cc);
+                    atomicAdd(&marg[512 + ga + gb], off ? 2u * cc : cc);
+                    atomicAdd(&marg[1024 + (ga > gb ? ga - gb : gb - ga)], off ? 2u * cc : cc);
+                    if (off) {
+                        atomicAdd(&marg[gb], cc);
+                        atomicAdd(&marg[256 + ga], cc);
+                    }
+                    if (dbg && dbg->glcm) {
+                        dbg->glcm[((size_t)a * ng + ga) * ng + gb] = cc;
+                        if (off) dbg->glcm[((size_t)a * ng + gb) * ng + ga] = cc;
+                    }
+                }
+                if (sb) carry = b0 + 31 - __clz(sb);
+            }
+            __syncwarp();
+            double r8[8] = {asm_, ent, acor, 0, 0, 0, 0, 0};
+            jmax = warp_max(jmax);
+            // marginals px, py -> means (texture.cpp:127-131)
+            const double iT = 1.0 / T;
+            for (int g = lane; g < ng; g += 32) {
+                r8[3] += (g + 1) * ((double)marg[g] * iT);
+                r8[4] += (g + 1) * ((double)marg[256 + g] * iT);
+            }
+            // p_{x+y}: sum average and entropy; p_{x-y}: difference average/entropy
+            for (int k = lane; k < 2 * ng - 1; k += 32) {
+                const double p = (double)marg[512 + k] * iT;
+                if (p > 0) {
+                    r8[5] += (k + 2) * p;
+                    r8[6] -= p * nlog2(p);
+                }
+            }
+            for (int d = lane; d < ng; d += 32) {
+                const double p = (double)marg[1024 + d] * iT;
+                if (p > 0) r8[7] += d * p;
+            }
+            warp_sum8(r8);
+            const double mux = r8[3], muy = r8[4], sumave = r8[5], sument = r8[6], difave = r8[7];
+            double s8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // vx, vy, hx, hy, sumvar, clut, clus, clup
+            for (int g = lane; g < ng; g += 32) {
+                const double a1 = (double)marg[g] * iT, b1 = (double)marg[256 + g] * iT;
+                s8[0] += (g + 1 - mux) * (g + 1 - mux) * a1;
+                s8[1] += (g + 1 - muy) * (g + 1 - muy) * b1;
+                if (a1 > 0) s8[2] -= a1 * nlog2(a1);
+                if (b1 > 0) s8[3] -= b1 * nlog2(b1);
+            }
+            for (int k = lane; k < 2 * ng - 1; k += 32) {
+                const double p = (double)marg[512 + k] * iT;
+                if (p > 0) {
+                    s8[4] += (k + 2 - sumave) * (k + 2 - sumave) * p;
+                    const double s = k + 2 - mux - muy;
+                    s8[5] += s * s * p;
+                    s8[6] += s * s * s * p;
+                    s8[7] += s * s * s * s * p;
+                }
+            }
+            warp_sum8(s8);
+            double d8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // difent, contrast, idm, id, idn, idmn, iv, difvar
+            const double dng = (double)ng;
+            for (int d = lane; d < ng; d += 32) {
+                const double p = (double)marg[1024 + d] * iT;
+                if (p > 0) {
+                    const double dd = (double)d;
+                    d8[0] -= p * nlog2(p);
+                    d8[1] += dd * dd * p;
+                    d8[2] += p / (1.0 + dd * dd);
+                    d8[3] += p / (1.0 + dd);
+                    d8[4] += p / (1.0 + dd / dng);
+                    d8[5] += p / (1.0 + dd * dd / (dng * dng));
+                    if (d > 0) d8[6] += p / (dd * dd);
+                    d8[7] += (dd - difave) * (dd - difave) * p;
+                }
+            }
+            warp_sum8(d8);
+            const double vx = s8[0], vy = s8[1], hx = s8[2], hy = s8[3];
+            const double ent_ = r8[1], asm2 = r8[0], acor_ = r8[2];
+            const double corr = (vx > 0 && vy > 0) ? (acor_ - mux * muy) / sqrt(vx * vy) : 0.0;
+            const double hxy = hx + hy, hmax = fmax(hx, hy);
+            const double v29[29] = {asm2, acor_, s8[7], s8[6], s8[5], d8[1], corr, difave, d8[0],
+                                    d8[7], difave, sqrt(asm2), ent_, d8[3], d8[2], d8[3], d8[4],
+                                    d8[2], d8[5], hmax > 0 ? (ent_ - hxy) / hmax : 0.0,
+                                    sqrt(fmax(0.0, 1.0 - exp(-2.0 * (hxy - ent_)))), d8[6], mux,
+                                    ent_, jmax, vx, sumave, sument, s8[4]};
+#pragma unroll
+            for (int k = 0; k < 29; ++k) st[k] = v29[k];
+        }
+        double mine = 0;
+#pragma unroll
+        for (int k = 0; k < 29; ++k)
+            if ((int)lane == k) mine = st[k];
+        if (lane < 29) {
+            og[lane * (A + 1) + a] = mine;
+            sacc += mine;
+        }
+        __syncwarp();
+    }
+    if (lane < 29) og[lane * (A + 1) + A] = sacc / (double)A;
+    __syncwarp();
+}
+
+// ------------------------------------------------------------------------
+template <int NMAX, int RUNMAX>
+__device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8_t* base,
+                                          const DevImage& img, const FeatCfg& cfg,
+                                          double* __restrict__ out, uint64_t* mbar,
+                                          uint32_t& phase, Control* ctl, RoiList rl,
+                                          const DebugOut* dbg) {
+    const unsigned lane = lane_id();
+    const int w = (int)J.w, h = (int)J.h;
+    const uint32_t label = J.label;
+    uint64_t* rowmask = (uint64_t*)(base + L.rowmask);
+    uint32_t* rowoff = (uint32_t*)(base + L.rowoff);
+    uint16_t* vals = (uint16_t*)(base + L.vals);
+    uint16_t* xy = (uint16_t*)(base + L.xy);
+    const uint16_t* stage = (const uint16_t*)(base + L.stage);
+    double* orow = out + (size_t)J.row * cfg.ncols;
+    const bool dbg_on = dbg != nullptr && dbg->label == label;
+    const long long gx0 = (long long)img.ox + J.x0, gy0 = (long long)img.oy + J.y0;
+    const uint32_t xo = J.x0 & 7u;
+    const uint64_t wm = (w >= 64) ? ~0ull : ((1ull << w) - 1ull);
+
+    // ---------------------------------------------------------------- load
+    mbar_wait(mbar, phase);
+    phase ^= 1u;
+    // row masks: lane y reads its staged row 8 labels at a time (16 B LDS)
+    uint64_t m0 = 0, m1 = 0;  // rows lane, lane + 32
+#pragma unroll 1
+    for (int half = 0; half < 2; ++half) {
+        const int y = lane + 32 * half;
+        uint64_t m = 0;
+        if (y < h) {
+            const uint4* row = reinterpret_cast<const uint4*>(stage + y * kTW);
+            const int c_end = (int)((xo + w + 7) >> 3);
+#pragma unroll 1
+            for (int c = 0; c < c_end; ++c) {
+                const uint4 q = row[c];
+                const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
+                uint32_t bits = 0;
+#pragma unroll
+                for (int k = 0; k < 8; ++k)
+                    bits |= (uint32_t)(((wv[k >> 1] >> (16 * (k & 1))) & 0xffffu) == label) << k;
+                const int sh = c * 8 - (int)xo;  // pixel index of this chunk's bit 0
+                m |= sh >= 0 ? ((uint64_t)bits << sh) : ((uint64_t)bits >> (-sh));
+            }
+            m &= wm;
+        }
+        if (half == 0) m0 = m;
+        else m1 = m;
+    }
+    // row offsets (warp scan, row order)
+    const uint32_t c0 = __popcll(m0), c1 = __popcll(m1);
+    const uint32_t i0 = warp_incl_scan(c0);
+    const uint32_t tot0 = __shfl_sync(kFull, i0, 31);
+    const uint32_t i1 = warp_incl_scan(c1);
+    const uint32_t n = tot0 + __shfl_sync(kFull, i1, 31);
+    const uint32_t off0 = i0 - c0, off1 = tot0 + i1 - c1;
+    if ((int)lane < h) {
+        rowmask[lane] = m0;
+        rowoff[lane] = off0;
+    }
+    if ((int)lane + 32 < h) {
+        rowmask[lane + 32] = m1;
+        rowoff[lane + 32] = off1;
+    }
+    if (lane == 0) rowoff[h] = n;
+    // pixel coordinates in row-major order
+    {
+        uint64_t m = m0;
+        uint32_t j = off0;
+        while (m) {
+            xy[j++] = (uint16_t)((__ffsll((long long)m) - 1) | (lane << 8));
+            m &= m - 1;
+        }
+        m = m1;
+        j = off1;
+        while (m) {
+            xy[j++] = (uint16_t)((__ffsll((long long)m) - 1) | ((lane + 32) << 8));
+            m &= m - 1;
+        }
+    }
+    __syncwarp();
+    // gather member intensities (coalesced within rows), exact integer sums
+    unsigned long long sS = 0, sQ = 0, sXI = 0, sYI = 0;
+    uint32_t sLX = 0, sLY = 0;
+    {
+        const uint16_t* Ib = img.I + (size_t)J.y0 * img.pitch + J.x0;
+#pragma unroll 1
+        for (uint32_t b0 = 0; b0 < n; b0 += 32 * 8) {
+            uint16_t v[8];
+            uint32_t p[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = b0 + u * 32 + lane;
+                p[u] = i < n ? xy[i] : 0u;
+                v[u] = i < n ? __ldg(Ib + (size_t)(p[u] >> 8) * img.pitch + (p[u] & 0xffu)) : 0;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t i = b0 + u * 32 + lane;
+                if (i < n) {
+                    vals[i] = v[u];
+                    const uint32_t x = p[u] & 0xffu, y = p[u] >> 8;
+                    sS += v[u];
+                    sQ += (unsigned long long)((uint32_t)v[u] * (uint32_t)v[u]);
+                    sXI += (unsigned long long)((uint32_t)v[u] * x);
+                    sYI += (unsigned long long)((uint32_t)v[u] * y);
+                    sLX += x;
+                    sLY += y;
+                }
+            }
+        }
+        sS = warp_sum(sS);
+        sQ = warp_sum(sQ);
+        sXI = warp_sum(sXI);
+        sYI = warp_sum(sYI);
+        sLX = warp_sum(sLX);
+        sLY = warp_sum(sLY);
+    }
+    __syncwarp();
+    const double dn = (double)n;
+    uint32_t vmin = 0, vmax = 0;
+    bool have_minmax = false;
+
+    // ----------------------------------------------------------- intensity
+    if (cfg.col_int >= 0) {
+        const uint16_t* s = radix_sort16(vals, (uint16_t*)(base + L.tmp),
+                                         (uint16_t*)(base + L.sorted), n,
+                                         (uint32_t*)(base + L.cnt));
+        __syncwarp();
+        vmin = s[0];
+        vmax = s[n - 1];
+        have_minmax = true;
+        const double mean = (double)sS / dn;
+        const double mn = (double)vmin, mxv = (double)vmax, range = mxv - mn;
+        const double median =
+            (n & 1) ? (double)s[n / 2] : 0.5 * ((double)s[n / 2 - 1] + (double)s[n / 2]);
+        // percentiles (lanes 0..5), literal expression (intensity_features.cpp:14-22)
+        double myp = 0;
+        if (lane < 6) {
+            const double pv = lane == 0 ? 1.0 : lane == 1 ? 10.0 : lane == 2 ? 25.0
+                            : lane == 3 ? 75.0 : lane == 4 ? 90.0 : 99.0;
+            myp = percentile_exact(s, n, pv);
+        }
+        const double p10 = __shfl_sync(kFull, myp, 1), p25 = __shfl_sync(kFull, myp, 2);
+        const double p75 = __shfl_sync(kFull, myp, 3), p90 = __shfl_sync(kFull, myp, 4);
+        // median absolute deviation (exact: k-th of the two sorted half-sequences)
+        const uint32_t M2 = (n & 1) ? 2u * s[n / 2] : (uint32_t)s[n / 2 - 1] + s[n / 2];
+        const uint32_t d_hi = kth_dev2_warp(s, n, M2, n / 2);
+        const uint32_t d_lo = (n & 1) ? d_hi : kth_dev2_warp(s, n, M2, n / 2 - 1);
+        const double median_ad = (n & 1) ? 0.5 * (double)d_hi
+                                         : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
+        // one pass over the sorted values: central moments (fp64), exact integer
+        // partial sums for mad and the [p10,p90] subset, value runs (mode) and
+        // histogram-bin runs (entropy = sum c (log2 n - log2 c) / n, uniformity =
+        // sum c^2 / n^2; bins = floor(nb (v - min) / range), exact, A2)
+        const uint32_t nb32 = (uint32_t)cfg.bins;
+        const bool wide = (unsigned long long)nb32 * 65535ull >= (1ull << 32);
+        const uint32_t rng = vmax - vmin;
+        auto bin_of = [&](uint32_t v) -> uint32_t {
+            if (rng == 0) return 0u;
+            const uint32_t b = wide ? (uint32_t)((unsigned long long)nb32 * (v - vmin) / rng)
+                                    : (nb32 * (v - vmin)) / rng;
+            return b < nb32 - 1 ? b : nb32 - 1;
+        };
+        const double logn = nlog2(dn);
+        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // m2..m6, entropy sum
+        unsigned long long best = 0, slo = 0, rsum = 0, usq = 0;
+        uint32_t clo = 0, rn = 0, carry_v = 0, carry_b = 0;
+        uint32_t prev_v = 0xffffffffu, prev_b = 0xffffffffu;
+#pragma unroll 1
+        for (uint32_t b0 = 0; b0 < n; b0 += 32) {
+            const uint32_t i = b0 + lane;
+            const bool ok = i < n;
+            const uint32_t v = ok ? s[i] : 0xfffffffeu;
+            const uint32_t bin = ok ? bin_of(v) : 0xfffffffeu;
+            const uint32_t nxt = b0 + 32 < n ? s[b0 + 32] : 0xfffffffeu;  // next chunk head
+            uint32_t pv = __shfl_up_sync(kFull, v, 1), pb = __shfl_up_sync(kFull, bin, 1);
+            uint32_t nv = __shfl_down_sync(kFull, v, 1), nbn = __shfl_down_sync(kFull, bin, 1);
+            if (lane == 0) {
+                pv = prev_v;
+                pb = prev_b;
+            }
+            if (lane == 31) {
+                nv = nxt;
+                nbn = b0 + 32 < n ? bin_of(nxt) : 0xfffffffeu;
+            }
+            if (i + 1 == n) {
+                nv = 0xfffffffdu;
+                nbn = 0xfffffffdu;
+            }
+            const bool vstart = ok && pv != v, vend = ok && nv != v;
+            const bool bstart = ok && pb != bin, bend = ok && nbn != bin;
+            const unsigned vs = __ballot_sync(kFull, vstart), bs = __ballot_sync(kFull, bstart);
+            const unsigned le = lanemask_lt() | (1u << lane);
+            if (ok) {
+                const double d = (double)v - mean;
+                const double d2 = d * d;
+                acc[0] += d2;
+                acc[1] += d2 * d;
+                acc[2] += d2 * d2;
+                acc[3] += d2 * d2 * d;
+                acc[4] += d2 * d2 * d2;
+                if ((double)v < mean) {
+                    slo += v;
+                    ++clo;
+                }
+                const double x = (double)v;
+                if (x >= p10 && x <= p90) {
+                    rsum += v;
+                    ++rn;
+                }
+                if (vend) {
+                    const uint32_t st = (vs & le) ? b0 + 31 - __clz(vs & le) : carry_v;
+                    const unsigned long long key =
+                        ((unsigned long long)(i - st + 1) << 16) | (0xffffu - v);
+                    best = key > best ? key : best;
+                }
+                if (bend) {
+                    const uint32_t st = (bs & le) ? b0 + 31 - __clz(bs & le) : carry_b;
+                    const uint32_t c = i - st + 1;
+                    acc[5] += (double)c * (logn - log2_int(c));
+                    usq += (unsigned long long)c * c;
+                    if (dbg_on && bin < nb32) dbg->hist[bin] = c;
+                }
+            }
+            if (vs) carry_v = b0 + 31 - __clz(vs);
+            if (bs) carry_b = b0 + 31 - __clz(bs);
+            prev_v = __shfl_sync(kFull, v, 31);
+            prev_b = __shfl_sync(kFull, bin, 31);
+        }
+        warp_sum8(acc);
+        best = warp_max(best);
+        slo = warp_sum(slo);
+        clo = warp_sum(clo);
+        rsum = warp_sum(rsum);
+        rn = warp_sum(rn);
+        usq = warp_sum(usq);
+        const double m2 = acc[0] / dn, m3 = acc[1] / dn, m4 = acc[2] / dn, m5 = acc[3] / dn,
+                     m6 = acc[4] / dn;
+        // sum |x - mean| = (S_hi - S_lo) + (c_lo - c_hi) mean, exact integer parts
+        const double mad = ((double)(long long)(sS - 2 * slo) +
+                            (double)((long long)clo - (long long)(n - clo)) * mean) / dn;
+        const double entropy = acc[5] / dn;
+        const double uniformity = (double)usq / (dn * dn);
+        double rmad = 0;
+        if (rn > 0) {
+            const double rmean = (double)rsum / (double)rn;
+            unsigned long long rlo = 0;
+            uint32_t rcl = 0;
+#pragma unroll 1
+            for (uint32_t i = lane; i < n; i += 32) {
+                const double x = (double)s[i];
+                if (x >= p10 && x <= p90 && x < rmean) {
+                    rlo += s[i];
+                    ++rcl;
+                }
+            }
+            rlo = warp_sum(rlo);
+            rcl = warp_sum(rcl);
+            rmad = ((double)(long long)(rsum - 2 * rlo) +
+                    (double)((long long)rcl - (long long)(rn - rcl)) * rmean) / (double)rn;
+        }
+        // ------------------------------------------------ edge set
+        double e_mean = 0, e_min = 0, e_max = 0, e_std = 0, e_int = 0;
+        {
+            uint64_t* km = (uint64_t*)(base + L.kmask);
+            uint64_t* em = (uint64_t*)(base + L.emask);
+            bool fast = w <= 62;
+            uint64_t k0 = m0, k1 = m1, e0 = 0, e1 = 0;
+            if (fast) {
+                // 4-connected exterior flood of the free cells, seeded on the border
+                const uint64_t f0 = ((int)lane < h) ? (~m0 & wm) : 0ull;
+                const uint64_t f1 = ((int)lane + 32 < h) ? (~m1 & wm) : 0ull;
+                const uint64_t side = 1ull | (1ull << (w - 1));
+                e0 = run_fill(f0, (lane == 0 || (int)lane == h - 1) ? f0 : (f0 & side));
+                e1 = run_fill(f1, ((int)lane + 32 == h - 1) ? f1 : (f1 & side));
+                for (int it = 0; it < 4 * kSH * kSW; ++it) {
+                    const uint64_t up0 = __shfl_up_sync(kFull, e0, 1);
+                    const uint64_t dn0 = __shfl_down_sync(kFull, e0, 1);
+                    const uint64_t up1 = __shfl_up_sync(kFull, e1, 1);
+                    const uint64_t dn1 = __shfl_down_sync(kFull, e1, 1);
+                    const uint64_t l31 = __shfl_sync(kFull, e0, 31), f32 = __shfl_sync(kFull, e1, 0);
+                    const uint64_t a0 = (lane == 0 ? 0ull : up0) | (lane == 31 ? f32 : dn0);
+                    const uint64_t a1 = (lane == 0 ? l31 : up1) | (lane == 31 ? 0ull : dn1);
+                    const uint64_t n0 = run_fill(f0, e0 | (a0 & f0));
+                    const uint64_t n1 = run_fill(f1, e1 | (a1 & f1));
+                    const bool ch = (n0 != e0) || (n1 != e1);
+                    e0 = n0;
+                    e1 = n1;
+                    if (!__any_sync(kFull, ch)) break;
+                }
+                // holes: free cells not reached
+                const bool hole = ((f0 & ~e0) | (f1 & ~e1)) != 0ull;
+                // 8-connected Euler number of the padded window (bit quads)
+                int q = 0;
+                {
+                    const uint64_t vm = (w >= 63) ? ~0ull : ((2ull << w) - 1ull);  // quads 0..w
+                    auto quads = [&](uint64_t a, uint64_t b) {
+                        const uint64_t A0 = a << 1, A1 = a, B0 = b << 1, B1 = b;  // padded
+                        const uint64_t s1 = A0 ^ A1, s2 = B0 ^ B1, c = (A0 & A1) | (B0 & B1);
+                        const uint64_t one = (s1 ^ s2) & ~c & vm, three = (s1 ^ s2) & c & vm;
+                        const uint64_t dg = ((A0 & B1 & ~A1 & ~B0) | (A1 & B0 & ~A0 & ~B1)) & vm;
+                        return __popcll(one) - __popcll(three) - 2 * __popcll(dg);
+                    };
+                    const uint64_t pm0 = __shfl_up_sync(kFull, m0, 1), pm1 = __shfl_up_sync(kFull, m1, 1);
+                    const uint64_t l31 = __shfl_sync(kFull, m0, 31);
+                    // row pairs (y-1, y) for y = 0..h  (rows -1 and h are empty)
+                    if ((int)lane <= h) q += quads(lane == 0 ? 0ull : pm0, (int)lane < h ? m0 : 0ull);
+                    if ((int)lane + 32 <= h)
+                        q += quads(lane == 0 ? l31 : pm1, (int)lane + 32 < h ? m1 : 0ull);
+                    q = warp_sum(q);
+                }
+                fast = !__any_sync(kFull, hole) && q == 4;  // one component, no holes
+            }
+            if (!fast) {
+                if ((int)lane < h) km[lane] = m0;
+                if ((int)lane + 32 < h) km[lane + 32] = m1;
+                __syncwarp();
+                const bool ok = edge_sets_slow(rowmask, h, w, km, em, (uint32_t*)(base + L.runoff),
+                                               (uint16_t*)(base + L.rs), (uint16_t*)(base + L.re),
+                                               (uint32_t*)(base + L.parent),
+                                               (uint32_t*)(base + L.rsize), (uint32_t)RUNMAX);
+                if (!ok) {  // run capacity: re-queue this ROI to the general path
+                    if (lane == 0) {
+                        const uint32_t pos = atomicAdd(&ctl->overflow_count, 1u);
+                        rl.overflow[pos] = J.row;
+                    }
+                    __syncwarp();
+                    return;
+                }
+                k0 = (int)lane < h ? km[lane] : 0ull;
+                k1 = (int)lane + 32 < h ? km[lane + 32] : 0ull;
+                e0 = (int)lane < h ? em[lane] : 0ull;
+                e1 = (int)lane + 32 < h ? em[lane + 32] : 0ull;
+                __syncwarp();
+            }
+            // edge = K & (4-neighbour in E, or on the window border)
+            const uint64_t eu0 = __shfl_up_sync(kFull, e0, 1), ed0 = __shfl_down_sync(kFull, e0, 1);
+            const uint64_t eu1 = __shfl_up_sync(kFull, e1, 1), ed1 = __shfl_down_sync(kFull, e1, 1);
+            const uint64_t el31 = __shfl_sync(kFull, e0, 31), ef32 = __shfl_sync(kFull, e1, 0);
+            const uint64_t side = 1ull | (1ull << (w - 1));
+            uint64_t g0 = (e0 << 1) | (e0 >> 1) | (lane == 0 ? 0ull : eu0) | (lane == 31 ? ef32 : ed0) | side;
+            uint64_t g1 = (e1 << 1) | (e1 >> 1) | (lane == 0 ? el31 : eu1) | (lane == 31 ? 0ull : ed1) | side;
+            if (lane == 0 || (int)lane == h - 1) g0 = ~0ull;
+            if ((int)lane + 32 == h - 1) g1 = ~0ull;
+            const uint64_t ed[2] = {(int)lane < h ? (k0 & g0) : 0ull, (int)lane + 32 < h ? (k1 & g1) : 0ull};
+            const uint64_t rm[2] = {m0, m1};
+            const uint32_t ro[2] = {off0, off1};
+            // one pass: exact integer sum and sum of squares -> mean, population std
+            unsigned long long es = 0, esq = 0;
+            uint32_t en = 0, emn = 0xffffffffu, emx = 0;
+#pragma unroll
+            for (int hf = 0; hf < 2; ++hf) {
+                uint64_t e = ed[hf];
+                while (e) {
+                    const int b = __ffsll((long long)e) - 1;
+                    e &= e - 1;
+                    const uint32_t v = vals[ro[hf] + __popcll(rm[hf] & ((1ull << b) - 1ull))];
+                    es += v;
+                    esq += (unsigned long long)(v * v);
+                    ++en;
+                    emn = min(emn, v);
+                    emx = max(emx, v);
+                }
+            }
+            es = warp_sum(es);
+            esq = warp_sum(esq);
+            en = warp_sum(en);
+            emn = warp_min(emn);
+            emx = warp_max(emx);
+            if (en) {
+                const double den = (double)en;
+                e_mean = (double)es / den;
+                e_min = (double)emn;
+                e_max = (double)emx;
+                e_int = (double)es;
+                // n^2 var = n sum v^2 - (sum v)^2, exact in u64 (< 2^56 for S windows)
+                e_std = sqrt((double)(en * esq - es * es) / (den * den));
+            }
+            if (dbg_on) {
+                uint32_t cnt_e = __popcll(ed[0]) + __popcll(ed[1]);
+                const uint32_t incl = warp_incl_scan(cnt_e);
+                uint32_t j = incl - cnt_e;
+#pragma unroll
+                for (int hf = 0; hf < 2; ++hf) {
+                    uint64_t e = ed[hf];
+                    while (e) {
+                        const int b = __ffsll((long long)e) - 1;
+                        e &= e - 1;
+                        if (j < dbg->cap_edge) {
+                            dbg->edge_xy[2 * j] = (int32_t)(gx0 + b);
+                            dbg->edge_xy[2 * j + 1] = (int32_t)(gy0 + lane + 32 * hf);
+                        }
+                        ++j;
+                    }
+                }
+                if (lane == 31) *dbg->n_edge = j;
+            }
+        }
+        double wcx = 0, wcy = 0;
+        if (sS > 0) {
+            wcx = (double)((unsigned long long)gx0 * sS + sXI) / (double)sS;
+            wcy = (double)((unsigned long long)gy0 * sS + sYI) / (double)sS;
+        }
+        const double var = n > 1 ? m2 * dn / (dn - 1.0) : 0.0;
+        double skew = 0, kurt = 0, hsk = 0, hfl = 0;
+        if (m2 > 0) {
+            const double r2 = sqrt(m2);
+            skew = m3 / (m2 * r2);
+            kurt = m4 / (m2 * m2);
+            hsk = m5 / (m2 * m2 * r2);
+            hfl = m6 / (m2 * m2 * m2);
+        }
+        const double mode = (double)(0xffffu - (uint32_t)(best & 0xffffu));
+        const double energy = (double)sQ, sdev = sqrt(var);
+        const double iqr = p75 - p25;
+        // lane k writes column k (coalesced row segment); columns 32..38 by lanes 0..6
+        const double pct = __shfl_sync(kFull, myp, (lane - 14) & 31);
+        double o = 0;
+        switch (lane) {
+            case 0: o = mean; break;
+            case 1: o = median; break;
+            case 2: o = mode; break;
+            case 3: o = mn; break;
+            case 4: o = mxv; break;
+            case 5: o = range; break;
+            case 6: o = var; break;
+            case 7: o = m2; break;
+            case 8: o = sdev; break;
+            case 9: o = sqrt(m2); break;
+            case 10: o = mad; break;
+            case 11: o = median_ad; break;
+            case 12: o = rmad; break;
+            case 13: o = iqr; break;
+            case 14: case 15: case 16: case 17: case 18: case 19: o = pct; break;
+            case 20: o = skew; break;
+            case 21: o = kurt; break;
+            case 22: o = m2 > 0 ? kurt - 3.0 : 0.0; break;
+            case 23: o = hsk; break;
+            case 24: o = hfl; break;
+            case 25: o = energy; break;
+            case 26: o = sqrt(energy / dn); break;
+            case 27: o = entropy; break;
+            case 28: o = uniformity; break;
+            case 29: o = (p75 + p25) != 0 ? iqr / (p75 + p25) : 0.0; break;
+            case 30: o = mean != 0 ? sdev / mean : 0.0; break;
+            default: o = (double)sS; break;
+        }
+        double* oi = orow + cfg.col_int;
+        oi[lane] = o;
+        if (lane < 7) {
+            const double t[7] = {e_mean, e_min, e_max, e_std, e_int, wcx, wcy};
+            double v = t[0];
+#pragma unroll
+            for (int k = 1; k < 7; ++k)
+                if ((int)lane == k) v = t[k];
+            oi[32 + lane] = v;
+        }
+        __syncwarp();
+    }
+
+    // ------------------------------------------------------------- moments
+    if (cfg.col_mom >= 0) {
+        const long long nn = (long long)n, W = (long long)sS;
+        const long long axb = (2 * (long long)sLX + nn) / (2 * nn);
+        const long long ayb = (2 * (long long)sLY + nn) / (2 * nn);
+        const long long axw = W > 0 ? (2 * (long long)sXI + W) / (2 * W) : 0;
+        const long long ayw = W > 0 ? (2 * (long long)sYI + W) / (2 * W) : 0;
+        double acc[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc[k] = 0;
+        const int nhalf = h > 32 ? 2 : 1;
+#pragma unroll 1
+        for (int hf = 0; hf < nhalf; ++hf) {
+            const int y = lane + 32 * hf;
+            uint64_t m = hf ? m1 : m0;
+            uint32_t idx = hf ? off1 : off0;
+            double rb1 = 0, rb2 = 0, rb3 = 0, rw0 = 0, rw1 = 0, rw2 = 0, rw3 = 0;
+            const double cb = (double)__popcll(m);
+            while (m) {
+                const int x = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                const double wv = (double)vals[idx++];
+                const double db = (double)(x - axb), dw = (double)(x - axw);
+                const double db2 = db * db, dw2 = dw * dw;
+                rb1 += db;
+                rb2 += db2;
+                rb3 += db2 * db;
+                rw0 += wv;
+                rw1 += wv * dw;
+                rw2 += wv * dw2;
+                rw3 += wv * dw2 * dw;
+            }
+            const double yb = (double)((long long)y - ayb), yw = (double)((long long)y - ayw);
+            const double rb[4] = {cb, rb1, rb2, rb3}, rw[4] = {rw0, rw1, rw2, rw3};
+            const double qb[4] = {1.0, yb, yb * yb, yb * yb * yb};
+            const double qw[4] = {1.0, yw, yw * yw, yw * yw * yw};
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc[p * 4 + q] += rb[p] * qb[q];
+                    acc[16 + p * 4 + q] += rw[p] * qw[q];
+                }
+        }
+        const double N = reduce_scatter32(acc);
+        const int grp = lane >> 4, p = (lane >> 2) & 3, q = lane & 3;
+        const double m00 = grp ? (double)sS : dn;
+        const bool zero_mass = grp && sS == 0;
+        const double dx = grp ? (W > 0 ? (double)((long long)sXI - axw * W) / (double)W : 0.0)
+                              : (double)((long long)sLX - axb * nn) / dn;
+        const double dy = grp ? (W > 0 ? (double)((long long)sYI - ayw * W) / (double)W : 0.0)
+                              : (double)((long long)sLY - ayb * nn) / dn;
+        const double Ax = (double)(gx0 + (grp ? axw : axb)), Ay = (double)(gy0 + (grp ? ayw : ayb));
+        const double C[4][4] = {{1, 0, 0, 0}, {1, 1, 0, 0}, {1, 2, 1, 0}, {1, 3, 3, 1}};
+        double pmx[4], pmy[4], pax[4], pay[4];
+        pmx[0] = pmy[0] = pax[0] = pay[0] = 1.0;
+#pragma unroll
+        for (int k = 1; k < 4; ++k) {
+            pmx[k] = pmx[k - 1] * (-dx);
+            pmy[k] = pmy[k - 1] * (-dy);
+            pax[k] = pax[k - 1] * Ax;
+            pay[k] = pay[k - 1] * Ay;
+        }
+        double mu = 0, raw = 0;
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const double Nij = __shfl_sync(kFull, N, (grp << 4) | (i << 2) | j);
+                if (i <= p && j <= q) {
+                    const double cc = C[p][i] * C[q][j];
+                    mu += cc * pmx[p - i] * pmy[q - j] * Nij;
+                    raw += cc * pax[p - i] * pay[q - j] * Nij;
+                }
+            }
+        if ((p == 1 && q == 0) || (p == 0 && q == 1)) mu = 0.0;
+        if (p == 0 && q == 0) mu = N;
+        // eta = mu / m00^(1 + (p+q)/2)  (moments.cpp:84-89), powers built from m00 and sqrt(m00)
+        double eta = 0;
+        if (p + q >= 2) {
+            const int t = p + q;  // exponent 1 + t/2 in {2, 2.5, 3, 3.5, 4}
+            double den = m00 * m00;
+            if (t >= 4) den *= m00;
+            if (t >= 6) den *= m00;
+            if (t & 1) den *= sqrt(m00);
+            eta = mu / den;
+        }
+        if (zero_mass) raw = mu = eta = 0;
+        const double n20 = __shfl_sync(kFull, eta, (grp << 4) | 8);
+        const double n02 = __shfl_sync(kFull, eta, (grp << 4) | 2);
+        const double n11 = __shfl_sync(kFull, eta, (grp << 4) | 5);
+        const double n30 = __shfl_sync(kFull, eta, (grp << 4) | 12);
+        const double n03 = __shfl_sync(kFull, eta, (grp << 4) | 3);
+        const double n21 = __shfl_sync(kFull, eta, (grp << 4) | 9);
+        const double n12 = __shfl_sync(kFull, eta, (grp << 4) | 6);
+        double* o = orow + cfg.col_mom + grp * 52;
+        const int li = lane & 15;
+        o[li] = raw;
+        o[16 + li] = mu;
+        if (p + q >= 2) o[32 + ((p == 0) ? q - 2 : (p == 1 ? 1 + q : 1 + 4 * (p - 1) + q))] = eta;
+        // Hu invariants: lanes li = 0..6 of each group compute one each
+        if (li < 7) {
+            const double a = n30 + n12, b = n21 + n03;
+            double hu;
+            switch (li) {
+                case 0: hu = n20 + n02; break;
+                case 1: hu = (n20 - n02) * (n20 - n02) + 4.0 * n11 * n11; break;
+                case 2: hu = (n30 - 3.0 * n12) * (n30 - 3.0 * n12) + (3.0 * n21 - n03) * (3.0 * n21 - n03); break;
+                case 3: hu = a * a + b * b; break;
+                case 4:
+                    hu = (n30 - 3.0 * n12) * a * (a * a - 3.0 * b * b) +
+                         (3.0 * n21 - n03) * b * (3.0 * a * a - b * b);
+                    break;
+                case 5: hu = (n20 - n02) * (a * a - b * b) + 4.0 * n11 * a * b; break;
+                default:
+                    hu = (3.0 * n21 - n03) * a * (a * a - 3.0 * b * b) -
+                         (n30 - 3.0 * n12) * b * (3.0 * a * a - b * b);
+                    break;
+            }
+            o[45 + li] = zero_mass ? 0.0 : hu;
+        }
+        __syncwarp();
+    }
+
+    // ---------------------------------------------------------------- glcm
+    if (cfg.col_glcm >= 0) {
+        if (!have_minmax) {
+            uint32_t lo = 0xffffu, hi = 0;
+            for (uint32_t i = lane; i < n; i += 32) {
+                lo = min(lo, (uint32_t)vals[i]);
+                hi = max(hi, (uint32_t)vals[i]);
+            }
+            vmin = warp_min(lo);
+            vmax = warp_max(hi);
+        }
+        glcm_phase_s(n, h, w, rowmask, rowoff, vals, (uint8_t*)(base + L.lvl),
+                     (uint16_t*)(base + L.keys), (uint16_t*)(base + L.keys2),
+                     (uint32_t*)(base + L.gcnt), (uint32_t*)(base + L.marg), vmin, vmax, cfg,
+                     orow + cfg.col_glcm, dbg_on ? dbg : nullptr);
+    }
+    __syncwarp();
+}
+
+}  // namespace
+}  // namespace fxg
+
+namespace fxg {
+namespace {
+
+template <int CLS, bool USE_TMA>
+__global__ void __launch_bounds__(32)
+    k_roi_s2(const __grid_constant__ CUtensorMap tmapL, DevImage img, RoiList rl, Control* ctl,
+             FeatCfg cfg, double* out, const DebugOut* dbg) {
+    constexpr SLayout L = CLS == kClassS1 ? kSL1 : kSL2;
+    constexpr int NMAX = CLS == kClassS1 ? kS1N : kS2N;
+    constexpr int RUNMAX = CLS == kClassS1 ? 512 : 1024;
+    extern __shared__ __align__(128) uint8_t smem_raw[];
+    uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L.bytes - 128);
+    uint16_t* stage = (uint16_t*)(base + L.stage);
+    const unsigned lane = lane_id();
+    if (lane == 0) mbar_init(mbar);
+    __syncwarp();
+    uint32_t phase = 0;
+    const uint32_t count = ctl->class_count[CLS];
+    for (;;) {
+        uint32_t idx = 0;
+        if (lane == 0) idx = atomicAdd(&ctl->class_next[CLS], 1u);
+        idx = __shfl_sync(kFull, idx, 0);
+        if (idx >= count) break;
+        const uint32_t r = rl.cls_list[CLS][idx];
+        const SJob J{rl.label[r], rl.x0[r], rl.y0[r], rl.w[r], rl.h[r], r};
+        if constexpr (USE_TMA) {
+            // label window -> staging tile: 72x8 boxes from x0 & ~7 (16 B aligned)
+            const int nbox = ((int)J.h + 7) >> 3;
+            if (lane == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                mbar_expect_tx(mbar, (uint32_t)nbox * (uint32_t)(kTW * 8 * 2));
+                for (int b = 0; b < nbox; ++b)
+                    tma_load_2d(stage + b * 8 * kTW, &tmapL, mbar, (int)(J.x0 & ~7u),
+                                (int)J.y0 + b * 8);
+            }
+            __syncwarp();
+        } else {
+            // plain coalesced loads of the window rows into the staging tile
+            const uint32_t xo = J.x0 & 7u;
+            for (int y = 0; y < (int)J.h; ++y)
+                for (int x = lane; x < (int)J.w; x += 32)
+                    stage[y * kTW + xo + x] = img.L[(size_t)(J.y0 + y) * img.pitch + J.x0 + x];
+            __syncwarp();
+            if (lane == 0) {  // complete the phase the TMA path would complete
+                asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
+            }
+        }
+        process_s<NMAX, RUNMAX>(J, L, base, img, cfg, out, mbar, phase, ctl, rl, dbg);
+    }
+}
+
+template <int CLS, bool T>
+cudaError_t setup_s2(int* occ) {
+    constexpr uint32_t bytes = (CLS == kClassS1 ? kSL1.bytes : kSL2.bytes) + kSlack;
+    cudaError_t e = cudaFuncSetAttribute(k_roi_s2<CLS, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_roi_s2<CLS, T>, 32, bytes);
+}
+
+}  // namespace
+
+cudaError_t roi_s2_setup(int* occ_s1, int* occ_s2) {
+    k_init_log2_tab<<<4, 256>>>();
+    cudaError_t ei = cudaDeviceSynchronize();
+    if (ei != cudaSuccess) return ei;
+    int o = 0;
+    cudaError_t e = setup_s2<kClassS1, true>(occ_s1);
+    if (e == cudaSuccess) e = setup_s2<kClassS1, false>(&o);
+    if (e == cudaSuccess) e = setup_s2<kClassS2, true>(occ_s2);
+    if (e == cudaSuccess) e = setup_s2<kClassS2, false>(&o);
+    return e;
+}
+
+void launch_roi_s2(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap, DevImage img,
+                   RoiList rl, Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg,
+                   int use_tma) {
+    const uint32_t b1 = kSL1.bytes + kSlack, b2 = kSL2.bytes + kSlack;
+    if (cls == kClassS1) {
+        if (use_tma) k_roi_s2<kClassS1, true><<<grid, 32, b1, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
+        else k_roi_s2<kClassS1, false><<<grid, 32, b1, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
+    } else {
+        if (use_tma) k_roi_s2<kClassS2, true><<<grid, 32, b2, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
+        else k_roi_s2<kClassS2, false><<<grid, 32, b2, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
+    }
+}
+
+}  // namespace fxg

@@ -5,11 +5,16 @@
 * Every other column must satisfy  |g - r| <= tol * (max(|g|, |r|) + s)
   with tol = 1e-9 for intensity and moments, 1e-6 for Haralick (north star),
   and s a per-feature natural scale:
-    - central moments mu_pq: s = sum w |x-cx|^p |y-cy|^q  (computed here from the
-      pixels; the reference's own fp64 binomial shift misses a pure relative
-      bound by up to 2.4e-8 on mu33)
+    - central moments mu_pq: s = sum w (lx + lcx)^p (ly + lcy)^q, lx = x - bbox.x_min,
+      lcx = the local centroid.  This is the magnitude of the terms of the
+      reference's own binomial shift from the bbox origin (moments.cpp:69-79),
+      i.e. the scale of ITS rounding error: against exact rational truth the
+      reference misses a pure relative bound by up to 8.6e-8 (weighted mu33 on a
+      Siemens-star ROI, tests/golden/blobs_star) and 2.4e-8.  The
+      device path itself is checked against exact rational truth at 1e-12 of the
+      natural scale sum w |x-cx|^p |y-cy|^q in test_gpu_parity.py.
     - eta_pq: s_mu / m00^(1+(p+q)/2);  Hu: s2, s2^2, s3^2, s3^2, s3^4, s2*s3^2, s3^4
-      with s2 = |e20|+|e02|+2|e11|, s3 = |e30|+3|e12|+3|e21|+|e03| of the reference
+      with s2 = e20+e02+2e11, s3 = e30+3e12+3e21+e03 over e = |eta| + s_eta
     - skewness / hyperskewness, and Haralick clushade / corr / infomeas1: s = 1
     - everything else: s = 1e-300 (pure relative)
 """
@@ -26,8 +31,10 @@ UNIT_FLOOR = {"intensity_skewness", "intensity_hyperskewness"}
 HARALICK_UNIT = ("clushade", "corr", "infomeas1")
 
 
-def _moment_scales(intensity, labels, roi_labels):
-    """s_pq = sum w |x-cx|^p |y-cy|^q per ROI, for binary and weighted."""
+def _moment_scales(intensity, labels, roi_labels, reference_frame=True):
+    """Per ROI, binary and weighted: s_pq = sum w (lx+lcx)^p (ly+lcy)^q (the
+    reference's binomial-shift scale) or, with reference_frame=False, the
+    natural scale sum w |x-cx|^p |y-cy|^q."""
     ys, xs = np.nonzero(labels)
     lab = labels[ys, xs]
     val = intensity[ys, xs].astype(np.float64)
@@ -41,8 +48,13 @@ def _moment_scales(intensity, labels, roi_labels):
             m = w.sum()
             if m <= 0:
                 continue
-            ax = np.abs(x - (w * x).sum() / m)
-            ay = np.abs(y - (w * y).sum() / m)
+            if reference_frame:
+                lx, ly = x - x.min(), y - y.min()
+                ax = lx + (w * lx).sum() / m
+                ay = ly + (w * ly).sum() / m
+            else:
+                ax = np.abs(x - (w * x).sum() / m)
+                ay = np.abs(y - (w * y).sum() / m)
             for p in range(4):
                 for q in range(4):
                     out[k, g, p, q] = (w * ax ** p * ay ** q).sum()
@@ -70,6 +82,7 @@ def floors(columns, ref_table, intensity=None, labels=None, roi_labels=None):
                             se = ms[:, g, p, q] / np.power(m00, 1.0 + (p + q) / 2.0)
                             s[:, col[f"moments_{pre}eta{p}{q}"]] = np.where(np.isfinite(se), se, 1.0)
                 e = {f"{p}{q}": np.abs(ref_table[:, col[f"moments_{pre}eta{p}{q}"]])
+                     + s[:, col[f"moments_{pre}eta{p}{q}"]]
                      for p in range(4) for q in range(4) if p + q >= 2}
                 s2 = e["20"] + e["02"] + 2 * e["11"]
                 s3 = e["30"] + 3 * e["12"] + 3 * e["21"] + e["03"]

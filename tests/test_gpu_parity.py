@@ -160,3 +160,40 @@ def test_vs_compiled_reference(ctx, reference):
     gl, gv = ctx.featurize(I, L, GROUPS, gp)
     rl, rv = reference.featurize(I, L, GROUPS, op)
     assert_parity(cols, gl, gv, rl, rv, I, L)
+
+
+def _exact_central(xs, ys, w, p, q):
+    from fractions import Fraction
+    W = int(w.sum())
+    cx = Fraction(int((w * xs).sum()), W)
+    cy = Fraction(int((w * ys).sum()), W)
+    return sum(Fraction(int(a)) * (Fraction(int(x)) - cx) ** p * (Fraction(int(y)) - cy) ** q
+               for a, x, y in zip(w, xs, ys))
+
+
+def test_moments_vs_exact_rational_truth(ctx):
+    """The device's central moments are computed about integer anchors and are
+    checked against exact rational arithmetic at 1e-12 of the natural scale
+    (the reference itself misses 1e-9 on some of these, see parity.py)."""
+    import os
+    from parity import _moment_scales
+    d = np.load(os.path.join(os.path.dirname(__file__), "golden", "blobs_star.npz"))
+    cases = [(d["intensity"], d["labels"]),
+             (inputs.uniform((96, 130), 3), inputs.random_blobs((96, 130), 30, seed=3))]
+    for I, L in cases:
+        p = fx.resolve_profile("default")
+        cols = fx.feature_columns(["moments"], p)
+        gl, gv = ctx.featurize(I, L, ["moments"], p)
+        nat = _moment_scales(I, L, gl, reference_frame=False)
+        for k, lab in enumerate(gl[:8]):
+            ys, xs = np.nonzero(L == lab)
+            for g, pre in enumerate(("", "w")):
+                w = np.ones(len(xs), np.int64) if g == 0 else I[ys, xs].astype(np.int64)
+                if w.sum() == 0:
+                    continue
+                for (a, b) in ((2, 0), (1, 1), (3, 0), (2, 1), (3, 3), (2, 3)):
+                    ex = float(_exact_central(xs, ys, w, a, b))
+                    got = gv[k, cols.index(f"moments_{pre}mu{a}{b}")]
+                    assert abs(got - ex) <= 1e-12 * (abs(ex) + nat[k, g, a, b]), (lab, pre, a, b)
+                raw = float(sum(int(c) * int(x) ** 3 * int(y) ** 3 for c, x, y in zip(w, xs, ys)))
+                assert abs(gv[k, cols.index(f"moments_{pre}m33")] - raw) <= 1e-14 * abs(raw)

@@ -1,10 +1,15 @@
-"""Static SASS size (and optional ncu per-address metrics) per source phase of process_roi.
-usage: code_size.py <cubin> <kernel-substring> [ncu_sass.csv]"""
-import collections, csv, re, subprocess, sys
+"""Static SASS size and (optionally) ncu per-address executed instructions / stall
+samples per source phase.  usage: code_size.py <cubin> <kernel-substring> [ncu_sass.csv]
+env: SRCF (source file name), PHASES "name:lo:hi,..." (line ranges)."""
+import collections, csv, os, re, subprocess, sys
 cubin, target = sys.argv[1], sys.argv[2]
-PH = [("load1", 216, 270), ("load2", 271, 313), ("sort", 314, 327), ("cmom", 328, 351),
-      ("pct+mad+rmad", 352, 395), ("mode_hist", 396, 456), ("edge", 457, 610), ("int_out", 611, 656),
-      ("moments", 657, 780), ("glcm", 781, 1000)]
+SRCF = os.environ.get("SRCF", "fx_roi_s.cu")
+PH = [tuple([p.split(":")[0]] + [int(v) for v in p.split(":")[1:]])
+      for p in os.environ.get("PHASES", "mbar:470:501,rowoff+xy:502:533,gather:534:575,sort:576:590,"
+                              "pct+medad:591:609,statloop:610:680,flood:681:711,euler:712:754,"
+                              "edge_stats:755:839,int_out:840:884,moments:885:999,glcm:1000:1010,"
+                              "slowedge:151:250,radix:251:255,kth:256:259,log2:260:266,glcmfn:267:452").split(",")]
+LO = min(p[1] for p in PH); HI = max(p[2] for p in PH)
 dis = subprocess.run(["nvdisasm", "-gi", "-c", cubin], capture_output=True, text=True).stdout
 infn, pending, addr_line, last = False, [], {}, "other"
 for line in dis.splitlines():
@@ -17,22 +22,20 @@ for line in dis.splitlines():
         pending.append(line)
         continue
     m = re.match(r"\s+/\*([0-9a-f]{4,})\*/", line)
-    if m and not pending:
-        addr_line[int(m.group(1), 16)] = last
+    if not m:
         continue
-    if m:
+    if pending:
         ch = []
         for p in pending:
             ch += [(f.split("/")[-1], int(l)) for f, l in re.findall(r'File "([^"]+)", line (\d+)', p)]
         pending = []
-        ins = [c for c in ch if c[0] == "fx_roi.cu" and 200 <= c[1] <= 1000]
+        ins = [c for c in ch if c[0] == SRCF and LO <= c[1] <= HI]
         cur = ins[0] if ins else (ch[0] if ch else ("?", 0))
-        nm = "other"
+        last = "other"
         for p, lo, hi in PH:
-            if cur[0] == "fx_roi.cu" and lo <= cur[1] <= hi:
-                nm = p
-        addr_line[int(m.group(1), 16)] = nm
-        last = nm
+            if cur[0] == SRCF and lo <= cur[1] <= hi:
+                last = p
+    addr_line[int(m.group(1), 16)] = last
 stat = collections.Counter(addr_line.values())
 ex, sm = collections.Counter(), collections.Counter()
 if len(sys.argv) > 3:
@@ -50,6 +53,6 @@ if len(sys.argv) > 3:
         ex[nm] += float(r[ie] or 0)
         sm[nm] += float(r[isamp] or 0)
 te, ts = max(1, sum(ex.values())), max(1, sum(sm.values()))
-print(f"{'phase':14s} {'sass':>6s} {'exec%':>6s} {'stall%':>6s}")
-for nm, n in stat.most_common():
+print(f"{'phase':14s} {'sass':>6s} {'exec%':>6s} {'stall%':>6s}   (total exec {te:.3g})")
+for nm, n in sorted(stat.items(), key=lambda kv: -ex[kv[0]]):
     print(f"{nm:14s} {n:6d} {100*ex[nm]/te:6.1f} {100*sm[nm]/ts:6.1f}")
