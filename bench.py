@@ -276,7 +276,8 @@ def main():
     fg = int(np.count_nonzero(labels))
     algo_bytes = {  # per launch, SURVEY.md 8(d) per-unit figures
         "k_label_scan": h * w * 2,                      # label raster read once
-        "k_roi_s1": fg * 4 + n_rois * ncols * 8,        # ROI pixels (label+intensity) + table
+        "k_roi_s0": fg * 4 + n_rois * ncols * 8,        # ROI pixels (label+intensity) + table
+        "k_roi_s1": fg * 4 + n_rois * ncols * 8,
         "k_roi_s2": fg * 4 + n_rois * ncols * 8,
     }
     per_launch_s = dom_ms / 1e3 / max(1, dom_cnt)

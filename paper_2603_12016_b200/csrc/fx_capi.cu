@@ -28,10 +28,10 @@ __global__ void k_label_scan(const uint16_t* L, int W, int H, size_t pitch, int 
                              LabelTable t);
 __global__ void k_compact_count(LabelTable t, Control* ctl);
 __global__ void k_compact_emit(LabelTable t, Control* ctl, RoiList r);
-cudaError_t roi_s2_setup(int* occ_s1, int* occ_s2);
-void launch_roi_s2(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap, DevImage img,
-                   RoiList rl, Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg,
-                   int use_tma);
+cudaError_t roi_s_setup(int* occ /* [3][2]: class x glcm */);
+void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
+                  const CUtensorMap& tmap72, int tma40, int tma72, DevImage img, RoiList rl,
+                  Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg);
 void launch_roi_l(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                   double* out, const DebugOut* dbg, uint8_t* scratch, const Layout& L);
 }  // namespace fxg
@@ -62,7 +62,7 @@ struct fx_ctx {
     Control* d_ctl = nullptr;
     Control* h_ctl = nullptr;  // pinned
     // ROI list
-    uint32_t* d_roi32 = nullptr;  // label,x0,y0,w,h + 3 class lists + overflow: 9 x 65536
+    uint32_t* d_roi32 = nullptr;  // label,x0,y0,w,h + 4 class lists + overflow: 10 x 65536
     unsigned long long* d_roin = nullptr;
     // staging for host inputs / outputs
     uint16_t* d_img = nullptr;  // intensity then labels, pitched
@@ -81,7 +81,7 @@ struct fx_ctx {
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> ev_pool;
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    int occ_s1 = 1, occ_s2 = 1;
+    int occ_s[3][2] = {{1, 1}, {1, 1}, {1, 1}};
     bool sync_debug = false;
     bool no_tma = false;
 };
@@ -96,10 +96,8 @@ RoiList roi_list(fx_ctx* c) {
     r.y0 = b + 2 * kMaxLabels;
     r.w = b + 3 * kMaxLabels;
     r.h = b + 4 * kMaxLabels;
-    r.cls_list[0] = b + 5 * kMaxLabels;
-    r.cls_list[1] = b + 6 * kMaxLabels;
-    r.cls_list[2] = b + 7 * kMaxLabels;
-    r.overflow = b + 8 * kMaxLabels;
+    for (int k = 0; k < kNumClasses; ++k) r.cls_list[k] = b + (5 + k) * kMaxLabels;
+    r.overflow = b + (5 + kNumClasses) * kMaxLabels;
     r.n = c->d_roin;
     return r;
 }
@@ -249,13 +247,13 @@ int ensure_img(fx_ctx* c, int w, int h) {
     return FX_OK;
 }
 
-bool make_tmap(fx_ctx* c, const DevImage& img, CUtensorMap* m) {
+bool make_tmap(fx_ctx* c, const DevImage& img, CUtensorMap* m, int box_w) {
     if (!c->encode) return false;
     if ((reinterpret_cast<uintptr_t>(img.L) & 15u) || ((img.pitch * 2) & 15u)) return false;
-    if (img.w < kStageW || img.h < 8) return false;
+    if (img.w < box_w || img.h < 8) return false;
     cuuint64_t dims[2] = {(cuuint64_t)img.w, (cuuint64_t)img.h};
     cuuint64_t strides[1] = {(cuuint64_t)img.pitch * 2};
-    cuuint32_t box[2] = {(cuuint32_t)kStageW, 8};
+    cuuint32_t box[2] = {(cuuint32_t)box_w, 8};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = c->encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (void*)img.L, dims, strides, box,
                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
@@ -299,9 +297,9 @@ int run_pipeline(fx_ctx* c, const DevImage& img, unsigned groups, const fx_textu
     {
         const int vec_ok = ((reinterpret_cast<uintptr_t>(img.L) & 15u) == 0) && (img.pitch % 8 == 0);
         const int tiles = ((img.w + 255) / 256) * ((img.h + 63) / 64);
-        const int grid = std::max(1, std::min(tiles, c->sm_count * 6));
+        const int grid = std::max(1, std::min((tiles + 3) / 4, c->sm_count * 8));
         Launch l(c, "k_label_scan");
-        k_label_scan<<<grid, 256, 0, s>>>(img.L, img.w, img.h, img.pitch, vec_ok, t);
+        k_label_scan<<<grid, 128, 0, s>>>(img.L, img.w, img.h, img.pitch, vec_ok, t);
     }
     {
         Launch l(c, "k_compact_count");
@@ -322,19 +320,19 @@ int run_pipeline(fx_ctx* c, const DevImage& img, unsigned groups, const fx_textu
         *n_rois = c->h_ctl->n_rois;
         return c->h_ctl->n_rois ? vrc : FX_OK;
     }
-    CUtensorMap tmap;
-    std::memset(&tmap, 0, sizeof tmap);
-    int use_tma = (!c->no_tma && make_tmap(c, img, &tmap)) ? 1 : 0;
-    if (use_tma && getenv("FXG_TMA_DIAG")) use_tma = atoi(getenv("FXG_TMA_DIAG"));
+    CUtensorMap tmap40, tmap72;
+    std::memset(&tmap40, 0, sizeof tmap40);
+    std::memset(&tmap72, 0, sizeof tmap72);
+    const int tma40 = (!c->no_tma && make_tmap(c, img, &tmap40, kStageW0)) ? 1 : 0;
+    const int tma72 = (!c->no_tma && make_tmap(c, img, &tmap72, kStageW)) ? 1 : 0;
+    const int glcm = (groups & FX_GROUP_GLCM) ? 1 : 0;
     {
-        Launch l(c, "k_roi_s1");
-        launch_roi_s2(kClassS1, c->sm_count * c->occ_s1, s, tmap, img, rl, c->d_ctl, cfg, out_dev,
-                      dbg_dev, use_tma);
-    }
-    {
-        Launch l(c, "k_roi_s2");
-        launch_roi_s2(kClassS2, c->sm_count * c->occ_s2, s, tmap, img, rl, c->d_ctl, cfg, out_dev,
-                      dbg_dev, use_tma);
+        static const char* names[3] = {"k_roi_s0", "k_roi_s1", "k_roi_s2"};
+        for (int cls = kClassS0; cls <= kClassS2; ++cls) {
+            Launch l(c, names[cls]);
+            launch_roi_s(cls, c->sm_count * c->occ_s[cls][glcm], s, tmap40, tmap72, tma40, tma72,
+                         img, rl, c->d_ctl, cfg, out_dev, dbg_dev);
+        }
     }
     CK(cudaGetLastError());
     CK(cudaEventSynchronize(c->ev_stats));
@@ -351,7 +349,8 @@ int run_pipeline(fx_ctx* c, const DevImage& img, unsigned groups, const fx_textu
         const uint32_t grid = (uint32_t)std::min<uint64_t>(
             (uint64_t)c->sm_count * 2,
             std::max<uint64_t>(std::max<uint64_t>(nl, 1),
-                               hc.class_count[kClassS1] + hc.class_count[kClassS2] > 0 ? 16 : 1));
+                               hc.class_count[kClassS0] + hc.class_count[kClassS1] +
+                                           hc.class_count[kClassS2] > 0 ? 16 : 1));
         size_t bytes = (size_t)L.bytes * grid;
         int rc = ensure_lscratch(c, bytes);
         if (rc) return rc;
@@ -460,12 +459,12 @@ int fx_ctx_create(int device, fx_ctx** out) {
     CKC(cudaMalloc(&c->d_bb, 4 * kMaxLabels * sizeof(uint32_t)));
     CKC(cudaMalloc(&c->d_ctl, sizeof(Control)));
     CKC(cudaMallocHost(&c->h_ctl, sizeof(Control)));
-    CKC(cudaMalloc(&c->d_roi32, 9 * kMaxLabels * sizeof(uint32_t)));
+    CKC(cudaMalloc(&c->d_roi32, (6 + kNumClasses) * kMaxLabels * sizeof(uint32_t)));
     CKC(cudaMalloc(&c->d_roin, kMaxLabels * sizeof(unsigned long long)));
     CKC(cudaMalloc(&c->d_dbg, sizeof(DebugOut)));
-    CKC(roi_s2_setup(&c->occ_s1, &c->occ_s2));
-    c->occ_s1 = std::max(1, c->occ_s1);
-    c->occ_s2 = std::max(1, c->occ_s2);
+    CKC(roi_s_setup(&c->occ_s[0][0]));
+    for (auto& row : c->occ_s)
+        for (int& o : row) o = std::max(1, o);
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
@@ -649,8 +648,8 @@ int fx_roi_table(fx_ctx* c, const fx_image* im, uint32_t* out_labels, uint64_t* 
     const int tiles = ((d.w + 255) / 256) * ((d.h + 63) / 64);
     {
         Launch l(c, "k_label_scan");
-        k_label_scan<<<std::max(1, std::min(tiles, c->sm_count * 6)), 256, 0, s>>>(d.L, d.w, d.h,
-                                                                                 d.pitch, vec_ok, t);
+        k_label_scan<<<std::max(1, std::min((tiles + 3) / 4, c->sm_count * 8)), 128, 0, s>>>(
+            d.L, d.w, d.h, d.pitch, vec_ok, t);
     }
     {
         Launch l(c, "k_compact_count");

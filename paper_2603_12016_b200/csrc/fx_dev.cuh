@@ -21,7 +21,7 @@ struct LabelTable {
 };
 
 // ROI classes by window (bbox) size; each is consumed by its own persistent kernel.
-enum RoiClass { kClassS1 = 0, kClassS2 = 1, kClassL = 2, kNumClasses = 3 };
+enum RoiClass { kClassS0 = 0, kClassS1 = 1, kClassS2 = 2, kClassL = 3, kNumClasses = 4 };
 
 // S-class limits: window fits a 64x64 TMA staging tile, one u64 mask word per row.
 constexpr int kSW = 64, kSH = 64;
@@ -29,6 +29,8 @@ constexpr int kSW = 64, kSH = 64;
 // sm_100a (an unaligned innermost coordinate raises "illegal instruction"),
 // so the box starts at x0 & ~7 and is 72 wide to cover any 64-wide window.
 constexpr int kStageW = 72;
+// S0: small windows (w <= 33, h <= 40) staged in a 40-wide tile -> half the slab
+constexpr int kS0W = 33, kS0H = 40, kStageW0 = 40;
 constexpr int kS1N = 1024;  // max ROI pixels for S1
 constexpr int kS2N = 4096;  // = kSW*kSH
 constexpr int kS1Runs = 512;

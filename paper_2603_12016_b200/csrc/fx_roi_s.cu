@@ -26,8 +26,6 @@ namespace fxg {
 
 namespace {
 
-constexpr int kTW = kStageW;  // staging tile row stride (u16)
-
 // ---- slab layout for S windows ---------------------------------------------
 struct SLayout {
     uint32_t rowmask, rowoff, vals, xy;        // region A
@@ -38,28 +36,29 @@ struct SLayout {
     uint32_t bytes;
 };
 
-__host__ __device__ constexpr SLayout make_slayout(uint32_t NMAX, uint32_t RUNMAX) {
+__host__ __device__ constexpr SLayout make_slayout(uint32_t TW, uint32_t TH, uint32_t NMAX,
+                                                   uint32_t RUNMAX, bool glcm) {
     SLayout L{};
     uint32_t o = 0;
     L.rowmask = o;
-    o += kSH * 8;
+    o += TH * 8;
     L.rowoff = o;
-    o = al(o + (kSH + 1) * 4, 16);
+    o = al(o + (TH + 1) * 4, 16);
     L.vals = o;
     o = al(o + NMAX * 2, 16);
     L.xy = o;
     o = al(o + NMAX * 2, 128);
     const uint32_t B = o;
     L.stage = B;
-    const uint32_t e_load = B + kTW * kSH * 2;
+    const uint32_t e_load = B + TW * TH * 2;
     L.tmp = B;
     L.sorted = al(L.tmp + NMAX * 2, 16);
     L.cnt = al(L.sorted + NMAX * 2, 16);
     const uint32_t e_sort = L.cnt + 512 * 4;
     L.kmask = B;
-    L.emask = L.kmask + kSH * 8;
-    L.runoff = L.emask + kSH * 8;
-    L.rs = al(L.runoff + (kSH + 1) * 4, 16);
+    L.emask = L.kmask + TH * 8;
+    L.runoff = L.emask + TH * 8;
+    L.rs = al(L.runoff + (TH + 1) * 4, 16);
     L.re = al(L.rs + RUNMAX * 2, 16);
     L.parent = al(L.re + RUNMAX * 2, 16);
     L.rsize = al(L.parent + RUNMAX * 4, 16);
@@ -69,13 +68,30 @@ __host__ __device__ constexpr SLayout make_slayout(uint32_t NMAX, uint32_t RUNMA
     L.keys2 = al(L.keys + NMAX * 2, 16);
     L.gcnt = al(L.keys2 + NMAX * 2, 16);
     L.marg = L.gcnt + 512 * 4;
-    const uint32_t e_glcm = L.marg + 1280 * 4;
+    const uint32_t e_glcm = glcm ? L.marg + 1280 * 4 : B;
     L.bytes = al(mx(mx(e_load, e_sort), mx(e_edge, e_glcm)), 128) + 128;  // + mbarrier
     return L;
 }
 
-constexpr SLayout kSL1 = make_slayout(kS1N, 512);
-constexpr SLayout kSL2 = make_slayout(kS2N, 1024);
+// window-class variants: stage width, max rows, max pixels, run capacity
+template <int CLS>
+struct SVar;
+template <>
+struct SVar<kClassS0> {
+    static constexpr int TW = kStageW0, TH = kS0H, NMAX = kS1N, RUNMAX = 256;
+};
+template <>
+struct SVar<kClassS1> {
+    static constexpr int TW = kStageW, TH = kSH, NMAX = kS1N, RUNMAX = 512;
+};
+template <>
+struct SVar<kClassS2> {
+    static constexpr int TW = kStageW, TH = kSH, NMAX = kS2N, RUNMAX = 1024;
+};
+template <int CLS, bool GLCM>
+constexpr SLayout slayout() {
+    return make_slayout(SVar<CLS>::TW, SVar<CLS>::TH, SVar<CLS>::NMAX, SVar<CLS>::RUNMAX, GLCM);
+}
 constexpr uint32_t kSlack = 128;  // dynamic smem base alignment
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar) {
@@ -268,7 +284,7 @@ __device__ __forceinline__ void radix_scatter(const uint16_t* src, uint16_t* dst
 // Stable 16-bit LSD radix sort by one warp: both digit histograms in one pass,
 // the high-digit pass skipped when every key shares its high byte.  Returns the
 // buffer holding the sorted keys (tmp or dst).  cnt: 512 u32.
-__device__ __noinline__ const uint16_t* radix_sort16(const uint16_t* src, uint16_t* tmp,
+__device__ __forceinline__ const uint16_t* radix_sort16(const uint16_t* src, uint16_t* tmp,
                                                      uint16_t* dst, uint32_t n, uint32_t* cnt) {
     const unsigned lane = lane_id();
     for (int i = lane; i < 512; i += 32) cnt[i] = 0;
@@ -559,7 +575,7 @@ __device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64
 }
 
 // ------------------------------------------------------------------------
-template <int NMAX, int RUNMAX>
+template <int TW, int TH, int NMAX, int RUNMAX, bool GLCM>
 __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8_t* base,
                                           const DevImage& img, const FeatCfg& cfg,
                                           double* __restrict__ out, uint64_t* mbar,
@@ -589,7 +605,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
         const int y = lane + 32 * half;
         uint64_t m = 0;
         if (y < h) {
-            const uint4* row = reinterpret_cast<const uint4*>(stage + y * kTW);
+            const uint4* row = reinterpret_cast<const uint4*>(stage + y * TW);
             const int c_end = (int)((xo + w + 7) >> 3);
 #pragma unroll 1
             for (int c = 0; c < c_end; ++c) {
@@ -716,10 +732,18 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
         const uint32_t nb32 = (uint32_t)cfg.bins;
         const bool wide = (unsigned long long)nb32 * 65535ull >= (1ull << 32);
         const uint32_t rng = vmax - vmin;
+        // floor(num / rng) by multiply-high with one correction step (num < 2^32)
+        const uint32_t magic = rng ? (uint32_t)(0xffffffffull / rng) : 0u;
         auto bin_of = [&](uint32_t v) -> uint32_t {
             if (rng == 0) return 0u;
-            const uint32_t b = wide ? (uint32_t)((unsigned long long)nb32 * (v - vmin) / rng)
-                                    : (nb32 * (v - vmin)) / rng;
+            uint32_t b;
+            if (!wide) {
+                const uint32_t num = nb32 * (v - vmin);
+                b = __umulhi(num, magic);
+                if (num - b * rng >= rng) ++b;
+            } else {
+                b = (uint32_t)((unsigned long long)nb32 * (v - vmin) / rng);
+            }
             return b < nb32 - 1 ? b : nb32 - 1;
         };
         const double logn = nlog2(dn);
@@ -834,7 +858,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
                 const uint64_t side = 1ull | (1ull << (w - 1));
                 e0 = run_fill(f0, (lane == 0 || (int)lane == h - 1) ? f0 : (f0 & side));
                 e1 = run_fill(f1, ((int)lane + 32 == h - 1) ? f1 : (f1 & side));
-                for (int it = 0; it < 4 * kSH * kSW; ++it) {
+                for (int it = 0; it < 64 * TH; ++it) {
                     const uint64_t up0 = __shfl_up_sync(kFull, e0, 1);
                     const uint64_t dn0 = __shfl_down_sync(kFull, e0, 1);
                     const uint64_t up1 = __shfl_up_sync(kFull, e1, 1);
@@ -1026,44 +1050,69 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
         const long long ayb = (2 * (long long)sLY + nn) / (2 * nn);
         const long long axw = W > 0 ? (2 * (long long)sXI + W) / (2 * W) : 0;
         const long long ayw = W > 0 ? (2 * (long long)sYI + W) / (2 * W) : 0;
-        double acc[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) acc[k] = 0;
+        // two passes (unit mass, then intensity) of 16 separable row accumulators
+        // about the integer anchor: A_pq = sum_rows (sum_x w dx^p) dy^q
         const int nhalf = h > 32 ? 2 : 1;
+        double Nb = 0, Nw = 0;
 #pragma unroll 1
-        for (int hf = 0; hf < nhalf; ++hf) {
-            const int y = lane + 32 * hf;
-            uint64_t m = hf ? m1 : m0;
-            uint32_t idx = hf ? off1 : off0;
-            double rb1 = 0, rb2 = 0, rb3 = 0, rw0 = 0, rw1 = 0, rw2 = 0, rw3 = 0;
-            const double cb = (double)__popcll(m);
-            while (m) {
-                const int x = __ffsll((long long)m) - 1;
-                m &= m - 1;
-                const double wv = (double)vals[idx++];
-                const double db = (double)(x - axb), dw = (double)(x - axw);
-                const double db2 = db * db, dw2 = dw * dw;
-                rb1 += db;
-                rb2 += db2;
-                rb3 += db2 * db;
-                rw0 += wv;
-                rw1 += wv * dw;
-                rw2 += wv * dw2;
-                rw3 += wv * dw2 * dw;
-            }
-            const double yb = (double)((long long)y - ayb), yw = (double)((long long)y - ayw);
-            const double rb[4] = {cb, rb1, rb2, rb3}, rw[4] = {rw0, rw1, rw2, rw3};
-            const double qb[4] = {1.0, yb, yb * yb, yb * yb * yb};
-            const double qw[4] = {1.0, yw, yw * yw, yw * yw * yw};
+        for (int g = 0; g < 2; ++g) {
+            const long long ax = g ? axw : axb, ay = g ? ayw : ayb;
+            double acc[16];
 #pragma unroll
-            for (int p = 0; p < 4; ++p)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    acc[p * 4 + q] += rb[p] * qb[q];
-                    acc[16 + p * 4 + q] += rw[p] * qw[q];
+            for (int k = 0; k < 16; ++k) acc[k] = 0;
+#pragma unroll 1
+            for (int hf = 0; hf < nhalf; ++hf) {
+                const int y = lane + 32 * hf;
+                uint64_t m = hf ? m1 : m0;
+                uint32_t idx = hf ? off1 : off0;
+                double r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+                if (g == 0) {
+                    r0 = (double)__popcll(m);
+                    while (m) {
+                        const double d = (double)((long long)(__ffsll((long long)m) - 1) - ax);
+                        m &= m - 1;
+                        const double d2 = d * d;
+                        r1 += d;
+                        r2 += d2;
+                        r3 += d2 * d;
+                    }
+                } else {
+                    while (m) {
+                        const double d = (double)((long long)(__ffsll((long long)m) - 1) - ax);
+                        m &= m - 1;
+                        const double wv = (double)vals[idx++];
+                        const double wd = wv * d, wd2 = wd * d;
+                        r0 += wv;
+                        r1 += wd;
+                        r2 += wd2;
+                        r3 += wd2 * d;
+                    }
                 }
+                const double yy = (double)((long long)y - ay);
+                const double q2 = yy * yy;
+                const double rr[4] = {r0, r1, r2, r3}, qq[4] = {1.0, yy, q2, q2 * yy};
+#pragma unroll
+                for (int a = 0; a < 4; ++a)
+#pragma unroll
+                    for (int b = 0; b < 4; ++b) acc[a * 4 + b] += rr[a] * qq[b];
+            }
+            // reduce-scatter: after 4 halving steps lane L holds index L >> 1
+#pragma unroll
+            for (int st = 16, half = 8; st >= 2; st >>= 1, half >>= 1) {
+                const bool up = (lane & st) != 0;
+#pragma unroll
+                for (int j = 0; j < half; ++j) {
+                    const double send = up ? acc[j] : acc[j + half];
+                    const double recv = __shfl_xor_sync(kFull, send, st);
+                    acc[j] = (up ? acc[j + half] : acc[j]) + recv;
+                }
+            }
+            double t = acc[0] + __shfl_xor_sync(kFull, acc[0], 1);
+            t = __shfl_sync(kFull, t, 2 * (lane & 15));  // lane L: index L & 15
+            if (g == 0) Nb = t;
+            else Nw = t;
         }
-        const double N = reduce_scatter32(acc);
+        const double N = (lane >> 4) ? Nw : Nb;
         const int grp = lane >> 4, p = (lane >> 2) & 3, q = lane & 3;
         const double m00 = grp ? (double)sS : dn;
         const bool zero_mass = grp && sS == 0;
@@ -1072,28 +1121,29 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
         const double dy = grp ? (W > 0 ? (double)((long long)sYI - ayw * W) / (double)W : 0.0)
                               : (double)((long long)sLY - ayb * nn) / dn;
         const double Ax = (double)(gx0 + (grp ? axw : axb)), Ay = (double)(gy0 + (grp ? ayw : ayb));
-        const double C[4][4] = {{1, 0, 0, 0}, {1, 1, 0, 0}, {1, 2, 1, 0}, {1, 3, 3, 1}};
-        double pmx[4], pmy[4], pax[4], pay[4];
-        pmx[0] = pmy[0] = pax[0] = pay[0] = 1.0;
+        // separable binomial shift in two shuffle stages (no lane-indexed arrays):
+        //   T_pq = sum_j C(q,j) t^(q-j) N_pj,  mu_pq = sum_i C(p,i) s^(p-i) T_iq
+        auto coef = [](int e, int k, double t) -> double {  // C(e,k) t^(e-k), 0 if k > e
+            if (k > e) return 0.0;
+            const int d = e - k;
+            const double c = (k == 0 || k == e) ? 1.0 : (e == 3 ? 3.0 : 2.0);
+            const double t2 = t * t;
+            return c * (d == 0 ? 1.0 : d == 1 ? t : d == 2 ? t2 : t2 * t);
+        };
+        double Tm = 0, Tr = 0;
 #pragma unroll
-        for (int k = 1; k < 4; ++k) {
-            pmx[k] = pmx[k - 1] * (-dx);
-            pmy[k] = pmy[k - 1] * (-dy);
-            pax[k] = pax[k - 1] * Ax;
-            pay[k] = pay[k - 1] * Ay;
+        for (int j = 0; j < 4; ++j) {
+            const double Npj = __shfl_sync(kFull, N, (grp << 4) | (p << 2) | j);
+            Tm += coef(q, j, -dy) * Npj;
+            Tr += coef(q, j, Ay) * Npj;
         }
         double mu = 0, raw = 0;
 #pragma unroll
-        for (int i = 0; i < 4; ++i)
-#pragma unroll
-            for (int j = 0; j < 4; ++j) {
-                const double Nij = __shfl_sync(kFull, N, (grp << 4) | (i << 2) | j);
-                if (i <= p && j <= q) {
-                    const double cc = C[p][i] * C[q][j];
-                    mu += cc * pmx[p - i] * pmy[q - j] * Nij;
-                    raw += cc * pax[p - i] * pay[q - j] * Nij;
-                }
-            }
+        for (int i = 0; i < 4; ++i) {
+            const int src = (grp << 4) | (i << 2) | q;
+            mu += coef(p, i, -dx) * __shfl_sync(kFull, Tm, src);
+            raw += coef(p, i, Ax) * __shfl_sync(kFull, Tr, src);
+        }
         if ((p == 1 && q == 0) || (p == 0 && q == 1)) mu = 0.0;
         if (p == 0 && q == 0) mu = N;
         // eta = mu / m00^(1 + (p+q)/2)  (moments.cpp:84-89), powers built from m00 and sqrt(m00)
@@ -1144,7 +1194,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     }
 
     // ---------------------------------------------------------------- glcm
-    if (cfg.col_glcm >= 0) {
+    if (GLCM && cfg.col_glcm >= 0) {
         if (!have_minmax) {
             uint32_t lo = 0xffffu, hi = 0;
             for (uint32_t i = lane; i < n; i += 32) {
@@ -1168,13 +1218,12 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
 namespace fxg {
 namespace {
 
-template <int CLS, bool USE_TMA>
-__global__ void __launch_bounds__(32)
-    k_roi_s2(const __grid_constant__ CUtensorMap tmapL, DevImage img, RoiList rl, Control* ctl,
-             FeatCfg cfg, double* out, const DebugOut* dbg) {
-    constexpr SLayout L = CLS == kClassS1 ? kSL1 : kSL2;
-    constexpr int NMAX = CLS == kClassS1 ? kS1N : kS2N;
-    constexpr int RUNMAX = CLS == kClassS1 ? 512 : 1024;
+template <int CLS, bool GLCM>
+__global__ void __launch_bounds__(32, 20)
+    k_roi_s(const __grid_constant__ CUtensorMap tmapL, int use_tma, DevImage img, RoiList rl,
+            Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg) {
+    using V = SVar<CLS>;
+    constexpr SLayout L = slayout<CLS, GLCM>();
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L.bytes - 128);
@@ -1191,14 +1240,15 @@ __global__ void __launch_bounds__(32)
         if (idx >= count) break;
         const uint32_t r = rl.cls_list[CLS][idx];
         const SJob J{rl.label[r], rl.x0[r], rl.y0[r], rl.w[r], rl.h[r], r};
-        if constexpr (USE_TMA) {
-            // label window -> staging tile: 72x8 boxes from x0 & ~7 (16 B aligned)
+        if (use_tma) {
+            // label window -> staging tile: TWx8 boxes from x0 & ~7 (16 B aligned
+            // innermost coordinate, required on sm_100a)
             const int nbox = ((int)J.h + 7) >> 3;
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(mbar, (uint32_t)nbox * (uint32_t)(kTW * 8 * 2));
+                mbar_expect_tx(mbar, (uint32_t)nbox * (uint32_t)(V::TW * 8 * 2));
                 for (int b = 0; b < nbox; ++b)
-                    tma_load_2d(stage + b * 8 * kTW, &tmapL, mbar, (int)(J.x0 & ~7u),
+                    tma_load_2d(stage + b * 8 * V::TW, &tmapL, mbar, (int)(J.x0 & ~7u),
                                 (int)J.y0 + b * 8);
             }
             __syncwarp();
@@ -1207,48 +1257,65 @@ __global__ void __launch_bounds__(32)
             const uint32_t xo = J.x0 & 7u;
             for (int y = 0; y < (int)J.h; ++y)
                 for (int x = lane; x < (int)J.w; x += 32)
-                    stage[y * kTW + xo + x] = img.L[(size_t)(J.y0 + y) * img.pitch + J.x0 + x];
+                    stage[y * V::TW + xo + x] = img.L[(size_t)(J.y0 + y) * img.pitch + J.x0 + x];
             __syncwarp();
-            if (lane == 0) {  // complete the phase the TMA path would complete
+            if (lane == 0)  // complete the phase the TMA path would complete
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
-            }
         }
-        process_s<NMAX, RUNMAX>(J, L, base, img, cfg, out, mbar, phase, ctl, rl, dbg);
+        process_s<V::TW, V::TH, V::NMAX, V::RUNMAX, GLCM>(J, L, base, img, cfg, out, mbar, phase,
+                                                         ctl, rl, dbg);
     }
 }
 
-template <int CLS, bool T>
-cudaError_t setup_s2(int* occ) {
-    constexpr uint32_t bytes = (CLS == kClassS1 ? kSL1.bytes : kSL2.bytes) + kSlack;
-    cudaError_t e = cudaFuncSetAttribute(k_roi_s2<CLS, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+template <int CLS, bool G>
+cudaError_t setup_one(int* occ) {
+    constexpr uint32_t bytes = slayout<CLS, G>().bytes + kSlack;
+    cudaError_t e = cudaFuncSetAttribute(k_roi_s<CLS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
     if (e != cudaSuccess) return e;
-    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_roi_s2<CLS, T>, 32, bytes);
+    e = cudaFuncSetAttribute(k_roi_s<CLS, G>, cudaFuncAttributePreferredSharedMemoryCarveout,
+                             cudaSharedmemCarveoutMaxShared);
+    if (e != cudaSuccess) return e;
+    return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_roi_s<CLS, G>, 32, bytes);
+}
+
+template <int CLS, bool G>
+void launch_one(int grid, cudaStream_t s, const CUtensorMap& tm, int use_tma, DevImage img,
+                RoiList rl, Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg) {
+    k_roi_s<CLS, G><<<grid, 32, slayout<CLS, G>().bytes + kSlack, s>>>(tm, use_tma, img, rl, ctl,
+                                                                      cfg, out, dbg);
 }
 
 }  // namespace
 
-cudaError_t roi_s2_setup(int* occ_s1, int* occ_s2) {
+cudaError_t roi_s_setup(int* occ) {
     k_init_log2_tab<<<4, 256>>>();
-    cudaError_t ei = cudaDeviceSynchronize();
-    if (ei != cudaSuccess) return ei;
-    int o = 0;
-    cudaError_t e = setup_s2<kClassS1, true>(occ_s1);
-    if (e == cudaSuccess) e = setup_s2<kClassS1, false>(&o);
-    if (e == cudaSuccess) e = setup_s2<kClassS2, true>(occ_s2);
-    if (e == cudaSuccess) e = setup_s2<kClassS2, false>(&o);
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess) e = setup_one<kClassS0, false>(&occ[0]);
+    if (e == cudaSuccess) e = setup_one<kClassS0, true>(&occ[1]);
+    if (e == cudaSuccess) e = setup_one<kClassS1, false>(&occ[2]);
+    if (e == cudaSuccess) e = setup_one<kClassS1, true>(&occ[3]);
+    if (e == cudaSuccess) e = setup_one<kClassS2, false>(&occ[4]);
+    if (e == cudaSuccess) e = setup_one<kClassS2, true>(&occ[5]);
     return e;
 }
 
-void launch_roi_s2(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap, DevImage img,
-                   RoiList rl, Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg,
-                   int use_tma) {
-    const uint32_t b1 = kSL1.bytes + kSlack, b2 = kSL2.bytes + kSlack;
-    if (cls == kClassS1) {
-        if (use_tma) k_roi_s2<kClassS1, true><<<grid, 32, b1, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
-        else k_roi_s2<kClassS1, false><<<grid, 32, b1, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
-    } else {
-        if (use_tma) k_roi_s2<kClassS2, true><<<grid, 32, b2, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
-        else k_roi_s2<kClassS2, false><<<grid, 32, b2, s>>>(tmap, img, rl, ctl, cfg, out, dbg);
+void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
+                  const CUtensorMap& tmap72, int tma40, int tma72, DevImage img, RoiList rl,
+                  Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg) {
+    const bool g = cfg.col_glcm >= 0;
+    switch (cls) {
+        case kClassS0:
+            if (g) launch_one<kClassS0, true>(grid, s, tmap40, tma40, img, rl, ctl, cfg, out, dbg);
+            else launch_one<kClassS0, false>(grid, s, tmap40, tma40, img, rl, ctl, cfg, out, dbg);
+            break;
+        case kClassS1:
+            if (g) launch_one<kClassS1, true>(grid, s, tmap72, tma72, img, rl, ctl, cfg, out, dbg);
+            else launch_one<kClassS1, false>(grid, s, tmap72, tma72, img, rl, ctl, cfg, out, dbg);
+            break;
+        default:
+            if (g) launch_one<kClassS2, true>(grid, s, tmap72, tma72, img, rl, ctl, cfg, out, dbg);
+            else launch_one<kClassS2, false>(grid, s, tmap72, tma72, img, rl, ctl, cfg, out, dbg);
+            break;
     }
 }
 

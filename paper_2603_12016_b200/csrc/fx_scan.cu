@@ -2,13 +2,13 @@
 // reference roi.cpp:76-117).
 //
 // k_label_scan: one coalesced HBM sweep over the uint16 label raster (16 B vector
-// loads, 8 labels per thread).  Each thread owns an 8-pixel-wide x 8-row strip
-// and folds the pixels it sees into a 2-entry register cache; evictions go to a
-// per-CTA shared-memory hash table (smem atomics), which is flushed to the
-// direct-mapped global LabelTable with one set of global atomics per (tile,
-// label).  Integer min/max/sum are order-free, so the table is bit-exact and
-// deterministic.  Intensities are not read here (the per-ROI kernels gather
-// them), so the sweep moves 2 B/px.
+// loads, 8 labels per lane, 8 rows in flight).  Each lane owns an 8-pixel-wide
+// x 32-row strip and folds it into a 2-entry register cache using SIMD-in-word
+// tests (one label per chunk is the fast path); the warp then merges equal
+// labels with REDUX and issues one set of global atomics per (strip, label) into
+// the direct-mapped LabelTable.  Integer min/max/sum are order-free, so the
+// table is bit-exact and deterministic.  Intensities are not read here (the
+// per-ROI kernels gather them), so the sweep moves 2 B/px.
 //
 // k_compact_count / k_compact_emit: ascending list of present labels (rank =
 // output row), bbox -> window, window-size class lists for the per-ROI kernels.
@@ -18,72 +18,107 @@ namespace fxg {
 
 namespace {
 
-constexpr int kScanThreads = 256;  // 8 warps
-constexpr int kTileW = 256;        // 32 lanes x 8 px
-constexpr int kRowsPerWarp = 8;
-constexpr int kTileH = 8 * kRowsPerWarp;  // 64
-constexpr int kHashBits = 9;
-constexpr int kHash = 1 << kHashBits;
+// Warp tile: 32 lanes x 8 px = 256 px wide, kStripRows rows tall.  Each lane
+// owns an 8-px-wide column strip and folds what it sees into a 2-entry register
+// cache (blob ROIs give 1-2 labels per strip); at the end of the strip the warp
+// merges equal labels with REDUX and one lane issues the global atomics.
+constexpr int kScanThreads = 128;
+constexpr int kStripRows = 64;
+constexpr int kBatch = 8;  // rows per load batch (8 x 16 B in flight per lane)
 
 struct CacheEnt {
     uint32_t label, cnt, x0, x1, y0, y1;
 };
 
-struct ScanSmem {
-    uint32_t key[kHash];
-    uint32_t cnt[kHash];
-    uint32_t x0[kHash], x1[kHash], y0[kHash], y1[kHash];
-};
-
-__device__ __forceinline__ void global_fold(const LabelTable& t, uint32_t l, uint32_t cnt,
-                                            uint32_t x0, uint32_t x1, uint32_t y0,
-                                            uint32_t y1) {
-    atomicAdd(&t.cnt[l], (unsigned long long)cnt);
-    atomicMin(&t.xmin[l], x0);
-    atomicMax(&t.xmax[l], x1);
-    atomicMin(&t.ymin[l], y0);
-    atomicMax(&t.ymax[l], y1);
+__device__ __noinline__ void global_fold(const LabelTable& t, const CacheEnt& e) {
+    if (!e.label) return;
+    atomicAdd(&t.cnt[e.label], (unsigned long long)e.cnt);
+    atomicMin(&t.xmin[e.label], e.x0);
+    atomicMax(&t.xmax[e.label], e.x1);
+    atomicMin(&t.ymin[e.label], e.y0);
+    atomicMax(&t.ymax[e.label], e.y1);
 }
 
-__device__ __forceinline__ void hash_fold(ScanSmem& s, const LabelTable& t, const CacheEnt& e) {
-    if (e.label == 0) return;
-    uint32_t slot = (e.label * 2654435761u) >> (32 - kHashBits);
-    for (int probe = 0; probe < kHash; ++probe) {
-        uint32_t k = s.key[slot];
-        if (k == 0) {
-            k = atomicCAS(&s.key[slot], 0u, e.label);
-            if (k == 0) k = e.label;
-        }
-        if (k == e.label) {
-            atomicAdd(&s.cnt[slot], e.cnt);
-            atomicMin(&s.x0[slot], e.x0);
-            atomicMax(&s.x1[slot], e.x1);
-            atomicMin(&s.y0[slot], e.y0);
-            atomicMax(&s.y1[slot], e.y1);
-            return;
-        }
-        slot = (slot + 1) & (kHash - 1);
-    }
-    global_fold(t, e.label, e.cnt, e.x0, e.x1, e.y0, e.y1);  // table full: direct
-}
-
-__device__ __forceinline__ void cache_add(CacheEnt& c0, CacheEnt& c1, ScanSmem& s,
-                                          const LabelTable& t, uint32_t l, uint32_t x,
+// fold a run summary (label, count, first x, last x) of row y into the cache
+__device__ __forceinline__ void cache_put(CacheEnt& c0, CacheEnt& c1, const LabelTable& t,
+                                          uint32_t l, uint32_t cnt, uint32_t xa, uint32_t xb,
                                           uint32_t y) {
     if (l == c0.label) {
-        c0.cnt++;
-        c0.x0 = min(c0.x0, x);
-        c0.x1 = max(c0.x1, x);
-        c0.y1 = y;  // rows are visited in increasing order
+        c0.cnt += cnt;
+        c0.x0 = min(c0.x0, xa);
+        c0.x1 = max(c0.x1, xb);
+        c0.y1 = y;
     } else if (l == c1.label) {
-        c1.cnt++;
-        c1.x0 = min(c1.x0, x);
-        c1.x1 = max(c1.x1, x);
+        c1.cnt += cnt;
+        c1.x0 = min(c1.x0, xa);
+        c1.x1 = max(c1.x1, xb);
         c1.y1 = y;
     } else {
-        hash_fold(s, t, c1);
+        global_fold(t, c1);
         c1 = c0;
-        c0 = CacheEnt{l, 1u, x, x, y, y};
+        c0 = CacheEnt{l, cnt, xa, xb, y, y};
+    }
+}
+
+// several distinct labels inside one 8-px chunk: per pixel
+__device__ __noinline__ void chunk_slow(uint4 v, uint32_t x, uint32_t y, CacheEnt& c0, CacheEnt& c1,
+                                        const LabelTable& t) {
+    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
+    for (int k = 0; k < 8; ++k) {
+        const uint32_t l = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+        if (l) cache_put(c0, c1, t, l, 1u, x + k, x + k, y);
+    }
+}
+
+__device__ __forceinline__ void chunk(uint4 v, uint32_t x, uint32_t y, CacheEnt& c0, CacheEnt& c1,
+                                      const LabelTable& t) {
+    if ((v.x | v.y | v.z | v.w) == 0u) return;
+    // nonzero halfwords and the largest label in the chunk (SIMD-in-word)
+    const uint32_t n0 = __vcmpne2(v.x, 0u), n1 = __vcmpne2(v.y, 0u), n2 = __vcmpne2(v.z, 0u),
+                   n3 = __vcmpne2(v.w, 0u);
+    const uint32_t mx2 = __vmaxu2(__vmaxu2(v.x, v.y), __vmaxu2(v.z, v.w));
+    const uint32_t L = max(mx2 & 0xffffu, mx2 >> 16);
+    const uint32_t LL = L | (L << 16);
+    // every nonzero halfword equal to L ?
+    const uint32_t bad = (n0 & ~__vcmpeq2(v.x, LL)) | (n1 & ~__vcmpeq2(v.y, LL)) |
+                         (n2 & ~__vcmpeq2(v.z, LL)) | (n3 & ~__vcmpeq2(v.w, LL));
+    if (bad) {
+        chunk_slow(v, x, y, c0, c1, t);
+        return;
+    }
+    const uint32_t m8 = (n0 & 1u) | ((n0 >> 15) & 2u) | ((n1 & 1u) << 2) | ((n1 >> 13) & 8u) |
+                        ((n2 & 1u) << 4) | ((n2 >> 11) & 32u) | ((n3 & 1u) << 6) |
+                        ((n3 >> 9) & 128u);
+    cache_put(c0, c1, t, L, __popc(m8), x + __ffs(m8) - 1, x + 31 - __clz(m8), y);
+}
+
+__device__ __forceinline__ uint4 load_chunk(const uint16_t* __restrict__ L, size_t pitch, int W,
+                                            int H, int x, int y, bool vec) {
+    if (y >= H || x >= W) return make_uint4(0, 0, 0, 0);
+    const uint16_t* p = L + (size_t)y * pitch + x;
+    if (vec && x + 8 <= W) return __ldg(reinterpret_cast<const uint4*>(p));
+    uint32_t wv[4] = {0, 0, 0, 0};
+    for (int k = 0; k < 8; ++k)
+        if (x + k < W) wv[k >> 1] |= (uint32_t)p[k] << (16 * (k & 1));
+    return make_uint4(wv[0], wv[1], wv[2], wv[3]);
+}
+
+// warp-aggregated flush of one cache entry per lane (REDUX per distinct label)
+__device__ __forceinline__ void warp_flush(const CacheEnt& e, const LabelTable& t) {
+    const unsigned lane = lane_id();
+    unsigned todo = __ballot_sync(kFull, e.label != 0);
+    while (todo) {
+        const int leader = __ffs(todo) - 1;
+        const uint32_t L = __shfl_sync(kFull, e.label, leader);
+        const bool mine = e.label == L;
+        const unsigned peers = __ballot_sync(kFull, mine);
+        todo &= ~peers;
+        const uint32_t cnt = __reduce_add_sync(kFull, mine ? e.cnt : 0u);
+        const uint32_t x0 = __reduce_min_sync(kFull, mine ? e.x0 : 0xffffffffu);
+        const uint32_t x1 = __reduce_max_sync(kFull, mine ? e.x1 : 0u);
+        const uint32_t y0 = __reduce_min_sync(kFull, mine ? e.y0 : 0xffffffffu);
+        const uint32_t y1 = __reduce_max_sync(kFull, mine ? e.y1 : 0u);
+        if ((int)lane == leader) global_fold(t, CacheEnt{L, cnt, x0, x1, y0, y1});
     }
 }
 
@@ -92,74 +127,33 @@ __device__ __forceinline__ void cache_add(CacheEnt& c0, CacheEnt& c1, ScanSmem& 
 __global__ void __launch_bounds__(kScanThreads)
     k_label_scan(const uint16_t* __restrict__ L, int W, int H, size_t pitch, int vec_ok,
                  LabelTable t) {
-    __shared__ ScanSmem s;
-    for (int i = threadIdx.x; i < kHash; i += kScanThreads) {
-        s.key[i] = 0;
-        s.cnt[i] = 0;
-        s.x0[i] = 0xffffffffu;
-        s.x1[i] = 0;
-        s.y0[i] = 0xffffffffu;
-        s.y1[i] = 0;
-    }
-    __syncthreads();
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int tiles_x = (W + kTileW - 1) / kTileW;
-    const int tiles_y = (H + kTileH - 1) / kTileH;
-    const int n_tiles = tiles_x * tiles_y;
-    for (int tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
-        const int tx = tile % tiles_x, ty = tile / tiles_x;
-        const int x = tx * kTileW + lane * 8;
-        const int ybase = ty * kTileH + warp * kRowsPerWarp;
+    const unsigned lane = lane_id();
+    const int warps_total = gridDim.x * (kScanThreads / 32);
+    const int gw = blockIdx.x * (kScanThreads / 32) + (threadIdx.x >> 5);
+    const int tiles_x = (W + 255) / 256;
+    const int n_tiles = tiles_x * ((H + kStripRows - 1) / kStripRows);
+    for (int tile = gw; tile < n_tiles; tile += warps_total) {
+        const int x = (tile % tiles_x) * 256 + (int)lane * 8;
+        const int y0 = (tile / tiles_x) * kStripRows;
         CacheEnt c0{0, 0, 0, 0, 0, 0}, c1{0, 0, 0, 0, 0, 0};
-        uint4 v[kRowsPerWarp];
-        if (vec_ok && x + 8 <= W) {
+        // software pipeline: batch r0 + kBatch is in flight while batch r0 is folded
+        uint4 v[kBatch], nx[kBatch];
 #pragma unroll
-            for (int r = 0; r < kRowsPerWarp; ++r) {
-                const int y = ybase + r;
-                v[r] = (y < H) ? __ldcs(reinterpret_cast<const uint4*>(L + (size_t)y * pitch + x))
-                               : make_uint4(0, 0, 0, 0);
+        for (int r = 0; r < kBatch; ++r) v[r] = load_chunk(L, pitch, W, H, x, y0 + r, vec_ok);
+#pragma unroll 1
+        for (int r0 = 0; r0 < kStripRows; r0 += kBatch) {
+            if (r0 + kBatch < kStripRows) {
+#pragma unroll
+                for (int r = 0; r < kBatch; ++r)
+                    nx[r] = load_chunk(L, pitch, W, H, x, y0 + r0 + kBatch + r, vec_ok);
             }
-        } else {
 #pragma unroll
-            for (int r = 0; r < kRowsPerWarp; ++r) {
-                const int y = ybase + r;
-                uint32_t wv[4] = {0, 0, 0, 0};
-                if (y < H) {
+            for (int r = 0; r < kBatch; ++r) chunk(v[r], (uint32_t)x, (uint32_t)(y0 + r0 + r), c0, c1, t);
 #pragma unroll
-                    for (int k = 0; k < 8; ++k)
-                        if (x + k < W)
-                            wv[k >> 1] |= (uint32_t)L[(size_t)y * pitch + x + k] << (16 * (k & 1));
-                }
-                v[r] = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-            }
+            for (int r = 0; r < kBatch; ++r) v[r] = nx[r];
         }
-#pragma unroll
-        for (int r = 0; r < kRowsPerWarp; ++r) {
-            const uint32_t wv[4] = {v[r].x, v[r].y, v[r].z, v[r].w};
-            if ((wv[0] | wv[1] | wv[2] | wv[3]) == 0) continue;
-            const uint32_t y = (uint32_t)(ybase + r);
-#pragma unroll
-            for (int k = 0; k < 8; ++k) {
-                const uint32_t l = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu;
-                if (l) cache_add(c0, c1, s, t, l, (uint32_t)(x + k), y);
-            }
-        }
-        hash_fold(s, t, c0);
-        hash_fold(s, t, c1);
-        __syncthreads();
-        for (int i = threadIdx.x; i < kHash; i += kScanThreads) {
-            const uint32_t k = s.key[i];
-            if (k) {
-                global_fold(t, k, s.cnt[i], s.x0[i], s.x1[i], s.y0[i], s.y1[i]);
-                s.key[i] = 0;
-                s.cnt[i] = 0;
-                s.x0[i] = 0xffffffffu;
-                s.x1[i] = 0;
-                s.y0[i] = 0xffffffffu;
-                s.y1[i] = 0;
-            }
-        }
-        __syncthreads();
+        warp_flush(c0, t);
+        warp_flush(c1, t);
     }
 }
 
@@ -174,6 +168,7 @@ __global__ void __launch_bounds__(1024) k_compact_count(LabelTable t, Control* c
 
 // class of a window (w x h) with n pixels
 __device__ __forceinline__ int roi_class(uint32_t w, uint32_t h, unsigned long long n) {
+    if (w <= (uint32_t)kS0W && h <= (uint32_t)kS0H && n <= (unsigned long long)kS1N) return kClassS0;
     if (w <= (uint32_t)kSW && h <= (uint32_t)kSH) return n <= (unsigned long long)kS1N ? kClassS1 : kClassS2;
     return kClassL;
 }
@@ -216,7 +211,13 @@ __global__ void __launch_bounds__(1024) k_compact_emit(LabelTable t, Control* ct
     r.h[rank] = h;
     r.n[rank] = n;
     const int c = roi_class(w, h, n);
-    const uint32_t pos = atomicAdd(&ctl->class_count[c], 1u);
+    // one atomic per (warp, class): the class lists are consumed in any order
+    const unsigned peers = __match_any_sync(__activemask(), c);
+    const int leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if ((int)lane == leader) base = atomicAdd(&ctl->class_count[c], (uint32_t)__popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    const uint32_t pos = base + __popc(peers & lanemask_lt());
     r.cls_list[c][pos] = rank;
     if (c == kClassL) {
         atomicMax(&ctl->l_max_h, h);
