@@ -1,0 +1,148 @@
+// featurex_gpu/engine.hpp -- drop-in C++ engine API of the B200 featurize path.
+//
+// Same namespace, type names, function names, argument meaning and exception
+// types as the reference's engine (/root/reference/proj/include/featurex/
+// engine.hpp:14-81, roi.hpp:13-34, image.hpp:11-27, texture.hpp:30-35,
+// errors.hpp:8-58), so callers of the reference compile unchanged against this
+// header and link libfxg.so instead of libfeaturex.a.  Every compute call runs
+// the sm_100a kernels through the C ABI (include/fxg.h); there is no CPU path.
+//
+// Differences (documented in INTEGRATION.md):
+//  - ExtractionConfig::threads / parallel / memory_budget / spill_dir are
+//    validated like the reference but do not change the (device) execution.
+//  - groups shape / glrlm / glszm / ngtdm have no device kernel yet and raise
+//    ConfigError from compute_roi_features / run (never a silent CPU fallback).
+#pragma once
+
+#include <cstdint>
+#include <filesystem>
+#include <limits>
+#include <optional>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace featurex {
+
+// ---- errors (errors.hpp:8-58) -----------------------------------------------
+struct IoError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct FormatError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct PairingError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct SpillIoError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ZeroMassError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct UnknownProfile : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
+// device-side failures (no reference counterpart)
+struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+// ---- data types -------------------------------------------------------------
+struct IntensityImage {  // image.hpp:11-18
+    int width = 0;
+    int height = 0;
+    int bit_depth = 16;
+    std::vector<uint16_t> pixels;
+    uint16_t at(int x, int y) const { return pixels[static_cast<size_t>(y) * width + x]; }
+};
+
+struct LabelMask {  // image.hpp:20-27
+    int width = 0;
+    int height = 0;
+    std::vector<uint16_t> labels;
+    uint16_t at(int x, int y) const { return labels[static_cast<size_t>(y) * width + x]; }
+};
+
+struct Pixel {  // roi.hpp:13-17
+    uint32_t x = 0;
+    uint32_t y = 0;
+    uint16_t intensity = 0;
+};
+
+struct BoundingBox {  // roi.hpp:19-24
+    uint32_t x_min = 0, y_min = 0, x_max = 0, y_max = 0;
+    int width() const { return static_cast<int>(x_max - x_min) + 1; }
+    int height() const { return static_cast<int>(y_max - y_min) + 1; }
+};
+
+struct PixelCloud {  // roi.hpp:28-34
+    uint32_t label = 0;
+    std::vector<Pixel> pixels;
+    BoundingBox bbox;
+    size_t count() const { return pixels.size(); }
+};
+
+struct GlcmParams {  // texture.hpp:30-35
+    int ng = 256;
+    int offset = 1;
+    std::vector<int> angles = {0, 45, 90, 135};
+    bool symmetric = true;
+};
+
+struct TextureParams {  // engine.hpp:14-17
+    GlcmParams glcm;
+    int histogram_bins = 256;
+};
+
+TextureParams resolve_profile(const std::string& name);
+
+struct ExtractionConfig {  // engine.hpp:24-38
+    std::filesystem::path intensity_dir;
+    std::filesystem::path mask_dir;
+    std::string file_pattern = "*.pgm";
+    std::vector<std::string> features = {"*ALL*"};
+    std::string profile = "default";
+    int threads = 1;
+    size_t memory_budget = std::numeric_limits<size_t>::max();
+    std::optional<GlcmParams> glcm_override;
+    std::optional<int> histogram_bins_override;
+    std::filesystem::path output_path;
+    std::filesystem::path spill_dir;
+    int rows_per_tile = 256;
+    bool parallel = true;
+    int device = 0;  // extension: CUDA device used by run()
+};
+
+struct FeatureRow {  // engine.hpp:41-46
+    std::string image_name;
+    std::string mask_name;
+    uint32_t roi_label = 0;
+    std::vector<double> values;
+};
+
+struct RunSummary {  // engine.hpp:48-56
+    int images = 0;
+    size_t rois = 0;
+    size_t rows = 0;
+    double elapsed_seconds = 0;
+    int failed_pairs = 0;
+    bool completed_with_errors() const { return failed_pairs > 0; }
+};
+
+std::vector<std::string> resolve_feature_groups(const std::vector<std::string>& requested);
+std::vector<std::string> feature_columns(const std::vector<std::string>& groups,
+                                         const TextureParams& params);
+std::vector<double> compute_roi_features(const PixelCloud& cloud,
+                                         const std::vector<std::string>& groups,
+                                         const TextureParams& params);
+RunSummary run(const ExtractionConfig& config);
+size_t write_csv(const std::vector<std::string>& columns, std::vector<FeatureRow> rows,
+                 const std::filesystem::path& path);
+
+// ---- in-memory image-level featurization (the device-native entry point) ----
+struct FeatureTable {
+    std::vector<std::string> columns;
+    std::vector<uint32_t> labels;  // ascending
+    std::vector<double> values;    // [labels.size() x columns.size()] row-major
+};
+// RoiRegistry::accumulate + compute_roi_features for every label of one pair,
+// on the GPU (engine.cpp:300-336 without file I/O).
+FeatureTable featurize(const IntensityImage& image, const LabelMask& mask,
+                       const std::vector<std::string>& groups, const TextureParams& params,
+                       int device = 0);
+
+// PGM P5 I/O (pgm.hpp:14-21), host-side.
+IntensityImage load_intensity(const std::filesystem::path& path);
+LabelMask load_mask(const std::filesystem::path& path);
+void write_pgm(const std::filesystem::path& path, int width, int height, int maxval,
+               const std::vector<uint16_t>& samples);
+
+}  // namespace featurex

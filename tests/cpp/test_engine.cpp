@@ -1,0 +1,202 @@
+// C++ engine-layer tests, re-expressing the reference's engine contract tests
+// (/root/reference/proj/tests/test_engine.cpp:60-227) against the drop-in
+// header include/featurex_gpu/engine.hpp.  Built and run by tests/test_engine_cpp.py.
+//   ./test_engine            all cases (needs a B200)
+//   ./test_engine --host     host-only cases (profiles, groups, columns, CSV)
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <random>
+#include <sstream>
+
+#include "featurex_gpu/engine.hpp"
+
+using namespace featurex;
+
+static int g_fail = 0, g_checks = 0;
+#define CHECK(c)                                                              \
+    do {                                                                      \
+        ++g_checks;                                                           \
+        if (!(c)) {                                                           \
+            ++g_fail;                                                         \
+            std::fprintf(stderr, "CHECK failed %s:%d: %s\n", __FILE__, __LINE__, #c); \
+        }                                                                     \
+    } while (0)
+#define CHECK_THROWS_AS(expr, T)          \
+    do {                                  \
+        bool ok_ = false;                 \
+        try {                             \
+            expr;                         \
+        } catch (const T&) {              \
+            ok_ = true;                   \
+        } catch (...) {                   \
+        }                                 \
+        CHECK(ok_ && #T);                 \
+    } while (0)
+
+static std::filesystem::path fresh_dir(const std::string& name) {
+    const auto d = std::filesystem::temp_directory_path() / name;
+    std::filesystem::remove_all(d);
+    std::filesystem::create_directories(d / "int");
+    std::filesystem::create_directories(d / "seg");
+    return d;
+}
+
+static std::string slurp(const std::filesystem::path& p) {
+    std::ifstream in(p, std::ios::binary);
+    return std::string((std::istreambuf_iterator<char>(in)), std::istreambuf_iterator<char>());
+}
+
+static void write_simple_pair(const std::filesystem::path& d) {  // test_engine.cpp:30-35
+    write_pgm(d / "int" / "a.pgm", 4, 4, 255,
+              {10, 20, 30, 40, 50, 60, 70, 80, 90, 100, 110, 120, 130, 140, 150, 160});
+    write_pgm(d / "seg" / "a.pgm", 4, 4, 255, {1, 1, 0, 0, 1, 1, 0, 0, 0, 0, 2, 2, 0, 0, 2, 2});
+}
+
+static void host_cases() {
+    CHECK(resolve_profile("performance").glcm.angles.size() == 1);
+    CHECK(resolve_profile("default").glcm.ng == 64);
+    CHECK(resolve_profile("ibsi-like").glcm.ng == 256 && resolve_profile("ibsi-like").glcm.symmetric);
+    CHECK_THROWS_AS(resolve_profile("bogus"), UnknownProfile);
+    CHECK_THROWS_AS(resolve_feature_groups({"intensity", "nope"}), ConfigError);
+    CHECK_THROWS_AS(resolve_feature_groups({}), ConfigError);
+    CHECK(resolve_feature_groups({"*ALL*"}).size() == 7);
+    CHECK((resolve_feature_groups({"shape", "intensity"}) == std::vector<std::string>{"intensity", "shape"}));
+    TextureParams p = resolve_profile("performance");
+    auto cols = feature_columns({"glcm"}, p);
+    CHECK(cols.size() == 58 && cols[0] == "glcm_asm_0" && cols[1] == "glcm_asm_ave");
+    CHECK(feature_columns({"glcm"}, resolve_profile("default")).size() == 145);
+    CHECK(feature_columns({"*ALL*"}, resolve_profile("default")).size() == 427);
+    const auto path = std::filesystem::temp_directory_path() / "fxg_csv.csv";  // :135-152
+    CHECK(write_csv({"x"}, {}, path) == 0);
+    CHECK(slurp(path) == "image,mask,label,x\n");
+    write_csv({"x"}, {{"a.pgm", "a.pgm", 2, {1.0}}, {"a.pgm", "a.pgm", 1, {2.0}}}, path);
+    CHECK(slurp(path) == "image,mask,label,x\na.pgm,a.pgm,1,2\na.pgm,a.pgm,2,1\n");
+    write_csv({"x"}, {{"a", "a", 1, {1.0 / 3.0}}}, path);
+    CHECK(slurp(path) == "image,mask,label,x\na,a,1,0.3333333333\n");
+    // PGM round trip
+    const auto pg = std::filesystem::temp_directory_path() / "fxg_rt.pgm";
+    write_pgm(pg, 3, 2, 65535, {1, 2, 3, 65535, 0, 7});
+    const IntensityImage im = load_intensity(pg);
+    CHECK(im.width == 3 && im.height == 2 && im.bit_depth == 16 && im.pixels[3] == 65535);
+    std::ofstream(pg) << "P5\n2 2\n255\nX";
+    CHECK_THROWS_AS(load_intensity(pg), FormatError);
+    CHECK_THROWS_AS(load_mask("/nonexistent/x.pgm"), IoError);
+}
+
+static void device_cases() {
+    {  // one row per ROI (:77-97)
+        const auto d = fresh_dir("fxg_engine_simple");
+        write_simple_pair(d);
+        ExtractionConfig c;
+        c.intensity_dir = d / "int";
+        c.mask_dir = d / "seg";
+        c.output_path = d / "features.csv";
+        c.features = {"intensity"};
+        const RunSummary s = run(c);
+        CHECK(s.images == 1 && s.rois == 2 && s.rows == 2 && !s.completed_with_errors());
+        std::ifstream in(c.output_path);
+        std::string header, r1, r2, extra;
+        CHECK(bool(std::getline(in, header)) && header.substr(0, 17) == "image,mask,label,");
+        CHECK(bool(std::getline(in, r1)) && r1.substr(0, 14) == "a.pgm,a.pgm,1,");
+        CHECK(bool(std::getline(in, r2)) && r2.substr(0, 14) == "a.pgm,a.pgm,2,");
+        CHECK(!std::getline(in, extra));
+    }
+    {  // empty mask -> header only (:99-111); default features *ALL* -> ConfigError? no: empty pair
+        const auto d = fresh_dir("fxg_engine_empty");
+        write_pgm(d / "int" / "a.pgm", 2, 2, 255, {1, 2, 3, 4});
+        write_pgm(d / "seg" / "a.pgm", 2, 2, 255, {0, 0, 0, 0});
+        ExtractionConfig c;
+        c.intensity_dir = d / "int";
+        c.mask_dir = d / "seg";
+        c.output_path = d / "f.csv";
+        c.features = {"intensity", "moments", "glcm"};
+        const RunSummary s = run(c);
+        CHECK(s.rois == 0 && s.rows == 0);
+        std::ifstream in(c.output_path);
+        std::string line;
+        CHECK(bool(std::getline(in, line)));
+        CHECK(!std::getline(in, line));
+    }
+    {  // unmatched and corrupt pairs are skipped (:113-133)
+        const auto d = fresh_dir("fxg_engine_skip");
+        write_simple_pair(d);
+        write_pgm(d / "seg" / "orphan.pgm", 1, 1, 255, {1});
+        std::ofstream(d / "int" / "bad.pgm") << "P5\n2 2\n255\nX";
+        write_pgm(d / "seg" / "bad.pgm", 2, 2, 255, {1, 0, 0, 0});
+        ExtractionConfig c;
+        c.intensity_dir = d / "int";
+        c.mask_dir = d / "seg";
+        c.output_path = d / "f.csv";
+        c.features = {"intensity", "moments"};
+        const RunSummary s = run(c);
+        CHECK(s.images == 1 && s.rows == 2 && s.completed_with_errors() && s.failed_pairs == 2);
+    }
+    {  // groups without a device kernel fail loudly per pair (no CPU fallback)
+        const auto d = fresh_dir("fxg_engine_shape");
+        write_simple_pair(d);
+        ExtractionConfig c;
+        c.intensity_dir = d / "int";
+        c.mask_dir = d / "seg";
+        c.output_path = d / "f.csv";
+        c.features = {"shape"};
+        const RunSummary s = run(c);
+        CHECK(s.images == 0 && s.failed_pairs == 1);
+        PixelCloud pc;
+        pc.pixels = {{1, 1, 5}};
+        CHECK_THROWS_AS(compute_roi_features(pc, {"shape"}, resolve_profile("default")), ConfigError);
+    }
+    {  // rerun idempotent (:174-182) and per-ROI operator == image-level row
+        const auto d = fresh_dir("fxg_engine_idem");
+        write_simple_pair(d);
+        ExtractionConfig c;
+        c.intensity_dir = d / "int";
+        c.mask_dir = d / "seg";
+        c.output_path = d / "f.csv";
+        c.features = {"intensity", "moments", "glcm"};
+        run(c);
+        const std::string first = slurp(c.output_path);
+        run(c);
+        CHECK(slurp(c.output_path) == first);
+        PixelCloud pc;
+        pc.label = 2;
+        pc.pixels = {{2, 2, 110}, {3, 2, 120}, {2, 3, 150}, {3, 3, 160}};
+        pc.bbox = {2, 2, 3, 3};
+        const auto v = compute_roi_features(pc, c.features, resolve_profile("default"));
+        IntensityImage im = load_intensity(d / "int" / "a.pgm");
+        LabelMask mk = load_mask(d / "seg" / "a.pgm");
+        const FeatureTable t = featurize(im, mk, c.features, resolve_profile("default"));
+        CHECK(t.labels.size() == 2 && t.labels[1] == 2);
+        bool same = v.size() == t.columns.size();
+        for (size_t i = 0; same && i < v.size(); ++i) same = v[i] == t.values[t.columns.size() + i];
+        CHECK(same);
+    }
+    {  // pairing errors
+        IntensityImage im;
+        im.width = 2;
+        im.height = 2;
+        im.pixels = {1, 2, 3, 4};
+        LabelMask mk;
+        mk.width = 1;
+        mk.height = 4;
+        mk.labels = {1, 1, 1, 1};
+        CHECK_THROWS_AS(featurize(im, mk, {"intensity"}, resolve_profile("default")), PairingError);
+        ExtractionConfig c;
+        c.threads = 0;
+        CHECK_THROWS_AS(run(c), ConfigError);
+    }
+}
+
+int main(int argc, char** argv) {
+    const bool host_only = argc > 1 && std::strcmp(argv[1], "--host") == 0;
+    try {
+        host_cases();
+        if (!host_only) device_cases();
+    } catch (const std::exception& e) {
+        std::fprintf(stderr, "unexpected exception: %s\n", e.what());
+        return 2;
+    }
+    std::printf("%d checks, %d failures\n", g_checks, g_fail);
+    return g_fail ? 1 : 0;
+}
