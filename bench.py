@@ -109,6 +109,18 @@ class ClockSampler:
                 "reasons": sorted(reasons), "samples": len(sm)}
 
 
+def profiled_traffic(kernel):
+    """dram read+write bytes per launch from the committed ncu capture, or None."""
+    import re
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f).get("bytes_per_launch", {})
+    norm = {re.sub(r"<(\d+).*>", r"\1", k): v for k, v in d.items()}
+    return norm.get(kernel)
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -299,7 +311,7 @@ def main():
         "kernels_ms_per_step": {k: round(v[0] / args.steps, 4) for k, v in ktimes.items()},
         "roofline": {"kernel": dom_name, "bound": "hbm", "achieved": round(achieved, 1),
                      "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
-                     "traffic": None, "peak_source": peak_src,
+                     "traffic": profiled_traffic(dom_name), "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": int(algo_bytes.get(dom_name, call_bytes))},
         "clocks": clk.summary(),
     }
