@@ -148,6 +148,23 @@ int fx_roi_features(fx_ctx* ctx, const uint32_t* xs, const uint32_t* ys,
                     const uint16_t* intensities, size_t n, unsigned groups,
                     const fx_texture_params* params, double* out, size_t cap);
 
+/* ---- band sharding (C5: a whole slide split into row bands across GPUs) -----
+ * 1. every rank: fx_scan_accumulate(own band, reset=1)  -> partial label table in
+ *    GLOBAL coordinates (origin_x/origin_y of the band image);
+ * 2. merge the partial tables across ranks (count: sum; xmin,ymin: min; xmax,ymax:
+ *    max) -- fx_label_table_copy out, NCCL all-reduce, copy back in;
+ * 3. every rank: fx_featurize_owned(band + halo rows, own rows [y0, y1)) -> rows of
+ *    the ROIs whose first row lies in its band (the owner holds the whole window,
+ *    so order statistics and the contour edge set need no merging).
+ * Results are identical to fx_featurize on the whole image, for any band count. */
+int fx_scan_accumulate(fx_ctx* ctx, const fx_image* band, int reset);
+/* cnt: u64[65536]; bbox: u32[4][65536] = xmin | ymin | xmax | ymax (global coords).
+ * to_ctx = 0 copies the ctx's table out, 1 loads it in.  mem_kind: the buffers. */
+int fx_label_table_copy(fx_ctx* ctx, uint64_t* cnt, uint32_t* bbox, int to_ctx, int mem_kind);
+int fx_featurize_owned(fx_ctx* ctx, const fx_image* image, int own_y0, int own_y1,
+                       unsigned groups, const fx_texture_params* params, uint32_t* out_labels,
+                       double* out_values, size_t cap_rois, size_t* n_rois);
+
 /* Label scan only (RoiRegistry::accumulate + labels(), roi.cpp:76-117):
  * ascending labels, pixel counts and inclusive bboxes [xmin,ymin,xmax,ymax]
  * in image coordinates (origin added).  Host output buffers. */

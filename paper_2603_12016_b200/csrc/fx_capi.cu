@@ -25,9 +25,9 @@
 
 namespace fxg {
 __global__ void k_label_scan(const uint16_t* L, int W, int H, size_t pitch, int vec_ok,
-                             LabelTable t);
-__global__ void k_compact_count(LabelTable t, Control* ctl);
-__global__ void k_compact_emit(LabelTable t, Control* ctl, RoiList r);
+                             uint32_t ox, uint32_t oy, LabelTable t);
+__global__ void k_compact_count(LabelTable t, Control* ctl, CompactArgs a);
+__global__ void k_compact_emit(LabelTable t, Control* ctl, RoiList r, CompactArgs a);
 cudaError_t roi_s_setup(int* occ /* [3][2]: class x glcm */);
 void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
                   const CUtensorMap& tmap72, int tma40, int tma72, DevImage img, RoiList rl,
@@ -282,32 +282,46 @@ struct DebugHost {
     unsigned long long* pairs = nullptr;
 };
 
-// Core pipeline on a device-resident image.  out_dev: [cap_rois x ncols] device.
-int run_pipeline(fx_ctx* c, const DevImage& img, unsigned groups, const fx_texture_params& p,
-                 double* out_dev, size_t cap_rois, size_t* n_rois, const DebugOut* dbg_dev) {
+// Label scan of one image (or band) into the ctx's label table, in global
+// coordinates (image origin added).  reset clears the table first.
+int scan_stage(fx_ctx* c, const DevImage& img, bool reset) {
+    LabelTable t = label_table(c);
+    cudaStream_t s = c->stream;
+    if (reset) {
+        CK(cudaMemsetAsync(c->d_cnt, 0, kMaxLabels * sizeof(unsigned long long), s));
+        CK(cudaMemsetAsync(c->d_bb, 0xff, 2 * kMaxLabels * sizeof(uint32_t), s));
+        CK(cudaMemsetAsync(c->d_bb + 2 * kMaxLabels, 0, 2 * kMaxLabels * sizeof(uint32_t), s));
+    }
+    const int vec_ok = ((reinterpret_cast<uintptr_t>(img.L) & 15u) == 0) && (img.pitch % 8 == 0);
+    const int tiles = ((img.w + 255) / 256) * ((img.h + 63) / 64);
+    const int grid = std::max(1, std::min((tiles + 3) / 4, c->sm_count * 8));
+    Launch l(c, "k_label_scan");
+    k_label_scan<<<grid, 128, 0, s>>>(img.L, img.w, img.h, img.pitch, vec_ok, (uint32_t)img.ox,
+                                      (uint32_t)img.oy, t);
+    CK(cudaGetLastError());
+    return FX_OK;
+}
+
+// Compaction (owned rows [own_y0, own_y1)) + per-ROI kernels over the ctx's label
+// table, reading pixels of img.  out_dev: [cap_rois x ncols] device.
+int featurize_stage(fx_ctx* c, const DevImage& img, uint32_t own_y0, uint32_t own_y1,
+                    unsigned groups, const fx_texture_params& p, double* out_dev, size_t cap_rois,
+                    size_t* n_rois, const DebugOut* dbg_dev) {
     const FeatCfg cfg = make_cfg(groups, p);
     const int vrc = validate_texture(groups, p);
     LabelTable t = label_table(c);
     RoiList rl = roi_list(c);
     cudaStream_t s = c->stream;
-    CK(cudaMemsetAsync(c->d_cnt, 0, kMaxLabels * sizeof(unsigned long long), s));
-    CK(cudaMemsetAsync(c->d_bb, 0xff, 2 * kMaxLabels * sizeof(uint32_t), s));
-    CK(cudaMemsetAsync(c->d_bb + 2 * kMaxLabels, 0, 2 * kMaxLabels * sizeof(uint32_t), s));
     CK(cudaMemsetAsync(c->d_ctl, 0, sizeof(Control), s));
-    {
-        const int vec_ok = ((reinterpret_cast<uintptr_t>(img.L) & 15u) == 0) && (img.pitch % 8 == 0);
-        const int tiles = ((img.w + 255) / 256) * ((img.h + 63) / 64);
-        const int grid = std::max(1, std::min((tiles + 3) / 4, c->sm_count * 8));
-        Launch l(c, "k_label_scan");
-        k_label_scan<<<grid, 128, 0, s>>>(img.L, img.w, img.h, img.pitch, vec_ok, t);
-    }
+    const CompactArgs ca{(uint32_t)img.ox, (uint32_t)img.oy, own_y0, own_y1, (uint32_t)img.w,
+                         (uint32_t)img.h};
     {
         Launch l(c, "k_compact_count");
-        k_compact_count<<<64, 1024, 0, s>>>(t, c->d_ctl);
+        k_compact_count<<<64, 1024, 0, s>>>(t, c->d_ctl, ca);
     }
     {
         Launch l(c, "k_compact_emit");
-        k_compact_emit<<<64, 1024, 0, s>>>(t, c->d_ctl, rl);
+        k_compact_emit<<<64, 1024, 0, s>>>(t, c->d_ctl, rl, ca);
     }
     CK(cudaGetLastError());
     CK(cudaEventRecord(c->ev_compact, s));
@@ -338,6 +352,10 @@ int run_pipeline(fx_ctx* c, const DevImage& img, unsigned groups, const fx_textu
     CK(cudaEventSynchronize(c->ev_stats));
     const Control hc = *c->h_ctl;
     *n_rois = hc.n_rois;
+    if (hc.error & kErrWindow) {
+        cudaStreamSynchronize(s);
+        return set_error(FX_E_ARG, "an owned ROI window extends beyond the image (halo too small)");
+    }
     if (hc.n_rois > cap_rois) {
         cudaStreamSynchronize(s);
         return set_error(FX_E_CAPACITY, "output capacity " + std::to_string(cap_rois) +
@@ -360,6 +378,13 @@ int run_pipeline(fx_ctx* c, const DevImage& img, unsigned groups, const fx_textu
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
     return FX_OK;
+}
+
+int run_pipeline(fx_ctx* c, const DevImage& img, unsigned groups, const fx_texture_params& p,
+                 double* out_dev, size_t cap_rois, size_t* n_rois, const DebugOut* dbg_dev) {
+    int rc = scan_stage(c, img, true);
+    if (rc) return rc;
+    return featurize_stage(c, img, 0u, 0xffffffffu, groups, p, out_dev, cap_rois, n_rois, dbg_dev);
 }
 
 int finish(fx_ctx* c) {
@@ -587,6 +612,75 @@ int fx_featurize(fx_ctx* c, const fx_image* im, unsigned groups, const fx_textur
     return finish(c);
 }
 
+int fx_scan_accumulate(fx_ctx* c, const fx_image* im, int reset) {
+    if (!c || !im || !im->labels) return set_error(FX_E_ARG, "null argument");
+    if (im->width < 1 || im->height < 1) return set_error(FX_E_PAIRING, "empty raster");
+    CK(cudaSetDevice(c->device));
+    fx_image lab_only = *im;
+    if (!lab_only.intensity) lab_only.intensity = lab_only.labels;  // scan reads labels only
+    DevImage d;
+    int rc = stage_image(c, &lab_only, &d);
+    if (!rc) rc = scan_stage(c, d, reset != 0);
+    if (rc) return rc;
+    CK(cudaStreamSynchronize(c->stream));
+    return FX_OK;
+}
+
+int fx_label_table_copy(fx_ctx* c, uint64_t* cnt, uint32_t* bbox, int to_ctx, int mem_kind) {
+    if (!c || !cnt || !bbox) return set_error(FX_E_ARG, "null argument");
+    CK(cudaSetDevice(c->device));
+    const cudaMemcpyKind k = to_ctx ? (mem_kind == FX_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                 : cudaMemcpyHostToDevice)
+                                    : (mem_kind == FX_MEM_DEVICE ? cudaMemcpyDeviceToDevice
+                                                                 : cudaMemcpyDeviceToHost);
+    const size_t bc = kMaxLabels * sizeof(unsigned long long), bb = 4 * kMaxLabels * sizeof(uint32_t);
+    if (to_ctx) {
+        CK(cudaMemcpyAsync(c->d_cnt, cnt, bc, k, c->stream));
+        CK(cudaMemcpyAsync(c->d_bb, bbox, bb, k, c->stream));
+    } else {
+        CK(cudaMemcpyAsync(cnt, c->d_cnt, bc, k, c->stream));
+        CK(cudaMemcpyAsync(bbox, c->d_bb, bb, k, c->stream));
+    }
+    CK(cudaStreamSynchronize(c->stream));
+    return FX_OK;
+}
+
+int fx_featurize_owned(fx_ctx* c, const fx_image* im, int own_y0, int own_y1, unsigned groups,
+                       const fx_texture_params* p, uint32_t* out_labels, double* out_values,
+                       size_t cap_rois, size_t* n_rois) {
+    if (!c || !im || !p || !n_rois) return set_error(FX_E_ARG, "null argument");
+    if (!im->intensity || !im->labels) return set_error(FX_E_ARG, "null raster");
+    if (own_y0 < 0 || own_y1 < own_y0) return set_error(FX_E_ARG, "bad owned row range");
+    *n_rois = 0;
+    int rc = check_groups(groups);
+    if (rc) return rc;
+    CK(cudaSetDevice(c->device));
+    DevImage d;
+    rc = stage_image(c, im, &d);
+    if (rc) return rc;
+    const FeatCfg cfg = make_cfg(groups, *p);
+    double* out_dev = out_values;
+    if (im->mem_kind == FX_MEM_HOST) {
+        rc = ensure_out(c, std::max<size_t>(1, cap_rois) * (size_t)cfg.ncols);
+        if (rc) return rc;
+        out_dev = c->d_out;
+    }
+    rc = featurize_stage(c, d, (uint32_t)own_y0, (uint32_t)own_y1, groups, *p, out_dev, cap_rois,
+                         n_rois, nullptr);
+    if (rc) {
+        cudaStreamSynchronize(c->stream);
+        return rc;
+    }
+    const size_t nr = *n_rois;
+    if (nr) {
+        const cudaMemcpyKind k = im->mem_kind == FX_MEM_HOST ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+        if (im->mem_kind == FX_MEM_HOST)
+            CK(cudaMemcpyAsync(out_values, out_dev, nr * cfg.ncols * sizeof(double), k, c->stream));
+        CK(cudaMemcpyAsync(out_labels, roi_list(c).label, nr * sizeof(uint32_t), k, c->stream));
+    }
+    return finish(c);
+}
+
 int fx_featurize_u16(fx_ctx* c, const uint16_t* intensity, const uint16_t* labels, int width,
                      int height, size_t pitch, int mem_kind, unsigned groups,
                      const fx_texture_params* p, uint32_t* out_labels, double* out_values,
@@ -637,27 +731,20 @@ int fx_roi_table(fx_ctx* c, const fx_image* im, uint32_t* out_labels, uint64_t* 
     DevImage d;
     int rc = stage_image(c, im, &d);
     if (rc) return rc;
-    LabelTable t = label_table(c);
     RoiList rl = roi_list(c);
     cudaStream_t s = c->stream;
-    CK(cudaMemsetAsync(c->d_cnt, 0, kMaxLabels * sizeof(unsigned long long), s));
-    CK(cudaMemsetAsync(c->d_bb, 0xff, 2 * kMaxLabels * sizeof(uint32_t), s));
-    CK(cudaMemsetAsync(c->d_bb + 2 * kMaxLabels, 0, 2 * kMaxLabels * sizeof(uint32_t), s));
+    rc = scan_stage(c, d, true);
+    if (rc) return rc;
+    LabelTable t = label_table(c);
     CK(cudaMemsetAsync(c->d_ctl, 0, sizeof(Control), s));
-    const int vec_ok = ((reinterpret_cast<uintptr_t>(d.L) & 15u) == 0) && (d.pitch % 8 == 0);
-    const int tiles = ((d.w + 255) / 256) * ((d.h + 63) / 64);
-    {
-        Launch l(c, "k_label_scan");
-        k_label_scan<<<std::max(1, std::min((tiles + 3) / 4, c->sm_count * 8)), 128, 0, s>>>(
-            d.L, d.w, d.h, d.pitch, vec_ok, t);
-    }
+    const CompactArgs ca{(uint32_t)d.ox, (uint32_t)d.oy, 0u, 0xffffffffu, (uint32_t)d.w, (uint32_t)d.h};
     {
         Launch l(c, "k_compact_count");
-        k_compact_count<<<64, 1024, 0, s>>>(t, c->d_ctl);
+        k_compact_count<<<64, 1024, 0, s>>>(t, c->d_ctl, ca);
     }
     {
         Launch l(c, "k_compact_emit");
-        k_compact_emit<<<64, 1024, 0, s>>>(t, c->d_ctl, rl);
+        k_compact_emit<<<64, 1024, 0, s>>>(t, c->d_ctl, rl, ca);
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));

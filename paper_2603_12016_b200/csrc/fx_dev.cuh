@@ -53,6 +53,15 @@ struct Control {
 
 constexpr uint32_t kErrCapacity = 1u;  // L slab too small for a ROI
 constexpr uint32_t kErrRuns = 2u;      // L run capacity exceeded
+constexpr uint32_t kErrWindow = 4u;    // an owned ROI window is not inside the image
+
+// compaction parameters: origin of the image being read (the label table holds
+// global coordinates) and the owned row range (band sharding; [0, ~0) = all)
+struct CompactArgs {
+    uint32_t ox, oy;
+    uint32_t own_y0, own_y1;
+    uint32_t img_w, img_h;
+};
 
 // Compacted ROI list: rank r == output row r (labels ascending).
 struct RoiList {

@@ -126,7 +126,7 @@ __device__ __forceinline__ void warp_flush(const CacheEnt& e, const LabelTable& 
 
 __global__ void __launch_bounds__(kScanThreads)
     k_label_scan(const uint16_t* __restrict__ L, int W, int H, size_t pitch, int vec_ok,
-                 LabelTable t) {
+                 uint32_t ox, uint32_t oy, LabelTable t) {
     const unsigned lane = lane_id();
     const int warps_total = gridDim.x * (kScanThreads / 32);
     const int gw = blockIdx.x * (kScanThreads / 32) + (threadIdx.x >> 5);
@@ -148,7 +148,8 @@ __global__ void __launch_bounds__(kScanThreads)
                     nx[r] = load_chunk(L, pitch, W, H, x, y0 + r0 + kBatch + r, vec_ok);
             }
 #pragma unroll
-            for (int r = 0; r < kBatch; ++r) chunk(v[r], (uint32_t)x, (uint32_t)(y0 + r0 + r), c0, c1, t);
+            for (int r = 0; r < kBatch; ++r)
+                chunk(v[r], (uint32_t)x + ox, (uint32_t)(y0 + r0 + r) + oy, c0, c1, t);
 #pragma unroll
             for (int r = 0; r < kBatch; ++r) v[r] = nx[r];
         }
@@ -159,9 +160,16 @@ __global__ void __launch_bounds__(kScanThreads)
 
 // --- compaction -------------------------------------------------------------
 
-__global__ void __launch_bounds__(1024) k_compact_count(LabelTable t, Control* ctl) {
+// a label is emitted when present and owned (its first row in [own_y0, own_y1))
+__device__ __forceinline__ bool owned(const LabelTable& t, uint32_t l, const CompactArgs& a) {
+    if (l == 0 || t.cnt[l] == 0ull) return false;
+    const uint32_t y = t.ymin[l];
+    return y >= a.own_y0 && y < a.own_y1;
+}
+
+__global__ void __launch_bounds__(1024) k_compact_count(LabelTable t, Control* ctl, CompactArgs a) {
     const uint32_t l = blockIdx.x * 1024 + threadIdx.x;
-    const int present = (l != 0 && t.cnt[l] != 0ull);
+    const int present = owned(t, l, a);
     const int c = __syncthreads_count(present);
     if (threadIdx.x == 0) ctl->block_sum[blockIdx.x] = (uint32_t)c;
 }
@@ -173,15 +181,16 @@ __device__ __forceinline__ int roi_class(uint32_t w, uint32_t h, unsigned long l
     return kClassL;
 }
 
-__global__ void __launch_bounds__(1024) k_compact_emit(LabelTable t, Control* ctl, RoiList r) {
+__global__ void __launch_bounds__(1024) k_compact_emit(LabelTable t, Control* ctl, RoiList r,
+                                                       CompactArgs a) {
     __shared__ uint32_t warp_cnt[32];
     __shared__ uint32_t block_base;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     if (warp == 0) {
-        uint32_t a = (lane < blockIdx.x) ? ctl->block_sum[lane] : 0;
-        uint32_t b = (lane + 32 < blockIdx.x) ? ctl->block_sum[lane + 32] : 0;
-        uint32_t s = warp_sum(a + b);
-        if (lane == 0) block_base = s;
+        const uint32_t s0 = (lane < blockIdx.x) ? ctl->block_sum[lane] : 0;
+        const uint32_t s1 = (lane + 32 < blockIdx.x) ? ctl->block_sum[lane + 32] : 0;
+        const uint32_t sum = warp_sum(s0 + s1);
+        if (lane == 0) block_base = sum;
         if (blockIdx.x == gridDim.x - 1) {
             uint32_t tot = warp_sum((lane < gridDim.x ? ctl->block_sum[lane] : 0u) +
                                     (lane + 32 < gridDim.x ? ctl->block_sum[lane + 32] : 0u));
@@ -189,8 +198,8 @@ __global__ void __launch_bounds__(1024) k_compact_emit(LabelTable t, Control* ct
         }
     }
     const uint32_t l = blockIdx.x * 1024 + tid;
-    const unsigned long long n = (l != 0) ? t.cnt[l] : 0ull;
-    const bool present = n != 0ull;
+    const bool present = owned(t, l, a);
+    const unsigned long long n = present ? t.cnt[l] : 0ull;
     const unsigned m = __ballot_sync(kFull, present);
     if (lane == 0) warp_cnt[warp] = __popc(m);
     __syncthreads();
@@ -202,8 +211,11 @@ __global__ void __launch_bounds__(1024) k_compact_emit(LabelTable t, Control* ct
     __syncthreads();
     if (!present) return;
     const uint32_t rank = block_base + warp_cnt[warp] + __popc(m & lanemask_lt());
-    const uint32_t x0 = t.xmin[l], y0 = t.ymin[l];
-    const uint32_t w = t.xmax[l] - x0 + 1, h = t.ymax[l] - y0 + 1;
+    // table holds global coordinates; windows are local to the image being read
+    const uint32_t x0 = t.xmin[l] - a.ox, y0 = t.ymin[l] - a.oy;
+    const uint32_t w = t.xmax[l] - t.xmin[l] + 1, h = t.ymax[l] - t.ymin[l] + 1;
+    if (t.xmin[l] < a.ox || t.ymin[l] < a.oy || x0 + w > a.img_w || y0 + h > a.img_h)
+        atomicOr(&ctl->error, kErrWindow);  // window not inside the image (halo too small)
     r.label[rank] = l;
     r.x0[rank] = x0;
     r.y0[rank] = y0;

@@ -1,0 +1,167 @@
+"""Row-band sharding of one large image across ranks (C5).
+
+One process per GPU.  Rank k owns image rows [y0_k, y1_k).  The exchange steps,
+all through torch.distributed (NCCL on GPUs, gloo in the CPU tests):
+
+1. local label scan of the own band into a label table in global coordinates;
+2. merge of the partial tables (the mergeable accumulators): count = SUM,
+   xmin/ymin = MIN, xmax/ymax = MAX  -- one all-reduce per array, 1.5 MB total,
+   integer-exact, so the merged table is bit-identical to a whole-image scan;
+3. ownership: a ROI belongs to the band that holds its first row (ymin);
+4. halo: each rank needs the rows below its band up to the last row of its owned
+   ROIs; the rows are sent by the ranks that own them (send/recv of label and
+   intensity rows) -- only ROIs straddling a seam make a halo non-empty;
+5. each rank featurizes its owned ROIs on band + halo.  Non-mergeable statistics
+   (order statistics, the contour edge set) need no merge: the owner holds the
+   whole window.  Rows are therefore identical to a single-GPU featurize of the
+   whole image, for any number of bands.
+
+The device backend drives libfxg (fx_scan_accumulate, fx_label_table_copy,
+fx_featurize_owned); tests/test_shard.py drives the same plan with the C oracle
+on CPU ranks over gloo.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+NL = 65536
+SENT = 0xFFFFFFFF
+
+
+def band_plan(height: int, world: int):
+    """Equal row bands [y0, y1) per rank (the last absorbs the remainder)."""
+    base = height // world
+    return [(k * base, height if k == world - 1 else (k + 1) * base) for k in range(world)]
+
+
+def owned_need(cnt, bbox, y0, y1):
+    """Rows past y1 needed by the ROIs owned by band [y0, y1): max(ymax)+1 - y1, >= 0."""
+    ymin, ymax = bbox[1], bbox[3]
+    own = (cnt > 0) & (ymin >= y0) & (ymin < y1)
+    if not own.any():
+        return 0
+    return max(0, int(ymax[own].max()) + 1 - y1)
+
+
+def halo_transfers(bands, needs):
+    """(src, dst, row_lo, row_hi) for every halo slice: rank dst needs rows
+    [y1_dst, y1_dst + need_dst), held by the ranks whose bands intersect them."""
+    out = []
+    for dst, ((_, y1), need) in enumerate(zip(bands, needs)):
+        lo, hi = y1, y1 + int(need)
+        for src, (b0, b1) in enumerate(bands):
+            a, b = max(lo, b0), min(hi, b1)
+            if a < b:
+                out.append((src, dst, a, b))
+    return out
+
+
+def merge_tables(dist, cnt, bbox):
+    """All-reduce of the partial label tables (torch tensors, int64):
+    cnt [65536] SUM; bbox [4, 65536] = xmin, ymin (MIN), xmax, ymax (MAX)."""
+    dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
+    mins, maxs = bbox[:2].contiguous(), bbox[2:].contiguous()
+    dist.all_reduce(mins, op=dist.ReduceOp.MIN)
+    dist.all_reduce(maxs, op=dist.ReduceOp.MAX)
+    bbox[:2] = mins
+    bbox[2:] = maxs
+    return cnt, bbox
+
+
+def featurize_band(backend, dist, rank, world, band_intensity, band_labels, y0, height,
+                   width):
+    """Runs steps 1-5 for this rank.  band_* are [y1-y0, width] arrays/tensors of
+    the rank's own rows.  Returns (labels, values) of the ROIs this rank owns."""
+    import torch
+
+    bands = band_plan(height, world)
+    assert bands[rank][0] == y0
+    y1 = bands[rank][1]
+    # 1-2: scan + merge
+    cnt, bbox = backend.scan(band_intensity, band_labels, y0)
+    cnt, bbox = merge_tables(dist, cnt, bbox)
+    backend.set_table(cnt, bbox)
+    # 3-4: halo plan from the merged table (needs on the host: 1.5 MB)
+    hc, hb = cnt.cpu().numpy(), bbox.cpu().numpy()
+    need = owned_need(hc, hb, y0, y1)
+    needs_t = backend.tensor([need])
+    gathered = [backend.tensor([0]) for _ in range(world)]
+    dist.all_gather(gathered, needs_t)
+    needs = [int(t.item()) for t in gathered]
+    plan = halo_transfers(bands, needs)
+    ext_rows = (y1 - y0) + needs[rank]
+    ext_I = backend.empty_rows(ext_rows, width)
+    ext_L = backend.empty_rows(ext_rows, width)
+    ext_I[: y1 - y0] = band_intensity
+    ext_L[: y1 - y0] = band_labels
+    ops = []
+    for src, dst, a, b in plan:
+        if src == dst:
+            continue
+        if src == rank:  # send my rows [a, b)
+            ops.append(dist.P2POp(dist.isend, band_intensity[a - y0:b - y0].contiguous(), dst))
+            ops.append(dist.P2POp(dist.isend, band_labels[a - y0:b - y0].contiguous(), dst))
+        if dst == rank:
+            ops.append(dist.P2POp(dist.irecv, ext_I[a - y0:b - y0], src))
+            ops.append(dist.P2POp(dist.irecv, ext_L[a - y0:b - y0], src))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    # 5: featurize owned ROIs on band + halo
+    return backend.featurize_owned(ext_I, ext_L, y0, y0, y1)
+
+
+class DeviceBackend:
+    """libfxg on this rank's GPU; tensors are torch CUDA tensors (NCCL)."""
+
+    def __init__(self, ctx, groups, params):
+        import torch
+
+        from . import fxg
+        self.torch, self.fxg, self.ctx = torch, fxg, ctx
+        self.groups, self.params = groups, params
+        self.mask = groups if isinstance(groups, int) else fxg.resolve_groups(list(groups))
+        self.ncols = len(fxg.feature_columns(self.mask, params))
+
+    def tensor(self, values):
+        return self.torch.tensor(values, dtype=self.torch.int64, device="cuda")
+
+    def empty_rows(self, rows, width):
+        return self.torch.empty((rows, width), dtype=self.torch.int16, device="cuda")
+
+    def _image(self, I, L, oy):
+        h, w = L.shape
+        return self.fxg.FxImage(I.data_ptr(), L.data_ptr(), w, h, w, 0, oy, self.fxg.MEM_DEVICE)
+
+    def scan(self, I, L, oy):
+        import ctypes as C
+        lib = self.fxg.lib()
+        im = self._image(I, L, oy)
+        self.fxg._check(lib.fx_scan_accumulate(self.ctx.h, C.byref(im), 1))
+        cnt = self.torch.empty(NL, dtype=self.torch.int64, device="cuda")
+        bb = self.torch.empty((4, NL), dtype=self.torch.int32, device="cuda")
+        self.fxg._check(lib.fx_label_table_copy(self.ctx.h, C.c_void_p(cnt.data_ptr()),
+                                                C.c_void_p(bb.data_ptr()), 0, self.fxg.MEM_DEVICE))
+        return cnt, bb.to(self.torch.int64) & SENT
+
+    def set_table(self, cnt, bbox):
+        import ctypes as C
+        bb = bbox.to(self.torch.int32).contiguous()
+        cnt = cnt.contiguous()
+        self.fxg._check(self.fxg.lib().fx_label_table_copy(
+            self.ctx.h, C.c_void_p(cnt.data_ptr()), C.c_void_p(bb.data_ptr()), 1,
+            self.fxg.MEM_DEVICE))
+
+    def featurize_owned(self, I, L, oy, own_y0, own_y1):
+        import ctypes as C
+        cap = NL
+        out_l = self.torch.empty(cap, dtype=self.torch.int32, device="cuda")
+        out_v = self.torch.empty((cap, self.ncols), dtype=self.torch.float64, device="cuda")
+        im = self._image(I, L, oy)
+        n = C.c_size_t()
+        self.fxg._check(self.fxg.lib().fx_featurize_owned(
+            self.ctx.h, C.byref(im), own_y0, own_y1, C.c_uint(self.mask), C.byref(self.params),
+            C.c_void_p(out_l.data_ptr()), C.c_void_p(out_v.data_ptr()), C.c_size_t(cap),
+            C.byref(n)))
+        k = n.value
+        return out_l[:k], out_v[:k]
