@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libfxg.so")
+LIB_PATH = os.environ.get("FXG_LIB") or os.path.join(_HERE, "lib", "libfxg.so")
 
 FX_OK = 0
 ERRORS = {1: "ConfigError", 2: "UnknownProfile", 3: "PairingError", 4: "IoError",
