@@ -134,6 +134,18 @@ int fx_featurize(fx_ctx* ctx, const fx_image* image, unsigned groups,
                  const fx_texture_params* params, uint32_t* out_labels, double* out_values,
                  size_t cap_rois, size_t* n_rois);
 
+/* A batch of image pairs (the per-file loop of featurex::run, engine.cpp:300-336,
+ * and the C4 tile stacks): every image is featurized exactly as by fx_featurize,
+ * rows of image i are out_labels/out_values[row_offsets[i] .. row_offsets[i+1]).
+ * All images share one mem_kind; outputs live in that kind of memory.  Images
+ * are stacked in HBM and processed up to 128 per launch set (one label-table slot
+ * each); device images that are already stacked in one pitched allocation
+ * (heights multiple of 64, common pitch, contiguous) are read in place.  On
+ * FX_E_CAPACITY, row_offsets[n] holds a lower bound of the rows needed. */
+int fx_featurize_batch(fx_ctx* ctx, const fx_image* images, int n_images, unsigned groups,
+                       const fx_texture_params* params, uint32_t* out_labels, double* out_values,
+                       size_t cap_rois, size_t* row_offsets);
+
 /* Convenience form of fx_featurize with origin (0,0). */
 int fx_featurize_u16(fx_ctx* ctx, const uint16_t* intensity, const uint16_t* labels, int width,
                      int height, size_t pitch, int mem_kind, unsigned groups,

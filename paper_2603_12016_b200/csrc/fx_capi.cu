@@ -24,10 +24,10 @@
 #include "fxg.h"
 
 namespace fxg {
-__global__ void k_label_scan(const uint16_t* L, int W, int H, size_t pitch, int vec_ok,
-                             uint32_t ox, uint32_t oy, LabelTable t);
-__global__ void k_compact_count(LabelTable t, Control* ctl, CompactArgs a);
-__global__ void k_compact_emit(LabelTable t, Control* ctl, RoiList r, CompactArgs a);
+__global__ void k_label_scan(const uint16_t* L, int W, int H, size_t pitch, int vec_ok, SlotMap m,
+                             LabelTable t);
+__global__ void k_compact_count(LabelTable t, Control* ctl, CompactArgs a, int nslots);
+__global__ void k_compact_emit(LabelTable t, Control* ctl, RoiList r, CompactArgs a, SlotMap m);
 cudaError_t roi_s_setup(int* occ /* [3][2]: class x glcm */);
 void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
                   const CUtensorMap& tmap72, int tma40, int tma72, DevImage img, RoiList rl,
@@ -55,15 +55,34 @@ struct fx_ctx {
     int device = 0;
     int sm_count = 0;
     cudaStream_t own_stream = nullptr, stream = nullptr, side = nullptr;
+    cudaStream_t copy = nullptr;  // batch staging (H2D of the next sub-batch)
     cudaEvent_t ev_compact = nullptr, ev_stats = nullptr;
-    // label table + control
+    cudaEvent_t ev_staged[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+    // label table: tab_slots slices of 65536 entries, left reset by each compaction
+    int tab_slots = 0;
+    bool table_clean = false;  // every entry in the reset state
     unsigned long long* d_cnt = nullptr;
-    uint32_t* d_bb = nullptr;  // xmin | ymin | xmax | ymax, 65536 each
+    uint32_t* d_bb = nullptr;  // xmin | ymin | xmax | ymax, tab_slots*65536 each
+    uint32_t* d_maxlab = nullptr;
+    uint32_t* d_csum = nullptr;       // block_sum | block_base | live | slot_base | done
+    uint32_t* h_slot_base = nullptr;  // pinned [tab_slots+1]
     Control* d_ctl = nullptr;
     Control* h_ctl = nullptr;  // pinned
-    // ROI list
-    uint32_t* d_roi32 = nullptr;  // label,x0,y0,w,h + 4 class lists + overflow: 10 x 65536
+    // ROI list: roi_cap entries (tab_slots * 65536)
+    size_t roi_cap = 0;
+    uint32_t* d_roi32 = nullptr;  // label,gx,gy,x0,y0,w,h + 4 class lists + overflow
     unsigned long long* d_roin = nullptr;
+    // batch slot maps (double-buffered with pinned host mirrors)
+    SlotInfo* d_slots[2] = {nullptr, nullptr};
+    uint16_t* d_strips[2] = {nullptr, nullptr};
+    SlotInfo* h_slots[2] = {nullptr, nullptr};
+    uint16_t* h_strips[2] = {nullptr, nullptr};
+    size_t map_slots_cap = 0, map_strips_cap = 0;
+    // batch staging rasters (intensity then labels), double-buffered
+    uint16_t* d_stage[2] = {nullptr, nullptr};
+    size_t stage_elems = 0;  // per raster
+    uint32_t* d_blab = nullptr;  // batch output labels (host outputs)
+    size_t blab_cap = 0;
     // staging for host inputs / outputs
     uint16_t* d_img = nullptr;  // intensity then labels, pitched
     size_t img_pitch = 0, img_rows_cap = 0;
@@ -88,28 +107,94 @@ struct fx_ctx {
 
 namespace {
 
+constexpr int kRoiArrays = 8 + kNumClasses;  // u32 arrays of the ROI list
+
 RoiList roi_list(fx_ctx* c) {
     RoiList r;
     uint32_t* b = c->d_roi32;
+    const size_t N = c->roi_cap;
     r.label = b;
-    r.x0 = b + 1 * kMaxLabels;
-    r.y0 = b + 2 * kMaxLabels;
-    r.w = b + 3 * kMaxLabels;
-    r.h = b + 4 * kMaxLabels;
-    for (int k = 0; k < kNumClasses; ++k) r.cls_list[k] = b + (5 + k) * kMaxLabels;
-    r.overflow = b + (5 + kNumClasses) * kMaxLabels;
+    r.gx = reinterpret_cast<int32_t*>(b + 1 * N);
+    r.gy = reinterpret_cast<int32_t*>(b + 2 * N);
+    r.x0 = b + 3 * N;
+    r.y0 = b + 4 * N;
+    r.w = b + 5 * N;
+    r.h = b + 6 * N;
+    for (int k = 0; k < kNumClasses; ++k) r.cls_list[k] = b + (7 + k) * N;
+    r.overflow = b + (7 + kNumClasses) * N;
     r.n = c->d_roin;
     return r;
 }
 
 LabelTable label_table(fx_ctx* c) {
     LabelTable t;
+    const size_t N = (size_t)c->tab_slots * kMaxLabels;
     t.cnt = c->d_cnt;
     t.xmin = c->d_bb;
-    t.ymin = c->d_bb + kMaxLabels;
-    t.xmax = c->d_bb + 2 * kMaxLabels;
-    t.ymax = c->d_bb + 3 * kMaxLabels;
+    t.ymin = c->d_bb + N;
+    t.xmax = c->d_bb + 2 * N;
+    t.ymax = c->d_bb + 3 * N;
+    t.maxlab = c->d_maxlab;
     return t;
+}
+
+CompactArgs compact_args(fx_ctx* c, uint32_t own_y0, uint32_t own_y1) {
+    const size_t nb = (size_t)c->tab_slots * kBlocksPerSlot;
+    uint32_t* b = c->d_csum;
+    return CompactArgs{own_y0,     own_y1,     b, b + nb, b + 3 * nb, b + 2 * nb,
+                       b + 3 * nb + c->tab_slots + 1};
+}
+
+// memset the whole table to the reset state (cnt 0, min ~0, max 0, maxlab 0)
+int reset_table(fx_ctx* c) {
+    const size_t N = (size_t)c->tab_slots * kMaxLabels;
+    cudaStream_t s = c->stream;
+    CK(cudaMemsetAsync(c->d_cnt, 0, N * sizeof(unsigned long long), s));
+    CK(cudaMemsetAsync(c->d_bb, 0xff, 2 * N * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(c->d_bb + 2 * N, 0, 2 * N * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(c->d_maxlab, 0, (size_t)c->tab_slots * sizeof(uint32_t), s));
+    c->table_clean = true;
+    return FX_OK;
+}
+
+// table, compaction scratch and ROI list for `slots` images per launch
+int ensure_slots(fx_ctx* c, int slots) {
+    if (slots <= c->tab_slots) return FX_OK;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    cudaFree(c->d_cnt);
+    cudaFree(c->d_bb);
+    cudaFree(c->d_maxlab);
+    cudaFree(c->d_csum);
+    if (c->h_slot_base) cudaFreeHost(c->h_slot_base);
+    cudaFree(c->d_roi32);
+    cudaFree(c->d_roin);
+    c->d_cnt = nullptr;
+    c->d_bb = c->d_maxlab = c->d_csum = c->h_slot_base = c->d_roi32 = nullptr;
+    c->d_roin = nullptr;
+    c->tab_slots = 0;
+    c->roi_cap = 0;
+    const size_t N = (size_t)slots * kMaxLabels;
+    CK(cudaMalloc(&c->d_cnt, N * sizeof(unsigned long long)));
+    CK(cudaMalloc(&c->d_bb, 4 * N * sizeof(uint32_t)));
+    CK(cudaMalloc(&c->d_maxlab, (size_t)slots * sizeof(uint32_t)));
+    const size_t csum = 3 * (size_t)slots * kBlocksPerSlot + slots + 1 + 2;
+    CK(cudaMalloc(&c->d_csum, csum * sizeof(uint32_t)));
+    CK(cudaMemset(c->d_csum, 0, csum * sizeof(uint32_t)));
+    CK(cudaMallocHost(&c->h_slot_base, ((size_t)slots + 1) * sizeof(uint32_t)));
+    CK(cudaMalloc(&c->d_roi32, (size_t)kRoiArrays * N * sizeof(uint32_t)));
+    CK(cudaMalloc(&c->d_roin, N * sizeof(unsigned long long)));
+    c->tab_slots = slots;
+    c->roi_cap = N;
+    return reset_table(c);
+}
+
+SlotMap single_map(const DevImage& img) {
+    SlotMap m;
+    m.info = nullptr;
+    m.strip_slot = nullptr;
+    m.s0 = SlotInfo{0, img.w, img.h, img.ox, img.oy};
+    m.nslots = 1;
+    return m;
 }
 
 cudaEvent_t get_event(fx_ctx* c) {
@@ -284,49 +369,64 @@ struct DebugHost {
 
 // Label scan of one image (or band) into the ctx's label table, in global
 // coordinates (image origin added).  reset clears the table first.
-int scan_stage(fx_ctx* c, const DevImage& img, bool reset) {
+// reset: start from an empty table (a memset only when the last use left it dirty).
+int scan_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, bool reset) {
+    if (reset && !c->table_clean) {
+        int rc = reset_table(c);
+        if (rc) return rc;
+    }
     LabelTable t = label_table(c);
     cudaStream_t s = c->stream;
-    if (reset) {
-        CK(cudaMemsetAsync(c->d_cnt, 0, kMaxLabels * sizeof(unsigned long long), s));
-        CK(cudaMemsetAsync(c->d_bb, 0xff, 2 * kMaxLabels * sizeof(uint32_t), s));
-        CK(cudaMemsetAsync(c->d_bb + 2 * kMaxLabels, 0, 2 * kMaxLabels * sizeof(uint32_t), s));
-    }
     const int vec_ok = ((reinterpret_cast<uintptr_t>(img.L) & 15u) == 0) && (img.pitch % 8 == 0);
     const int tiles = ((img.w + 255) / 256) * ((img.h + 63) / 64);
     const int grid = std::max(1, std::min((tiles + 3) / 4, c->sm_count * 8));
     Launch l(c, "k_label_scan");
-    k_label_scan<<<grid, 128, 0, s>>>(img.L, img.w, img.h, img.pitch, vec_ok, (uint32_t)img.ox,
-                                      (uint32_t)img.oy, t);
+    k_label_scan<<<grid, 128, 0, s>>>(img.L, img.w, img.h, img.pitch, vec_ok, m, t);
+    CK(cudaGetLastError());
+    return FX_OK;
+}
+
+// compaction of the table (slots of m) into the ROI list; consumes the table
+int compact_stage(fx_ctx* c, const SlotMap& m, uint32_t own_y0, uint32_t own_y1) {
+    LabelTable t = label_table(c);
+    RoiList rl = roi_list(c);
+    const CompactArgs ca = compact_args(c, own_y0, own_y1);
+    cudaStream_t s = c->stream;
+    const int nb = m.nslots * kBlocksPerSlot;
+    const int grid = std::min(nb, 2 * c->sm_count);
+    CK(cudaMemsetAsync(c->d_ctl, 0, sizeof(Control), s));
+    {
+        Launch l(c, "k_compact_count");
+        k_compact_count<<<grid, 1024, m.nslots * sizeof(uint32_t), s>>>(t, c->d_ctl, ca, m.nslots);
+    }
+    {
+        Launch l(c, "k_compact_emit");
+        k_compact_emit<<<grid, 1024, 0, s>>>(t, c->d_ctl, rl, ca, m);
+    }
     CK(cudaGetLastError());
     return FX_OK;
 }
 
 // Compaction (owned rows [own_y0, own_y1)) + per-ROI kernels over the ctx's label
 // table, reading pixels of img.  out_dev: [cap_rois x ncols] device.
-int featurize_stage(fx_ctx* c, const DevImage& img, uint32_t own_y0, uint32_t own_y1,
-                    unsigned groups, const fx_texture_params& p, double* out_dev, size_t cap_rois,
-                    size_t* n_rois, const DebugOut* dbg_dev) {
+// With slot_base (host, [m.nslots+1]) the first output row of every slot is returned.
+int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t own_y0,
+                    uint32_t own_y1, unsigned groups, const fx_texture_params& p, double* out_dev,
+                    size_t cap_rois, size_t* n_rois, const DebugOut* dbg_dev,
+                    uint32_t* slot_base = nullptr) {
     const FeatCfg cfg = make_cfg(groups, p);
     const int vrc = validate_texture(groups, p);
-    LabelTable t = label_table(c);
     RoiList rl = roi_list(c);
     cudaStream_t s = c->stream;
-    CK(cudaMemsetAsync(c->d_ctl, 0, sizeof(Control), s));
-    const CompactArgs ca{(uint32_t)img.ox, (uint32_t)img.oy, own_y0, own_y1, (uint32_t)img.w,
-                         (uint32_t)img.h};
-    {
-        Launch l(c, "k_compact_count");
-        k_compact_count<<<64, 1024, 0, s>>>(t, c->d_ctl, ca);
-    }
-    {
-        Launch l(c, "k_compact_emit");
-        k_compact_emit<<<64, 1024, 0, s>>>(t, c->d_ctl, rl, ca);
-    }
-    CK(cudaGetLastError());
+    int rc0 = compact_stage(c, m, own_y0, own_y1);
+    if (rc0) return rc0;
     CK(cudaEventRecord(c->ev_compact, s));
     CK(cudaStreamWaitEvent(c->side, c->ev_compact, 0));
     CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, c->side));
+    if (slot_base)
+        CK(cudaMemcpyAsync(c->h_slot_base, compact_args(c, 0, 0).slot_base,
+                           ((size_t)m.nslots + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                           c->side));
     CK(cudaEventRecord(c->ev_stats, c->side));
 
     if (vrc != FX_OK) {  // texture parameters are only an error when a ROI exists
@@ -352,6 +452,7 @@ int featurize_stage(fx_ctx* c, const DevImage& img, uint32_t own_y0, uint32_t ow
     CK(cudaEventSynchronize(c->ev_stats));
     const Control hc = *c->h_ctl;
     *n_rois = hc.n_rois;
+    if (slot_base) std::memcpy(slot_base, c->h_slot_base, ((size_t)m.nslots + 1) * sizeof(uint32_t));
     if (hc.error & kErrWindow) {
         cudaStreamSynchronize(s);
         return set_error(FX_E_ARG, "an owned ROI window extends beyond the image (halo too small)");
@@ -382,9 +483,10 @@ int featurize_stage(fx_ctx* c, const DevImage& img, uint32_t own_y0, uint32_t ow
 
 int run_pipeline(fx_ctx* c, const DevImage& img, unsigned groups, const fx_texture_params& p,
                  double* out_dev, size_t cap_rois, size_t* n_rois, const DebugOut* dbg_dev) {
-    int rc = scan_stage(c, img, true);
+    const SlotMap m = single_map(img);
+    int rc = scan_stage(c, img, m, true);
     if (rc) return rc;
-    return featurize_stage(c, img, 0u, 0xffffffffu, groups, p, out_dev, cap_rois, n_rois, dbg_dev);
+    return featurize_stage(c, img, m, 0u, 0xffffffffu, groups, p, out_dev, cap_rois, n_rois, dbg_dev);
 }
 
 int finish(fx_ctx* c) {
@@ -442,6 +544,63 @@ int stage_image(fx_ctx* c, const fx_image* im, DevImage* d) {
     return FX_OK;
 }
 
+constexpr int kBatchSlots = 128;                 // images per launch set
+constexpr size_t kStageBudget = 64ull << 20;     // staged elements per raster per sub-batch
+
+int ensure_maps(fx_ctx* c, size_t slots, size_t strips) {
+    if (slots <= c->map_slots_cap && strips <= c->map_strips_cap) return FX_OK;
+    cudaStreamSynchronize(c->copy);
+    cudaStreamSynchronize(c->stream);
+    slots = std::max(slots, c->map_slots_cap);
+    strips = std::max(strips, c->map_strips_cap);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(c->d_slots[b]);
+        cudaFree(c->d_strips[b]);
+        if (c->h_slots[b]) cudaFreeHost(c->h_slots[b]);
+        if (c->h_strips[b]) cudaFreeHost(c->h_strips[b]);
+        c->d_slots[b] = nullptr;
+        c->d_strips[b] = nullptr;
+        c->h_slots[b] = nullptr;
+        c->h_strips[b] = nullptr;
+    }
+    c->map_slots_cap = c->map_strips_cap = 0;
+    for (int b = 0; b < 2; ++b) {
+        CK(cudaMalloc(&c->d_slots[b], slots * sizeof(SlotInfo)));
+        CK(cudaMalloc(&c->d_strips[b], strips * sizeof(uint16_t)));
+        CK(cudaMallocHost(&c->h_slots[b], slots * sizeof(SlotInfo)));
+        CK(cudaMallocHost(&c->h_strips[b], strips * sizeof(uint16_t)));
+    }
+    c->map_slots_cap = slots;
+    c->map_strips_cap = strips;
+    return FX_OK;
+}
+
+int ensure_stage(fx_ctx* c, size_t elems) {
+    if (elems <= c->stage_elems) return FX_OK;
+    cudaStreamSynchronize(c->copy);
+    cudaStreamSynchronize(c->stream);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(c->d_stage[b]);
+        c->d_stage[b] = nullptr;
+    }
+    c->stage_elems = 0;
+    elems = (elems + 63) / 64 * 64;
+    for (int b = 0; b < 2; ++b) CK(cudaMalloc(&c->d_stage[b], 2 * elems * sizeof(uint16_t)));
+    c->stage_elems = elems;
+    return FX_OK;
+}
+
+int ensure_blab(fx_ctx* c, size_t n) {
+    if (n <= c->blab_cap) return FX_OK;
+    cudaStreamSynchronize(c->stream);
+    cudaFree(c->d_blab);
+    c->d_blab = nullptr;
+    c->blab_cap = 0;
+    CK(cudaMalloc(&c->d_blab, n * sizeof(uint32_t)));
+    c->blab_cap = n;
+    return FX_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -480,13 +639,19 @@ int fx_ctx_create(int device, fx_ctx** out) {
     c->stream = c->own_stream;
     CKC(cudaEventCreateWithFlags(&c->ev_compact, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
-    CKC(cudaMalloc(&c->d_cnt, kMaxLabels * sizeof(unsigned long long)));
-    CKC(cudaMalloc(&c->d_bb, 4 * kMaxLabels * sizeof(uint32_t)));
+    CKC(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+        CKC(cudaEventCreateWithFlags(&c->ev_staged[b], cudaEventDisableTiming));
+        CKC(cudaEventCreateWithFlags(&c->ev_free[b], cudaEventDisableTiming));
+    }
     CKC(cudaMalloc(&c->d_ctl, sizeof(Control)));
     CKC(cudaMallocHost(&c->h_ctl, sizeof(Control)));
-    CKC(cudaMalloc(&c->d_roi32, (6 + kNumClasses) * kMaxLabels * sizeof(uint32_t)));
-    CKC(cudaMalloc(&c->d_roin, kMaxLabels * sizeof(unsigned long long)));
     CKC(cudaMalloc(&c->d_dbg, sizeof(DebugOut)));
+    {
+        int rc = ensure_slots(c, 1);
+        if (rc) return fail(rc);
+        CKC(cudaStreamSynchronize(c->stream));
+    }
     CKC(roi_s_setup(&c->occ_s[0][0]));
     for (auto& row : c->occ_s)
         for (int& o : row) o = std::max(1, o);
@@ -505,12 +670,26 @@ int fx_ctx_destroy(fx_ctx* c) {
     if (!c) return FX_OK;
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->copy) cudaStreamSynchronize(c->copy);
     cudaFree(c->d_cnt);
     cudaFree(c->d_bb);
+    cudaFree(c->d_maxlab);
+    cudaFree(c->d_csum);
+    if (c->h_slot_base) cudaFreeHost(c->h_slot_base);
     cudaFree(c->d_ctl);
     if (c->h_ctl) cudaFreeHost(c->h_ctl);
     cudaFree(c->d_roi32);
     cudaFree(c->d_roin);
+    for (int b = 0; b < 2; ++b) {
+        cudaFree(c->d_slots[b]);
+        cudaFree(c->d_strips[b]);
+        if (c->h_slots[b]) cudaFreeHost(c->h_slots[b]);
+        if (c->h_strips[b]) cudaFreeHost(c->h_strips[b]);
+        cudaFree(c->d_stage[b]);
+        if (c->ev_staged[b]) cudaEventDestroy(c->ev_staged[b]);
+        if (c->ev_free[b]) cudaEventDestroy(c->ev_free[b]);
+    }
+    cudaFree(c->d_blab);
     cudaFree(c->d_img);
     cudaFree(c->d_out);
     cudaFree(c->d_lscratch);
@@ -523,6 +702,7 @@ int fx_ctx_destroy(fx_ctx* c) {
     if (c->ev_compact) cudaEventDestroy(c->ev_compact);
     if (c->ev_stats) cudaEventDestroy(c->ev_stats);
     if (c->side) cudaStreamDestroy(c->side);
+    if (c->copy) cudaStreamDestroy(c->copy);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
     return FX_OK;
@@ -620,7 +800,7 @@ int fx_scan_accumulate(fx_ctx* c, const fx_image* im, int reset) {
     if (!lab_only.intensity) lab_only.intensity = lab_only.labels;  // scan reads labels only
     DevImage d;
     int rc = stage_image(c, &lab_only, &d);
-    if (!rc) rc = scan_stage(c, d, reset != 0);
+    if (!rc) rc = scan_stage(c, d, single_map(d), reset != 0);
     if (rc) return rc;
     CK(cudaStreamSynchronize(c->stream));
     return FX_OK;
@@ -633,13 +813,19 @@ int fx_label_table_copy(fx_ctx* c, uint64_t* cnt, uint32_t* bbox, int to_ctx, in
                                                                  : cudaMemcpyHostToDevice)
                                     : (mem_kind == FX_MEM_DEVICE ? cudaMemcpyDeviceToDevice
                                                                  : cudaMemcpyDeviceToHost);
-    const size_t bc = kMaxLabels * sizeof(unsigned long long), bb = 4 * kMaxLabels * sizeof(uint32_t);
+    // slot 0 of the ctx table; its bbox rows are tab_slots*65536 apart
+    const size_t bc = kMaxLabels * sizeof(unsigned long long), row = kMaxLabels * sizeof(uint32_t);
+    const size_t tab_pitch = (size_t)c->tab_slots * row;
     if (to_ctx) {
         CK(cudaMemcpyAsync(c->d_cnt, cnt, bc, k, c->stream));
-        CK(cudaMemcpyAsync(c->d_bb, bbox, bb, k, c->stream));
+        CK(cudaMemcpy2DAsync(c->d_bb, tab_pitch, bbox, row, row, 4, k, c->stream));
+        // the loaded table is consumed by the next compaction over all labels
+        const uint32_t full = kMaxLabels - 1;
+        CK(cudaMemcpyAsync(c->d_maxlab, &full, sizeof full, cudaMemcpyHostToDevice, c->stream));
+        c->table_clean = false;
     } else {
         CK(cudaMemcpyAsync(cnt, c->d_cnt, bc, k, c->stream));
-        CK(cudaMemcpyAsync(bbox, c->d_bb, bb, k, c->stream));
+        CK(cudaMemcpy2DAsync(bbox, row, c->d_bb, tab_pitch, row, 4, k, c->stream));
     }
     CK(cudaStreamSynchronize(c->stream));
     return FX_OK;
@@ -665,8 +851,8 @@ int fx_featurize_owned(fx_ctx* c, const fx_image* im, int own_y0, int own_y1, un
         if (rc) return rc;
         out_dev = c->d_out;
     }
-    rc = featurize_stage(c, d, (uint32_t)own_y0, (uint32_t)own_y1, groups, *p, out_dev, cap_rois,
-                         n_rois, nullptr);
+    rc = featurize_stage(c, d, single_map(d), (uint32_t)own_y0, (uint32_t)own_y1, groups, *p,
+                         out_dev, cap_rois, n_rois, nullptr);
     if (rc) {
         cudaStreamSynchronize(c->stream);
         return rc;
@@ -677,6 +863,179 @@ int fx_featurize_owned(fx_ctx* c, const fx_image* im, int own_y0, int own_y1, un
         if (im->mem_kind == FX_MEM_HOST)
             CK(cudaMemcpyAsync(out_values, out_dev, nr * cfg.ncols * sizeof(double), k, c->stream));
         CK(cudaMemcpyAsync(out_labels, roi_list(c).label, nr * sizeof(uint32_t), k, c->stream));
+    }
+    return finish(c);
+}
+
+// ---- batch of images (C4): stacked in HBM, one table slot per image -------------
+
+int fx_featurize_batch(fx_ctx* c, const fx_image* ims, int n, unsigned groups,
+                       const fx_texture_params* p, uint32_t* out_labels, double* out_values,
+                       size_t cap_rois, size_t* row_offsets) {
+    if (!c || (n && !ims) || !p || !row_offsets || n < 0) return set_error(FX_E_ARG, "null argument");
+    row_offsets[0] = 0;
+    if (n == 0) return FX_OK;
+    const int kind = ims[0].mem_kind;
+    int maxw = 0;
+    for (int i = 0; i < n; ++i) {
+        const fx_image& im = ims[i];
+        if (!im.intensity || !im.labels) return set_error(FX_E_ARG, "null raster in batch");
+        if (im.width < 1 || im.height < 1) return set_error(FX_E_PAIRING, "empty raster in batch");
+        if (im.pitch && im.pitch < (size_t)im.width) return set_error(FX_E_ARG, "pitch < width");
+        if (im.mem_kind != kind) return set_error(FX_E_ARG, "mixed host/device images in one batch");
+        maxw = std::max(maxw, im.width);
+        row_offsets[i + 1] = 0;
+    }
+    int rc = check_groups(groups);
+    if (rc) return rc;
+    CK(cudaSetDevice(c->device));
+    const FeatCfg cfg = make_cfg(groups, *p);
+    const size_t P = ((size_t)maxw + 63) / 64 * 64;  // staging pitch (elements)
+    auto pitch_of = [](const fx_image& im) { return im.pitch ? im.pitch : (size_t)im.width; };
+    // plan: sub-batches of <= kBatchSlots images within the staging budget
+    struct Sub {
+        int first, count;
+        size_t rows;  // stacked rows (each image padded to a multiple of 64)
+        bool zero_copy;
+    };
+    std::vector<Sub> plan;
+    for (int i = 0; i < n; ++i) {
+        const size_t r = ((size_t)ims[i].height + 63) / 64 * 64;
+        if (plan.empty() || plan.back().count == kBatchSlots ||
+            (plan.back().rows + r) * P > kStageBudget)
+            plan.push_back(Sub{i, 0, 0, false});
+        plan.back().count++;
+        plan.back().rows += r;
+    }
+    size_t max_rows = 0, max_strips = 0;
+    int max_count = 0;
+    bool need_stage = false;
+    for (Sub& b : plan) {
+        // device images already stacked in one pitched allocation are read in place
+        bool zc = kind == FX_MEM_DEVICE;
+        const size_t pt = pitch_of(ims[b.first]);
+        for (int j = b.first; zc && j < b.first + b.count; ++j) {
+            const fx_image& im = ims[j];
+            zc = pitch_of(im) == pt;
+            if (zc && j + 1 < b.first + b.count) {
+                const size_t step = pt * (size_t)im.height;
+                zc = im.height % 64 == 0 && ims[j + 1].labels == im.labels + step &&
+                     ims[j + 1].intensity == im.intensity + step;
+            }
+        }
+        b.zero_copy = zc;
+        if (zc) {
+            b.rows = 0;
+            for (int j = b.first; j < b.first + b.count; ++j) b.rows += (size_t)ims[j].height;
+        } else {
+            need_stage = true;
+            max_rows = std::max(max_rows, b.rows);
+        }
+        max_strips = std::max(max_strips, (b.rows + 63) / 64);
+        max_count = std::max(max_count, b.count);
+    }
+    rc = ensure_slots(c, max_count);
+    if (!rc) rc = ensure_maps(c, (size_t)max_count, max_strips);
+    if (!rc && need_stage) rc = ensure_stage(c, P * max_rows);
+    if (rc) return rc;
+    double* out_dev = out_values;
+    uint32_t* lab_dev = out_labels;
+    if (kind == FX_MEM_HOST) {
+        rc = ensure_out(c, std::max<size_t>(1, cap_rois) * (size_t)cfg.ncols);
+        if (!rc) rc = ensure_blab(c, std::max<size_t>(1, cap_rois));
+        if (rc) return rc;
+        out_dev = c->d_out;
+        lab_dev = c->d_blab;
+    }
+    // stage sub-batch k into buffer k%2 on the copy stream (slot map included)
+    auto stage = [&](int k) -> int {
+        const Sub& b = plan[k];
+        const int buf = k % 2;
+        CK(cudaStreamWaitEvent(c->copy, c->ev_free[buf], 0));
+        SlotInfo* hs = c->h_slots[buf];
+        uint16_t* hst = c->h_strips[buf];
+        size_t row0 = 0;
+        for (int j = 0; j < b.count; ++j) {
+            const fx_image& im = ims[b.first + j];
+            hs[j] = SlotInfo{(int32_t)row0, im.width, im.height, im.origin_x, im.origin_y};
+            const size_t r = b.zero_copy ? (size_t)im.height : ((size_t)im.height + 63) / 64 * 64;
+            for (size_t st = row0 / 64; st < (row0 + r + 63) / 64; ++st) hst[st] = (uint16_t)j;
+            if (!b.zero_copy) {
+                const cudaMemcpyKind mk =
+                    kind == FX_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+                const size_t sp = pitch_of(im) * 2;
+                uint16_t* dI = c->d_stage[buf] + row0 * P;
+                uint16_t* dL = c->d_stage[buf] + c->stage_elems + row0 * P;
+                CK(cudaMemcpy2DAsync(dI, P * 2, im.intensity, sp, (size_t)im.width * 2,
+                                     (size_t)im.height, mk, c->copy));
+                CK(cudaMemcpy2DAsync(dL, P * 2, im.labels, sp, (size_t)im.width * 2,
+                                     (size_t)im.height, mk, c->copy));
+            }
+            row0 += r;
+        }
+        CK(cudaMemcpyAsync(c->d_slots[buf], hs, (size_t)b.count * sizeof(SlotInfo),
+                           cudaMemcpyHostToDevice, c->copy));
+        CK(cudaMemcpyAsync(c->d_strips[buf], hst, ((b.rows + 63) / 64) * sizeof(uint16_t),
+                           cudaMemcpyHostToDevice, c->copy));
+        CK(cudaEventRecord(c->ev_staged[buf], c->copy));
+        return FX_OK;
+    };
+    size_t base = 0;
+    std::vector<uint32_t> sb((size_t)max_count + 1);
+    rc = stage(0);
+    for (size_t k = 0; !rc && k < plan.size(); ++k) {
+        if (k + 1 < plan.size()) rc = stage((int)k + 1);
+        if (rc) break;
+        const Sub& b = plan[k];
+        const int buf = (int)(k % 2);
+        CK(cudaStreamWaitEvent(c->stream, c->ev_staged[buf], 0));
+        DevImage d;
+        int wmax = 0;
+        for (int j = b.first; j < b.first + b.count; ++j) wmax = std::max(wmax, ims[j].width);
+        if (b.zero_copy) {
+            d.I = ims[b.first].intensity;
+            d.L = ims[b.first].labels;
+            d.pitch = pitch_of(ims[b.first]);
+        } else {
+            d.I = c->d_stage[buf];
+            d.L = c->d_stage[buf] + c->stage_elems;
+            d.pitch = P;
+        }
+        d.w = wmax;
+        d.h = (int)b.rows;
+        d.ox = d.oy = 0;
+        SlotMap m;
+        m.info = c->d_slots[buf];
+        m.strip_slot = c->d_strips[buf];
+        m.s0 = SlotInfo{0, 0, 0, 0, 0};
+        m.nslots = b.count;
+        size_t nr = 0;
+        rc = scan_stage(c, d, m, true);
+        if (!rc)
+            rc = featurize_stage(c, d, m, 0u, 0xffffffffu, groups, *p, out_dev + base * cfg.ncols,
+                                 cap_rois >= base ? cap_rois - base : 0, &nr, nullptr, sb.data());
+        if (rc) {
+            if (rc == FX_E_CAPACITY) row_offsets[n] = base + nr;  // rows needed so far
+            break;
+        }
+        for (int j = 0; j < b.count; ++j) row_offsets[b.first + j] = base + sb[j];
+        if (nr)
+            CK(cudaMemcpyAsync(lab_dev + base, roi_list(c).label, nr * sizeof(uint32_t),
+                               cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaEventRecord(c->ev_free[buf], c->stream));
+        base += nr;
+    }
+    if (rc) {
+        cudaStreamSynchronize(c->copy);
+        cudaStreamSynchronize(c->stream);
+        return rc;
+    }
+    row_offsets[n] = base;
+    if (kind == FX_MEM_HOST && base) {
+        CK(cudaMemcpyAsync(out_values, out_dev, base * cfg.ncols * sizeof(double),
+                           cudaMemcpyDeviceToHost, c->stream));
+        CK(cudaMemcpyAsync(out_labels, lab_dev, base * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                           c->stream));
     }
     return finish(c);
 }
@@ -733,40 +1092,31 @@ int fx_roi_table(fx_ctx* c, const fx_image* im, uint32_t* out_labels, uint64_t* 
     if (rc) return rc;
     RoiList rl = roi_list(c);
     cudaStream_t s = c->stream;
-    rc = scan_stage(c, d, true);
+    const SlotMap m = single_map(d);
+    rc = scan_stage(c, d, m, true);
+    if (!rc) rc = compact_stage(c, m, 0u, 0xffffffffu);
     if (rc) return rc;
-    LabelTable t = label_table(c);
-    CK(cudaMemsetAsync(c->d_ctl, 0, sizeof(Control), s));
-    const CompactArgs ca{(uint32_t)d.ox, (uint32_t)d.oy, 0u, 0xffffffffu, (uint32_t)d.w, (uint32_t)d.h};
-    {
-        Launch l(c, "k_compact_count");
-        k_compact_count<<<64, 1024, 0, s>>>(t, c->d_ctl, ca);
-    }
-    {
-        Launch l(c, "k_compact_emit");
-        k_compact_emit<<<64, 1024, 0, s>>>(t, c->d_ctl, rl, ca);
-    }
-    CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));
     const size_t nr = c->h_ctl->n_rois;
     *n_rois = nr;
     if (nr > cap) return set_error(FX_E_CAPACITY, "output capacity too small");
     if (!nr) return finish(c);
-    std::vector<uint32_t> x0(nr), y0(nr), w(nr), h(nr);
+    std::vector<int32_t> x0(nr), y0(nr);
+    std::vector<uint32_t> w(nr), h(nr);
     std::vector<unsigned long long> cnt(nr);
     CK(cudaMemcpy(out_labels, rl.label, nr * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(x0.data(), rl.x0, nr * 4, cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(y0.data(), rl.y0, nr * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(x0.data(), rl.gx, nr * 4, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(y0.data(), rl.gy, nr * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(w.data(), rl.w, nr * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(h.data(), rl.h, nr * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(cnt.data(), rl.n, nr * 8, cudaMemcpyDeviceToHost));
     for (size_t i = 0; i < nr; ++i) {
         out_count[i] = cnt[i];
-        out_bbox[4 * i + 0] = x0[i] + im->origin_x;
-        out_bbox[4 * i + 1] = y0[i] + im->origin_y;
-        out_bbox[4 * i + 2] = x0[i] + w[i] - 1 + im->origin_x;
-        out_bbox[4 * i + 3] = y0[i] + h[i] - 1 + im->origin_y;
+        out_bbox[4 * i + 0] = (uint32_t)x0[i];
+        out_bbox[4 * i + 1] = (uint32_t)y0[i];
+        out_bbox[4 * i + 2] = (uint32_t)x0[i] + w[i] - 1;
+        out_bbox[4 * i + 3] = (uint32_t)y0[i] + h[i] - 1;
     }
     return finish(c);
 }

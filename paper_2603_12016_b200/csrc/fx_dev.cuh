@@ -10,14 +10,30 @@ namespace fxg {
 constexpr int kMaxLabels = 65536;  // uint16 labels (reference image.hpp:24)
 constexpr unsigned kFull = 0xffffffffu;
 
-// Per-label accumulators of the label scan, direct-mapped by label value
-// (replaces RoiRegistry's std::map<label, Entry>, roi.cpp:76-110).
+// Per-label accumulators of the label scan, direct-mapped by (slot, label value)
+// (replaces RoiRegistry's std::map<label, Entry>, roi.cpp:76-110).  A slot is one
+// image of a batch; slot s owns entries [s*65536, (s+1)*65536).  Entries are left
+// in the reset state (cnt 0, min ~0, max 0) by the compaction that consumes them.
 struct LabelTable {
-    unsigned long long* cnt;  // [65536] pixel count
-    uint32_t* xmin;           // [65536] inclusive bbox, image-local
+    unsigned long long* cnt;  // [slots*65536] pixel count
+    uint32_t* xmin;           // inclusive bbox, global coordinates (origin added)
     uint32_t* ymin;
     uint32_t* xmax;
     uint32_t* ymax;
+    uint32_t* maxlab;         // [slots] largest label seen (bounds the compaction)
+};
+
+// One image of a batch, stacked row-wise in one pitched raster: image rows
+// [row0, row0+h) of the stack, columns [0, w); origin (ox, oy) is added to the
+// table coordinates.  row0 is a multiple of the scan strip height (64).
+struct SlotInfo {
+    int32_t row0, w, h, ox, oy;
+};
+struct SlotMap {
+    const SlotInfo* info;        // [nslots] device; null -> single image s0
+    const uint16_t* strip_slot;  // [stack rows / 64] slot of each 64-row strip
+    SlotInfo s0;
+    int nslots;
 };
 
 // ROI classes by window (bbox) size; each is consumed by its own persistent kernel.
@@ -48,25 +64,33 @@ struct Control {
     uint32_t l_max_wpr;       // max 64-bit words per row among L ROIs
     unsigned long long l_max_n;      // max pixel count among L ROIs
     unsigned long long l_max_cells;  // max window cells among L ROIs
-    uint32_t block_sum[64];   // compaction: present labels per 1024-label block
 };
+
+// compaction scratch: per (slot, 1024-label block) counts and exclusive bases
+constexpr int kBlocksPerSlot = kMaxLabels / 1024;
+constexpr uint32_t kBlockLive = 0x80000000u;  // block_sum flag: block <= maxlab
 
 constexpr uint32_t kErrCapacity = 1u;  // L slab too small for a ROI
 constexpr uint32_t kErrRuns = 2u;      // L run capacity exceeded
 constexpr uint32_t kErrWindow = 4u;    // an owned ROI window is not inside the image
 
-// compaction parameters: origin of the image being read (the label table holds
-// global coordinates) and the owned row range (band sharding; [0, ~0) = all)
+// compaction parameters: owned row range (band sharding; [0, ~0) = all), in
+// global coordinates, and the scratch arrays
 struct CompactArgs {
-    uint32_t ox, oy;
     uint32_t own_y0, own_y1;
-    uint32_t img_w, img_h;
+    uint32_t* block_sum;   // [nslots*64]
+    uint32_t* block_base;  // [nslots*64]
+    uint32_t* slot_base;   // [nslots+1] first output row of each slot, + total
+    uint32_t* live;        // [nslots*64] live pairs, ascending
+    uint32_t* done;        // [2]: blocks finished (last-block scan), live pair count
 };
 
 // Compacted ROI list: rank r == output row r (labels ascending).
 struct RoiList {
     uint32_t* label;
-    uint32_t* x0;
+    int32_t* gx;  // global coordinates of the window origin (table xmin, ymin)
+    int32_t* gy;
+    uint32_t* x0;  // window origin in the (stacked) raster being read
     uint32_t* y0;
     uint32_t* w;
     uint32_t* h;

@@ -307,7 +307,7 @@ __device__ __forceinline__ void process_roi(const Job& J, Slab& S, const DevImag
     __syncwarp();
 
     const double dn = (double)n;
-    const long long gx0 = (long long)img.ox + J.x0, gy0 = (long long)img.oy + J.y0;
+    const long long gx0 = rl.gx[rank], gy0 = rl.gy[rank];
     uint16_t vmin = 0, vmax = 0;
     bool have_minmax = false;
 

@@ -591,7 +591,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     const uint16_t* stage = (const uint16_t*)(base + L.stage);
     double* orow = out + (size_t)J.row * cfg.ncols;
     const bool dbg_on = dbg != nullptr && dbg->label == label;
-    const long long gx0 = (long long)img.ox + J.x0, gy0 = (long long)img.oy + J.y0;
+    const long long gx0 = rl.gx[J.row], gy0 = rl.gy[J.row];
     const uint32_t xo = J.x0 & 7u;
     const uint64_t wm = (w >= 64) ? ~0ull : ((1ull << w) - 1ull);
 

@@ -61,17 +61,18 @@ __device__ __forceinline__ void cache_put(CacheEnt& c0, CacheEnt& c1, const Labe
 }
 
 // several distinct labels inside one 8-px chunk: per pixel
-__device__ __noinline__ void chunk_slow(uint4 v, uint32_t x, uint32_t y, CacheEnt& c0, CacheEnt& c1,
-                                        const LabelTable& t) {
+__device__ __noinline__ void chunk_slow(uint4 v, uint32_t x, uint32_t y, uint32_t sb,
+                                        CacheEnt& c0, CacheEnt& c1, const LabelTable& t) {
     const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
     for (int k = 0; k < 8; ++k) {
         const uint32_t l = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu;
-        if (l) cache_put(c0, c1, t, l, 1u, x + k, x + k, y);
+        if (l) cache_put(c0, c1, t, sb | l, 1u, x + k, x + k, y);
     }
 }
 
-__device__ __forceinline__ void chunk(uint4 v, uint32_t x, uint32_t y, CacheEnt& c0, CacheEnt& c1,
-                                      const LabelTable& t) {
+// sb = slot << 16: cache keys and table indices are slot * 65536 + label
+__device__ __forceinline__ void chunk(uint4 v, uint32_t x, uint32_t y, uint32_t sb, CacheEnt& c0,
+                                      CacheEnt& c1, const LabelTable& t) {
     if ((v.x | v.y | v.z | v.w) == 0u) return;
     // nonzero halfwords and the largest label in the chunk (SIMD-in-word)
     const uint32_t n0 = __vcmpne2(v.x, 0u), n1 = __vcmpne2(v.y, 0u), n2 = __vcmpne2(v.z, 0u),
@@ -83,18 +84,18 @@ __device__ __forceinline__ void chunk(uint4 v, uint32_t x, uint32_t y, CacheEnt&
     const uint32_t bad = (n0 & ~__vcmpeq2(v.x, LL)) | (n1 & ~__vcmpeq2(v.y, LL)) |
                          (n2 & ~__vcmpeq2(v.z, LL)) | (n3 & ~__vcmpeq2(v.w, LL));
     if (bad) {
-        chunk_slow(v, x, y, c0, c1, t);
+        chunk_slow(v, x, y, sb, c0, c1, t);
         return;
     }
     const uint32_t m8 = (n0 & 1u) | ((n0 >> 15) & 2u) | ((n1 & 1u) << 2) | ((n1 >> 13) & 8u) |
                         ((n2 & 1u) << 4) | ((n2 >> 11) & 32u) | ((n3 & 1u) << 6) |
                         ((n3 >> 9) & 128u);
-    cache_put(c0, c1, t, L, __popc(m8), x + __ffs(m8) - 1, x + 31 - __clz(m8), y);
+    cache_put(c0, c1, t, sb | L, __popc(m8), x + __ffs(m8) - 1, x + 31 - __clz(m8), y);
 }
 
 __device__ __forceinline__ uint4 load_chunk(const uint16_t* __restrict__ L, size_t pitch, int W,
                                             int H, int x, int y, bool vec) {
-    if (y >= H || x >= W) return make_uint4(0, 0, 0, 0);
+    if (y >= H || x >= W) return make_uint4(0, 0, 0, 0);  // H: end row of the slot
     const uint16_t* p = L + (size_t)y * pitch + x;
     if (vec && x + 8 <= W) return __ldg(reinterpret_cast<const uint4*>(p));
     uint32_t wv[4] = {0, 0, 0, 0};
@@ -125,53 +126,131 @@ __device__ __forceinline__ void warp_flush(const CacheEnt& e, const LabelTable& 
 }  // namespace
 
 __global__ void __launch_bounds__(kScanThreads)
-    k_label_scan(const uint16_t* __restrict__ L, int W, int H, size_t pitch, int vec_ok,
-                 uint32_t ox, uint32_t oy, LabelTable t) {
+    k_label_scan(const uint16_t* __restrict__ L, int W, int H, size_t pitch, int vec_ok, SlotMap m,
+                 LabelTable t) {
     const unsigned lane = lane_id();
     const int warps_total = gridDim.x * (kScanThreads / 32);
     const int gw = blockIdx.x * (kScanThreads / 32) + (threadIdx.x >> 5);
     const int tiles_x = (W + 255) / 256;
     const int n_tiles = tiles_x * ((H + kStripRows - 1) / kStripRows);
     for (int tile = gw; tile < n_tiles; tile += warps_total) {
+        const int strip = tile / tiles_x;
+        const uint32_t slot = m.strip_slot ? m.strip_slot[strip] : 0u;
+        const SlotInfo si = m.info ? m.info[slot] : m.s0;
+        const int sw = si.w, send = si.row0 + si.h;  // slot bounds in the stack
+        const uint32_t sb = slot << 16;
+        const uint32_t gxo = (uint32_t)si.ox, gyo = (uint32_t)(si.oy - si.row0);
         const int x = (tile % tiles_x) * 256 + (int)lane * 8;
-        const int y0 = (tile / tiles_x) * kStripRows;
+        const int y0 = strip * kStripRows;
         CacheEnt c0{0, 0, 0, 0, 0, 0}, c1{0, 0, 0, 0, 0, 0};
         // software pipeline: batch r0 + kBatch is in flight while batch r0 is folded
         uint4 v[kBatch], nx[kBatch];
 #pragma unroll
-        for (int r = 0; r < kBatch; ++r) v[r] = load_chunk(L, pitch, W, H, x, y0 + r, vec_ok);
+        for (int r = 0; r < kBatch; ++r) v[r] = load_chunk(L, pitch, sw, send, x, y0 + r, vec_ok);
 #pragma unroll 1
         for (int r0 = 0; r0 < kStripRows; r0 += kBatch) {
             if (r0 + kBatch < kStripRows) {
 #pragma unroll
                 for (int r = 0; r < kBatch; ++r)
-                    nx[r] = load_chunk(L, pitch, W, H, x, y0 + r0 + kBatch + r, vec_ok);
+                    nx[r] = load_chunk(L, pitch, sw, send, x, y0 + r0 + kBatch + r, vec_ok);
             }
 #pragma unroll
             for (int r = 0; r < kBatch; ++r)
-                chunk(v[r], (uint32_t)x + ox, (uint32_t)(y0 + r0 + r) + oy, c0, c1, t);
+                chunk(v[r], (uint32_t)x + gxo, (uint32_t)(y0 + r0 + r) + gyo, sb, c0, c1, t);
 #pragma unroll
             for (int r = 0; r < kBatch; ++r) v[r] = nx[r];
         }
         warp_flush(c0, t);
         warp_flush(c1, t);
+        const uint32_t mx = warp_max(max(c0.label & 0xffffu, c1.label & 0xffffu));
+        if (lane == 0 && mx) atomicMax(&t.maxlab[slot], mx);
     }
 }
 
 // --- compaction -------------------------------------------------------------
+//
+// Work unit: a "pair" = (slot, 1024-label block); pairs above the slot's max
+// label are dead (no table reads).  k_compact_count (persistent, grid-stride over
+// pairs) counts present + owned labels per live pair; the last block to finish
+// turns the counts into output rows (slot-major, labels ascending = the order of
+// running the images one by one), lists the live pairs and clears maxlab.
+// k_compact_emit walks the live pairs only, writes the ROI list and resets every
+// table entry it consumed, so the next scan starts from a clean table without a
+// memset.
 
 // a label is emitted when present and owned (its first row in [own_y0, own_y1))
-__device__ __forceinline__ bool owned(const LabelTable& t, uint32_t l, const CompactArgs& a) {
-    if (l == 0 || t.cnt[l] == 0ull) return false;
-    const uint32_t y = t.ymin[l];
+__device__ __forceinline__ bool owned(const LabelTable& t, uint32_t key, const CompactArgs& a) {
+    if ((key & 0xffffu) == 0 || t.cnt[key] == 0ull) return false;
+    const uint32_t y = t.ymin[key];
     return y >= a.own_y0 && y < a.own_y1;
 }
 
-__global__ void __launch_bounds__(1024) k_compact_count(LabelTable t, Control* ctl, CompactArgs a) {
-    const uint32_t l = blockIdx.x * 1024 + threadIdx.x;
-    const int present = owned(t, l, a);
-    const int c = __syncthreads_count(present);
-    if (threadIdx.x == 0) ctl->block_sum[blockIdx.x] = (uint32_t)c;
+__global__ void __launch_bounds__(1024) k_compact_count(LabelTable t, Control* ctl, CompactArgs a,
+                                                        int nslots) {
+    extern __shared__ uint32_t s_max[];  // [nslots]
+    __shared__ uint32_t wt_n[32], wt_l[32];
+    __shared__ uint32_t carry_n, carry_l;
+    __shared__ int is_last;
+    const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = (int)tid; i < nslots; i += 1024) s_max[i] = t.maxlab[i];
+    __syncthreads();
+    const int nb = nslots * kBlocksPerSlot;
+    for (int pair = blockIdx.x; pair < nb; pair += gridDim.x) {
+        const uint32_t slot = pair / kBlocksPerSlot, blk = pair % kBlocksPerSlot;
+        if (blk * 1024u > s_max[slot]) {  // uniform per block
+            if (tid == 0) a.block_sum[pair] = 0u;
+            continue;
+        }
+        const uint32_t key = slot * (uint32_t)kMaxLabels + blk * 1024u + tid;
+        const int c = __syncthreads_count(owned(t, key, a));
+        if (tid == 0) a.block_sum[pair] = (uint32_t)c | kBlockLive;
+    }
+    // last block: exclusive scans of the counts and of the live flags
+    __threadfence();
+    __syncthreads();
+    if (tid == 0) is_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    if (tid == 0) carry_n = carry_l = 0;
+    __syncthreads();
+    for (int b0 = 0; b0 < nb; b0 += 1024) {
+        const int b = b0 + (int)tid;
+        const uint32_t raw = b < nb ? __ldcg(&a.block_sum[b]) : 0u;
+        const uint32_t v = raw & ~kBlockLive, f = raw >> 31;
+        const uint32_t in_n = warp_incl_scan(v), in_l = warp_incl_scan(f);
+        if (lane == 31) {
+            wt_n[warp] = in_n;
+            wt_l[warp] = in_l;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t x = wt_n[lane], y = wt_l[lane];
+            wt_n[lane] = warp_incl_scan(x) - x;
+            wt_l[lane] = warp_incl_scan(y) - y;
+        }
+        __syncthreads();
+        const uint32_t ex_n = carry_n + wt_n[warp] + in_n - v;
+        const uint32_t ex_l = carry_l + wt_l[warp] + in_l - f;
+        if (b < nb) {
+            a.block_base[b] = ex_n;
+            if (f) a.live[ex_l] = (uint32_t)b;
+            if (b % kBlocksPerSlot == 0) a.slot_base[b / kBlocksPerSlot] = ex_n;
+        }
+        __syncthreads();
+        if (tid == 1023) {
+            carry_n = ex_n + v;
+            carry_l = ex_l + f;
+        }
+        __syncthreads();
+    }
+    if (tid == 0) {
+        ctl->n_rois = carry_n;
+        a.slot_base[nslots] = carry_n;
+        a.done[1] = carry_l;  // live pair count
+        a.done[0] = 0u;       // ready for the next compaction
+    }
+    for (int i = (int)tid; i < nslots; i += 1024) t.maxlab[i] = 0u;
 }
 
 // class of a window (w x h) with n pixels
@@ -182,60 +261,67 @@ __device__ __forceinline__ int roi_class(uint32_t w, uint32_t h, unsigned long l
 }
 
 __global__ void __launch_bounds__(1024) k_compact_emit(LabelTable t, Control* ctl, RoiList r,
-                                                       CompactArgs a) {
+                                                       CompactArgs a, SlotMap m) {
     __shared__ uint32_t warp_cnt[32];
-    __shared__ uint32_t block_base;
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (warp == 0) {
-        const uint32_t s0 = (lane < blockIdx.x) ? ctl->block_sum[lane] : 0;
-        const uint32_t s1 = (lane + 32 < blockIdx.x) ? ctl->block_sum[lane + 32] : 0;
-        const uint32_t sum = warp_sum(s0 + s1);
-        if (lane == 0) block_base = sum;
-        if (blockIdx.x == gridDim.x - 1) {
-            uint32_t tot = warp_sum((lane < gridDim.x ? ctl->block_sum[lane] : 0u) +
-                                    (lane + 32 < gridDim.x ? ctl->block_sum[lane + 32] : 0u));
-            if (lane == 0) ctl->n_rois = tot;
+    const uint32_t n_live = a.done[1];
+    for (uint32_t i = blockIdx.x; i < n_live; i += gridDim.x) {
+        const uint32_t pair = a.live[i];
+        const uint32_t slot = pair / kBlocksPerSlot, blk = pair % kBlocksPerSlot;
+        const uint32_t l = blk * 1024u + tid;
+        const uint32_t key = slot * (uint32_t)kMaxLabels + l;
+        const unsigned long long n = t.cnt[key];
+        const bool present = owned(t, key, a);
+        const unsigned msk = __ballot_sync(kFull, present);
+        if (lane == 0) warp_cnt[warp] = __popc(msk);
+        __syncthreads();
+        if (warp == 0) {
+            const uint32_t c = warp_cnt[lane];
+            warp_cnt[lane] = warp_incl_scan(c) - c;
         }
-    }
-    const uint32_t l = blockIdx.x * 1024 + tid;
-    const bool present = owned(t, l, a);
-    const unsigned long long n = present ? t.cnt[l] : 0ull;
-    const unsigned m = __ballot_sync(kFull, present);
-    if (lane == 0) warp_cnt[warp] = __popc(m);
-    __syncthreads();
-    if (warp == 0) {
-        uint32_t c = warp_cnt[lane];
-        uint32_t incl = warp_incl_scan(c);
-        warp_cnt[lane] = incl - c;
-    }
-    __syncthreads();
-    if (!present) return;
-    const uint32_t rank = block_base + warp_cnt[warp] + __popc(m & lanemask_lt());
-    // table holds global coordinates; windows are local to the image being read
-    const uint32_t x0 = t.xmin[l] - a.ox, y0 = t.ymin[l] - a.oy;
-    const uint32_t w = t.xmax[l] - t.xmin[l] + 1, h = t.ymax[l] - t.ymin[l] + 1;
-    if (t.xmin[l] < a.ox || t.ymin[l] < a.oy || x0 + w > a.img_w || y0 + h > a.img_h)
-        atomicOr(&ctl->error, kErrWindow);  // window not inside the image (halo too small)
-    r.label[rank] = l;
-    r.x0[rank] = x0;
-    r.y0[rank] = y0;
-    r.w[rank] = w;
-    r.h[rank] = h;
-    r.n[rank] = n;
-    const int c = roi_class(w, h, n);
-    // one atomic per (warp, class): the class lists are consumed in any order
-    const unsigned peers = __match_any_sync(__activemask(), c);
-    const int leader = __ffs(peers) - 1;
-    uint32_t base = 0;
-    if ((int)lane == leader) base = atomicAdd(&ctl->class_count[c], (uint32_t)__popc(peers));
-    base = __shfl_sync(peers, base, leader);
-    const uint32_t pos = base + __popc(peers & lanemask_lt());
-    r.cls_list[c][pos] = rank;
-    if (c == kClassL) {
-        atomicMax(&ctl->l_max_h, h);
-        atomicMax(&ctl->l_max_wpr, (w + 63) / 64);
-        atomicMax(&ctl->l_max_n, n);
-        atomicMax(&ctl->l_max_cells, (unsigned long long)w * h);
+        __syncthreads();
+        const uint32_t wbase = warp_cnt[warp];
+        __syncthreads();  // warp_cnt is rewritten by the next pair
+        if (n == 0ull) continue;
+        const uint32_t gx0 = t.xmin[key], gy0 = t.ymin[key], gx1 = t.xmax[key], gy1 = t.ymax[key];
+        // consume: reset the entry for the next scan
+        t.cnt[key] = 0ull;
+        t.xmin[key] = 0xffffffffu;
+        t.ymin[key] = 0xffffffffu;
+        t.xmax[key] = 0u;
+        t.ymax[key] = 0u;
+        if (!present) continue;
+        const uint32_t rank = a.block_base[pair] + wbase + __popc(msk & lanemask_lt());
+        // table holds global coordinates; windows are local to the (stacked) raster read
+        const SlotInfo si = m.info ? m.info[slot] : m.s0;
+        const uint32_t x0 = gx0 - (uint32_t)si.ox, ly0 = gy0 - (uint32_t)si.oy;
+        const uint32_t w = gx1 - gx0 + 1, h = gy1 - gy0 + 1;
+        if (gx0 < (uint32_t)si.ox || gy0 < (uint32_t)si.oy || x0 + w > (uint32_t)si.w ||
+            ly0 + h > (uint32_t)si.h)
+            atomicOr(&ctl->error, kErrWindow);  // window not inside the image (halo too small)
+        r.label[rank] = l;
+        r.gx[rank] = (int32_t)gx0;
+        r.gy[rank] = (int32_t)gy0;
+        r.x0[rank] = x0;
+        r.y0[rank] = ly0 + (uint32_t)si.row0;
+        r.w[rank] = w;
+        r.h[rank] = h;
+        r.n[rank] = n;
+        const int c = roi_class(w, h, n);
+        // one atomic per (warp, class): the class lists are consumed in any order
+        const unsigned peers = __match_any_sync(__activemask(), c);
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if ((int)lane == leader) base = atomicAdd(&ctl->class_count[c], (uint32_t)__popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        const uint32_t pos = base + __popc(peers & lanemask_lt());
+        r.cls_list[c][pos] = rank;
+        if (c == kClassL) {
+            atomicMax(&ctl->l_max_h, h);
+            atomicMax(&ctl->l_max_wpr, (w + 63) / 64);
+            atomicMax(&ctl->l_max_n, n);
+            atomicMax(&ctl->l_max_cells, (unsigned long long)w * h);
+        }
     }
 }
 

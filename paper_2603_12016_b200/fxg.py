@@ -205,6 +205,56 @@ class Context:
                                   C.c_size_t(cap_rois), C.byref(n)))
         return n.value
 
+    def featurize_batch(self, pairs, groups=("intensity",), params=None, origins=None,
+                        cap_rois=None):
+        """Host list of (intensity, labels) pairs -> list of (labels, table) per image,
+        each identical to featurize() on that pair (fx_featurize_batch)."""
+        params = params or resolve_profile("default")
+        mask = groups if isinstance(groups, int) else resolve_groups(list(groups))
+        ncols = len(feature_columns(mask, params))
+        keep, ims = [], (FxImage * max(1, len(pairs)))()
+        cap = 0
+        for i, (I, L) in enumerate(pairs):
+            I = np.ascontiguousarray(I, dtype=np.uint16)
+            L = np.ascontiguousarray(L, dtype=np.uint16)
+            if I.shape != L.shape:
+                raise FxError(3, "image/mask dimension mismatch")
+            keep.append((I, L))
+            h, w = L.shape
+            ox, oy = origins[i] if origins is not None else (0, 0)
+            ims[i] = FxImage(I.ctypes.data, L.ctypes.data, w, h, w, int(ox), int(oy), MEM_HOST)
+            if cap_rois is None:
+                cap += int(np.count_nonzero(np.bincount(L.ravel(), minlength=65536)[1:]))
+        cap = cap if cap_rois is None else cap_rois
+        offs = self.featurize_batch_raw(ims, len(pairs), mask, params, None, None, cap,
+                                        ncols=ncols)
+        out_l, out_v, offs = offs
+        return [(out_l[offs[i]:offs[i + 1]], out_v[offs[i]:offs[i + 1], :ncols])
+                for i in range(len(pairs))]
+
+    def featurize_batch_raw(self, images, n, groups, params, out_labels_ptr, out_values_ptr,
+                            cap_rois, ncols=None):
+        """images: ctypes FxImage array.  With out_*_ptr None, host numpy outputs are
+        allocated and (labels, values, row_offsets) returned; otherwise the row
+        offsets only (outputs already written through the pointers)."""
+        mask = groups if isinstance(groups, int) else resolve_groups(list(groups))
+        offs = np.zeros(n + 1, np.uint64)
+        if out_labels_ptr is None:
+            ncols = ncols if ncols is not None else len(feature_columns(mask, params))
+            out_l = np.zeros(max(cap_rois, 1), np.uint32)
+            out_v = np.zeros((max(cap_rois, 1), max(ncols, 1)), np.float64)
+            lp, vp = _p(out_l, C.c_uint32), _p(out_v, C.c_double)
+        else:
+            lp, vp = C.c_void_p(out_labels_ptr), C.c_void_p(out_values_ptr)
+        _check(lib().fx_featurize_batch(self.h, images, C.c_int(n), C.c_uint(mask),
+                                        C.byref(params), lp, vp, C.c_size_t(cap_rois),
+                                        _p(offs, C.c_size_t)))
+        offs = offs.astype(np.int64)
+        if out_labels_ptr is None:
+            k = int(offs[n])
+            return out_l[:k], out_v[:k], offs
+        return offs
+
     def roi_features(self, xs, ys, vs, groups=("intensity",), params=None):
         """compute_roi_features on one cloud (engine.hpp:68-70)."""
         xs = np.ascontiguousarray(xs, np.uint32)

@@ -1,0 +1,149 @@
+"""Batch path (C4: many image pairs per call, fx_featurize_batch).
+
+Every image of a batch must give exactly the rows fx_featurize gives for it alone
+(bit-exact), whatever the batch composition: mixed sizes, heights that are not a
+multiple of the 64-row scan strip, origins, empty images, more images than one
+launch set holds (128 slots), host or device rasters, stacked device tensors read
+in place.  The single-image rows are themselves pinned to the oracle by
+test_gpu_parity.py; one case here also checks a batch against the oracle directly.
+"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+import pytest
+
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+import inputs  # noqa: E402
+from parity import assert_parity  # noqa: E402
+
+GROUPS = ["intensity", "moments", "glcm"]
+
+
+def _pairs(specs, seed=0):
+    out = []
+    for k, (h, w, n) in enumerate(specs):
+        L = inputs.random_blobs((h, w), n, seed=seed + k, max_r=min(h, w) // 4 + 1) if n else \
+            np.zeros((h, w), np.uint16)
+        I = inputs.uniform((h, w), seed + 100 + k)
+        out.append((I, L))
+    return out
+
+
+def _check_same(ctx, pairs, res, params, origins=None):
+    assert len(res) == len(pairs)
+    for k, ((I, L), (bl, bv)) in enumerate(zip(pairs, res)):
+        o = origins[k] if origins is not None else (0, 0)
+        sl, sv = ctx.featurize(I, L, GROUPS, params, origin=o)
+        assert np.array_equal(bl, sl), k
+        assert np.array_equal(bv, sv), k
+
+
+@pytest.mark.gpu
+def test_batch_mixed_sizes_bitwise(ctx):
+    import paper_2603_12016_b200 as fx
+    p = fx.resolve_profile("default")
+    specs = [(100, 90, 12), (64, 64, 5), (1, 1, 0), (37, 200, 9), (130, 61, 15), (10, 10, 0),
+             (256, 256, 40), (65, 300, 20)]
+    pairs = _pairs(specs, seed=11)
+    pairs[2] = (np.array([[7]], np.uint16), np.array([[3]], np.uint16))  # one-pixel image
+    # labels spread over many 1024-label compaction blocks, up to 65535
+    pairs[4] = (pairs[4][0], inputs.random_blobs((130, 61), 15, seed=4, max_r=12,
+                                                 label_values=[1500, 40000, 65535, 2049, 1024]))
+    origins = [(k * 13, 1000 + k * 7) for k in range(len(pairs))]
+    res = ctx.featurize_batch(pairs, GROUPS, p, origins=origins)
+    _check_same(ctx, pairs, res, p, origins)
+
+
+@pytest.mark.gpu
+def test_batch_vs_oracle(ctx, oracle):
+    import paper_2603_12016_b200 as fx
+    from oracle import make_params
+    p = make_params("default")
+    cols = fx.feature_columns(GROUPS, fx.resolve_profile("default"))
+    pairs = _pairs([(120, 140, 10), (77, 50, 6), (200, 64, 14)], seed=5)
+    res = ctx.featurize_batch(pairs, GROUPS, fx.resolve_profile("default"))
+    for (I, L), (bl, bv) in zip(pairs, res):
+        ol, ov = oracle.featurize(I, L, GROUPS, p)
+        assert_parity(cols, bl, bv, ol, ov, I, L)
+
+
+@pytest.mark.gpu
+def test_batch_more_than_one_launch_set(ctx):
+    """300 images > 128 slots: three sub-batches, staged double-buffered."""
+    import paper_2603_12016_b200 as fx
+    p = fx.resolve_profile("performance")
+    specs = [(48 + (k % 5) * 16, 40 + (k % 7) * 8, 1 + k % 6) for k in range(300)]
+    pairs = _pairs(specs, seed=21)
+    res = ctx.featurize_batch(pairs, GROUPS, p)
+    _check_same(ctx, pairs, res, p)
+    # the context stays usable for single calls afterwards (table left clean)
+    I, L = pairs[7]
+    sl, sv = ctx.featurize(I, L, GROUPS, p)
+    assert np.array_equal(res[7][0], sl) and np.array_equal(res[7][1], sv)
+
+
+@pytest.mark.gpu
+def test_batch_all_empty_and_empty_list(ctx):
+    import paper_2603_12016_b200 as fx
+    p = fx.resolve_profile("default")
+    assert ctx.featurize_batch([], GROUPS, p) == []
+    pairs = _pairs([(50, 50, 0), (20, 70, 0)])
+    res = ctx.featurize_batch(pairs, GROUPS, p)
+    assert [len(r[0]) for r in res] == [0, 0]
+
+
+@pytest.mark.gpu
+def test_batch_capacity_error(ctx):
+    import paper_2603_12016_b200 as fx
+    p = fx.resolve_profile("default")
+    pairs = _pairs([(100, 100, 10), (100, 100, 10)], seed=3)
+    with pytest.raises(fx.FxError) as e:
+        ctx.featurize_batch(pairs, GROUPS, p, cap_rois=5)
+    assert e.value.code == 10
+    res = ctx.featurize_batch(pairs, GROUPS, p)  # recovers
+    _check_same(ctx, pairs, res, p)
+
+
+def _device_batch(ctx, tI, tL, views, p, mask, ncols, cap):
+    import torch
+    from paper_2603_12016_b200 import fxg
+    ims = (fxg.FxImage * len(views))()
+    for k, (vi, vl) in enumerate(views):
+        h, w = vl.shape
+        ims[k] = fxg.FxImage(vi.data_ptr(), vl.data_ptr(), w, h, vl.stride(0), 0, 0,
+                             fxg.MEM_DEVICE)
+    out_l = torch.zeros(cap, dtype=torch.int32, device="cuda")
+    out_v = torch.zeros((cap, ncols), dtype=torch.float64, device="cuda")
+    offs = ctx.featurize_batch_raw(ims, len(views), mask, p, out_l.data_ptr(), out_v.data_ptr(),
+                                   cap)
+    torch.cuda.synchronize()
+    return out_l.cpu().numpy().view(np.uint32), out_v.cpu().numpy(), offs
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("stacked", [True, False])
+def test_batch_device_rasters(ctx, stacked):
+    """[T, 192, 160] device stack read in place (stacked) or separate tensors (staged)."""
+    import torch
+    import paper_2603_12016_b200 as fx
+    p = fx.resolve_profile("default")
+    mask = fx.resolve_groups(GROUPS)
+    ncols = len(fx.feature_columns(mask, p))
+    T, H, W = 9, 192, 160
+    pairs = _pairs([(H, W, 8 + k) for k in range(T)], seed=31)
+    if stacked:
+        tI = torch.from_numpy(np.stack([a for a, _ in pairs]).view(np.int16)).cuda()
+        tL = torch.from_numpy(np.stack([b for _, b in pairs]).view(np.int16)).cuda()
+        views = [(tI[k], tL[k]) for k in range(T)]
+    else:
+        views = [(torch.from_numpy(a.view(np.int16)).cuda(), torch.from_numpy(b.view(np.int16)).cuda())
+                 for a, b in pairs]
+        tI = tL = None
+    cap = 4096
+    bl, bv, offs = _device_batch(ctx, tI, tL, views, p, mask, ncols, cap)
+    for k, (I, L) in enumerate(pairs):
+        sl, sv = ctx.featurize(I, L, GROUPS, p)
+        assert np.array_equal(bl[offs[k]:offs[k + 1]], sl), k
+        assert np.array_equal(bv[offs[k]:offs[k + 1]], sv), k
