@@ -8,7 +8,7 @@ OBJ      := $(PKG)/build
 LIBDIR   := $(PKG)/lib
 LIB      := $(LIBDIR)/libfxg.so
 NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -I$(SRC) \
-            --expt-relaxed-constexpr -Xptxas -warn-spills
+            --expt-relaxed-constexpr -Xptxas -warn-spills $(FXG_DEFS)
 CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude -I$(SRC) -I/usr/local/cuda/include
 
 CU_SRCS  := $(SRC)/fx_scan.cu $(SRC)/fx_roi.cu $(SRC)/fx_roi_s.cu $(SRC)/fx_capi.cu

@@ -195,6 +195,13 @@ int fx_debug_roi(fx_ctx* ctx, const fx_image* image, uint32_t label,
                  const fx_texture_params* params, uint64_t* hist, int32_t* edge_xy,
                  size_t cap_edge, size_t* n_edge, uint32_t* glcm_counts, uint64_t* glcm_pairs);
 
+/* Per-phase clock totals of the S-class ROI kernels (summed over ROIs, lane 0's
+ * clock64 deltas): 0 load+gather, 1 intensity sort, 2 intensity statistics,
+ * 3 edge set + edge statistics, 4 moments, 5 GLCM levels+pair keys, 6 GLCM key
+ * sort, 7 GLCM run-length counts, 8 Haralick.  Only in builds with
+ * -DFXG_PHASE_TIMING (tools/); others return FX_E_CONFIG. */
+int fx_debug_phase_clocks(unsigned long long* out, int n, int reset);
+
 /* ---- synthetic inputs (the reference's synth.hpp generators) --------------- */
 
 /* blob_mask_grid (synth.hpp:22-26): disk-with-ears blobs on a grid, labels

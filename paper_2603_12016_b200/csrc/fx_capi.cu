@@ -28,7 +28,7 @@ __global__ void k_label_scan(const uint16_t* L, int W, int H, size_t pitch, int 
                              LabelTable t);
 __global__ void k_compact_count(LabelTable t, Control* ctl, CompactArgs a, int nslots);
 __global__ void k_compact_emit(LabelTable t, Control* ctl, RoiList r, CompactArgs a, SlotMap m);
-cudaError_t roi_s_setup(int* occ /* [3][2]: class x glcm */);
+cudaError_t roi_s_setup(int* occ /* [3][3]: class x GlcmMode */);
 void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
                   const CUtensorMap& tmap72, int tma40, int tma72, DevImage img, RoiList rl,
                   Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg);
@@ -100,7 +100,7 @@ struct fx_ctx {
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> ev_pool;
     PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
-    int occ_s[3][2] = {{1, 1}, {1, 1}, {1, 1}};
+    int occ_s[3][3] = {{1, 1, 1}, {1, 1, 1}, {1, 1, 1}};
     bool sync_debug = false;
     bool no_tma = false;
 };
@@ -439,7 +439,7 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
     std::memset(&tmap72, 0, sizeof tmap72);
     const int tma40 = (!c->no_tma && make_tmap(c, img, &tmap40, kStageW0)) ? 1 : 0;
     const int tma72 = (!c->no_tma && make_tmap(c, img, &tmap72, kStageW)) ? 1 : 0;
-    const int glcm = (groups & FX_GROUP_GLCM) ? 1 : 0;
+    const int glcm = s_glcm_mode(cfg);
     {
         static const char* names[3] = {"k_roi_s0", "k_roi_s1", "k_roi_s2"};
         for (int cls = kClassS0; cls <= kClassS2; ++cls) {

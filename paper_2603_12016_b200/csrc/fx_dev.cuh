@@ -118,6 +118,14 @@ struct FeatCfg {
     int dx[8], dy[8];                // angle_offset (texture.cpp:15-23)
 };
 
+// GLCM variants of the S kernels: none, key sort (ng > 64), shared histogram
+// (ng <= 64: keys la*64+lb < 4096, packed u16 counts)
+enum GlcmMode { kGlNone = 0, kGlSort = 1, kGlHist = 2 };
+constexpr int kGlHistMaxNg = 64;
+__host__ __device__ inline int s_glcm_mode(const FeatCfg& c) {
+    return c.col_glcm < 0 ? kGlNone : (c.ng <= kGlHistMaxNg ? kGlHist : kGlSort);
+}
+
 __device__ __forceinline__ unsigned lane_id() {
     unsigned r;
     asm volatile("mov.u32 %0, %%laneid;" : "=r"(r));

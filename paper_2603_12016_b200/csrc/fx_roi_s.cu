@@ -22,6 +22,22 @@
 
 #include "fx_roi.cuh"
 
+// Optional per-phase clock accounting (build with -DFXG_PHASE_TIMING; read with
+// fx_debug_phase_clocks).  Off in the product build.
+#ifdef FXG_PHASE_TIMING
+__device__ unsigned long long g_phase_clk[16];
+#define PT_DECL long long pt_t_ = clock64();
+#define PT(k)                                                                              \
+    do {                                                                                   \
+        const long long t_ = clock64();                                                    \
+        if (lane_id() == 0) atomicAdd(&g_phase_clk[k], (unsigned long long)(t_ - pt_t_)); \
+        pt_t_ = t_;                                                                        \
+    } while (0)
+#else
+#define PT_DECL
+#define PT(k)
+#endif
+
 namespace fxg {
 
 namespace {
@@ -32,12 +48,14 @@ struct SLayout {
     uint32_t stage;                            // B: load
     uint32_t tmp, sorted, cnt;                 // B: sort / stats
     uint32_t kmask, emask, runoff, rs, re, parent, rsize;  // B: edge slow path
-    uint32_t lvl, keys, keys2, gcnt, marg;     // B: glcm
+    uint32_t lvl, keys, keys2, gcnt, marg;     // B: glcm, sort path (ng > 64)
+    uint32_t lmap, hist, list;                 // B: glcm, histogram path (ng <= 64)
     uint32_t bytes;
 };
 
+
 __host__ __device__ constexpr SLayout make_slayout(uint32_t TW, uint32_t TH, uint32_t NMAX,
-                                                   uint32_t RUNMAX, bool glcm) {
+                                                   uint32_t RUNMAX, int glcm) {
     SLayout L{};
     uint32_t o = 0;
     L.rowmask = o;
@@ -68,7 +86,17 @@ __host__ __device__ constexpr SLayout make_slayout(uint32_t TW, uint32_t TH, uin
     L.keys2 = al(L.keys + NMAX * 2, 16);
     L.gcnt = al(L.keys2 + NMAX * 2, 16);
     L.marg = L.gcnt + 512 * 4;
-    const uint32_t e_glcm = glcm ? L.marg + 1280 * 4 : B;
+    uint32_t e_glcm = B;
+    if (glcm == kGlSort) e_glcm = L.marg + 1280 * 4;
+    if (glcm == kGlHist) {  // level raster [TH][64] u8, histogram 4096 x u16, marginals
+        L.lmap = B;
+        L.hist = al(L.lmap + TH * 64, 16);
+        L.marg = L.hist + 4096 * 2;
+        // keys of the non-empty cells (<= pairs <= NMAX, u16): overlays vals (region
+        // A), dead once the level raster is built
+        L.list = L.vals;
+        e_glcm = L.marg + 321 * 4;
+    }
     L.bytes = al(mx(mx(e_load, e_sort), mx(e_edge, e_glcm)), 128) + 128;  // + mbarrier
     return L;
 }
@@ -88,7 +116,7 @@ template <>
 struct SVar<kClassS2> {
     static constexpr int TW = kStageW, TH = kSH, NMAX = kS2N, RUNMAX = 1024;
 };
-template <int CLS, bool GLCM>
+template <int CLS, int GLCM>
 constexpr SLayout slayout() {
     return make_slayout(SVar<CLS>::TW, SVar<CLS>::TH, SVar<CLS>::NMAX, SVar<CLS>::RUNMAX, GLCM);
 }
@@ -333,9 +361,17 @@ __device__ double g_log2_tab[kLog2Tab + 1];
 __device__ __forceinline__ double log2_int(uint32_t c) {
     return c <= (uint32_t)kLog2Tab ? __ldg(&g_log2_tab[c]) : nlog2((double)c);
 }
+// 1/(1+d^2), 1/(1+d), 1/d^2 for grey-level differences d < 64 (Haralick weights)
+__device__ double g_rcp_tab[3][64];
 __global__ void k_init_log2_tab() {
     for (int i = threadIdx.x + blockIdx.x * blockDim.x; i <= kLog2Tab; i += blockDim.x * gridDim.x)
         g_log2_tab[i] = i ? log2((double)i) : 0.0;
+    for (int d = threadIdx.x + blockIdx.x * blockDim.x; d < 64; d += blockDim.x * gridDim.x) {
+        const double dd = (double)d;
+        g_rcp_tab[0][d] = 1.0 / (1.0 + dd * dd);
+        g_rcp_tab[1][d] = 1.0 / (1.0 + dd);
+        g_rcp_tab[2][d] = d ? 1.0 / (dd * dd) : 0.0;
+    }
 }
 
 // k-th smallest (0-based) of |2 s[i] - M2| over sorted s by the whole warp:
@@ -388,6 +424,216 @@ __device__ __noinline__ uint32_t kth_dev2_warp(const uint16_t* s, uint32_t n, ui
 }
 
 
+// GLCM group for an S window with ng <= 64 (kGlHist): discretize (texture.cpp:45-53,
+// exact integer floor) into a level raster, count pair keys per sorted angle
+// (texture.cpp:58-80) in a packed-u16 shared histogram (key = la*64 + lb, or the
+// canonical min/max key when symmetric), then one pass over the non-empty cells:
+// ASM, autocorrelation and max probability from exact integer sums, entropy from
+// one fp64 sum of c*log2(c), marginals by shared atomics; Haralick statistics
+// from the integer marginals (texture.cpp:87-217; hxy1 == hxy2 == hx + hy).
+__device__ __noinline__ void glcm_phase_h(uint32_t n, int h, const uint64_t* rowmask,
+                                          const uint16_t* xy, const uint16_t* vals,
+                                          uint8_t* lmap, uint32_t* hist, uint32_t* marg,
+                                          uint16_t* list,
+                                          uint32_t vmin, uint32_t vmax, const FeatCfg& cfg,
+                                          double* og, const DebugOut* dbg) {
+    const unsigned lane = lane_id();
+    const int ng = cfg.ng, A = cfg.n_angles;
+    const uint32_t span = vmax - vmin + 1u;
+    const uint32_t mdiv = 0xffffffffu / span;
+    PT_DECL
+    for (uint32_t i = lane; i < n; i += 32) {
+        uint32_t lv = 0;
+        if (vmax > vmin) {  // floor(ng * (v - vmin) / span) by multiply-high + one fix-up
+            const uint32_t num = (uint32_t)ng * (vals[i] - vmin);
+            uint32_t q = __umulhi(num, mdiv);
+            if (num - q * span >= span) ++q;
+            lv = min((uint32_t)(ng - 1), q);
+        }
+        const uint32_t p = xy[i];
+        lmap[(p >> 8) * 64 + (p & 0xffu)] = (uint8_t)lv;
+    }
+    uint4* h4 = reinterpret_cast<uint4*>(hist);
+    const int nq = ng * 8;  // uint4 words covering keys < ng * 64
+    for (int j = lane; j < nq; j += 32) h4[j] = make_uint4(0u, 0u, 0u, 0u);
+    __syncwarp();
+    const bool sym = cfg.symmetric != 0;
+    uint32_t* px = marg;
+    uint32_t* py = sym ? marg : marg + 64;  // symmetric: p_y == p_x
+    uint32_t* psum = marg + 128;            // [2ng-1]
+    uint32_t* pdif = marg + 256;            // [ng]
+    double sacc = 0;
+    for (int a = 0; a < A; ++a) {
+        const int ddx = cfg.dx[a], ddy = cfg.dy[a];
+        for (int k = lane; k < 321; k += 32) marg[k] = 0u;  // + marg[320]: list length
+        // pairs, pixel-parallel: (x, y) and (x + dx, y + dy) both in the ROI; the
+        // first pair of a cell appends its key to the cell list (warp-aggregated)
+        uint32_t npr = 0;
+        for (uint32_t b = 0; b < n; b += 32) {
+            const uint32_t i = b + lane;
+            bool pair = false, fresh = false;
+            uint32_t key = 0;
+            if (i < n) {
+                const uint32_t p = xy[i];
+                const int x = (int)(p & 0xffu), y = (int)(p >> 8);
+                const int nx = x + ddx, ny = y + ddy;
+                pair = ny >= 0 && ny < h && nx >= 0 && nx < 64 && ((rowmask[ny] >> nx) & 1ull);
+                if (pair) {
+                    const uint32_t la = lmap[y * 64 + x], lb = lmap[ny * 64 + nx];
+                    key = sym ? min(la, lb) * 64u + max(la, lb) : la * 64u + lb;
+                    const uint32_t sh = (key & 1u) * 16u;
+                    const uint32_t old = atomicAdd(&hist[key >> 1], 1u << sh);
+                    fresh = ((old >> sh) & 0xffffu) == 0u;
+                }
+            }
+            npr += pair;
+            const unsigned fm = __ballot_sync(kFull, fresh);
+            if (fm) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(&marg[320], (uint32_t)__popc(fm));
+                base = __shfl_sync(kFull, base, 0);
+                if (fresh) list[base + __popc(fm & lanemask_lt())] = (uint16_t)key;
+            }
+        }
+        __syncwarp();
+        const uint32_t np = warp_sum(npr);
+        __syncwarp();
+        PT(5);
+        if (dbg && dbg->pairs && lane == 0) dbg->pairs[a] = np;
+        double st[29];
+#pragma unroll
+        for (int k = 0; k < 29; ++k) st[k] = 0;
+        if (np > 0) {
+            const uint32_t Ti = sym ? 2u * np : np;
+            const double T = (double)Ti, iT = 1.0 / T, logT = log2_int(Ti);
+            const uint32_t nc = marg[320];  // non-empty cells, keys in list (any order)
+            unsigned long long s2 = 0, sa = 0;
+            uint32_t jm = 0;
+            double el = 0;
+            for (uint32_t i = lane; i < nc; i += 32) {
+                const uint32_t key = list[i];
+                const uint32_t c = (hist[key >> 1] >> ((key & 1u) * 16u)) & 0xffffu;
+                const uint32_t ga = key >> 6, gb = key & 63u;
+                const bool off = sym && ga != gb;
+                const uint32_t cc = (sym && !off) ? 2u * c : c;
+                const uint32_t mcc = off ? 2u * cc : cc;  // mass of the cell(s)
+                s2 += (unsigned long long)mcc * cc;
+                sa += (unsigned long long)((ga + 1) * (gb + 1)) * mcc;
+                jm = max(jm, cc);
+                el += (double)mcc * (logT - log2_int(cc));  // exactly 0 for a single cell
+                atomicAdd(&px[ga], cc);
+                if (off) atomicAdd(&px[gb], cc);
+                if (!sym) atomicAdd(&py[gb], cc);
+                atomicAdd(&psum[ga + gb], mcc);
+                atomicAdd(&pdif[ga > gb ? ga - gb : gb - ga], mcc);
+                if (dbg && dbg->glcm) {
+                    dbg->glcm[((size_t)a * ng + ga) * ng + gb] = cc;
+                    if (off) dbg->glcm[((size_t)a * ng + gb) * ng + ga] = cc;
+                }
+            }
+            __syncwarp();
+            for (uint32_t i = lane; i < nc; i += 32) hist[list[i] >> 1] = 0u;  // empty again
+            s2 = warp_sum(s2);
+            sa = warp_sum(sa);
+            jm = warp_max(jm);
+            el = warp_sum(el);
+            __syncwarp();
+            PT(7);
+            const double asm2 = (double)s2 / (T * T), acor_ = (double)sa * iT;
+            const double ent_ = el * iT, jmax = (double)jm * iT;
+            // marginals -> means, entropies (p log p from integer counts)
+            double r8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // mux, muy, sumave, sument, difave, hx, hy
+            for (int g = lane; g < ng; g += 32) {  // symmetric: p_y == p_x
+                const uint32_t ma = px[g];
+                const double pa = (double)ma * iT;
+                r8[0] += (g + 1) * pa;
+                if (ma) r8[5] -= pa * (log2_int(ma) - logT);
+                if (!sym) {
+                    const uint32_t mb = py[g];
+                    const double pb = (double)mb * iT;
+                    r8[1] += (g + 1) * pb;
+                    if (mb) r8[6] -= pb * (log2_int(mb) - logT);
+                }
+            }
+            for (int k = lane; k < 2 * ng - 1; k += 32) {
+                const uint32_t m = psum[k];
+                if (m) {
+                    const double p = (double)m * iT;
+                    r8[2] += (k + 2) * p;
+                    r8[3] -= p * (log2_int(m) - logT);
+                }
+            }
+            for (int d = lane; d < ng; d += 32) {
+                const uint32_t m = pdif[d];
+                if (m) r8[4] += d * ((double)m * iT);
+            }
+            warp_sum8(r8);
+            const double mux = r8[0], muy = sym ? r8[0] : r8[1], sumave = r8[2], sument = r8[3];
+            const double difave = r8[4], hx = r8[5], hy = sym ? r8[5] : r8[6];
+            double s8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // vx, vy, sumvar, clut, clus, clup, difent
+            for (int g = lane; g < ng; g += 32) {
+                const double a1 = (double)px[g] * iT;
+                s8[0] += (g + 1 - mux) * (g + 1 - mux) * a1;
+                if (!sym) {
+                    const double b1 = (double)py[g] * iT;
+                    s8[1] += (g + 1 - muy) * (g + 1 - muy) * b1;
+                }
+            }
+            for (int k = lane; k < 2 * ng - 1; k += 32) {
+                const uint32_t m = psum[k];
+                if (m) {
+                    const double p = (double)m * iT;
+                    s8[2] += (k + 2 - sumave) * (k + 2 - sumave) * p;
+                    const double sv = k + 2 - mux - muy;
+                    s8[3] += sv * sv * p;
+                    s8[4] += sv * sv * sv * p;
+                    s8[5] += sv * sv * sv * sv * p;
+                }
+            }
+            double d8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // difent, contrast, idm, id, idn, idmn, iv, difvar
+            const double dng = (double)ng;
+            for (int d = lane; d < ng; d += 32) {
+                const uint32_t m = pdif[d];
+                if (m) {
+                    const double p = (double)m * iT, dd = (double)d;
+                    d8[0] -= p * (log2_int(m) - logT);
+                    d8[1] += dd * dd * p;
+                    d8[2] += p * __ldg(&g_rcp_tab[0][d]);  // 1 / (1 + d^2)
+                    d8[3] += p * __ldg(&g_rcp_tab[1][d]);  // 1 / (1 + d)
+                    d8[4] += p * dng / (dng + dd);
+                    d8[5] += p * (dng * dng) / (dng * dng + dd * dd);
+                    if (d > 0) d8[6] += p * __ldg(&g_rcp_tab[2][d]);  // 1 / d^2
+                    d8[7] += (dd - difave) * (dd - difave) * p;
+                }
+            }
+            warp_sum8(s8);
+            warp_sum8(d8);
+            const double vx = s8[0], vy = sym ? s8[0] : s8[1];
+            const double corr = (vx > 0 && vy > 0) ? (acor_ - mux * muy) / sqrt(vx * vy) : 0.0;
+            const double hxy = hx + hy, hmax = fmax(hx, hy);
+            const double v29[29] = {asm2, acor_, s8[5], s8[4], s8[3], d8[1], corr, difave, d8[0],
+                                    d8[7], difave, sqrt(asm2), ent_, d8[3], d8[2], d8[3], d8[4],
+                                    d8[2], d8[5], hmax > 0 ? (ent_ - hxy) / hmax : 0.0,
+                                    sqrt(fmax(0.0, 1.0 - exp(-2.0 * (hxy - ent_)))), d8[6], mux,
+                                    ent_, jmax, vx, sumave, sument, s8[2]};
+#pragma unroll
+            for (int k = 0; k < 29; ++k) st[k] = v29[k];
+            PT(8);
+        }
+        double mine = 0;
+#pragma unroll
+        for (int k = 0; k < 29; ++k)
+            if ((int)lane == k) mine = st[k];
+        if (lane < 29) {
+            og[lane * (A + 1) + a] = mine;
+            sacc += mine;
+        }
+        __syncwarp();
+    }
+    if (lane < 29) og[lane * (A + 1) + A] = sacc / (double)A;
+    __syncwarp();
+}
+
 // GLCM group for an S window (ng <= 256): discretize (texture.cpp:45-53, exact
 // integer floor), pair keys per sorted angle (texture.cpp:58-80), radix sort,
 // run-length counts, Haralick statistics from integer marginals
@@ -401,6 +647,7 @@ __device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64
     const unsigned lane = lane_id();
     const int ng = cfg.ng, A = cfg.n_angles;
     const uint32_t span = vmax - vmin + 1u;
+    PT_DECL
     for (uint32_t i = lane; i < n; i += 32) {
         uint32_t lv = 0;
         if (vmax > vmin) lv = min((uint32_t)(ng - 1), ((uint32_t)ng * (vals[i] - vmin)) / span);
@@ -443,6 +690,7 @@ __device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64
         }
         for (int k = lane; k < 1280; k += 32) marg[k] = 0;
         __syncwarp();
+        PT(5);
         double st[29];
 #pragma unroll
         for (int k = 0; k < 29; ++k) st[k] = 0;
@@ -450,6 +698,7 @@ __device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64
         if (np > 0) {
             const uint16_t* sk = radix_sort16(keys, keys2, keys, np, gcnt);
             __syncwarp();
+            PT(6);
             const double T = sym ? 2.0 * (double)np : (double)np;
             const double logT = nlog2(T);
             double asm_ = 0, ent = 0, acor = 0, jmax = 0;
@@ -490,6 +739,7 @@ __device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64
                 if (sb) carry = b0 + 31 - __clz(sb);
             }
             __syncwarp();
+            PT(7);
             double r8[8] = {asm_, ent, acor, 0, 0, 0, 0, 0};
             jmax = warp_max(jmax);
             // marginals px, py -> means (texture.cpp:127-131)
@@ -559,6 +809,7 @@ __device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64
                                     ent_, jmax, vx, sumave, sument, s8[4]};
 #pragma unroll
             for (int k = 0; k < 29; ++k) st[k] = v29[k];
+            PT(8);
         }
         double mine = 0;
 #pragma unroll
@@ -575,7 +826,7 @@ __device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64
 }
 
 // ------------------------------------------------------------------------
-template <int TW, int TH, int NMAX, int RUNMAX, bool GLCM>
+template <int TW, int TH, int NMAX, int RUNMAX, int GLCM>
 __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8_t* base,
                                           const DevImage& img, const FeatCfg& cfg,
                                           double* __restrict__ out, uint64_t* mbar,
@@ -596,6 +847,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     const uint64_t wm = (w >= 64) ? ~0ull : ((1ull << w) - 1ull);
 
     // ---------------------------------------------------------------- load
+    PT_DECL
     mbar_wait(mbar, phase);
     phase ^= 1u;
     // row masks: lane y reads its staged row 8 labels at a time (16 B LDS)
@@ -698,11 +950,13 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     bool have_minmax = false;
 
     // ----------------------------------------------------------- intensity
+    PT(0);
     if (cfg.col_int >= 0) {
         const uint16_t* s = radix_sort16(vals, (uint16_t*)(base + L.tmp),
                                          (uint16_t*)(base + L.sorted), n,
                                          (uint32_t*)(base + L.cnt));
         __syncwarp();
+        PT(1);
         vmin = s[0];
         vmax = s[n - 1];
         have_minmax = true;
@@ -845,6 +1099,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
                     (double)((long long)rcl - (long long)(rn - rcl)) * rmean) / (double)rn;
         }
         // ------------------------------------------------ edge set
+        PT(2);
         double e_mean = 0, e_min = 0, e_max = 0, e_std = 0, e_int = 0;
         {
             uint64_t* km = (uint64_t*)(base + L.kmask);
@@ -1044,6 +1299,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     }
 
     // ------------------------------------------------------------- moments
+    PT(3);
     if (cfg.col_mom >= 0) {
         const long long nn = (long long)n, W = (long long)sS;
         const long long axb = (2 * (long long)sLX + nn) / (2 * nn);
@@ -1194,6 +1450,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     }
 
     // ---------------------------------------------------------------- glcm
+    PT(4);
     if (GLCM && cfg.col_glcm >= 0) {
         if (!have_minmax) {
             uint32_t lo = 0xffffu, hi = 0;
@@ -1204,10 +1461,16 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
             vmin = warp_min(lo);
             vmax = warp_max(hi);
         }
-        glcm_phase_s(n, h, w, rowmask, rowoff, vals, (uint8_t*)(base + L.lvl),
-                     (uint16_t*)(base + L.keys), (uint16_t*)(base + L.keys2),
-                     (uint32_t*)(base + L.gcnt), (uint32_t*)(base + L.marg), vmin, vmax, cfg,
-                     orow + cfg.col_glcm, dbg_on ? dbg : nullptr);
+        if constexpr (GLCM == kGlHist)
+            glcm_phase_h(n, h, rowmask, xy, vals, base + L.lmap, (uint32_t*)(base + L.hist),
+                         (uint32_t*)(base + L.marg), (uint16_t*)(base + L.list), vmin, vmax, cfg,
+                         orow + cfg.col_glcm,
+                         dbg_on ? dbg : nullptr);
+        else
+            glcm_phase_s(n, h, w, rowmask, rowoff, vals, (uint8_t*)(base + L.lvl),
+                         (uint16_t*)(base + L.keys), (uint16_t*)(base + L.keys2),
+                         (uint32_t*)(base + L.gcnt), (uint32_t*)(base + L.marg), vmin, vmax, cfg,
+                         orow + cfg.col_glcm, dbg_on ? dbg : nullptr);
     }
     __syncwarp();
 }
@@ -1218,7 +1481,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
 namespace fxg {
 namespace {
 
-template <int CLS, bool GLCM>
+template <int CLS, int GLCM>
 __global__ void __launch_bounds__(32, 20)
     k_roi_s(const __grid_constant__ CUtensorMap tmapL, int use_tma, DevImage img, RoiList rl,
             Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg) {
@@ -1267,7 +1530,7 @@ __global__ void __launch_bounds__(32, 20)
     }
 }
 
-template <int CLS, bool G>
+template <int CLS, int G>
 cudaError_t setup_one(int* occ) {
     constexpr uint32_t bytes = slayout<CLS, G>().bytes + kSlack;
     cudaError_t e = cudaFuncSetAttribute(k_roi_s<CLS, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
@@ -1278,7 +1541,7 @@ cudaError_t setup_one(int* occ) {
     return cudaOccupancyMaxActiveBlocksPerMultiprocessor(occ, k_roi_s<CLS, G>, 32, bytes);
 }
 
-template <int CLS, bool G>
+template <int CLS, int G>
 void launch_one(int grid, cudaStream_t s, const CUtensorMap& tm, int use_tma, DevImage img,
                 RoiList rl, Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg) {
     k_roi_s<CLS, G><<<grid, 32, slayout<CLS, G>().bytes + kSlack, s>>>(tm, use_tma, img, rl, ctl,
@@ -1290,33 +1553,52 @@ void launch_one(int grid, cudaStream_t s, const CUtensorMap& tm, int use_tma, De
 cudaError_t roi_s_setup(int* occ) {
     k_init_log2_tab<<<4, 256>>>();
     cudaError_t e = cudaDeviceSynchronize();
-    if (e == cudaSuccess) e = setup_one<kClassS0, false>(&occ[0]);
-    if (e == cudaSuccess) e = setup_one<kClassS0, true>(&occ[1]);
-    if (e == cudaSuccess) e = setup_one<kClassS1, false>(&occ[2]);
-    if (e == cudaSuccess) e = setup_one<kClassS1, true>(&occ[3]);
-    if (e == cudaSuccess) e = setup_one<kClassS2, false>(&occ[4]);
-    if (e == cudaSuccess) e = setup_one<kClassS2, true>(&occ[5]);
+    if (e == cudaSuccess) e = setup_one<kClassS0, kGlNone>(&occ[0]);
+    if (e == cudaSuccess) e = setup_one<kClassS0, kGlSort>(&occ[1]);
+    if (e == cudaSuccess) e = setup_one<kClassS0, kGlHist>(&occ[2]);
+    if (e == cudaSuccess) e = setup_one<kClassS1, kGlNone>(&occ[3]);
+    if (e == cudaSuccess) e = setup_one<kClassS1, kGlSort>(&occ[4]);
+    if (e == cudaSuccess) e = setup_one<kClassS1, kGlHist>(&occ[5]);
+    if (e == cudaSuccess) e = setup_one<kClassS2, kGlNone>(&occ[6]);
+    if (e == cudaSuccess) e = setup_one<kClassS2, kGlSort>(&occ[7]);
+    if (e == cudaSuccess) e = setup_one<kClassS2, kGlHist>(&occ[8]);
     return e;
 }
 
 void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
                   const CUtensorMap& tmap72, int tma40, int tma72, DevImage img, RoiList rl,
                   Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg) {
-    const bool g = cfg.col_glcm >= 0;
+    const int g = s_glcm_mode(cfg);
+#define FXG_LAUNCH(C, TM, TA)                                                              \
+    do {                                                                                   \
+        if (g == kGlHist) launch_one<C, kGlHist>(grid, s, TM, TA, img, rl, ctl, cfg, out, dbg); \
+        else if (g == kGlSort) launch_one<C, kGlSort>(grid, s, TM, TA, img, rl, ctl, cfg, out, dbg); \
+        else launch_one<C, kGlNone>(grid, s, TM, TA, img, rl, ctl, cfg, out, dbg);      \
+    } while (0)
     switch (cls) {
-        case kClassS0:
-            if (g) launch_one<kClassS0, true>(grid, s, tmap40, tma40, img, rl, ctl, cfg, out, dbg);
-            else launch_one<kClassS0, false>(grid, s, tmap40, tma40, img, rl, ctl, cfg, out, dbg);
-            break;
-        case kClassS1:
-            if (g) launch_one<kClassS1, true>(grid, s, tmap72, tma72, img, rl, ctl, cfg, out, dbg);
-            else launch_one<kClassS1, false>(grid, s, tmap72, tma72, img, rl, ctl, cfg, out, dbg);
-            break;
-        default:
-            if (g) launch_one<kClassS2, true>(grid, s, tmap72, tma72, img, rl, ctl, cfg, out, dbg);
-            else launch_one<kClassS2, false>(grid, s, tmap72, tma72, img, rl, ctl, cfg, out, dbg);
-            break;
+        case kClassS0: FXG_LAUNCH(kClassS0, tmap40, tma40); break;
+        case kClassS1: FXG_LAUNCH(kClassS1, tmap72, tma72); break;
+        default: FXG_LAUNCH(kClassS2, tmap72, tma72); break;
     }
+#undef FXG_LAUNCH
 }
 
 }  // namespace fxg
+
+extern "C" int fx_debug_phase_clocks(unsigned long long* out, int n, int reset) {
+#ifdef FXG_PHASE_TIMING
+    unsigned long long h[16];
+    if (cudaMemcpyFromSymbol(h, ::g_phase_clk, sizeof h) != cudaSuccess) return 7;
+    for (int i = 0; i < n && i < 16; ++i) out[i] = h[i];
+    if (reset) {
+        const unsigned long long z[16] = {};
+        cudaMemcpyToSymbol(::g_phase_clk, z, sizeof z);
+    }
+    return 0;
+#else
+    (void)out;
+    (void)n;
+    (void)reset;
+    return 1;  // FX_E_CONFIG: not a phase-timing build
+#endif
+}

@@ -1,0 +1,40 @@
+"""Per-phase clock shares of the S-class ROI kernels (phase-timing build).
+usage: FXG_LIB=.../libfxg_pt.so python tools/phase_clocks.py c2|c4 [tiles]"""
+import ctypes as C
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import paper_2603_12016_b200 as fx  # noqa: E402
+from paper_2603_12016_b200 import fxg  # noqa: E402
+
+NAMES = ["load+gather", "int sort", "int stats", "edge", "moments", "glcm keys", "glcm sort",
+         "glcm rle", "haralick"]
+which = sys.argv[1]
+ctx = fx.Context(0)
+lib = fxg.lib()
+buf = (C.c_ulonglong * 16)()
+if which == "c2":
+    L, _ = fx.packed_blob_mask_grid(8192, 400, 50000, 1)
+    I = fx.uniform_u16(L.shape, 0)
+    run = lambda: ctx.featurize(I, L, ["intensity", "moments"], fx.resolve_profile("default"))
+    nroi = 50000
+else:
+    T = int(sys.argv[2]) if len(sys.argv) > 2 else 256
+    pairs = []
+    for t in range(T):
+        Lt, _ = fx.packed_blob_mask_grid(512, 1000, 100, t % 16)
+        pairs.append((fx.uniform_u16(Lt.shape, t), Lt))
+    run = lambda: ctx.featurize_batch(pairs, ["intensity", "moments", "glcm"],
+                                      fx.resolve_profile("default"))
+    nroi = sum(int(np.count_nonzero(np.bincount(p[1].ravel(), minlength=65536)[1:])) for p in pairs)
+run()
+lib.fx_debug_phase_clocks(buf, 16, 1)
+run()
+assert lib.fx_debug_phase_clocks(buf, 16, 1) == 0, "not a phase-timing build"
+tot = sum(buf[:9])
+print(f"{which}: {nroi} ROIs, {tot / nroi:.0f} clocks per ROI (lane 0, S kernels)")
+for k, nm in enumerate(NAMES):
+    print(f"  {nm:12s} {buf[k] / nroi:9.0f} clk/ROI  {100 * buf[k] / max(tot, 1):5.1f}%")
