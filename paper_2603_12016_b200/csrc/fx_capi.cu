@@ -378,8 +378,8 @@ int scan_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, bool reset) {
     LabelTable t = label_table(c);
     cudaStream_t s = c->stream;
     const int vec_ok = ((reinterpret_cast<uintptr_t>(img.L) & 15u) == 0) && (img.pitch % 8 == 0);
-    const int tiles = ((img.w + 255) / 256) * ((img.h + 63) / 64);
-    const int grid = std::max(1, std::min((tiles + 3) / 4, c->sm_count * 8));
+    const int tiles = ((img.w + 255) / 256) * ((img.h + FXG_SCAN_ROWS - 1) / FXG_SCAN_ROWS);
+    const int grid = std::max(1, std::min((tiles + 3) / 4, c->sm_count * FXG_SCAN_WAVES));
     Launch l(c, "k_label_scan");
     k_label_scan<<<grid, 128, 0, s>>>(img.L, img.w, img.h, img.pitch, vec_ok, m, t);
     CK(cudaGetLastError());

@@ -7,6 +7,23 @@
 
 namespace fxg {
 
+// label-scan tuning (rows per load batch, min blocks/SM, grid waves, strip rows;
+// the strip height divides the 64-row slot-map granularity).  Measured on C2
+// (tools/kbench.py): 8 rows x 1 block/SM 130 us, 2 rows x 8 blocks/SM 86 us --
+// the sweep is latency-bound, occupancy (bytes in flight) is the lever.
+#ifndef FXG_SCAN_BATCH
+#define FXG_SCAN_BATCH 2
+#endif
+#ifndef FXG_SCAN_MINB
+#define FXG_SCAN_MINB 8
+#endif
+#ifndef FXG_SCAN_WAVES
+#define FXG_SCAN_WAVES 16
+#endif
+#ifndef FXG_SCAN_ROWS
+#define FXG_SCAN_ROWS 32
+#endif
+
 constexpr int kMaxLabels = 65536;  // uint16 labels (reference image.hpp:24)
 constexpr unsigned kFull = 0xffffffffu;
 

@@ -2,8 +2,8 @@
 // reference roi.cpp:76-117).
 //
 // k_label_scan: one coalesced HBM sweep over the uint16 label raster (16 B vector
-// loads, 8 labels per lane, 8 rows in flight).  Each lane owns an 8-pixel-wide
-// x 32-row strip and folds it into a 2-entry register cache using SIMD-in-word
+// loads, 8 labels per lane, software-pipelined row batches).  Each lane owns an
+// 8-pixel-wide x kStripRows-row strip and folds it into a 2-entry register cache using SIMD-in-word
 // tests (one label per chunk is the fast path); the warp then merges equal
 // labels with REDUX and issues one set of global atomics per (strip, label) into
 // the direct-mapped LabelTable.  Integer min/max/sum are order-free, so the
@@ -23,8 +23,8 @@ namespace {
 // cache (blob ROIs give 1-2 labels per strip); at the end of the strip the warp
 // merges equal labels with REDUX and one lane issues the global atomics.
 constexpr int kScanThreads = 128;
-constexpr int kStripRows = 64;
-constexpr int kBatch = 8;  // rows per load batch (8 x 16 B in flight per lane)
+constexpr int kStripRows = FXG_SCAN_ROWS;
+constexpr int kBatch = FXG_SCAN_BATCH;  // rows per load batch (16 B per lane each)
 
 struct CacheEnt {
     uint32_t label, cnt, x0, x1, y0, y1;
@@ -125,7 +125,7 @@ __device__ __forceinline__ void warp_flush(const CacheEnt& e, const LabelTable& 
 
 }  // namespace
 
-__global__ void __launch_bounds__(kScanThreads)
+__global__ void __launch_bounds__(kScanThreads, FXG_SCAN_MINB)
     k_label_scan(const uint16_t* __restrict__ L, int W, int H, size_t pitch, int vec_ok, SlotMap m,
                  LabelTable t) {
     const unsigned lane = lane_id();
@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kScanThreads)
     const int n_tiles = tiles_x * ((H + kStripRows - 1) / kStripRows);
     for (int tile = gw; tile < n_tiles; tile += warps_total) {
         const int strip = tile / tiles_x;
-        const uint32_t slot = m.strip_slot ? m.strip_slot[strip] : 0u;
+        const uint32_t slot = m.strip_slot ? m.strip_slot[(strip * kStripRows) >> 6] : 0u;
         const SlotInfo si = m.info ? m.info[slot] : m.s0;
         const int sw = si.w, send = si.row0 + si.h;  // slot bounds in the stack
         const uint32_t sb = slot << 16;
