@@ -16,6 +16,12 @@ if which == "c2":
     L, _ = fx.packed_blob_mask_grid(8192, 400, 50000, 1)
     groups = ["intensity", "moments"]
     prof = "default"
+elif which.startswith("c5"):  # C5 regime at reduced size: 16384^2, ~2e5-px blobs
+    size = int(os.environ.get("C5_SIZE", "16384"))
+    n = (size // 680) ** 2
+    L, _ = fx.packed_blob_mask_grid(size, 200000, n, 1)
+    groups = ["intensity", "moments", "glcm"]
+    prof = "default"
 else:  # c3: 4096^2, 10k ROIs, GLCM 4 angles ng=256
     L, _ = fx.packed_blob_mask_grid(4096, 400, 10000, 1)
     groups = ["glcm"]
