@@ -2,7 +2,7 @@
 //
 //   H2D (host inputs only) -> k_label_scan -> k_compact_count -> k_compact_emit
 //   -> k_roi_s<S1> / k_roi_s<S2> (TMA-staged windows, warp per ROI)
-//   -> k_roi_l (large windows + S overflow, global slabs) -> D2H table
+//   -> k_roi_b (large windows + S overflow: one CTA per ROI, global slabs) -> D2H table
 //
 // The only host synchronisation before the table readback is a small
 // side-stream copy of the compaction counters (L-path slab sizing), which
@@ -32,8 +32,10 @@ cudaError_t roi_s_setup(int* occ /* [3][3]: class x GlcmMode */);
 void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
                   const CUtensorMap& tmap72, int tma40, int tma72, DevImage img, RoiList rl,
                   Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg);
-void launch_roi_l(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
-                  double* out, const DebugOut* dbg, uint8_t* scratch, const Layout& L);
+cudaError_t roi_b_setup();
+BLayout make_blayout(uint32_t H, uint32_t WPR, uint32_t NMAX, uint32_t RUNMAX, uint32_t NB);
+void launch_roi_b(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
+                  double* out, const DebugOut* dbg, uint8_t* scratch, const BLayout& B);
 }  // namespace fxg
 
 using namespace fxg;
@@ -91,6 +93,8 @@ struct fx_ctx {
     // L-path slabs
     uint8_t* d_lscratch = nullptr;
     size_t lscratch_bytes = 0;
+    BLayout lay_prev{};  // layout of the last large-ROI launch (zeroed regions valid)
+    int lay_grid = 0;
     // debug capture
     DebugOut* d_dbg = nullptr;
     // accounting
@@ -315,6 +319,7 @@ int ensure_lscratch(fx_ctx* c, size_t bytes) {
     }
     c->d_lscratch = nullptr;
     c->lscratch_bytes = 0;
+    c->lay_grid = 0;
     CK(cudaMalloc(&c->d_lscratch, bytes));
     c->lscratch_bytes = bytes;
     return FX_OK;
@@ -346,14 +351,15 @@ bool make_tmap(fx_ctx* c, const DevImage& img, CUtensorMap* m, int box_w) {
     return r == CUDA_SUCCESS;
 }
 
-Layout l_layout(const Control& h) {
+// large-ROI slab layout from the compaction maxima (>= an S2 window, for overflow)
+BLayout b_layout(const Control& h, int bins) {
     const uint32_t H = std::max<uint32_t>(h.l_max_h, kSH);
     const uint32_t WPR = std::max<uint32_t>(h.l_max_wpr, 1);
     const uint32_t NMAX = (uint32_t)std::max<unsigned long long>(h.l_max_n, kS2N);
     const unsigned long long cells = std::max<unsigned long long>(h.l_max_cells, (unsigned long long)kSW * kSH);
     const uint32_t RUNMAX =
-        (uint32_t)std::min<unsigned long long>(cells / 2 + H + 64, 16ull << 20);
-    return make_layout(H, WPR, NMAX, RUNMAX, 4, 0);
+        (uint32_t)std::min<unsigned long long>(cells / 2 + H + 64, 64ull << 20);
+    return make_blayout(H, WPR, NMAX, RUNMAX, (uint32_t)std::max(bins, 2));
 }
 
 struct DebugHost {
@@ -463,18 +469,29 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
                                             " < " + std::to_string(hc.n_rois) + " ROIs");
     }
     {
-        const Layout L = l_layout(hc);
+        // large ROIs + S overflow: one CTA per ROI; the slabs' histograms are kept
+        // zero by the kernel, so they are cleared only when the layout changes
+        const BLayout B = b_layout(hc, cfg.bins);
         const uint32_t nl = hc.class_count[kClassL];
-        const uint32_t grid = (uint32_t)std::min<uint64_t>(
-            (uint64_t)c->sm_count * 2,
-            std::max<uint64_t>(std::max<uint64_t>(nl, 1),
-                               hc.class_count[kClassS0] + hc.class_count[kClassS1] +
-                                           hc.class_count[kClassS2] > 0 ? 16 : 1));
-        size_t bytes = (size_t)L.bytes * grid;
-        int rc = ensure_lscratch(c, bytes);
+        const uint64_t s_rois = (uint64_t)hc.class_count[kClassS0] + hc.class_count[kClassS1] +
+                                hc.class_count[kClassS2];
+        uint64_t grid = std::min<uint64_t>((uint64_t)c->sm_count * 2,
+                                           std::max<uint64_t>(std::max<uint64_t>(nl, 1),
+                                                              s_rois > 0 ? 16 : 1));
+        const uint64_t budget = 8ull << 30;  // scratch cap: fewer CTAs for huge windows
+        grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, budget / std::max<size_t>(B.bytes, 1)));
+        int rc = ensure_lscratch(c, (size_t)B.bytes * grid);
         if (rc) return rc;
-        Launch l(c, "k_roi_l");
-        launch_roi_l((int)grid, s, img, rl, c->d_ctl, cfg, out_dev, dbg_dev, c->d_lscratch, L);
+        const bool same = c->lay_grid >= (int)grid && B.bytes == c->lay_prev.bytes &&
+                          B.vhist == c->lay_prev.vhist && B.ghist == c->lay_prev.ghist &&
+                          B.bins == c->lay_prev.bins && B.NB == c->lay_prev.NB;
+        if (!same) {
+            CK(cudaMemsetAsync(c->d_lscratch, 0, (size_t)B.bytes * grid, s));
+            c->lay_prev = B;
+            c->lay_grid = (int)grid;
+        }
+        Launch l(c, "k_roi_b");
+        launch_roi_b((int)grid, s, img, rl, c->d_ctl, cfg, out_dev, dbg_dev, c->d_lscratch, B);
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
@@ -653,6 +670,7 @@ int fx_ctx_create(int device, fx_ctx** out) {
         CKC(cudaStreamSynchronize(c->stream));
     }
     CKC(roi_s_setup(&c->occ_s[0][0]));
+    CKC(roi_b_setup());
     for (auto& row : c->occ_s)
         for (int& o : row) o = std::max(1, o);
     void* fn = nullptr;

@@ -1,6 +1,6 @@
-// Per-ROI warp pipeline: one warp computes every requested group of one ROI
-// from its bbox window.  Shared by the S kernels (window staged in shared
-// memory by TMA) and the L kernel (global-memory slab, plain loads).
+// Device helpers shared by the per-ROI kernels: the S kernels (one warp per ROI,
+// window staged in shared memory by TMA, fx_roi_s.cu) and the large-ROI kernel
+// (one CTA per ROI, global-memory slab, fx_roi_b.cu).
 //
 // Reference functions restated on the device (paths relative to
 // /root/reference/proj):
@@ -19,71 +19,8 @@
 namespace fxg {
 
 // ------------------------------------------------------------------ layout --
-
-struct Layout {  // byte offsets inside one warp's slab
-    uint32_t rowmask, rowoff, vals, xy;         // region A (whole ROI lifetime)
-    uint32_t stage;                             // region B, load phase (TMA tile)
-    uint32_t tmp, sorted, cnt;                  // region B, sort / intensity phase
-    uint32_t kmask, emask, runoff, rs, re, parent, rsize;  // region B, edge phase
-    uint32_t lvl, keys, keys2, gcnt, marg, gstat;          // region B, glcm phase
-    uint32_t bytes;
-    uint32_t H, WPR, NMAX, RUNMAX;
-};
-
 __host__ __device__ constexpr uint32_t al(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 __host__ __device__ constexpr uint32_t mx(uint32_t a, uint32_t b) { return a > b ? a : b; }
-
-__host__ __device__ constexpr Layout make_layout(uint32_t H, uint32_t WPR, uint32_t NMAX,
-                                                 uint32_t RUNMAX, uint32_t xy_bytes,
-                                                 uint32_t stage_bytes) {
-    Layout L{};
-    L.H = H;
-    L.WPR = WPR;
-    L.NMAX = NMAX;
-    L.RUNMAX = RUNMAX;
-    uint32_t o = 0;
-    L.rowmask = o;
-    o += H * WPR * 8;
-    L.rowoff = o;
-    o = al(o + (H + 1) * 4, 16);
-    L.vals = o;
-    o = al(o + NMAX * 2, 16);
-    L.xy = o;
-    o = al(o + NMAX * xy_bytes, 128);
-    const uint32_t B = o;
-    // load phase
-    L.stage = B;
-    uint32_t e_load = B + stage_bytes;
-    // sort / intensity phase
-    L.tmp = B;
-    L.sorted = al(L.tmp + NMAX * 2, 16);
-    L.cnt = al(L.sorted + NMAX * 2, 16);
-    uint32_t e_sort = L.cnt + 256 * 4;
-    // edge phase
-    L.kmask = B;
-    L.emask = L.kmask + H * WPR * 8;
-    L.runoff = L.emask + H * WPR * 8;
-    L.rs = al(L.runoff + (H + 1) * 4, 16);
-    L.re = al(L.rs + RUNMAX * 2, 16);
-    L.parent = al(L.re + RUNMAX * 2, 16);
-    L.rsize = al(L.parent + RUNMAX * 4, 16);
-    uint32_t e_edge = L.rsize + RUNMAX * 4;
-    // glcm phase (ng <= 256)
-    L.lvl = B;
-    L.keys = al(L.lvl + NMAX, 16);
-    L.keys2 = al(L.keys + NMAX * 2, 16);
-    L.gcnt = al(L.keys2 + NMAX * 2, 16);
-    L.marg = L.gcnt + 256 * 4;
-    L.gstat = al(L.marg + (256 + 256 + 512 + 256) * 4, 16);
-    uint32_t e_glcm = L.gstat + 32 * 8;
-    L.bytes = al(mx(mx(e_load, e_sort), mx(e_edge, e_glcm)), 128);
-    return L;
-}
-
-// S-class slabs (64x64 window, one mask word per row, 8 KB TMA label tile).
-constexpr uint32_t kStageBytes = kStageW * kSH * 2;
-constexpr Layout kLayoutS1 = make_layout(kSH, 1, kS1N, kS1Runs, 2, kStageBytes);
-constexpr Layout kLayoutS2 = make_layout(kSH, 1, kS2N, 1024, 2, kStageBytes);
 
 // --------------------------------------------------------- debug capture --
 
@@ -104,57 +41,6 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// stable LSD radix pass on 16-bit keys by one warp (8-bit digit at `shift`)
-__device__ inline void radix_pass16(const uint16_t* src, uint16_t* dst, uint32_t n, int shift,
-                             uint32_t* cnt) {
-    const unsigned lane = lane_id();
-    for (int i = lane; i < 256; i += 32) cnt[i] = 0;
-    __syncwarp();
-    for (uint32_t base = 0; base < n; base += 32) {
-        const uint32_t i = base + lane;
-        const bool ok = i < n;
-        const uint32_t d = ok ? ((uint32_t)src[i] >> shift) & 0xffu : 256u + lane;
-        const unsigned peers = __match_any_sync(kFull, d);
-        if (ok && lane == (unsigned)(__ffs(peers) - 1)) cnt[d] += __popc(peers);
-        __syncwarp();
-    }
-    uint32_t c[8], s = 0;
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        c[k] = cnt[lane * 8 + k];
-        s += c[k];
-    }
-    const uint32_t incl = warp_incl_scan(s);
-    uint32_t run = incl - s;
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-        cnt[lane * 8 + k] = run;
-        run += c[k];
-    }
-    __syncwarp();
-    for (uint32_t base = 0; base < n; base += 32) {
-        const uint32_t i = base + lane;
-        const bool ok = i < n;
-        const uint16_t key = ok ? src[i] : 0;
-        const uint32_t d = ok ? ((uint32_t)key >> shift) & 0xffu : 256u + lane;
-        const unsigned peers = __match_any_sync(kFull, d);
-        if (ok) dst[cnt[d] + __popc(peers & lanemask_lt())] = key;
-        __syncwarp();
-        if (ok && lane == (unsigned)(31 - __clz(peers))) cnt[d] += __popc(peers);
-        __syncwarp();
-    }
-}
-
-// sort n 16-bit keys (src != tmp != dst; src == dst allowed).  A single pass
-// (all keys < 256) lands in tmp; returns the buffer holding the sorted keys.
-__device__ inline uint16_t* warp_sort16(const uint16_t* src, uint16_t* tmp, uint16_t* dst,
-                                        uint32_t n, uint32_t* cnt, bool one_pass) {
-    radix_pass16(src, tmp, n, 0, cnt);
-    if (one_pass) return tmp;
-    radix_pass16(tmp, dst, n, 8, cnt);
-    return dst;
-}
 
 // Butterfly reduce-scatter of 32 per-lane doubles: lane i ends with sum_j v[i] over lanes.
 __device__ __forceinline__ double reduce_scatter32(double (&v)[32]) {
@@ -181,6 +67,15 @@ __device__ __forceinline__ uint32_t uf_find(volatile uint32_t* parent, uint32_t 
         if (gp != p) parent[x] = gp;
         x = p;
         p = gp;
+    }
+    return x;
+}
+// root without path compression: safe to run concurrently with other readers
+__device__ __forceinline__ uint32_t uf_root(const uint32_t* parent, uint32_t x) {
+    uint32_t p = parent[x];
+    while (p != x) {
+        x = p;
+        p = parent[x];
     }
     return x;
 }
@@ -219,37 +114,103 @@ __device__ __forceinline__ double percentile_exact(const uint16_t* s, unsigned l
     return __dadd_rn(a, __dmul_rn(frac, __dsub_rn(b, a)));
 }
 
-// k-th smallest (0-based) of |2*s[i] - M2| over sorted s: the deviations form
-// a V (decreasing on [0,m), increasing on [m,n)); classic k-th of two sorted
-// arrays.  A[j] = M2 - 2 s[m-1-j] (j < m), B[j] = 2 s[m+j] - M2.
-__device__ inline uint32_t kth_dev2(const uint16_t* s, uint32_t n, uint32_t M2, uint32_t k) {
-    // m = first index with 2*s[i] >= M2
-    uint32_t lo = 0, hi = n;
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (2u * s[mid] >= M2) hi = mid;
-        else lo = mid + 1;
+
+// Moments epilogue (moments.cpp:32-92), warp-level.  Lane i holds N_i: the sums
+// of w dx^p dy^q about the integer anchors (binary lanes 0..15: w = 1 about
+// (axb, ayb); weighted lanes 16..31: w = I about (axw, ayw)), p = (i>>2)&3,
+// q = i&3.  Binomial shift to the exact centroid (central) and to the image origin
+// (raw, global coordinates via the window origin gx0/gy0); eta, Hu.  Writes the
+// 104 moment columns at o.
+__device__ __forceinline__ void moments_epilogue(double N, double dn, unsigned long long n,
+                                                 unsigned long long sS, unsigned long long sLX,
+                                                 unsigned long long sLY, unsigned long long sXI,
+                                                 unsigned long long sYI, long long axb,
+                                                 long long ayb, long long axw, long long ayw,
+                                                 long long gx0, long long gy0, double* o) {
+    const unsigned lane = lane_id();
+    const long long nb_ = (long long)n, W = (long long)sS;
+    const int grp = lane >> 4, p = (lane >> 2) & 3, q = lane & 3;
+    const double m00 = grp ? (double)sS : dn;
+    const bool zero_mass = grp && sS == 0;
+    // fractional offset of the true centroid from the anchor
+    const double dx = grp ? (W > 0 ? (double)((long long)sXI - axw * W) / (double)W : 0.0)
+                          : (double)((long long)sLX - axb * nb_) / dn;
+    const double dy = grp ? (W > 0 ? (double)((long long)sYI - ayw * W) / (double)W : 0.0)
+                          : (double)((long long)sLY - ayb * nb_) / dn;
+    const double Ax = (double)(gx0 + (grp ? axw : axb));
+    const double Ay = (double)(gy0 + (grp ? ayw : ayb));
+    const double C[4][4] = {{1, 0, 0, 0}, {1, 1, 0, 0}, {1, 2, 1, 0}, {1, 3, 3, 1}};
+    double pmx[4], pmy[4], pax[4], pay[4];
+    pmx[0] = pmy[0] = pax[0] = pay[0] = 1.0;
+#pragma unroll
+    for (int k = 1; k < 4; ++k) {
+        pmx[k] = pmx[k - 1] * (-dx);
+        pmy[k] = pmy[k - 1] * (-dy);
+        pax[k] = pax[k - 1] * Ax;
+        pay[k] = pay[k - 1] * Ay;
     }
-    const uint32_t m = lo, na = m, nb = n - m;
-    // find split: take i from A, k+1-i from B
-    uint32_t ilo = (k + 1 > nb) ? k + 1 - nb : 0, ihi = (k + 1 < na) ? k + 1 : na;
-    while (ilo < ihi) {
-        const uint32_t i = (ilo + ihi) >> 1;  // elements taken from A
-        const uint32_t j = k + 1 - i;         // from B
-        // A[i] < B[j-1] -> need more from A
-        const uint32_t Ai = M2 - 2u * s[m - 1 - i];
-        const uint32_t Bj1 = 2u * s[m + j - 1] - M2;
-        if (Ai < Bj1) ilo = i + 1;
-        else ihi = i;
+    double mu = 0, raw = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const double Nij = __shfl_sync(kFull, N, (grp << 4) | (i << 2) | j);
+            if (i <= p && j <= q) {
+                const double cc = C[p][i] * C[q][j];
+                mu += cc * pmx[p - i] * pmy[q - j] * Nij;
+                raw += cc * pax[p - i] * pay[q - j] * Nij;
+            }
+        }
+    if ((p == 1 && q == 0) || (p == 0 && q == 1)) mu = 0.0;  // moments.cpp:80-81
+    if (p == 0 && q == 0) mu = N;
+    double eta = 0;
+    if (p + q >= 2) eta = mu / pow(m00, 1.0 + (p + q) / 2.0);
+    if (zero_mass) {
+        raw = 0;
+        mu = 0;
+        eta = 0;
     }
-    const uint32_t i = ilo, j = k + 1 - i;
-    uint32_t best = 0;
-    if (i > 0) best = M2 - 2u * s[m - i];
-    if (j > 0) {
-        const uint32_t b = 2u * s[m + j - 1] - M2;
-        if (i == 0 || b > best) best = b;
+    // Hu invariants (moments.cpp:14-28) on lanes 0 / 16
+    const double n20 = __shfl_sync(kFull, eta, (grp << 4) | 8);
+    const double n02 = __shfl_sync(kFull, eta, (grp << 4) | 2);
+    const double n11 = __shfl_sync(kFull, eta, (grp << 4) | 5);
+    const double n30 = __shfl_sync(kFull, eta, (grp << 4) | 12);
+    const double n03 = __shfl_sync(kFull, eta, (grp << 4) | 3);
+    const double n21 = __shfl_sync(kFull, eta, (grp << 4) | 9);
+    const double n12 = __shfl_sync(kFull, eta, (grp << 4) | 6);
+    o += grp * 52;
+    const int li = lane & 15;
+    o[li] = raw;
+    o[16 + li] = mu;
+    if (p + q >= 2) {
+        const int eidx = (p == 0) ? q - 2 : (p == 1 ? 1 + q : 1 + 4 * (p - 1) + q);
+        o[32 + eidx] = eta;
     }
-    return best;
+    if (li == 0) {
+        const double a = n30 + n12, b = n21 + n03;
+        double hu[7];
+        hu[0] = n20 + n02;
+        hu[1] = (n20 - n02) * (n20 - n02) + 4.0 * n11 * n11;
+        hu[2] = (n30 - 3.0 * n12) * (n30 - 3.0 * n12) + (3.0 * n21 - n03) * (3.0 * n21 - n03);
+        hu[3] = a * a + b * b;
+        hu[4] = (n30 - 3.0 * n12) * a * (a * a - 3.0 * b * b) +
+                (3.0 * n21 - n03) * b * (3.0 * a * a - b * b);
+        hu[5] = (n20 - n02) * (a * a - b * b) + 4.0 * n11 * a * b;
+        hu[6] = (3.0 * n21 - n03) * a * (a * a - 3.0 * b * b) -
+                (n30 - 3.0 * n12) * b * (3.0 * a * a - b * b);
+#pragma unroll
+        for (int k = 0; k < 7; ++k) o[45 + k] = zero_mass ? 0.0 : hu[k];
+    }
+    __syncwarp();
 }
+
+// Byte offsets of one CTA's global scratch slab in the large-ROI kernel (fx_roi_b.cu),
+// sized on the host from the largest L window / pixel count of the launch.
+struct BLayout {
+    size_t rowmask, kmask, emask, wordoff, tmpw, xy, vals, lvl, vhist, runoff, rs, re, parent,
+        rsize, bins, ghist;
+    size_t bytes;
+    uint32_t H, WPR, NMAX, RUNMAX, NB;
+};
 
 }  // namespace fxg

@@ -1,0 +1,919 @@
+// Large-ROI path (class L: window wider or taller than 64, plus S-class ROIs
+// re-queued for run capacity): one 512-thread CTA per ROI, persistent over the
+// L work list, per-CTA scratch slab in global memory (L2-resident).
+//
+// Same columns and the same exact-integer / literal-expression rules as the S
+// kernels (fx_roi_s.cu), re-designed for windows of up to 65536 x 65536:
+//  - membership words (u64 per 64 window columns) by warp ballots, pixel list in
+//    row-major order by a block scan of word popcounts;
+//  - intensity statistics from a 65536-bin value histogram (global) plus a
+//    256-bin coarse prefix in shared memory: every order statistic is a two-level
+//    search, the median absolute deviation a binary search over deviations d with
+//    F(d) = C((M2+d)/2) - C((M2-d)/2 - 1); no sort (reference intensity_features
+//    .cpp:14-215);
+//  - contour edge set ("definition B" == trace_contour's visited set): run
+//    union-find over the window (8-connected components, largest with row-major
+//    tie-break; 4-connected exterior of the rest), edge = K & (dilate4(E) | border)
+//    (contour.cpp:30-144);
+//  - moments: separable row sums about integer anchors, fp64 block reduction,
+//    binomial shift (moments.cpp:32-92);
+//  - GLCM (ng <= 256): pair counts in a global ng x ng histogram, one dense pass
+//    in fixed thread order (deterministic), integer cell sums, shared-memory
+//    marginals, Haralick from marginals (texture.cpp:29-217).
+#include "fx_dev.cuh"
+#include "fx_glcm.cuh"
+#include "fx_roi.cuh"
+
+namespace fxg {
+
+namespace {
+
+constexpr int kBT = 512;
+constexpr int kBW = kBT / 32;
+
+__device__ __forceinline__ unsigned warp_id() { return threadIdx.x >> 5; }
+
+// all-reduce over the CTA; sh: >= kBW + 1 elements of T, reusable after return
+template <typename T, typename Op>
+__device__ __forceinline__ T block_all(T v, T* sh, Op op) {
+    const unsigned lane = lane_id(), w = warp_id();
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = op(v, __shfl_xor_sync(kFull, v, o));
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    if (w == 0) {  // lanes 0..kBW-1 reduce the warp partials (xor offsets < kBW)
+        T t = sh[lane & (kBW - 1)];
+#pragma unroll
+        for (int o = kBW / 2; o; o >>= 1) t = op(t, __shfl_xor_sync(kFull, t, o));
+        if (lane == 0) sh[kBW] = t;
+    }
+    __syncthreads();
+    const T r = sh[kBW];
+    __syncthreads();
+    return r;
+}
+struct OpAdd {
+    template <typename T>
+    __device__ T operator()(T a, T b) const { return a + b; }
+};
+struct OpMin {
+    template <typename T>
+    __device__ T operator()(T a, T b) const { return b < a ? b : a; }
+};
+struct OpMax {
+    template <typename T>
+    __device__ T operator()(T a, T b) const { return b > a ? b : a; }
+};
+
+// exclusive scan of a[0..N) in place (a[N] = total); sh: >= kBW + 2 u32
+__device__ uint32_t block_exscan(uint32_t* a, uint32_t N, uint32_t* sh) {
+    const unsigned lane = lane_id(), w = warp_id();
+    uint32_t carry = 0;
+    for (uint32_t b0 = 0; b0 < N; b0 += kBT) {
+        const uint32_t i = b0 + threadIdx.x;
+        const uint32_t v = i < N ? a[i] : 0u;
+        const uint32_t incl = warp_incl_scan(v);
+        if (lane == 31) sh[w] = incl;
+        __syncthreads();
+        if (w == 0) {
+            const uint32_t t = lane < kBW ? sh[lane] : 0u;
+            const uint32_t ti = warp_incl_scan(t);
+            if (lane < kBW) sh[lane] = ti - t;
+            if (lane == 31) sh[kBW] = ti;
+        }
+        __syncthreads();
+        if (i < N) a[i] = carry + sh[w] + incl - v;
+        carry += sh[kBW];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) a[N] = carry;
+    __syncthreads();
+    return carry;
+}
+
+// number of values <= x (x in [-1, 65535]); warp-level
+__device__ __forceinline__ unsigned long long count_le(int x, const uint32_t* cpre,
+                                                       const uint32_t* vhist) {
+    if (x < 0) return 0ull;
+    if (x > 65535) x = 65535;
+    const unsigned lane = lane_id();
+    const int hb = x >> 8, lb = x & 255;
+    const uint4* f = reinterpret_cast<const uint4*>(vhist + hb * 256 + lane * 8);
+    const uint4 a = f[0], b = f[1];
+    const uint32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t s = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        if ((int)lane * 8 + j <= lb) s += c[j];
+    return (unsigned long long)cpre[hb] + warp_sum(s);
+}
+
+// r-th smallest value (0-based) of the multiset; warp-level
+__device__ __forceinline__ uint32_t kth_value(unsigned long long r, const uint32_t* cpre,
+                                              const uint32_t* vhist) {
+    const unsigned lane = lane_id();
+    // bucket: number of buckets whose end prefix is <= r
+    uint32_t nb = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) nb += (unsigned long long)cpre[lane * 8 + j + 1] <= r;
+    const uint32_t hb = warp_sum(nb);
+    const uint4* f = reinterpret_cast<const uint4*>(vhist + hb * 256 + lane * 8);
+    const uint4 a = f[0], b = f[1];
+    const uint32_t c[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    uint32_t t = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) t += c[j];
+    const uint32_t incl = warp_incl_scan(t);
+    unsigned long long run = (unsigned long long)cpre[hb] + incl - t;
+    uint32_t found = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        if (r >= run && r < run + c[j]) found = hb * 256 + lane * 8 + j + 1;
+        run += c[j];
+    }
+    return __reduce_max_sync(kFull, found) - 1;
+}
+
+// percentile_exact on the implicit sorted sequence (same literal expression)
+__device__ __forceinline__ double percentile_h(double p, unsigned long long n, const uint32_t* cpre,
+                                               const uint32_t* vhist) {
+    if (n == 1) return (double)kth_value(0, cpre, vhist);
+    const double rank = __dmul_rn(__ddiv_rn(p, 100.0), (double)(n - 1));
+    const unsigned long long lo = (unsigned long long)rank;
+    if (lo + 1 >= n) return (double)kth_value(n - 1, cpre, vhist);
+    const double frac = __dsub_rn(rank, (double)lo);
+    const double a = (double)kth_value(lo, cpre, vhist), b = (double)kth_value(lo + 1, cpre, vhist);
+    return __dadd_rn(a, __dmul_rn(frac, __dsub_rn(b, a)));
+}
+
+// k-th smallest (0-based) of |2 v - M2| over the multiset; warp-level binary search
+__device__ uint32_t kth_dev_h(unsigned long long k, uint32_t M2, const uint32_t* cpre,
+                              const uint32_t* vhist) {
+    uint32_t lo = 0, hi = 131071;
+    while (lo < hi) {
+        const uint32_t d = (lo + hi) >> 1;
+        // v with M2 - d <= 2 v <= M2 + d
+        const int vhi = (int)((M2 + d) >> 1);
+        const int dlo = (int)M2 - (int)d;
+        const int vlo = dlo <= 0 ? 0 : (dlo + 1) >> 1;
+        const unsigned long long F = count_le(vhi, cpre, vhist) - count_le(vlo - 1, cpre, vhist);
+        if (F > k) hi = d;
+        else lo = d + 1;
+    }
+    return lo;
+}
+
+struct BSlab {
+    uint64_t *rowmask, *kmask, *emask;
+    uint32_t *wordoff, *tmpw, *xy;
+    uint16_t* vals;
+    uint8_t* lvl;
+    uint32_t *vhist, *runoff, *parent, *rsize, *bins, *ghist;
+    uint16_t *rs, *re;
+};
+
+__device__ __forceinline__ BSlab bslab(uint8_t* base, const BLayout& B) {
+    BSlab S;
+    S.rowmask = (uint64_t*)(base + B.rowmask);
+    S.kmask = (uint64_t*)(base + B.kmask);
+    S.emask = (uint64_t*)(base + B.emask);
+    S.wordoff = (uint32_t*)(base + B.wordoff);
+    S.tmpw = (uint32_t*)(base + B.tmpw);
+    S.xy = (uint32_t*)(base + B.xy);
+    S.vals = (uint16_t*)(base + B.vals);
+    S.lvl = base + B.lvl;
+    S.vhist = (uint32_t*)(base + B.vhist);
+    S.runoff = (uint32_t*)(base + B.runoff);
+    S.rs = (uint16_t*)(base + B.rs);
+    S.re = (uint16_t*)(base + B.re);
+    S.parent = (uint32_t*)(base + B.parent);
+    S.rsize = (uint32_t*)(base + B.rsize);
+    S.bins = (uint32_t*)(base + B.bins);
+    S.ghist = (uint32_t*)(base + B.ghist);
+    return S;
+}
+
+// runs of set bits of m (rows of wpr words) -> rs/re, runoff; parent[r] = r.
+// Returns the run count, or ~0u past capacity.
+__device__ uint32_t build_runs(const uint64_t* m, int h, int wpr, const BSlab& S, uint32_t runmax,
+                               uint32_t* sh) {
+    for (int y = threadIdx.x; y < h; y += kBT) {
+        uint32_t c = 0;
+        uint64_t prev = 0;
+        for (int k = 0; k < wpr; ++k) {
+            const uint64_t x = m[(size_t)y * wpr + k];
+            c += __popcll(x & ~((x << 1) | (prev >> 63)));
+            prev = x;
+        }
+        S.runoff[y] = c;
+    }
+    __syncthreads();
+    const uint32_t total = block_exscan(S.runoff, (uint32_t)h, sh);
+    if (total > runmax) return ~0u;
+    for (int y = threadIdx.x; y < h; y += kBT) {
+        uint32_t j = S.runoff[y];
+        int open = 0;
+        for (int k = 0; k < wpr; ++k) {
+            const uint64_t x = m[(size_t)y * wpr + k];
+            const uint64_t pv = k ? m[(size_t)y * wpr + k - 1] : 0ull;
+            const uint64_t nx = k + 1 < wpr ? m[(size_t)y * wpr + k + 1] : 0ull;
+            uint64_t st = x & ~((x << 1) | (pv >> 63));
+            uint64_t en = x & ~((x >> 1) | (nx << 63));
+            while (st | en) {
+                const int bs = st ? __ffsll((long long)st) - 1 : 64;
+                const int be = en ? __ffsll((long long)en) - 1 : 64;
+                if (bs <= be) {
+                    open = k * 64 + bs;
+                    st &= st - 1;
+                } else {
+                    S.rs[j] = (uint16_t)open;
+                    S.re[j] = (uint16_t)(k * 64 + be);
+                    ++j;
+                    en &= en - 1;
+                }
+            }
+        }
+    }
+    for (uint32_t r = threadIdx.x; r < total; r += kBT) S.parent[r] = r;
+    __syncthreads();
+    return total;
+}
+
+// union of runs in adjacent rows (ext 1: 8-connected, 0: 4-connected), then flatten
+__device__ void unite_runs(int h, int ext, const BSlab& S) {
+    for (int y = 1 + threadIdx.x; y < h; y += kBT) {
+        uint32_t i = S.runoff[y], ie = S.runoff[y + 1], j = S.runoff[y - 1], je = S.runoff[y];
+        while (i < ie && j < je) {
+            const int as = S.rs[i], ae = S.re[i], bs = S.rs[j], be = S.re[j];
+            if (be + ext < as) ++j;
+            else if (ae + ext < bs) ++i;
+            else {
+                uf_union(S.parent, i, j);
+                if (ae < be) ++i;
+                else ++j;
+            }
+        }
+    }
+    __syncthreads();
+    // flatten in two phases: a compressing find could overwrite a root another
+    // thread has just published with an older ancestor
+    const uint32_t nr = S.runoff[h];
+    for (uint32_t r = threadIdx.x; r < nr; r += kBT) S.rsize[r] = uf_root(S.parent, r);
+    __syncthreads();
+    for (uint32_t r = threadIdx.x; r < nr; r += kBT) S.parent[r] = S.rsize[r];
+    __syncthreads();
+}
+
+// set bits [a, b] of a row of words
+__device__ __forceinline__ void set_bits(uint64_t* row, int a, int b) {
+    for (int k = a >> 6; k <= (b >> 6); ++k) {
+        const int lo = k == (a >> 6) ? (a & 63) : 0, hi = k == (b >> 6) ? (b & 63) : 63;
+        row[k] |= bits_between(lo, hi);
+    }
+}
+
+struct BShared {
+    uint32_t coarse[256];
+    uint32_t cpre[257];
+    uint32_t scan[kBW + 2];
+    unsigned long long u64s[kBW + 1];
+    double f64s[kBW + 1];
+    uint32_t u32s[kBW + 1];
+    double red[kBW][33];
+    uint32_t px[256], py[256], psum[512], pdif[256];
+    uint32_t job;
+};
+
+__device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Control* ctl,
+                          const FeatCfg& cfg, double* __restrict__ out, const DebugOut* dbg,
+                          const BSlab& S, const BLayout& B, BShared& sm) {
+    const unsigned tid = threadIdx.x, lane = lane_id(), wid = warp_id();
+    const uint32_t label = rl.label[r];
+    const int w = (int)rl.w[r], h = (int)rl.h[r];
+    const uint32_t x0 = rl.x0[r], y0 = rl.y0[r];
+    const long long gx0 = rl.gx[r], gy0 = rl.gy[r];
+    const int wpr = (w + 63) >> 6;
+    const uint32_t nw = (uint32_t)h * (uint32_t)wpr;
+    double* orow = out + (size_t)r * cfg.ncols;
+    const bool dbg_on = dbg != nullptr && dbg->label == label;
+    const bool want_int = cfg.col_int >= 0, want_mom = cfg.col_mom >= 0, want_glcm = cfg.col_glcm >= 0;
+
+    // ---- membership words (warp per 64-column word) and popcounts
+    for (uint32_t wi = wid; wi < nw; wi += kBW) {
+        const int y = (int)(wi / wpr), k = (int)(wi % wpr);
+        const uint16_t* row = img.L + (size_t)(y0 + y) * img.pitch + x0;
+        const int xa = k * 64 + (int)lane, xb = xa + 32;
+        const unsigned lo = __ballot_sync(kFull, xa < w && row[xa] == label);
+        const unsigned hi = __ballot_sync(kFull, xb < w && row[xb] == label);
+        if (lane == 0) {
+            const uint64_t m = (uint64_t)lo | ((uint64_t)hi << 32);
+            S.rowmask[wi] = m;
+            S.wordoff[wi] = __popcll(m);
+        }
+    }
+    for (int i = tid; i < 256; i += kBT) sm.coarse[i] = 0u;
+    __syncthreads();
+    const uint32_t n = block_exscan(S.wordoff, nw, sm.scan);
+    const double dn = (double)n;
+
+    // ---- pixel list (row-major), intensities, exact integer sums, value histogram
+    unsigned long long sS = 0, sQ = 0, sX = 0, sY = 0, sXI = 0, sYI = 0;
+    uint32_t vlo = 0xffffu, vhi = 0u;
+    for (uint32_t wi = wid; wi < nw; wi += kBW) {
+        const uint64_t m = S.rowmask[wi];
+        if (!m) continue;
+        const uint32_t base = S.wordoff[wi];
+        const uint32_t y = wi / wpr, k = wi % wpr;
+        const uint16_t* Irow = img.I + (size_t)(y0 + y) * img.pitch + x0;
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf) {
+            const int bit = (int)lane + 32 * hf;
+            if (!((m >> bit) & 1ull)) continue;
+            const uint32_t pos = base + __popcll(m & ((1ull << bit) - 1ull));
+            const uint32_t x = k * 64 + bit;
+            const uint32_t v = Irow[x];
+            S.xy[pos] = x | (y << 16);
+            S.vals[pos] = (uint16_t)v;
+            sS += v;
+            sQ += (unsigned long long)v * v;
+            sX += x;
+            sY += y;
+            sXI += (unsigned long long)x * v;
+            sYI += (unsigned long long)y * v;
+            vlo = min(vlo, v);
+            vhi = max(vhi, v);
+            if (want_int) {
+                atomicAdd(&S.vhist[v], 1u);
+                atomicAdd(&sm.coarse[v >> 8], 1u);
+            }
+        }
+    }
+    sS = block_all(sS, sm.u64s, OpAdd());
+    sQ = block_all(sQ, sm.u64s, OpAdd());
+    sX = block_all(sX, sm.u64s, OpAdd());
+    sY = block_all(sY, sm.u64s, OpAdd());
+    sXI = block_all(sXI, sm.u64s, OpAdd());
+    sYI = block_all(sYI, sm.u64s, OpAdd());
+    const uint32_t vmin = block_all(vlo, sm.u32s, OpMin());
+    const uint32_t vmax = block_all(vhi, sm.u32s, OpMax());
+
+    // ------------------------------------------------------------ intensity
+    if (want_int) {
+        if (wid == 0) {  // coarse exclusive prefix
+            uint32_t c[8], t = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                c[j] = sm.coarse[lane * 8 + j];
+                t += c[j];
+            }
+            uint32_t run = warp_incl_scan(t) - t;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                sm.cpre[lane * 8 + j] = run;
+                run += c[j];
+            }
+            if (lane == 31) sm.cpre[256] = run;
+        }
+        __syncthreads();
+        const double mean = (double)sS / dn;
+        // per-pixel passes: central moments, mad partials, mode, entropy bins
+        const uint32_t nb32 = (uint32_t)cfg.bins;
+        const uint32_t rng = vmax - vmin;
+        double acc[5] = {0, 0, 0, 0, 0};
+        unsigned long long slo = 0, best = 0;
+        uint32_t clo = 0;
+        for (uint32_t i = tid; i < n; i += kBT) {
+            const uint32_t v = S.vals[i];
+            const double d = (double)v - mean, d2 = d * d;
+            acc[0] += d2;
+            acc[1] += d2 * d;
+            acc[2] += d2 * d2;
+            acc[3] += d2 * d2 * d;
+            acc[4] += d2 * d2 * d2;
+            if ((double)v < mean) {
+                slo += v;
+                ++clo;
+            }
+            const unsigned long long key = ((unsigned long long)S.vhist[v] << 16) | (0xffffu - v);
+            best = key > best ? key : best;
+            uint32_t bin = 0;
+            if (rng) {
+                const unsigned long long q = (unsigned long long)nb32 * (v - vmin) / rng;
+                bin = q < nb32 - 1 ? (uint32_t)q : nb32 - 1;
+            }
+            atomicAdd(&S.bins[bin], 1u);
+        }
+#pragma unroll
+        for (int k = 0; k < 5; ++k) acc[k] = block_all(acc[k], sm.f64s, OpAdd());
+        slo = block_all(slo, sm.u64s, OpAdd());
+        clo = block_all(clo, sm.u32s, OpAdd());
+        best = block_all(best, sm.u64s, OpMax());
+        // entropy / uniformity over the bins; bins left zero
+        const double logn = nlog2(dn);
+        double ent = 0;
+        unsigned long long usq = 0;
+        for (uint32_t b = tid; b < nb32; b += kBT) {
+            const uint32_t c = S.bins[b];
+            if (c) {
+                ent += (double)c * (logn - log2_int(c));
+                usq += (unsigned long long)c * c;
+                S.bins[b] = 0u;
+                if (dbg_on) dbg->hist[b] = c;
+            }
+        }
+        ent = block_all(ent, sm.f64s, OpAdd());
+        usq = block_all(usq, sm.u64s, OpAdd());
+        // order statistics (warp 0), shared through sm.red
+        if (wid == 0) {
+            const double median = (n & 1) ? (double)kth_value(n / 2, sm.cpre, S.vhist)
+                                          : 0.5 * ((double)kth_value(n / 2 - 1, sm.cpre, S.vhist) +
+                                                   (double)kth_value(n / 2, sm.cpre, S.vhist));
+            const double pv[6] = {1.0, 10.0, 25.0, 75.0, 90.0, 99.0};
+            double pc[6];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) pc[j] = percentile_h(pv[j], n, sm.cpre, S.vhist);
+            const uint32_t shi = kth_value(n / 2, sm.cpre, S.vhist);
+            const uint32_t M2 = (n & 1) ? 2u * shi : kth_value(n / 2 - 1, sm.cpre, S.vhist) + shi;
+            const uint32_t d_hi = kth_dev_h(n / 2, M2, sm.cpre, S.vhist);
+            const uint32_t d_lo = (n & 1) ? d_hi : kth_dev_h(n / 2 - 1, M2, sm.cpre, S.vhist);
+            const double median_ad = (n & 1) ? 0.5 * (double)d_hi
+                                             : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
+            if (lane == 0) {
+                sm.red[0][0] = median;
+#pragma unroll
+                for (int j = 0; j < 6; ++j) sm.red[0][1 + j] = pc[j];
+                sm.red[0][7] = median_ad;
+            }
+        }
+        __syncthreads();
+        const double median = sm.red[0][0], p10 = sm.red[0][2], p25 = sm.red[0][3];
+        const double p75 = sm.red[0][4], p90 = sm.red[0][5], median_ad = sm.red[0][7];
+        double pct[6];
+#pragma unroll
+        for (int j = 0; j < 6; ++j) pct[j] = sm.red[0][1 + j];
+        __syncthreads();
+        // robust mean absolute deviation over [p10, p90]
+        unsigned long long rsum = 0;
+        uint32_t rn = 0;
+        for (uint32_t i = tid; i < n; i += kBT) {
+            const double x = (double)S.vals[i];
+            if (x >= p10 && x <= p90) {
+                rsum += S.vals[i];
+                ++rn;
+            }
+        }
+        rsum = block_all(rsum, sm.u64s, OpAdd());
+        rn = block_all(rn, sm.u32s, OpAdd());
+        double rmad = 0;
+        if (rn > 0) {
+            const double rmean = (double)rsum / (double)rn;
+            unsigned long long rlo = 0;
+            uint32_t rcl = 0;
+            for (uint32_t i = tid; i < n; i += kBT) {
+                const double x = (double)S.vals[i];
+                if (x >= p10 && x <= p90 && x < rmean) {
+                    rlo += S.vals[i];
+                    ++rcl;
+                }
+            }
+            rlo = block_all(rlo, sm.u64s, OpAdd());
+            rcl = block_all(rcl, sm.u32s, OpAdd());
+            rmad = ((double)(long long)(rsum - 2 * rlo) +
+                    (double)((long long)rcl - (long long)(rn - rcl)) * rmean) / (double)rn;
+        }
+        // value histogram back to zero
+        for (uint32_t i = tid; i < n; i += kBT) S.vhist[S.vals[i]] = 0u;
+
+        // ---- edge set: K = largest 8-connected component, E = 4-connected exterior
+        double e_mean = 0, e_min = 0, e_max = 0, e_std = 0, e_int = 0;
+        {
+            const uint64_t lastm = (w & 63) ? ((1ull << (w & 63)) - 1ull) : ~0ull;
+            uint32_t nr = build_runs(S.rowmask, h, wpr, S, B.RUNMAX, sm.scan);
+            bool ok = nr != ~0u;
+            if (ok) {
+                unite_runs(h, 1, S);
+                for (uint32_t q = tid; q < nr; q += kBT) S.rsize[q] = 0u;
+                __syncthreads();
+                for (uint32_t q = tid; q < nr; q += kBT)
+                    atomicAdd(&S.rsize[S.parent[q]], (uint32_t)(S.re[q] - S.rs[q] + 1));
+                __syncthreads();
+                unsigned long long bk = 0;
+                for (uint32_t q = tid; q < nr; q += kBT)
+                    if (S.parent[q] == q) {
+                        const unsigned long long key = ((unsigned long long)S.rsize[q] << 32) |
+                                                       (0xffffffffu - q);
+                        bk = key > bk ? key : bk;
+                    }
+                bk = block_all(bk, sm.u64s, OpMax());
+                const uint32_t broot = 0xffffffffu - (uint32_t)(bk & 0xffffffffu);
+                for (uint32_t wi = tid; wi < nw; wi += kBT) S.kmask[wi] = 0ull;
+                __syncthreads();
+                for (int y = tid; y < h; y += kBT)
+                    for (uint32_t q = S.runoff[y]; q < S.runoff[y + 1]; ++q)
+                        if (S.parent[q] == broot) set_bits(S.kmask + (size_t)y * wpr, S.rs[q], S.re[q]);
+                __syncthreads();
+                // free cells of the window (not in K) -> 4-connected exterior
+                for (uint32_t wi = tid; wi < nw; wi += kBT)
+                    S.emask[wi] = ~S.kmask[wi] & ((int)(wi % wpr) == wpr - 1 ? lastm : ~0ull);
+                __syncthreads();
+                const uint32_t nf = build_runs(S.emask, h, wpr, S, B.RUNMAX, sm.scan);
+                ok = nf != ~0u;
+                if (ok) {
+                    unite_runs(h, 0, S);
+                    for (uint32_t q = tid; q < nf; q += kBT) S.rsize[q] = 0u;
+                    __syncthreads();
+                    for (int y = tid; y < h; y += kBT)
+                        for (uint32_t q = S.runoff[y]; q < S.runoff[y + 1]; ++q)
+                            if (y == 0 || y == h - 1 || S.rs[q] == 0 || S.re[q] == w - 1)
+                                S.rsize[S.parent[q]] = 1u;
+                    __syncthreads();
+                    for (uint32_t wi = tid; wi < nw; wi += kBT) S.emask[wi] = 0ull;
+                    __syncthreads();
+                    for (int y = tid; y < h; y += kBT)
+                        for (uint32_t q = S.runoff[y]; q < S.runoff[y + 1]; ++q)
+                            if (S.rsize[S.parent[q]]) set_bits(S.emask + (size_t)y * wpr, S.rs[q], S.re[q]);
+                    __syncthreads();
+                }
+            }
+            if (!ok) {
+                if (tid == 0) atomicOr(&ctl->error, kErrRuns);
+                return;
+            }
+            // edge = K & (4-neighbour in E, or on the window border); exact integer sums
+            unsigned long long es = 0, esq = 0;
+            uint32_t en = 0, emn = 0xffffffffu, emx = 0;
+            for (uint32_t wi = tid; wi < nw; wi += kBT) {
+                const int y = (int)(wi / wpr), k = (int)(wi % wpr);
+                const uint64_t kk = S.kmask[wi];
+                uint32_t cnt = 0;
+                if (kk) {
+                    const uint64_t e = S.emask[wi];
+                    const uint64_t el = k ? S.emask[wi - 1] : 0ull, er = k + 1 < wpr ? S.emask[wi + 1] : 0ull;
+                    uint64_t g = (e << 1) | (el >> 63) | (e >> 1) | (er << 63);
+                    if (y > 0) g |= S.emask[wi - wpr];
+                    if (y + 1 < h) g |= S.emask[wi + wpr];
+                    if (y == 0 || y == h - 1) g = ~0ull;
+                    if (k == 0) g |= 1ull;
+                    if (k == (w - 1) >> 6) g |= 1ull << ((w - 1) & 63);
+                    uint64_t ed = kk & g;
+                    cnt = __popcll(ed);
+                    const uint64_t m = S.rowmask[wi];
+                    const uint32_t base = S.wordoff[wi];
+                    while (ed) {
+                        const int b = __ffsll((long long)ed) - 1;
+                        ed &= ed - 1;
+                        const uint32_t v = S.vals[base + __popcll(m & ((1ull << b) - 1ull))];
+                        es += v;
+                        esq += (unsigned long long)v * v;
+                        emn = min(emn, v);
+                        emx = max(emx, v);
+                    }
+                }
+                en += cnt;
+                if (dbg_on) S.tmpw[wi] = cnt;
+            }
+            es = block_all(es, sm.u64s, OpAdd());
+            esq = block_all(esq, sm.u64s, OpAdd());
+            en = block_all(en, sm.u32s, OpAdd());
+            emn = block_all(emn, sm.u32s, OpMin());
+            emx = block_all(emx, sm.u32s, OpMax());
+            if (en) {
+                const double den = (double)en;
+                e_mean = (double)es / den;
+                e_min = (double)emn;
+                e_max = (double)emx;
+                e_int = (double)es;
+                const unsigned __int128 var =
+                    (unsigned __int128)en * esq - (unsigned __int128)es * es;  // n^2 var, exact
+                e_std = sqrt((double)var / (den * den));
+            }
+            if (dbg_on) {  // edge pixels in row-major order
+                __syncthreads();
+                const uint32_t ne = block_exscan(S.tmpw, nw, sm.scan);
+                for (uint32_t wi = tid; wi < nw; wi += kBT) {
+                    const int y = (int)(wi / wpr), k = (int)(wi % wpr);
+                    const uint64_t kk = S.kmask[wi];
+                    if (!kk) continue;
+                    const uint64_t e = S.emask[wi];
+                    const uint64_t el = k ? S.emask[wi - 1] : 0ull, er = k + 1 < wpr ? S.emask[wi + 1] : 0ull;
+                    uint64_t g = (e << 1) | (el >> 63) | (e >> 1) | (er << 63);
+                    if (y > 0) g |= S.emask[wi - wpr];
+                    if (y + 1 < h) g |= S.emask[wi + wpr];
+                    if (y == 0 || y == h - 1) g = ~0ull;
+                    if (k == 0) g |= 1ull;
+                    if (k == (w - 1) >> 6) g |= 1ull << ((w - 1) & 63);
+                    uint64_t ed = kk & g;
+                    uint32_t j = S.tmpw[wi];
+                    while (ed) {
+                        const int b = __ffsll((long long)ed) - 1;
+                        ed &= ed - 1;
+                        if (j < dbg->cap_edge) {
+                            dbg->edge_xy[2 * j] = (int32_t)(gx0 + k * 64 + b);
+                            dbg->edge_xy[2 * j + 1] = (int32_t)(gy0 + y);
+                        }
+                        ++j;
+                    }
+                }
+                if (tid == 0) *dbg->n_edge = ne;
+            }
+        }
+        // ---- intensity columns (intensity_features.cpp:42-215), as the S kernel
+        if (wid == 0) {
+            double wcx = 0, wcy = 0;
+            if (sS > 0) {
+                wcx = (double)((unsigned long long)gx0 * sS + sXI) / (double)sS;
+                wcy = (double)((unsigned long long)gy0 * sS + sYI) / (double)sS;
+            }
+            const double m2 = acc[0] / dn, m3 = acc[1] / dn, m4 = acc[2] / dn, m5 = acc[3] / dn,
+                         m6 = acc[4] / dn;
+            const double mad = ((double)(long long)(sS - 2 * slo) +
+                                (double)((long long)clo - (long long)(n - clo)) * mean) / dn;
+            const double var = n > 1 ? m2 * dn / (dn - 1.0) : 0.0;
+            double skew = 0, kurt = 0, hsk = 0, hfl = 0;
+            if (m2 > 0) {
+                const double r2 = sqrt(m2);
+                skew = m3 / (m2 * r2);
+                kurt = m4 / (m2 * m2);
+                hsk = m5 / (m2 * m2 * r2);
+                hfl = m6 / (m2 * m2 * m2);
+            }
+            const double mode = (double)(0xffffu - (uint32_t)(best & 0xffffu));
+            const double energy = (double)sQ, sdev = sqrt(var), iqr = p75 - p25;
+            const double mn = (double)vmin, mxv = (double)vmax;
+            double o = 0;
+            switch (lane) {
+                case 0: o = mean; break;
+                case 1: o = median; break;
+                case 2: o = mode; break;
+                case 3: o = mn; break;
+                case 4: o = mxv; break;
+                case 5: o = mxv - mn; break;
+                case 6: o = var; break;
+                case 7: o = m2; break;
+                case 8: o = sdev; break;
+                case 9: o = sqrt(m2); break;
+                case 10: o = mad; break;
+                case 11: o = median_ad; break;
+                case 12: o = rmad; break;
+                case 13: o = iqr; break;
+                case 14: o = pct[0]; break;
+                case 15: o = pct[1]; break;
+                case 16: o = pct[2]; break;
+                case 17: o = pct[3]; break;
+                case 18: o = pct[4]; break;
+                case 19: o = pct[5]; break;
+                case 20: o = skew; break;
+                case 21: o = kurt; break;
+                case 22: o = m2 > 0 ? kurt - 3.0 : 0.0; break;
+                case 23: o = hsk; break;
+                case 24: o = hfl; break;
+                case 25: o = energy; break;
+                case 26: o = sqrt(energy / dn); break;
+                case 27: o = ent / dn; break;
+                case 28: o = (double)usq / (dn * dn); break;
+                case 29: o = (p75 + p25) != 0 ? iqr / (p75 + p25) : 0.0; break;
+                case 30: o = mean != 0 ? sdev / mean : 0.0; break;
+                default: o = (double)sS; break;
+            }
+            double* oi = orow + cfg.col_int;
+            oi[lane] = o;
+            if (lane < 7) {
+                const double t[7] = {e_mean, e_min, e_max, e_std, e_int, wcx, wcy};
+                double v = t[0];
+#pragma unroll
+                for (int k = 1; k < 7; ++k)
+                    if ((int)lane == k) v = t[k];
+                oi[32 + lane] = v;
+            }
+        }
+        __syncthreads();
+    }
+
+    // ------------------------------------------------------------- moments
+    if (want_mom) {
+        // integer anchors (rounded centroids); binary uses unit mass, weighted I
+        const long long nb_ = (long long)n;
+        const long long axb = (2 * (long long)sX + nb_) / (2 * nb_);
+        const long long ayb = (2 * (long long)sY + nb_) / (2 * nb_);
+        const long long W = (long long)sS;
+        const long long axw = W > 0 ? (2 * (long long)sXI + W) / (2 * W) : 0;
+        const long long ayw = W > 0 ? (2 * (long long)sYI + W) / (2 * W) : 0;
+        double acc[32];
+#pragma unroll
+        for (int k = 0; k < 32; ++k) acc[k] = 0;
+        // warp per row: separable row sums of w dx^p, then times dy^q
+        for (int y = wid; y < h; y += kBW) {
+            const uint32_t a = S.wordoff[(size_t)y * wpr], e = S.wordoff[(size_t)(y + 1) * wpr];
+            double rb0 = 0, rb1 = 0, rb2 = 0, rb3 = 0, rw0 = 0, rw1 = 0, rw2 = 0, rw3 = 0;
+            for (uint32_t i = a + lane; i < e; i += 32) {
+                const long long x = (long long)(S.xy[i] & 0xffffu);
+                const double wv = (double)S.vals[i];
+                const double db = (double)(x - axb), dw = (double)(x - axw);
+                const double db2 = db * db, dw2 = dw * dw;
+                rb0 += 1.0;
+                rb1 += db;
+                rb2 += db2;
+                rb3 += db2 * db;
+                rw0 += wv;
+                rw1 += wv * dw;
+                rw2 += wv * dw2;
+                rw3 += wv * dw2 * dw;
+            }
+            const double yb = (double)((long long)y - ayb), yw = (double)((long long)y - ayw);
+            const double rb[4] = {rb0, rb1, rb2, rb3};
+            const double rw[4] = {rw0, rw1, rw2, rw3};
+            const double qb[4] = {1.0, yb, yb * yb, yb * yb * yb};
+            const double qw[4] = {1.0, yw, yw * yw, yw * yw * yw};
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    acc[p * 4 + q] += rb[p] * qb[q];
+                    acc[16 + p * 4 + q] += rw[p] * qw[q];
+                }
+        }
+        const double Nw = reduce_scatter32(acc);  // lane i: this warp's N_i
+        sm.red[wid][lane] = Nw;
+        __syncthreads();
+        if (wid == 0) {
+            double N = 0;
+            for (int k = 0; k < kBW; ++k) N += sm.red[k][lane];
+            moments_epilogue(N, dn, n, sS, sX, sY, sXI, sYI, axb, ayb, axw, ayw, gx0, gy0,
+                             orow + cfg.col_mom);
+        }
+        __syncthreads();
+    }
+
+    // ---------------------------------------------------------------- glcm
+    if (want_glcm) {
+        const int ng = cfg.ng, A = cfg.n_angles;
+        const bool sym = cfg.symmetric != 0;
+        const unsigned long long span = (unsigned long long)(vmax - vmin) + 1ull;
+        for (uint32_t i = tid; i < n; i += kBT) {
+            uint32_t lv = 0;
+            if (vmax > vmin) {
+                const unsigned long long q = (unsigned long long)ng * (S.vals[i] - vmin) / span;
+                lv = q < (unsigned long long)(ng - 1) ? (uint32_t)q : (uint32_t)(ng - 1);
+            }
+            S.lvl[i] = (uint8_t)lv;
+        }
+        __syncthreads();
+        double sacc = 0;
+        for (int a = 0; a < A; ++a) {
+            const int ddx = cfg.dx[a], ddy = cfg.dy[a];
+            for (int k = tid; k < 256; k += kBT) {
+                sm.px[k] = 0u;
+                sm.py[k] = 0u;
+                sm.pdif[k] = 0u;
+            }
+            for (int k = tid; k < 512; k += kBT) sm.psum[k] = 0u;
+            __syncthreads();
+            // pairs (x, y) -> (x + dx, y + dy), both in the ROI
+            uint32_t npr = 0;
+            for (uint32_t i = tid; i < n; i += kBT) {
+                const uint32_t p = S.xy[i];
+                const int x = (int)(p & 0xffffu), y = (int)(p >> 16);
+                const int nx = x + ddx, ny = y + ddy;
+                if (nx >= 0 && nx < w && ny >= 0 && ny < h) {
+                    const uint32_t wi = (uint32_t)ny * wpr + (uint32_t)(nx >> 6);
+                    const uint64_t m = S.rowmask[wi];
+                    if ((m >> (nx & 63)) & 1ull) {
+                        ++npr;
+                        const uint32_t jn = S.wordoff[wi] + __popcll(m & ((1ull << (nx & 63)) - 1ull));
+                        const uint32_t la = S.lvl[i], lb = S.lvl[jn];
+                        const uint32_t key = sym ? min(la, lb) * (uint32_t)ng + max(la, lb)
+                                                 : la * (uint32_t)ng + lb;
+                        atomicAdd(&S.ghist[key], 1u);
+                    }
+                }
+            }
+            const unsigned long long np = block_all((unsigned long long)npr, sm.u64s, OpAdd());
+            const uint32_t ncells = (uint32_t)ng * (uint32_t)ng;
+            if (dbg_on && dbg->pairs && tid == 0) dbg->pairs[a] = np;
+            double st[29];
+#pragma unroll
+            for (int k = 0; k < 29; ++k) st[k] = 0;
+            if (np > 0) {
+                const double T = sym ? 2.0 * (double)np : (double)np;
+                const double logT = nlog2(T);
+                unsigned long long s2 = 0, sa = 0;
+                uint32_t jm = 0;
+                double el = 0;
+                // dense pass in fixed thread order (deterministic fp64 entropy sum)
+                for (uint32_t key = tid; key < ncells; key += kBT) {
+                    const uint32_t c = S.ghist[key];
+                    if (!c) continue;
+                    S.ghist[key] = 0u;  // leave the histogram empty
+                    const uint32_t ga = key / (uint32_t)ng, gb = key % (uint32_t)ng;
+                    const bool off = sym && ga != gb;
+                    const uint32_t cc = (sym && !off) ? 2u * c : c;
+                    const uint32_t mcc = off ? 2u * cc : cc;
+                    s2 += (unsigned long long)mcc * cc;
+                    sa += (unsigned long long)((ga + 1) * (gb + 1)) * mcc;
+                    jm = max(jm, cc);
+                    el += (double)mcc * (logT - log2_int(cc));
+                    atomicAdd(&sm.px[ga], cc);
+                    if (off) atomicAdd(&sm.px[gb], cc);
+                    if (!sym) atomicAdd(&sm.py[gb], cc);
+                    atomicAdd(&sm.psum[ga + gb], mcc);
+                    atomicAdd(&sm.pdif[ga > gb ? ga - gb : gb - ga], mcc);
+                    if (dbg_on && dbg->glcm) {
+                        dbg->glcm[((size_t)a * ng + ga) * ng + gb] = cc;
+                        if (off) dbg->glcm[((size_t)a * ng + gb) * ng + ga] = cc;
+                    }
+                }
+                s2 = block_all(s2, sm.u64s, OpAdd());
+                sa = block_all(sa, sm.u64s, OpAdd());
+                jm = block_all(jm, sm.u32s, OpMax());
+                el = block_all(el, sm.f64s, OpAdd());
+                if (wid == 0)
+                    haralick_finish(sm.px, sym ? sm.px : sm.py, sm.psum, sm.pdif, ng, sym, T, logT, s2,
+                                    sa, jm, el, st);
+            }
+            if (wid == 0) {
+                double mine = 0;
+#pragma unroll
+                for (int k = 0; k < 29; ++k)
+                    if ((int)lane == k) mine = st[k];
+                if (lane < 29) {
+                    orow[cfg.col_glcm + lane * (A + 1) + a] = mine;
+                    sacc += mine;
+                }
+            }
+            __syncthreads();
+        }
+        if (wid == 0 && lane < 29) orow[cfg.col_glcm + lane * (A + 1) + A] = sacc / (double)A;
+    }
+    __syncthreads();
+}
+
+__global__ void __launch_bounds__(kBT) k_roi_b(DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
+                                               double* out, const DebugOut* dbg, uint8_t* scratch,
+                                               BLayout B) {
+    __shared__ BShared sm;
+    const BSlab S = bslab(scratch + (size_t)blockIdx.x * B.bytes, B);
+    const uint32_t nl = ctl->class_count[kClassL];
+    const uint32_t total = nl + ctl->overflow_count;  // S kernels have finished
+    for (;;) {
+        if (threadIdx.x == 0) sm.job = atomicAdd(&ctl->class_next[kClassL], 1u);
+        __syncthreads();
+        const uint32_t idx = sm.job;
+        __syncthreads();
+        if (idx >= total) break;
+        const uint32_t r = idx < nl ? rl.cls_list[kClassL][idx] : rl.overflow[idx - nl];
+        const uint32_t w = rl.w[r], h = rl.h[r];
+        if (h > B.H || (w + 63) / 64 > B.WPR || rl.n[r] > (unsigned long long)B.NMAX) {
+            if (threadIdx.x == 0) atomicOr(&ctl->error, kErrCapacity);
+            continue;
+        }
+        process_b(r, img, rl, ctl, cfg, out, dbg, S, B, sm);
+    }
+}
+
+}  // namespace
+
+cudaError_t roi_b_setup() {
+    k_init_log2_tab<<<4, 256>>>();
+    return cudaDeviceSynchronize();
+}
+
+BLayout make_blayout(uint32_t H, uint32_t WPR, uint32_t NMAX, uint32_t RUNMAX, uint32_t NB) {
+    BLayout B{};
+    size_t o = 0;
+    auto take = [&](size_t bytes) {
+        const size_t at = o;
+        o = (o + bytes + 255) & ~(size_t)255;
+        return at;
+    };
+    const size_t NW = (size_t)H * WPR;
+    B.rowmask = take(NW * 8);
+    B.kmask = take(NW * 8);
+    B.emask = take(NW * 8);
+    B.wordoff = take((NW + 1) * 4);
+    B.tmpw = take((NW + 1) * 4);
+    B.xy = take((size_t)NMAX * 4);
+    B.vals = take((size_t)NMAX * 2);
+    B.lvl = take((size_t)NMAX);
+    B.vhist = take(65536 * 4);
+    B.runoff = take(((size_t)H + 1) * 4);
+    B.rs = take((size_t)RUNMAX * 2);
+    B.re = take((size_t)RUNMAX * 2);
+    B.parent = take((size_t)RUNMAX * 4);
+    B.rsize = take((size_t)RUNMAX * 4);
+    B.bins = take((size_t)NB * 4);
+    B.ghist = take(65536 * 4);
+    B.bytes = o;
+    B.H = H;
+    B.WPR = WPR;
+    B.NMAX = NMAX;
+    B.RUNMAX = RUNMAX;
+    B.NB = NB;
+    return B;
+}
+
+void launch_roi_b(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
+                  double* out, const DebugOut* dbg, uint8_t* scratch, const BLayout& B) {
+    k_roi_b<<<grid, kBT, 0, s>>>(img, rl, ctl, cfg, out, dbg, scratch, B);
+}
+
+}  // namespace fxg

@@ -197,3 +197,63 @@ def test_moments_vs_exact_rational_truth(ctx):
                     assert abs(got - ex) <= 1e-12 * (abs(ex) + nat[k, g, a, b]), (lab, pre, a, b)
                 raw = float(sum(int(c) * int(x) ** 3 * int(y) ** 3 for c, x, y in zip(w, xs, ys)))
                 assert abs(gv[k, cols.index(f"moments_{pre}m33")] - raw) <= 1e-14 * abs(raw)
+
+
+# ---- large-ROI path (k_roi_b: one CTA per ROI) ------------------------------
+
+def _large_masks():
+    """Windows > 64: big disc/ring with holes, two equal-size components of one
+    label (row-major tie-break), a spiral-ish comb, a thin diagonal, sparse pixels."""
+    yy, xx = np.mgrid[0:300, 0:280]
+    L = np.zeros((300, 280), np.uint16)
+    r2 = (xx - 140) ** 2 + (yy - 150) ** 2
+    L[(r2 <= 120 ** 2) & (r2 >= 30 ** 2)] = 5                 # ring: one big hole
+    L[(r2 <= 12 ** 2)] = 5                                     # island inside the hole
+    L[((xx - 140) ** 2 + (yy - 150) ** 2 <= 60 ** 2) & ((xx + yy) % 17 == 0)] = 0  # slits
+    L[5:25, 5:80] = 7
+    L[270:290, 190:265] = 7                                    # equal-size twin
+    for k in range(0, 260, 8):
+        L[k:k + 4, 270:278] = 9                                # comb teeth
+    L[0:300:1, 279] = 9
+    for d in range(0, 250):
+        L[40 + d // 2, 10 + d // 3] = 11                        # thin diagonal
+    rng = np.random.default_rng(4)
+    L[rng.integers(0, 300, 400), rng.integers(0, 280, 400)] = 13  # scattered pixels
+    return L
+
+
+@pytest.mark.parametrize("profile", ["default", "performance", "ibsi-like"])
+@pytest.mark.parametrize("fill", ["uniform", "levels", "constant"])
+def test_large_rois_cta_path(ctx, oracle, profile, fill):
+    L = _large_masks()
+    I = {"uniform": inputs.uniform(L.shape, 6), "levels": inputs.per_roi_levels(L, 2),
+         "constant": np.full(L.shape, 321, np.uint16)}[fill]
+    check(ctx, oracle, I, L, GROUPS, profile)
+
+
+def test_large_rois_cta_debug_bit_exact(ctx, oracle):
+    """Histogram counts, edge pixel set and GLCM counts of large ROIs, ng 64 and 256."""
+    L = _large_masks()
+    I = inputs.uniform(L.shape, 8)
+    for profile, bins in [("default", 16), ("ibsi-like", 300)]:
+        p = fx.make_params(profile, histogram_bins=bins)
+        for lab in [5, 7, 9, 11, 13]:
+            ys, xs = np.nonzero(L == lab)
+            vs = I[ys, xs]
+            hist, edge, glcm, pairs = ctx.debug_roi(I, L, int(lab), p)
+            assert np.array_equal(hist, oracle.intensity_hist(vs, bins)), lab
+            pts = oracle.trace_contour(xs, ys)
+            assert set(map(tuple, edge.tolist())) == set(map(tuple, pts.tolist())), lab
+            for a, ang in enumerate(sorted(p.angles[: p.n_angles])):
+                cnt, pc = oracle.glcm_counts(xs, ys, vs, p.ng, p.offset, ang, p.symmetric)
+                assert pairs[a] == pc, (lab, ang)
+                assert np.array_equal(glcm[a].astype(np.uint64), cnt), (lab, ang)
+
+
+def test_large_rois_deterministic(ctx):
+    L = _large_masks()
+    I = inputs.uniform(L.shape, 1)
+    a = ctx.featurize(I, L, GROUPS)
+    for _ in range(4):
+        b = ctx.featurize(I, L, GROUPS)
+        assert np.array_equal(a[1], b[1])
