@@ -33,7 +33,8 @@ void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
                   const CUtensorMap& tmap72, int tma40, int tma72, DevImage img, RoiList rl,
                   Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg);
 cudaError_t roi_b_setup();
-BLayout make_blayout(uint32_t H, uint32_t WPR, uint32_t NMAX, uint32_t RUNMAX, uint32_t NB);
+BLayout make_blayout(uint32_t H, uint32_t WPR, uint32_t NMAX, uint32_t RUNMAX, uint32_t NB,
+                     unsigned long long CELLS);
 void launch_roi_b(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                   double* out, const DebugOut* dbg, uint8_t* scratch, const BLayout& B);
 }  // namespace fxg
@@ -359,7 +360,7 @@ BLayout b_layout(const Control& h, int bins) {
     const unsigned long long cells = std::max<unsigned long long>(h.l_max_cells, (unsigned long long)kSW * kSH);
     const uint32_t RUNMAX =
         (uint32_t)std::min<unsigned long long>(cells / 2 + H + 64, 64ull << 20);
-    return make_blayout(H, WPR, NMAX, RUNMAX, (uint32_t)std::max(bins, 2));
+    return make_blayout(H, WPR, NMAX, RUNMAX, (uint32_t)std::max(bins, 2), cells);
 }
 
 struct DebugHost {

@@ -20,6 +20,9 @@ namespace fxg {
 #ifndef FXG_SCAN_WAVES
 #define FXG_SCAN_WAVES 16
 #endif
+#ifndef FXG_B_MINB
+#define FXG_B_MINB 2  // large-ROI kernel: min CTAs per SM (register cap; 2: 7.1 -> 5.2 ms on C5-regime)
+#endif
 #ifndef FXG_SCAN_ROWS
 #define FXG_SCAN_ROWS 32
 #endif

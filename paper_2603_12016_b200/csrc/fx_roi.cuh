@@ -207,9 +207,10 @@ __device__ __forceinline__ void moments_epilogue(double N, double dn, unsigned l
 // Byte offsets of one CTA's global scratch slab in the large-ROI kernel (fx_roi_b.cu),
 // sized on the host from the largest L window / pixel count of the launch.
 struct BLayout {
-    size_t rowmask, kmask, emask, wordoff, tmpw, xy, vals, lvl, vhist, runoff, rs, re, parent,
+    size_t rowmask, kmask, emask, wordoff, tmpw, xy, vals, lraster, lvl, vhist, runoff, rs, re, parent,
         rsize, bins, ghist;
     size_t bytes;
+    unsigned long long RCAP;  // level-raster capacity (cells): dense windows only
     uint32_t H, WPR, NMAX, RUNMAX, NB;
 };
 

@@ -24,12 +24,27 @@
 #include "fx_glcm.cuh"
 #include "fx_roi.cuh"
 
+#ifdef FXG_PHASE_TIMING
+__device__ unsigned long long g_phase_clk_b[8];
+#define BT_DECL long long bt_t_ = clock64();
+#define BT(k)                                                                  \
+    do {                                                                       \
+        const long long t_ = clock64();                                        \
+        if (threadIdx.x == 0) atomicAdd(&g_phase_clk_b[k], (unsigned long long)(t_ - bt_t_)); \
+        bt_t_ = t_;                                                            \
+    } while (0)
+#else
+#define BT_DECL
+#define BT(k)
+#endif
+
 namespace fxg {
 
 namespace {
 
 constexpr int kBT = 512;
 constexpr int kBW = kBT / 32;
+constexpr uint32_t kSmemCells = 128 * 128;  // shared GLCM histogram up to ng = 128 (64 KB)
 
 __device__ __forceinline__ unsigned warp_id() { return threadIdx.x >> 5; }
 
@@ -167,6 +182,7 @@ struct BSlab {
     uint64_t *rowmask, *kmask, *emask;
     uint32_t *wordoff, *tmpw, *xy;
     uint16_t* vals;
+    uint16_t* lraster;
     uint8_t* lvl;
     uint32_t *vhist, *runoff, *parent, *rsize, *bins, *ghist;
     uint16_t *rs, *re;
@@ -181,6 +197,7 @@ __device__ __forceinline__ BSlab bslab(uint8_t* base, const BLayout& B) {
     S.tmpw = (uint32_t*)(base + B.tmpw);
     S.xy = (uint32_t*)(base + B.xy);
     S.vals = (uint16_t*)(base + B.vals);
+    S.lraster = (uint16_t*)(base + B.lraster);
     S.lvl = base + B.lvl;
     S.vhist = (uint32_t*)(base + B.vhist);
     S.runoff = (uint32_t*)(base + B.runoff);
@@ -286,7 +303,7 @@ struct BShared {
 
 __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Control* ctl,
                           const FeatCfg& cfg, double* __restrict__ out, const DebugOut* dbg,
-                          const BSlab& S, const BLayout& B, BShared& sm) {
+                          const BSlab& S, const BLayout& B, BShared& sm, uint32_t* dyn) {
     const unsigned tid = threadIdx.x, lane = lane_id(), wid = warp_id();
     const uint32_t label = rl.label[r];
     const int w = (int)rl.w[r], h = (int)rl.h[r];
@@ -298,6 +315,7 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
     const bool dbg_on = dbg != nullptr && dbg->label == label;
     const bool want_int = cfg.col_int >= 0, want_mom = cfg.col_mom >= 0, want_glcm = cfg.col_glcm >= 0;
 
+    BT_DECL
     // ---- membership words (warp per 64-column word) and popcounts
     for (uint32_t wi = wid; wi < nw; wi += kBW) {
         const int y = (int)(wi / wpr), k = (int)(wi % wpr);
@@ -315,6 +333,7 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
     __syncthreads();
     const uint32_t n = block_exscan(S.wordoff, nw, sm.scan);
     const double dn = (double)n;
+    BT(0);
 
     // ---- pixel list (row-major), intensities, exact integer sums, value histogram
     unsigned long long sS = 0, sQ = 0, sX = 0, sY = 0, sXI = 0, sYI = 0;
@@ -356,6 +375,7 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
     sYI = block_all(sYI, sm.u64s, OpAdd());
     const uint32_t vmin = block_all(vlo, sm.u32s, OpMin());
     const uint32_t vmax = block_all(vhi, sm.u32s, OpMax());
+    BT(1);
 
     // ------------------------------------------------------------ intensity
     if (want_int) {
@@ -483,6 +503,7 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
         }
         // value histogram back to zero
         for (uint32_t i = tid; i < n; i += kBT) S.vhist[S.vals[i]] = 0u;
+        BT(2);
 
         // ---- edge set: K = largest 8-connected component, E = 4-connected exterior
         double e_mean = 0, e_min = 0, e_max = 0, e_std = 0, e_int = 0;
@@ -689,6 +710,7 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
         __syncthreads();
     }
 
+    BT(3);
     // ------------------------------------------------------------- moments
     if (want_mom) {
         // integer anchors (rounded centroids); binary uses unit mass, weighted I
@@ -698,42 +720,37 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
         const long long W = (long long)sS;
         const long long axw = W > 0 ? (2 * (long long)sXI + W) / (2 * W) : 0;
         const long long ayw = W > 0 ? (2 * (long long)sYI + W) / (2 * W) : 0;
-        double acc[32];
-#pragma unroll
-        for (int k = 0; k < 32; ++k) acc[k] = 0;
-        // warp per row: separable row sums of w dx^p, then times dy^q
+        // warp per row: separable row sums of w dx^p (warp-reduced), then lane i
+        // accumulates its own moment N_i += rowsum_p * dy^q (i: grp<<4 | p<<2 | q)
+        const int grp = lane >> 4, pp = (lane >> 2) & 3, qq = lane & 3;
+        double acc = 0;
         for (int y = wid; y < h; y += kBW) {
             const uint32_t a = S.wordoff[(size_t)y * wpr], e = S.wordoff[(size_t)(y + 1) * wpr];
-            double rb0 = 0, rb1 = 0, rb2 = 0, rb3 = 0, rw0 = 0, rw1 = 0, rw2 = 0, rw3 = 0;
+            double r8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // b^0..3, w b^0..3
             for (uint32_t i = a + lane; i < e; i += 32) {
                 const long long x = (long long)(S.xy[i] & 0xffffu);
                 const double wv = (double)S.vals[i];
                 const double db = (double)(x - axb), dw = (double)(x - axw);
                 const double db2 = db * db, dw2 = dw * dw;
-                rb0 += 1.0;
-                rb1 += db;
-                rb2 += db2;
-                rb3 += db2 * db;
-                rw0 += wv;
-                rw1 += wv * dw;
-                rw2 += wv * dw2;
-                rw3 += wv * dw2 * dw;
+                r8[0] += 1.0;
+                r8[1] += db;
+                r8[2] += db2;
+                r8[3] += db2 * db;
+                r8[4] += wv;
+                r8[5] += wv * dw;
+                r8[6] += wv * dw2;
+                r8[7] += wv * dw2 * dw;
             }
-            const double yb = (double)((long long)y - ayb), yw = (double)((long long)y - ayw);
-            const double rb[4] = {rb0, rb1, rb2, rb3};
-            const double rw[4] = {rw0, rw1, rw2, rw3};
-            const double qb[4] = {1.0, yb, yb * yb, yb * yb * yb};
-            const double qw[4] = {1.0, yw, yw * yw, yw * yw * yw};
+            warp_sum8(r8);
+            const double dy = grp ? (double)((long long)y - ayw) : (double)((long long)y - ayb);
+            double rp = r8[0];
 #pragma unroll
-            for (int p = 0; p < 4; ++p)
-#pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    acc[p * 4 + q] += rb[p] * qb[q];
-                    acc[16 + p * 4 + q] += rw[p] * qw[q];
-                }
+            for (int k = 1; k < 8; ++k)
+                if (k == grp * 4 + pp) rp = r8[k];
+            const double qy = qq == 0 ? 1.0 : qq == 1 ? dy : qq == 2 ? dy * dy : dy * dy * dy;
+            acc += rp * qy;
         }
-        const double Nw = reduce_scatter32(acc);  // lane i: this warp's N_i
-        sm.red[wid][lane] = Nw;
+        sm.red[wid][lane] = acc;
         __syncthreads();
         if (wid == 0) {
             double N = 0;
@@ -744,23 +761,70 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
         __syncthreads();
     }
 
+    BT(4);
     // ---------------------------------------------------------------- glcm
     if (want_glcm) {
         const int ng = cfg.ng, A = cfg.n_angles;
         const bool sym = cfg.symmetric != 0;
         const unsigned long long span = (unsigned long long)(vmax - vmin) + 1ull;
-        for (uint32_t i = tid; i < n; i += kBT) {
-            uint32_t lv = 0;
-            if (vmax > vmin) {
-                const unsigned long long q = (unsigned long long)ng * (S.vals[i] - vmin) / span;
-                lv = q < (unsigned long long)(ng - 1) ? (uint32_t)q : (uint32_t)(ng - 1);
+        // dense windows (cells <= raster capacity, ~4 n): a level raster of the window
+        // (u16, kNoLevel outside the ROI) lets pair counting walk window cells
+        // coalesced with one load per neighbour; sparse windows (multi-component ROIs
+        // spread over a large bbox) walk the pixel list instead
+        constexpr uint16_t kNoLevel = 0xffffu;
+        const uint32_t cells = (uint32_t)w * (uint32_t)h;
+        const bool dense = (unsigned long long)w * h <= B.RCAP;
+        auto level = [&](uint32_t v) -> uint32_t {
+            if (vmax <= vmin) return 0u;
+            const unsigned long long q = (unsigned long long)ng * (v - vmin) / span;
+            return q < (unsigned long long)(ng - 1) ? (uint32_t)q : (uint32_t)(ng - 1);
+        };
+        if (dense) {
+            for (uint32_t c = tid; c < cells; c += kBT) {
+                const uint32_t y = c / (uint32_t)w, x = c - y * (uint32_t)w;
+                uint16_t lv = kNoLevel;
+                if ((S.rowmask[y * wpr + (x >> 6)] >> (x & 63)) & 1ull)
+                    lv = (uint16_t)level(img.I[(size_t)(y0 + y) * img.pitch + x0 + x]);
+                S.lraster[c] = lv;
             }
-            S.lvl[i] = (uint8_t)lv;
+        } else {
+            for (uint32_t i = tid; i < n; i += kBT) S.lvl[i] = (uint8_t)level(S.vals[i]);
+        }
+        __syncthreads();
+        BT(5);
+        // pair histograms: shared memory when ng*ng fits (kept zero), else the slab's.
+        // Dense windows with ng <= 64 and <= 4 angles count every angle in one pass
+        // over the cells (4 shared histograms of 64 x 64)
+        const bool fused = dense && ng <= 64 && A <= 4;
+        uint32_t npa0 = 0, npa1 = 0, npa2 = 0, npa3 = 0;
+        if (fused) {
+            const uint32_t ngu = (uint32_t)ng;
+            for (uint32_t c = tid; c < cells; c += kBT) {
+                const uint32_t la = S.lraster[c];
+                if (la == kNoLevel) continue;
+                const int y = (int)(c / (uint32_t)w), x = (int)(c - (uint32_t)y * (uint32_t)w);
+#pragma unroll
+                for (int a = 0; a < 4; ++a) {
+                    if (a >= A) break;
+                    const int nx = x + cfg.dx[a], ny = y + cfg.dy[a];
+                    if (nx < 0 || nx >= w || ny < 0 || ny >= h) continue;
+                    const uint32_t lb = S.lraster[(uint32_t)ny * (uint32_t)w + (uint32_t)nx];
+                    if (lb == kNoLevel) continue;
+                    const uint32_t key = sym ? min(la, lb) * ngu + max(la, lb) : la * ngu + lb;
+                    atomicAdd(&dyn[a * 4096 + key], 1u);
+                    if (a == 0) ++npa0;
+                    else if (a == 1) ++npa1;
+                    else if (a == 2) ++npa2;
+                    else ++npa3;
+                }
+            }
         }
         __syncthreads();
         double sacc = 0;
         for (int a = 0; a < A; ++a) {
             const int ddx = cfg.dx[a], ddy = cfg.dy[a];
+            uint32_t* hist = fused ? dyn + a * 4096
+                                   : ((uint32_t)ng * (uint32_t)ng <= kSmemCells ? dyn : S.ghist);
             for (int k = tid; k < 256; k += kBT) {
                 sm.px[k] = 0u;
                 sm.py[k] = 0u;
@@ -769,22 +833,39 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
             for (int k = tid; k < 512; k += kBT) sm.psum[k] = 0u;
             __syncthreads();
             // pairs (x, y) -> (x + dx, y + dy), both in the ROI
-            uint32_t npr = 0;
-            for (uint32_t i = tid; i < n; i += kBT) {
-                const uint32_t p = S.xy[i];
-                const int x = (int)(p & 0xffffu), y = (int)(p >> 16);
-                const int nx = x + ddx, ny = y + ddy;
-                if (nx >= 0 && nx < w && ny >= 0 && ny < h) {
+            uint32_t npr = a == 0 ? npa0 : a == 1 ? npa1 : a == 2 ? npa2 : npa3;
+            auto count = [&](uint32_t la, uint32_t lb) {
+                ++npr;
+                const uint32_t key = sym ? min(la, lb) * (uint32_t)ng + max(la, lb)
+                                         : la * (uint32_t)ng + lb;
+                atomicAdd(&hist[key], 1u);
+            };
+            if (fused) {
+                // counted above
+            } else if (dense) {  // window cells whose neighbour is inside the window
+                const int xa = ddx < 0 ? -ddx : 0, xb = ddx > 0 ? w - ddx : w;
+                const int ya = ddy < 0 ? -ddy : 0, yb = ddy > 0 ? h - ddy : h;
+                const uint32_t cw = xb > xa ? (uint32_t)(xb - xa) : 0u;
+                const uint32_t ch = yb > ya ? (uint32_t)(yb - ya) : 0u;
+                for (uint32_t c = tid; c < cw * ch; c += kBT) {
+                    const uint32_t yy = c / cw, xx = c - yy * cw;
+                    const int x = (int)xx + xa, y = (int)yy + ya;
+                    const uint32_t la = S.lraster[(uint32_t)y * (uint32_t)w + (uint32_t)x];
+                    const uint32_t lb =
+                        S.lraster[(uint32_t)(y + ddy) * (uint32_t)w + (uint32_t)(x + ddx)];
+                    if (la != kNoLevel && lb != kNoLevel) count(la, lb);
+                }
+            } else {  // member pixels; neighbour by row mask + word offsets
+                for (uint32_t i = tid; i < n; i += kBT) {
+                    const uint32_t p = S.xy[i];
+                    const int x = (int)(p & 0xffffu), y = (int)(p >> 16);
+                    const int nx = x + ddx, ny = y + ddy;
+                    if (nx < 0 || nx >= w || ny < 0 || ny >= h) continue;
                     const uint32_t wi = (uint32_t)ny * wpr + (uint32_t)(nx >> 6);
                     const uint64_t m = S.rowmask[wi];
-                    if ((m >> (nx & 63)) & 1ull) {
-                        ++npr;
-                        const uint32_t jn = S.wordoff[wi] + __popcll(m & ((1ull << (nx & 63)) - 1ull));
-                        const uint32_t la = S.lvl[i], lb = S.lvl[jn];
-                        const uint32_t key = sym ? min(la, lb) * (uint32_t)ng + max(la, lb)
-                                                 : la * (uint32_t)ng + lb;
-                        atomicAdd(&S.ghist[key], 1u);
-                    }
+                    if (!((m >> (nx & 63)) & 1ull)) continue;
+                    const uint32_t jn = S.wordoff[wi] + __popcll(m & ((1ull << (nx & 63)) - 1ull));
+                    count(S.lvl[i], S.lvl[jn]);
                 }
             }
             const unsigned long long np = block_all((unsigned long long)npr, sm.u64s, OpAdd());
@@ -801,9 +882,9 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
                 double el = 0;
                 // dense pass in fixed thread order (deterministic fp64 entropy sum)
                 for (uint32_t key = tid; key < ncells; key += kBT) {
-                    const uint32_t c = S.ghist[key];
+                    const uint32_t c = hist[key];
                     if (!c) continue;
-                    S.ghist[key] = 0u;  // leave the histogram empty
+                    hist[key] = 0u;  // leave the histogram empty
                     const uint32_t ga = key / (uint32_t)ng, gb = key % (uint32_t)ng;
                     const bool off = sym && ga != gb;
                     const uint32_t cc = (sym && !off) ? 2u * c : c;
@@ -845,12 +926,16 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
         if (wid == 0 && lane < 29) orow[cfg.col_glcm + lane * (A + 1) + A] = sacc / (double)A;
     }
     __syncthreads();
+    BT(6);
 }
 
-__global__ void __launch_bounds__(kBT) k_roi_b(DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
+__global__ void __launch_bounds__(kBT, FXG_B_MINB) k_roi_b(DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                                                double* out, const DebugOut* dbg, uint8_t* scratch,
                                                BLayout B) {
     __shared__ BShared sm;
+    extern __shared__ uint32_t dyn[];  // [kSmemCells] GLCM pair histogram, kept zero
+    for (uint32_t i = threadIdx.x; i < kSmemCells; i += kBT) dyn[i] = 0u;
+    __syncthreads();
     const BSlab S = bslab(scratch + (size_t)blockIdx.x * B.bytes, B);
     const uint32_t nl = ctl->class_count[kClassL];
     const uint32_t total = nl + ctl->overflow_count;  // S kernels have finished
@@ -866,18 +951,40 @@ __global__ void __launch_bounds__(kBT) k_roi_b(DevImage img, RoiList rl, Control
             if (threadIdx.x == 0) atomicOr(&ctl->error, kErrCapacity);
             continue;
         }
-        process_b(r, img, rl, ctl, cfg, out, dbg, S, B, sm);
+        process_b(r, img, rl, ctl, cfg, out, dbg, S, B, sm, dyn);
     }
 }
 
 }  // namespace
 
-cudaError_t roi_b_setup() {
-    k_init_log2_tab<<<4, 256>>>();
-    return cudaDeviceSynchronize();
+// phase clocks of k_roi_b (tools/phase_clocks.py via fx_debug_phase_clocks)
+int roi_b_phase_clocks(unsigned long long* out, int reset) {
+#ifdef FXG_PHASE_TIMING
+    if (cudaMemcpyFromSymbol(out, g_phase_clk_b, 8 * sizeof(unsigned long long)) != cudaSuccess)
+        return 7;
+    if (reset) {
+        const unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(g_phase_clk_b, z, sizeof z);
+    }
+    return 0;
+#else
+    (void)out;
+    (void)reset;
+    return 1;
+#endif
 }
 
-BLayout make_blayout(uint32_t H, uint32_t WPR, uint32_t NMAX, uint32_t RUNMAX, uint32_t NB) {
+cudaError_t roi_b_setup() {
+    k_init_log2_tab<<<4, 256>>>();
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_roi_b, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(kSmemCells * sizeof(uint32_t)));
+    return e;
+}
+
+BLayout make_blayout(uint32_t H, uint32_t WPR, uint32_t NMAX, uint32_t RUNMAX, uint32_t NB,
+                     unsigned long long CELLS) {
     BLayout B{};
     size_t o = 0;
     auto take = [&](size_t bytes) {
@@ -893,6 +1000,8 @@ BLayout make_blayout(uint32_t H, uint32_t WPR, uint32_t NMAX, uint32_t RUNMAX, u
     B.tmpw = take((NW + 1) * 4);
     B.xy = take((size_t)NMAX * 4);
     B.vals = take((size_t)NMAX * 2);
+    B.RCAP = CELLS < 4ull * NMAX ? CELLS : 4ull * NMAX;
+    B.lraster = take((size_t)B.RCAP * 2);
     B.lvl = take((size_t)NMAX);
     B.vhist = take(65536 * 4);
     B.runoff = take(((size_t)H + 1) * 4);
@@ -913,7 +1022,7 @@ BLayout make_blayout(uint32_t H, uint32_t WPR, uint32_t NMAX, uint32_t RUNMAX, u
 
 void launch_roi_b(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                   double* out, const DebugOut* dbg, uint8_t* scratch, const BLayout& B) {
-    k_roi_b<<<grid, kBT, 0, s>>>(img, rl, ctl, cfg, out, dbg, scratch, B);
+    k_roi_b<<<grid, kBT, kSmemCells * sizeof(uint32_t), s>>>(img, rl, ctl, cfg, out, dbg, scratch, B);
 }
 
 }  // namespace fxg

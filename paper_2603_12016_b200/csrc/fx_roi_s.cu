@@ -1476,10 +1476,18 @@ void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
 
 }  // namespace fxg
 
+namespace fxg {
+int roi_b_phase_clocks(unsigned long long* out, int reset);
+}
+
+// slots 0..8: S kernels (lane 0 per ROI); 9..15: k_roi_b (thread 0 per ROI)
 extern "C" int fx_debug_phase_clocks(unsigned long long* out, int n, int reset) {
 #ifdef FXG_PHASE_TIMING
     unsigned long long h[16];
     if (cudaMemcpyFromSymbol(h, ::g_phase_clk, sizeof h) != cudaSuccess) return 7;
+    unsigned long long b[8];
+    if (fxg::roi_b_phase_clocks(b, reset)) return 7;
+    for (int i = 0; i < 7; ++i) h[9 + i] = b[i];
     for (int i = 0; i < n && i < 16; ++i) out[i] = h[i];
     if (reset) {
         const unsigned long long z[16] = {};

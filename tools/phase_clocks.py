@@ -12,6 +12,8 @@ from paper_2603_12016_b200 import fxg  # noqa: E402
 
 NAMES = ["load+gather", "int sort", "int stats", "edge", "moments", "glcm keys", "glcm sort",
          "glcm rle", "haralick"]
+BNAMES = ["B words+scan", "B pixels", "B int hist/order", "B edge+int out", "B moments",
+          "B glcm levels", "B glcm angles"]
 which = sys.argv[1]
 ctx = fx.Context(0)
 lib = fxg.lib()
@@ -21,7 +23,7 @@ if which == "c2":
     I = fx.uniform_u16(L.shape, 0)
     run = lambda: ctx.featurize(I, L, ["intensity", "moments"], fx.resolve_profile("default"))
     nroi = 50000
-else:
+elif which == "c4":
     T = int(sys.argv[2]) if len(sys.argv) > 2 else 256
     pairs = []
     for t in range(T):
@@ -30,6 +32,11 @@ else:
     run = lambda: ctx.featurize_batch(pairs, ["intensity", "moments", "glcm"],
                                       fx.resolve_profile("default"))
     nroi = sum(int(np.count_nonzero(np.bincount(p[1].ravel(), minlength=65536)[1:])) for p in pairs)
+if which == "c5":
+    L, _ = fx.packed_blob_mask_grid(16384, 200000, 576, 1)
+    I = fx.uniform_u16(L.shape, 0)
+    run = lambda: ctx.featurize(I, L, ["intensity", "moments", "glcm"], fx.resolve_profile("default"))
+    nroi = int(L.max())
 run()
 lib.fx_debug_phase_clocks(buf, 16, 1)
 run()
@@ -38,3 +45,8 @@ tot = sum(buf[:9])
 print(f"{which}: {nroi} ROIs, {tot / nroi:.0f} clocks per ROI (lane 0, S kernels)")
 for k, nm in enumerate(NAMES):
     print(f"  {nm:12s} {buf[k] / nroi:9.0f} clk/ROI  {100 * buf[k] / max(tot, 1):5.1f}%")
+totb = sum(buf[9:16])
+if totb:
+    print(f"large-ROI kernel: {totb / nroi:.0f} clocks per ROI (thread 0)")
+    for k, nm in enumerate(BNAMES):
+        print(f"  {nm:16s} {buf[9 + k] / nroi:10.0f} clk/ROI  {100 * buf[9 + k] / totb:5.1f}%")
