@@ -443,27 +443,36 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
         }
         ent = block_all(ent, sm.f64s, OpAdd());
         usq = block_all(usq, sm.u64s, OpAdd());
-        // order statistics (warp 0), shared through sm.red
-        if (wid == 0) {
-            const double median = (n & 1) ? (double)kth_value(n / 2, sm.cpre, S.vhist)
-                                          : 0.5 * ((double)kth_value(n / 2 - 1, sm.cpre, S.vhist) +
-                                                   (double)kth_value(n / 2, sm.cpre, S.vhist));
-            const double pv[6] = {1.0, 10.0, 25.0, 75.0, 90.0, 99.0};
-            double pc[6];
-#pragma unroll
-            for (int j = 0; j < 6; ++j) pc[j] = percentile_h(pv[j], n, sm.cpre, S.vhist);
-            const uint32_t shi = kth_value(n / 2, sm.cpre, S.vhist);
-            const uint32_t M2 = (n & 1) ? 2u * shi : kth_value(n / 2 - 1, sm.cpre, S.vhist) + shi;
-            const uint32_t d_hi = kth_dev_h(n / 2, M2, sm.cpre, S.vhist);
-            const uint32_t d_lo = (n & 1) ? d_hi : kth_dev_h(n / 2 - 1, M2, sm.cpre, S.vhist);
-            const double median_ad = (n & 1) ? 0.5 * (double)d_hi
-                                             : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
-            if (lane == 0) {
-                sm.red[0][0] = median;
-#pragma unroll
-                for (int j = 0; j < 6; ++j) sm.red[0][1 + j] = pc[j];
-                sm.red[0][7] = median_ad;
+        // order statistics, one query set per warp, shared through sm.red[0]:
+        // warp 0 median + deviation k = n/2, warp 1 deviation k = n/2 - 1 (even n),
+        // warps 2..7 the percentiles 1, 10, 25, 75, 90, 99
+        if (wid < 8) {
+            double r = 0;
+            if (wid < 2) {
+                const uint32_t shi = kth_value(n / 2, sm.cpre, S.vhist);
+                const uint32_t slo = (n & 1) ? shi : kth_value(n / 2 - 1, sm.cpre, S.vhist);
+                const uint32_t M2 = (n & 1) ? 2u * shi : slo + shi;
+                if (wid == 0) {
+                    const uint32_t d_hi = kth_dev_h(n / 2, M2, sm.cpre, S.vhist);
+                    if (lane == 0) {
+                        sm.red[0][0] = (n & 1) ? (double)shi : 0.5 * ((double)slo + (double)shi);
+                        sm.red[0][8] = (double)d_hi;
+                    }
+                } else {
+                    r = (n & 1) ? -1.0 : (double)kth_dev_h(n / 2 - 1, M2, sm.cpre, S.vhist);
+                    if (lane == 0) sm.red[0][9] = r;
+                }
+            } else {
+                const double pv = wid == 2 ? 1.0 : wid == 3 ? 10.0 : wid == 4 ? 25.0
+                                : wid == 5 ? 75.0 : wid == 6 ? 90.0 : 99.0;
+                r = percentile_h(pv, n, sm.cpre, S.vhist);
+                if (lane == 0) sm.red[0][wid - 1] = r;
             }
+        }
+        __syncthreads();
+        if (tid == 0) {  // median absolute deviation (intensity_features.cpp), exact
+            const double d_hi = sm.red[0][8], d_lo = sm.red[0][9];
+            sm.red[0][7] = (n & 1) ? 0.5 * d_hi : 0.5 * (0.5 * d_lo + 0.5 * d_hi);
         }
         __syncthreads();
         const double median = sm.red[0][0], p10 = sm.red[0][2], p25 = sm.red[0][3];
