@@ -773,22 +773,293 @@ static int glcm_group(const cloud_t* c, const fxo_params* prm, double* out) {
     return rc;
 }
 
+/* ----------------------------------------------------------------- shape -- */
+
+typedef struct {
+    int x, y;
+} pt_t;
+
+static long long cross3(pt_t o, pt_t a, pt_t b) {
+    return (long long)(a.x - o.x) * (b.y - o.y) - (long long)(a.y - o.y) * (b.x - o.x);
+}
+
+static int cmp_pt(const void* a, const void* b) {
+    const pt_t* p = a;
+    const pt_t* q = b;
+    if (p->x != q->x) return p->x < q->x ? -1 : 1;
+    return (p->y > q->y) - (p->y < q->y);
+}
+
+/* convex_hull (hull.cpp:17-55): Andrew's monotone chain over the sorted unique
+ * pixel centres, pops on cross <= 0 (collinear points removed); <= 2 points are
+ * returned as they are, an all-collinear set as its two end points. */
+static int convex_hull(const cloud_t* c, pt_t** out, size_t* nv) {
+    pt_t* pts = malloc((c->n ? c->n : 1) * sizeof(pt_t));
+    if (!pts) return 8;
+    for (size_t i = 0; i < c->n; ++i) pts[i] = (pt_t){(int)c->p[i].x, (int)c->p[i].y};
+    qsort(pts, c->n, sizeof(pt_t), cmp_pt);
+    size_t n = 0;
+    for (size_t i = 0; i < c->n; ++i)
+        if (!n || pts[i].x != pts[n - 1].x || pts[i].y != pts[n - 1].y) pts[n++] = pts[i];
+    if (n <= 2) {
+        *out = pts;
+        *nv = n;
+        return 0;
+    }
+    pt_t* h = malloc(2 * n * sizeof(pt_t));
+    if (!h) {
+        free(pts);
+        return 8;
+    }
+    size_t k = 0;
+    for (size_t i = 0; i < n; ++i) {
+        while (k >= 2 && cross3(h[k - 2], h[k - 1], pts[i]) <= 0) --k;
+        h[k++] = pts[i];
+    }
+    const size_t lower = k + 1;
+    for (size_t i = n - 1; i-- > 0;) {
+        while (k >= lower && cross3(h[k - 2], h[k - 1], pts[i]) <= 0) --k;
+        h[k++] = pts[i];
+    }
+    k -= 1;
+    if (k < 3) {
+        h[0] = pts[0];
+        h[1] = pts[n - 1];
+        k = 2;
+    }
+    free(pts);
+    *out = h;
+    *nv = k;
+    return 0;
+}
+
+/* point_in_hull (hull.cpp:66-87), eps 1e-9 */
+static int point_in_hull(const pt_t* v, size_t nv, double px, double py) {
+    const double eps = 1e-9;
+    if (nv == 0) return 0;
+    if (nv == 1) return fabs(px - v[0].x) < eps && fabs(py - v[0].y) < eps;
+    if (nv == 2) {
+        const double ax = v[0].x, ay = v[0].y, bx = v[1].x, by = v[1].y;
+        const double cr = (bx - ax) * (py - ay) - (by - ay) * (px - ax);
+        if (fabs(cr) > eps) return 0;
+        const double dot = (px - ax) * (bx - ax) + (py - ay) * (by - ay);
+        const double len2 = (bx - ax) * (bx - ax) + (by - ay) * (by - ay);
+        return dot >= -eps && dot <= len2 + eps;
+    }
+    for (size_t i = 0; i < nv; ++i) {
+        const pt_t a = v[i], b = v[(i + 1) % nv];
+        const double cr = (double)(b.x - a.x) * (py - a.y) - (double)(b.y - a.y) * (px - a.x);
+        if (cr < -eps) return 0;
+    }
+    return 1;
+}
+
+/* euler_number (shape_features.cpp:24-99): 8-connected foreground components
+ * minus 4-connected background components of the 1-padded bbox grid that do not
+ * reach the padding. */
+static int euler_number(const cloud_t* c) {
+    const int w = (int)(c->bb.xmax - c->bb.xmin) + 3, h = (int)(c->bb.ymax - c->bb.ymin) + 3;
+    const int x0 = (int)c->bb.xmin - 1, y0 = (int)c->bb.ymin - 1;
+    const size_t cells = (size_t)w * h;
+    uint8_t* fg = calloc(cells, 1);
+    int* mark = calloc(cells, sizeof(int));
+    int* st = malloc(cells * 2 * 8 * sizeof(int) + 16);
+    for (size_t i = 0; i < c->n; ++i)
+        fg[(size_t)((int)c->p[i].y - y0) * w + ((int)c->p[i].x - x0)] = 1;
+    static const int k4[4][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}};
+    int comps = 0, holes = 0;
+    for (int pass = 0; pass < 3; ++pass) {
+        /* pass 0: 8-connected fg components; 1: outer background from (0,0);
+         * 2: remaining background components (holes) */
+        for (int y = 0; y < h; ++y) {
+            for (int x = 0; x < w; ++x) {
+                const size_t at = (size_t)y * w + x;
+                if (pass == 1 && (x || y)) continue;
+                if (pass == 0 ? (!fg[at] || mark[at]) : (fg[at] || mark[at])) continue;
+                if (pass == 0) ++comps;
+                if (pass == 2) ++holes;
+                size_t sp = 0;
+                st[sp++] = x;
+                st[sp++] = y;
+                mark[at] = pass + 1;
+                while (sp) {
+                    const int cy = st[--sp], cx = st[--sp];
+                    const int nk = pass == 0 ? 8 : 4;
+                    for (int k = 0; k < nk; ++k) {
+                        const int nx = cx + (pass == 0 ? kRing[k][0] : k4[k][0]);
+                        const int ny = cy + (pass == 0 ? kRing[k][1] : k4[k][1]);
+                        if (nx < 0 || nx >= w || ny < 0 || ny >= h) continue;
+                        const size_t nat = (size_t)ny * w + nx;
+                        if ((pass == 0 ? fg[nat] : !fg[nat]) && !mark[nat]) {
+                            mark[nat] = pass + 1;
+                            st[sp++] = nx;
+                            st[sp++] = ny;
+                        }
+                    }
+                }
+            }
+        }
+    }
+    free(fg);
+    free(mark);
+    free(st);
+    return comps - holes;
+}
+
+/* shape_features (shape_features.cpp:147-251) + shape_feature_values order:
+ * area, perimeter, bbox x/y/w/h, centroid x/y, circularity, extent,
+ * aspect_ratio, convex_area, solidity, equivalent_diameter, major/minor axis,
+ * eccentricity, elongation, orientation, euler_number, feret max/min, then the
+ * 8 extrema as (x, y) pairs in regionprops order. */
+static int shape_group(const cloud_t* c, double* o) {
+    const double PI = 3.141592653589793, SQRT2 = 1.4142135623730951;
+    memset(o, 0, 38 * sizeof(double));
+    const size_t n = c->n;
+    if (n == 0) return 0;
+    const double dn = (double)n;
+    const double bw = (double)((int)(c->bb.xmax - c->bb.xmin) + 1);
+    const double bh = (double)((int)(c->bb.ymax - c->bb.ymin) + 1);
+    o[0] = dn;
+    o[2] = c->bb.xmin;
+    o[3] = c->bb.ymin;
+    o[4] = bw;
+    o[5] = bh;
+    o[9] = dn / (bw * bh);
+    o[10] = bw / bh;
+    double sx = 0, sy = 0;
+    for (size_t i = 0; i < n; ++i) {
+        sx += c->p[i].x;
+        sy += c->p[i].y;
+    }
+    const double cx = sx / dn, cy = sy / dn;
+    o[6] = cx;
+    o[7] = cy;
+    if (n == 1) {
+        o[1] = 4.0;
+        o[8] = 1.0;
+    } else {  /* contour_perimeter (shape_features.cpp:11-21) over the traced cycle */
+        int32_t* pts = NULL;
+        size_t np = 0;
+        int rc = trace_contour(c, &pts, &np);
+        if (rc) return rc;
+        double per = 4.0;
+        if (np >= 2) {
+            per = 0;
+            for (size_t i = 0; i < np; ++i) {
+                const size_t j = (i + 1) % np;
+                const int dx = abs(pts[2 * i] - pts[2 * j]), dy = abs(pts[2 * i + 1] - pts[2 * j + 1]);
+                per += (dx + dy == 2) ? SQRT2 : 1.0;
+            }
+        }
+        free(pts);
+        o[1] = per;
+        o[8] = 4.0 * PI * dn / (per * per);
+    }
+    pt_t* hv = NULL;
+    size_t nv = 0;
+    if (convex_hull(c, &hv, &nv)) return 8;
+    double carea = 0;  /* rasterized_hull_area (shape_features.cpp:102-115) */
+    if (nv >= 3) {
+        long long cnt = 0;
+        for (int y = (int)c->bb.ymin; y <= (int)c->bb.ymax; ++y)
+            for (int x = (int)c->bb.xmin; x <= (int)c->bb.xmax; ++x)
+                if (point_in_hull(hv, nv, x, y)) ++cnt;
+        carea = (double)cnt;
+    }
+    o[11] = carea;
+    o[12] = carea > 0 ? dn / carea : 0.0;
+    o[13] = sqrt(4.0 * dn / PI);
+    {  /* +1/12 second-moment ellipse (shape_features.cpp:176-197), pixel order */
+        double m20 = 0, m02 = 0, m11 = 0;
+        for (size_t i = 0; i < n; ++i) {
+            const double dx = c->p[i].x - cx, dy = c->p[i].y - cy;
+            m20 += dx * dx;
+            m02 += dy * dy;
+            m11 += dx * dy;
+        }
+        const double a = m20 / dn + 1.0 / 12.0, cc = m02 / dn + 1.0 / 12.0, b = m11 / dn;
+        const double disc = sqrt((a - cc) * (a - cc) / 4.0 + b * b);
+        const double l1 = (a + cc) / 2.0 + disc, l2 = (a + cc) / 2.0 - disc;
+        o[14] = 4.0 * sqrt(l1 > 0 ? l1 : 0.0);
+        o[15] = 4.0 * sqrt(l2 > 0 ? l2 : 0.0);
+        o[16] = l1 > 0 ? sqrt(fmax(0.0, 1.0 - l2 / l1)) : 0.0;
+        o[17] = o[15] > 0 ? o[14] / o[15] : 0.0;
+        double th = 0.5 * atan2(2.0 * b, a - cc);
+        if (th <= -PI / 2.0) th += PI;
+        o[18] = th;
+    }
+    o[19] = (double)euler_number(c);
+    {  /* feret_diameters (shape_features.cpp:117-143) */
+        double fmaxd = 0, fmind = 0;
+        if (nv >= 2) {
+            for (size_t i = 0; i < nv; ++i)
+                for (size_t j = i + 1; j < nv; ++j)
+                    fmaxd = fmax(fmaxd, hypot((double)(hv[i].x - hv[j].x), (double)(hv[i].y - hv[j].y)));
+            if (nv > 2) {
+                fmind = 1.79769313486231570815e308;
+                for (size_t i = 0; i < nv; ++i) {
+                    const pt_t a = hv[i], b = hv[(i + 1) % nv];
+                    const double ex = b.x - a.x, ey = b.y - a.y, len = hypot(ex, ey);
+                    double wd = 0;
+                    for (size_t k = 0; k < nv; ++k) {
+                        const double d = fabs(ex * (hv[k].y - a.y) - ey * (hv[k].x - a.x)) / len;
+                        wd = fmax(wd, d);
+                    }
+                    fmind = fmin(fmind, wd);
+                }
+            }
+        }
+        o[20] = fmaxd;
+        o[21] = fmind;
+    }
+    free(hv);
+    {  /* extrema (shape_features.cpp:202-238) */
+        int top = 1 << 30, bot = -1, left = 1 << 30, right = -1;
+        for (size_t i = 0; i < n; ++i) {
+            const int x = (int)c->p[i].x, y = (int)c->p[i].y;
+            top = y < top ? y : top;
+            bot = y > bot ? y : bot;
+            left = x < left ? x : left;
+            right = x > right ? x : right;
+        }
+        int tl = 1 << 30, tr = -1, bl = 1 << 30, br = -1, lt = 1 << 30, lb = -1, rt = 1 << 30, rb = -1;
+        for (size_t i = 0; i < n; ++i) {
+            const int x = (int)c->p[i].x, y = (int)c->p[i].y;
+            if (y == top) { tl = x < tl ? x : tl; tr = x > tr ? x : tr; }
+            if (y == bot) { bl = x < bl ? x : bl; br = x > br ? x : br; }
+            if (x == left) { lt = y < lt ? y : lt; lb = y > lb ? y : lb; }
+            if (x == right) { rt = y < rt ? y : rt; rb = y > rb ? y : rb; }
+        }
+        const int ex[8] = {tl, tr, right, right, br, bl, left, left};
+        const int ey[8] = {top, top, rt, rb, bot, bot, lb, lt};
+        for (int i = 0; i < 8; ++i) {
+            o[22 + 2 * i] = ex[i];
+            o[23 + 2 * i] = ey[i];
+        }
+    }
+    return 0;
+}
+
 /* ------------------------------------------------------------- dispatch -- */
 
 static int check_groups(unsigned groups) {
     if (groups == 0) return fail(1, "feature list is empty");
-    if (groups & (FXO_SHAPE | FXO_GLRLM | FXO_GLSZM | FXO_NGTDM))
+    if (groups & (FXO_GLRLM | FXO_GLSZM | FXO_NGTDM))
         return fail(1, "group outside the restated hot path");
     return 0;
 }
 
-/* compute_roi_features (engine.cpp:138-209) for intensity/moments/glcm. */
+/* compute_roi_features (engine.cpp:138-209) for intensity/shape/moments/glcm. */
 static int roi_features(const cloud_t* c, unsigned groups, const fxo_params* prm, double* out) {
     double* o = out;
     int rc;
     if (groups & FXO_INTENSITY) {
         if ((rc = intensity_group(c, prm->histogram_bins, o))) return rc;
         o += 39;
+    }
+    if (groups & FXO_SHAPE) {
+        if ((rc = shape_group(c, o))) return rc;
+        o += 38;
     }
     if (groups & FXO_MOMENTS) {
         moments_t b, w;

@@ -4,7 +4,7 @@ fixtures in tests/golden/ (made by tests/golden/make_golden.py from oracle/_ref)
 
 CPU tests check the oracle; the gpu-marked tests check the device path against
 the same numbers.  Sources (paths relative to /root/reference/proj):
-  tests/test_intensity.cpp:29-79, tests/test_shape.cpp:124-140,
+  tests/test_intensity.cpp:29-79, tests/test_shape.cpp:32-140,
   tests/test_texture.cpp:45-126, tests/test_roistore.cpp:34-64,138-154,
   tests/test_engine.cpp:60-75,203-213.
 """
@@ -29,6 +29,48 @@ G_COLS = ["asm", "acor", "cluprom", "clushade", "clutend", "contrast", "corr", "
           "difentro", "difvar", "dis", "energy", "entropy", "hom1", "hom2", "id", "idn", "idm",
           "idmn", "infomeas1", "infomeas2", "iv", "jave", "je", "jmax", "jvar", "sumave",
           "sument", "sumvar"]
+
+
+S_COLS = ["area", "perimeter", "bbox_x", "bbox_y", "bbox_w", "bbox_h", "centroid_x", "centroid_y",
+          "circularity", "extent", "aspect_ratio", "convex_area", "solidity",
+          "equivalent_diameter", "major_axis_len", "minor_axis_len", "eccentricity", "elongation",
+          "orientation", "euler_number", "feret_max", "feret_min"] + [
+          f"extrema_{c}_{a}" for c in ("topleft", "topright", "righttop", "rightbottom",
+                                       "bottomright", "bottomleft", "leftbottom", "lefttop")
+          for a in ("x", "y")]
+
+
+def shape(fn, xs, ys):
+    xs, ys = np.asarray(xs), np.asarray(ys)
+    return dict(zip(S_COLS, fn(xs, ys, np.ones(len(xs), np.uint16), ["shape"],
+                               make_params("default"))))
+
+
+def run_shape_known_answers(fn):                                 # test_shape.cpp:32-120
+    ys, xs = np.mgrid[3:13, 5:15]
+    f = shape(fn, xs.ravel(), ys.ravel())                        # 10x10 solid square
+    assert f["area"] == 100 and f["bbox_w"] == 10 and f["bbox_h"] == 10
+    assert f["extent"] == pytest.approx(1) and f["euler_number"] == 1
+    assert f["feret_max"] == pytest.approx(9 * np.sqrt(2)) and f["feret_min"] == pytest.approx(9)
+    assert f["solidity"] == pytest.approx(1) and f["convex_area"] == pytest.approx(100)
+    assert f["aspect_ratio"] == pytest.approx(1)
+    ys, xs = np.nonzero(np.array([[1, 1, 1], [1, 0, 1], [1, 1, 1]]))
+    assert shape(fn, xs, ys)["euler_number"] == 0                # one hole
+    xs = np.arange(10)
+    f = shape(fn, xs, np.full(10, 5))                            # 1x10 line
+    mu20 = np.sum((xs - xs.mean()) ** 2) / 10 + 1 / 12
+    mu02 = 1 / 12
+    assert f["major_axis_len"] == pytest.approx(4 * np.sqrt(mu20), rel=1e-12)
+    assert f["minor_axis_len"] == pytest.approx(4 * np.sqrt(mu02), rel=1e-12)
+    assert f["eccentricity"] == pytest.approx(np.sqrt(1 - mu02 / mu20), rel=1e-12)
+    assert f["orientation"] == pytest.approx(0) and f["minor_axis_len"] > 0
+    f = shape(fn, [3], [4])                                      # single pixel
+    assert f["area"] == 1 and f["perimeter"] == pytest.approx(4)
+    assert f["circularity"] == pytest.approx(1) and f["convex_area"] == 0
+    assert f["solidity"] == 0 and f["feret_max"] == 0
+    f = shape(fn, [0, 1, 2], [0, 0, 0])                          # collinear cloud
+    assert f["convex_area"] == 0 and f["solidity"] == 0
+    assert f["feret_max"] == pytest.approx(2) and f["feret_min"] == 0
 
 
 def line(values):
@@ -97,6 +139,7 @@ def run_known_answers(fn):
 
 def test_known_answers_oracle(oracle):
     run_known_answers(oracle.roi_features)
+    run_shape_known_answers(oracle.roi_features)
 
 
 @pytest.mark.gpu
@@ -111,6 +154,7 @@ def test_known_answers_device(ctx):
             fp.angles[i] = p.angles[i]
         return ctx.roi_features(xs, ys, vs, groups, fp)
     run_known_answers(fn)
+    run_shape_known_answers(fn)
 
 
 def test_label_scan_known_answer(oracle):                      # test_roistore.cpp:34-64
