@@ -10,7 +10,7 @@
 // Differences (documented in INTEGRATION.md):
 //  - ExtractionConfig::threads / parallel / memory_budget / spill_dir are
 //    validated like the reference but do not change the (device) execution.
-//  - groups shape / glrlm / glszm / ngtdm have no device kernel yet and raise
+//  - groups glrlm / glszm / ngtdm have no device kernel yet and raise
 //    ConfigError from compute_roi_features / run (never a silent CPU fallback).
 #pragma once
 

@@ -270,10 +270,14 @@ FeatCfg make_cfg(unsigned groups, const fx_texture_params& p) {
     FeatCfg f{};
     f.groups = groups;
     int col = 0;
-    f.col_int = f.col_mom = f.col_glcm = -1;
+    f.col_int = f.col_shape = f.col_mom = f.col_glcm = -1;
     if (groups & FX_GROUP_INTENSITY) {
         f.col_int = col;
         col += 39;
+    }
+    if (groups & FX_GROUP_SHAPE) {  // engine.cpp:22-23 canonical order
+        f.col_shape = col;
+        col += 38;
     }
     if (groups & FX_GROUP_MOMENTS) {
         f.col_mom = col;

@@ -131,7 +131,7 @@ struct DevImage {
 struct FeatCfg {
     uint32_t groups;
     int ncols;
-    int col_int, col_mom, col_glcm;  // column offsets, -1 if absent
+    int col_int, col_shape, col_mom, col_glcm;  // column offsets, -1 if absent
     int bins;                        // max(2, histogram_bins)
     int ng, symmetric, n_angles;
     int angle[8];                    // sorted (engine.cpp:36-40)

@@ -208,7 +208,7 @@ __device__ __forceinline__ void moments_epilogue(double N, double dn, unsigned l
 // sized on the host from the largest L window / pixel count of the launch.
 struct BLayout {
     size_t rowmask, kmask, emask, wordoff, tmpw, xy, vals, lraster, lvl, vhist, runoff, rs, re, parent,
-        rsize, bins, ghist;
+        rsize, bins, ghist, ctop, cbot, hv;
     size_t bytes;
     unsigned long long RCAP;  // level-raster capacity (cells): dense windows only
     uint32_t H, WPR, NMAX, RUNMAX, NB;

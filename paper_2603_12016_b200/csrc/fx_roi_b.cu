@@ -186,6 +186,7 @@ struct BSlab {
     uint8_t* lvl;
     uint32_t *vhist, *runoff, *parent, *rsize, *bins, *ghist;
     uint16_t *rs, *re;
+    uint32_t *ctop, *cbot, *hv;  // shape: column extremes, hull chain
 };
 
 __device__ __forceinline__ BSlab bslab(uint8_t* base, const BLayout& B) {
@@ -207,6 +208,9 @@ __device__ __forceinline__ BSlab bslab(uint8_t* base, const BLayout& B) {
     S.rsize = (uint32_t*)(base + B.rsize);
     S.bins = (uint32_t*)(base + B.bins);
     S.ghist = (uint32_t*)(base + B.ghist);
+    S.ctop = (uint32_t*)(base + B.ctop);
+    S.cbot = (uint32_t*)(base + B.cbot);
+    S.hv = (uint32_t*)(base + B.hv);
     return S;
 }
 
@@ -301,6 +305,383 @@ struct BShared {
     uint32_t job;
 };
 
+// K (largest 8-connected component, row-major tie-break) into S.kmask and E
+// (4-connected exterior of the window cells outside K) into S.emask, by run
+// union-find; false past the run capacity (contour.cpp:30-66)
+__device__ bool block_ke(int h, int w, int wpr, uint32_t nw, const BSlab& S, const BLayout& B,
+                         BShared& sm) {
+    const unsigned tid = threadIdx.x;
+    const uint64_t lastm = (w & 63) ? ((1ull << (w & 63)) - 1ull) : ~0ull;
+    uint32_t nr = build_runs(S.rowmask, h, wpr, S, B.RUNMAX, sm.scan);
+    bool ok = nr != ~0u;
+    if (ok) {
+        unite_runs(h, 1, S);
+        for (uint32_t q = tid; q < nr; q += kBT) S.rsize[q] = 0u;
+        __syncthreads();
+        for (uint32_t q = tid; q < nr; q += kBT)
+            atomicAdd(&S.rsize[S.parent[q]], (uint32_t)(S.re[q] - S.rs[q] + 1));
+        __syncthreads();
+        unsigned long long bk = 0;
+        for (uint32_t q = tid; q < nr; q += kBT)
+            if (S.parent[q] == q) {
+                const unsigned long long key = ((unsigned long long)S.rsize[q] << 32) |
+                                               (0xffffffffu - q);
+                bk = key > bk ? key : bk;
+            }
+        bk = block_all(bk, sm.u64s, OpMax());
+        const uint32_t broot = 0xffffffffu - (uint32_t)(bk & 0xffffffffu);
+        for (uint32_t wi = tid; wi < nw; wi += kBT) S.kmask[wi] = 0ull;
+        __syncthreads();
+        for (int y = tid; y < h; y += kBT)
+            for (uint32_t q = S.runoff[y]; q < S.runoff[y + 1]; ++q)
+                if (S.parent[q] == broot) set_bits(S.kmask + (size_t)y * wpr, S.rs[q], S.re[q]);
+        __syncthreads();
+        // free cells of the window (not in K) -> 4-connected exterior
+        for (uint32_t wi = tid; wi < nw; wi += kBT)
+            S.emask[wi] = ~S.kmask[wi] & ((int)(wi % wpr) == wpr - 1 ? lastm : ~0ull);
+        __syncthreads();
+        const uint32_t nf = build_runs(S.emask, h, wpr, S, B.RUNMAX, sm.scan);
+        ok = nf != ~0u;
+        if (ok) {
+            unite_runs(h, 0, S);
+            for (uint32_t q = tid; q < nf; q += kBT) S.rsize[q] = 0u;
+            __syncthreads();
+            for (int y = tid; y < h; y += kBT)
+                for (uint32_t q = S.runoff[y]; q < S.runoff[y + 1]; ++q)
+                    if (y == 0 || y == h - 1 || S.rs[q] == 0 || S.re[q] == w - 1)
+                        S.rsize[S.parent[q]] = 1u;
+            __syncthreads();
+            for (uint32_t wi = tid; wi < nw; wi += kBT) S.emask[wi] = 0ull;
+            __syncthreads();
+            for (int y = tid; y < h; y += kBT)
+                for (uint32_t q = S.runoff[y]; q < S.runoff[y + 1]; ++q)
+                    if (S.rsize[S.parent[q]]) set_bits(S.emask + (size_t)y * wpr, S.rs[q], S.re[q]);
+            __syncthreads();
+        }
+    }
+    return ok;
+}
+
+// ---------------------------------------------------------------------------
+// Shape group of a large ROI (shape_features.cpp:147-251), block-level; same
+// rules as shape_phase_s (fx_roi_s.cu).  Thread 0 replays the Moore walk of
+// contour.cpp:70-144 on K with Brent's cycle detection (no per-state memory for
+// windows of any size) and builds the monotone-chain hull of the column extremes;
+// threads 1..3 sum the ellipse terms in pixel order; the rest is parallel.
+__constant__ int8_t c_ring_b[8][2] = {{-1, 0}, {-1, -1}, {0, -1}, {1, -1},
+                                      {1, 0},  {1, 1},   {0, 1},  {-1, 1}};
+__constant__ int8_t c_ring_of_b[9] = {1, 0, 7, 2, -1, 6, 3, 4, 5};
+
+struct WalkState {
+    int x, y, b;
+    __device__ bool operator==(const WalkState& o) const { return x == o.x && y == o.y && b == o.b; }
+    __device__ bool operator!=(const WalkState& o) const { return !(*this == o); }
+};
+
+__device__ __forceinline__ bool kb_at(const uint64_t* km, int h, int w, int wpr, int x, int y) {
+    return x >= 0 && x < w && y >= 0 && y < h &&
+           ((km[(size_t)y * wpr + (x >> 6)] >> (x & 63)) & 1ull);
+}
+
+__device__ WalkState walk_next(const uint64_t* km, int h, int w, int wpr, WalkState s) {
+    int found = -1;
+    for (int k = 1; k <= 8; ++k) {
+        const int idx = (s.b + k) & 7;
+        if (kb_at(km, h, w, wpr, s.x + c_ring_b[idx][0], s.y + c_ring_b[idx][1])) {
+            found = idx;
+            break;
+        }
+    }
+    const int prev = (found + 7) & 7;
+    const int ddx = c_ring_b[prev][0] - c_ring_b[found][0], ddy = c_ring_b[prev][1] - c_ring_b[found][1];
+    return WalkState{s.x + c_ring_b[found][0], s.y + c_ring_b[found][1],
+                     c_ring_of_b[(ddx + 1) * 3 + (ddy + 1)]};
+}
+
+__device__ __forceinline__ long long floor_div_b(long long a, long long b) {  // b > 0
+    return a >= 0 ? a / b : -((-a + b - 1) / b);
+}
+
+__device__ void shape_b(int h, int w, int wpr, uint32_t nw, uint32_t n, long long gx0,
+                        long long gy0, unsigned long long sX, unsigned long long sY,
+                        const BSlab& S, BShared& sm, double* o) {
+    const unsigned tid = threadIdx.x, lane = lane_id(), wid = warp_id();
+    const double PI = 3.141592653589793, SQRT2 = 1.4142135623730951;
+    const double dn = (double)n;
+    constexpr uint32_t kNone = 0xffffffffu;
+    // column extremes of all pixels
+    for (int x = tid; x < w; x += kBT) {
+        uint32_t t = kNone, bt = kNone;
+        for (int y = 0; y < h; ++y)
+            if ((S.rowmask[(size_t)y * wpr + (x >> 6)] >> (x & 63)) & 1ull) {
+                if (t == kNone) t = (uint32_t)y;
+                bt = (uint32_t)y;
+            }
+        S.ctop[x] = t;
+        S.cbot[x] = bt;
+    }
+    // |K| and the 8-connected Euler number (bit quads over the zero-padded window:
+    // row pairs (y-1, y), y = 0..h; word k covers columns 64k..64k+63, word wpr the
+    // padded column when w is a multiple of 64)
+    unsigned long long kc = 0;
+    for (uint32_t wi = tid; wi < nw; wi += kBT) kc += __popcll(S.kmask[wi]);
+    long long q = 0;
+    const uint32_t nq = (uint32_t)(h + 1) * (uint32_t)(wpr + 1);
+    for (uint32_t qi = tid; qi < nq; qi += kBT) {
+        const int y = (int)(qi / (wpr + 1)), k = (int)(qi % (wpr + 1));
+        auto word = [&](int yy, int kk) -> uint64_t {
+            return (yy >= 0 && yy < h && kk >= 0 && kk < wpr) ? S.rowmask[(size_t)yy * wpr + kk] : 0ull;
+        };
+        const uint64_t a = word(y - 1, k), b = word(y, k), ap = word(y - 1, k - 1), bp = word(y, k - 1);
+        const int lim = w - 64 * k;  // positions j <= lim are columns 0..w
+        const uint64_t vm = lim >= 63 ? ~0ull : ((2ull << lim) - 1ull);
+        const uint64_t A0 = (a << 1) | (ap >> 63), A1 = a, B0 = (b << 1) | (bp >> 63), B1 = b;
+        const uint64_t s1 = A0 ^ A1, s2 = B0 ^ B1, c = (A0 & A1) | (B0 & B1);
+        const uint64_t one = (s1 ^ s2) & ~c & vm, three = (s1 ^ s2) & c & vm;
+        const uint64_t dg = ((A0 & B1 & ~A1 & ~B0) | (A1 & B0 & ~A0 & ~B1)) & vm;
+        q += __popcll(one) - __popcll(three) - 2 * __popcll(dg);
+    }
+    kc = block_all(kc, sm.u64s, OpAdd());
+    q = (long long)block_all((unsigned long long)q, sm.u64s, OpAdd());
+    const double cx = (double)((unsigned long long)gx0 * n + sX) / dn;
+    const double cy = (double)((unsigned long long)gy0 * n + sY) / dn;
+    // thread 0: perimeter and hull; threads 1..3: ellipse sums
+    if (tid == 0) {
+        double per = 4.0;
+        if (n > 1 && kc > 1) {
+            int sy = 0;
+            while (true) {
+                bool any = false;
+                for (int k = 0; k < wpr; ++k) any |= S.kmask[(size_t)sy * wpr + k] != 0ull;
+                if (any) break;
+                ++sy;
+            }
+            int sx = 0;
+            for (int k = 0; k < wpr; ++k) {
+                const uint64_t m = S.kmask[(size_t)sy * wpr + k];
+                if (m) {
+                    sx = k * 64 + __ffsll((long long)m) - 1;
+                    break;
+                }
+            }
+            const WalkState s0{sx, sy, 0};
+            // Brent: cycle length lam, then the first state of the cycle
+            uint32_t power = 1, lam = 1;
+            WalkState tort = s0, hare = walk_next(S.kmask, h, w, wpr, s0);
+            while (tort != hare) {
+                if (power == lam) {
+                    tort = hare;
+                    power *= 2;
+                    lam = 0;
+                }
+                hare = walk_next(S.kmask, h, w, wpr, hare);
+                ++lam;
+            }
+            tort = hare = s0;
+            for (uint32_t i = 0; i < lam; ++i) hare = walk_next(S.kmask, h, w, wpr, hare);
+            while (tort != hare) {
+                tort = walk_next(S.kmask, h, w, wpr, tort);
+                hare = walk_next(S.kmask, h, w, wpr, hare);
+            }
+            per = 0;
+            WalkState cur = tort;
+            for (uint32_t i = 0; i < lam; ++i) {
+                const WalkState nx = walk_next(S.kmask, h, w, wpr, cur);
+                per = __dadd_rn(per, (abs(nx.x - cur.x) + abs(nx.y - cur.y) == 2) ? SQRT2 : 1.0);
+                cur = nx;
+            }
+        }
+        sm.red[0][0] = per;
+        // monotone-chain hull of the column extremes (hull.cpp:17-55)
+        uint32_t* hv = S.hv;  // (x | y << 16), chain stack
+        auto X = [&](int i) { return (long long)(hv[i] & 0xffffu); };
+        auto Y = [&](int i) { return (long long)(hv[i] >> 16); };
+        int k = 0, npt = 0, fx = -1;
+        uint32_t fy = 0, lx = 0, ly = 0;
+        auto push = [&](int px, uint32_t py, int lo) {
+            while (k >= lo && (X(k - 1) - X(k - 2)) * ((long long)py - Y(k - 2)) -
+                                      (Y(k - 1) - Y(k - 2)) * ((long long)px - X(k - 2)) <= 0)
+                --k;
+            hv[k++] = (uint32_t)px | (py << 16);
+        };
+        for (int x = 0; x < w; ++x)
+            if (S.ctop[x] != kNone) {
+                npt += S.ctop[x] == S.cbot[x] ? 1 : 2;
+                if (fx < 0) {
+                    fx = x;
+                    fy = S.ctop[x];
+                }
+                lx = (uint32_t)x;
+                ly = S.cbot[x];
+            }
+        if (npt <= 2) {
+            for (int x = 0; x < w; ++x)
+                if (S.ctop[x] != kNone) {
+                    hv[k++] = (uint32_t)x | (S.ctop[x] << 16);
+                    if (S.cbot[x] != S.ctop[x]) hv[k++] = (uint32_t)x | (S.cbot[x] << 16);
+                }
+        } else {
+            for (int x = 0; x < w; ++x)
+                if (S.ctop[x] != kNone) {
+                    push(x, S.ctop[x], 2);
+                    if (S.cbot[x] != S.ctop[x]) push(x, S.cbot[x], 2);
+                }
+            const int lower = k + 1;
+            bool skip_last = true;
+            for (int x = w - 1; x >= 0; --x)
+                if (S.ctop[x] != kNone) {
+                    if (S.cbot[x] != S.ctop[x]) {
+                        if (!skip_last) push(x, S.cbot[x], lower);
+                        skip_last = false;
+                        push(x, S.ctop[x], lower);
+                    } else {
+                        if (!skip_last) push(x, S.ctop[x], lower);
+                        skip_last = false;
+                    }
+                }
+            k -= 1;
+            if (k < 3) {
+                hv[0] = (uint32_t)fx | (fy << 16);
+                hv[1] = lx | (ly << 16);
+                k = 2;
+            }
+        }
+        sm.u32s[kBW] = (uint32_t)k;  // hull vertex count
+    } else if (tid <= 3) {
+        double e = 0;  // m20 (1), m02 (2), m11 (3), pixel order, no FMA
+        for (uint32_t i = 0; i < n; ++i) {
+            const uint32_t p = S.xy[i];
+            const double dx = __dsub_rn((double)(gx0 + (long long)(p & 0xffffu)), cx);
+            const double dy = __dsub_rn((double)(gy0 + (long long)(p >> 16)), cy);
+            const double t = tid == 1 ? __dmul_rn(dx, dx) : tid == 2 ? __dmul_rn(dy, dy) : __dmul_rn(dx, dy);
+            e = __dadd_rn(e, t);
+        }
+        sm.red[0][tid] = e;
+    }
+    __syncthreads();
+    const double per = sm.red[0][0], m20 = sm.red[0][1], m02 = sm.red[0][2], m11 = sm.red[0][3];
+    const int nv = (int)sm.u32s[kBW];
+    const uint32_t* hv = S.hv;
+    // convex area: lattice points inside or on the hull, rows in parallel
+    unsigned long long carea = 0;
+    if (nv >= 3)
+        for (int y = tid; y < h; y += kBT) {
+            long long xl = 0, xr = w - 1;
+            for (int i = 0; i < nv && xl <= xr; ++i) {
+                const int j = i + 1 < nv ? i + 1 : 0;
+                const long long ax = hv[i] & 0xffffu, ay = hv[i] >> 16, bx = hv[j] & 0xffffu,
+                                by = hv[j] >> 16;
+                const long long Bq = by - ay, Aq = (bx - ax) * (y - ay) + Bq * ax;  // Aq - Bq x >= 0
+                if (Bq > 0) xr = min(xr, floor_div_b(Aq, Bq));
+                else if (Bq < 0) xl = max(xl, -floor_div_b(Aq, -Bq));
+                else if (Aq < 0) xr = -1;
+            }
+            if (xr >= xl) carea += (unsigned long long)(xr - xl + 1);
+        }
+    carea = block_all(carea, sm.u64s, OpAdd());
+    // Feret diameters over the hull vertices
+    double fmx = 0, fmn = 1.79769313486231570815e308;
+    const unsigned long long npair = (unsigned long long)nv * (unsigned long long)nv;
+    for (unsigned long long pi = tid; pi < npair; pi += kBT) {
+        const int i = (int)(pi / nv), j = (int)(pi % nv);
+        if (j > i) {
+            const double dx = (double)((long long)(hv[i] & 0xffffu) - (long long)(hv[j] & 0xffffu));
+            const double dy = (double)((long long)(hv[i] >> 16) - (long long)(hv[j] >> 16));
+            fmx = fmax(fmx, hypot(dx, dy));
+        }
+    }
+    for (int i = tid; i < nv && nv > 2; i += kBT) {
+        const int j = i + 1 < nv ? i + 1 : 0;
+        const long long ax = hv[i] & 0xffffu, ay = hv[i] >> 16;
+        const long long ex = (long long)(hv[j] & 0xffffu) - ax, ey = (long long)(hv[j] >> 16) - ay;
+        long long mc = 0;
+        for (int kk = 0; kk < nv; ++kk) {
+            const long long c = ex * ((long long)(hv[kk] >> 16) - ay) - ey * ((long long)(hv[kk] & 0xffffu) - ax);
+            mc = max(mc, c < 0 ? -c : c);
+        }
+        fmn = fmin(fmn, (double)mc / hypot((double)ex, (double)ey));
+    }
+    fmx = block_all(fmx, sm.f64s, OpMax());
+    fmn = block_all(fmn, sm.f64s, OpMin());
+    if (nv <= 2) fmn = 0;
+    if (wid == 0) {
+        const double bw = (double)w, bh = (double)h;
+        double v = 0;
+        if (lane < 22) {
+            switch (lane) {
+                case 0: v = dn; break;
+                case 1: v = per; break;
+                case 2: v = (double)gx0; break;
+                case 3: v = (double)gy0; break;
+                case 4: v = bw; break;
+                case 5: v = bh; break;
+                case 6: v = cx; break;
+                case 7: v = cy; break;
+                case 8: v = n == 1 ? 1.0 : 4.0 * PI * dn / (per * per); break;
+                case 9: v = dn / (bw * bh); break;
+                case 10: v = bw / bh; break;
+                case 11: v = (double)carea; break;
+                case 12: v = carea ? dn / (double)carea : 0.0; break;
+                case 13: v = sqrt(4.0 * dn / PI); break;
+                case 19: v = (double)(q / 4); break;
+                case 20: v = fmx; break;
+                case 21: v = fmn; break;
+                default: {
+                    const double a = __dadd_rn(__ddiv_rn(m20, dn), 1.0 / 12.0);
+                    const double c = __dadd_rn(__ddiv_rn(m02, dn), 1.0 / 12.0);
+                    const double bb = __ddiv_rn(m11, dn);
+                    const double amc = __dsub_rn(a, c);
+                    const double disc =
+                        sqrt(__dadd_rn(__ddiv_rn(__dmul_rn(amc, amc), 4.0), __dmul_rn(bb, bb)));
+                    const double hs = __ddiv_rn(__dadd_rn(a, c), 2.0);
+                    const double l1 = __dadd_rn(hs, disc), l2 = __dsub_rn(hs, disc);
+                    const double maj = 4.0 * sqrt(fmax(0.0, l1)), mnr = 4.0 * sqrt(fmax(0.0, l2));
+                    if (lane == 14) v = maj;
+                    else if (lane == 15) v = mnr;
+                    else if (lane == 16) v = l1 > 0 ? sqrt(fmax(0.0, 1.0 - l2 / l1)) : 0.0;
+                    else if (lane == 17) v = mnr > 0 ? maj / mnr : 0.0;
+                    else {
+                        double th = 0.5 * atan2(2.0 * bb, amc);
+                        if (th <= -PI / 2.0) th += PI;
+                        v = th;
+                    }
+                }
+            }
+            o[lane] = v;
+        } else if (lane < 30) {  // extrema
+            const int e = lane - 22;
+            auto row_lo = [&](int y) {
+                for (int k = 0; k < wpr; ++k) {
+                    const uint64_t m = S.rowmask[(size_t)y * wpr + k];
+                    if (m) return k * 64 + __ffsll((long long)m) - 1;
+                }
+                return 0;
+            };
+            auto row_hi = [&](int y) {
+                for (int k = wpr - 1; k >= 0; --k) {
+                    const uint64_t m = S.rowmask[(size_t)y * wpr + k];
+                    if (m) return k * 64 + 63 - __clzll((long long)m);
+                }
+                return 0;
+            };
+            int ex = 0, ey = 0;
+            switch (e) {
+                case 0: ex = row_lo(0); ey = 0; break;
+                case 1: ex = row_hi(0); ey = 0; break;
+                case 2: ex = w - 1; ey = (int)S.ctop[w - 1]; break;
+                case 3: ex = w - 1; ey = (int)S.cbot[w - 1]; break;
+                case 4: ex = row_hi(h - 1); ey = h - 1; break;
+                case 5: ex = row_lo(h - 1); ey = h - 1; break;
+                case 6: ex = 0; ey = (int)S.cbot[0]; break;
+                default: ex = 0; ey = (int)S.ctop[0]; break;
+            }
+            o[22 + 2 * e] = (double)(gx0 + ex);
+            o[23 + 2 * e] = (double)(gy0 + ey);
+        }
+    }
+    __syncthreads();
+}
+
 __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Control* ctl,
                           const FeatCfg& cfg, double* __restrict__ out, const DebugOut* dbg,
                           const BSlab& S, const BLayout& B, BShared& sm, uint32_t* dyn) {
@@ -314,6 +695,7 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
     double* orow = out + (size_t)r * cfg.ncols;
     const bool dbg_on = dbg != nullptr && dbg->label == label;
     const bool want_int = cfg.col_int >= 0, want_mom = cfg.col_mom >= 0, want_glcm = cfg.col_glcm >= 0;
+    const bool want_shape = cfg.col_shape >= 0;
 
     BT_DECL
     // ---- membership words (warp per 64-column word) and popcounts
@@ -377,6 +759,7 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
     const uint32_t vmax = block_all(vhi, sm.u32s, OpMax());
     BT(1);
 
+    bool have_k = false;
     // ------------------------------------------------------------ intensity
     if (want_int) {
         if (wid == 0) {  // coarse exclusive prefix
@@ -517,58 +900,11 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
         // ---- edge set: K = largest 8-connected component, E = 4-connected exterior
         double e_mean = 0, e_min = 0, e_max = 0, e_std = 0, e_int = 0;
         {
-            const uint64_t lastm = (w & 63) ? ((1ull << (w & 63)) - 1ull) : ~0ull;
-            uint32_t nr = build_runs(S.rowmask, h, wpr, S, B.RUNMAX, sm.scan);
-            bool ok = nr != ~0u;
-            if (ok) {
-                unite_runs(h, 1, S);
-                for (uint32_t q = tid; q < nr; q += kBT) S.rsize[q] = 0u;
-                __syncthreads();
-                for (uint32_t q = tid; q < nr; q += kBT)
-                    atomicAdd(&S.rsize[S.parent[q]], (uint32_t)(S.re[q] - S.rs[q] + 1));
-                __syncthreads();
-                unsigned long long bk = 0;
-                for (uint32_t q = tid; q < nr; q += kBT)
-                    if (S.parent[q] == q) {
-                        const unsigned long long key = ((unsigned long long)S.rsize[q] << 32) |
-                                                       (0xffffffffu - q);
-                        bk = key > bk ? key : bk;
-                    }
-                bk = block_all(bk, sm.u64s, OpMax());
-                const uint32_t broot = 0xffffffffu - (uint32_t)(bk & 0xffffffffu);
-                for (uint32_t wi = tid; wi < nw; wi += kBT) S.kmask[wi] = 0ull;
-                __syncthreads();
-                for (int y = tid; y < h; y += kBT)
-                    for (uint32_t q = S.runoff[y]; q < S.runoff[y + 1]; ++q)
-                        if (S.parent[q] == broot) set_bits(S.kmask + (size_t)y * wpr, S.rs[q], S.re[q]);
-                __syncthreads();
-                // free cells of the window (not in K) -> 4-connected exterior
-                for (uint32_t wi = tid; wi < nw; wi += kBT)
-                    S.emask[wi] = ~S.kmask[wi] & ((int)(wi % wpr) == wpr - 1 ? lastm : ~0ull);
-                __syncthreads();
-                const uint32_t nf = build_runs(S.emask, h, wpr, S, B.RUNMAX, sm.scan);
-                ok = nf != ~0u;
-                if (ok) {
-                    unite_runs(h, 0, S);
-                    for (uint32_t q = tid; q < nf; q += kBT) S.rsize[q] = 0u;
-                    __syncthreads();
-                    for (int y = tid; y < h; y += kBT)
-                        for (uint32_t q = S.runoff[y]; q < S.runoff[y + 1]; ++q)
-                            if (y == 0 || y == h - 1 || S.rs[q] == 0 || S.re[q] == w - 1)
-                                S.rsize[S.parent[q]] = 1u;
-                    __syncthreads();
-                    for (uint32_t wi = tid; wi < nw; wi += kBT) S.emask[wi] = 0ull;
-                    __syncthreads();
-                    for (int y = tid; y < h; y += kBT)
-                        for (uint32_t q = S.runoff[y]; q < S.runoff[y + 1]; ++q)
-                            if (S.rsize[S.parent[q]]) set_bits(S.emask + (size_t)y * wpr, S.rs[q], S.re[q]);
-                    __syncthreads();
-                }
-            }
-            if (!ok) {
+            if (!block_ke(h, w, wpr, nw, S, B, sm)) {
                 if (tid == 0) atomicOr(&ctl->error, kErrRuns);
                 return;
             }
+            have_k = true;
             // edge = K & (4-neighbour in E, or on the window border); exact integer sums
             unsigned long long es = 0, esq = 0;
             uint32_t en = 0, emn = 0xffffffffu, emx = 0;
@@ -719,6 +1055,14 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
         __syncthreads();
     }
 
+    // --------------------------------------------------------------- shape
+    if (want_shape) {
+        if (!have_k && !block_ke(h, w, wpr, nw, S, B, sm)) {
+            if (tid == 0) atomicOr(&ctl->error, kErrRuns);
+            return;
+        }
+        shape_b(h, w, wpr, nw, n, gx0, gy0, sX, sY, S, sm, orow + cfg.col_shape);
+    }
     BT(3);
     // ------------------------------------------------------------- moments
     if (want_mom) {
@@ -1020,6 +1364,9 @@ BLayout make_blayout(uint32_t H, uint32_t WPR, uint32_t NMAX, uint32_t RUNMAX, u
     B.rsize = take((size_t)RUNMAX * 4);
     B.bins = take((size_t)NB * 4);
     B.ghist = take(65536 * 4);
+    B.ctop = take((size_t)WPR * 64 * 4);
+    B.cbot = take((size_t)WPR * 64 * 4);
+    B.hv = take(((size_t)WPR * 64 * 4 + 8) * 4);
     B.bytes = o;
     B.H = H;
     B.WPR = WPR;

@@ -51,6 +51,7 @@ struct SLayout {
     uint32_t kmask, emask, runoff, rs, re, parent, rsize;  // B: edge slow path
     uint32_t lvl, keys, keys2, gcnt, marg;     // B: glcm, sort path (ng > 64)
     uint32_t lmap, hist, list;                 // B: glcm, histogram path (ng <= 64)
+    uint32_t shp;                              // B: shape (after K rows at kmask)
     uint32_t bytes;
 };
 
@@ -82,6 +83,9 @@ __host__ __device__ constexpr SLayout make_slayout(uint32_t TW, uint32_t TH, uin
     L.parent = al(L.re + RUNMAX * 2, 16);
     L.rsize = al(L.parent + RUNMAX * 4, 16);
     const uint32_t e_edge = L.rsize + RUNMAX * 4;
+    // shape: contour-walk state bytes [TH][64], column extremes, hull vertices
+    L.shp = L.runoff;
+    const uint32_t e_shape = L.shp + TH * 64 + 128 + 2 * 256;  // hull stack <= 2 x 128 points
     L.lvl = B;
     L.keys = al(L.lvl + NMAX, 16);
     L.keys2 = al(L.keys + NMAX * 2, 16);
@@ -98,7 +102,7 @@ __host__ __device__ constexpr SLayout make_slayout(uint32_t TW, uint32_t TH, uin
         L.list = L.vals;
         e_glcm = L.marg + 321 * 4;
     }
-    L.bytes = al(mx(mx(e_load, e_sort), mx(e_edge, e_glcm)), 128) + 128;  // + mbarrier
+    L.bytes = al(mx(mx(mx(e_load, e_sort), mx(e_edge, e_glcm)), e_shape), 128) + 128;  // + mbarrier
     return L;
 }
 
@@ -392,6 +396,305 @@ __device__ __noinline__ uint32_t kth_dev2_warp(const uint16_t* s, uint32_t n, ui
     return best;
 }
 
+
+// ---------------------------------------------------------------------------
+// Shape group of an S window (shape_features.cpp:147-251), warp-level.
+//   km     : rows of K (largest 8-connected component), the grid trace_contour walks
+//   rowmask: rows of all ROI pixels (hull, Euler number, ellipse, extrema)
+//   scr    : [h][64] walk-state bytes, column extremes, hull vertices
+// Exact: area, bbox, centroid (integer sums), perimeter (the Moore walk of
+// contour.cpp:70-144 replayed: the first repeated (position, backtrack) state
+// starts the cycle, whose steps are summed in walk order), convex area (lattice
+// points per row from the hull edges' integer half-planes), Euler number (bit
+// quads, 8-connected foreground / 4-connected background), extrema, and the
+// ellipse sums (sequential in pixel order without FMA, as the reference).
+__constant__ int8_t c_ring[8][2] = {{-1, 0}, {-1, -1}, {0, -1}, {1, -1},
+                                    {1, 0},  {1, 1},   {0, 1},  {-1, 1}};
+
+// ring index of a unit offset (dx, dy) in [-1, 1]^2: (dx + 1) * 3 + (dy + 1)
+__constant__ int8_t c_ring_of[9] = {1, 0, 7, 2, -1, 6, 3, 4, 5};
+
+__device__ __forceinline__ bool k_at(const uint64_t* km, int h, int w, int x, int y) {
+    return x >= 0 && x < w && y >= 0 && y < h && ((km[y] >> x) & 1ull);
+}
+
+// one step of the Moore walk: position (x, y), backtrack ring index b
+__device__ __forceinline__ void walk_step(const uint64_t* km, int h, int w, int& x, int& y, int& b) {
+    int found = -1;
+#pragma unroll 1
+    for (int k = 1; k <= 8; ++k) {
+        const int idx = (b + k) & 7;
+        if (k_at(km, h, w, x + c_ring[idx][0], y + c_ring[idx][1])) {
+            found = idx;
+            break;
+        }
+    }
+    const int prev = (found + 7) & 7;
+    const int ddx = c_ring[prev][0] - c_ring[found][0], ddy = c_ring[prev][1] - c_ring[found][1];
+    x += c_ring[found][0];
+    y += c_ring[found][1];
+    b = c_ring_of[(ddx + 1) * 3 + (ddy + 1)];
+}
+
+__device__ __forceinline__ long long floor_div(long long a, long long b) {  // b > 0
+    return a >= 0 ? a / b : -((-a + b - 1) / b);
+}
+
+// 8-connected Euler number contributions of row pair (a above b) over the
+// zero-padded columns 0..w (bit quads)
+__device__ __forceinline__ int quads_pair(uint64_t a, uint64_t b, int w) {
+    const uint64_t vm = (w >= 63) ? ~0ull : ((2ull << w) - 1ull);
+    const uint64_t A0 = a << 1, A1 = a, B0 = b << 1, B1 = b;
+    const uint64_t s1 = A0 ^ A1, s2 = B0 ^ B1, c = (A0 & A1) | (B0 & B1);
+    const uint64_t one = (s1 ^ s2) & ~c & vm, three = (s1 ^ s2) & c & vm;
+    const uint64_t dg = ((A0 & B1 & ~A1 & ~B0) | (A1 & B0 & ~A0 & ~B1)) & vm;
+    int q = __popcll(one) - __popcll(three) - 2 * __popcll(dg);
+    if (w == 64) q += (int)(((a >> 63) ^ (b >> 63)) & 1ull);  // quad at padded column 64
+    return q;
+}
+
+__device__ __noinline__ void shape_phase_s(const uint64_t* rowmask, const uint64_t* km, int h,
+                                           int w, uint32_t n, long long gx0, long long gy0,
+                                           unsigned long long sLX, unsigned long long sLY,
+                                           uint8_t* scr, double* o) {
+    const unsigned lane = lane_id();
+    const double PI = 3.141592653589793, SQRT2 = 1.4142135623730951;
+    const double dn = (double)n;
+    uint8_t* state = scr;                   // [h][64]
+    uint8_t* ctop = scr + h * 64;           // [64]
+    uint8_t* cbot = ctop + 64;              // [64]
+    uint8_t* hv = cbot + 64;                // hull chain (x, y) bytes, <= 2 x 128 entries
+    // ---- column extremes of all pixels, walk-state bytes cleared
+    for (int x = lane; x < 64; x += 32) {
+        uint32_t t = 255, bt = 255;
+        if (x < w)
+            for (int y = 0; y < h; ++y)
+                if ((rowmask[y] >> x) & 1ull) {
+                    if (t == 255) t = (uint32_t)y;
+                    bt = (uint32_t)y;
+                }
+        ctop[x] = (uint8_t)t;
+        cbot[x] = (uint8_t)bt;
+    }
+    for (int i = lane; i < h * 16; i += 32) reinterpret_cast<uint32_t*>(state)[i] = 0u;
+    uint32_t kc = 0;
+    for (int y = lane; y < h; y += 32) kc += __popcll(km[y]);
+    kc = warp_sum(kc);
+    // ---- Euler number (bit quads over the padded window)
+    int q = 0;
+    for (int y = lane; y <= h; y += 32) q += quads_pair(y ? rowmask[y - 1] : 0ull, y < h ? rowmask[y] : 0ull, w);
+    q = warp_sum(q);
+    __syncwarp();
+    // ---- lane 0: contour walk (perimeter) and the monotone-chain hull
+    // lane 1..3: ellipse sums in pixel order (sequential, no FMA)
+    double per = 4.0, ell = 0;
+    int nv = 0;
+    const double cx = (double)((unsigned long long)gx0 * n + sLX) / dn;
+    const double cy = (double)((unsigned long long)gy0 * n + sLY) / dn;
+    if (lane == 0) {
+        if (n > 1 && kc > 1) {
+            int sx = 0, sy = 0;
+            while (!km[sy]) ++sy;
+            sx = __ffsll((long long)km[sy]) - 1;
+            int x = sx, y = sy, b = 0;
+            for (;;) {  // first repeated state starts the cycle (contour.cpp:98-106)
+                uint8_t& cell = state[y * 64 + x];
+                if ((cell >> b) & 1u) break;
+                cell |= (uint8_t)(1u << b);
+                walk_step(km, h, w, x, y, b);
+            }
+            const int x0 = x, y0 = y, b0 = b;
+            per = 0;
+            do {
+                const int px = x, py = y;
+                walk_step(km, h, w, x, y, b);
+                per = __dadd_rn(per, (abs(x - px) + abs(y - py) == 2) ? SQRT2 : 1.0);
+            } while (x != x0 || y != y0 || b != b0);
+        }
+        // hull of the column extremes (== hull of all pixels), hull.cpp:17-55
+        auto cross = [&](int i, int j, int px, int py) -> long long {  // (v_i, v_j, p)
+            return (long long)(hv[2 * j] - hv[2 * i]) * (py - hv[2 * i + 1]) -
+                   (long long)(hv[2 * j + 1] - hv[2 * i + 1]) * (px - hv[2 * i]);
+        };
+        int npt = 0, fx = -1, fy = -1, lx = -1, ly = -1;
+        for (int x = 0; x < w; ++x)
+            if (ctop[x] != 255) {
+                npt += (ctop[x] == cbot[x]) ? 1 : 2;
+                if (fx < 0) {
+                    fx = x;
+                    fy = ctop[x];
+                }
+                lx = x;
+                ly = cbot[x];
+            }
+        if (npt <= 2) {  // returned as they are
+            int k = 0;
+            for (int x = 0; x < w; ++x)
+                if (ctop[x] != 255) {
+                    hv[2 * k] = (uint8_t)x;
+                    hv[2 * k + 1] = ctop[x];
+                    ++k;
+                    if (cbot[x] != ctop[x]) {
+                        hv[2 * k] = (uint8_t)x;
+                        hv[2 * k + 1] = cbot[x];
+                        ++k;
+                    }
+                }
+            nv = k;
+        } else {
+            int k = 0;
+            auto push = [&](int px, int py, int lo) {
+                while (k >= lo && cross(k - 2, k - 1, px, py) <= 0) --k;
+                hv[2 * k] = (uint8_t)px;
+                hv[2 * k + 1] = (uint8_t)py;
+                ++k;
+            };
+            for (int x = 0; x < w; ++x)  // lower chain, (x, y) ascending
+                if (ctop[x] != 255) {
+                    push(x, ctop[x], 2);
+                    if (cbot[x] != ctop[x]) push(x, cbot[x], 2);
+                }
+            const int lower = k + 1;
+            bool skip_last = true;  // the last point is already on the chain
+            for (int x = w - 1; x >= 0; --x)  // upper chain, descending
+                if (ctop[x] != 255) {
+                    if (cbot[x] != ctop[x]) {
+                        if (!skip_last) push(x, cbot[x], lower);
+                        skip_last = false;
+                        push(x, ctop[x], lower);
+                    } else {
+                        if (!skip_last) push(x, ctop[x], lower);
+                        skip_last = false;
+                    }
+                }
+            k -= 1;
+            if (k < 3) {  // all collinear: the two end points
+                hv[0] = (uint8_t)fx;
+                hv[1] = (uint8_t)fy;
+                hv[2] = (uint8_t)lx;
+                hv[3] = (uint8_t)ly;
+                k = 2;
+            }
+            nv = k;
+        }
+    } else if (lane <= 3) {
+        // m20 (lane 1), m02 (lane 2), m11 (lane 3), pixel order
+        for (int y = 0; y < h; ++y) {
+            uint64_t m = rowmask[y];
+            const double dy = __dsub_rn((double)(gy0 + y), cy);
+            while (m) {
+                const int x = __ffsll((long long)m) - 1;
+                m &= m - 1;
+                const double dx = __dsub_rn((double)(gx0 + x), cx);
+                const double t = lane == 1 ? __dmul_rn(dx, dx) : lane == 2 ? __dmul_rn(dy, dy)
+                                                                          : __dmul_rn(dx, dy);
+                ell = __dadd_rn(ell, t);
+            }
+        }
+    }
+    per = __shfl_sync(kFull, per, 0);
+    nv = __shfl_sync(kFull, nv, 0);
+    const double m20 = __shfl_sync(kFull, ell, 1), m02 = __shfl_sync(kFull, ell, 2),
+                 m11 = __shfl_sync(kFull, ell, 3);
+    __syncwarp();
+    // ---- convex area: lattice points inside or on the hull, rows in parallel
+    unsigned long long carea = 0;
+    if (nv >= 3)
+        for (int y = lane; y < h; y += 32) {
+            long long xl = 0, xr = w - 1;
+            for (int i = 0; i < nv && xl <= xr; ++i) {
+                const int j = i + 1 < nv ? i + 1 : 0;
+                const long long ax = hv[2 * i], ay = hv[2 * i + 1], bx = hv[2 * j], by = hv[2 * j + 1];
+                const long long B = by - ay, A = (bx - ax) * (y - ay) + B * ax;  // A - B x >= 0
+                if (B > 0) xr = min(xr, floor_div(A, B));
+                else if (B < 0) xl = max(xl, -floor_div(A, -B));
+                else if (A < 0) xr = -1;
+            }
+            if (xr >= xl) carea += (unsigned long long)(xr - xl + 1);
+        }
+    carea = warp_sum(carea);
+    // ---- Feret diameters over the hull vertices
+    double fmx = 0, fmn = 1.79769313486231570815e308;
+    for (int p = lane; p < nv * nv; p += 32) {
+        const int i = p / nv, j = p - i * nv;
+        if (j > i)
+            fmx = fmax(fmx, hypot((double)(hv[2 * i] - hv[2 * j]), (double)(hv[2 * i + 1] - hv[2 * j + 1])));
+    }
+    for (int i = lane; i < nv && nv > 2; i += 32) {
+        const int j = i + 1 < nv ? i + 1 : 0;
+        const long long ex = hv[2 * j] - hv[2 * i], ey = hv[2 * j + 1] - hv[2 * i + 1];
+        long long mc = 0;
+        for (int k = 0; k < nv; ++k) {
+            const long long c = ex * (hv[2 * k + 1] - hv[2 * i + 1]) - ey * (hv[2 * k] - hv[2 * i]);
+            mc = max(mc, c < 0 ? -c : c);
+        }
+        fmn = fmin(fmn, (double)mc / hypot((double)ex, (double)ey));
+    }
+    fmx = warp_max(fmx);
+    fmn = warp_min(fmn);
+    if (nv <= 2) fmn = 0;
+    // ---- outputs (shape_feature_values order)
+    const double bw = (double)w, bh = (double)h;
+    double v = 0;
+    if (lane < 22) {
+        switch (lane) {
+            case 0: v = dn; break;
+            case 1: v = per; break;
+            case 2: v = (double)gx0; break;
+            case 3: v = (double)gy0; break;
+            case 4: v = bw; break;
+            case 5: v = bh; break;
+            case 6: v = cx; break;
+            case 7: v = cy; break;
+            case 8: v = n == 1 ? 1.0 : 4.0 * PI * dn / (per * per); break;
+            case 9: v = dn / (bw * bh); break;
+            case 10: v = bw / bh; break;
+            case 11: v = (double)carea; break;
+            case 12: v = carea ? dn / (double)carea : 0.0; break;
+            case 13: v = sqrt(4.0 * dn / PI); break;
+            case 19: v = (double)(q / 4); break;
+            case 20: v = fmx; break;
+            case 21: v = fmn; break;
+            default: {  // ellipse with the +1/12 correction
+                const double a = __dadd_rn(__ddiv_rn(m20, dn), 1.0 / 12.0);
+                const double c = __dadd_rn(__ddiv_rn(m02, dn), 1.0 / 12.0);
+                const double bb = __ddiv_rn(m11, dn);
+                const double amc = __dsub_rn(a, c);
+                const double disc = sqrt(__dadd_rn(__ddiv_rn(__dmul_rn(amc, amc), 4.0), __dmul_rn(bb, bb)));
+                const double hs = __ddiv_rn(__dadd_rn(a, c), 2.0);
+                const double l1 = __dadd_rn(hs, disc), l2 = __dsub_rn(hs, disc);
+                const double maj = 4.0 * sqrt(fmax(0.0, l1)), mnr = 4.0 * sqrt(fmax(0.0, l2));
+                if (lane == 14) v = maj;
+                else if (lane == 15) v = mnr;
+                else if (lane == 16) v = l1 > 0 ? sqrt(fmax(0.0, 1.0 - l2 / l1)) : 0.0;
+                else if (lane == 17) v = mnr > 0 ? maj / mnr : 0.0;
+                else {
+                    double th = 0.5 * atan2(2.0 * bb, amc);
+                    if (th <= -PI / 2.0) th += PI;
+                    v = th;
+                }
+            }
+        }
+        o[lane] = v;
+    } else if (lane < 30) {  // extrema (x, y) pairs, lanes 22..29 -> pairs 0..7
+        const int e = lane - 22;
+        const uint64_t r0 = rowmask[0], rl = rowmask[h - 1];
+        int ex = 0, ey = 0;
+        switch (e) {
+            case 0: ex = __ffsll((long long)r0) - 1; ey = 0; break;
+            case 1: ex = 63 - __clzll((long long)r0); ey = 0; break;
+            case 2: ex = w - 1; ey = ctop[w - 1]; break;
+            case 3: ex = w - 1; ey = cbot[w - 1]; break;
+            case 4: ex = 63 - __clzll((long long)rl); ey = h - 1; break;
+            case 5: ex = __ffsll((long long)rl) - 1; ey = h - 1; break;
+            case 6: ex = 0; ey = cbot[0]; break;
+            default: ex = 0; ey = ctop[0]; break;
+        }
+        o[22 + 2 * e] = (double)(gx0 + ex);
+        o[23 + 2 * e] = (double)(gy0 + ey);
+    }
+    __syncwarp();
+}
 
 // GLCM group for an S window with ng <= 64 (kGlHist): discretize (texture.cpp:45-53,
 // exact integer floor) into a level raster, count pair keys per sorted angle
@@ -840,6 +1143,88 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     uint32_t vmin = 0, vmax = 0;
     bool have_minmax = false;
 
+    // K (largest 8-connected component, row-major tie-break) and E (4-connected
+    // exterior of the window cells outside K) as row masks (lanes = rows); false:
+    // run capacity exceeded, the ROI was re-queued to the large-ROI kernel
+    auto edge_ke = [&](uint64_t& k0, uint64_t& k1, uint64_t& e0, uint64_t& e1) -> bool {
+        uint64_t* km = (uint64_t*)(base + L.kmask);
+        uint64_t* em = (uint64_t*)(base + L.emask);
+        bool fast = w <= 62;
+        k0 = m0;
+        k1 = m1;
+        e0 = e1 = 0;
+        if (fast) {
+            // 4-connected exterior flood of the free cells, seeded on the border
+            const uint64_t f0 = ((int)lane < h) ? (~m0 & wm) : 0ull;
+            const uint64_t f1 = ((int)lane + 32 < h) ? (~m1 & wm) : 0ull;
+            const uint64_t side = 1ull | (1ull << (w - 1));
+            e0 = run_fill(f0, (lane == 0 || (int)lane == h - 1) ? f0 : (f0 & side));
+            e1 = run_fill(f1, ((int)lane + 32 == h - 1) ? f1 : (f1 & side));
+            for (int it = 0; it < 64 * TH; ++it) {
+                const uint64_t up0 = __shfl_up_sync(kFull, e0, 1);
+                const uint64_t dn0 = __shfl_down_sync(kFull, e0, 1);
+                const uint64_t up1 = __shfl_up_sync(kFull, e1, 1);
+                const uint64_t dn1 = __shfl_down_sync(kFull, e1, 1);
+                const uint64_t l31 = __shfl_sync(kFull, e0, 31), f32 = __shfl_sync(kFull, e1, 0);
+                const uint64_t a0 = (lane == 0 ? 0ull : up0) | (lane == 31 ? f32 : dn0);
+                const uint64_t a1 = (lane == 0 ? l31 : up1) | (lane == 31 ? 0ull : dn1);
+                const uint64_t n0 = run_fill(f0, e0 | (a0 & f0));
+                const uint64_t n1 = run_fill(f1, e1 | (a1 & f1));
+                const bool ch = (n0 != e0) || (n1 != e1);
+                e0 = n0;
+                e1 = n1;
+                if (!__any_sync(kFull, ch)) break;
+            }
+            // holes: free cells not reached
+            const bool hole = ((f0 & ~e0) | (f1 & ~e1)) != 0ull;
+            // 8-connected Euler number of the padded window (bit quads)
+            int q = 0;
+            {
+                const uint64_t vm = (w >= 63) ? ~0ull : ((2ull << w) - 1ull);  // quads 0..w
+                auto quads = [&](uint64_t a, uint64_t b) {
+                    const uint64_t A0 = a << 1, A1 = a, B0 = b << 1, B1 = b;  // padded
+                    const uint64_t s1 = A0 ^ A1, s2 = B0 ^ B1, c = (A0 & A1) | (B0 & B1);
+                    const uint64_t one = (s1 ^ s2) & ~c & vm, three = (s1 ^ s2) & c & vm;
+                    const uint64_t dg = ((A0 & B1 & ~A1 & ~B0) | (A1 & B0 & ~A0 & ~B1)) & vm;
+                    return __popcll(one) - __popcll(three) - 2 * __popcll(dg);
+                };
+                const uint64_t pm0 = __shfl_up_sync(kFull, m0, 1), pm1 = __shfl_up_sync(kFull, m1, 1);
+                const uint64_t l31 = __shfl_sync(kFull, m0, 31);
+                // row pairs (y-1, y) for y = 0..h  (rows -1 and h are empty)
+                if ((int)lane <= h) q += quads(lane == 0 ? 0ull : pm0, (int)lane < h ? m0 : 0ull);
+                if ((int)lane + 32 <= h)
+                    q += quads(lane == 0 ? l31 : pm1, (int)lane + 32 < h ? m1 : 0ull);
+                q = warp_sum(q);
+            }
+            fast = !__any_sync(kFull, hole) && q == 4;  // one component, no holes
+        }
+        if (!fast) {
+            if ((int)lane < h) km[lane] = m0;
+            if ((int)lane + 32 < h) km[lane + 32] = m1;
+            __syncwarp();
+            const bool ok = edge_sets_slow(rowmask, h, w, km, em, (uint32_t*)(base + L.runoff),
+                                           (uint16_t*)(base + L.rs), (uint16_t*)(base + L.re),
+                                           (uint32_t*)(base + L.parent),
+                                           (uint32_t*)(base + L.rsize), (uint32_t)RUNMAX);
+            if (!ok) {  // run capacity: re-queue this ROI to the general path
+                if (lane == 0) {
+                    const uint32_t pos = atomicAdd(&ctl->overflow_count, 1u);
+                    rl.overflow[pos] = J.row;
+                }
+                __syncwarp();
+                return false;
+            }
+            k0 = (int)lane < h ? km[lane] : 0ull;
+            k1 = (int)lane + 32 < h ? km[lane + 32] : 0ull;
+            e0 = (int)lane < h ? em[lane] : 0ull;
+            e1 = (int)lane + 32 < h ? em[lane + 32] : 0ull;
+            __syncwarp();
+        }
+        return true;
+    };
+    uint64_t ks0 = 0, ks1 = 0, e_unused0 = 0, e_unused1 = 0;  // K rows kept for the shape group
+    bool have_k = false;
+
     // ----------------------------------------------------------- intensity
     PT(0);
     if (cfg.col_int >= 0) {
@@ -993,77 +1378,11 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
         PT(2);
         double e_mean = 0, e_min = 0, e_max = 0, e_std = 0, e_int = 0;
         {
-            uint64_t* km = (uint64_t*)(base + L.kmask);
-            uint64_t* em = (uint64_t*)(base + L.emask);
-            bool fast = w <= 62;
-            uint64_t k0 = m0, k1 = m1, e0 = 0, e1 = 0;
-            if (fast) {
-                // 4-connected exterior flood of the free cells, seeded on the border
-                const uint64_t f0 = ((int)lane < h) ? (~m0 & wm) : 0ull;
-                const uint64_t f1 = ((int)lane + 32 < h) ? (~m1 & wm) : 0ull;
-                const uint64_t side = 1ull | (1ull << (w - 1));
-                e0 = run_fill(f0, (lane == 0 || (int)lane == h - 1) ? f0 : (f0 & side));
-                e1 = run_fill(f1, ((int)lane + 32 == h - 1) ? f1 : (f1 & side));
-                for (int it = 0; it < 64 * TH; ++it) {
-                    const uint64_t up0 = __shfl_up_sync(kFull, e0, 1);
-                    const uint64_t dn0 = __shfl_down_sync(kFull, e0, 1);
-                    const uint64_t up1 = __shfl_up_sync(kFull, e1, 1);
-                    const uint64_t dn1 = __shfl_down_sync(kFull, e1, 1);
-                    const uint64_t l31 = __shfl_sync(kFull, e0, 31), f32 = __shfl_sync(kFull, e1, 0);
-                    const uint64_t a0 = (lane == 0 ? 0ull : up0) | (lane == 31 ? f32 : dn0);
-                    const uint64_t a1 = (lane == 0 ? l31 : up1) | (lane == 31 ? 0ull : dn1);
-                    const uint64_t n0 = run_fill(f0, e0 | (a0 & f0));
-                    const uint64_t n1 = run_fill(f1, e1 | (a1 & f1));
-                    const bool ch = (n0 != e0) || (n1 != e1);
-                    e0 = n0;
-                    e1 = n1;
-                    if (!__any_sync(kFull, ch)) break;
-                }
-                // holes: free cells not reached
-                const bool hole = ((f0 & ~e0) | (f1 & ~e1)) != 0ull;
-                // 8-connected Euler number of the padded window (bit quads)
-                int q = 0;
-                {
-                    const uint64_t vm = (w >= 63) ? ~0ull : ((2ull << w) - 1ull);  // quads 0..w
-                    auto quads = [&](uint64_t a, uint64_t b) {
-                        const uint64_t A0 = a << 1, A1 = a, B0 = b << 1, B1 = b;  // padded
-                        const uint64_t s1 = A0 ^ A1, s2 = B0 ^ B1, c = (A0 & A1) | (B0 & B1);
-                        const uint64_t one = (s1 ^ s2) & ~c & vm, three = (s1 ^ s2) & c & vm;
-                        const uint64_t dg = ((A0 & B1 & ~A1 & ~B0) | (A1 & B0 & ~A0 & ~B1)) & vm;
-                        return __popcll(one) - __popcll(three) - 2 * __popcll(dg);
-                    };
-                    const uint64_t pm0 = __shfl_up_sync(kFull, m0, 1), pm1 = __shfl_up_sync(kFull, m1, 1);
-                    const uint64_t l31 = __shfl_sync(kFull, m0, 31);
-                    // row pairs (y-1, y) for y = 0..h  (rows -1 and h are empty)
-                    if ((int)lane <= h) q += quads(lane == 0 ? 0ull : pm0, (int)lane < h ? m0 : 0ull);
-                    if ((int)lane + 32 <= h)
-                        q += quads(lane == 0 ? l31 : pm1, (int)lane + 32 < h ? m1 : 0ull);
-                    q = warp_sum(q);
-                }
-                fast = !__any_sync(kFull, hole) && q == 4;  // one component, no holes
-            }
-            if (!fast) {
-                if ((int)lane < h) km[lane] = m0;
-                if ((int)lane + 32 < h) km[lane + 32] = m1;
-                __syncwarp();
-                const bool ok = edge_sets_slow(rowmask, h, w, km, em, (uint32_t*)(base + L.runoff),
-                                               (uint16_t*)(base + L.rs), (uint16_t*)(base + L.re),
-                                               (uint32_t*)(base + L.parent),
-                                               (uint32_t*)(base + L.rsize), (uint32_t)RUNMAX);
-                if (!ok) {  // run capacity: re-queue this ROI to the general path
-                    if (lane == 0) {
-                        const uint32_t pos = atomicAdd(&ctl->overflow_count, 1u);
-                        rl.overflow[pos] = J.row;
-                    }
-                    __syncwarp();
-                    return;
-                }
-                k0 = (int)lane < h ? km[lane] : 0ull;
-                k1 = (int)lane + 32 < h ? km[lane + 32] : 0ull;
-                e0 = (int)lane < h ? em[lane] : 0ull;
-                e1 = (int)lane + 32 < h ? em[lane + 32] : 0ull;
-                __syncwarp();
-            }
+            uint64_t k0, k1, e0, e1;
+            if (!edge_ke(k0, k1, e0, e1)) return;
+            ks0 = k0;
+            ks1 = k1;
+            have_k = true;
             // edge = K & (4-neighbour in E, or on the window border)
             const uint64_t eu0 = __shfl_up_sync(kFull, e0, 1), ed0 = __shfl_down_sync(kFull, e0, 1);
             const uint64_t eu1 = __shfl_up_sync(kFull, e1, 1), ed1 = __shfl_down_sync(kFull, e1, 1);
@@ -1189,6 +1508,15 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
         __syncwarp();
     }
 
+    // ---------------------------------------------------------------- shape
+    if (cfg.col_shape >= 0) {
+        if (!have_k && !edge_ke(ks0, ks1, e_unused0, e_unused1)) return;
+        uint64_t* km = (uint64_t*)(base + L.kmask);
+        if ((int)lane < h) km[lane] = ks0;
+        if ((int)lane + 32 < h) km[lane + 32] = ks1;
+        __syncwarp();
+        shape_phase_s(rowmask, km, h, w, n, gx0, gy0, sLX, sLY, base + L.shp, orow + cfg.col_shape);
+    }
     // ------------------------------------------------------------- moments
     PT(3);
     if (cfg.col_mom >= 0) {

@@ -134,18 +134,24 @@ static void device_cases() {
         CHECK(s.images == 1 && s.rows == 2 && s.completed_with_errors() && s.failed_pairs == 2);
     }
     {  // groups without a device kernel fail loudly per pair (no CPU fallback)
-        const auto d = fresh_dir("fxg_engine_shape");
+        const auto d = fresh_dir("fxg_engine_glrlm");
         write_simple_pair(d);
         ExtractionConfig c;
         c.intensity_dir = d / "int";
         c.mask_dir = d / "seg";
         c.output_path = d / "f.csv";
-        c.features = {"shape"};
+        c.features = {"glrlm"};
         const RunSummary s = run(c);
         CHECK(s.images == 0 && s.failed_pairs == 1);
         PixelCloud pc;
         pc.pixels = {{1, 1, 5}};
-        CHECK_THROWS_AS(compute_roi_features(pc, {"shape"}, resolve_profile("default")), ConfigError);
+        CHECK_THROWS_AS(compute_roi_features(pc, {"glszm"}, resolve_profile("default")), ConfigError);
+    }
+    {  // the shape group runs on the device: a 1-pixel cloud reports the conventions
+        PixelCloud pc;
+        pc.pixels = {{7, 3, 5}};
+        const std::vector<double> v = compute_roi_features(pc, {"shape"}, resolve_profile("default"));
+        CHECK(v.size() == 38 && v[0] == 1.0 && v[1] == 4.0 && v[2] == 7.0 && v[3] == 3.0);
     }
     {  // rerun idempotent (:174-182) and per-ROI operator == image-level row
         const auto d = fresh_dir("fxg_engine_idem");

@@ -26,8 +26,17 @@ EXACT_INTENSITY = ["mean", "median", "mode", "min", "max", "range", "median_ad",
                    "p10", "p25", "p75", "p90", "p99", "energy", "rms", "qcod",
                    "integrated_intensity", "edge_mean", "edge_min", "edge_max",
                    "edge_integrated", "weighted_centroid_x", "weighted_centroid_y"]
-EXACT = {"intensity_" + n for n in EXACT_INTENSITY}
-UNIT_FLOOR = {"intensity_skewness", "intensity_hyperskewness"}
+# shape: everything but orientation (atan2) and the Feret diameters (hypot),
+# whose libm implementations differ in the last ulp between CUDA and glibc
+EXACT_SHAPE = ["area", "perimeter", "bbox_x", "bbox_y", "bbox_w", "bbox_h", "centroid_x",
+               "centroid_y", "circularity", "extent", "aspect_ratio", "convex_area", "solidity",
+               "equivalent_diameter", "major_axis_len", "minor_axis_len", "eccentricity",
+               "elongation", "euler_number"] + [
+               f"extrema_{c}_{a}" for c in ("topleft", "topright", "righttop", "rightbottom",
+                                            "bottomright", "bottomleft", "leftbottom", "lefttop")
+               for a in ("x", "y")]
+EXACT = {"intensity_" + n for n in EXACT_INTENSITY} | {"shape_" + n for n in EXACT_SHAPE}
+UNIT_FLOOR = {"intensity_skewness", "intensity_hyperskewness", "shape_orientation"}
 HARALICK_UNIT = ("clushade", "corr", "infomeas1")
 
 

@@ -15,7 +15,7 @@ from oracle import make_params as oparams
 
 pytestmark = pytest.mark.gpu
 
-GROUPS = ["intensity", "moments", "glcm"]
+GROUPS = ["intensity", "shape", "moments", "glcm"]
 
 
 def both_params(profile="default", **over):
