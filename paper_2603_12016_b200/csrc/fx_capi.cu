@@ -33,6 +33,8 @@ void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
                   const CUtensorMap& tmap72, int tma40, int tma72, DevImage img, RoiList rl,
                   Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg);
 cudaError_t roi_b_setup();
+void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
+                         double* out);
 BLayout make_blayout(uint32_t H, uint32_t WPR, uint32_t NMAX, uint32_t RUNMAX, uint32_t NB,
                      unsigned long long CELLS);
 void launch_roi_b(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
@@ -86,6 +88,10 @@ struct fx_ctx {
     size_t stage_elems = 0;  // per raster
     uint32_t* d_blab = nullptr;  // batch output labels (host outputs)
     size_t blab_cap = 0;
+    // shape group: per-ROI staged row masks (S ROIs) for k_shape_serial
+    uint64_t* d_shape_rows = nullptr;
+    uint32_t* d_shape_hdr = nullptr;
+    size_t shape_cap = 0;
     // staging for host inputs / outputs
     uint16_t* d_img = nullptr;  // intensity then labels, pitched
     size_t img_pitch = 0, img_rows_cap = 0;
@@ -380,6 +386,23 @@ struct DebugHost {
 
 // Label scan of one image (or band) into the ctx's label table, in global
 // coordinates (image origin added).  reset clears the table first.
+// shape staging for roi_cap ROIs: 128 row masks each, headers zeroed (consumed
+// and reset by k_shape_serial)
+int ensure_shape(fx_ctx* c) {
+    if (c->roi_cap <= c->shape_cap) return FX_OK;
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    cudaFree(c->d_shape_rows);
+    cudaFree(c->d_shape_hdr);
+    c->d_shape_rows = nullptr;
+    c->d_shape_hdr = nullptr;
+    c->shape_cap = 0;
+    CK(cudaMalloc(&c->d_shape_rows, c->roi_cap * 128 * sizeof(uint64_t)));
+    CK(cudaMalloc(&c->d_shape_hdr, c->roi_cap * sizeof(uint32_t)));
+    CK(cudaMemset(c->d_shape_hdr, 0, c->roi_cap * sizeof(uint32_t)));
+    c->shape_cap = c->roi_cap;
+    return FX_OK;
+}
+
 // reset: start from an empty table (a memset only when the last use left it dirty).
 int scan_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, bool reset) {
     if (reset && !c->table_clean) {
@@ -425,7 +448,13 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
                     uint32_t own_y1, unsigned groups, const fx_texture_params& p, double* out_dev,
                     size_t cap_rois, size_t* n_rois, const DebugOut* dbg_dev,
                     uint32_t* slot_base = nullptr) {
-    const FeatCfg cfg = make_cfg(groups, p);
+    FeatCfg cfg = make_cfg(groups, p);
+    if (cfg.col_shape >= 0) {
+        const int rs = ensure_shape(c);
+        if (rs) return rs;
+        cfg.shape_rows = c->d_shape_rows;
+        cfg.shape_hdr = c->d_shape_hdr;
+    }
     const int vrc = validate_texture(groups, p);
     RoiList rl = roi_list(c);
     cudaStream_t s = c->stream;
@@ -472,6 +501,12 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         cudaStreamSynchronize(s);
         return set_error(FX_E_CAPACITY, "output capacity " + std::to_string(cap_rois) +
                                             " < " + std::to_string(hc.n_rois) + " ROIs");
+    }
+    if (cfg.col_shape >= 0) {  // serial shape columns of the S ROIs, before k_roi_b
+        const int n_s = (int)(hc.class_count[kClassS0] + hc.class_count[kClassS1] +
+                              hc.class_count[kClassS2]);
+        Launch l(c, "k_shape_serial");
+        launch_shape_serial(n_s, s, rl, c->d_ctl, cfg, out_dev);
     }
     {
         // large ROIs + S overflow: one CTA per ROI; the slabs' histograms are kept
@@ -713,6 +748,8 @@ int fx_ctx_destroy(fx_ctx* c) {
         if (c->ev_free[b]) cudaEventDestroy(c->ev_free[b]);
     }
     cudaFree(c->d_blab);
+    cudaFree(c->d_shape_rows);
+    cudaFree(c->d_shape_hdr);
     cudaFree(c->d_img);
     cudaFree(c->d_out);
     cudaFree(c->d_lscratch);

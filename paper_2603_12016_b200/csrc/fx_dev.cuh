@@ -136,6 +136,8 @@ struct FeatCfg {
     int ng, symmetric, n_angles;
     int angle[8];                    // sorted (engine.cpp:36-40)
     int dx[8], dy[8];                // angle_offset (texture.cpp:15-23)
+    uint64_t* shape_rows;            // shape: per ROI rank, 64 rows of all pixels + 64 of K
+    uint32_t* shape_hdr;             // shape: per ROI rank, h | w << 8 | staged << 16
 };
 
 // GLCM variants of the S kernels: none, key sort (ng > 64), shared histogram

@@ -39,6 +39,7 @@ __device__ unsigned long long g_phase_clk[16];
 #define PT(k)
 #endif
 
+
 namespace fxg {
 
 namespace {
@@ -51,7 +52,6 @@ struct SLayout {
     uint32_t kmask, emask, runoff, rs, re, parent, rsize;  // B: edge slow path
     uint32_t lvl, keys, keys2, gcnt, marg;     // B: glcm, sort path (ng > 64)
     uint32_t lmap, hist, list;                 // B: glcm, histogram path (ng <= 64)
-    uint32_t shp;                              // B: shape (after K rows at kmask)
     uint32_t bytes;
 };
 
@@ -83,9 +83,8 @@ __host__ __device__ constexpr SLayout make_slayout(uint32_t TW, uint32_t TH, uin
     L.parent = al(L.re + RUNMAX * 2, 16);
     L.rsize = al(L.parent + RUNMAX * 4, 16);
     const uint32_t e_edge = L.rsize + RUNMAX * 4;
-    // shape: contour-walk state bytes [TH][64], column extremes, hull vertices
-    L.shp = L.runoff;
-    const uint32_t e_shape = L.shp + TH * 64 + 128 + 2 * 256;  // hull stack <= 2 x 128 points
+    // shape: K rows at kmask (staged to global for k_shape_serial)
+    const uint32_t e_shape = L.emask;
     L.lvl = B;
     L.keys = al(L.lvl + NMAX, 16);
     L.keys2 = al(L.keys + NMAX * 2, 16);
@@ -418,22 +417,28 @@ __device__ __forceinline__ bool k_at(const uint64_t* km, int h, int w, int x, in
     return x >= 0 && x < w && y >= 0 && y < h && ((km[y] >> x) & 1ull);
 }
 
-// one step of the Moore walk: position (x, y), backtrack ring index b
+// one step of the Moore walk: position (x, y), backtrack ring index b.  The 8
+// neighbours come from three K rows as one byte in ring order; the next
+// direction is the first set bit after b (rotate + ffs).
+__device__ __forceinline__ uint32_t three_bits(uint64_t row, int x) {  // cols x-1, x, x+1
+    return (uint32_t)((x > 0 ? (row >> (x - 1)) : (row << 1)) & 7ull);
+}
 __device__ __forceinline__ void walk_step(const uint64_t* km, int h, int w, int& x, int& y, int& b) {
-    int found = -1;
-#pragma unroll 1
-    for (int k = 1; k <= 8; ++k) {
-        const int idx = (b + k) & 7;
-        if (k_at(km, h, w, x + c_ring[idx][0], y + c_ring[idx][1])) {
-            found = idx;
-            break;
-        }
-    }
+    const uint32_t u = y > 0 ? three_bits(km[y - 1], x) : 0u;
+    const uint32_t m = three_bits(km[y], x);
+    const uint32_t d = y + 1 < h ? three_bits(km[y + 1], x) : 0u;
+    // ring: W, NW, N, NE, E, SE, S, SW
+    const uint32_t nb = (m & 1u) | ((u & 1u) << 1) | ((u & 2u) << 1) | ((u & 4u) << 1) |
+                        ((m & 4u) << 2) | ((d & 4u) << 3) | ((d & 2u) << 5) | ((d & 1u) << 7);
+    const int st = (b + 1) & 7;
+    const uint32_t rot = ((nb >> st) | (nb << (8 - st))) & 0xffu;
+    const int found = (st + __ffs(rot) - 1) & 7;
     const int prev = (found + 7) & 7;
     const int ddx = c_ring[prev][0] - c_ring[found][0], ddy = c_ring[prev][1] - c_ring[found][1];
     x += c_ring[found][0];
     y += c_ring[found][1];
     b = c_ring_of[(ddx + 1) * 3 + (ddy + 1)];
+    (void)w;
 }
 
 __device__ __forceinline__ long long floor_div(long long a, long long b) {  // b > 0
@@ -453,247 +458,327 @@ __device__ __forceinline__ int quads_pair(uint64_t a, uint64_t b, int w) {
     return q;
 }
 
+// Warp part of the S shape group: the columns computable in parallel (area,
+// bbox, centroid, extent, aspect ratio, equivalent diameter, Euler number,
+// extrema) and the staging of the row masks (all pixels, K) for k_shape_serial.
 __device__ __noinline__ void shape_phase_s(const uint64_t* rowmask, const uint64_t* km, int h,
                                            int w, uint32_t n, long long gx0, long long gy0,
                                            unsigned long long sLX, unsigned long long sLY,
-                                           uint8_t* scr, double* o) {
+                                           uint32_t row, const FeatCfg& cfg, double* o) {
     const unsigned lane = lane_id();
-    const double PI = 3.141592653589793, SQRT2 = 1.4142135623730951;
+    const double PI = 3.141592653589793;
     const double dn = (double)n;
-    uint8_t* state = scr;                   // [h][64]
-    uint8_t* ctop = scr + h * 64;           // [64]
-    uint8_t* cbot = ctop + 64;              // [64]
-    uint8_t* hv = cbot + 64;                // hull chain (x, y) bytes, <= 2 x 128 entries
-    // ---- column extremes of all pixels, walk-state bytes cleared
-    for (int x = lane; x < 64; x += 32) {
-        uint32_t t = 255, bt = 255;
-        if (x < w)
-            for (int y = 0; y < h; ++y)
-                if ((rowmask[y] >> x) & 1ull) {
-                    if (t == 255) t = (uint32_t)y;
-                    bt = (uint32_t)y;
-                }
-        ctop[x] = (uint8_t)t;
-        cbot[x] = (uint8_t)bt;
-    }
-    for (int i = lane; i < h * 16; i += 32) reinterpret_cast<uint32_t*>(state)[i] = 0u;
-    uint32_t kc = 0;
-    for (int y = lane; y < h; y += 32) kc += __popcll(km[y]);
-    kc = warp_sum(kc);
-    // ---- Euler number (bit quads over the padded window)
+    // Euler number (bit quads over the padded window)
     int q = 0;
     for (int y = lane; y <= h; y += 32) q += quads_pair(y ? rowmask[y - 1] : 0ull, y < h ? rowmask[y] : 0ull, w);
     q = warp_sum(q);
+    // extrema: first/last pixel of the first/last row and column
+    int ct = 0x7fffffff, cb = -1, rt = 0x7fffffff, rb = -1;  // column 0, column w-1
+    for (int y = lane; y < h; y += 32) {
+        const uint64_t m = rowmask[y];
+        if (m & 1ull) {
+            ct = min(ct, y);
+            cb = max(cb, y);
+        }
+        if ((m >> (w - 1)) & 1ull) {
+            rt = min(rt, y);
+            rb = max(rb, y);
+        }
+    }
+    ct = warp_min(ct);
+    cb = warp_max(cb);
+    rt = warp_min(rt);
+    rb = warp_max(rb);
+    // stage the rows for the serial pass: [0..63] all pixels, [64..127] K
+    uint64_t* st = cfg.shape_rows + (size_t)row * 128;
+    for (int y = lane; y < h; y += 32) {
+        st[y] = rowmask[y];
+        st[64 + y] = km[y];
+    }
     __syncwarp();
-    // ---- lane 0: contour walk (perimeter) and the monotone-chain hull
-    // lane 1..3: ellipse sums in pixel order (sequential, no FMA)
-    double per = 4.0, ell = 0;
-    int nv = 0;
+    if (lane == 0) cfg.shape_hdr[row] = (uint32_t)h | ((uint32_t)w << 8) | (1u << 16);
+    const double bw = (double)w, bh = (double)h;
     const double cx = (double)((unsigned long long)gx0 * n + sLX) / dn;
     const double cy = (double)((unsigned long long)gy0 * n + sLY) / dn;
-    if (lane == 0) {
-        if (n > 1 && kc > 1) {
-            int sx = 0, sy = 0;
-            while (!km[sy]) ++sy;
-            sx = __ffsll((long long)km[sy]) - 1;
-            int x = sx, y = sy, b = 0;
-            for (;;) {  // first repeated state starts the cycle (contour.cpp:98-106)
-                uint8_t& cell = state[y * 64 + x];
-                if ((cell >> b) & 1u) break;
-                cell |= (uint8_t)(1u << b);
-                walk_step(km, h, w, x, y, b);
-            }
-            const int x0 = x, y0 = y, b0 = b;
-            per = 0;
-            do {
-                const int px = x, py = y;
-                walk_step(km, h, w, x, y, b);
-                per = __dadd_rn(per, (abs(x - px) + abs(y - py) == 2) ? SQRT2 : 1.0);
-            } while (x != x0 || y != y0 || b != b0);
-        }
-        // hull of the column extremes (== hull of all pixels), hull.cpp:17-55
-        auto cross = [&](int i, int j, int px, int py) -> long long {  // (v_i, v_j, p)
-            return (long long)(hv[2 * j] - hv[2 * i]) * (py - hv[2 * i + 1]) -
-                   (long long)(hv[2 * j + 1] - hv[2 * i + 1]) * (px - hv[2 * i]);
-        };
-        int npt = 0, fx = -1, fy = -1, lx = -1, ly = -1;
-        for (int x = 0; x < w; ++x)
-            if (ctop[x] != 255) {
-                npt += (ctop[x] == cbot[x]) ? 1 : 2;
-                if (fx < 0) {
-                    fx = x;
-                    fy = ctop[x];
-                }
-                lx = x;
-                ly = cbot[x];
-            }
-        if (npt <= 2) {  // returned as they are
-            int k = 0;
-            for (int x = 0; x < w; ++x)
-                if (ctop[x] != 255) {
-                    hv[2 * k] = (uint8_t)x;
-                    hv[2 * k + 1] = ctop[x];
-                    ++k;
-                    if (cbot[x] != ctop[x]) {
-                        hv[2 * k] = (uint8_t)x;
-                        hv[2 * k + 1] = cbot[x];
-                        ++k;
-                    }
-                }
-            nv = k;
-        } else {
-            int k = 0;
-            auto push = [&](int px, int py, int lo) {
-                while (k >= lo && cross(k - 2, k - 1, px, py) <= 0) --k;
-                hv[2 * k] = (uint8_t)px;
-                hv[2 * k + 1] = (uint8_t)py;
-                ++k;
-            };
-            for (int x = 0; x < w; ++x)  // lower chain, (x, y) ascending
-                if (ctop[x] != 255) {
-                    push(x, ctop[x], 2);
-                    if (cbot[x] != ctop[x]) push(x, cbot[x], 2);
-                }
-            const int lower = k + 1;
-            bool skip_last = true;  // the last point is already on the chain
-            for (int x = w - 1; x >= 0; --x)  // upper chain, descending
-                if (ctop[x] != 255) {
-                    if (cbot[x] != ctop[x]) {
-                        if (!skip_last) push(x, cbot[x], lower);
-                        skip_last = false;
-                        push(x, ctop[x], lower);
-                    } else {
-                        if (!skip_last) push(x, ctop[x], lower);
-                        skip_last = false;
-                    }
-                }
-            k -= 1;
-            if (k < 3) {  // all collinear: the two end points
-                hv[0] = (uint8_t)fx;
-                hv[1] = (uint8_t)fy;
-                hv[2] = (uint8_t)lx;
-                hv[3] = (uint8_t)ly;
-                k = 2;
-            }
-            nv = k;
-        }
-    } else if (lane <= 3) {
-        // m20 (lane 1), m02 (lane 2), m11 (lane 3), pixel order
-        for (int y = 0; y < h; ++y) {
-            uint64_t m = rowmask[y];
-            const double dy = __dsub_rn((double)(gy0 + y), cy);
-            while (m) {
-                const int x = __ffsll((long long)m) - 1;
-                m &= m - 1;
-                const double dx = __dsub_rn((double)(gx0 + x), cx);
-                const double t = lane == 1 ? __dmul_rn(dx, dx) : lane == 2 ? __dmul_rn(dy, dy)
-                                                                          : __dmul_rn(dx, dy);
-                ell = __dadd_rn(ell, t);
-            }
-        }
-    }
-    per = __shfl_sync(kFull, per, 0);
-    nv = __shfl_sync(kFull, nv, 0);
-    const double m20 = __shfl_sync(kFull, ell, 1), m02 = __shfl_sync(kFull, ell, 2),
-                 m11 = __shfl_sync(kFull, ell, 3);
-    __syncwarp();
-    // ---- convex area: lattice points inside or on the hull, rows in parallel
-    unsigned long long carea = 0;
-    if (nv >= 3)
-        for (int y = lane; y < h; y += 32) {
-            long long xl = 0, xr = w - 1;
-            for (int i = 0; i < nv && xl <= xr; ++i) {
-                const int j = i + 1 < nv ? i + 1 : 0;
-                const long long ax = hv[2 * i], ay = hv[2 * i + 1], bx = hv[2 * j], by = hv[2 * j + 1];
-                const long long B = by - ay, A = (bx - ax) * (y - ay) + B * ax;  // A - B x >= 0
-                if (B > 0) xr = min(xr, floor_div(A, B));
-                else if (B < 0) xl = max(xl, -floor_div(A, -B));
-                else if (A < 0) xr = -1;
-            }
-            if (xr >= xl) carea += (unsigned long long)(xr - xl + 1);
-        }
-    carea = warp_sum(carea);
-    // ---- Feret diameters over the hull vertices
-    double fmx = 0, fmn = 1.79769313486231570815e308;
-    for (int p = lane; p < nv * nv; p += 32) {
-        const int i = p / nv, j = p - i * nv;
-        if (j > i)
-            fmx = fmax(fmx, hypot((double)(hv[2 * i] - hv[2 * j]), (double)(hv[2 * i + 1] - hv[2 * j + 1])));
-    }
-    for (int i = lane; i < nv && nv > 2; i += 32) {
-        const int j = i + 1 < nv ? i + 1 : 0;
-        const long long ex = hv[2 * j] - hv[2 * i], ey = hv[2 * j + 1] - hv[2 * i + 1];
-        long long mc = 0;
-        for (int k = 0; k < nv; ++k) {
-            const long long c = ex * (hv[2 * k + 1] - hv[2 * i + 1]) - ey * (hv[2 * k] - hv[2 * i]);
-            mc = max(mc, c < 0 ? -c : c);
-        }
-        fmn = fmin(fmn, (double)mc / hypot((double)ex, (double)ey));
-    }
-    fmx = warp_max(fmx);
-    fmn = warp_min(fmn);
-    if (nv <= 2) fmn = 0;
-    // ---- outputs (shape_feature_values order)
-    const double bw = (double)w, bh = (double)h;
     double v = 0;
-    if (lane < 22) {
-        switch (lane) {
-            case 0: v = dn; break;
-            case 1: v = per; break;
-            case 2: v = (double)gx0; break;
-            case 3: v = (double)gy0; break;
-            case 4: v = bw; break;
-            case 5: v = bh; break;
-            case 6: v = cx; break;
-            case 7: v = cy; break;
-            case 8: v = n == 1 ? 1.0 : 4.0 * PI * dn / (per * per); break;
-            case 9: v = dn / (bw * bh); break;
-            case 10: v = bw / bh; break;
-            case 11: v = (double)carea; break;
-            case 12: v = carea ? dn / (double)carea : 0.0; break;
-            case 13: v = sqrt(4.0 * dn / PI); break;
-            case 19: v = (double)(q / 4); break;
-            case 20: v = fmx; break;
-            case 21: v = fmn; break;
-            default: {  // ellipse with the +1/12 correction
-                const double a = __dadd_rn(__ddiv_rn(m20, dn), 1.0 / 12.0);
-                const double c = __dadd_rn(__ddiv_rn(m02, dn), 1.0 / 12.0);
-                const double bb = __ddiv_rn(m11, dn);
-                const double amc = __dsub_rn(a, c);
-                const double disc = sqrt(__dadd_rn(__ddiv_rn(__dmul_rn(amc, amc), 4.0), __dmul_rn(bb, bb)));
-                const double hs = __ddiv_rn(__dadd_rn(a, c), 2.0);
-                const double l1 = __dadd_rn(hs, disc), l2 = __dsub_rn(hs, disc);
-                const double maj = 4.0 * sqrt(fmax(0.0, l1)), mnr = 4.0 * sqrt(fmax(0.0, l2));
-                if (lane == 14) v = maj;
-                else if (lane == 15) v = mnr;
-                else if (lane == 16) v = l1 > 0 ? sqrt(fmax(0.0, 1.0 - l2 / l1)) : 0.0;
-                else if (lane == 17) v = mnr > 0 ? maj / mnr : 0.0;
-                else {
-                    double th = 0.5 * atan2(2.0 * bb, amc);
-                    if (th <= -PI / 2.0) th += PI;
-                    v = th;
-                }
-            }
-        }
-        o[lane] = v;
-    } else if (lane < 30) {  // extrema (x, y) pairs, lanes 22..29 -> pairs 0..7
+    int col = -1;
+    switch (lane) {
+        case 0: v = dn; col = 0; break;
+        case 2: v = (double)gx0; col = 2; break;
+        case 3: v = (double)gy0; col = 3; break;
+        case 4: v = bw; col = 4; break;
+        case 5: v = bh; col = 5; break;
+        case 6: v = cx; col = 6; break;
+        case 7: v = cy; col = 7; break;
+        case 9: v = dn / (bw * bh); col = 9; break;
+        case 10: v = bw / bh; col = 10; break;
+        case 13: v = sqrt(4.0 * dn / PI); col = 13; break;
+        case 19: v = (double)(q / 4); col = 19; break;
+        default: break;
+    }
+    if (col >= 0) o[col] = v;
+    if (lane >= 22 && lane < 30) {  // extrema (x, y) pairs in regionprops order
         const int e = lane - 22;
         const uint64_t r0 = rowmask[0], rl = rowmask[h - 1];
         int ex = 0, ey = 0;
         switch (e) {
             case 0: ex = __ffsll((long long)r0) - 1; ey = 0; break;
             case 1: ex = 63 - __clzll((long long)r0); ey = 0; break;
-            case 2: ex = w - 1; ey = ctop[w - 1]; break;
-            case 3: ex = w - 1; ey = cbot[w - 1]; break;
+            case 2: ex = w - 1; ey = rt; break;
+            case 3: ex = w - 1; ey = rb; break;
             case 4: ex = 63 - __clzll((long long)rl); ey = h - 1; break;
             case 5: ex = __ffsll((long long)rl) - 1; ey = h - 1; break;
-            case 6: ex = 0; ey = cbot[0]; break;
-            default: ex = 0; ey = ctop[0]; break;
+            case 6: ex = 0; ey = cb; break;
+            default: ex = 0; ey = ct; break;
         }
         o[22 + 2 * e] = (double)(gx0 + ex);
         o[23 + 2 * e] = (double)(gy0 + ey);
     }
     __syncwarp();
+}
+
+// Serial part of the S shape group, one thread per ROI (the warp path would run
+// these sequential loops on single lanes, one divergent branch after another):
+// perimeter (the Moore walk of contour.cpp:70-144 replayed on K with Brent's
+// cycle detection: the first state of the cycle is where the reference's
+// first-repeated-state rule cuts it, steps summed in walk order), hull of the
+// column extremes (hull.cpp:17-55) with its lattice-point count and Feret
+// diameters, the +1/12 ellipse from sums in pixel order without FMA.
+__device__ __forceinline__ bool ks_at(const uint64_t* km, int h, int w, int x, int y) {
+    return x >= 0 && x < w && y >= 0 && y < h && ((km[y] >> x) & 1ull);
+}
+
+__global__ void __launch_bounds__(128) k_shape_serial(RoiList rl, Control* ctl, FeatCfg cfg,
+                                                      double* out) {
+    const uint32_t n0 = ctl->class_count[kClassS0], n1 = ctl->class_count[kClassS1];
+    const uint32_t nt = n0 + n1 + ctl->class_count[kClassS2];
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const uint32_t r = t < n0 ? rl.cls_list[kClassS0][t]
+                     : t < n0 + n1 ? rl.cls_list[kClassS1][t - n0] : rl.cls_list[kClassS2][t - n0 - n1];
+    const uint32_t hd = cfg.shape_hdr[r];
+    if (!(hd >> 16)) return;  // re-queued to the large-ROI kernel, which does its own
+    cfg.shape_hdr[r] = 0u;
+    const int h = (int)(hd & 0xffu), w = (int)((hd >> 8) & 0xffu);
+    const uint64_t* rows = cfg.shape_rows + (size_t)r * 128;
+    const uint64_t* km = rows + 64;
+    const double PI = 3.141592653589793, SQRT2 = 1.4142135623730951;
+    const long long gx0 = rl.gx[r], gy0 = rl.gy[r];
+    const unsigned long long n = rl.n[r];
+    const double dn = (double)n;
+    double* o = out + (size_t)r * cfg.ncols + cfg.col_shape;
+    // ---- ellipse sums (three independent sequential chains) and |K|
+    unsigned long long sx = 0, sy = 0;
+    uint32_t kc = 0;
+    for (int y = 0; y < h; ++y) {
+        const uint64_t m = rows[y];
+        const int c = __popcll(m);
+        sy += (unsigned long long)c * (unsigned long long)(gy0 + y);
+        uint64_t mm = m;
+        while (mm) {
+            sx += (unsigned long long)(gx0 + __ffsll((long long)mm) - 1);
+            mm &= mm - 1;
+        }
+        kc += __popcll(km[y]);
+    }
+    const double cx = (double)sx / dn, cy = (double)sy / dn;
+    double m20 = 0, m02 = 0, m11 = 0;
+    for (int y = 0; y < h; ++y) {
+        uint64_t m = rows[y];
+        const double dy = __dsub_rn((double)(gy0 + y), cy), dy2 = __dmul_rn(dy, dy);
+        while (m) {
+            const int x = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            const double dx = __dsub_rn((double)(gx0 + x), cx);
+            m20 = __dadd_rn(m20, __dmul_rn(dx, dx));
+            m02 = __dadd_rn(m02, dy2);
+            m11 = __dadd_rn(m11, __dmul_rn(dx, dy));
+        }
+    }
+    // ---- perimeter: Brent on the walk, then the cycle's steps in order
+    double per = 4.0;
+    if (n > 1 && kc > 1) {
+        int sy0 = 0;
+        while (!km[sy0]) ++sy0;
+        const int sx0 = __ffsll((long long)km[sy0]) - 1;
+        int tx = sx0, ty = sy0, tb = 0, hx = sx0, hy = sy0, hb = 0;
+        walk_step(km, h, w, hx, hy, hb);
+        uint32_t power = 1, lam = 1;
+        while (tx != hx || ty != hy || tb != hb) {
+            if (power == lam) {
+                tx = hx;
+                ty = hy;
+                tb = hb;
+                power *= 2;
+                lam = 0;
+            }
+            walk_step(km, h, w, hx, hy, hb);
+            ++lam;
+        }
+        tx = hx = sx0;
+        ty = hy = sy0;
+        tb = hb = 0;
+        for (uint32_t i = 0; i < lam; ++i) walk_step(km, h, w, hx, hy, hb);
+        while (tx != hx || ty != hy || tb != hb) {
+            walk_step(km, h, w, tx, ty, tb);
+            walk_step(km, h, w, hx, hy, hb);
+        }
+        per = 0;
+        for (uint32_t i = 0; i < lam; ++i) {
+            const int px = tx, py = ty;
+            walk_step(km, h, w, tx, ty, tb);
+            per = __dadd_rn(per, (abs(tx - px) + abs(ty - py) == 2) ? SQRT2 : 1.0);
+        }
+    }
+    // ---- hull of the column extremes: chain stack of packed (x | y << 8)
+    uint16_t hs[2 * 128 + 2];
+    uint8_t ctop[64], cbot[64];  // column extremes (255: empty column)
+    for (int x = 0; x < w; ++x) ctop[x] = cbot[x] = 255;
+    for (int y = 0; y < h; ++y) {
+        uint64_t m = rows[y];
+        while (m) {
+            const int x = __ffsll((long long)m) - 1;
+            m &= m - 1;
+            if (ctop[x] == 255) ctop[x] = (uint8_t)y;
+            cbot[x] = (uint8_t)y;
+        }
+    }
+    int k = 0, npt = 0, fx = -1, fy = 0, lx = 0, ly = 0;
+    auto col_ext = [&](int x, int& top, int& bot) {
+        top = ctop[x] == 255 ? -1 : ctop[x];
+        bot = cbot[x] == 255 ? -1 : cbot[x];
+    };
+    for (int x = 0; x < w; ++x) {
+        int tp, bt;
+        col_ext(x, tp, bt);
+        if (tp < 0) continue;
+        npt += tp == bt ? 1 : 2;
+        if (fx < 0) {
+            fx = x;
+            fy = tp;
+        }
+        lx = x;
+        ly = bt;
+    }
+    if (npt <= 2) {
+        for (int x = 0; x < w; ++x) {
+            int tp, bt;
+            col_ext(x, tp, bt);
+            if (tp < 0) continue;
+            hs[k++] = (uint16_t)(x | (tp << 8));
+            if (bt != tp) hs[k++] = (uint16_t)(x | (bt << 8));
+        }
+    } else {
+        int ax = 0, ay = 0, bx = 0, by = 0;  // hs[k-2], hs[k-1]
+        auto push = [&](int px, int py, int lo) {
+            while (k >= lo && (bx - ax) * (py - ay) - (by - ay) * (px - ax) <= 0) {
+                --k;
+                bx = ax;
+                by = ay;
+                if (k >= 2) {
+                    ax = hs[k - 2] & 0xff;
+                    ay = hs[k - 2] >> 8;
+                }
+            }
+            hs[k++] = (uint16_t)(px | (py << 8));
+            ax = bx;
+            ay = by;
+            bx = px;
+            by = py;
+        };
+        for (int x = 0; x < w; ++x) {
+            int tp, bt;
+            col_ext(x, tp, bt);
+            if (tp < 0) continue;
+            push(x, tp, 2);
+            if (bt != tp) push(x, bt, 2);
+        }
+        const int lower = k + 1;
+        bool skip_last = true;
+        for (int x = w - 1; x >= 0; --x) {
+            int tp, bt;
+            col_ext(x, tp, bt);
+            if (tp < 0) continue;
+            if (bt != tp) {
+                if (!skip_last) push(x, bt, lower);
+                skip_last = false;
+                push(x, tp, lower);
+            } else {
+                if (!skip_last) push(x, tp, lower);
+                skip_last = false;
+            }
+        }
+        k -= 1;
+        if (k < 3) {
+            hs[0] = (uint16_t)(fx | (fy << 8));
+            hs[1] = (uint16_t)(lx | (ly << 8));
+            k = 2;
+        }
+    }
+    const int nv = k;
+    // ---- convex area (lattice points inside or on the hull) and Feret diameters
+    unsigned long long carea = 0;
+    if (nv >= 3)
+        for (int y = 0; y < h; ++y) {
+            int xl = 0, xr = w - 1;
+            for (int i = 0; i < nv && xl <= xr; ++i) {
+                const int j = i + 1 < nv ? i + 1 : 0;
+                const int ax = hs[i] & 0xff, ay = hs[i] >> 8, bx = hs[j] & 0xff, by = hs[j] >> 8;
+                const int B = by - ay, A = (bx - ax) * (y - ay) + B * ax;  // A - B x >= 0
+                if (B > 0) xr = min(xr, (int)floor_div(A, B));
+                else if (B < 0) xl = max(xl, -(int)floor_div(A, -B));
+                else if (A < 0) xr = -1;
+            }
+            if (xr >= xl) carea += (unsigned long long)(xr - xl + 1);
+        }
+    double fmx = 0, fmn = 0;
+    if (nv >= 2) {  // max over vertex pairs of the exact squared distance, one sqrt
+        int d2 = 0;
+        for (int i = 0; i < nv; ++i)
+            for (int j = i + 1; j < nv; ++j) {
+                const int dx = (hs[i] & 0xff) - (hs[j] & 0xff), dy = (hs[i] >> 8) - (hs[j] >> 8);
+                d2 = max(d2, dx * dx + dy * dy);
+            }
+        fmx = sqrt((double)d2);
+        if (nv > 2) {
+            fmn = 1.79769313486231570815e308;
+            for (int i = 0; i < nv; ++i) {
+                const int j = i + 1 < nv ? i + 1 : 0;
+                const int ax = hs[i] & 0xff, ay = hs[i] >> 8;
+                const int ex = (hs[j] & 0xff) - ax, ey = (hs[j] >> 8) - ay;
+                int mc = 0;
+                for (int kk = 0; kk < nv; ++kk) {
+                    const int c = ex * ((hs[kk] >> 8) - ay) - ey * ((hs[kk] & 0xff) - ax);
+                    mc = max(mc, c < 0 ? -c : c);
+                }
+                fmn = fmin(fmn, (double)mc / hypot((double)ex, (double)ey));
+            }
+        }
+    }
+    // ---- columns (shape_feature_values order)
+    o[1] = per;
+    o[8] = n == 1 ? 1.0 : 4.0 * PI * dn / (per * per);
+    o[11] = (double)carea;
+    o[12] = carea ? dn / (double)carea : 0.0;
+    {
+        const double a = __dadd_rn(__ddiv_rn(m20, dn), 1.0 / 12.0);
+        const double c = __dadd_rn(__ddiv_rn(m02, dn), 1.0 / 12.0);
+        const double bb = __ddiv_rn(m11, dn);
+        const double amc = __dsub_rn(a, c);
+        const double disc = sqrt(__dadd_rn(__ddiv_rn(__dmul_rn(amc, amc), 4.0), __dmul_rn(bb, bb)));
+        const double hsum = __ddiv_rn(__dadd_rn(a, c), 2.0);
+        const double l1 = __dadd_rn(hsum, disc), l2 = __dsub_rn(hsum, disc);
+        const double maj = 4.0 * sqrt(fmax(0.0, l1)), mnr = 4.0 * sqrt(fmax(0.0, l2));
+        o[14] = maj;
+        o[15] = mnr;
+        o[16] = l1 > 0 ? sqrt(fmax(0.0, 1.0 - l2 / l1)) : 0.0;
+        o[17] = mnr > 0 ? maj / mnr : 0.0;
+        double th = 0.5 * atan2(2.0 * bb, amc);
+        if (th <= -PI / 2.0) th += PI;
+        o[18] = th;
+    }
+    o[20] = fmx;
+    o[21] = fmn;
 }
 
 // GLCM group for an S window with ng <= 64 (kGlHist): discretize (texture.cpp:45-53,
@@ -1509,16 +1594,17 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     }
 
     // ---------------------------------------------------------------- shape
+    PT(3);
     if (cfg.col_shape >= 0) {
         if (!have_k && !edge_ke(ks0, ks1, e_unused0, e_unused1)) return;
         uint64_t* km = (uint64_t*)(base + L.kmask);
         if ((int)lane < h) km[lane] = ks0;
         if ((int)lane + 32 < h) km[lane + 32] = ks1;
         __syncwarp();
-        shape_phase_s(rowmask, km, h, w, n, gx0, gy0, sLX, sLY, base + L.shp, orow + cfg.col_shape);
+        shape_phase_s(rowmask, km, h, w, n, gx0, gy0, sLX, sLY, J.row, cfg, orow + cfg.col_shape);
     }
     // ------------------------------------------------------------- moments
-    PT(3);
+    PT(6);
     if (cfg.col_mom >= 0) {
         const long long nn = (long long)n, W = (long long)sS;
         const long long axb = (2 * (long long)sLX + nn) / (2 * nn);
@@ -1782,6 +1868,11 @@ cudaError_t roi_s_setup(int* occ) {
     if (e == cudaSuccess) e = setup_one<kClassS2, kGlSort>(&occ[7]);
     if (e == cudaSuccess) e = setup_one<kClassS2, kGlHist>(&occ[8]);
     return e;
+}
+
+void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
+                         double* out) {
+    if (n_s > 0) k_shape_serial<<<(n_s + 127) / 128, 128, 0, s>>>(rl, ctl, cfg, out);
 }
 
 void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,

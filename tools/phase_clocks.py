@@ -29,8 +29,8 @@ elif which == "c4":
     for t in range(T):
         Lt, _ = fx.packed_blob_mask_grid(512, 1000, 100, t % 16)
         pairs.append((fx.uniform_u16(Lt.shape, t), Lt))
-    run = lambda: ctx.featurize_batch(pairs, ["intensity", "moments", "glcm"],
-                                      fx.resolve_profile("default"))
+    groups = os.environ.get("FX_GROUPS", "intensity,moments,glcm").split(",")
+    run = lambda: ctx.featurize_batch(pairs, groups, fx.resolve_profile("default"))
     nroi = sum(int(np.count_nonzero(np.bincount(p[1].ravel(), minlength=65536)[1:])) for p in pairs)
 if which == "c5":
     L, _ = fx.packed_blob_mask_grid(16384, 200000, 576, 1)
