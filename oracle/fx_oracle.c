@@ -773,6 +773,268 @@ static int glcm_group(const cloud_t* c, const fxo_params* prm, double* out) {
     return rc;
 }
 
+/* ------------------------------------------------- glrlm / glszm / ngtdm -- */
+
+static int d_level(const droi_t* r, int x, int y) { return r->grid[(size_t)y * r->w + x]; }
+
+/* (level, extent) entries -> sorted cells with counts (the reference's std::map
+ * iteration order), then the features of glrlm_features (texture.cpp:282-341) /
+ * glszm_features (:382-441), which share this form. */
+typedef struct {
+    int level, extent;
+} le_t;
+
+static int cmp_le(const void* a, const void* b) {
+    const le_t* p = a;
+    const le_t* q = b;
+    if (p->level != q->level) return p->level < q->level ? -1 : 1;
+    return (p->extent > q->extent) - (p->extent < q->extent);
+}
+
+static void grey_count_features(le_t* ent, size_t ne, int ng, uint64_t roi_pixels,
+                                double out[16]) {
+    memset(out, 0, 16 * sizeof(double));
+    if (ne == 0) return;
+    qsort(ent, ne, sizeof(le_t), cmp_le);
+    /* aggregate in place: cells (level, extent, count) */
+    size_t nc = 0;
+    uint64_t* cnt = malloc(ne * sizeof(uint64_t));
+    int max_ext = 0;
+    for (size_t i = 0; i < ne; ++i) {
+        if (nc && ent[nc - 1].level == ent[i].level && ent[nc - 1].extent == ent[i].extent) {
+            cnt[nc - 1] += 1;
+        } else {
+            ent[nc] = ent[i];
+            cnt[nc++] = 1;
+        }
+        if (ent[i].extent > max_ext) max_ext = ent[i].extent;
+    }
+    const double nr = (double)ne, np = (double)roi_pixels;
+    double sre = 0, lre = 0, lglre = 0, hglre = 0, srlgle = 0, srhgle = 0, lrlgle = 0, lrhgle = 0;
+    double re = 0, glv = 0, rv = 0, mu_g = 0, mu_l = 0;
+    double* per_level = calloc((size_t)ng, sizeof(double));
+    double* per_len = calloc((size_t)max_ext + 1, sizeof(double));
+    for (size_t i = 0; i < nc; ++i) {
+        const double r = (double)cnt[i], g = ent[i].level + 1, l = ent[i].extent;
+        sre += r / (l * l);
+        lre += r * l * l;
+        lglre += r / (g * g);
+        hglre += r * g * g;
+        srlgle += r / (g * g * l * l);
+        srhgle += r * g * g / (l * l);
+        lrlgle += r * l * l / (g * g);
+        lrhgle += r * g * g * l * l;
+        per_level[ent[i].level] += r;
+        per_len[ent[i].extent] += r;
+        const double p = r / nr;
+        re -= p * log2(p);
+        mu_g += p * g;
+        mu_l += p * l;
+    }
+    for (size_t i = 0; i < nc; ++i) {
+        const double p = (double)cnt[i] / nr;
+        glv += p * (ent[i].level + 1 - mu_g) * (ent[i].level + 1 - mu_g);
+        rv += p * (ent[i].extent - mu_l) * (ent[i].extent - mu_l);
+    }
+    double glnu = 0, rlnu = 0;
+    for (int lv = 0; lv < ng; ++lv)
+        if (per_level[lv] != 0) glnu += per_level[lv] * per_level[lv];
+    for (int e = 0; e <= max_ext; ++e)
+        if (per_len[e] != 0) rlnu += per_len[e] * per_len[e];
+    const double v[16] = {sre / nr, lre / nr, glnu / nr, glnu / (nr * nr), rlnu / nr,
+                          rlnu / (nr * nr), nr / np, glv, rv, re, lglre / nr, hglre / nr,
+                          srlgle / nr, srhgle / nr, lrlgle / nr, lrhgle / nr};
+    memcpy(out, v, sizeof v);
+    free(cnt);
+    free(per_level);
+    free(per_len);
+}
+
+/* glrlm (texture.cpp:242-280): runs of equal level along the scan direction;
+ * a run starts where the predecessor is outside or differs. */
+static int glrlm_angle(const droi_t* r, int angle, uint64_t roi_pixels, double out[16]) {
+    int dx = 0, dy = 0;
+    switch (angle) {
+        case 0: dx = 1; dy = 0; break;
+        case 45: dx = 1; dy = -1; break;
+        case 90: dx = 0; dy = 1; break;
+        case 135: dx = 1; dy = 1; break;
+        default: return fail(1, "unsupported angle");
+    }
+    le_t* ent = malloc(((size_t)r->w * r->h + 1) * sizeof(le_t));
+    if (!ent) return 8;
+    size_t ne = 0;
+    for (int y = 0; y < r->h; ++y)
+        for (int x = 0; x < r->w; ++x) {
+            if (!d_inside(r, x, y)) continue;
+            const int g = d_level(r, x, y);
+            if (d_inside(r, x - dx, y - dy) && d_level(r, x - dx, y - dy) == g) continue;
+            int len = 1, nx = x + dx, ny = y + dy;
+            while (d_inside(r, nx, ny) && d_level(r, nx, ny) == g) {
+                ++len;
+                nx += dx;
+                ny += dy;
+            }
+            ent[ne++] = (le_t){g, len};
+        }
+    grey_count_features(ent, ne, r->ng, roi_pixels, out);
+    free(ent);
+    return 0;
+}
+
+/* glszm (texture.cpp:343-380): 8-connected zones of equal level, row-major scan */
+static int glszm_all(const droi_t* r, uint64_t roi_pixels, double out[16]) {
+    const size_t cells = (size_t)r->w * r->h;
+    uint8_t* seen = calloc(cells, 1);
+    int* st = malloc(cells * 2 * sizeof(int) + 16);
+    le_t* ent = malloc((cells + 1) * sizeof(le_t));
+    if (!seen || !st || !ent) {
+        free(seen);
+        free(st);
+        free(ent);
+        return 8;
+    }
+    static const int k8[8][2] = {{1, 0}, {-1, 0}, {0, 1}, {0, -1}, {1, 1}, {1, -1}, {-1, 1}, {-1, -1}};
+    size_t ne = 0;
+    for (int y = 0; y < r->h; ++y)
+        for (int x = 0; x < r->w; ++x) {
+            if (!d_inside(r, x, y) || seen[(size_t)y * r->w + x]) continue;
+            const int g = d_level(r, x, y);
+            size_t size = 0, sp = 0;
+            st[sp++] = x;
+            st[sp++] = y;
+            seen[(size_t)y * r->w + x] = 1;
+            while (sp) {
+                const int cy = st[--sp], cx = st[--sp];
+                ++size;
+                for (int k = 0; k < 8; ++k) {
+                    const int nx = cx + k8[k][0], ny = cy + k8[k][1];
+                    if (!d_inside(r, nx, ny) || d_level(r, nx, ny) != g) continue;
+                    uint8_t* sn = &seen[(size_t)ny * r->w + nx];
+                    if (!*sn) {
+                        *sn = 1;
+                        st[sp++] = nx;
+                        st[sp++] = ny;
+                    }
+                }
+            }
+            ent[ne++] = (le_t){g, (int)size};
+        }
+    grey_count_features(ent, ne, r->ng, roi_pixels, out);
+    free(seen);
+    free(st);
+    free(ent);
+    return 0;
+}
+
+/* ngtdm + ngtdm_features (texture.cpp:443-528) */
+static int ngtdm_all(const droi_t* r, double out[5]) {
+    const int ng = r->ng;
+    uint64_t* n = calloc((size_t)ng, sizeof(uint64_t));
+    double* sv = calloc((size_t)ng, sizeof(double));
+    double* p = calloc((size_t)ng, sizeof(double));
+    uint64_t valid = 0;
+    for (int y = 0; y < r->h; ++y)
+        for (int x = 0; x < r->w; ++x) {
+            if (!d_inside(r, x, y)) continue;
+            double sum = 0;
+            int count = 0;
+            for (int dy = -1; dy <= 1; ++dy)
+                for (int dx = -1; dx <= 1; ++dx) {
+                    if (dx == 0 && dy == 0) continue;
+                    if (d_inside(r, x + dx, y + dy)) {
+                        sum += d_level(r, x + dx, y + dy) + 1;
+                        ++count;
+                    }
+                }
+            if (count == 0) continue;
+            const int g = d_level(r, x, y);
+            n[g] += 1;
+            sv[g] += fabs((g + 1) - sum / count);
+            ++valid;
+        }
+    memset(out, 0, 5 * sizeof(double));
+    if (valid) {
+        const double nv = (double)valid;
+        int present = 0;
+        double s_total = 0, ps_total = 0;
+        for (int i = 0; i < ng; ++i) {
+            p[i] = (double)n[i] / nv;
+            if (p[i] > 0) ++present;
+            s_total += sv[i];
+            ps_total += p[i] * sv[i];
+        }
+        const double coarseness = ps_total > 0 ? 1.0 / ps_total : 1e6;
+        double contrast = 0;
+        if (present > 1) {
+            double acc = 0;
+            for (int i = 0; i < ng; ++i) {
+                if (p[i] == 0) continue;
+                for (int j = 0; j < ng; ++j) {
+                    if (p[j] == 0) continue;
+                    acc += p[i] * p[j] * (i - j) * (i - j);
+                }
+            }
+            contrast = acc / ((double)present * (present - 1)) * (s_total / nv);
+        }
+        double busy = 0, cplx = 0, strn = 0;
+        for (int i = 0; i < ng; ++i) {
+            if (p[i] == 0) continue;
+            const double gi = i + 1;
+            for (int j = 0; j < ng; ++j) {
+                if (p[j] == 0) continue;
+                const double gj = j + 1;
+                busy += fabs(gi * p[i] - gj * p[j]);
+                cplx += fabs(gi - gj) * (p[i] * sv[i] + p[j] * sv[j]) / (p[i] + p[j]);
+                strn += (p[i] + p[j]) * (gi - gj) * (gi - gj);
+            }
+        }
+        out[0] = busy > 0 ? ps_total / busy : 0.0;
+        out[1] = coarseness;
+        out[2] = cplx / nv;
+        out[3] = contrast;
+        out[4] = s_total > 0 ? strn / s_total : 0.0;
+    }
+    free(n);
+    free(sv);
+    free(p);
+    return 0;
+}
+
+static int rlzn_groups(const cloud_t* c, unsigned groups, const fxo_params* prm, double** o) {
+    droi_t r;
+    memset(&r, 0, sizeof r);
+    int rc = discretize(c, prm->ng, &r);
+    if (rc) return rc;
+    if (groups & FXO_GLRLM) {
+        const int A = prm->n_angles;
+        int angles[8];
+        memcpy(angles, prm->angles, (size_t)A * sizeof(int));
+        qsort(angles, (size_t)A, sizeof(int), cmp_int);
+        double f[8][16];
+        for (int a = 0; a < A && !rc; ++a) rc = glrlm_angle(&r, angles[a], c->n, f[a]);
+        if (!rc)
+            for (int s2 = 0; s2 < 16; ++s2) {
+                double acc = 0;
+                for (int a = 0; a < A; ++a) {
+                    *(*o)++ = f[a][s2];
+                    acc += f[a][s2];
+                }
+                *(*o)++ = acc / (double)A;
+            }
+    }
+    if (!rc && (groups & FXO_GLSZM)) {
+        rc = glszm_all(&r, c->n, *o);
+        *o += 16;
+    }
+    if (!rc && (groups & FXO_NGTDM)) {
+        rc = ngtdm_all(&r, *o);
+        *o += 5;
+    }
+    free(r.grid);
+    return rc;
+}
+
 /* ----------------------------------------------------------------- shape -- */
 
 typedef struct {
@@ -1044,12 +1306,10 @@ static int shape_group(const cloud_t* c, double* o) {
 
 static int check_groups(unsigned groups) {
     if (groups == 0) return fail(1, "feature list is empty");
-    if (groups & (FXO_GLRLM | FXO_GLSZM | FXO_NGTDM))
-        return fail(1, "group outside the restated hot path");
     return 0;
 }
 
-/* compute_roi_features (engine.cpp:138-209) for intensity/shape/moments/glcm. */
+/* compute_roi_features (engine.cpp:138-209), all seven groups. */
 static int roi_features(const cloud_t* c, unsigned groups, const fxo_params* prm, double* out) {
     double* o = out;
     int rc;
@@ -1070,6 +1330,10 @@ static int roi_features(const cloud_t* c, unsigned groups, const fxo_params* prm
     }
     if (groups & FXO_GLCM) {
         if ((rc = glcm_group(c, prm, o))) return rc;
+        o += 29 * (prm->n_angles + 1);
+    }
+    if (groups & (FXO_GLRLM | FXO_GLSZM | FXO_NGTDM)) {
+        if ((rc = rlzn_groups(c, groups, prm, &o))) return rc;
     }
     return 0;
 }

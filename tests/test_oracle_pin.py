@@ -11,7 +11,7 @@ import pytest
 import inputs
 from oracle import make_params
 
-GROUPS = ["intensity", "shape", "moments", "glcm"]
+GROUPS = ["intensity", "shape", "moments", "glcm", "glrlm", "glszm", "ngtdm"]
 
 
 def _blob(reference, size, roi_size, count, seed):
