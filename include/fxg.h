@@ -57,8 +57,8 @@ typedef enum fx_mem_kind { FX_MEM_HOST = 0, FX_MEM_DEVICE = 1 } fx_mem_kind;
 #define FX_GROUP_GLSZM 0x20u
 #define FX_GROUP_NGTDM 0x40u
 #define FX_GROUP_ALL 0x7Fu
-/* Groups with device kernels in this build (others return FX_E_CONFIG). */
-#define FX_GROUP_DEVICE (FX_GROUP_INTENSITY | FX_GROUP_SHAPE | FX_GROUP_MOMENTS | FX_GROUP_GLCM)
+/* Groups with device kernels in this build (all seven). */
+#define FX_GROUP_DEVICE FX_GROUP_ALL
 
 /* TextureParams (engine.hpp:14-17) + GlcmParams (texture.hpp:30-35). */
 typedef struct fx_texture_params {

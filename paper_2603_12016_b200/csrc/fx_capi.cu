@@ -35,6 +35,10 @@ void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
 cudaError_t roi_b_setup();
 void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
                          double* out);
+cudaError_t roi_t_setup();
+TLayout make_tlayout(unsigned long long CELLS, uint32_t NMAX);
+void launch_roi_t(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
+                  double* out, uint8_t* scratch, const TLayout& T, int which, bool init);
 BLayout make_blayout(uint32_t H, uint32_t WPR, uint32_t NMAX, uint32_t RUNMAX, uint32_t NB,
                      unsigned long long CELLS);
 void launch_roi_b(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
@@ -88,6 +92,11 @@ struct fx_ctx {
     size_t stage_elems = 0;  // per raster
     uint32_t* d_blab = nullptr;  // batch output labels (host outputs)
     size_t blab_cap = 0;
+    // GLRLM/GLSZM/NGTDM slabs: [0] S-class windows, [1] large windows
+    uint8_t* d_tscratch[2] = {nullptr, nullptr};
+    size_t tscratch_bytes[2] = {0, 0};
+    TLayout tlay_prev[2] = {};
+    int tlay_grid[2] = {0, 0};
     // shape group: per-ROI staged row masks (S ROIs) for k_shape_serial
     uint64_t* d_shape_rows = nullptr;
     uint32_t* d_shape_hdr = nullptr;
@@ -259,10 +268,11 @@ void collect_times(fx_ctx* c) {
 }
 
 int validate_texture(unsigned groups, const fx_texture_params& p) {
-    if (!(groups & FX_GROUP_GLCM)) return FX_OK;
+    if (!(groups & (FX_GROUP_GLCM | FX_GROUP_GLRLM | FX_GROUP_GLSZM | FX_GROUP_NGTDM)))
+        return FX_OK;
     if (p.ng < 2) return set_error(FX_E_CONFIG, "grey level count must be >= 2");
     if (p.ng > 256)
-        return set_error(FX_E_CONFIG, "device GLCM supports ng <= 256 in this build");
+        return set_error(FX_E_CONFIG, "device texture groups support ng <= 256 in this build");
     if (p.n_angles < 1 || p.n_angles > 8) return set_error(FX_E_CONFIG, "1..8 angles supported");
     for (int i = 0; i < p.n_angles; ++i) {
         const int a = p.angles[i];
@@ -292,6 +302,19 @@ FeatCfg make_cfg(unsigned groups, const fx_texture_params& p) {
     if (groups & FX_GROUP_GLCM) {
         f.col_glcm = col;
         col += 29 * (p.n_angles + 1);
+    }
+    f.col_glrlm = f.col_glszm = f.col_ngtdm = -1;
+    if (groups & FX_GROUP_GLRLM) {
+        f.col_glrlm = col;
+        col += 16 * (p.n_angles + 1);
+    }
+    if (groups & FX_GROUP_GLSZM) {
+        f.col_glszm = col;
+        col += 16;
+    }
+    if (groups & FX_GROUP_NGTDM) {
+        f.col_ngtdm = col;
+        col += 5;
     }
     f.ncols = col;
     f.bins = std::max(2, p.histogram_bins);
@@ -502,6 +525,40 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         return set_error(FX_E_CAPACITY, "output capacity " + std::to_string(cap_rois) +
                                             " < " + std::to_string(hc.n_rois) + " ROIs");
     }
+    if (cfg.col_glrlm >= 0 || cfg.col_glszm >= 0 || cfg.col_ngtdm >= 0) {
+        // GLRLM/GLSZM/NGTDM: S-class windows, then large windows (own slabs)
+        const uint64_t n_s = (uint64_t)hc.class_count[kClassS0] + hc.class_count[kClassS1] +
+                             hc.class_count[kClassS2];
+        const uint64_t n_l = hc.class_count[kClassL];
+        for (int which = 0; which < 2; ++which) {
+            const uint64_t nw = which ? n_l : n_s;
+            if (!nw) continue;
+            const TLayout T = which ? make_tlayout(std::max<unsigned long long>(hc.l_max_cells, 4096ull),
+                                                   (uint32_t)std::max<unsigned long long>(hc.l_max_n, 4096ull))
+                                    : make_tlayout(4096ull, 4096u);
+            uint64_t grid = std::min<uint64_t>((uint64_t)c->sm_count * 4, nw);
+            grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, (4ull << 30) / std::max<size_t>(T.bytes, 1)));
+            const size_t need = (size_t)T.bytes * grid;
+            if (need > c->tscratch_bytes[which]) {
+                cudaStreamSynchronize(s);
+                cudaFree(c->d_tscratch[which]);
+                c->d_tscratch[which] = nullptr;
+                c->tscratch_bytes[which] = 0;
+                c->tlay_grid[which] = 0;
+                CK(cudaMalloc(&c->d_tscratch[which], need));
+                c->tscratch_bytes[which] = need;
+            }
+            const bool same = c->tlay_grid[which] >= (int)grid && T.bytes == c->tlay_prev[which].bytes &&
+                              T.HC == c->tlay_prev[which].HC && T.hjk == c->tlay_prev[which].hjk;
+            Launch l(c, which ? "k_roi_t_large" : "k_roi_t");
+            launch_roi_t((int)grid, s, img, rl, c->d_ctl, cfg, out_dev, c->d_tscratch[which], T,
+                         which, !same);
+            if (!same) {
+                c->tlay_prev[which] = T;
+                c->tlay_grid[which] = (int)grid;
+            }
+        }
+    }
     if (cfg.col_shape >= 0) {  // serial shape columns of the S ROIs, before k_roi_b
         const int n_s = (int)(hc.class_count[kClassS0] + hc.class_count[kClassS1] +
                               hc.class_count[kClassS2]);
@@ -711,6 +768,7 @@ int fx_ctx_create(int device, fx_ctx** out) {
     }
     CKC(roi_s_setup(&c->occ_s[0][0]));
     CKC(roi_b_setup());
+    CKC(roi_t_setup());
     for (auto& row : c->occ_s)
         for (int& o : row) o = std::max(1, o);
     void* fn = nullptr;
@@ -750,6 +808,8 @@ int fx_ctx_destroy(fx_ctx* c) {
     cudaFree(c->d_blab);
     cudaFree(c->d_shape_rows);
     cudaFree(c->d_shape_hdr);
+    cudaFree(c->d_tscratch[0]);
+    cudaFree(c->d_tscratch[1]);
     cudaFree(c->d_img);
     cudaFree(c->d_out);
     cudaFree(c->d_lscratch);

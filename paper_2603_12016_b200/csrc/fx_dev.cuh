@@ -84,6 +84,7 @@ struct Control {
     uint32_t l_max_wpr;       // max 64-bit words per row among L ROIs
     unsigned long long l_max_n;      // max pixel count among L ROIs
     unsigned long long l_max_cells;  // max window cells among L ROIs
+    uint32_t t_next[2];              // GLRLM/GLSZM/NGTDM work counters (S lists, L list)
 };
 
 // compaction scratch: per (slot, 1024-label block) counts and exclusive bases
@@ -132,6 +133,7 @@ struct FeatCfg {
     uint32_t groups;
     int ncols;
     int col_int, col_shape, col_mom, col_glcm;  // column offsets, -1 if absent
+    int col_glrlm, col_glszm, col_ngtdm;
     int bins;                        // max(2, histogram_bins)
     int ng, symmetric, n_angles;
     int angle[8];                    // sorted (engine.cpp:36-40)

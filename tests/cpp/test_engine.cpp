@@ -133,19 +133,24 @@ static void device_cases() {
         const RunSummary s = run(c);
         CHECK(s.images == 1 && s.rows == 2 && s.completed_with_errors() && s.failed_pairs == 2);
     }
-    {  // groups without a device kernel fail loudly per pair (no CPU fallback)
-        const auto d = fresh_dir("fxg_engine_glrlm");
+    {  // texture limits of the device path fail loudly per pair (no CPU fallback)
+        const auto d = fresh_dir("fxg_engine_ng");
         write_simple_pair(d);
         ExtractionConfig c;
         c.intensity_dir = d / "int";
         c.mask_dir = d / "seg";
         c.output_path = d / "f.csv";
         c.features = {"glrlm"};
+        GlcmParams gp = resolve_profile("default").glcm;
+        gp.ng = 300;
+        c.glcm_override = gp;
         const RunSummary s = run(c);
         CHECK(s.images == 0 && s.failed_pairs == 1);
         PixelCloud pc;
-        pc.pixels = {{1, 1, 5}};
-        CHECK_THROWS_AS(compute_roi_features(pc, {"glszm"}, resolve_profile("default")), ConfigError);
+        pc.pixels = {{1, 1, 5}, {2, 1, 6}};
+        TextureParams tp = resolve_profile("default");
+        tp.glcm.ng = 300;
+        CHECK_THROWS_AS(compute_roi_features(pc, {"glszm"}, tp), ConfigError);
     }
     {  // the shape group runs on the device: a 1-pixel cloud reports the conventions
         PixelCloud pc;

@@ -79,6 +79,27 @@ def floors(columns, ref_table, intensity=None, labels=None, roi_labels=None):
             s[:, i] = 1.0
         if c.startswith("glcm_") and any(c.startswith("glcm_" + h + "_") for h in HARALICK_UNIT):
             s[:, i] = 1.0
+    # GLRLM/GLSZM variances sum p (x - mu)^2: the reference's rounding noise scales
+    # with E[x^2] (its own lre / hglre / lae / hglze columns), not with the variance.
+    # Scale columns are found by position (feature-major blocks, names may repeat
+    # when an angle is listed twice).
+    feats = ["sre", "lre", "glnu", "glnun", "rlnu", "rlnun", "rp", "glv", "rv", "re", "lglre",
+             "hglre", "srlgle", "srhgle", "lrlgle", "lrhgle"]
+    for pre, pairs in (("glrlm_", (("glv", "hglre"), ("rv", "lre"))),
+                       ("glszm_", (("glv", "hglze"), ("zv", "lae")))):
+        idx = [i for i, c in enumerate(columns) if c.startswith(pre)]
+        if not idx:
+            continue
+        per = len(idx) // 16  # angles + 1 (glrlm), 1 (glszm)
+        names = feats
+        if pre == "glszm_":
+            names = ["sae", "lae", "glnu", "glnun", "sznu", "sznun", "zp", "glv", "zv", "ze",
+                     "lglze", "hglze", "salgle", "sahgle", "lalgle", "lahgle"]
+        for var, scale in pairs:
+            dv, ds = names.index(var), names.index(scale)
+            for k in range(per):
+                i, j = idx[dv * per + k], idx[ds * per + k]
+                s[:, i] = np.maximum(s[:, i], np.abs(ref_table[:, j]))
     if "moments_mu00" in col and intensity is not None:
         ms = _moment_scales(intensity, labels, roi_labels)
         for g, pre in enumerate(("", "w")):

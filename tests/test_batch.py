@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 import inputs  # noqa: E402
 from parity import assert_parity  # noqa: E402
 
-GROUPS = ["intensity", "shape", "moments", "glcm"]
+GROUPS = ["intensity", "shape", "moments", "glcm", "glrlm", "glszm", "ngtdm"]
 
 
 def _pairs(specs, seed=0):

@@ -15,7 +15,7 @@ from oracle import make_params as oparams
 
 pytestmark = pytest.mark.gpu
 
-GROUPS = ["intensity", "shape", "moments", "glcm"]
+GROUPS = ["intensity", "shape", "moments", "glcm", "glrlm", "glszm", "ngtdm"]
 
 
 def both_params(profile="default", **over):
