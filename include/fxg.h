@@ -201,6 +201,9 @@ int fx_debug_roi(fx_ctx* ctx, const fx_image* image, uint32_t label,
  * sort, 7 GLCM run-length counts, 8 Haralick.  Only in builds with
  * -DFXG_PHASE_TIMING (tools/); others return FX_E_CONFIG. */
 int fx_debug_phase_clocks(unsigned long long* out, int n, int reset);
+/* Same for the GLRLM/GLSZM/NGTDM kernel (thread 0 per ROI): 0 discretize,
+ * 1 GLRLM (other), 2 GLSZM, 3 NGTDM, 4 GLRLM run counting, 5 GLRLM features. */
+int fx_debug_texture_clocks(unsigned long long* out, int n, int reset);
 
 /* ---- synthetic inputs (the reference's synth.hpp generators) --------------- */
 

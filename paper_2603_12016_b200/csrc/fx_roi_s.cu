@@ -413,10 +413,6 @@ __constant__ int8_t c_ring[8][2] = {{-1, 0}, {-1, -1}, {0, -1}, {1, -1},
 // ring index of a unit offset (dx, dy) in [-1, 1]^2: (dx + 1) * 3 + (dy + 1)
 __constant__ int8_t c_ring_of[9] = {1, 0, 7, 2, -1, 6, 3, 4, 5};
 
-__device__ __forceinline__ bool k_at(const uint64_t* km, int h, int w, int x, int y) {
-    return x >= 0 && x < w && y >= 0 && y < h && ((km[y] >> x) & 1ull);
-}
-
 // one step of the Moore walk: position (x, y), backtrack ring index b.  The 8
 // neighbours come from three K rows as one byte in ring order; the next
 // direction is the first set bit after b (rotate + ffs).
@@ -544,10 +540,6 @@ __device__ __noinline__ void shape_phase_s(const uint64_t* rowmask, const uint64
 // first-repeated-state rule cuts it, steps summed in walk order), hull of the
 // column extremes (hull.cpp:17-55) with its lattice-point count and Feret
 // diameters, the +1/12 ellipse from sums in pixel order without FMA.
-__device__ __forceinline__ bool ks_at(const uint64_t* km, int h, int w, int x, int y) {
-    return x >= 0 && x < w && y >= 0 && y < h && ((km[y] >> x) & 1ull);
-}
-
 __global__ void __launch_bounds__(128) k_shape_serial(RoiList rl, Control* ctl, FeatCfg cfg,
                                                       double* out) {
     const uint32_t n0 = ctl->class_count[kClassS0], n1 = ctl->class_count[kClassS1];

@@ -20,6 +20,20 @@
 #include "fx_glcm.cuh"
 #include "fx_roi.cuh"
 
+#ifdef FXG_PHASE_TIMING
+__device__ unsigned long long g_phase_clk_t[8];
+#define TT_DECL long long tt_t_ = clock64();
+#define TT(k)                                                                  \
+    do {                                                                       \
+        const long long t_ = clock64();                                        \
+        if (threadIdx.x == 0) atomicAdd(&g_phase_clk_t[k], (unsigned long long)(t_ - tt_t_)); \
+        tt_t_ = t_;                                                            \
+    } while (0)
+#else
+#define TT_DECL
+#define TT(k)
+#endif
+
 namespace fxg {
 
 namespace {
@@ -49,6 +63,31 @@ __device__ __forceinline__ T tblock_all(T v, T* sh, Op op) {
     __syncthreads();
     return r;
 }
+// block sums of K <= 8 doubles in one pass (fixed order: lanes, then warps)
+template <int K>
+__device__ __forceinline__ void tblock_sum(double (&v)[K], double (*sh)[8]) {
+    const unsigned lane = lane_id(), w = twarp();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double x = v[k];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+        v[k] = x;
+    }
+    if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < K; ++k) sh[w][k] = v[k];
+    __syncthreads();
+    if (threadIdx.x < K) {
+        double t = 0;
+        for (int i = 0; i < kTW; ++i) t += sh[i][threadIdx.x];
+        sh[kTW][threadIdx.x] = t;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = sh[kTW][k];
+    __syncthreads();
+}
 struct TAdd {
     template <typename T>
     __device__ T operator()(T a, T b) const { return a + b; }
@@ -68,6 +107,7 @@ struct TSlab {
     uint32_t* zsz;   // [cells] flatten scratch, then zone sizes
     uint32_t* hjk;   // [HC] (level, extent) keys  } open addressing, kept empty
     uint32_t* hjc;   // [HC] counts                 }
+    uint32_t* hjl;   // [HC] slots filled since the last reset (in any order)
     uint32_t* ext;   // [NMAX+1] units per extent (dense: fixed summation order)
     uint32_t* ccnt;  // [NMAX+1] joint cells per cell count (entropy by count value)
 };
@@ -76,10 +116,20 @@ struct TShared {
     uint32_t plev[256];            // runs / zones per level; NGTDM pixels per level
     unsigned long long sng[256];   // NGTDM 840 * sum |(g+1) - mean| per level
     double red[kTW + 1];
+    double red8[kTW + 1][8];
     unsigned long long u64[kTW + 1];
     uint32_t u32[kTW + 1];
     uint32_t job;
+    uint32_t nfill;                // slots listed in hjl
+    // dynamic shared memory (kDynBytes), S-class windows:
+    uint16_t* slev;                // [4096] level raster
+    uint32_t* skey;                // [4096] (level, extent) keys   } distinct keys <=
+    uint32_t* scnt;                // [4096] counts                 } units <= pixels
+    uint32_t* slst;                // [4096] filled slots           } <= 4096
+    uint16_t* spar;                // [4096] GLSZM union-find parents (cell index)
+    uint16_t* szsz;                // [4096] flatten scratch, then zone sizes
 };
+constexpr size_t kDynBytes = 4096 * 2 + 3 * 4096 * 4 + 2 * 4096 * 2;
 
 __device__ __forceinline__ uint32_t thash(uint32_t k) {
     k ^= k >> 16;
@@ -90,12 +140,14 @@ __device__ __forceinline__ uint32_t thash(uint32_t k) {
     return k;
 }
 
-__device__ __forceinline__ void table_add(uint32_t* keys, uint32_t* cnts, uint32_t mask, uint32_t key) {
+__device__ __forceinline__ void table_add(uint32_t* keys, uint32_t* cnts, uint32_t* list,
+                                          uint32_t* nfill, uint32_t mask, uint32_t key) {
     uint32_t h = thash(key) & mask;
     for (;;) {
         const uint32_t old = atomicCAS(&keys[h], kEmpty, key);
         if (old == kEmpty || old == key) {
             atomicAdd(&cnts[h], 1u);
+            if (old == kEmpty) list[atomicAdd(nfill, 1u)] = h;
             return;
         }
         h = (h + 1) & mask;
@@ -107,69 +159,69 @@ __device__ __forceinline__ void table_add(uint32_t* keys, uint32_t* cnts, uint32
 // lglre, hglre, srlgle, srhgle, lrlgle, lrhgle numerators); nr units, np pixels.
 // Empties the count tables and the per-level counts.
 __device__ void extent_features(const double* t8, unsigned long long nr_u, unsigned long long np_u,
-                                int ng, const TSlab& S, uint32_t HC, uint32_t NMAX, TShared& sm,
-                                double* out16) {
+                                int ng, const TSlab& S, uint32_t* hk, uint32_t* hc, uint32_t* hl,
+                                uint32_t emax, TShared& sm, double* out16) {
     const unsigned tid = threadIdx.x;
     if (nr_u == 0) {
         for (int k = tid; k < 16; k += kTT) out16[k] = 0.0;
         for (int g = tid; g < ng; g += kTT) sm.plev[g] = 0u;
+        if (tid == 0) sm.nfill = 0u;
         __syncthreads();
         return;
     }
     const double nr = (double)nr_u, np = (double)np_u, logn = nlog2(nr);
-    // per-level: glnu, mean level
-    double a_glnu = 0, a_mug = 0;
+    // pass A: per-level (glnu, mean level), per-extent (rlnu, mean extent), joint
+    // cells -> histogram of their counts (the table's slot layout depends on the
+    // insertion order, the counts do not), emptying the table
+    double a[4] = {0, 0, 0, 0};
     for (int g = tid; g < ng; g += kTT) {
         const double c = (double)sm.plev[g];
-        a_glnu += c * c;
-        a_mug += c * (g + 1);
+        a[0] += c * c;
+        a[1] += c * (g + 1);
     }
-    const double glnu = tblock_all(a_glnu, sm.red, TAdd());
-    const double mu_g = tblock_all(a_mug, sm.red, TAdd()) / nr;
-    // per-extent counts (dense, ascending extent): rlnu, mean extent
-    double a_rlnu = 0, a_mul = 0;
-    for (uint32_t e = tid; e <= NMAX; e += kTT) {
+    for (uint32_t e = tid; e <= emax; e += kTT) {
         const uint32_t c = S.ext[e];
         if (c) {
-            a_rlnu += (double)c * (double)c;
-            a_mul += (double)c * (double)e;
+            a[2] += (double)c * (double)c;
+            a[3] += (double)c * (double)e;
         }
     }
-    const double rlnu = tblock_all(a_rlnu, sm.red, TAdd());
-    const double mu_l = tblock_all(a_mul, sm.red, TAdd()) / nr;
-    // joint cells -> histogram of their counts (the slot layout of the table depends
-    // on insertion order; the counts do not), emptying the table
-    for (uint32_t i = tid; i < HC; i += kTT) {
-        if (S.hjk[i] != kEmpty) {
-            atomicAdd(&S.ccnt[S.hjc[i]], 1u);
-            S.hjk[i] = kEmpty;
-            S.hjc[i] = 0u;
-        }
+    const uint32_t nfill = sm.nfill;
+    uint32_t cmax = 0;
+    for (uint32_t i = tid; i < nfill; i += kTT) {
+        const uint32_t slot = hl[i];
+        const uint32_t c = hc[slot];
+        atomicAdd(&S.ccnt[c], 1u);
+        cmax = max(cmax, c);
+        hk[slot] = kEmpty;
+        hc[slot] = 0u;
     }
-    __syncthreads();
-    double a_re = 0;  // entropy = sum over cells c (log2 nr - log2 c) / nr
-    for (uint32_t c = tid; c <= NMAX; c += kTT) {
+    cmax = tblock_all(cmax, sm.u32, TMax());
+    tblock_sum<4>(a, sm.red8);
+    if (tid == 0) sm.nfill = 0u;
+    const double glnu = a[0], mu_g = a[1] / nr, rlnu = a[2], mu_l = a[3] / nr;
+    // pass B: entropy = sum over cells c (log2 nr - log2 c) / nr, variances
+    double b[3] = {0, 0, 0};
+    for (uint32_t c = tid; c <= cmax; c += kTT) {
         const uint32_t k = S.ccnt[c];
         if (k) {
-            a_re += (double)k * (double)c * (logn - log2_int(c));
+            b[0] += (double)k * (double)c * (logn - log2_int(c));
             S.ccnt[c] = 0u;
         }
     }
-    const double re = tblock_all(a_re, sm.red, TAdd()) / nr;
-    double a_glv = 0, a_rv = 0;
     for (int g = tid; g < ng; g += kTT) {
         const double c = (double)sm.plev[g];
-        a_glv += c / nr * (g + 1 - mu_g) * (g + 1 - mu_g);
+        b[1] += c / nr * (g + 1 - mu_g) * (g + 1 - mu_g);
     }
-    for (uint32_t e = tid; e <= NMAX; e += kTT) {
+    for (uint32_t e = tid; e <= emax; e += kTT) {
         const uint32_t c = S.ext[e];
         if (c) {
-            a_rv += (double)c / nr * ((double)e - mu_l) * ((double)e - mu_l);
+            b[2] += (double)c / nr * ((double)e - mu_l) * ((double)e - mu_l);
             S.ext[e] = 0u;
         }
     }
-    const double glv = tblock_all(a_glv, sm.red, TAdd());
-    const double rv = tblock_all(a_rv, sm.red, TAdd());
+    tblock_sum<3>(b, sm.red8);
+    const double re = b[0] / nr, glv = b[1], rv = b[2];
     if (tid == 0) {
         const double v[16] = {t8[0] / nr, t8[1] / nr, glnu / nr, glnu / (nr * nr), rlnu / nr,
                               rlnu / (nr * nr), nr / np, glv, rv, re, t8[2] / nr, t8[3] / nr,
@@ -177,6 +229,83 @@ __device__ void extent_features(const double* t8, unsigned long long nr_u, unsig
         for (int k = 0; k < 16; ++k) out16[k] = v[k];
     }
     for (int g = tid; g < ng; g += kTT) sm.plev[g] = 0u;
+    __syncthreads();
+}
+
+// union-find with T-bit cell indices (u16 in shared memory for S windows)
+template <typename T>
+__device__ __forceinline__ uint32_t t_root(const volatile T* par, uint32_t x) {
+    uint32_t p = par[x];
+    while (p != x) {
+        x = p;
+        p = par[x];
+    }
+    return x;
+}
+__device__ __forceinline__ uint32_t t_cas(uint16_t* a, uint32_t cmp, uint32_t val) {
+    return atomicCAS(reinterpret_cast<unsigned short*>(a), (unsigned short)cmp, (unsigned short)val);
+}
+__device__ __forceinline__ uint32_t t_cas(uint32_t* a, uint32_t cmp, uint32_t val) {
+    return atomicCAS(a, cmp, val);
+}
+template <typename T>
+__device__ __forceinline__ void t_union(T* par, uint32_t a, uint32_t b) {
+    for (;;) {
+        a = t_root(par, a);
+        b = t_root(par, b);
+        if (a == b) return;
+        if (a > b) {
+            const uint32_t t = a;
+            a = b;
+            b = t;
+        }
+        const uint32_t old = t_cas(&par[b], b, a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
+// 8-connected zones of equal level: par[c] = root (smallest cell index of the
+// zone), zsz[root] = zone size (reads of par use volatile-free loads after
+// barriers; concurrent links only ever move a root under a smaller index)
+template <typename T>
+__device__ void glszm_zones(T* par, T* zsz, const uint16_t* lv, int w, int h, uint32_t cells) {
+    const unsigned tid = threadIdx.x;
+    for (uint32_t c = tid; c < cells; c += kTT) {
+        par[c] = (T)c;
+        zsz[c] = 0;
+    }
+    __syncthreads();
+    for (uint32_t c = tid; c < cells; c += kTT) {  // forward neighbours E, SW, S, SE
+        const uint32_t g = lv[c];
+        if (g == kNoLevel) continue;
+        const int y = (int)(c / (uint32_t)w), x = (int)(c - (uint32_t)y * (uint32_t)w);
+        const int nx[4] = {x + 1, x - 1, x, x + 1}, ny[4] = {y, y + 1, y + 1, y + 1};
+        for (int k = 0; k < 4; ++k)
+            if (nx[k] >= 0 && nx[k] < w && ny[k] < h &&
+                lv[(uint32_t)ny[k] * (uint32_t)w + (uint32_t)nx[k]] == g)
+                t_union(par, c, (uint32_t)ny[k] * (uint32_t)w + (uint32_t)nx[k]);
+    }
+    __syncthreads();
+    for (uint32_t c = tid; c < cells; c += kTT)  // flatten: roots first, then publish
+        if (lv[c] != kNoLevel) zsz[c] = (T)t_root(par, c);
+    __syncthreads();
+    for (uint32_t c = tid; c < cells; c += kTT)
+        if (lv[c] != kNoLevel) par[c] = zsz[c];
+    __syncthreads();
+    for (uint32_t c = tid; c < cells; c += kTT) zsz[c] = 0;
+    __syncthreads();
+    for (uint32_t c = tid; c < cells; c += kTT)
+        if (lv[c] != kNoLevel) {
+            if constexpr (sizeof(T) == 2) {
+                // 16-bit atomics: add into the containing word
+                const uint32_t r = par[c];
+                uint32_t* word = reinterpret_cast<uint32_t*>(zsz + (r & ~1u));
+                atomicAdd(word, 1u << ((r & 1u) * 16u));
+            } else {
+                atomicAdd(reinterpret_cast<uint32_t*>(&zsz[par[c]]), 1u);
+            }
+        }
     __syncthreads();
 }
 
@@ -212,6 +341,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
         const uint32_t y = c / (uint32_t)w, x = c - y * (uint32_t)w;
         return img.I[(size_t)(y0 + y) * img.pitch + x0 + x];
     };
+    TT_DECL
     // ---- discretize (texture.cpp:29-56): min/max, then the level raster
     uint32_t lo = 0xffffu, hi = 0u;
     for (uint32_t c = tid; c < cells; c += kTT)
@@ -222,21 +352,28 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
         }
     const uint32_t vmin = tblock_all(lo, sm.u32, TMin()), vmax = tblock_all(hi, sm.u32, TMax());
     const unsigned long long span = (unsigned long long)(vmax - vmin) + 1ull;
+    uint16_t* lv = cells <= 4096u ? sm.slev : S.lev;  // shared memory for S-class windows
     for (uint32_t c = tid; c < cells; c += kTT) {
-        uint16_t lv = kNoLevel;
+        uint16_t l = kNoLevel;
         if (lab_at(c) == label) {
-            lv = 0;
+            l = 0;
             if (vmax > vmin) {
                 const unsigned long long q = (unsigned long long)ng * (int_at(c) - vmin) / span;
-                lv = (uint16_t)(q < (unsigned long long)(ng - 1) ? q : (unsigned long long)(ng - 1));
+                l = (uint16_t)(q < (unsigned long long)(ng - 1) ? q : (unsigned long long)(ng - 1));
             }
         }
-        S.lev[c] = lv;
+        lv[c] = l;
     }
     __syncthreads();
-    const uint32_t mask = HC - 1u;
+    TT(0);
+    // (level, extent) count table: shared memory for S-class windows (kept empty)
+    const bool small = cells <= 4096u && n <= 4096ull;
+    uint32_t* hk = small ? sm.skey : S.hjk;
+    uint32_t* hcn = small ? sm.scnt : S.hjc;
+    uint32_t* hl = small ? sm.slst : S.hjl;
+    const uint32_t mask = small ? 4095u : HC - 1u;
     auto lev = [&](int x, int y) -> uint32_t {
-        return (x >= 0 && x < w && y >= 0 && y < h) ? S.lev[(uint32_t)y * (uint32_t)w + (uint32_t)x]
+        return (x >= 0 && x < w && y >= 0 && y < h) ? lv[(uint32_t)y * (uint32_t)w + (uint32_t)x]
                                                     : (uint32_t)kNoLevel;
     };
     // ---- GLRLM per sorted angle (texture.cpp:242-280)
@@ -255,8 +392,9 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
             }
             double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
             unsigned long long runs = 0;
+            uint32_t emax = 0;
             for (uint32_t c = tid; c < cells; c += kTT) {
-                const uint32_t g = S.lev[c];
+                const uint32_t g = lv[c];
                 if (g == kNoLevel) continue;
                 const int y = (int)(c / (uint32_t)w), x = (int)(c - (uint32_t)y * (uint32_t)w);
                 if (lev(x - dx, y - dy) == g) continue;  // not a run start
@@ -269,16 +407,20 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                 }
                 unit_terms(t, (int)g, len);
                 ++runs;
+                emax = max(emax, len);
                 atomicAdd(&sm.plev[g], 1u);
-                table_add(S.hjk, S.hjc, mask, (g << 24) | len);
+                table_add(hk, hcn, hl, &sm.nfill, mask, (g << 24) | len);
                 atomicAdd(&S.ext[len], 1u);
             }
-            double tt[8];
-            for (int k = 0; k < 8; ++k) tt[k] = tblock_all(t[k], sm.red, TAdd());
+            TT(4);
+            tblock_sum<8>(t, sm.red8);
             const unsigned long long nr = tblock_all(runs, sm.u64, TAdd());
+            emax = tblock_all(emax, sm.u32, TMax());
+            const double* tt = t;
             __shared__ double f16[16];
-            extent_features(tt, nr, n, ng, S, HC, NMAX, sm, f16);
+            extent_features(tt, nr, n, ng, S, hk, hcn, hl, emax, sm, f16);
             __syncthreads();
+            TT(5);
             if (tid < 16) {
                 og[tid * (A + 1) + a] = f16[tid];
                 acc16[tid] += f16[tid];
@@ -287,54 +429,38 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
         }
         if (tid < 16) og[tid * (A + 1) + A] = acc16[tid] / (double)A;
     }
+    TT(1);
     // ---- GLSZM (texture.cpp:343-380): 8-connected zones of equal level
     if (cfg.col_glszm >= 0) {
-        for (uint32_t c = tid; c < cells; c += kTT) {
-            S.par[c] = c;
-            S.zsz[c] = 0u;
-        }
-        __syncthreads();
-        for (uint32_t c = tid; c < cells; c += kTT) {  // forward neighbours E, SW, S, SE
-            const uint32_t g = S.lev[c];
-            if (g == kNoLevel) continue;
-            const int y = (int)(c / (uint32_t)w), x = (int)(c - (uint32_t)y * (uint32_t)w);
-            const int nx[4] = {x + 1, x - 1, x, x + 1}, ny[4] = {y, y + 1, y + 1, y + 1};
-            for (int k = 0; k < 4; ++k)
-                if (lev(nx[k], ny[k]) == g) uf_union(S.par, c, (uint32_t)ny[k] * (uint32_t)w + (uint32_t)nx[k]);
-        }
-        __syncthreads();
-        for (uint32_t c = tid; c < cells; c += kTT)  // flatten: roots first, then publish
-            if (S.lev[c] != kNoLevel) S.zsz[c] = uf_root(S.par, c);
-        __syncthreads();
-        for (uint32_t c = tid; c < cells; c += kTT)
-            if (S.lev[c] != kNoLevel) S.par[c] = S.zsz[c];
-        __syncthreads();
-        for (uint32_t c = tid; c < cells; c += kTT) S.zsz[c] = 0u;
-        __syncthreads();
-        for (uint32_t c = tid; c < cells; c += kTT)
-            if (S.lev[c] != kNoLevel) atomicAdd(&S.zsz[S.par[c]], 1u);
-        __syncthreads();
+        if (small) glszm_zones<uint16_t>(sm.spar, sm.szsz, lv, w, h, cells);
+        else glszm_zones<uint32_t>(S.par, S.zsz, lv, w, h, cells);
+        auto par_at = [&](uint32_t c) -> uint32_t { return small ? sm.spar[c] : S.par[c]; };
+        auto zsz_at = [&](uint32_t c) -> uint32_t { return small ? sm.szsz[c] : S.zsz[c]; };
         double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         unsigned long long zones = 0;
+        uint32_t emax = 0;
         for (uint32_t c = tid; c < cells; c += kTT) {
-            const uint32_t g = S.lev[c];
-            if (g == kNoLevel || S.par[c] != c) continue;
-            const uint32_t size = S.zsz[c];
+            const uint32_t g = lv[c];
+            if (g == kNoLevel || par_at(c) != c) continue;
+            const uint32_t size = zsz_at(c);
             unit_terms(t, (int)g, size);
             ++zones;
+            emax = max(emax, size);
             atomicAdd(&sm.plev[g], 1u);
-            table_add(S.hjk, S.hjc, mask, (g << 24) | size);
+            table_add(hk, hcn, hl, &sm.nfill, mask, (g << 24) | size);
             atomicAdd(&S.ext[size], 1u);
         }
-        double tt[8];
-        for (int k = 0; k < 8; ++k) tt[k] = tblock_all(t[k], sm.red, TAdd());
+        tblock_sum<8>(t, sm.red8);
+        const double* tt = t;
         const unsigned long long nz = tblock_all(zones, sm.u64, TAdd());
+        emax = tblock_all(emax, sm.u32, TMax());
         __shared__ double f16z[16];
-        extent_features(tt, nz, n, ng, S, HC, NMAX, sm, f16z);
+        extent_features(tt, nz, n, ng, S, hk, hcn, hl, emax, sm, f16z);
         __syncthreads();
         if (tid < 16) orow[cfg.col_glszm + tid] = f16z[tid];
         __syncthreads();
     }
+    TT(2);
     // ---- NGTDM (texture.cpp:443-528)
     if (cfg.col_ngtdm >= 0) {
         for (int g = tid; g < ng; g += kTT) {
@@ -344,7 +470,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
         __syncthreads();
         unsigned long long valid = 0;
         for (uint32_t c = tid; c < cells; c += kTT) {
-            const uint32_t g = S.lev[c];
+            const uint32_t g = lv[c];
             if (g == kNoLevel) continue;
             const int y = (int)(c / (uint32_t)w), x = (int)(c - (uint32_t)y * (uint32_t)w);
             int sum = 0, cnt = 0;
@@ -375,9 +501,10 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                 a_s += sv;
                 a_ps += p * sv;
             }
-            const double s_total = tblock_all(a_s, sm.red, TAdd());
-            const double ps_total = tblock_all(a_ps, sm.red, TAdd());
-            const uint32_t present = tblock_all(a_pres, sm.u32, TAdd());
+            double r3[3] = {a_s, a_ps, (double)a_pres};
+            tblock_sum<3>(r3, sm.red8);
+            const double s_total = r3[0], ps_total = r3[1];
+            const uint32_t present = (uint32_t)r3[2];
             double a_con = 0, a_busy = 0, a_cplx = 0, a_strn = 0;
             const uint32_t pairs = (uint32_t)ng * (uint32_t)ng;
             for (uint32_t q = tid; q < pairs; q += kTT) {
@@ -391,10 +518,9 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                 a_cplx += fabs(gi - gj) * (pi * si + pj * sj) / (pi + pj);
                 a_strn += (pi + pj) * (gi - gj) * (gi - gj);
             }
-            const double con = tblock_all(a_con, sm.red, TAdd());
-            const double busy = tblock_all(a_busy, sm.red, TAdd());
-            const double cplx = tblock_all(a_cplx, sm.red, TAdd());
-            const double strn = tblock_all(a_strn, sm.red, TAdd());
+            double r4[4] = {a_con, a_busy, a_cplx, a_strn};
+            tblock_sum<4>(r4, sm.red8);
+            const double con = r4[0], busy = r4[1], cplx = r4[2], strn = r4[3];
             o5[0] = busy > 0 ? ps_total / busy : 0.0;
             o5[1] = ps_total > 0 ? 1.0 / ps_total : 1e6;
             o5[2] = cplx / nv;
@@ -406,6 +532,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
         for (int g = tid; g < ng; g += kTT) sm.plev[g] = 0u;
         __syncthreads();
     }
+    TT(3);
     (void)ctl;
 }
 
@@ -413,6 +540,13 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
 __global__ void __launch_bounds__(kTT) k_roi_t(DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                                                double* out, uint8_t* scratch, TLayout T, int which) {
     __shared__ TShared sm;
+    extern __shared__ __align__(16) uint8_t tdyn[];
+    sm.slev = reinterpret_cast<uint16_t*>(tdyn);
+    sm.skey = reinterpret_cast<uint32_t*>(tdyn + 4096 * 2);
+    sm.scnt = sm.skey + 4096;
+    sm.slst = sm.scnt + 4096;
+    sm.spar = reinterpret_cast<uint16_t*>(sm.slst + 4096);
+    sm.szsz = sm.spar + 4096;
     uint8_t* base = scratch + (size_t)blockIdx.x * T.bytes;
     TSlab S;
     S.lev = (uint16_t*)(base + T.lev);
@@ -420,9 +554,15 @@ __global__ void __launch_bounds__(kTT) k_roi_t(DevImage img, RoiList rl, Control
     S.zsz = (uint32_t*)(base + T.zsz);
     S.hjk = (uint32_t*)(base + T.hjk);
     S.hjc = (uint32_t*)(base + T.hjc);
+    S.hjl = (uint32_t*)(base + T.hjl);
     S.ext = (uint32_t*)(base + T.ext);
     S.ccnt = (uint32_t*)(base + T.ccnt);
     for (int g = threadIdx.x; g < 256; g += kTT) sm.plev[g] = 0u;
+    for (int i = threadIdx.x; i < 4096; i += kTT) {
+        sm.skey[i] = kEmpty;
+        sm.scnt[i] = 0u;
+    }
+    if (threadIdx.x == 0) sm.nfill = 0u;
     __syncthreads();
     const uint32_t n0 = ctl->class_count[kClassS0], n1 = ctl->class_count[kClassS1];
     const uint32_t n2 = ctl->class_count[kClassS2], nl = ctl->class_count[kClassL];
@@ -451,7 +591,10 @@ __global__ void __launch_bounds__(kTT) k_roi_t(DevImage img, RoiList rl, Control
 
 cudaError_t roi_t_setup() {
     k_init_log2_tab<<<4, 256>>>();
-    return cudaDeviceSynchronize();
+    cudaError_t e = cudaDeviceSynchronize();
+    if (e == cudaSuccess)
+        e = cudaFuncSetAttribute(k_roi_t, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kDynBytes);
+    return e;
 }
 
 TLayout make_tlayout(unsigned long long CELLS, uint32_t NMAX) {
@@ -469,6 +612,7 @@ TLayout make_tlayout(unsigned long long CELLS, uint32_t NMAX) {
     T.zsz = take((size_t)CELLS * 4);
     T.hjk = take((size_t)hc * 4);
     T.hjc = take((size_t)hc * 4);
+    T.hjl = take((size_t)hc * 4);
     T.ext = take(((size_t)NMAX + 1) * 4);
     T.ccnt = take(((size_t)NMAX + 1) * 4);
     T.bytes = o;
@@ -500,7 +644,27 @@ __global__ void k_t_init(uint8_t* scratch, TLayout T, int grid) {
 void launch_roi_t(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                   double* out, uint8_t* scratch, const TLayout& T, int which, bool init) {
     if (init) k_t_init<<<grid < 1024 ? grid : 1024, 256, 0, s>>>(scratch, T, grid);
-    k_roi_t<<<grid, kTT, 0, s>>>(img, rl, ctl, cfg, out, scratch, T, which);
+    k_roi_t<<<grid, kTT, kDynBytes, s>>>(img, rl, ctl, cfg, out, scratch, T, which);
+}
+
+// phase clocks of k_roi_t (thread 0 per ROI): 0 discretize, 1 GLRLM (rest),
+// 2 GLSZM, 3 NGTDM, 4 GLRLM run counting, 5 GLRLM features
+extern "C" int fx_debug_texture_clocks(unsigned long long* out, int n, int reset) {
+#ifdef FXG_PHASE_TIMING
+    unsigned long long h[8];
+    if (cudaMemcpyFromSymbol(h, ::g_phase_clk_t, sizeof h) != cudaSuccess) return 7;
+    for (int i = 0; i < n && i < 8; ++i) out[i] = h[i];
+    if (reset) {
+        const unsigned long long z[8] = {};
+        cudaMemcpyToSymbol(::g_phase_clk_t, z, sizeof z);
+    }
+    return 0;
+#else
+    (void)out;
+    (void)n;
+    (void)reset;
+    return 1;
+#endif
 }
 
 }  // namespace fxg

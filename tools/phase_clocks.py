@@ -37,10 +37,13 @@ if which == "c5":
     I = fx.uniform_u16(L.shape, 0)
     run = lambda: ctx.featurize(I, L, ["intensity", "moments", "glcm"], fx.resolve_profile("default"))
     nroi = int(L.max())
+tbuf = (C.c_ulonglong * 8)()
 run()
 lib.fx_debug_phase_clocks(buf, 16, 1)
+lib.fx_debug_texture_clocks(tbuf, 8, 1)
 run()
 assert lib.fx_debug_phase_clocks(buf, 16, 1) == 0, "not a phase-timing build"
+lib.fx_debug_texture_clocks(tbuf, 8, 1)
 tot = sum(buf[:9])
 print(f"{which}: {nroi} ROIs, {tot / nroi:.0f} clocks per ROI (lane 0, S kernels)")
 for k, nm in enumerate(NAMES):
@@ -50,3 +53,9 @@ if totb:
     print(f"large-ROI kernel: {totb / nroi:.0f} clocks per ROI (thread 0)")
     for k, nm in enumerate(BNAMES):
         print(f"  {nm:16s} {buf[9 + k] / nroi:10.0f} clk/ROI  {100 * buf[9 + k] / totb:5.1f}%")
+tt = sum(tbuf[:4])
+if tt:
+    names = ["discretize", "GLRLM other", "GLSZM", "NGTDM", "GLRLM runs", "GLRLM features"]
+    print(f"texture kernel: {tt / nroi:.0f} clocks per ROI (thread 0)")
+    for k, nm in enumerate(names):
+        print(f"  {nm:16s} {tbuf[k] / nroi:10.0f} clk/ROI")
