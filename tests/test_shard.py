@@ -19,7 +19,7 @@ import torch.multiprocessing as mp
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-GROUPS = ["intensity", "moments", "glcm"]
+GROUPS = ["intensity", "shape", "moments", "glcm", "glrlm", "glszm", "ngtdm"]
 
 
 def straddling_image(h=150, w=120, seed=3):
