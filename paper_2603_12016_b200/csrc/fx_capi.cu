@@ -36,6 +36,8 @@ cudaError_t roi_b_setup();
 void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
                          double* out);
 cudaError_t roi_t_setup();
+void launch_moments_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
+                           double* out);
 TLayout make_tlayout(unsigned long long CELLS, uint32_t NMAX);
 void launch_roi_t(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                   double* out, uint8_t* scratch, const TLayout& T, int which, bool init);
@@ -97,6 +99,11 @@ struct fx_ctx {
     size_t tscratch_bytes[2] = {0, 0};
     TLayout tlay_prev[2] = {};
     int tlay_grid[2] = {0, 0};
+    // moments: staged pixels of the S ROIs for k_moments_serial
+    uint32_t* d_mom_px = nullptr;
+    unsigned long long* d_mom_off = nullptr;
+    unsigned long long* d_mom_sums = nullptr;
+    size_t mom_cap = 0, mom_off_cap = 0;
     // shape group: per-ROI staged row masks (S ROIs) for k_shape_serial
     uint64_t* d_shape_rows = nullptr;
     uint32_t* d_shape_hdr = nullptr;
@@ -409,6 +416,29 @@ struct DebugHost {
 
 // Label scan of one image (or band) into the ctx's label table, in global
 // coordinates (image origin added).  reset clears the table first.
+// moments staging: pixels of the S ROIs (bounded; ROIs past the capacity keep the
+// in-warp path) and per-ROI offsets
+constexpr size_t kMomStagePixels = 64ull << 20;
+int ensure_moments(fx_ctx* c, size_t img_pixels) {
+    const size_t want = std::min(kMomStagePixels, std::max<size_t>(img_pixels, 1 << 20));
+    if (want > c->mom_cap || c->roi_cap > c->mom_off_cap) {
+        if (c->stream) cudaStreamSynchronize(c->stream);
+        cudaFree(c->d_mom_px);
+        cudaFree(c->d_mom_off);
+        cudaFree(c->d_mom_sums);
+        c->d_mom_px = nullptr;
+        c->d_mom_off = nullptr;
+        c->d_mom_sums = nullptr;
+        c->mom_cap = c->mom_off_cap = 0;
+        CK(cudaMalloc(&c->d_mom_px, want * sizeof(uint32_t)));
+        CK(cudaMalloc(&c->d_mom_off, c->roi_cap * sizeof(unsigned long long)));
+        CK(cudaMalloc(&c->d_mom_sums, c->roi_cap * 5 * sizeof(unsigned long long)));
+        c->mom_cap = want;
+        c->mom_off_cap = c->roi_cap;
+    }
+    return FX_OK;
+}
+
 // shape staging for roi_cap ROIs: 128 row masks each, headers zeroed (consumed
 // and reset by k_shape_serial)
 int ensure_shape(fx_ctx* c) {
@@ -477,6 +507,14 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         if (rs) return rs;
         cfg.shape_rows = c->d_shape_rows;
         cfg.shape_hdr = c->d_shape_hdr;
+    }
+    if (cfg.col_mom >= 0 && !dbg_dev) {
+        const int rm = ensure_moments(c, (size_t)img.w * (size_t)img.h);
+        if (rm) return rm;
+        cfg.mom_px = c->d_mom_px;
+        cfg.mom_off = c->d_mom_off;
+        cfg.mom_sums = c->d_mom_sums;
+        cfg.mom_cap = c->mom_cap;
     }
     const int vrc = validate_texture(groups, p);
     RoiList rl = roi_list(c);
@@ -558,6 +596,12 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
                 c->tlay_grid[which] = (int)grid;
             }
         }
+    }
+    if (cfg.mom_px) {  // moments of the staged S ROIs
+        const int n_s = (int)(hc.class_count[kClassS0] + hc.class_count[kClassS1] +
+                              hc.class_count[kClassS2]);
+        Launch l(c, "k_moments_serial");
+        launch_moments_serial(n_s, s, rl, c->d_ctl, cfg, out_dev);
     }
     if (cfg.col_shape >= 0) {  // serial shape columns of the S ROIs, before k_roi_b
         const int n_s = (int)(hc.class_count[kClassS0] + hc.class_count[kClassS1] +
@@ -810,6 +854,9 @@ int fx_ctx_destroy(fx_ctx* c) {
     cudaFree(c->d_shape_hdr);
     cudaFree(c->d_tscratch[0]);
     cudaFree(c->d_tscratch[1]);
+    cudaFree(c->d_mom_px);
+    cudaFree(c->d_mom_off);
+    cudaFree(c->d_mom_sums);
     cudaFree(c->d_img);
     cudaFree(c->d_out);
     cudaFree(c->d_lscratch);

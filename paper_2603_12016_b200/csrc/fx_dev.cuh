@@ -85,6 +85,7 @@ struct Control {
     unsigned long long l_max_n;      // max pixel count among L ROIs
     unsigned long long l_max_cells;  // max window cells among L ROIs
     uint32_t t_next[2];              // GLRLM/GLSZM/NGTDM work counters (S lists, L list)
+    unsigned long long mom_alloc;    // moments: pixels staged so far (bump allocator)
 };
 
 // compaction scratch: per (slot, 1024-label block) counts and exclusive bases
@@ -140,6 +141,10 @@ struct FeatCfg {
     int dx[8], dy[8];                // angle_offset (texture.cpp:15-23)
     uint64_t* shape_rows;            // shape: per ROI rank, 64 rows of all pixels + 64 of K
     uint32_t* shape_hdr;             // shape: per ROI rank, h | w << 8 | staged << 16
+    uint32_t* mom_px;                // moments: staged pixels (x | y << 8 | v << 16), or null
+    unsigned long long* mom_off;     // moments: per ROI rank, offset into mom_px (~0: not staged)
+    unsigned long long* mom_sums;    // moments: per ROI rank, sS, sXI, sYI, sLX, sLY (exact)
+    unsigned long long mom_cap;      // moments: capacity of mom_px (pixels)
 };
 
 // GLCM variants of the S kernels: none, key sort (ng > 64), shared histogram

@@ -1181,6 +1181,16 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     // gather member intensities (coalesced within rows), exact integer sums
     unsigned long long sS = 0, sQ = 0, sXI = 0, sYI = 0;
     uint32_t sLX = 0, sLY = 0;
+    // moments by k_moments_serial: stage this ROI's pixels when the buffer has room
+    uint32_t* mst = nullptr;
+    if (cfg.col_mom >= 0 && cfg.mom_px) {
+        unsigned long long off = 0;
+        if (lane == 0) off = atomicAdd(&ctl->mom_alloc, (unsigned long long)((n + 3u) & ~3u));
+        off = __shfl_sync(kFull, off, 0);
+        const bool fits = off + n <= cfg.mom_cap;
+        if (lane == 0) cfg.mom_off[J.row] = fits ? off : ~0ull;
+        if (fits) mst = cfg.mom_px + off;
+    }
     {
         const uint16_t* Ib = img.I + (size_t)J.y0 * img.pitch + J.x0;
 #pragma unroll 1
@@ -1198,6 +1208,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
                 const uint32_t i = b0 + u * 32 + lane;
                 if (i < n) {
                     vals[i] = v[u];
+                    if (mst) mst[i] = p[u] | ((uint32_t)v[u] << 16);
                     const uint32_t x = p[u] & 0xffu, y = p[u] >> 8;
                     sS += v[u];
                     sQ += (unsigned long long)((uint32_t)v[u] * (uint32_t)v[u]);
@@ -1214,6 +1225,11 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
         sYI = warp_sum(sYI);
         sLX = warp_sum(sLX);
         sLY = warp_sum(sLY);
+        if (mst && lane < 5) {
+            const unsigned long long v5 = lane == 0 ? sS : lane == 1 ? sXI : lane == 2 ? sYI
+                                        : lane == 3 ? (unsigned long long)sLX : (unsigned long long)sLY;
+            cfg.mom_sums[(size_t)J.row * 5 + lane] = v5;
+        }
     }
     __syncwarp();
     const double dn = (double)n;
@@ -1597,7 +1613,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     }
     // ------------------------------------------------------------- moments
     PT(6);
-    if (cfg.col_mom >= 0) {
+    if (cfg.col_mom >= 0 && !mst) {  // staged ROIs: k_moments_serial
         const long long nn = (long long)n, W = (long long)sS;
         const long long axb = (2 * (long long)sLX + nn) / (2 * nn);
         const long long ayb = (2 * (long long)sLY + nn) / (2 * nn);
@@ -1860,6 +1876,132 @@ cudaError_t roi_s_setup(int* occ) {
     if (e == cudaSuccess) e = setup_one<kClassS2, kGlSort>(&occ[7]);
     if (e == cudaSuccess) e = setup_one<kClassS2, kGlHist>(&occ[8]);
     return e;
+}
+
+// Moments of the staged S ROIs (moments.cpp:32-92), one thread per ROI: exact
+// integer sums, separable row sums of w dx^p about the integer anchors (pixels are
+// in row-major order), then the binomial shifts to the centroid and the origin,
+// eta and Hu; the same formulas as the warp path, scalar and amortised over 32
+// ROIs per warp.
+__global__ void __launch_bounds__(128) k_moments_serial(RoiList rl, Control* ctl, FeatCfg cfg,
+                                                        double* out) {
+    const uint32_t n0 = ctl->class_count[kClassS0], n1 = ctl->class_count[kClassS1];
+    const uint32_t nt = n0 + n1 + ctl->class_count[kClassS2];
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const uint32_t r = t < n0 ? rl.cls_list[kClassS0][t]
+                     : t < n0 + n1 ? rl.cls_list[kClassS1][t - n0] : rl.cls_list[kClassS2][t - n0 - n1];
+    const unsigned long long off = cfg.mom_off[r];
+    if (off == ~0ull) return;  // not staged: the warp path wrote the columns
+    const uint32_t n = (uint32_t)rl.n[r];
+    const unsigned long long* sums = cfg.mom_sums + (size_t)r * 5;
+    const unsigned long long sS = sums[0], sXI = sums[1], sYI = sums[2], sLX = sums[3], sLY = sums[4];
+    const long long nn = (long long)n, W = (long long)sS;
+    const long long axb = (2 * (long long)sLX + nn) / (2 * nn), ayb = (2 * (long long)sLY + nn) / (2 * nn);
+    const long long axw = W > 0 ? (2 * (long long)sXI + W) / (2 * W) : 0;
+    const long long ayw = W > 0 ? (2 * (long long)sYI + W) / (2 * W) : 0;
+    // every pixel adds its 32 terms (no row flush: divergent flushes across the 32
+    // ROIs of a warp cost more than the extra products); 16 B loads, two in flight
+    double Nb[16], Nw[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) Nb[k] = Nw[k] = 0;
+    auto pixel = [&](uint32_t e) {
+        const double db = (double)((long long)(e & 0xffu) - axb), dw = (double)((long long)(e & 0xffu) - axw);
+        const double yb = (double)((long long)((e >> 8) & 0xffu) - ayb);
+        const double yw = (double)((long long)((e >> 8) & 0xffu) - ayw);
+        const double wv = (double)(e >> 16);
+        const double pb[4] = {1.0, db, db * db, db * db * db};
+        const double pw[4] = {wv, wv * dw, wv * dw * dw, wv * dw * dw * dw};
+        const double qb[4] = {1.0, yb, yb * yb, yb * yb * yb};
+        const double qw[4] = {1.0, yw, yw * yw, yw * yw * yw};
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                Nb[p * 4 + q] += pb[p] * qb[q];
+                Nw[p * 4 + q] += pw[p] * qw[q];
+            }
+    };
+    const uint4* px4 = reinterpret_cast<const uint4*>(cfg.mom_px + off);  // 16 B aligned
+    const uint32_t nq = (n + 3u) >> 2;
+    uint4 cur = px4[0], nxt = nq > 1 ? px4[1] : make_uint4(0, 0, 0, 0);
+    for (uint32_t q4 = 0; q4 < nq; ++q4) {
+        const uint4 fut = q4 + 2 < nq ? px4[q4 + 2] : make_uint4(0, 0, 0, 0);
+        const uint32_t base = q4 * 4u;
+        pixel(cur.x);
+        if (base + 1 < n) pixel(cur.y);
+        if (base + 2 < n) pixel(cur.z);
+        if (base + 3 < n) pixel(cur.w);
+        cur = nxt;
+        nxt = fut;
+    }
+    const long long gx0 = rl.gx[r], gy0 = rl.gy[r];
+    const double dn = (double)n;
+    double* o0 = out + (size_t)r * cfg.ncols + cfg.col_mom;
+    for (int grp = 0; grp < 2; ++grp) {
+        const double* N = grp ? Nw : Nb;
+        double* o = o0 + grp * 52;
+        const bool zero_mass = grp && sS == 0;
+        const double m00 = grp ? (double)sS : dn;
+        const double dx = grp ? (W > 0 ? (double)((long long)sXI - axw * W) / (double)W : 0.0)
+                              : (double)((long long)sLX - axb * nn) / dn;
+        const double dy = grp ? (W > 0 ? (double)((long long)sYI - ayw * W) / (double)W : 0.0)
+                              : (double)((long long)sLY - ayb * nn) / dn;
+        const double Ax = (double)(gx0 + (grp ? axw : axb)), Ay = (double)(gy0 + (grp ? ayw : ayb));
+        const double C[4][4] = {{1, 0, 0, 0}, {1, 1, 0, 0}, {1, 2, 1, 0}, {1, 3, 3, 1}};
+        double pmx[4], pmy[4], pax[4], pay[4];
+        pmx[0] = pmy[0] = pax[0] = pay[0] = 1.0;
+        for (int k = 1; k < 4; ++k) {
+            pmx[k] = pmx[k - 1] * (-dx);
+            pmy[k] = pmy[k - 1] * (-dy);
+            pax[k] = pax[k - 1] * Ax;
+            pay[k] = pay[k - 1] * Ay;
+        }
+        double eta[4][4];
+        for (int p = 0; p < 4; ++p)
+            for (int q = 0; q < 4; ++q) {
+                double mu = 0, raw = 0;
+                for (int i = 0; i <= p; ++i)
+                    for (int j = 0; j <= q; ++j) {
+                        const double cc = C[p][i] * C[q][j];
+                        mu += cc * pmx[p - i] * pmy[q - j] * N[i * 4 + j];
+                        raw += cc * pax[p - i] * pay[q - j] * N[i * 4 + j];
+                    }
+                if ((p == 1 && q == 0) || (p == 0 && q == 1)) mu = 0.0;  // moments.cpp:80-81
+                if (p == 0 && q == 0) mu = N[0];
+                double et = 0;
+                if (p + q >= 2) {  // eta = mu / m00^(1 + (p+q)/2)
+                    double den = m00 * m00;
+                    if (p + q >= 4) den *= m00;
+                    if (p + q >= 6) den *= m00;
+                    if ((p + q) & 1) den *= sqrt(m00);
+                    et = mu / den;
+                }
+                if (zero_mass) raw = mu = et = 0;
+                eta[p][q] = et;
+                o[p * 4 + q] = raw;
+                o[16 + p * 4 + q] = mu;
+                if (p + q >= 2) o[32 + ((p == 0) ? q - 2 : (p == 1 ? 1 + q : 1 + 4 * (p - 1) + q))] = et;
+            }
+        const double n20 = eta[2][0], n02 = eta[0][2], n11 = eta[1][1], n30 = eta[3][0],
+                     n03 = eta[0][3], n21 = eta[2][1], n12 = eta[1][2];
+        const double a = n30 + n12, b = n21 + n03;
+        const double hu[7] = {n20 + n02,
+                              (n20 - n02) * (n20 - n02) + 4.0 * n11 * n11,
+                              (n30 - 3.0 * n12) * (n30 - 3.0 * n12) + (3.0 * n21 - n03) * (3.0 * n21 - n03),
+                              a * a + b * b,
+                              (n30 - 3.0 * n12) * a * (a * a - 3.0 * b * b) +
+                                  (3.0 * n21 - n03) * b * (3.0 * a * a - b * b),
+                              (n20 - n02) * (a * a - b * b) + 4.0 * n11 * a * b,
+                              (3.0 * n21 - n03) * a * (a * a - 3.0 * b * b) -
+                                  (n30 - 3.0 * n12) * b * (3.0 * a * a - b * b)};
+        for (int k = 0; k < 7; ++k) o[45 + k] = zero_mass ? 0.0 : hu[k];
+    }
+}
+
+void launch_moments_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
+                           double* out) {
+    if (n_s > 0) k_moments_serial<<<(n_s + 127) / 128, 128, 0, s>>>(rl, ctl, cfg, out);
 }
 
 void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
