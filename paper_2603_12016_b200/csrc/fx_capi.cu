@@ -38,6 +38,8 @@ void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, Feat
 cudaError_t roi_t_setup();
 void launch_moments_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
                            double* out);
+void launch_intensity_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
+                             double* out);
 TLayout make_tlayout(unsigned long long CELLS, uint32_t NMAX);
 void launch_roi_t(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                   double* out, uint8_t* scratch, const TLayout& T, int which, bool init);
@@ -103,6 +105,10 @@ struct fx_ctx {
     uint32_t* d_mom_px = nullptr;
     unsigned long long* d_mom_off = nullptr;
     unsigned long long* d_mom_sums = nullptr;
+    uint16_t* d_int_vals = nullptr;  // intensity: staged sorted values of the S ROIs
+    unsigned long long* d_int_off = nullptr;
+    unsigned long long* d_int_sums = nullptr;
+    size_t int_cap = 0, int_off_cap = 0;
     size_t mom_cap = 0, mom_off_cap = 0;
     // shape group: per-ROI staged row masks (S ROIs) for k_shape_serial
     uint64_t* d_shape_rows = nullptr;
@@ -439,6 +445,26 @@ int ensure_moments(fx_ctx* c, size_t img_pixels) {
     return FX_OK;
 }
 
+int ensure_intensity(fx_ctx* c, size_t img_pixels) {
+    const size_t want = std::min(kMomStagePixels, std::max<size_t>(img_pixels, 1 << 20));
+    if (want > c->int_cap || c->roi_cap > c->int_off_cap) {
+        if (c->stream) cudaStreamSynchronize(c->stream);
+        cudaFree(c->d_int_vals);
+        cudaFree(c->d_int_off);
+        cudaFree(c->d_int_sums);
+        c->d_int_vals = nullptr;
+        c->d_int_off = nullptr;
+        c->d_int_sums = nullptr;
+        c->int_cap = c->int_off_cap = 0;
+        CK(cudaMalloc(&c->d_int_vals, want * sizeof(uint16_t)));
+        CK(cudaMalloc(&c->d_int_off, c->roi_cap * sizeof(unsigned long long)));
+        CK(cudaMalloc(&c->d_int_sums, c->roi_cap * 2 * sizeof(unsigned long long)));
+        c->int_cap = want;
+        c->int_off_cap = c->roi_cap;
+    }
+    return FX_OK;
+}
+
 // shape staging for roi_cap ROIs: 128 row masks each, headers zeroed (consumed
 // and reset by k_shape_serial)
 int ensure_shape(fx_ctx* c) {
@@ -507,6 +533,14 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         if (rs) return rs;
         cfg.shape_rows = c->d_shape_rows;
         cfg.shape_hdr = c->d_shape_hdr;
+    }
+    if (cfg.col_int >= 0 && !dbg_dev) {
+        const int ri = ensure_intensity(c, (size_t)img.w * (size_t)img.h);
+        if (ri) return ri;
+        cfg.int_vals = c->d_int_vals;
+        cfg.int_off = c->d_int_off;
+        cfg.int_sums = c->d_int_sums;
+        cfg.int_cap = c->int_cap;
     }
     if (cfg.col_mom >= 0 && !dbg_dev) {
         const int rm = ensure_moments(c, (size_t)img.w * (size_t)img.h);
@@ -596,6 +630,12 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
                 c->tlay_grid[which] = (int)grid;
             }
         }
+    }
+    if (cfg.int_vals) {  // intensity statistics of the staged S ROIs
+        const int n_s = (int)(hc.class_count[kClassS0] + hc.class_count[kClassS1] +
+                              hc.class_count[kClassS2]);
+        Launch l(c, "k_intensity_serial");
+        launch_intensity_serial(n_s, s, rl, c->d_ctl, cfg, out_dev);
     }
     if (cfg.mom_px) {  // moments of the staged S ROIs
         const int n_s = (int)(hc.class_count[kClassS0] + hc.class_count[kClassS1] +
@@ -857,6 +897,9 @@ int fx_ctx_destroy(fx_ctx* c) {
     cudaFree(c->d_mom_px);
     cudaFree(c->d_mom_off);
     cudaFree(c->d_mom_sums);
+    cudaFree(c->d_int_vals);
+    cudaFree(c->d_int_off);
+    cudaFree(c->d_int_sums);
     cudaFree(c->d_img);
     cudaFree(c->d_out);
     cudaFree(c->d_lscratch);

@@ -86,6 +86,7 @@ struct Control {
     unsigned long long l_max_cells;  // max window cells among L ROIs
     uint32_t t_next[2];              // GLRLM/GLSZM/NGTDM work counters (S lists, L list)
     unsigned long long mom_alloc;    // moments: pixels staged so far (bump allocator)
+    unsigned long long int_alloc;    // intensity: sorted values staged so far
 };
 
 // compaction scratch: per (slot, 1024-label block) counts and exclusive bases
@@ -145,6 +146,10 @@ struct FeatCfg {
     unsigned long long* mom_off;     // moments: per ROI rank, offset into mom_px (~0: not staged)
     unsigned long long* mom_sums;    // moments: per ROI rank, sS, sXI, sYI, sLX, sLY (exact)
     unsigned long long mom_cap;      // moments: capacity of mom_px (pixels)
+    uint16_t* int_vals;              // intensity: staged sorted values, or null
+    unsigned long long* int_off;     // intensity: per ROI rank, offset (~0: not staged)
+    unsigned long long* int_sums;    // intensity: per ROI rank, sum v, sum v^2 (exact)
+    unsigned long long int_cap;      // intensity: capacity of int_vals (values)
 };
 
 // GLCM variants of the S kernels: none, key sort (ng > 64), shared histogram

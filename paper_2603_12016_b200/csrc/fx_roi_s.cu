@@ -1326,279 +1326,318 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
                                          (uint32_t*)(base + L.cnt));
         __syncwarp();
         PT(1);
-        vmin = s[0];
-        vmax = s[n - 1];
-        have_minmax = true;
-        const double mean = (double)sS / dn;
-        const double mn = (double)vmin, mxv = (double)vmax, range = mxv - mn;
-        const double median =
-            (n & 1) ? (double)s[n / 2] : 0.5 * ((double)s[n / 2 - 1] + (double)s[n / 2]);
-        // percentiles (lanes 0..5), literal expression (intensity_features.cpp:14-22)
-        double myp = 0;
-        if (lane < 6) {
-            const double pv = lane == 0 ? 1.0 : lane == 1 ? 10.0 : lane == 2 ? 25.0
-                            : lane == 3 ? 75.0 : lane == 4 ? 90.0 : 99.0;
-            myp = percentile_exact(s, n, pv);
-        }
-        const double p10 = __shfl_sync(kFull, myp, 1), p25 = __shfl_sync(kFull, myp, 2);
-        const double p75 = __shfl_sync(kFull, myp, 3), p90 = __shfl_sync(kFull, myp, 4);
-        // median absolute deviation (exact: k-th of the two sorted half-sequences)
-        const uint32_t M2 = (n & 1) ? 2u * s[n / 2] : (uint32_t)s[n / 2 - 1] + s[n / 2];
-        const uint32_t d_hi = kth_dev2_warp(s, n, M2, n / 2);
-        const uint32_t d_lo = (n & 1) ? d_hi : kth_dev2_warp(s, n, M2, n / 2 - 1);
-        const double median_ad = (n & 1) ? 0.5 * (double)d_hi
-                                         : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
-        // one pass over the sorted values: central moments (fp64), exact integer
-        // partial sums for mad and the [p10,p90] subset, value runs (mode) and
-        // histogram-bin runs (entropy = sum c (log2 n - log2 c) / n, uniformity =
-        // sum c^2 / n^2; bins = floor(nb (v - min) / range), exact, A2)
-        const uint32_t nb32 = (uint32_t)cfg.bins;
-        const bool wide = (unsigned long long)nb32 * 65535ull >= (1ull << 32);
-        const uint32_t rng = vmax - vmin;
-        // floor(num / rng) by multiply-high with one correction step (num < 2^32)
-        const uint32_t magic = rng ? (uint32_t)(0xffffffffull / rng) : 0u;
-        auto bin_of = [&](uint32_t v) -> uint32_t {
-            if (rng == 0) return 0u;
-            uint32_t b;
-            if (!wide) {
-                const uint32_t num = nb32 * (v - vmin);
-                b = __umulhi(num, magic);
-                if (num - b * rng >= rng) ++b;
-            } else {
-                b = (uint32_t)((unsigned long long)nb32 * (v - vmin) / rng);
+        // order statistics and moments of the values by k_intensity_serial when the
+        // sorted values can be staged (the warp keeps the edge set and edge stats)
+        bool staged = false;
+        if (cfg.int_vals) {
+            unsigned long long off = 0;
+            if (lane == 0) off = atomicAdd(&ctl->int_alloc, (unsigned long long)((n + 7u) & ~7u));
+            off = __shfl_sync(kFull, off, 0);
+            staged = off + n <= cfg.int_cap;
+            if (lane == 0) cfg.int_off[J.row] = staged ? off : ~0ull;
+            if (staged) {
+                uint16_t* dst = cfg.int_vals + off;
+                for (uint32_t i = lane; i < n; i += 32) dst[i] = s[i];
+                if (lane < 2) cfg.int_sums[(size_t)J.row * 2 + lane] = lane ? sQ : sS;
             }
-            return b < nb32 - 1 ? b : nb32 - 1;
-        };
-        const double logn = nlog2(dn);
-        double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // m2..m6, entropy sum
-        unsigned long long best = 0, slo = 0, rsum = 0, usq = 0;
-        uint32_t clo = 0, rn = 0, carry_v = 0, carry_b = 0;
-        uint32_t prev_v = 0xffffffffu, prev_b = 0xffffffffu;
-#pragma unroll 1
-        for (uint32_t b0 = 0; b0 < n; b0 += 32) {
-            const uint32_t i = b0 + lane;
-            const bool ok = i < n;
-            const uint32_t v = ok ? s[i] : 0xfffffffeu;
-            const uint32_t bin = ok ? bin_of(v) : 0xfffffffeu;
-            const uint32_t nxt = b0 + 32 < n ? s[b0 + 32] : 0xfffffffeu;  // next chunk head
-            uint32_t pv = __shfl_up_sync(kFull, v, 1), pb = __shfl_up_sync(kFull, bin, 1);
-            uint32_t nv = __shfl_down_sync(kFull, v, 1), nbn = __shfl_down_sync(kFull, bin, 1);
-            if (lane == 0) {
-                pv = prev_v;
-                pb = prev_b;
-            }
-            if (lane == 31) {
-                nv = nxt;
-                nbn = b0 + 32 < n ? bin_of(nxt) : 0xfffffffeu;
-            }
-            if (i + 1 == n) {
-                nv = 0xfffffffdu;
-                nbn = 0xfffffffdu;
-            }
-            const bool vstart = ok && pv != v, vend = ok && nv != v;
-            const bool bstart = ok && pb != bin, bend = ok && nbn != bin;
-            const unsigned vs = __ballot_sync(kFull, vstart), bs = __ballot_sync(kFull, bstart);
-            const unsigned le = lanemask_lt() | (1u << lane);
-            if (ok) {
-                const double d = (double)v - mean;
-                const double d2 = d * d;
-                acc[0] += d2;
-                acc[1] += d2 * d;
-                acc[2] += d2 * d2;
-                acc[3] += d2 * d2 * d;
-                acc[4] += d2 * d2 * d2;
-                if ((double)v < mean) {
-                    slo += v;
-                    ++clo;
-                }
-                const double x = (double)v;
-                if (x >= p10 && x <= p90) {
-                    rsum += v;
-                    ++rn;
-                }
-                if (vend) {
-                    const uint32_t st = (vs & le) ? b0 + 31 - __clz(vs & le) : carry_v;
-                    const unsigned long long key =
-                        ((unsigned long long)(i - st + 1) << 16) | (0xffffu - v);
-                    best = key > best ? key : best;
-                }
-                if (bend) {
-                    const uint32_t st = (bs & le) ? b0 + 31 - __clz(bs & le) : carry_b;
-                    const uint32_t c = i - st + 1;
-                    acc[5] += (double)c * (logn - log2_int(c));
-                    usq += (unsigned long long)c * c;
-                    if (dbg_on && bin < nb32) dbg->hist[bin] = c;
-                }
-            }
-            if (vs) carry_v = b0 + 31 - __clz(vs);
-            if (bs) carry_b = b0 + 31 - __clz(bs);
-            prev_v = __shfl_sync(kFull, v, 31);
-            prev_b = __shfl_sync(kFull, bin, 31);
-        }
-        warp_sum8(acc);
-        best = warp_max(best);
-        slo = warp_sum(slo);
-        clo = warp_sum(clo);
-        rsum = warp_sum(rsum);
-        rn = warp_sum(rn);
-        usq = warp_sum(usq);
-        const double m2 = acc[0] / dn, m3 = acc[1] / dn, m4 = acc[2] / dn, m5 = acc[3] / dn,
-                     m6 = acc[4] / dn;
-        // sum |x - mean| = (S_hi - S_lo) + (c_lo - c_hi) mean, exact integer parts
-        const double mad = ((double)(long long)(sS - 2 * slo) +
-                            (double)((long long)clo - (long long)(n - clo)) * mean) / dn;
-        const double entropy = acc[5] / dn;
-        const double uniformity = (double)usq / (dn * dn);
-        double rmad = 0;
-        if (rn > 0) {
-            const double rmean = (double)rsum / (double)rn;
-            unsigned long long rlo = 0;
-            uint32_t rcl = 0;
-#pragma unroll 1
-            for (uint32_t i = lane; i < n; i += 32) {
-                const double x = (double)s[i];
-                if (x >= p10 && x <= p90 && x < rmean) {
-                    rlo += s[i];
-                    ++rcl;
-                }
-            }
-            rlo = warp_sum(rlo);
-            rcl = warp_sum(rcl);
-            rmad = ((double)(long long)(rsum - 2 * rlo) +
-                    (double)((long long)rcl - (long long)(rn - rcl)) * rmean) / (double)rn;
+            __syncwarp();
         }
         // ------------------------------------------------ edge set
-        PT(2);
         double e_mean = 0, e_min = 0, e_max = 0, e_std = 0, e_int = 0;
-        {
-            uint64_t k0, k1, e0, e1;
-            if (!edge_ke(k0, k1, e0, e1)) return;
-            ks0 = k0;
-            ks1 = k1;
-            have_k = true;
-            // edge = K & (4-neighbour in E, or on the window border)
-            const uint64_t eu0 = __shfl_up_sync(kFull, e0, 1), ed0 = __shfl_down_sync(kFull, e0, 1);
-            const uint64_t eu1 = __shfl_up_sync(kFull, e1, 1), ed1 = __shfl_down_sync(kFull, e1, 1);
-            const uint64_t el31 = __shfl_sync(kFull, e0, 31), ef32 = __shfl_sync(kFull, e1, 0);
-            const uint64_t side = 1ull | (1ull << (w - 1));
-            uint64_t g0 = (e0 << 1) | (e0 >> 1) | (lane == 0 ? 0ull : eu0) | (lane == 31 ? ef32 : ed0) | side;
-            uint64_t g1 = (e1 << 1) | (e1 >> 1) | (lane == 0 ? el31 : eu1) | (lane == 31 ? 0ull : ed1) | side;
-            if (lane == 0 || (int)lane == h - 1) g0 = ~0ull;
-            if ((int)lane + 32 == h - 1) g1 = ~0ull;
-            const uint64_t ed[2] = {(int)lane < h ? (k0 & g0) : 0ull, (int)lane + 32 < h ? (k1 & g1) : 0ull};
-            const uint64_t rm[2] = {m0, m1};
-            const uint32_t ro[2] = {off0, off1};
-            // one pass: exact integer sum and sum of squares -> mean, population std
-            unsigned long long es = 0, esq = 0;
-            uint32_t en = 0, emn = 0xffffffffu, emx = 0;
-#pragma unroll
-            for (int hf = 0; hf < 2; ++hf) {
-                uint64_t e = ed[hf];
-                while (e) {
-                    const int b = __ffsll((long long)e) - 1;
-                    e &= e - 1;
-                    const uint32_t v = vals[ro[hf] + __popcll(rm[hf] & ((1ull << b) - 1ull))];
-                    es += v;
-                    esq += (unsigned long long)(v * v);
-                    ++en;
-                    emn = min(emn, v);
-                    emx = max(emx, v);
-                }
-            }
-            es = warp_sum(es);
-            esq = warp_sum(esq);
-            en = warp_sum(en);
-            emn = warp_min(emn);
-            emx = warp_max(emx);
-            if (en) {
-                const double den = (double)en;
-                e_mean = (double)es / den;
-                e_min = (double)emn;
-                e_max = (double)emx;
-                e_int = (double)es;
-                // n^2 var = n sum v^2 - (sum v)^2, exact in u64 (< 2^56 for S windows)
-                e_std = sqrt((double)(en * esq - es * es) / (den * den));
-            }
-            if (dbg_on) {
-                uint32_t cnt_e = __popcll(ed[0]) + __popcll(ed[1]);
-                const uint32_t incl = warp_incl_scan(cnt_e);
-                uint32_t j = incl - cnt_e;
-#pragma unroll
+        auto edge_stats = [&]() -> bool {
+            {
+                uint64_t k0, k1, e0, e1;
+                if (!edge_ke(k0, k1, e0, e1)) return false;
+                ks0 = k0;
+                ks1 = k1;
+                have_k = true;
+                // edge = K & (4-neighbour in E, or on the window border)
+                const uint64_t eu0 = __shfl_up_sync(kFull, e0, 1), ed0 = __shfl_down_sync(kFull, e0, 1);
+                const uint64_t eu1 = __shfl_up_sync(kFull, e1, 1), ed1 = __shfl_down_sync(kFull, e1, 1);
+                const uint64_t el31 = __shfl_sync(kFull, e0, 31), ef32 = __shfl_sync(kFull, e1, 0);
+                const uint64_t side = 1ull | (1ull << (w - 1));
+                uint64_t g0 = (e0 << 1) | (e0 >> 1) | (lane == 0 ? 0ull : eu0) | (lane == 31 ? ef32 : ed0) | side;
+                uint64_t g1 = (e1 << 1) | (e1 >> 1) | (lane == 0 ? el31 : eu1) | (lane == 31 ? 0ull : ed1) | side;
+                if (lane == 0 || (int)lane == h - 1) g0 = ~0ull;
+                if ((int)lane + 32 == h - 1) g1 = ~0ull;
+                const uint64_t ed[2] = {(int)lane < h ? (k0 & g0) : 0ull, (int)lane + 32 < h ? (k1 & g1) : 0ull};
+                const uint64_t rm[2] = {m0, m1};
+                const uint32_t ro[2] = {off0, off1};
+                // one pass: exact integer sum and sum of squares -> mean, population std
+                unsigned long long es = 0, esq = 0;
+                uint32_t en = 0, emn = 0xffffffffu, emx = 0;
+    #pragma unroll
                 for (int hf = 0; hf < 2; ++hf) {
                     uint64_t e = ed[hf];
                     while (e) {
                         const int b = __ffsll((long long)e) - 1;
                         e &= e - 1;
-                        if (j < dbg->cap_edge) {
-                            dbg->edge_xy[2 * j] = (int32_t)(gx0 + b);
-                            dbg->edge_xy[2 * j + 1] = (int32_t)(gy0 + lane + 32 * hf);
-                        }
-                        ++j;
+                        const uint32_t v = vals[ro[hf] + __popcll(rm[hf] & ((1ull << b) - 1ull))];
+                        es += v;
+                        esq += (unsigned long long)(v * v);
+                        ++en;
+                        emn = min(emn, v);
+                        emx = max(emx, v);
                     }
                 }
-                if (lane == 31) *dbg->n_edge = j;
+                es = warp_sum(es);
+                esq = warp_sum(esq);
+                en = warp_sum(en);
+                emn = warp_min(emn);
+                emx = warp_max(emx);
+                if (en) {
+                    const double den = (double)en;
+                    e_mean = (double)es / den;
+                    e_min = (double)emn;
+                    e_max = (double)emx;
+                    e_int = (double)es;
+                    // n^2 var = n sum v^2 - (sum v)^2, exact in u64 (< 2^56 for S windows)
+                    e_std = sqrt((double)(en * esq - es * es) / (den * den));
+                }
+                if (dbg_on) {
+                    uint32_t cnt_e = __popcll(ed[0]) + __popcll(ed[1]);
+                    const uint32_t incl = warp_incl_scan(cnt_e);
+                    uint32_t j = incl - cnt_e;
+    #pragma unroll
+                    for (int hf = 0; hf < 2; ++hf) {
+                        uint64_t e = ed[hf];
+                        while (e) {
+                            const int b = __ffsll((long long)e) - 1;
+                            e &= e - 1;
+                            if (j < dbg->cap_edge) {
+                                dbg->edge_xy[2 * j] = (int32_t)(gx0 + b);
+                                dbg->edge_xy[2 * j + 1] = (int32_t)(gy0 + lane + 32 * hf);
+                            }
+                            ++j;
+                        }
+                    }
+                    if (lane == 31) *dbg->n_edge = j;
+                }
             }
-        }
-        double wcx = 0, wcy = 0;
-        if (sS > 0) {
-            wcx = (double)((unsigned long long)gx0 * sS + sXI) / (double)sS;
-            wcy = (double)((unsigned long long)gy0 * sS + sYI) / (double)sS;
-        }
-        const double var = n > 1 ? m2 * dn / (dn - 1.0) : 0.0;
-        double skew = 0, kurt = 0, hsk = 0, hfl = 0;
-        if (m2 > 0) {
-            const double r2 = sqrt(m2);
-            skew = m3 / (m2 * r2);
-            kurt = m4 / (m2 * m2);
-            hsk = m5 / (m2 * m2 * r2);
-            hfl = m6 / (m2 * m2 * m2);
-        }
-        const double mode = (double)(0xffffu - (uint32_t)(best & 0xffffu));
-        const double energy = (double)sQ, sdev = sqrt(var);
-        const double iqr = p75 - p25;
-        // lane k writes column k (coalesced row segment); columns 32..38 by lanes 0..6
-        const double pct = __shfl_sync(kFull, myp, (lane - 14) & 31);
-        double o = 0;
-        switch (lane) {
-            case 0: o = mean; break;
-            case 1: o = median; break;
-            case 2: o = mode; break;
-            case 3: o = mn; break;
-            case 4: o = mxv; break;
-            case 5: o = range; break;
-            case 6: o = var; break;
-            case 7: o = m2; break;
-            case 8: o = sdev; break;
-            case 9: o = sqrt(m2); break;
-            case 10: o = mad; break;
-            case 11: o = median_ad; break;
-            case 12: o = rmad; break;
-            case 13: o = iqr; break;
-            case 14: case 15: case 16: case 17: case 18: case 19: o = pct; break;
-            case 20: o = skew; break;
-            case 21: o = kurt; break;
-            case 22: o = m2 > 0 ? kurt - 3.0 : 0.0; break;
-            case 23: o = hsk; break;
-            case 24: o = hfl; break;
-            case 25: o = energy; break;
-            case 26: o = sqrt(energy / dn); break;
-            case 27: o = entropy; break;
-            case 28: o = uniformity; break;
-            case 29: o = (p75 + p25) != 0 ? iqr / (p75 + p25) : 0.0; break;
-            case 30: o = mean != 0 ? sdev / mean : 0.0; break;
-            default: o = (double)sS; break;
-        }
-        double* oi = orow + cfg.col_int;
-        oi[lane] = o;
-        if (lane < 7) {
-            const double t[7] = {e_mean, e_min, e_max, e_std, e_int, wcx, wcy};
-            double v = t[0];
+            return true;
+        };
+        if (staged) {
+            PT(2);
+            if (!edge_stats()) return;
+            double wcx = 0, wcy = 0;
+            if (sS > 0) {
+                wcx = (double)((unsigned long long)gx0 * sS + sXI) / (double)sS;
+                wcy = (double)((unsigned long long)gy0 * sS + sYI) / (double)sS;
+            }
+            if (lane < 7) {
+                const double t[7] = {e_mean, e_min, e_max, e_std, e_int, wcx, wcy};
+                double v = t[0];
 #pragma unroll
-            for (int k = 1; k < 7; ++k)
-                if ((int)lane == k) v = t[k];
-            oi[32 + lane] = v;
+                for (int k = 1; k < 7; ++k)
+                    if ((int)lane == k) v = t[k];
+                orow[cfg.col_int + 32 + lane] = v;
+            }
+            __syncwarp();
+        } else {
+            vmin = s[0];
+            vmax = s[n - 1];
+            have_minmax = true;
+            const double mean = (double)sS / dn;
+            const double mn = (double)vmin, mxv = (double)vmax, range = mxv - mn;
+            const double median =
+                (n & 1) ? (double)s[n / 2] : 0.5 * ((double)s[n / 2 - 1] + (double)s[n / 2]);
+            // percentiles (lanes 0..5), literal expression (intensity_features.cpp:14-22)
+            double myp = 0;
+            if (lane < 6) {
+                const double pv = lane == 0 ? 1.0 : lane == 1 ? 10.0 : lane == 2 ? 25.0
+                                : lane == 3 ? 75.0 : lane == 4 ? 90.0 : 99.0;
+                myp = percentile_exact(s, n, pv);
+            }
+            const double p10 = __shfl_sync(kFull, myp, 1), p25 = __shfl_sync(kFull, myp, 2);
+            const double p75 = __shfl_sync(kFull, myp, 3), p90 = __shfl_sync(kFull, myp, 4);
+            // median absolute deviation (exact: k-th of the two sorted half-sequences)
+            const uint32_t M2 = (n & 1) ? 2u * s[n / 2] : (uint32_t)s[n / 2 - 1] + s[n / 2];
+            const uint32_t d_hi = kth_dev2_warp(s, n, M2, n / 2);
+            const uint32_t d_lo = (n & 1) ? d_hi : kth_dev2_warp(s, n, M2, n / 2 - 1);
+            const double median_ad = (n & 1) ? 0.5 * (double)d_hi
+                                             : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
+            // one pass over the sorted values: central moments (fp64), exact integer
+            // partial sums for mad and the [p10,p90] subset, value runs (mode) and
+            // histogram-bin runs (entropy = sum c (log2 n - log2 c) / n, uniformity =
+            // sum c^2 / n^2; bins = floor(nb (v - min) / range), exact, A2)
+            const uint32_t nb32 = (uint32_t)cfg.bins;
+            const bool wide = (unsigned long long)nb32 * 65535ull >= (1ull << 32);
+            const uint32_t rng = vmax - vmin;
+            // floor(num / rng) by multiply-high with one correction step (num < 2^32)
+            const uint32_t magic = rng ? (uint32_t)(0xffffffffull / rng) : 0u;
+            auto bin_of = [&](uint32_t v) -> uint32_t {
+                if (rng == 0) return 0u;
+                uint32_t b;
+                if (!wide) {
+                    const uint32_t num = nb32 * (v - vmin);
+                    b = __umulhi(num, magic);
+                    if (num - b * rng >= rng) ++b;
+                } else {
+                    b = (uint32_t)((unsigned long long)nb32 * (v - vmin) / rng);
+                }
+                return b < nb32 - 1 ? b : nb32 - 1;
+            };
+            const double logn = nlog2(dn);
+            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // m2..m6, entropy sum
+            unsigned long long best = 0, slo = 0, rsum = 0, usq = 0;
+            uint32_t clo = 0, rn = 0, carry_v = 0, carry_b = 0;
+            uint32_t prev_v = 0xffffffffu, prev_b = 0xffffffffu;
+    #pragma unroll 1
+            for (uint32_t b0 = 0; b0 < n; b0 += 32) {
+                const uint32_t i = b0 + lane;
+                const bool ok = i < n;
+                const uint32_t v = ok ? s[i] : 0xfffffffeu;
+                const uint32_t bin = ok ? bin_of(v) : 0xfffffffeu;
+                const uint32_t nxt = b0 + 32 < n ? s[b0 + 32] : 0xfffffffeu;  // next chunk head
+                uint32_t pv = __shfl_up_sync(kFull, v, 1), pb = __shfl_up_sync(kFull, bin, 1);
+                uint32_t nv = __shfl_down_sync(kFull, v, 1), nbn = __shfl_down_sync(kFull, bin, 1);
+                if (lane == 0) {
+                    pv = prev_v;
+                    pb = prev_b;
+                }
+                if (lane == 31) {
+                    nv = nxt;
+                    nbn = b0 + 32 < n ? bin_of(nxt) : 0xfffffffeu;
+                }
+                if (i + 1 == n) {
+                    nv = 0xfffffffdu;
+                    nbn = 0xfffffffdu;
+                }
+                const bool vstart = ok && pv != v, vend = ok && nv != v;
+                const bool bstart = ok && pb != bin, bend = ok && nbn != bin;
+                const unsigned vs = __ballot_sync(kFull, vstart), bs = __ballot_sync(kFull, bstart);
+                const unsigned le = lanemask_lt() | (1u << lane);
+                if (ok) {
+                    const double d = (double)v - mean;
+                    const double d2 = d * d;
+                    acc[0] += d2;
+                    acc[1] += d2 * d;
+                    acc[2] += d2 * d2;
+                    acc[3] += d2 * d2 * d;
+                    acc[4] += d2 * d2 * d2;
+                    if ((double)v < mean) {
+                        slo += v;
+                        ++clo;
+                    }
+                    const double x = (double)v;
+                    if (x >= p10 && x <= p90) {
+                        rsum += v;
+                        ++rn;
+                    }
+                    if (vend) {
+                        const uint32_t st = (vs & le) ? b0 + 31 - __clz(vs & le) : carry_v;
+                        const unsigned long long key =
+                            ((unsigned long long)(i - st + 1) << 16) | (0xffffu - v);
+                        best = key > best ? key : best;
+                    }
+                    if (bend) {
+                        const uint32_t st = (bs & le) ? b0 + 31 - __clz(bs & le) : carry_b;
+                        const uint32_t c = i - st + 1;
+                        acc[5] += (double)c * (logn - log2_int(c));
+                        usq += (unsigned long long)c * c;
+                        if (dbg_on && bin < nb32) dbg->hist[bin] = c;
+                    }
+                }
+                if (vs) carry_v = b0 + 31 - __clz(vs);
+                if (bs) carry_b = b0 + 31 - __clz(bs);
+                prev_v = __shfl_sync(kFull, v, 31);
+                prev_b = __shfl_sync(kFull, bin, 31);
+            }
+            warp_sum8(acc);
+            best = warp_max(best);
+            slo = warp_sum(slo);
+            clo = warp_sum(clo);
+            rsum = warp_sum(rsum);
+            rn = warp_sum(rn);
+            usq = warp_sum(usq);
+            const double m2 = acc[0] / dn, m3 = acc[1] / dn, m4 = acc[2] / dn, m5 = acc[3] / dn,
+                         m6 = acc[4] / dn;
+            // sum |x - mean| = (S_hi - S_lo) + (c_lo - c_hi) mean, exact integer parts
+            const double mad = ((double)(long long)(sS - 2 * slo) +
+                                (double)((long long)clo - (long long)(n - clo)) * mean) / dn;
+            const double entropy = acc[5] / dn;
+            const double uniformity = (double)usq / (dn * dn);
+            double rmad = 0;
+            if (rn > 0) {
+                const double rmean = (double)rsum / (double)rn;
+                unsigned long long rlo = 0;
+                uint32_t rcl = 0;
+    #pragma unroll 1
+                for (uint32_t i = lane; i < n; i += 32) {
+                    const double x = (double)s[i];
+                    if (x >= p10 && x <= p90 && x < rmean) {
+                        rlo += s[i];
+                        ++rcl;
+                    }
+                }
+                rlo = warp_sum(rlo);
+                rcl = warp_sum(rcl);
+                rmad = ((double)(long long)(rsum - 2 * rlo) +
+                        (double)((long long)rcl - (long long)(rn - rcl)) * rmean) / (double)rn;
+            }
+            PT(2);
+            if (!edge_stats()) return;
+            double wcx = 0, wcy = 0;
+            if (sS > 0) {
+                wcx = (double)((unsigned long long)gx0 * sS + sXI) / (double)sS;
+                wcy = (double)((unsigned long long)gy0 * sS + sYI) / (double)sS;
+            }
+            const double var = n > 1 ? m2 * dn / (dn - 1.0) : 0.0;
+            double skew = 0, kurt = 0, hsk = 0, hfl = 0;
+            if (m2 > 0) {
+                const double r2 = sqrt(m2);
+                skew = m3 / (m2 * r2);
+                kurt = m4 / (m2 * m2);
+                hsk = m5 / (m2 * m2 * r2);
+                hfl = m6 / (m2 * m2 * m2);
+            }
+            const double mode = (double)(0xffffu - (uint32_t)(best & 0xffffu));
+            const double energy = (double)sQ, sdev = sqrt(var);
+            const double iqr = p75 - p25;
+            // lane k writes column k (coalesced row segment); columns 32..38 by lanes 0..6
+            const double pct = __shfl_sync(kFull, myp, (lane - 14) & 31);
+            double o = 0;
+            switch (lane) {
+                case 0: o = mean; break;
+                case 1: o = median; break;
+                case 2: o = mode; break;
+                case 3: o = mn; break;
+                case 4: o = mxv; break;
+                case 5: o = range; break;
+                case 6: o = var; break;
+                case 7: o = m2; break;
+                case 8: o = sdev; break;
+                case 9: o = sqrt(m2); break;
+                case 10: o = mad; break;
+                case 11: o = median_ad; break;
+                case 12: o = rmad; break;
+                case 13: o = iqr; break;
+                case 14: case 15: case 16: case 17: case 18: case 19: o = pct; break;
+                case 20: o = skew; break;
+                case 21: o = kurt; break;
+                case 22: o = m2 > 0 ? kurt - 3.0 : 0.0; break;
+                case 23: o = hsk; break;
+                case 24: o = hfl; break;
+                case 25: o = energy; break;
+                case 26: o = sqrt(energy / dn); break;
+                case 27: o = entropy; break;
+                case 28: o = uniformity; break;
+                case 29: o = (p75 + p25) != 0 ? iqr / (p75 + p25) : 0.0; break;
+                case 30: o = mean != 0 ? sdev / mean : 0.0; break;
+                default: o = (double)sS; break;
+            }
+            double* oi = orow + cfg.col_int;
+            oi[lane] = o;
+            if (lane < 7) {
+                const double t[7] = {e_mean, e_min, e_max, e_std, e_int, wcx, wcy};
+                double v = t[0];
+    #pragma unroll
+                for (int k = 1; k < 7; ++k)
+                    if ((int)lane == k) v = t[k];
+                oi[32 + lane] = v;
+            }
+            __syncwarp();
         }
-        __syncwarp();
     }
 
     // ---------------------------------------------------------------- shape
@@ -1925,7 +1964,7 @@ __global__ void __launch_bounds__(128) k_moments_serial(RoiList rl, Control* ctl
     const uint4* px4 = reinterpret_cast<const uint4*>(cfg.mom_px + off);  // 16 B aligned
     const uint32_t nq = (n + 3u) >> 2;
     uint4 cur = px4[0], nxt = nq > 1 ? px4[1] : make_uint4(0, 0, 0, 0);
-    for (uint32_t q4 = 0; q4 < nq; ++q4) {
+    for (uint32_t q4 = 0; q4 < nq; ++q4) {  // one 16 B chunk in flight ahead
         const uint4 fut = q4 + 2 < nq ? px4[q4 + 2] : make_uint4(0, 0, 0, 0);
         const uint32_t base = q4 * 4u;
         pixel(cur.x);
@@ -1997,6 +2036,162 @@ __global__ void __launch_bounds__(128) k_moments_serial(RoiList rl, Control* ctl
                                   (n30 - 3.0 * n12) * b * (3.0 * a * a - b * b)};
         for (int k = 0; k < 7; ++k) o[45 + k] = zero_mass ? 0.0 : hu[k];
     }
+}
+
+// Intensity statistics of the staged S ROIs (intensity_features.cpp:42-215), one
+// thread per ROI over the warp-sorted values: order statistics by the literal
+// percentile expression, median absolute deviation as the k-th element of the
+// V-shaped deviations (two-pointer walk from the median split), one sequential
+// scan for the central moments, mad / rmad partial sums, mode and histogram runs.
+// Columns 32..38 (edge statistics, weighted centroid) come from the warp.
+__device__ uint32_t kth_dev_scan(const uint16_t* s, uint32_t n, uint32_t M2, uint32_t k) {
+    uint32_t lo = 0, hi = n;  // m = first index with 2 s[i] >= M2
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (2u * s[mid] >= M2) hi = mid;
+        else lo = mid + 1;
+    }
+    int i = (int)lo - 1;
+    uint32_t j = lo, cur = 0;
+    for (uint32_t step = 0; step <= k; ++step) {
+        const uint32_t dl = i >= 0 ? M2 - 2u * s[i] : 0xffffffffu;
+        const uint32_t dr = j < n ? 2u * s[j] - M2 : 0xffffffffu;
+        if (dl <= dr) {
+            cur = dl;
+            --i;
+        } else {
+            cur = dr;
+            ++j;
+        }
+    }
+    return cur;
+}
+
+__global__ void __launch_bounds__(128) k_intensity_serial(RoiList rl, Control* ctl, FeatCfg cfg,
+                                                          double* out) {
+    const uint32_t n0 = ctl->class_count[kClassS0], n1 = ctl->class_count[kClassS1];
+    const uint32_t nt = n0 + n1 + ctl->class_count[kClassS2];
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= nt) return;
+    const uint32_t r = t < n0 ? rl.cls_list[kClassS0][t]
+                     : t < n0 + n1 ? rl.cls_list[kClassS1][t - n0] : rl.cls_list[kClassS2][t - n0 - n1];
+    const unsigned long long off = cfg.int_off[r];
+    if (off == ~0ull) return;  // not staged: the warp path wrote the columns
+    const uint32_t n = (uint32_t)rl.n[r];
+    const uint16_t* s = cfg.int_vals + off;
+    const unsigned long long sS = cfg.int_sums[(size_t)r * 2], sQ = cfg.int_sums[(size_t)r * 2 + 1];
+    const double dn = (double)n, mean = (double)sS / dn;
+    const uint32_t vmin = s[0], vmax = s[n - 1];
+    const double mn = (double)vmin, mxv = (double)vmax;
+    const double median = (n & 1) ? (double)s[n / 2] : 0.5 * ((double)s[n / 2 - 1] + (double)s[n / 2]);
+    const double pv[6] = {1.0, 10.0, 25.0, 75.0, 90.0, 99.0};
+    double pct[6];
+    for (int k = 0; k < 6; ++k) pct[k] = percentile_exact(s, n, pv[k]);
+    const double p10 = pct[1], p25 = pct[2], p75 = pct[3], p90 = pct[4];
+    const uint32_t M2 = (n & 1) ? 2u * s[n / 2] : (uint32_t)s[n / 2 - 1] + s[n / 2];
+    const uint32_t d_hi = kth_dev_scan(s, n, M2, n / 2);
+    const uint32_t d_lo = (n & 1) ? d_hi : kth_dev_scan(s, n, M2, n / 2 - 1);
+    const double median_ad = (n & 1) ? 0.5 * (double)d_hi : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
+    // one scan: central moments, mad / rmad partials, value runs (mode), bin runs
+    const uint32_t nb32 = (uint32_t)cfg.bins, rng = vmax - vmin;
+    const bool wide = (unsigned long long)nb32 * 65535ull >= (1ull << 32);
+    const uint32_t magic = rng ? (uint32_t)(0xffffffffull / rng) : 0u;
+    auto bin_of = [&](uint32_t v) -> uint32_t {  // floor(nb (v - min) / range), exact
+        if (rng == 0) return 0u;
+        uint32_t b;
+        if (!wide) {
+            const uint32_t num = nb32 * (v - vmin);
+            b = __umulhi(num, magic);
+            if (num - b * rng >= rng) ++b;
+        } else {
+            b = (uint32_t)((unsigned long long)nb32 * (v - vmin) / rng);
+        }
+        return b < nb32 - 1 ? b : nb32 - 1;
+    };
+    const double logn = nlog2(dn);
+    double a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, ent = 0;
+    unsigned long long best = 0, slo = 0, rsum = 0, usq = 0;
+    uint32_t clo = 0, rn = 0, run_v = 0, run_b = 0, pv_ = s[0], pb_ = bin_of(s[0]);
+    for (uint32_t i = 0; i < n; ++i) {
+        const uint32_t v = s[i];
+        const double d = (double)v - mean, d2 = d * d;
+        a2 += d2;
+        a3 += d2 * d;
+        a4 += d2 * d2;
+        a5 += d2 * d2 * d;
+        a6 += d2 * d2 * d2;
+        if ((double)v < mean) {
+            slo += v;
+            ++clo;
+        }
+        const double x = (double)v;
+        if (x >= p10 && x <= p90) {
+            rsum += v;
+            ++rn;
+        }
+        if (v != pv_) {  // a value run ended
+            const unsigned long long key = ((unsigned long long)run_v << 16) | (0xffffu - pv_);
+            best = key > best ? key : best;
+            pv_ = v;
+            run_v = 0;
+        }
+        ++run_v;
+        const uint32_t b = bin_of(v);
+        if (b != pb_) {  // a bin run ended
+            ent += (double)run_b * (logn - log2_int(run_b));
+            usq += (unsigned long long)run_b * run_b;
+            pb_ = b;
+            run_b = 0;
+        }
+        ++run_b;
+    }
+    {
+        const unsigned long long key = ((unsigned long long)run_v << 16) | (0xffffu - pv_);
+        best = key > best ? key : best;
+        ent += (double)run_b * (logn - log2_int(run_b));
+        usq += (unsigned long long)run_b * run_b;
+    }
+    const double m2 = a2 / dn, m3 = a3 / dn, m4 = a4 / dn, m5 = a5 / dn, m6 = a6 / dn;
+    const double mad = ((double)(long long)(sS - 2 * slo) +
+                        (double)((long long)clo - (long long)(n - clo)) * mean) / dn;
+    double rmad = 0;
+    if (rn > 0) {
+        const double rmean = (double)rsum / (double)rn;
+        unsigned long long rlo = 0;
+        uint32_t rcl = 0;
+        for (uint32_t i = 0; i < n; ++i) {
+            const double x = (double)s[i];
+            if (x >= p10 && x <= p90 && x < rmean) {
+                rlo += s[i];
+                ++rcl;
+            }
+        }
+        rmad = ((double)(long long)(rsum - 2 * rlo) +
+                (double)((long long)rcl - (long long)(rn - rcl)) * rmean) / (double)rn;
+    }
+    const double var = n > 1 ? m2 * dn / (dn - 1.0) : 0.0;
+    double skew = 0, kurt = 0, hsk = 0, hfl = 0;
+    if (m2 > 0) {
+        const double r2 = sqrt(m2);
+        skew = m3 / (m2 * r2);
+        kurt = m4 / (m2 * m2);
+        hsk = m5 / (m2 * m2 * r2);
+        hfl = m6 / (m2 * m2 * m2);
+    }
+    const double energy = (double)sQ, sdev = sqrt(var), iqr = p75 - p25;
+    const double o32[32] = {mean, median, (double)(0xffffu - (uint32_t)(best & 0xffffu)), mn, mxv,
+                            mxv - mn, var, m2, sdev, sqrt(m2), mad, median_ad, rmad, iqr,
+                            pct[0], pct[1], pct[2], pct[3], pct[4], pct[5], skew, kurt,
+                            m2 > 0 ? kurt - 3.0 : 0.0, hsk, hfl, energy, sqrt(energy / dn), ent / dn,
+                            (double)usq / (dn * dn), (p75 + p25) != 0 ? iqr / (p75 + p25) : 0.0,
+                            mean != 0 ? sdev / mean : 0.0, (double)sS};
+    double* oi = out + (size_t)r * cfg.ncols + cfg.col_int;
+    for (int k = 0; k < 32; ++k) oi[k] = o32[k];
+}
+
+void launch_intensity_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
+                             double* out) {
+    if (n_s > 0) k_intensity_serial<<<(n_s + 127) / 128, 128, 0, s>>>(rl, ctl, cfg, out);
 }
 
 void launch_moments_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
