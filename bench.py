@@ -290,13 +290,12 @@ def main():
     # the S kernels read each ROI pixel's label + intensity (4 B), stage 6 B per pixel
     # (packed x,y,v for the moments pass, sorted value for the intensity pass) and
     # write 7 intensity columns; the serial passes read their staged bytes and write
-    # their columns (32 intensity, 104 moments)
+    # their columns (32 intensity + 104 moments, one launch: k_serial_stats)
     s_bytes = fg * 4 + fg * 6 + n_rois * 7 * 8
     algo_bytes = {
         "k_label_scan": h * w * 2,                      # label raster read once
         "k_roi_s0": s_bytes, "k_roi_s1": s_bytes, "k_roi_s2": s_bytes,
-        "k_intensity_serial": fg * 2 + n_rois * 32 * 8,
-        "k_moments_serial": fg * 4 + n_rois * 104 * 8,
+        "k_serial_stats": fg * 6 + n_rois * (32 + 104) * 8,
     }
     per_launch_s = dom_ms / 1e3 / max(1, dom_cnt)
     achieved = algo_bytes.get(dom_name, h * w * 4 + n_rois * ncols * 8) / per_launch_s / 1e9

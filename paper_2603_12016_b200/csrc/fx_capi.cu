@@ -36,10 +36,8 @@ cudaError_t roi_b_setup();
 void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
                          double* out);
 cudaError_t roi_t_setup();
-void launch_moments_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
-                           double* out);
-void launch_intensity_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
-                             double* out);
+void launch_serial_stats(int n_s, bool intensity, bool moments, cudaStream_t s, RoiList rl,
+                         Control* ctl, FeatCfg cfg, double* out);
 TLayout make_tlayout(unsigned long long CELLS, uint32_t NMAX);
 void launch_roi_t(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                   double* out, uint8_t* scratch, const TLayout& T, int which, bool init);
@@ -631,17 +629,12 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
             }
         }
     }
-    if (cfg.int_vals) {  // intensity statistics of the staged S ROIs
+    if (cfg.int_vals || cfg.mom_px) {  // intensity statistics + moments of the staged S ROIs
         const int n_s = (int)(hc.class_count[kClassS0] + hc.class_count[kClassS1] +
                               hc.class_count[kClassS2]);
-        Launch l(c, "k_intensity_serial");
-        launch_intensity_serial(n_s, s, rl, c->d_ctl, cfg, out_dev);
-    }
-    if (cfg.mom_px) {  // moments of the staged S ROIs
-        const int n_s = (int)(hc.class_count[kClassS0] + hc.class_count[kClassS1] +
-                              hc.class_count[kClassS2]);
-        Launch l(c, "k_moments_serial");
-        launch_moments_serial(n_s, s, rl, c->d_ctl, cfg, out_dev);
+        Launch l(c, "k_serial_stats");
+        launch_serial_stats(n_s, cfg.int_vals != nullptr, cfg.mom_px != nullptr, s, rl, c->d_ctl,
+                            cfg, out_dev);
     }
     if (cfg.col_shape >= 0) {  // serial shape columns of the S ROIs, before k_roi_b
         const int n_s = (int)(hc.class_count[kClassS0] + hc.class_count[kClassS1] +

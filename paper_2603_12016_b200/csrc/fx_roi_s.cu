@@ -1922,11 +1922,10 @@ cudaError_t roi_s_setup(int* occ) {
 // in row-major order), then the binomial shifts to the centroid and the origin,
 // eta and Hu; the same formulas as the warp path, scalar and amortised over 32
 // ROIs per warp.
-__global__ void __launch_bounds__(128) k_moments_serial(RoiList rl, Control* ctl, FeatCfg cfg,
-                                                        double* out) {
+__device__ void moments_serial(uint32_t t, const RoiList& rl, Control* ctl, const FeatCfg& cfg,
+                               double* out) {
     const uint32_t n0 = ctl->class_count[kClassS0], n1 = ctl->class_count[kClassS1];
     const uint32_t nt = n0 + n1 + ctl->class_count[kClassS2];
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nt) return;
     const uint32_t r = t < n0 ? rl.cls_list[kClassS0][t]
                      : t < n0 + n1 ? rl.cls_list[kClassS1][t - n0] : rl.cls_list[kClassS2][t - n0 - n1];
@@ -2067,11 +2066,10 @@ __device__ uint32_t kth_dev_scan(const uint16_t* s, uint32_t n, uint32_t M2, uin
     return cur;
 }
 
-__global__ void __launch_bounds__(128) k_intensity_serial(RoiList rl, Control* ctl, FeatCfg cfg,
-                                                          double* out) {
+__device__ void intensity_serial(uint32_t t, const RoiList& rl, Control* ctl, const FeatCfg& cfg,
+                                 double* out) {
     const uint32_t n0 = ctl->class_count[kClassS0], n1 = ctl->class_count[kClassS1];
     const uint32_t nt = n0 + n1 + ctl->class_count[kClassS2];
-    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     if (t >= nt) return;
     const uint32_t r = t < n0 ? rl.cls_list[kClassS0][t]
                      : t < n0 + n1 ? rl.cls_list[kClassS1][t - n0] : rl.cls_list[kClassS2][t - n0 - n1];
@@ -2189,14 +2187,20 @@ __global__ void __launch_bounds__(128) k_intensity_serial(RoiList rl, Control* c
     for (int k = 0; k < 32; ++k) oi[k] = o32[k];
 }
 
-void launch_intensity_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
-                             double* out) {
-    if (n_s > 0) k_intensity_serial<<<(n_s + 127) / 128, 128, 0, s>>>(rl, ctl, cfg, out);
+// the per-ROI serial passes of the S ROIs in one launch: blocks [0, bi) run the
+// intensity statistics, the rest the moments, so the two sparse waves overlap
+__global__ void __launch_bounds__(128) k_serial_stats(RoiList rl, Control* ctl, FeatCfg cfg,
+                                                      double* out, uint32_t bi) {
+    if (blockIdx.x < bi) intensity_serial(blockIdx.x * blockDim.x + threadIdx.x, rl, ctl, cfg, out);
+    else moments_serial((blockIdx.x - bi) * blockDim.x + threadIdx.x, rl, ctl, cfg, out);
 }
 
-void launch_moments_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
-                           double* out) {
-    if (n_s > 0) k_moments_serial<<<(n_s + 127) / 128, 128, 0, s>>>(rl, ctl, cfg, out);
+void launch_serial_stats(int n_s, bool intensity, bool moments, cudaStream_t s, RoiList rl,
+                         Control* ctl, FeatCfg cfg, double* out) {
+    if (n_s <= 0 || (!intensity && !moments)) return;
+    const uint32_t nb = (uint32_t)((n_s + 127) / 128);
+    const uint32_t bi = intensity ? nb : 0u, bm = moments ? nb : 0u;
+    k_serial_stats<<<bi + bm, 128, 0, s>>>(rl, ctl, cfg, out, bi);
 }
 
 void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
