@@ -285,6 +285,23 @@ __device__ __noinline__ bool edge_sets_slow(const uint64_t* rowmask, int h, int 
 
 
 // scatter pass of a stable LSD radix sort; cnt[] holds exclusive digit offsets
+// lanes holding the same 8-bit digit as this lane, among `valid` lanes: bit-sliced
+// ballots (8 votes) instead of __match_any_sync
+__device__ __forceinline__ unsigned digit_peers(uint32_t d, unsigned valid) {
+#ifdef FXG_SORT_MATCH
+    return __match_any_sync(kFull, d) & valid;
+#else
+    unsigned m = valid;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const bool bit = (d >> b) & 1u;
+        const unsigned bb = __ballot_sync(kFull, bit);
+        m &= bit ? bb : ~bb;
+    }
+    return m;
+#endif
+}
+
 __device__ __forceinline__ void radix_scatter(const uint16_t* src, uint16_t* dst, uint32_t n,
                                               int shift, uint32_t* cnt) {
     const unsigned lane = lane_id();
@@ -292,8 +309,8 @@ __device__ __forceinline__ void radix_scatter(const uint16_t* src, uint16_t* dst
         const uint32_t i = b0 + lane;
         const bool ok = i < n;
         const uint16_t key = ok ? src[i] : 0;
-        const uint32_t d = ok ? ((uint32_t)key >> shift) & 0xffu : 256u + lane;
-        const unsigned peers = __match_any_sync(kFull, d);
+        const uint32_t d = ((uint32_t)key >> shift) & 0xffu;
+        const unsigned peers = digit_peers(d, __ballot_sync(kFull, ok));
         if (ok) dst[cnt[d] + __popc(peers & lanemask_lt())] = key;
         __syncwarp();
         if (ok && lane == (unsigned)(31 - __clz(peers))) cnt[d] += __popc(peers);
@@ -313,8 +330,9 @@ __device__ __forceinline__ const uint16_t* radix_sort16(const uint16_t* src, uin
         const uint32_t i = b0 + lane;
         const bool ok = i < n;
         const uint32_t key = ok ? src[i] : 0u;
-        const uint32_t d0 = ok ? key & 0xffu : 256u + lane, d1 = ok ? key >> 8 : 256u + lane;
-        const unsigned p0 = __match_any_sync(kFull, d0), p1 = __match_any_sync(kFull, d1);
+        const uint32_t d0 = key & 0xffu, d1 = key >> 8;
+        const unsigned valid = __ballot_sync(kFull, ok);
+        const unsigned p0 = digit_peers(d0, valid), p1 = digit_peers(d1, valid);
         if (ok && lane == (unsigned)(__ffs(p0) - 1)) cnt[d0] += __popc(p0);
         if (ok && lane == (unsigned)(__ffs(p1) - 1)) cnt[256 + d1] += __popc(p1);
         __syncwarp();
