@@ -2068,20 +2068,22 @@ __device__ uint32_t kth_dev_scan(const uint16_t* s, uint32_t n, uint32_t M2, uin
         if (2u * s[mid] >= M2) hi = mid;
         else lo = mid + 1;
     }
-    int i = (int)lo - 1;
-    uint32_t j = lo, cur = 0;
-    for (uint32_t step = 0; step <= k; ++step) {
-        const uint32_t dl = i >= 0 ? M2 - 2u * s[i] : 0xffffffffu;
-        const uint32_t dr = j < n ? 2u * s[j] - M2 : 0xffffffffu;
-        if (dl <= dr) {
-            cur = dl;
-            --i;
-        } else {
-            cur = dr;
-            ++j;
-        }
+    // A[j] = M2 - 2 s[m-1-j] (j < m) and B[j] = 2 s[m+j] - M2 are ascending; the
+    // k-th (0-based) of their union by a binary search on the count taken from A
+    const uint32_t m = lo, na = m, nb = n - m, kk = k + 1;
+    auto A = [&](uint32_t j) { return M2 - 2u * s[m - 1 - j]; };
+    auto B = [&](uint32_t j) { return 2u * s[m + j] - M2; };
+    uint32_t a = kk > nb ? kk - nb : 0u, b = kk < na ? kk : na;  // t in [a, b]
+    while (a < b) {  // smallest t with A[t] >= B[kk-1-t] (t < na, kk-1-t >= 0)
+        const uint32_t t = (a + b) >> 1;
+        if (A(t) < B(kk - 1 - t)) a = t + 1;
+        else b = t;
     }
-    return cur;
+    const uint32_t t = a;
+    uint32_t best = 0;
+    if (t > 0) best = A(t - 1);
+    if (kk - t > 0) best = max(best, B(kk - t - 1));
+    return best;
 }
 
 __device__ void intensity_serial(uint32_t t, const RoiList& rl, Control* ctl, const FeatCfg& cfg,
@@ -2128,38 +2130,45 @@ __device__ void intensity_serial(uint32_t t, const RoiList& rl, Control* ctl, co
     double a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, ent = 0;
     unsigned long long best = 0, slo = 0, rsum = 0, usq = 0;
     uint32_t clo = 0, rn = 0, run_v = 0, run_b = 0, pv_ = s[0], pb_ = bin_of(s[0]);
-    for (uint32_t i = 0; i < n; ++i) {
-        const uint32_t v = s[i];
-        const double d = (double)v - mean, d2 = d * d;
-        a2 += d2;
-        a3 += d2 * d;
-        a4 += d2 * d2;
-        a5 += d2 * d2 * d;
-        a6 += d2 * d2 * d2;
-        if ((double)v < mean) {
-            slo += v;
-            ++clo;
+    const uint4* s4 = reinterpret_cast<const uint4*>(s);  // 16 B aligned (staging rounds to 8)
+    for (uint32_t q = 0; q * 8u < n; ++q) {
+        const uint4 w4 = s4[q];
+        const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            if (q * 8u + (uint32_t)u >= n) break;
+            const uint32_t v = (wv[u >> 1] >> ((u & 1) * 16)) & 0xffffu;
+            const double d = (double)v - mean, d2 = d * d;
+            a2 += d2;
+            a3 += d2 * d;
+            a4 += d2 * d2;
+            a5 += d2 * d2 * d;
+            a6 += d2 * d2 * d2;
+            if ((double)v < mean) {
+                slo += v;
+                ++clo;
+            }
+            const double x = (double)v;
+            if (x >= p10 && x <= p90) {
+                rsum += v;
+                ++rn;
+            }
+            if (v != pv_) {  // a value run ended
+                const unsigned long long key = ((unsigned long long)run_v << 16) | (0xffffu - pv_);
+                best = key > best ? key : best;
+                pv_ = v;
+                run_v = 0;
+            }
+            ++run_v;
+            const uint32_t b = bin_of(v);
+            if (b != pb_) {  // a bin run ended
+                ent += (double)run_b * (logn - log2_int(run_b));
+                usq += (unsigned long long)run_b * run_b;
+                pb_ = b;
+                run_b = 0;
+            }
+            ++run_b;
         }
-        const double x = (double)v;
-        if (x >= p10 && x <= p90) {
-            rsum += v;
-            ++rn;
-        }
-        if (v != pv_) {  // a value run ended
-            const unsigned long long key = ((unsigned long long)run_v << 16) | (0xffffu - pv_);
-            best = key > best ? key : best;
-            pv_ = v;
-            run_v = 0;
-        }
-        ++run_v;
-        const uint32_t b = bin_of(v);
-        if (b != pb_) {  // a bin run ended
-            ent += (double)run_b * (logn - log2_int(run_b));
-            usq += (unsigned long long)run_b * run_b;
-            pb_ = b;
-            run_b = 0;
-        }
-        ++run_b;
     }
     {
         const unsigned long long key = ((unsigned long long)run_v << 16) | (0xffffu - pv_);

@@ -14,7 +14,7 @@ which = sys.argv[1] if len(sys.argv) > 1 else "c2"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 if which == "c2":
     L, _ = fx.packed_blob_mask_grid(8192, 400, 50000, 1)
-    groups = ["intensity", "moments"]
+    groups = os.environ.get("FX_GROUPS", "intensity,moments").split(",")
     prof = "default"
 elif which.startswith("c5"):  # C5 regime at reduced size: 16384^2, ~2e5-px blobs
     size = int(os.environ.get("C5_SIZE", "16384"))
