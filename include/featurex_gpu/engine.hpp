@@ -10,8 +10,9 @@
 // Differences (documented in INTEGRATION.md):
 //  - ExtractionConfig::threads / parallel / memory_budget / spill_dir are
 //    validated like the reference but do not change the (device) execution.
-//  - groups glrlm / glszm / ngtdm have no device kernel yet and raise
-//    ConfigError from compute_roi_features / run (never a silent CPU fallback).
+//  - all seven groups (intensity, moments, shape, glcm, glrlm, glszm, ngtdm)
+//    run on the device; texture groups with ng > 256 raise ConfigError (the
+//    device kernels bound grey levels at 256; never a silent CPU fallback).
 #pragma once
 
 #include <cstdint>

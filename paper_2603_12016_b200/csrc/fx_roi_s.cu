@@ -362,6 +362,73 @@ __device__ __forceinline__ const uint16_t* radix_sort16(const uint16_t* src, uin
     return dst;
 }
 
+// Sort of plain u16 keys by one warp (no payload, so equal keys need no stable
+// order): bucket b = (v - vmin) >> s with s the least shift giving <= 512 buckets,
+// shared-atomic histogram and scatter, then each key ranks itself inside its
+// bucket.  With range < 512 the buckets hold equal keys and the scatter is the
+// sort.  Crowded buckets (sum of squared counts > 16 n) fall back to the radix
+// sort.  Returns the sorted buffer and vmin / vmax.  cnt: 512 u32.
+__device__ __forceinline__ const uint16_t* bucket_sort16(const uint16_t* src, uint16_t* tmp,
+                                                      uint16_t* dst, uint32_t n, uint32_t* cnt,
+                                                      uint32_t& vmin, uint32_t& vmax) {
+    const unsigned lane = lane_id();
+    uint32_t lo = 0xffffu, hi = 0;
+    for (uint32_t i = lane; i < n; i += 32) {
+        const uint32_t v = src[i];
+        lo = min(lo, v);
+        hi = max(hi, v);
+    }
+    vmin = lo = warp_min(lo);
+    vmax = hi = warp_max(hi);
+    const uint32_t r = hi - lo;
+    if (n == 0 || r == 0) return src;  // all keys equal: already sorted
+    const int s = max(0, 23 - __clz(r));  // (r >> s) < 512
+    // bucket b lives at cnt[(b & 15) * 32 + (b >> 4)]: lane l owns buckets 16 l ..
+    // 16 l + 15 as one bank column
+    auto slot = [](uint32_t b) { return ((b & 15u) << 5) | (b >> 4); };
+#pragma unroll
+    for (int k = 0; k < 16; ++k) cnt[k * 32 + lane] = 0;
+    __syncwarp();
+    for (uint32_t i = lane; i < n; i += 32) atomicAdd(&cnt[slot((src[i] - lo) >> s)], 1u);
+    __syncwarp();
+    uint32_t c[16], t = 0, sq = 0;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        c[k] = cnt[k * 32 + lane];
+        t += c[k];
+        sq += c[k] * c[k];
+    }
+    sq = warp_sum(sq);
+    if (s > 0 && sq > 16u * n) return radix_sort16(src, tmp, dst, n, cnt);
+    uint32_t run = warp_incl_scan(t) - t;
+    __syncwarp();
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        cnt[k * 32 + lane] = run;
+        run += c[k];
+    }
+    __syncwarp();
+    for (uint32_t i = lane; i < n; i += 32) {
+        const uint32_t v = src[i];
+        tmp[atomicAdd(&cnt[slot((v - lo) >> s)], 1u)] = (uint16_t)v;
+    }
+    __syncwarp();
+    if (s == 0) return tmp;  // buckets are single values
+    // cnt[b] is now the end of bucket b (= the start of bucket b + 1)
+    for (uint32_t i = lane; i < n; i += 32) {
+        const uint32_t v = tmp[i], b = (v - lo) >> s;
+        const uint32_t st = b ? cnt[slot(b - 1)] : 0u, en = cnt[slot(b)];
+        uint32_t rank = 0;
+        for (uint32_t j = st; j < en; ++j) {
+            const uint32_t u = tmp[j];
+            rank += (u < v) | ((u == v) & (j < i));
+        }
+        dst[st + rank] = (uint16_t)v;
+    }
+    __syncwarp();
+    return dst;
+}
+
 
 
 // k-th smallest (0-based) of |2 s[i] - M2| over sorted s by the whole warp:
@@ -1339,9 +1406,16 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     // ----------------------------------------------------------- intensity
     PT(0);
     if (cfg.col_int >= 0) {
+#ifdef FXG_SORT_RADIX
         const uint16_t* s = radix_sort16(vals, (uint16_t*)(base + L.tmp),
                                          (uint16_t*)(base + L.sorted), n,
                                          (uint32_t*)(base + L.cnt));
+#else
+        uint32_t smin, smax;
+        const uint16_t* s = bucket_sort16(vals, (uint16_t*)(base + L.tmp),
+                                          (uint16_t*)(base + L.sorted), n,
+                                          (uint32_t*)(base + L.cnt), smin, smax);
+#endif
         __syncwarp();
         PT(1);
         // order statistics and moments of the values by k_intensity_serial when the

@@ -16,6 +16,10 @@
     - eta_pq: s_mu / m00^(1+(p+q)/2);  Hu: s2, s2^2, s3^2, s3^2, s3^4, s2*s3^2, s3^4
       with s2 = e20+e02+2e11, s3 = e30+3e12+3e21+e03 over e = |eta| + s_eta
     - skewness / hyperskewness, and Haralick clushade / corr / infomeas1: s = 1
+    - Haralick infomeas2 = sqrt(1 - exp(-2 (HXY2 - HXY))): a rounding error d of
+      order c u (HXY + 1) in the entropy difference moves it by d / imc2 (by
+      sqrt(d) near 0), so s = d / (tol max(imc2, sqrt(d))), c = 4096; this only
+      matters where HXY2 ~ HXY (e.g. two-level ROIs, imc2 near 0)
     - everything else: s = 1e-300 (pure relative)
 """
 from __future__ import annotations
@@ -79,6 +83,13 @@ def floors(columns, ref_table, intensity=None, labels=None, roi_labels=None):
             s[:, i] = 1.0
         if c.startswith("glcm_") and any(c.startswith("glcm_" + h + "_") for h in HARALICK_UNIT):
             s[:, i] = 1.0
+    for c, i in col.items():
+        if c.startswith("glcm_infomeas2_"):
+            h = col.get("glcm_entropy_" + c[len("glcm_infomeas2_"):])
+            if h is None:
+                continue
+            d = 4096 * 2.2e-16 * (np.abs(ref_table[:, h]) + 1.0)
+            s[:, i] = d / (1e-6 * np.maximum(np.abs(ref_table[:, i]), np.sqrt(d)))
     # GLRLM/GLSZM variances sum p (x - mu)^2: the reference's rounding noise scales
     # with E[x^2] (its own lre / hglre / lae / hglze columns), not with the variance.
     # Scale columns are found by position (feature-major blocks, names may repeat

@@ -62,6 +62,27 @@ def test_adversarial_masks(ctx, oracle, name):
         check(ctx, oracle, I, L, GROUPS, "performance")
 
 
+def _value_distributions(shape):
+    """Intensity laws that drive each branch of the warp value sort: narrow range
+    (buckets are single values), 12-bit (in-bucket ranking), two modes and a narrow
+    body with rare extremes (crowded buckets, radix fallback)."""
+    rng = np.random.default_rng(11)
+    narrow = rng.integers(1000, 1300, shape).astype(np.uint16)
+    twelve = rng.integers(0, 4096, shape).astype(np.uint16)
+    bimodal = np.where(rng.random(shape) < 0.5, 0, 65535).astype(np.uint16)
+    outliers = rng.integers(500, 520, shape).astype(np.uint16)
+    outliers[rng.random(shape) < 0.01] = 65535
+    return {"narrow": narrow, "twelve_bit": twelve, "bimodal": bimodal, "outliers": outliers}
+
+
+@pytest.mark.parametrize("law", ["narrow", "twelve_bit", "bimodal", "outliers"])
+def test_value_sort_branches(ctx, oracle, law):
+    L, _ = fx.packed_blob_mask_grid(1024, 700, 300, 5)
+    I = _value_distributions(L.shape)[law]
+    check(ctx, oracle, I, L, ["intensity", "moments"])
+    check(ctx, oracle, I, L, GROUPS)
+
+
 @pytest.mark.parametrize("seed", range(6))
 def test_random_blobs(ctx, oracle, seed):
     L = inputs.random_blobs((96, 130), 40, seed=seed)

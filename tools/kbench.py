@@ -27,6 +27,11 @@ else:  # c3: 4096^2, 10k ROIs, GLCM 4 angles ng=256
     groups = ["glcm"]
     prof = "ibsi-like"
 I = fx.uniform_u16(L.shape, 0)
+law = os.environ.get("FX_LAW", "uniform")  # intensity law: uniform u16 | twelve (0..4095) | narrow
+if law == "twelve":
+    I = I & np.uint16(4095)
+elif law == "narrow":
+    I = (I % np.uint16(300) + np.uint16(1000)).astype(np.uint16)
 p = fx.resolve_profile(prof)
 mask = fx.resolve_groups(groups)
 ncols = len(fx.feature_columns(mask, p))
