@@ -122,6 +122,13 @@ int fx_ctx_kernel_times(fx_ctx* ctx, char* names, size_t names_cap, double* ms,
                         uint64_t* counts, int cap, int* n);
 int fx_ctx_reset_kernel_times(fx_ctx* ctx);
 
+/* Page-locked host memory for the input pipeline (decode straight into the
+ * buffers the H2D copies read, so the copy engine runs at full rate and
+ * overlaps the kernels).  No reference counterpart: the reference has no
+ * device.  FX_E_OOM when the allocation fails. */
+int fx_host_alloc(size_t bytes, void** out);
+int fx_host_free(void* p);
+
 /* ---- the hot path ---------------------------------------------------------- */
 
 /* Replaces the per-pair body of featurex::run (engine.cpp:300-336):
@@ -159,6 +166,22 @@ int fx_featurize_u16(fx_ctx* ctx, const uint16_t* intensity, const uint16_t* lab
 int fx_roi_features(fx_ctx* ctx, const uint32_t* xs, const uint32_t* ys,
                     const uint16_t* intensities, size_t n, unsigned groups,
                     const fx_texture_params* params, double* out, size_t cap);
+
+/* featurex::run (engine.hpp:77, engine.cpp:283-350) on PGM directories: pairs
+ * by basename under `pattern`, featurizes every pair on `device` through the
+ * batched pipeline of the C++ engine (include/featurex_gpu/engine.hpp) and
+ * writes the sorted "%.10g" CSV.  groups_csv: comma-separated group names.
+ * Per-pair failures are counted in failed_pairs, not returned. */
+typedef struct fx_run_summary {
+    int images;
+    uint64_t rois;
+    uint64_t rows;
+    double elapsed_seconds;
+    int failed_pairs;
+} fx_run_summary;
+int fx_run(const char* intensity_dir, const char* mask_dir, const char* pattern,
+           const char* groups_csv, const char* profile, int threads, int parallel, int device,
+           const char* output_path, fx_run_summary* out);
 
 /* ---- band sharding (C5: a whole slide split into row bands across GPUs) -----
  * 1. every rank: fx_scan_accumulate(own band, reset=1)  -> partial label table in

@@ -6,4 +6,4 @@ binds it for Python callers; see fxg.py.
 """
 from .fxg import (Context, FxError, TextureParams, blob_mask_grid, feature_columns,  # noqa: F401
                   make_params, packed_blob_mask_grid, resolve_groups, resolve_profile,
-                  siemens_star, uniform_u16, LIB_PATH)
+                  run, siemens_star, uniform_u16, write_pgm, LIB_PATH)

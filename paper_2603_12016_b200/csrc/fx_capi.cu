@@ -911,6 +911,26 @@ int fx_ctx_destroy(fx_ctx* c) {
     return FX_OK;
 }
 
+int fx_host_alloc(size_t bytes, void** out) {
+    if (!out) return set_error(FX_E_ARG, "null argument");
+    *out = nullptr;
+    if (bytes == 0) return FX_OK;
+    if (cudaMallocHost(out, bytes) != cudaSuccess) {
+        cudaGetLastError();
+        *out = nullptr;
+        return set_error(FX_E_OOM, "pinned host allocation failed");
+    }
+    return FX_OK;
+}
+
+int fx_host_free(void* p) {
+    if (p && cudaFreeHost(p) != cudaSuccess) {
+        cudaGetLastError();
+        return set_error(FX_E_CUDA, "cudaFreeHost failed");
+    }
+    return FX_OK;
+}
+
 int fx_ctx_set_stream(fx_ctx* c, void* stream) {
     if (!c) return set_error(FX_E_ARG, "null ctx");
     c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;

@@ -115,6 +115,33 @@ def feature_columns(groups, params: TextureParams):
     return s.split("\n") if s else []
 
 
+class RunSummary(C.Structure):
+    _fields_ = [("images", C.c_int), ("rois", C.c_uint64), ("rows", C.c_uint64),
+                ("elapsed_seconds", C.c_double), ("failed_pairs", C.c_int)]
+
+
+def run(intensity_dir, mask_dir, groups, profile="default", threads=1, parallel=True,
+        output_path="out.csv", pattern="*.pgm", device=0) -> RunSummary:
+    """featurex::run (engine.hpp:77) on PGM directories through the engine's
+    batched device pipeline (fx_run); writes the sorted %.10g CSV."""
+    s = RunSummary()
+    _check(lib().fx_run(str(intensity_dir).encode(), str(mask_dir).encode(), pattern.encode(),
+                        ",".join(groups).encode(), profile.encode(), int(threads),
+                        int(bool(parallel)), int(device), str(output_path).encode(), C.byref(s)))
+    return s
+
+
+def write_pgm(path, samples: np.ndarray, maxval: int | None = None):
+    """Binary PGM P5 (pgm.cpp:101-124): big-endian 16-bit samples when maxval > 255."""
+    a = np.asarray(samples)
+    mv = int(a.max()) if maxval is None else int(maxval)
+    mv = max(mv, 1)
+    body = a.astype(">u2").tobytes() if mv > 255 else a.astype(np.uint8).tobytes()
+    with open(path, "wb") as f:
+        f.write(b"P5\n%d %d\n%d\n" % (a.shape[1], a.shape[0], mv))
+        f.write(body)
+
+
 class Context:
     """One fx_ctx (device scratch + stream).  Not thread-safe."""
 

@@ -83,6 +83,47 @@ static void host_cases() {
     std::ofstream(pg) << "P5\n2 2\n255\nX";
     CHECK_THROWS_AS(load_intensity(pg), FormatError);
     CHECK_THROWS_AS(load_mask("/nonexistent/x.pgm"), IoError);
+    // 8-bit payloads widen; comments in the header; samples above maxval rejected
+    std::ofstream(pg, std::ios::binary) << "P5\n# c\n3 1\n# d\n200\n" << std::string("\x01\xc8\x00", 3);
+    const IntensityImage i8 = load_intensity(pg);
+    CHECK(i8.bit_depth == 8 && i8.pixels == (std::vector<uint16_t>{1, 200, 0}));
+    std::ofstream(pg, std::ios::binary) << "P5\n2 1\n100\n" << std::string("\x01\xc8", 2);
+    CHECK_THROWS_AS(load_intensity(pg), FormatError);
+    std::ofstream(pg, std::ios::binary) << "P5\n1 1\n1000\n" << std::string("\x03\xe9", 2);
+    CHECK_THROWS_AS(load_mask(pg), FormatError);
+    // CSV number format: write_csv's "%.10g" (engine.cpp:52-67) on random and edge values
+    {
+        std::mt19937_64 g(7);
+        std::vector<double> vs = {0.0, -0.0, 1.0 / 3.0, 1234567890.5, 1234567891.5, 5e-324, 1e-5,
+                                  123456.78905, 1.7976931348623157e308, INFINITY, -INFINITY, NAN};
+        for (int i = 0; i < 200000; ++i) {
+            uint64_t b = g();
+            double v;
+            std::memcpy(&v, &b, 8);
+            vs.push_back(v);
+            vs.push_back(std::ldexp(static_cast<double>(g() >> 11), static_cast<int>(g() % 160) - 120));
+            // every decade of the fast path, 10-digit decimals and their +-1 ulp
+            // neighbours (rounding boundaries), halfway cases, small integers
+            const int dec = static_cast<int>(g() % 56) - 16;
+            const double d10 = static_cast<double>(1000000000ull + g() % 9000000000ull) * std::pow(10.0, dec - 9);
+            vs.push_back(d10);
+            vs.push_back(std::nextafter(d10, 0.0));
+            vs.push_back(std::nextafter(d10, 1e300));
+            vs.push_back(static_cast<double>(1000000000ull + g() % 9000000000ull) + 0.5);
+            vs.push_back(static_cast<double>(static_cast<int64_t>(g() % 2000001) - 1000000));
+            vs.push_back(-static_cast<double>(g() % 100000) / static_cast<double>(1 + g() % 977));
+        }
+        std::vector<FeatureRow> rows;
+        std::string want = "image,mask,label,x\n";
+        char buf[64];
+        for (size_t i = 0; i < vs.size(); ++i) {
+            rows.push_back({"a", "a", static_cast<uint32_t>(i), {vs[i]}});
+            std::snprintf(buf, sizeof buf, "%.10g", vs[i]);
+            want += "a,a," + std::to_string(i) + "," + buf + "\n";
+        }
+        write_csv({"x"}, rows, path);
+        CHECK(slurp(path) == want);
+    }
 }
 
 static void device_cases() {
@@ -182,6 +223,47 @@ static void device_cases() {
         bool same = v.size() == t.columns.size();
         for (size_t i = 0; same && i < v.size(); ++i) same = v[i] == t.values[t.columns.size() + i];
         CHECK(same);
+    }
+    {  // the batched pipeline: 300 pairs over several batches (mixed sizes, 8- and
+       // 16-bit, one corrupt file) == per-pair featurize + write_csv, byte for byte
+        const auto d = fresh_dir("fxg_engine_many");
+        std::mt19937 g(3);
+        std::vector<std::string> names;
+        for (int i = 0; i < 300; ++i) {
+            char nm[32];
+            std::snprintf(nm, sizeof nm, "t%03d.pgm", i);
+            const int w = 8 + static_cast<int>(g() % 40), h = 8 + static_cast<int>(g() % 30);
+            std::vector<uint16_t> iv(static_cast<size_t>(w) * h), lv(iv.size());
+            for (auto& v : iv) v = static_cast<uint16_t>(g() % 65536);
+            for (int y = 0; y < h; ++y)
+                for (int x = 0; x < w; ++x)
+                    lv[static_cast<size_t>(y) * w + x] = static_cast<uint16_t>(((x / 5) + 3 * (y / 4)) % 7);
+            write_pgm(d / "int" / nm, w, h, 65535, iv);
+            write_pgm(d / "seg" / nm, w, h, i % 3 ? 65535 : 255, lv);
+            names.push_back(nm);
+        }
+        std::ofstream(d / "int" / "t150.pgm", std::ios::trunc) << "P5\n4 4\n255\nX";
+        ExtractionConfig c;
+        c.intensity_dir = d / "int";
+        c.mask_dir = d / "seg";
+        c.output_path = d / "f.csv";
+        c.features = {"*ALL*"};
+        const RunSummary s = run(c);
+        CHECK(s.images == 299 && s.failed_pairs == 1);
+        const TextureParams tp = resolve_profile("default");
+        std::vector<FeatureRow> rows;
+        for (const std::string& nm : names) {
+            if (nm == "t150.pgm") continue;
+            const FeatureTable t = featurize(load_intensity(d / "int" / nm), load_mask(d / "seg" / nm),
+                                             c.features, tp);
+            for (size_t i = 0; i < t.labels.size(); ++i)
+                rows.push_back({nm, nm, t.labels[i],
+                                std::vector<double>(t.values.begin() + i * t.columns.size(),
+                                                    t.values.begin() + (i + 1) * t.columns.size())});
+        }
+        CHECK(s.rows == rows.size() && s.rows > 299 * 5);
+        write_csv(feature_columns(c.features, tp), rows, d / "g.csv");
+        CHECK(slurp(d / "f.csv") == slurp(d / "g.csv"));
     }
     {  // pairing errors
         IntensityImage im;
