@@ -116,6 +116,10 @@ int fx_ctx_set_stream(fx_ctx* ctx, void* cuda_stream);
 uint64_t fx_ctx_launch_count(const fx_ctx* ctx);
 /* Optional per-kernel CUDA-event timing on the launching stream. */
 int fx_ctx_enable_timing(fx_ctx* ctx, int enable);
+/* Restrict timing to the kernel of this name (NULL or "" = every kernel): each
+ * timing event between launches costs device time, so a timed region that must
+ * not be perturbed times only the kernel it reports. */
+int fx_ctx_timing_filter(fx_ctx* ctx, const char* kernel);
 /* names: '\n'-joined kernel names; ms[i]: accumulated device ms; count[i]:
  * launches.  Returns the number of kernels in *n. */
 int fx_ctx_kernel_times(fx_ctx* ctx, char* names, size_t names_cap, double* ms,

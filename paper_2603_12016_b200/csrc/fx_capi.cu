@@ -127,6 +127,7 @@ struct fx_ctx {
     // accounting
     uint64_t launches = 0;
     bool timing = false;
+    std::string timing_only;  // non-empty: time only the kernel of this name
     std::map<std::string, KTime> ktimes;
     std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
     std::vector<cudaEvent_t> ev_pool;
@@ -244,16 +245,20 @@ struct Launch {
     fx_ctx* c;
     const char* name;
     cudaEvent_t a = nullptr, b = nullptr;
+    bool timed = false;
     Launch(fx_ctx* c_, const char* n) : c(c_), name(n) {
         c->launches++;
-        if (c->timing) {
+        // each timing event between launches costs ~3 us of device time (it breaks
+        // launch pipelining), so a filter can restrict timing to one kernel
+        timed = c->timing && (c->timing_only.empty() || c->timing_only == n);
+        if (timed) {
             a = get_event(c);
             b = get_event(c);
             cudaEventRecord(a, c->stream);
         }
     }
     ~Launch() {
-        if (c->timing) {
+        if (timed) {
             cudaEventRecord(b, c->stream);
             c->pending.push_back({name, {a, b}});
         }
@@ -682,7 +687,9 @@ int run_pipeline(fx_ctx* c, const DevImage& img, unsigned groups, const fx_textu
 
 int finish(fx_ctx* c) {
     CK(cudaStreamSynchronize(c->stream));
-    if (c->timing) collect_times(c);
+    // per-kernel event pairs are resolved when the times are queried, so timed
+    // steps carry no event synchronisation on the host (bounded backlog)
+    if (c->timing && c->pending.size() > 8192) collect_times(c);
     if (c->h_ctl->error & kErrCapacity)
         return set_error(FX_E_CAPACITY, "a large ROI exceeded the L-path slab");
     if (c->h_ctl->error & kErrRuns)
@@ -864,6 +871,9 @@ int fx_ctx_destroy(fx_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->copy) cudaStreamSynchronize(c->copy);
+    collect_times(c);
+    for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
+    c->ev_pool.clear();
     cudaFree(c->d_cnt);
     cudaFree(c->d_bb);
     cudaFree(c->d_maxlab);
@@ -942,6 +952,12 @@ uint64_t fx_ctx_launch_count(const fx_ctx* c) { return c ? c->launches : 0; }
 int fx_ctx_enable_timing(fx_ctx* c, int enable) {
     if (!c) return set_error(FX_E_ARG, "null ctx");
     c->timing = enable != 0;
+    return FX_OK;
+}
+
+int fx_ctx_timing_filter(fx_ctx* c, const char* kernel) {
+    if (!c) return set_error(FX_E_ARG, "null ctx");
+    c->timing_only = kernel ? kernel : "";
     return FX_OK;
 }
 

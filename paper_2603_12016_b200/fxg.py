@@ -63,6 +63,7 @@ def lib() -> C.CDLL:
         for fn in ("fx_ctx_destroy", "fx_ctx_enable_timing", "fx_ctx_reset_kernel_times"):
             getattr(L, fn).argtypes = [C.c_void_p] + ([C.c_int] if fn == "fx_ctx_enable_timing" else [])
         L.fx_ctx_set_stream.argtypes = [C.c_void_p, C.c_void_p]
+        L.fx_ctx_timing_filter.argtypes = [C.c_void_p, C.c_char_p]
         _lib = L
     return _lib
 
@@ -169,6 +170,9 @@ class Context:
 
     def enable_timing(self, on=True):
         _check(lib().fx_ctx_enable_timing(self.h, int(bool(on))))
+
+    def timing_filter(self, kernel: str | None):
+        _check(lib().fx_ctx_timing_filter(self.h, kernel.encode() if kernel else None))
 
     def reset_kernel_times(self):
         _check(lib().fx_ctx_reset_kernel_times(self.h))
