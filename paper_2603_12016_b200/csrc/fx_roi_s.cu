@@ -2009,13 +2009,14 @@ cudaError_t roi_s_setup(int* occ) {
     return e;
 }
 
-// Moments of the staged S ROIs (moments.cpp:32-92), one thread per ROI: exact
-// integer sums, separable row sums of w dx^p about the integer anchors (pixels are
-// in row-major order), then the binomial shifts to the centroid and the origin,
-// eta and Hu; the same formulas as the warp path, scalar and amortised over 32
-// ROIs per warp.
-__device__ void moments_serial(uint32_t t, const RoiList& rl, Control* ctl, const FeatCfg& cfg,
-                               double* out) {
+// Moments of the staged S ROIs (moments.cpp:32-92), one thread per ROI and group
+// (grp 0 binary, 1 intensity-weighted): sums of w dx^p dy^q about the integer
+// anchors (pixels in row-major order), then the binomial shifts to the centroid
+// and the origin, eta and Hu; the same formulas as the warp path, scalar and
+// amortised over 32 ROIs per warp.  Binary sums are exact integers (|dx^p dy^q|
+// < 2^32, IMAD.WIDE into int64 on the integer pipe); weighted sums are fp64.
+__device__ void moments_serial(uint32_t t, int grp, const RoiList& rl, Control* ctl,
+                               const FeatCfg& cfg, double* out) {
     const uint32_t n0 = ctl->class_count[kClassS0], n1 = ctl->class_count[kClassS1];
     const uint32_t nt = n0 + n1 + ctl->class_count[kClassS2];
     if (t >= nt) return;
@@ -2025,108 +2026,137 @@ __device__ void moments_serial(uint32_t t, const RoiList& rl, Control* ctl, cons
     if (off == ~0ull) return;  // not staged: the warp path wrote the columns
     const uint32_t n = (uint32_t)rl.n[r];
     const unsigned long long* sums = cfg.mom_sums + (size_t)r * 5;
-    const unsigned long long sS = sums[0], sXI = sums[1], sYI = sums[2], sLX = sums[3], sLY = sums[4];
-    const long long nn = (long long)n, W = (long long)sS;
-    const long long axb = (2 * (long long)sLX + nn) / (2 * nn), ayb = (2 * (long long)sLY + nn) / (2 * nn);
-    const long long axw = W > 0 ? (2 * (long long)sXI + W) / (2 * W) : 0;
-    const long long ayw = W > 0 ? (2 * (long long)sYI + W) / (2 * W) : 0;
-    // every pixel adds its 32 terms (no row flush: divergent flushes across the 32
-    // ROIs of a warp cost more than the extra products); 16 B loads, two in flight
-    double Nb[16], Nw[16];
-#pragma unroll
-    for (int k = 0; k < 16; ++k) Nb[k] = Nw[k] = 0;
-    auto pixel = [&](uint32_t e) {
-        const double db = (double)((long long)(e & 0xffu) - axb), dw = (double)((long long)(e & 0xffu) - axw);
-        const double yb = (double)((long long)((e >> 8) & 0xffu) - ayb);
-        const double yw = (double)((long long)((e >> 8) & 0xffu) - ayw);
-        const double wv = (double)(e >> 16);
-        const double pb[4] = {1.0, db, db * db, db * db * db};
-        const double pw[4] = {wv, wv * dw, wv * dw * dw, wv * dw * dw * dw};
-        const double qb[4] = {1.0, yb, yb * yb, yb * yb * yb};
-        const double qw[4] = {1.0, yw, yw * yw, yw * yw * yw};
-#pragma unroll
-        for (int p = 0; p < 4; ++p)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                Nb[p * 4 + q] += pb[p] * qb[q];
-                Nw[p * 4 + q] += pw[p] * qw[q];
-            }
-    };
+    const long long nn = (long long)n;
+    double N[16];
+    long long W = 0, ax, ay, SX, SY;
+    if (grp == 0) {
+        SX = (long long)sums[3];
+        SY = (long long)sums[4];
+        ax = (2 * SX + nn) / (2 * nn);
+        ay = (2 * SY + nn) / (2 * nn);
+    } else {
+        W = (long long)sums[0];
+        SX = (long long)sums[1];
+        SY = (long long)sums[2];
+        ax = W > 0 ? (2 * SX + W) / (2 * W) : 0;
+        ay = W > 0 ? (2 * SY + W) / (2 * W) : 0;
+    }
     const uint4* px4 = reinterpret_cast<const uint4*>(cfg.mom_px + off);  // 16 B aligned
     const uint32_t nq = (n + 3u) >> 2;
-    uint4 cur = px4[0], nxt = nq > 1 ? px4[1] : make_uint4(0, 0, 0, 0);
-    for (uint32_t q4 = 0; q4 < nq; ++q4) {  // one 16 B chunk in flight ahead
-        const uint4 fut = q4 + 2 < nq ? px4[q4 + 2] : make_uint4(0, 0, 0, 0);
-        const uint32_t base = q4 * 4u;
-        pixel(cur.x);
-        if (base + 1 < n) pixel(cur.y);
-        if (base + 2 < n) pixel(cur.z);
-        if (base + 3 < n) pixel(cur.w);
-        cur = nxt;
-        nxt = fut;
+    // every pixel adds its 16 terms (no row flush: divergent flushes across the 32
+    // ROIs of a warp cost more than the extra products); 16 B loads, two in flight
+    auto stream = [&](auto&& pixel) {
+        uint4 cur = px4[0], nxt = nq > 1 ? px4[1] : make_uint4(0, 0, 0, 0);
+        for (uint32_t q4 = 0; q4 < nq; ++q4) {
+            const uint4 fut = q4 + 2 < nq ? px4[q4 + 2] : make_uint4(0, 0, 0, 0);
+            const uint32_t base = q4 * 4u;
+            pixel(cur.x);
+            if (base + 1 < n) pixel(cur.y);
+            if (base + 2 < n) pixel(cur.z);
+            if (base + 3 < n) pixel(cur.w);
+            cur = nxt;
+            nxt = fut;
+        }
+    };
+    if (grp == 0) {
+        long long M[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) M[k] = 0;
+        stream([&](uint32_t e) {
+            const int dx = (int)(e & 0xffu) - (int)ax, dy = (int)((e >> 8) & 0xffu) - (int)ay;
+            const int X[4] = {1, dx, dx * dx, dx * dx * dx};
+            const int Y[4] = {1, dy, dy * dy, dy * dy * dy};
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) M[p * 4 + q] += (long long)X[p] * Y[q];
+        });
+#pragma unroll
+        for (int k = 0; k < 16; ++k) N[k] = (double)M[k];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) N[k] = 0;
+        stream([&](uint32_t e) {
+            const double dx = (double)((long long)(e & 0xffu) - ax);
+            const double dy = (double)((long long)((e >> 8) & 0xffu) - ay);
+            const double wv = (double)(e >> 16);
+            const double pw[4] = {wv, wv * dx, wv * dx * dx, wv * dx * dx * dx};
+            const double q[4] = {1.0, dy, dy * dy, dy * dy * dy};
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int k = 0; k < 4; ++k) N[p * 4 + k] += pw[p] * q[k];
+        });
     }
     const long long gx0 = rl.gx[r], gy0 = rl.gy[r];
-    const double dn = (double)n;
-    double* o0 = out + (size_t)r * cfg.ncols + cfg.col_mom;
-    for (int grp = 0; grp < 2; ++grp) {
-        const double* N = grp ? Nw : Nb;
-        double* o = o0 + grp * 52;
-        const bool zero_mass = grp && sS == 0;
-        const double m00 = grp ? (double)sS : dn;
-        const double dx = grp ? (W > 0 ? (double)((long long)sXI - axw * W) / (double)W : 0.0)
-                              : (double)((long long)sLX - axb * nn) / dn;
-        const double dy = grp ? (W > 0 ? (double)((long long)sYI - ayw * W) / (double)W : 0.0)
-                              : (double)((long long)sLY - ayb * nn) / dn;
-        const double Ax = (double)(gx0 + (grp ? axw : axb)), Ay = (double)(gy0 + (grp ? ayw : ayb));
-        const double C[4][4] = {{1, 0, 0, 0}, {1, 1, 0, 0}, {1, 2, 1, 0}, {1, 3, 3, 1}};
-        double pmx[4], pmy[4], pax[4], pay[4];
-        pmx[0] = pmy[0] = pax[0] = pay[0] = 1.0;
-        for (int k = 1; k < 4; ++k) {
-            pmx[k] = pmx[k - 1] * (-dx);
-            pmy[k] = pmy[k - 1] * (-dy);
-            pax[k] = pax[k - 1] * Ax;
-            pay[k] = pay[k - 1] * Ay;
+    double* o = out + (size_t)r * cfg.ncols + cfg.col_mom + grp * 52;
+    const bool zero_mass = grp && W == 0;
+    const double m00 = grp ? (double)W : (double)n;
+    const double dx = grp ? (W > 0 ? (double)(SX - ax * W) / (double)W : 0.0) : (double)(SX - ax * nn) / (double)nn;
+    const double dy = grp ? (W > 0 ? (double)(SY - ay * W) / (double)W : 0.0) : (double)(SY - ay * nn) / (double)nn;
+    const double Ax = (double)(gx0 + ax), Ay = (double)(gy0 + ay);
+    // binomial shifts, separable: T[i][q] = sum_j C(q,j) s_y^(q-j) N[i][j], then
+    // out[p][q] = sum_i C(p,i) s_x^(p-i) T[i][q] (one 4x4 tile live at a time);
+    // s = -d for the central moments, the anchor's origin A for the raw ones
+    auto shift = [&](double sx, double sy, double* R) {
+        const double y1 = sy, y2 = sy * sy, y3 = y2 * sy;
+        const double x1 = sx, x2 = sx * sx, x3 = x2 * sx;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double a0 = N[i * 4], a1 = N[i * 4 + 1], a2 = N[i * 4 + 2], a3 = N[i * 4 + 3];
+            R[i * 4] = a0;
+            R[i * 4 + 1] = a1 + y1 * a0;
+            R[i * 4 + 2] = a2 + 2.0 * y1 * a1 + y2 * a0;
+            R[i * 4 + 3] = a3 + 3.0 * y1 * a2 + 3.0 * y2 * a1 + y3 * a0;
         }
-        double eta[4][4];
-        for (int p = 0; p < 4; ++p)
-            for (int q = 0; q < 4; ++q) {
-                double mu = 0, raw = 0;
-                for (int i = 0; i <= p; ++i)
-                    for (int j = 0; j <= q; ++j) {
-                        const double cc = C[p][i] * C[q][j];
-                        mu += cc * pmx[p - i] * pmy[q - j] * N[i * 4 + j];
-                        raw += cc * pax[p - i] * pay[q - j] * N[i * 4 + j];
-                    }
-                if ((p == 1 && q == 0) || (p == 0 && q == 1)) mu = 0.0;  // moments.cpp:80-81
-                if (p == 0 && q == 0) mu = N[0];
-                double et = 0;
-                if (p + q >= 2) {  // eta = mu / m00^(1 + (p+q)/2)
-                    double den = m00 * m00;
-                    if (p + q >= 4) den *= m00;
-                    if (p + q >= 6) den *= m00;
-                    if ((p + q) & 1) den *= sqrt(m00);
-                    et = mu / den;
-                }
-                if (zero_mass) raw = mu = et = 0;
-                eta[p][q] = et;
-                o[p * 4 + q] = raw;
-                o[16 + p * 4 + q] = mu;
-                if (p + q >= 2) o[32 + ((p == 0) ? q - 2 : (p == 1 ? 1 + q : 1 + 4 * (p - 1) + q))] = et;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double a0 = R[q], a1 = R[4 + q], a2 = R[8 + q], a3 = R[12 + q];
+            R[4 + q] = a1 + x1 * a0;
+            R[8 + q] = a2 + 2.0 * x1 * a1 + x2 * a0;
+            R[12 + q] = a3 + 3.0 * x1 * a2 + 3.0 * x2 * a1 + x3 * a0;
+        }
+    };
+    double R[16];
+    shift(Ax, Ay, R);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) o[k] = zero_mass ? 0.0 : R[k];
+    shift(-dx, -dy, R);
+    R[1] = R[4] = 0.0;  // moments.cpp:80-81
+    R[0] = N[0];
+    double eta[4][4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double mu = R[p * 4 + q];
+            double et = 0;
+            if (p + q >= 2) {  // eta = mu / m00^(1 + (p+q)/2)
+                double den = m00 * m00;
+                if (p + q >= 4) den *= m00;
+                if (p + q >= 6) den *= m00;
+                if ((p + q) & 1) den *= sqrt(m00);
+                et = mu / den;
             }
-        const double n20 = eta[2][0], n02 = eta[0][2], n11 = eta[1][1], n30 = eta[3][0],
-                     n03 = eta[0][3], n21 = eta[2][1], n12 = eta[1][2];
-        const double a = n30 + n12, b = n21 + n03;
-        const double hu[7] = {n20 + n02,
-                              (n20 - n02) * (n20 - n02) + 4.0 * n11 * n11,
-                              (n30 - 3.0 * n12) * (n30 - 3.0 * n12) + (3.0 * n21 - n03) * (3.0 * n21 - n03),
-                              a * a + b * b,
-                              (n30 - 3.0 * n12) * a * (a * a - 3.0 * b * b) +
-                                  (3.0 * n21 - n03) * b * (3.0 * a * a - b * b),
-                              (n20 - n02) * (a * a - b * b) + 4.0 * n11 * a * b,
-                              (3.0 * n21 - n03) * a * (a * a - 3.0 * b * b) -
-                                  (n30 - 3.0 * n12) * b * (3.0 * a * a - b * b)};
-        for (int k = 0; k < 7; ++k) o[45 + k] = zero_mass ? 0.0 : hu[k];
-    }
+            if (zero_mass) et = 0;
+            eta[p][q] = et;
+            o[16 + p * 4 + q] = zero_mass ? 0.0 : mu;
+            if (p + q >= 2) o[32 + ((p == 0) ? q - 2 : (p == 1 ? 1 + q : 1 + 4 * (p - 1) + q))] = et;
+        }
+    const double n20 = eta[2][0], n02 = eta[0][2], n11 = eta[1][1], n30 = eta[3][0],
+                 n03 = eta[0][3], n21 = eta[2][1], n12 = eta[1][2];
+    const double a = n30 + n12, b = n21 + n03;
+    const double hu[7] = {n20 + n02,
+                          (n20 - n02) * (n20 - n02) + 4.0 * n11 * n11,
+                          (n30 - 3.0 * n12) * (n30 - 3.0 * n12) + (3.0 * n21 - n03) * (3.0 * n21 - n03),
+                          a * a + b * b,
+                          (n30 - 3.0 * n12) * a * (a * a - 3.0 * b * b) +
+                              (3.0 * n21 - n03) * b * (3.0 * a * a - b * b),
+                          (n20 - n02) * (a * a - b * b) + 4.0 * n11 * a * b,
+                          (3.0 * n21 - n03) * a * (a * a - 3.0 * b * b) -
+                              (n30 - 3.0 * n12) * b * (3.0 * a * a - b * b)};
+#pragma unroll
+    for (int k = 0; k < 7; ++k) o[45 + k] = zero_mass ? 0.0 : hu[k];
 }
 
 // Intensity statistics of the staged S ROIs (intensity_features.cpp:42-215), one
@@ -2178,13 +2208,12 @@ __device__ void intensity_serial(uint32_t t, const RoiList& rl, Control* ctl, co
     const double median = (n & 1) ? (double)s[n / 2] : 0.5 * ((double)s[n / 2 - 1] + (double)s[n / 2]);
     const double pv[6] = {1.0, 10.0, 25.0, 75.0, 90.0, 99.0};
     double pct[6];
+#pragma unroll
     for (int k = 0; k < 6; ++k) pct[k] = percentile_exact(s, n, pv[k]);
     const double p10 = pct[1], p25 = pct[2], p75 = pct[3], p90 = pct[4];
     const uint32_t M2 = (n & 1) ? 2u * s[n / 2] : (uint32_t)s[n / 2 - 1] + s[n / 2];
-    const uint32_t d_hi = kth_dev_scan(s, n, M2, n / 2);
-    const uint32_t d_lo = (n & 1) ? d_hi : kth_dev_scan(s, n, M2, n / 2 - 1);
-    const double median_ad = (n & 1) ? 0.5 * (double)d_hi : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
     // one scan: central moments, mad / rmad partials, value runs (mode), bin runs
+    // (it also pulls the values into L1 for the dependent searches that follow)
     const uint32_t nb32 = (uint32_t)cfg.bins, rng = vmax - vmin;
     const bool wide = (unsigned long long)nb32 * 65535ull >= (1ull << 32);
     const uint32_t magic = rng ? (uint32_t)(0xffffffffull / rng) : 0u;
@@ -2250,6 +2279,9 @@ __device__ void intensity_serial(uint32_t t, const RoiList& rl, Control* ctl, co
         ent += (double)run_b * (logn - log2_int(run_b));
         usq += (unsigned long long)run_b * run_b;
     }
+    const uint32_t d_hi = kth_dev_scan(s, n, M2, n / 2);
+    const uint32_t d_lo = (n & 1) ? d_hi : kth_dev_scan(s, n, M2, n / 2 - 1);
+    const double median_ad = (n & 1) ? 0.5 * (double)d_hi : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
     const double m2 = a2 / dn, m3 = a3 / dn, m4 = a4 / dn, m5 = a5 / dn, m6 = a6 / dn;
     const double mad = ((double)(long long)(sS - 2 * slo) +
                         (double)((long long)clo - (long long)(n - clo)) * mean) / dn;
@@ -2285,15 +2317,28 @@ __device__ void intensity_serial(uint32_t t, const RoiList& rl, Control* ctl, co
                             (double)usq / (dn * dn), (p75 + p25) != 0 ? iqr / (p75 + p25) : 0.0,
                             mean != 0 ? sdev / mean : 0.0, (double)sS};
     double* oi = out + (size_t)r * cfg.ncols + cfg.col_int;
+#pragma unroll
     for (int k = 0; k < 32; ++k) oi[k] = o32[k];
 }
 
 // the per-ROI serial passes of the S ROIs in one launch: blocks [0, bi) run the
-// intensity statistics, the rest the moments, so the two sparse waves overlap
-__global__ void __launch_bounds__(128) k_serial_stats(RoiList rl, Control* ctl, FeatCfg cfg,
-                                                      double* out, uint32_t bi) {
-    if (blockIdx.x < bi) intensity_serial(blockIdx.x * blockDim.x + threadIdx.x, rl, ctl, cfg, out);
-    else moments_serial((blockIdx.x - bi) * blockDim.x + threadIdx.x, rl, ctl, cfg, out);
+// intensity statistics, [bi, bi + bm) the binary moments, the rest the weighted
+// moments, so the sparse waves overlap (and binary moments use the integer pipe
+// while the other two use fp64)
+#ifndef FXG_SERIAL_MINB
+#define FXG_SERIAL_MINB 5
+#endif
+__global__ void __launch_bounds__(128, FXG_SERIAL_MINB)
+    k_serial_stats(RoiList rl, Control* ctl, FeatCfg cfg, double* out, uint32_t bi, uint32_t bm) {
+    const uint32_t b = blockIdx.x;
+#ifdef FXG_SERIAL_ONLY  // register-demand probe of one role (tools only)
+    if (FXG_SERIAL_ONLY == 0) intensity_serial(b * blockDim.x + threadIdx.x, rl, ctl, cfg, out);
+    else moments_serial(b * blockDim.x + threadIdx.x, FXG_SERIAL_ONLY - 1, rl, ctl, cfg, out);
+    return;
+#endif
+    if (b < bi) intensity_serial(b * blockDim.x + threadIdx.x, rl, ctl, cfg, out);
+    else if (b < bi + bm) moments_serial((b - bi) * blockDim.x + threadIdx.x, 0, rl, ctl, cfg, out);
+    else moments_serial((b - bi - bm) * blockDim.x + threadIdx.x, 1, rl, ctl, cfg, out);
 }
 
 void launch_serial_stats(int n_s, bool intensity, bool moments, cudaStream_t s, RoiList rl,
@@ -2301,7 +2346,7 @@ void launch_serial_stats(int n_s, bool intensity, bool moments, cudaStream_t s, 
     if (n_s <= 0 || (!intensity && !moments)) return;
     const uint32_t nb = (uint32_t)((n_s + 127) / 128);
     const uint32_t bi = intensity ? nb : 0u, bm = moments ? nb : 0u;
-    k_serial_stats<<<bi + bm, 128, 0, s>>>(rl, ctl, cfg, out, bi);
+    k_serial_stats<<<bi + 2 * bm, 128, 0, s>>>(rl, ctl, cfg, out, bi, bm);
 }
 
 void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,

@@ -30,7 +30,7 @@ for line in dis.splitlines():
         funcs.setdefault(cur, [])
         continue
     if "//## File" in line:
-        chain = [(f.split("/")[-1], int(l)) for f, l in re.findall(r'File "([^"]+)", line (\d+)', line)]
+        chain = [(f.split("/")[-1], int(l)) for f, l in re.findall(r'"([^"]+)", line (\d+)', line)]
         continue
     m = re.match(r"\s+/\*([0-9a-f]{4,})\*/\s+(.*?);", line)
     if m and cur:
