@@ -121,6 +121,17 @@ struct TShared {
     uint32_t u32[kTW + 1];
     uint32_t job;
     uint32_t nfill;                // slots listed in hjl
+    // dense GLRLM (S windows, ng <= 64, <= 4 angles)
+    uint32_t gl_plev[4 * 64];      // runs per (angle, level)
+    uint32_t gl_ext[4 * 65];       // runs per (angle, length 1..64)
+    double gl_red[kTW][10];        // per-warp cell sums
+    double gl_f[4][16];            // features per angle
+    double gl_rcp2[64];            // 1 / k^2, k = 1..64
+    // NGTDM: present levels in order, their p_i and s_i
+    uint8_t ng_lev[256];
+    double ng_p[256];
+    double ng_s[256];
+    uint32_t ng_np;
     // dynamic shared memory (kDynBytes), S-class windows:
     uint16_t* slev;                // [4096] level raster
     uint32_t* skey;                // [4096] (level, extent) keys   } distinct keys <=
@@ -130,6 +141,25 @@ struct TShared {
     uint16_t* szsz;                // [4096] flatten scratch, then zone sizes
 };
 constexpr size_t kDynBytes = 4096 * 2 + 3 * 4096 * 4 + 2 * 4096 * 2;
+
+// x, y of cell c of a row-major window of width w without an integer division:
+// m = ceil(2^32 / w) gives floor(c / w) or one more (c < 2^32), fixed by one step
+struct CellDiv {
+    uint32_t w, m;
+    __device__ explicit CellDiv(uint32_t w_) : w(w_), m(w_ > 1 ? (uint32_t)(0xffffffffu / w_) + 1u : 0u) {}
+    __device__ __forceinline__ void split(uint32_t c, int& x, int& y) const {
+        uint32_t q = w > 1 ? __umulhi(c, m) : c;
+        if (q * w > c) --q;
+        y = (int)q;
+        x = (int)(c - q * w);
+    }
+};
+
+// shared-memory reductions through explicit shared addresses (the slab pointers
+// are generic, which would compile to generic ATOM)
+__device__ __forceinline__ void sred_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
 
 __device__ __forceinline__ uint32_t thash(uint32_t k) {
     k ^= k >> 16;
@@ -276,10 +306,12 @@ __device__ void glszm_zones(T* par, T* zsz, const uint16_t* lv, int w, int h, ui
         zsz[c] = 0;
     }
     __syncthreads();
+    const CellDiv cd((uint32_t)w);
     for (uint32_t c = tid; c < cells; c += kTT) {  // forward neighbours E, SW, S, SE
         const uint32_t g = lv[c];
         if (g == kNoLevel) continue;
-        const int y = (int)(c / (uint32_t)w), x = (int)(c - (uint32_t)y * (uint32_t)w);
+        int x, y;
+        cd.split(c, x, y);
         const int nx[4] = {x + 1, x - 1, x, x + 1}, ny[4] = {y, y + 1, y + 1, y + 1};
         for (int k = 0; k < 4; ++k)
             if (nx[k] >= 0 && nx[k] < w && ny[k] < h &&
@@ -322,6 +354,158 @@ __device__ __forceinline__ void unit_terms(double (&t)[8], int g0, uint32_t l0) 
     t[7] += g2 * l2;
 }
 
+__device__ __forceinline__ void angle_dir(int angle, int& dx, int& dy) {
+    dx = 1;
+    dy = 0;
+    if (angle == 45) dy = -1;
+    else if (angle == 90) { dx = 0; dy = 1; }
+    else if (angle == 135) dy = 1;
+}
+
+// GLRLM (texture.cpp:242-341) of an S-class window with ng <= 64 and <= 4 angles:
+// the runs of every angle in one pass over the cells, counted densely per
+// (angle, level, length) as packed u16 in the (then idle) hash-table region of
+// shared memory (lengths <= 64 in a 64 x 64 window), with runs per level and per
+// length by shared atomics; then every feature from the dense counts: the cell
+// terms by the two warps of each angle, the level / length moments by one warp
+// per angle.  Counts are order free and every floating-point sum runs in fixed
+// order (deterministic).  Restores the hash table's empty state.
+__device__ void glrlm_dense(const uint16_t* lv, int w, int h, uint32_t cells, unsigned long long np_u,
+                            const FeatCfg& cfg, TShared& sm, double* og) {
+    const unsigned tid = threadIdx.x, lane = lane_id(), wp = twarp();
+    const int A = cfg.n_angles;
+    uint32_t* H = sm.skey;  // word (a * 4096 + g * 64 + l - 1) >> 1, A * 2048 words <= skey + scnt
+    for (uint32_t i = tid; i < (uint32_t)A * 2048u; i += kTT) H[i] = 0u;
+    for (uint32_t i = tid; i < 4u * 64u; i += kTT) sm.gl_plev[i] = 0u;
+    for (uint32_t i = tid; i < 4u * 65u; i += kTT) sm.gl_ext[i] = 0u;
+    __syncthreads();
+    const CellDiv cd((uint32_t)w);
+    for (uint32_t c = tid; c < cells; c += kTT) {
+        const uint32_t g = lv[c];
+        if (g == kNoLevel) continue;
+        int x, y;
+        cd.split(c, x, y);
+        for (int a = 0; a < A; ++a) {
+            int dx, dy;
+            angle_dir(cfg.angle[a], dx, dy);
+            const int px = x - dx, py = y - dy;
+            if (px >= 0 && px < w && py >= 0 && py < h && lv[(uint32_t)py * (uint32_t)w + (uint32_t)px] == g)
+                continue;  // not a run start
+            uint32_t len = 1;
+            int nx = x + dx, ny = y + dy;
+            while (nx >= 0 && nx < w && ny >= 0 && ny < h && lv[(uint32_t)ny * (uint32_t)w + (uint32_t)nx] == g) {
+                ++len;
+                nx += dx;
+                ny += dy;
+            }
+            const uint32_t e = (uint32_t)a * 4096u + g * 64u + (len - 1u);
+            sred_add(&H[e >> 1], 1u << ((e & 1u) * 16u));
+            sred_add(&sm.gl_plev[a * 64 + g], 1u);
+            sred_add(&sm.gl_ext[a * 65 + len], 1u);
+        }
+    }
+    __syncthreads();
+    // cell terms: warps 2a, 2a+1 cover angle a's 2048 words (lanes stride 64 words)
+    if (wp < 2u * (unsigned)A) {
+        const int a = (int)(wp >> 1);
+        double t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // t8, sum c, sum c log2 c
+        for (uint32_t wd = (wp & 1u) * 32u + lane; wd < 2048u; wd += 64u) {
+            const uint32_t word = H[(uint32_t)a * 2048u + wd];
+            if (!word) continue;
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                const uint32_t c = (word >> (16 * half)) & 0xffffu;
+                if (!c) continue;
+                const uint32_t e = wd * 2u + (uint32_t)half;
+                const double g = (double)(e >> 6) + 1.0, l = (double)(e & 63u) + 1.0;
+                const double cc = (double)c, g2 = g * g, l2 = l * l;
+                const double rg2 = sm.gl_rcp2[e >> 6], rl2 = sm.gl_rcp2[e & 63u];  // 1/g^2, 1/l^2
+                t[0] += cc * rl2;
+                t[1] += cc * l2;
+                t[2] += cc * rg2;
+                t[3] += cc * g2;
+                t[4] += cc * (rg2 * rl2);
+                t[5] += cc * (g2 * rl2);
+                t[6] += cc * (l2 * rg2);
+                t[7] += cc * g2 * l2;
+                t[8] += cc;
+                t[9] += cc * log2_int(c);
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 10; ++k) {
+            double v = t[k];
+#pragma unroll
+            for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+            if (lane == 0) sm.gl_red[wp][k] = v;
+        }
+    }
+    __syncthreads();
+    // level / length moments and the 16 features: warp 2a for angle a
+    if (wp < 2u * (unsigned)A && !(wp & 1u)) {
+        const int a = (int)(wp >> 1);
+        double t[10];
+#pragma unroll
+        for (int k = 0; k < 10; ++k) t[k] = sm.gl_red[wp][k] + sm.gl_red[wp + 1][k];
+        const double nr = t[8];
+        double f = 0;
+        if (nr > 0) {
+            const double logn = nlog2(nr), np = (double)np_u;
+            double s[4] = {0, 0, 0, 0};  // glnu, sum c (g+1), rlnu, sum c l
+            for (int g = (int)lane; g < 64; g += 32) {
+                const double c = (double)sm.gl_plev[a * 64 + g];
+                s[0] += c * c;
+                s[1] += c * (g + 1);
+            }
+            for (int l = (int)lane + 1; l <= 64; l += 32) {
+                const double c = (double)sm.gl_ext[a * 65 + l];
+                s[2] += c * c;
+                s[3] += c * l;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+#pragma unroll
+                for (int o = 16; o; o >>= 1) s[k] += __shfl_xor_sync(kFull, s[k], o);
+            const double mu_g = s[1] / nr, mu_l = s[3] / nr;
+            double v2[2] = {0, 0};  // glv, rv
+            for (int g = (int)lane; g < 64; g += 32) {
+                const double c = (double)sm.gl_plev[a * 64 + g];
+                v2[0] += c / nr * (g + 1 - mu_g) * (g + 1 - mu_g);
+            }
+            for (int l = (int)lane + 1; l <= 64; l += 32) {
+                const double c = (double)sm.gl_ext[a * 65 + l];
+                v2[1] += c / nr * ((double)l - mu_l) * ((double)l - mu_l);
+            }
+#pragma unroll
+            for (int k = 0; k < 2; ++k)
+#pragma unroll
+                for (int o = 16; o; o >>= 1) v2[k] += __shfl_xor_sync(kFull, v2[k], o);
+            const double v[16] = {t[0] / nr, t[1] / nr, s[0] / nr, s[0] / (nr * nr), s[2] / nr,
+                                  s[2] / (nr * nr), nr / np, v2[0], v2[1], logn - t[9] / nr,
+                                  t[2] / nr, t[3] / nr, t[4] / nr, t[5] / nr, t[6] / nr, t[7] / nr};
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                if ((int)lane == k) f = v[k];
+        }
+        if (lane < 16) sm.gl_f[a][lane] = f;
+    }
+    __syncthreads();
+    if (tid < 16) {
+        double acc = 0;
+        for (int a = 0; a < A; ++a) {
+            og[tid * (A + 1) + a] = sm.gl_f[a][tid];
+            acc += sm.gl_f[a][tid];
+        }
+        og[tid * (A + 1) + A] = acc / (double)A;
+    }
+    // the hash table (skey / scnt) is kept empty between uses
+    for (uint32_t i = tid; i < 4096u; i += kTT) {
+        sm.skey[i] = kEmpty;
+        sm.scnt[i] = 0u;
+    }
+    __syncthreads();
+}
+
 __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Control* ctl,
                           const FeatCfg& cfg, double* __restrict__ out, const TSlab& S, uint32_t HC,
                           uint32_t NMAX, TShared& sm) {
@@ -333,32 +517,33 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
     const unsigned long long n = rl.n[r];
     const int ng = cfg.ng;
     double* orow = out + (size_t)r * cfg.ncols;
-    auto lab_at = [&](uint32_t c) -> uint32_t {
-        const uint32_t y = c / (uint32_t)w, x = c - y * (uint32_t)w;
-        return img.L[(size_t)(y0 + y) * img.pitch + x0 + x];
-    };
-    auto int_at = [&](uint32_t c) -> uint32_t {
-        const uint32_t y = c / (uint32_t)w, x = c - y * (uint32_t)w;
-        return img.I[(size_t)(y0 + y) * img.pitch + x0 + x];
+    const CellDiv cd((uint32_t)w);
+    auto at = [&](uint32_t c) -> size_t {  // raster offset of window cell c
+        int x, y;
+        cd.split(c, x, y);
+        return (size_t)(y0 + (uint32_t)y) * img.pitch + x0 + (uint32_t)x;
     };
     TT_DECL
     // ---- discretize (texture.cpp:29-56): min/max, then the level raster
     uint32_t lo = 0xffffu, hi = 0u;
-    for (uint32_t c = tid; c < cells; c += kTT)
-        if (lab_at(c) == label) {
-            const uint32_t v = int_at(c);
+    for (uint32_t c = tid; c < cells; c += kTT) {
+        const size_t o = at(c);
+        if (img.L[o] == label) {
+            const uint32_t v = img.I[o];
             lo = min(lo, v);
             hi = max(hi, v);
         }
+    }
     const uint32_t vmin = tblock_all(lo, sm.u32, TMin()), vmax = tblock_all(hi, sm.u32, TMax());
     const unsigned long long span = (unsigned long long)(vmax - vmin) + 1ull;
     uint16_t* lv = cells <= 4096u ? sm.slev : S.lev;  // shared memory for S-class windows
     for (uint32_t c = tid; c < cells; c += kTT) {
         uint16_t l = kNoLevel;
-        if (lab_at(c) == label) {
+        const size_t o = at(c);
+        if (img.L[o] == label) {
             l = 0;
             if (vmax > vmin) {
-                const unsigned long long q = (unsigned long long)ng * (int_at(c) - vmin) / span;
+                const unsigned long long q = (unsigned long long)ng * (img.I[o] - vmin) / span;
                 l = (uint16_t)(q < (unsigned long long)(ng - 1) ? q : (unsigned long long)(ng - 1));
             }
         }
@@ -377,6 +562,11 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                                                     : (uint32_t)kNoLevel;
     };
     // ---- GLRLM per sorted angle (texture.cpp:242-280)
+#ifndef FXG_GLRLM_HASH
+    if (cfg.col_glrlm >= 0 && small && w <= 64 && h <= 64 && ng <= 64 && cfg.n_angles <= 4) {
+        glrlm_dense(lv, w, h, cells, n, cfg, sm, orow + cfg.col_glrlm);
+    } else
+#endif
     if (cfg.col_glrlm >= 0) {
         const int A = cfg.n_angles;
         double* og = orow + cfg.col_glrlm;
@@ -396,7 +586,8 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
             for (uint32_t c = tid; c < cells; c += kTT) {
                 const uint32_t g = lv[c];
                 if (g == kNoLevel) continue;
-                const int y = (int)(c / (uint32_t)w), x = (int)(c - (uint32_t)y * (uint32_t)w);
+                int x, y;
+                cd.split(c, x, y);
                 if (lev(x - dx, y - dy) == g) continue;  // not a run start
                 uint32_t len = 1;
                 int nx = x + dx, ny = y + dy;
@@ -472,7 +663,8 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
         for (uint32_t c = tid; c < cells; c += kTT) {
             const uint32_t g = lv[c];
             if (g == kNoLevel) continue;
-            const int y = (int)(c / (uint32_t)w), x = (int)(c - (uint32_t)y * (uint32_t)w);
+            int x, y;
+            cd.split(c, x, y);
             int sum = 0, cnt = 0;
             for (int ddy = -1; ddy <= 1; ++ddy)
                 for (int ddx = -1; ddx <= 1; ++ddx) {
@@ -506,17 +698,34 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
             const double s_total = r3[0], ps_total = r3[1];
             const uint32_t present = (uint32_t)r3[2];
             double a_con = 0, a_busy = 0, a_cplx = 0, a_strn = 0;
-            const uint32_t pairs = (uint32_t)ng * (uint32_t)ng;
-            for (uint32_t q = tid; q < pairs; q += kTT) {
-                const int i = (int)(q / (uint32_t)ng), j = (int)(q - (uint32_t)i * (uint32_t)ng);
-                if (!sm.plev[i] || !sm.plev[j]) continue;
-                const double pi = (double)sm.plev[i] / nv, pj = (double)sm.plev[j] / nv;
-                const double si = (double)sm.sng[i] / 840.0, sj = (double)sm.sng[j] / 840.0;
-                const double gi = i + 1, gj = j + 1;
-                a_con += pi * pj * (i - j) * (i - j);
-                a_busy += fabs(gi * pi - gj * pj);
-                a_cplx += fabs(gi - gj) * (pi * si + pj * sj) / (pi + pj);
-                a_strn += (pi + pj) * (gi - gj) * (gi - gj);
+            // pairs of present levels only (absent levels contribute nothing):
+            // compact list in level order with p_i and s_i computed once
+            if (tid == 0) {
+                uint32_t k = 0;
+                for (int i = 0; i < ng; ++i)
+                    if (sm.plev[i]) sm.ng_lev[k++] = (uint8_t)i;
+                sm.ng_np = k;
+            }
+            __syncthreads();
+            const uint32_t P = sm.ng_np;
+            for (uint32_t k = tid; k < P; k += kTT) {
+                const int i = sm.ng_lev[k];
+                sm.ng_p[k] = (double)sm.plev[i] / nv;
+                sm.ng_s[k] = (double)sm.sng[i] / 840.0;
+            }
+            __syncthreads();
+            const unsigned lane = lane_id();
+            for (uint32_t ki = twarp(); ki < P; ki += kTW) {
+                const int i = sm.ng_lev[ki];
+                const double pi = sm.ng_p[ki], si = sm.ng_s[ki], gi = i + 1;
+                for (uint32_t kj = lane; kj < P; kj += 32) {
+                    const int j = sm.ng_lev[kj];
+                    const double pj = sm.ng_p[kj], sj = sm.ng_s[kj], gj = j + 1;
+                    a_con += pi * pj * (i - j) * (i - j);
+                    a_busy += fabs(gi * pi - gj * pj);
+                    a_cplx += fabs(gi - gj) * (pi * si + pj * sj) / (pi + pj);
+                    a_strn += (pi + pj) * (gi - gj) * (gi - gj);
+                }
             }
             double r4[4] = {a_con, a_busy, a_cplx, a_strn};
             tblock_sum<4>(r4, sm.red8);
@@ -558,6 +767,7 @@ __global__ void __launch_bounds__(kTT) k_roi_t(DevImage img, RoiList rl, Control
     S.ext = (uint32_t*)(base + T.ext);
     S.ccnt = (uint32_t*)(base + T.ccnt);
     for (int g = threadIdx.x; g < 256; g += kTT) sm.plev[g] = 0u;
+    for (int k = threadIdx.x; k < 64; k += kTT) sm.gl_rcp2[k] = 1.0 / ((double)(k + 1) * (double)(k + 1));
     for (int i = threadIdx.x; i < 4096; i += kTT) {
         sm.skey[i] = kEmpty;
         sm.scnt[i] = 0u;
