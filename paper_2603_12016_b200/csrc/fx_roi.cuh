@@ -216,7 +216,7 @@ struct BLayout {
 
 // Byte offsets of one CTA's slab in the GLRLM/GLSZM/NGTDM kernel (fx_roi_t.cu).
 struct TLayout {
-    size_t lev, par, zsz, hjk, hjc, hjl, ext, ccnt;
+    size_t lev, par, zsz, hjk, hjc, ext, ccnt;
     size_t bytes;
     unsigned long long CELLS;  // max window cells
     uint32_t NMAX, HC;         // max ROI pixels; count-table capacity (power of 2)

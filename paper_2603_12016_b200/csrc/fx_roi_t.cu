@@ -107,7 +107,6 @@ struct TSlab {
     uint32_t* zsz;   // [cells] flatten scratch, then zone sizes
     uint32_t* hjk;   // [HC] (level, extent) keys  } open addressing, kept empty
     uint32_t* hjc;   // [HC] counts                 }
-    uint32_t* hjl;   // [HC] slots filled since the last reset (in any order)
     uint32_t* ext;   // [NMAX+1] units per extent (dense: fixed summation order)
     uint32_t* ccnt;  // [NMAX+1] joint cells per cell count (entropy by count value)
 };
@@ -120,7 +119,6 @@ struct TShared {
     unsigned long long u64[kTW + 1];
     uint32_t u32[kTW + 1];
     uint32_t job;
-    uint32_t nfill;                // slots listed in hjl
     // dense GLRLM (S windows, ng <= 64, <= 4 angles)
     uint32_t gl_plev[4 * 64];      // runs per (angle, level)
     uint32_t gl_ext[4 * 65];       // runs per (angle, length 1..64)
@@ -136,11 +134,10 @@ struct TShared {
     uint16_t* slev;                // [4096] level raster
     uint32_t* skey;                // [4096] (level, extent) keys   } distinct keys <=
     uint32_t* scnt;                // [4096] counts                 } units <= pixels
-    uint32_t* slst;                // [4096] filled slots           } <= 4096
     uint16_t* spar;                // [4096] GLSZM union-find parents (cell index)
     uint16_t* szsz;                // [4096] flatten scratch, then zone sizes
 };
-constexpr size_t kDynBytes = 4096 * 2 + 3 * 4096 * 4 + 2 * 4096 * 2;
+constexpr size_t kDynBytes = 4096 * 2 + 2 * 4096 * 4 + 2 * 4096 * 2;
 
 // x, y of cell c of a row-major window of width w without an integer division:
 // m = ceil(2^32 / w) gives floor(c / w) or one more (c < 2^32), fixed by one step
@@ -170,32 +167,30 @@ __device__ __forceinline__ uint32_t thash(uint32_t k) {
     return k;
 }
 
-__device__ __forceinline__ void table_add(uint32_t* keys, uint32_t* cnts, uint32_t* list,
-                                          uint32_t* nfill, uint32_t mask, uint32_t key) {
+__device__ __forceinline__ void table_add(uint32_t* keys, uint32_t* cnts, uint32_t mask, uint32_t key) {
     uint32_t h = thash(key) & mask;
     for (;;) {
         const uint32_t old = atomicCAS(&keys[h], kEmpty, key);
         if (old == kEmpty || old == key) {
             atomicAdd(&cnts[h], 1u);
-            if (old == kEmpty) list[atomicAdd(nfill, 1u)] = h;
             return;
         }
         h = (h + 1) & mask;
     }
 }
 
+
 // Features of the (level, extent) cells (glrlm_features texture.cpp:282-341,
 // glszm_features :382-441).  t8: block totals of the 8 per-unit sums (sre, lre,
 // lglre, hglre, srlgle, srhgle, lrlgle, lrhgle numerators); nr units, np pixels.
 // Empties the count tables and the per-level counts.
 __device__ void extent_features(const double* t8, unsigned long long nr_u, unsigned long long np_u,
-                                int ng, const TSlab& S, uint32_t* hk, uint32_t* hc, uint32_t* hl,
+                                int ng, const TSlab& S, uint32_t* hk, uint32_t* hc, uint32_t hsize,
                                 uint32_t emax, TShared& sm, double* out16) {
     const unsigned tid = threadIdx.x;
     if (nr_u == 0) {
         for (int k = tid; k < 16; k += kTT) out16[k] = 0.0;
         for (int g = tid; g < ng; g += kTT) sm.plev[g] = 0u;
-        if (tid == 0) sm.nfill = 0u;
         __syncthreads();
         return;
     }
@@ -216,10 +211,10 @@ __device__ void extent_features(const double* t8, unsigned long long nr_u, unsig
             a[3] += (double)c * (double)e;
         }
     }
-    const uint32_t nfill = sm.nfill;
+    // every slot of the table (no list of filled slots: one hot counter fewer)
     uint32_t cmax = 0;
-    for (uint32_t i = tid; i < nfill; i += kTT) {
-        const uint32_t slot = hl[i];
+    for (uint32_t slot = tid; slot < hsize; slot += kTT) {
+        if (hk[slot] == kEmpty) continue;
         const uint32_t c = hc[slot];
         atomicAdd(&S.ccnt[c], 1u);
         cmax = max(cmax, c);
@@ -228,7 +223,6 @@ __device__ void extent_features(const double* t8, unsigned long long nr_u, unsig
     }
     cmax = tblock_all(cmax, sm.u32, TMax());
     tblock_sum<4>(a, sm.red8);
-    if (tid == 0) sm.nfill = 0u;
     const double glnu = a[0], mu_g = a[1] / nr, rlnu = a[2], mu_l = a[3] / nr;
     // pass B: entropy = sum over cells c (log2 nr - log2 c) / nr, variances
     double b[3] = {0, 0, 0};
@@ -555,7 +549,6 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
     const bool small = cells <= 4096u && n <= 4096ull;
     uint32_t* hk = small ? sm.skey : S.hjk;
     uint32_t* hcn = small ? sm.scnt : S.hjc;
-    uint32_t* hl = small ? sm.slst : S.hjl;
     const uint32_t mask = small ? 4095u : HC - 1u;
     auto lev = [&](int x, int y) -> uint32_t {
         return (x >= 0 && x < w && y >= 0 && y < h) ? lv[(uint32_t)y * (uint32_t)w + (uint32_t)x]
@@ -600,7 +593,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                 ++runs;
                 emax = max(emax, len);
                 atomicAdd(&sm.plev[g], 1u);
-                table_add(hk, hcn, hl, &sm.nfill, mask, (g << 24) | len);
+                table_add(hk, hcn, mask, (g << 24) | len);
                 atomicAdd(&S.ext[len], 1u);
             }
             TT(4);
@@ -609,7 +602,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
             emax = tblock_all(emax, sm.u32, TMax());
             const double* tt = t;
             __shared__ double f16[16];
-            extent_features(tt, nr, n, ng, S, hk, hcn, hl, emax, sm, f16);
+            extent_features(tt, nr, n, ng, S, hk, hcn, mask + 1u, emax, sm, f16);
             __syncthreads();
             TT(5);
             if (tid < 16) {
@@ -638,7 +631,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
             ++zones;
             emax = max(emax, size);
             atomicAdd(&sm.plev[g], 1u);
-            table_add(hk, hcn, hl, &sm.nfill, mask, (g << 24) | size);
+            table_add(hk, hcn, mask, (g << 24) | size);
             atomicAdd(&S.ext[size], 1u);
         }
         tblock_sum<8>(t, sm.red8);
@@ -646,7 +639,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
         const unsigned long long nz = tblock_all(zones, sm.u64, TAdd());
         emax = tblock_all(emax, sm.u32, TMax());
         __shared__ double f16z[16];
-        extent_features(tt, nz, n, ng, S, hk, hcn, hl, emax, sm, f16z);
+        extent_features(tt, nz, n, ng, S, hk, hcn, mask + 1u, emax, sm, f16z);
         __syncthreads();
         if (tid < 16) orow[cfg.col_glszm + tid] = f16z[tid];
         __syncthreads();
@@ -746,15 +739,17 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
 }
 
 // which = 0: the S-class lists (windows <= 64 x 64); 1: the large-ROI list
-__global__ void __launch_bounds__(kTT) k_roi_t(DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
+#ifndef FXG_T_MINB
+#define FXG_T_MINB 3
+#endif
+__global__ void __launch_bounds__(kTT, FXG_T_MINB) k_roi_t(DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                                                double* out, uint8_t* scratch, TLayout T, int which) {
     __shared__ TShared sm;
     extern __shared__ __align__(16) uint8_t tdyn[];
     sm.slev = reinterpret_cast<uint16_t*>(tdyn);
     sm.skey = reinterpret_cast<uint32_t*>(tdyn + 4096 * 2);
     sm.scnt = sm.skey + 4096;
-    sm.slst = sm.scnt + 4096;
-    sm.spar = reinterpret_cast<uint16_t*>(sm.slst + 4096);
+    sm.spar = reinterpret_cast<uint16_t*>(sm.scnt + 4096);
     sm.szsz = sm.spar + 4096;
     uint8_t* base = scratch + (size_t)blockIdx.x * T.bytes;
     TSlab S;
@@ -763,7 +758,6 @@ __global__ void __launch_bounds__(kTT) k_roi_t(DevImage img, RoiList rl, Control
     S.zsz = (uint32_t*)(base + T.zsz);
     S.hjk = (uint32_t*)(base + T.hjk);
     S.hjc = (uint32_t*)(base + T.hjc);
-    S.hjl = (uint32_t*)(base + T.hjl);
     S.ext = (uint32_t*)(base + T.ext);
     S.ccnt = (uint32_t*)(base + T.ccnt);
     for (int g = threadIdx.x; g < 256; g += kTT) sm.plev[g] = 0u;
@@ -772,7 +766,6 @@ __global__ void __launch_bounds__(kTT) k_roi_t(DevImage img, RoiList rl, Control
         sm.skey[i] = kEmpty;
         sm.scnt[i] = 0u;
     }
-    if (threadIdx.x == 0) sm.nfill = 0u;
     __syncthreads();
     const uint32_t n0 = ctl->class_count[kClassS0], n1 = ctl->class_count[kClassS1];
     const uint32_t n2 = ctl->class_count[kClassS2], nl = ctl->class_count[kClassL];
@@ -822,7 +815,6 @@ TLayout make_tlayout(unsigned long long CELLS, uint32_t NMAX) {
     T.zsz = take((size_t)CELLS * 4);
     T.hjk = take((size_t)hc * 4);
     T.hjc = take((size_t)hc * 4);
-    T.hjl = take((size_t)hc * 4);
     T.ext = take(((size_t)NMAX + 1) * 4);
     T.ccnt = take(((size_t)NMAX + 1) * 4);
     T.bytes = o;
