@@ -368,6 +368,7 @@ __device__ void glrlm_dense(const uint16_t* lv, int w, int h, uint32_t cells, un
                             const FeatCfg& cfg, TShared& sm, double* og) {
     const unsigned tid = threadIdx.x, lane = lane_id(), wp = twarp();
     const int A = cfg.n_angles;
+    TT_DECL
     uint32_t* H = sm.skey;  // word (a * 4096 + g * 64 + l - 1) >> 1, A * 2048 words <= skey + scnt
     for (uint32_t i = tid; i < (uint32_t)A * 2048u; i += kTT) H[i] = 0u;
     for (uint32_t i = tid; i < 4u * 64u; i += kTT) sm.gl_plev[i] = 0u;
@@ -399,11 +400,16 @@ __device__ void glrlm_dense(const uint16_t* lv, int w, int h, uint32_t cells, un
         }
     }
     __syncthreads();
-    // cell terms: warps 2a, 2a+1 cover angle a's 2048 words (lanes stride 64 words)
+    TT(4);
+    // cell terms: warps 2a, 2a+1 cover angle a, lane L of the pair owns level L
+    // (counts crowd at short lengths, so level rows balance the lanes); the word
+    // order within a row is rotated by the level so the 32 lanes hit 32 banks
     if (wp < 2u * (unsigned)A) {
         const int a = (int)(wp >> 1);
+        const uint32_t gl = (wp & 1u) * 32u + lane;
         double t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // t8, sum c, sum c log2 c
-        for (uint32_t wd = (wp & 1u) * 32u + lane; wd < 2048u; wd += 64u) {
+        for (uint32_t k = 0; k < 32u; ++k) {
+            const uint32_t wd = gl * 32u + ((k + gl) & 31u);
             const uint32_t word = H[(uint32_t)a * 2048u + wd];
             if (!word) continue;
 #pragma unroll
@@ -492,12 +498,14 @@ __device__ void glrlm_dense(const uint16_t* lv, int w, int h, uint32_t cells, un
         }
         og[tid * (A + 1) + A] = acc / (double)A;
     }
+    TT(5);
     // the hash table (skey / scnt) is kept empty between uses
     for (uint32_t i = tid; i < 4096u; i += kTT) {
         sm.skey[i] = kEmpty;
         sm.scnt[i] = 0u;
     }
     __syncthreads();
+    TT(6);
 }
 
 __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Control* ctl,
@@ -707,11 +715,12 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                 sm.ng_s[k] = (double)sm.sng[i] / 840.0;
             }
             __syncthreads();
+            // every term is symmetric in (i, j) and 0 for i == j: pairs i < j, doubled
             const unsigned lane = lane_id();
             for (uint32_t ki = twarp(); ki < P; ki += kTW) {
                 const int i = sm.ng_lev[ki];
                 const double pi = sm.ng_p[ki], si = sm.ng_s[ki], gi = i + 1;
-                for (uint32_t kj = lane; kj < P; kj += 32) {
+                for (uint32_t kj = ki + 1 + lane; kj < P; kj += 32) {
                     const int j = sm.ng_lev[kj];
                     const double pj = sm.ng_p[kj], sj = sm.ng_s[kj], gj = j + 1;
                     a_con += pi * pj * (i - j) * (i - j);
@@ -720,6 +729,10 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                     a_strn += (pi + pj) * (gi - gj) * (gi - gj);
                 }
             }
+            a_con *= 2.0;
+            a_busy *= 2.0;
+            a_cplx *= 2.0;
+            a_strn *= 2.0;
             double r4[4] = {a_con, a_busy, a_cplx, a_strn};
             tblock_sum<4>(r4, sm.red8);
             const double con = r4[0], busy = r4[1], cplx = r4[2], strn = r4[3];
