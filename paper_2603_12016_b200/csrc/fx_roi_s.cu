@@ -1925,6 +1925,9 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
 namespace fxg {
 namespace {
 
+#ifndef FXG_S_PREFETCH
+#define FXG_S_PREFETCH 0  // 1: L2 prefetch of the next window (measured slower on C2)
+#endif
 template <int CLS, int GLCM>
 __global__ void __launch_bounds__(32, 20)
     k_roi_s(const __grid_constant__ CUtensorMap tmapL, int use_tma, DevImage img, RoiList rl,
@@ -1940,11 +1943,38 @@ __global__ void __launch_bounds__(32, 20)
     __syncwarp();
     uint32_t phase = 0;
     const uint32_t count = ctl->class_count[CLS];
+    uint32_t idx = 0;
+    if (lane == 0) idx = atomicAdd(&ctl->class_next[CLS], 1u);
+    idx = __shfl_sync(kFull, idx, 0);
     for (;;) {
-        uint32_t idx = 0;
-        if (lane == 0) idx = atomicAdd(&ctl->class_next[CLS], 1u);
-        idx = __shfl_sync(kFull, idx, 0);
         if (idx >= count) break;
+#if FXG_S_PREFETCH
+        // claim the next ROI now and pull its window rows (labels for the TMA
+        // tile, intensities for the gather) into L2 while this one is processed
+        uint32_t nidx = 0;
+        if (lane == 0) nidx = atomicAdd(&ctl->class_next[CLS], 1u);
+        nidx = __shfl_sync(kFull, nidx, 0);
+        if (nidx < count) {
+            const uint32_t r2 = rl.cls_list[CLS][nidx];
+            const uint32_t py = lane;
+            if (py < rl.h[r2]) {
+                const size_t o = (size_t)(rl.y0[r2] + py) * img.pitch + rl.x0[r2];
+                const size_t e = o + rl.w[r2] - 1;
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(img.L + o));
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(img.I + o));
+                if ((o >> 6) != (e >> 6)) {  // the row crosses a 128 B line
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(img.L + e));
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(img.I + e));
+                }
+            }
+        }
+#else
+        const uint32_t nidx = [&] {
+            uint32_t v = 0;
+            if (lane == 0) v = atomicAdd(&ctl->class_next[CLS], 1u);
+            return __shfl_sync(kFull, v, 0);
+        }();
+#endif
         const uint32_t r = rl.cls_list[CLS][idx];
         const SJob J{rl.label[r], rl.x0[r], rl.y0[r], rl.w[r], rl.h[r], r};
         if (use_tma) {
@@ -1971,6 +2001,7 @@ __global__ void __launch_bounds__(32, 20)
         }
         process_s<V::TW, V::TH, V::NMAX, V::RUNMAX, GLCM>(J, L, base, img, cfg, out, mbar, phase,
                                                          ctl, rl, dbg);
+        idx = nidx;
     }
 }
 
