@@ -244,9 +244,11 @@ cudaEvent_t get_event(fx_ctx* c) {
 struct Launch {
     fx_ctx* c;
     const char* name;
+    cudaStream_t st;
     cudaEvent_t a = nullptr, b = nullptr;
     bool timed = false;
-    Launch(fx_ctx* c_, const char* n) : c(c_), name(n) {
+    Launch(fx_ctx* c_, const char* n, cudaStream_t on = nullptr)
+        : c(c_), name(n), st(on ? on : c_->stream) {
         c->launches++;
         // each timing event between launches costs ~3 us of device time (it breaks
         // launch pipelining), so a filter can restrict timing to one kernel
@@ -254,16 +256,16 @@ struct Launch {
         if (timed) {
             a = get_event(c);
             b = get_event(c);
-            cudaEventRecord(a, c->stream);
+            cudaEventRecord(a, st);
         }
     }
     ~Launch() {
         if (timed) {
-            cudaEventRecord(b, c->stream);
+            cudaEventRecord(b, st);
             c->pending.push_back({name, {a, b}});
         }
         if (c->sync_debug) {  // FXG_SYNC_DEBUG=1: attribute device faults to a kernel
-            cudaError_t e = cudaStreamSynchronize(c->stream);
+            cudaError_t e = cudaStreamSynchronize(st);
             if (e != cudaSuccess) fprintf(stderr, "[fxg] %s: %s\n", name, cudaGetErrorString(e));
         }
     }
@@ -600,7 +602,23 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         return set_error(FX_E_CAPACITY, "output capacity " + std::to_string(cap_rois) +
                                             " < " + std::to_string(hc.n_rois) + " ROIs");
     }
-    if (cfg.col_glrlm >= 0 || cfg.col_glszm >= 0 || cfg.col_ngtdm >= 0) {
+    const bool texture = cfg.col_glrlm >= 0 || cfg.col_glszm >= 0 || cfg.col_ngtdm >= 0;
+    const uint64_t n_s_rois = (uint64_t)hc.class_count[kClassS0] + hc.class_count[kClassS1] +
+                              hc.class_count[kClassS2];
+    auto serial_passes = [&](cudaStream_t on) {
+        if (cfg.int_vals || cfg.mom_px) {
+            Launch l(c, "k_serial_stats", on);
+            launch_serial_stats((int)n_s_rois, cfg.int_vals != nullptr, cfg.mom_px != nullptr, on, rl,
+                                c->d_ctl, cfg, out_dev);
+        }
+        if (cfg.col_shape >= 0) {
+            Launch l(c, "k_shape_serial", on);
+            launch_shape_serial((int)n_s_rois, on, rl, c->d_ctl, cfg, out_dev);
+        }
+    };
+    // (running them on a second stream next to k_roi_t measured slower: its
+    // persistent CTAs leave no room, and 512-image batches fill the GPU anyway)
+    if (texture) {
         // GLRLM/GLSZM/NGTDM: S-class windows, then large windows (own slabs)
         const uint64_t n_s = (uint64_t)hc.class_count[kClassS0] + hc.class_count[kClassS1] +
                              hc.class_count[kClassS2];
@@ -634,19 +652,9 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
             }
         }
     }
-    if (cfg.int_vals || cfg.mom_px) {  // intensity statistics + moments of the staged S ROIs
-        const int n_s = (int)(hc.class_count[kClassS0] + hc.class_count[kClassS1] +
-                              hc.class_count[kClassS2]);
-        Launch l(c, "k_serial_stats");
-        launch_serial_stats(n_s, cfg.int_vals != nullptr, cfg.mom_px != nullptr, s, rl, c->d_ctl,
-                            cfg, out_dev);
-    }
-    if (cfg.col_shape >= 0) {  // serial shape columns of the S ROIs, before k_roi_b
-        const int n_s = (int)(hc.class_count[kClassS0] + hc.class_count[kClassS1] +
-                              hc.class_count[kClassS2]);
-        Launch l(c, "k_shape_serial");
-        launch_shape_serial(n_s, s, rl, c->d_ctl, cfg, out_dev);
-    }
+    // intensity statistics, moments and serial shape columns of the staged S ROIs,
+    // before k_roi_b (which rewrites the rows of overflowed S ROIs)
+    if (n_s_rois > 0) serial_passes(s);
     {
         // large ROIs + S overflow: one CTA per ROI; the slabs' histograms are kept
         // zero by the kernel, so they are cleared only when the layout changes
@@ -742,8 +750,13 @@ int stage_image(fx_ctx* c, const fx_image* im, DevImage* d) {
     return FX_OK;
 }
 
-constexpr int kBatchSlots = 128;                 // images per launch set
-constexpr size_t kStageBudget = 64ull << 20;     // staged elements per raster per sub-batch
+// images per launch set: each is one label-table slot (65536 labels x 24 B); the
+// thread-per-ROI passes want many ROIs per launch (C4: 100 per tile)
+#ifndef FXG_BATCH_SLOTS
+#define FXG_BATCH_SLOTS 512
+#endif
+constexpr int kBatchSlots = FXG_BATCH_SLOTS;
+constexpr size_t kStageBudget = (size_t)kBatchSlots << 19;  // staged elements per raster per sub-batch
 
 int ensure_maps(fx_ctx* c, size_t slots, size_t strips) {
     if (slots <= c->map_slots_cap && strips <= c->map_strips_cap) return FX_OK;
