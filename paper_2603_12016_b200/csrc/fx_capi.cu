@@ -29,9 +29,9 @@ __global__ void k_label_scan(const uint16_t* L, int W, int H, size_t pitch, int 
 __global__ void k_compact_count(LabelTable t, Control* ctl, CompactArgs a, int nslots);
 __global__ void k_compact_emit(LabelTable t, Control* ctl, RoiList r, CompactArgs a, SlotMap m);
 cudaError_t roi_s_setup(int* occ /* [3][3]: class x GlcmMode */);
-void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
-                  const CUtensorMap& tmap72, int tma40, int tma72, DevImage img, RoiList rl,
-                  Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg);
+void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap* tmaps, int tma40, int tma72,
+                  DevImage img, RoiList rl, Control* ctl, FeatCfg cfg, double* out,
+                  const DebugOut* dbg);
 cudaError_t roi_b_setup();
 void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
                          double* out);
@@ -389,15 +389,15 @@ int ensure_img(fx_ctx* c, int w, int h) {
     return FX_OK;
 }
 
-bool make_tmap(fx_ctx* c, const DevImage& img, CUtensorMap* m, int box_w) {
+bool make_tmap(fx_ctx* c, const DevImage& img, const uint16_t* raster, CUtensorMap* m, int box_w) {
     if (!c->encode) return false;
-    if ((reinterpret_cast<uintptr_t>(img.L) & 15u) || ((img.pitch * 2) & 15u)) return false;
+    if ((reinterpret_cast<uintptr_t>(raster) & 15u) || ((img.pitch * 2) & 15u)) return false;
     if (img.w < box_w || img.h < 8) return false;
     cuuint64_t dims[2] = {(cuuint64_t)img.w, (cuuint64_t)img.h};
     cuuint64_t strides[1] = {(cuuint64_t)img.pitch * 2};
     cuuint32_t box[2] = {(cuuint32_t)box_w, 8};
     cuuint32_t estr[2] = {1, 1};
-    CUresult r = c->encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (void*)img.L, dims, strides, box,
+    CUresult r = c->encode(m, CU_TENSOR_MAP_DATA_TYPE_UINT16, 2, (void*)raster, dims, strides, box,
                            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS;
@@ -574,18 +574,19 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         *n_rois = c->h_ctl->n_rois;
         return c->h_ctl->n_rois ? vrc : FX_OK;
     }
-    CUtensorMap tmap40, tmap72;
-    std::memset(&tmap40, 0, sizeof tmap40);
-    std::memset(&tmap72, 0, sizeof tmap72);
-    const int tma40 = (!c->no_tma && make_tmap(c, img, &tmap40, kStageW0)) ? 1 : 0;
-    const int tma72 = (!c->no_tma && make_tmap(c, img, &tmap72, kStageW)) ? 1 : 0;
+    CUtensorMap tmaps[4];  // labels / intensities, 40- and 72-wide boxes
+    std::memset(tmaps, 0, sizeof tmaps);
+    const int tma40 = (!c->no_tma && make_tmap(c, img, img.L, &tmaps[0], kStageW0) &&
+                       make_tmap(c, img, img.I, &tmaps[1], kStageW0)) ? 1 : 0;
+    const int tma72 = (!c->no_tma && make_tmap(c, img, img.L, &tmaps[2], kStageW) &&
+                       make_tmap(c, img, img.I, &tmaps[3], kStageW)) ? 1 : 0;
     const int glcm = s_glcm_mode(cfg);
     {
         static const char* names[3] = {"k_roi_s0", "k_roi_s1", "k_roi_s2"};
         for (int cls = kClassS0; cls <= kClassS2; ++cls) {
             Launch l(c, names[cls]);
-            launch_roi_s(cls, c->sm_count * c->occ_s[cls][glcm], s, tmap40, tmap72, tma40, tma72,
-                         img, rl, c->d_ctl, cfg, out_dev, dbg_dev);
+            launch_roi_s(cls, c->sm_count * c->occ_s[cls][glcm], s, tmaps, tma40, tma72, img, rl,
+                         c->d_ctl, cfg, out_dev, dbg_dev);
         }
     }
     CK(cudaGetLastError());

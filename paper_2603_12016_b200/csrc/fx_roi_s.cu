@@ -47,7 +47,7 @@ namespace {
 // ---- slab layout for S windows ---------------------------------------------
 struct SLayout {
     uint32_t rowmask, rowoff, vals, xy;        // region A
-    uint32_t stage;                            // B: load
+    uint32_t stage, stageI;                    // B: load (label and intensity tiles)
     uint32_t tmp, sorted, cnt;                 // B: sort / stats
     uint32_t kmask, emask, runoff, rs, re, parent, rsize;  // B: edge slow path
     uint32_t lvl, keys, keys2, gcnt, marg;     // B: glcm, sort path (ng > 64)
@@ -69,8 +69,12 @@ __host__ __device__ constexpr SLayout make_slayout(uint32_t TW, uint32_t TH, uin
     L.xy = o;
     o = al(o + NMAX * 2, 128);
     const uint32_t B = o;
+    // the intensity tile is staged for the 40-wide S0 windows only: for the 72 x 64
+    // tiles it would double the load region and cost S1/S2 occupancy (measured)
+    const bool stage_i = TW == (uint32_t)kStageW0;
     L.stage = B;
-    const uint32_t e_load = B + TW * TH * 2;
+    L.stageI = stage_i ? B + TW * TH * 2 : 0u;
+    const uint32_t e_load = B + (stage_i ? 2u : 1u) * TW * TH * 2;
     L.tmp = B;
     L.sorted = al(L.tmp + NMAX * 2, 16);
     L.cnt = al(L.sorted + NMAX * 2, 16);
@@ -1277,6 +1281,8 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
         if (fits) mst = cfg.mom_px + off;
     }
     {
+        constexpr bool kSI = TW == kStageW0;  // S0: staged intensity tile, else global gather
+        const uint16_t* Is = (const uint16_t*)(base + L.stageI) + xo;
         const uint16_t* Ib = img.I + (size_t)J.y0 * img.pitch + J.x0;
 #pragma unroll 1
         for (uint32_t b0 = 0; b0 < n; b0 += 32 * 8) {
@@ -1286,7 +1292,8 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
             for (int u = 0; u < 8; ++u) {
                 const uint32_t i = b0 + u * 32 + lane;
                 p[u] = i < n ? xy[i] : 0u;
-                v[u] = i < n ? __ldg(Ib + (size_t)(p[u] >> 8) * img.pitch + (p[u] & 0xffu)) : 0;
+                if (kSI) v[u] = i < n ? Is[(p[u] >> 8) * (uint32_t)TW + (p[u] & 0xffu)] : 0;
+                else v[u] = i < n ? __ldg(Ib + (size_t)(p[u] >> 8) * img.pitch + (p[u] & 0xffu)) : 0;
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
@@ -1930,14 +1937,16 @@ namespace {
 #endif
 template <int CLS, int GLCM>
 __global__ void __launch_bounds__(32, 20)
-    k_roi_s(const __grid_constant__ CUtensorMap tmapL, int use_tma, DevImage img, RoiList rl,
-            Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg) {
+    k_roi_s(const __grid_constant__ CUtensorMap tmapL, const __grid_constant__ CUtensorMap tmapI,
+            int use_tma, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg, double* out,
+            const DebugOut* dbg) {
     using V = SVar<CLS>;
     constexpr SLayout L = slayout<CLS, GLCM>();
     extern __shared__ __align__(128) uint8_t smem_raw[];
     uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L.bytes - 128);
     uint16_t* stage = (uint16_t*)(base + L.stage);
+    uint16_t* stageI = (uint16_t*)(base + L.stageI);
     const unsigned lane = lane_id();
     if (lane == 0) mbar_init(mbar);
     __syncwarp();
@@ -1980,21 +1989,30 @@ __global__ void __launch_bounds__(32, 20)
         if (use_tma) {
             // label window -> staging tile: TWx8 boxes from x0 & ~7 (16 B aligned
             // innermost coordinate, required on sm_100a)
+            // label (and for S0 intensity) windows -> staging tiles, one transaction
+            constexpr bool kSI = V::TW == kStageW0;
             const int nbox = ((int)J.h + 7) >> 3;
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                mbar_expect_tx(mbar, (uint32_t)nbox * (uint32_t)(V::TW * 8 * 2));
-                for (int b = 0; b < nbox; ++b)
+                mbar_expect_tx(mbar, (kSI ? 2u : 1u) * (uint32_t)nbox * (uint32_t)(V::TW * 8 * 2));
+                for (int b = 0; b < nbox; ++b) {
                     tma_load_2d(stage + b * 8 * V::TW, &tmapL, mbar, (int)(J.x0 & ~7u),
                                 (int)J.y0 + b * 8);
+                    if (kSI)
+                        tma_load_2d(stageI + b * 8 * V::TW, &tmapI, mbar, (int)(J.x0 & ~7u),
+                                    (int)J.y0 + b * 8);
+                }
             }
             __syncwarp();
         } else {
-            // plain coalesced loads of the window rows into the staging tile
+            // plain coalesced loads of the window rows into the staging tiles
             const uint32_t xo = J.x0 & 7u;
             for (int y = 0; y < (int)J.h; ++y)
-                for (int x = lane; x < (int)J.w; x += 32)
-                    stage[y * V::TW + xo + x] = img.L[(size_t)(J.y0 + y) * img.pitch + J.x0 + x];
+                for (int x = lane; x < (int)J.w; x += 32) {
+                    const size_t o = (size_t)(J.y0 + y) * img.pitch + J.x0 + x;
+                    stage[y * V::TW + xo + x] = img.L[o];
+                    if (V::TW == kStageW0) stageI[y * V::TW + xo + x] = img.I[o];
+                }
             __syncwarp();
             if (lane == 0)  // complete the phase the TMA path would complete
                 asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
@@ -2017,9 +2035,9 @@ cudaError_t setup_one(int* occ) {
 }
 
 template <int CLS, int G>
-void launch_one(int grid, cudaStream_t s, const CUtensorMap& tm, int use_tma, DevImage img,
-                RoiList rl, Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg) {
-    k_roi_s<CLS, G><<<grid, 32, slayout<CLS, G>().bytes + kSlack, s>>>(tm, use_tma, img, rl, ctl,
+void launch_one(int grid, cudaStream_t s, const CUtensorMap& tm, const CUtensorMap& ti, int use_tma,
+                DevImage img, RoiList rl, Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg) {
+    k_roi_s<CLS, G><<<grid, 32, slayout<CLS, G>().bytes + kSlack, s>>>(tm, ti, use_tma, img, rl, ctl,
                                                                       cfg, out, dbg);
 }
 
@@ -2385,20 +2403,21 @@ void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, Feat
     if (n_s > 0) k_shape_serial<<<(n_s + 127) / 128, 128, 0, s>>>(rl, ctl, cfg, out);
 }
 
-void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap& tmap40,
-                  const CUtensorMap& tmap72, int tma40, int tma72, DevImage img, RoiList rl,
-                  Control* ctl, FeatCfg cfg, double* out, const DebugOut* dbg) {
+void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap* tmaps, int tma40, int tma72,
+                  DevImage img, RoiList rl, Control* ctl, FeatCfg cfg, double* out,
+                  const DebugOut* dbg) {
+    // tmaps: labels / intensities for the 40-wide (S0) and 72-wide (S1, S2) tiles
     const int g = s_glcm_mode(cfg);
-#define FXG_LAUNCH(C, TM, TA)                                                              \
+#define FXG_LAUNCH(C, TM, TI, TA)                                                          \
     do {                                                                                   \
-        if (g == kGlHist) launch_one<C, kGlHist>(grid, s, TM, TA, img, rl, ctl, cfg, out, dbg); \
-        else if (g == kGlSort) launch_one<C, kGlSort>(grid, s, TM, TA, img, rl, ctl, cfg, out, dbg); \
-        else launch_one<C, kGlNone>(grid, s, TM, TA, img, rl, ctl, cfg, out, dbg);      \
+        if (g == kGlHist) launch_one<C, kGlHist>(grid, s, TM, TI, TA, img, rl, ctl, cfg, out, dbg); \
+        else if (g == kGlSort) launch_one<C, kGlSort>(grid, s, TM, TI, TA, img, rl, ctl, cfg, out, dbg); \
+        else launch_one<C, kGlNone>(grid, s, TM, TI, TA, img, rl, ctl, cfg, out, dbg);  \
     } while (0)
     switch (cls) {
-        case kClassS0: FXG_LAUNCH(kClassS0, tmap40, tma40); break;
-        case kClassS1: FXG_LAUNCH(kClassS1, tmap72, tma72); break;
-        default: FXG_LAUNCH(kClassS2, tmap72, tma72); break;
+        case kClassS0: FXG_LAUNCH(kClassS0, tmaps[0], tmaps[1], tma40); break;
+        case kClassS1: FXG_LAUNCH(kClassS1, tmaps[2], tmaps[3], tma72); break;
+        default: FXG_LAUNCH(kClassS2, tmaps[2], tmaps[3], tma72); break;
     }
 #undef FXG_LAUNCH
 }
