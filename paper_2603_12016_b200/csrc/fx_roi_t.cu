@@ -124,7 +124,7 @@ struct TShared {
     uint32_t gl_ext[4 * 65];       // runs per (angle, length 1..64)
     double gl_red[kTW][10];        // per-warp cell sums
     double gl_f[4][16];            // features per angle
-    double gl_rcp2[64];            // 1 / k^2, k = 1..64
+    double gl_rcp2[256];           // 1 / k^2, k = 1..256
     // NGTDM: present levels in order, their p_i and s_i
     uint8_t ng_lev[256];
     double ng_p[256];
@@ -335,16 +335,19 @@ __device__ void glszm_zones(T* par, T* zsz, const uint16_t* lv, int w, int h, ui
     __syncthreads();
 }
 
-// per-unit terms of one run / zone (level g 0-based, extent l), texture.cpp:296-309
-__device__ __forceinline__ void unit_terms(double (&t)[8], int g0, uint32_t l0) {
+// per-unit terms of one run / zone (level g 0-based, extent l), texture.cpp:296-309;
+// rcp2[k] = 1 / (k + 1)^2 for k < 256 (levels always, extents up to 256), so the
+// common case has no fp64 division
+__device__ __forceinline__ void unit_terms(double (&t)[8], int g0, uint32_t l0, const double* rcp2) {
     const double g = g0 + 1, l = (double)l0, g2 = g * g, l2 = l * l;
-    t[0] += 1.0 / l2;
+    const double rg2 = rcp2[g0], rl2 = l0 <= 256u ? rcp2[l0 - 1u] : 1.0 / l2;
+    t[0] += rl2;
     t[1] += l2;
-    t[2] += 1.0 / g2;
+    t[2] += rg2;
     t[3] += g2;
-    t[4] += 1.0 / (g2 * l2);
-    t[5] += g2 / l2;
-    t[6] += l2 / g2;
+    t[4] += rg2 * rl2;
+    t[5] += g2 * rl2;
+    t[6] += l2 * rg2;
     t[7] += g2 * l2;
 }
 
@@ -597,7 +600,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                     nx += dx;
                     ny += dy;
                 }
-                unit_terms(t, (int)g, len);
+                unit_terms(t, (int)g, len, sm.gl_rcp2);
                 ++runs;
                 emax = max(emax, len);
                 atomicAdd(&sm.plev[g], 1u);
@@ -635,7 +638,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
             const uint32_t g = lv[c];
             if (g == kNoLevel || par_at(c) != c) continue;
             const uint32_t size = zsz_at(c);
-            unit_terms(t, (int)g, size);
+            unit_terms(t, (int)g, size, sm.gl_rcp2);
             ++zones;
             emax = max(emax, size);
             atomicAdd(&sm.plev[g], 1u);
@@ -774,7 +777,7 @@ __global__ void __launch_bounds__(kTT, FXG_T_MINB) k_roi_t(DevImage img, RoiList
     S.ext = (uint32_t*)(base + T.ext);
     S.ccnt = (uint32_t*)(base + T.ccnt);
     for (int g = threadIdx.x; g < 256; g += kTT) sm.plev[g] = 0u;
-    for (int k = threadIdx.x; k < 64; k += kTT) sm.gl_rcp2[k] = 1.0 / ((double)(k + 1) * (double)(k + 1));
+    for (int k = threadIdx.x; k < 256; k += kTT) sm.gl_rcp2[k] = 1.0 / ((double)(k + 1) * (double)(k + 1));
     for (int i = threadIdx.x; i < 4096; i += kTT) {
         sm.skey[i] = kEmpty;
         sm.scnt[i] = 0u;
