@@ -372,8 +372,11 @@ __device__ void glrlm_dense(const uint16_t* lv, int w, int h, uint32_t cells, un
     const unsigned tid = threadIdx.x, lane = lane_id(), wp = twarp();
     const int A = cfg.n_angles;
     TT_DECL
-    uint32_t* H = sm.skey;  // word (a * 4096 + g * 64 + l - 1) >> 1, A * 2048 words <= skey + scnt
-    for (uint32_t i = tid; i < (uint32_t)A * 2048u; i += kTT) H[i] = 0u;
+    // word a * kHA + g * 33 + ((l - 1) >> 1): rows of 32 words padded to 33, so the
+    // lanes of the feature scan (lane = level, same word index) hit 32 banks
+    constexpr uint32_t kHA = 64u * 33u;
+    uint32_t* H = sm.skey;  // A * kHA words <= skey + scnt + spar (spar is rebuilt per ROI)
+    for (uint32_t i = tid; i < (uint32_t)A * kHA; i += kTT) H[i] = 0u;
     for (uint32_t i = tid; i < 4u * 64u; i += kTT) sm.gl_plev[i] = 0u;
     for (uint32_t i = tid; i < 4u * 65u; i += kTT) sm.gl_ext[i] = 0u;
     __syncthreads();
@@ -396,33 +399,34 @@ __device__ void glrlm_dense(const uint16_t* lv, int w, int h, uint32_t cells, un
                 nx += dx;
                 ny += dy;
             }
-            const uint32_t e = (uint32_t)a * 4096u + g * 64u + (len - 1u);
-            sred_add(&H[e >> 1], 1u << ((e & 1u) * 16u));
+            sred_add(&H[(uint32_t)a * kHA + g * 33u + ((len - 1u) >> 1)], 1u << (((len - 1u) & 1u) * 16u));
             sred_add(&sm.gl_plev[a * 64 + g], 1u);
             sred_add(&sm.gl_ext[a * 65 + len], 1u);
         }
     }
     __syncthreads();
     TT(4);
-    // cell terms: warps 2a, 2a+1 cover angle a, lane L of the pair owns level L
-    // (counts crowd at short lengths, so level rows balance the lanes); the word
-    // order within a row is rotated by the level so the 32 lanes hit 32 banks
+    // cell terms: warps 2a, 2a+1 cover angle a, lane L of the pair owns level L and
+    // walks its row in length order until all of the level's runs are counted
+    // (counts crowd at short lengths: the warp stops after the longest-run level)
     if (wp < 2u * (unsigned)A) {
         const int a = (int)(wp >> 1);
         const uint32_t gl = (wp & 1u) * 32u + lane;
+        uint32_t rem = gl < 64u ? sm.gl_plev[a * 64 + gl] : 0u;
         double t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // t8, sum c, sum c log2 c
-        for (uint32_t k = 0; k < 32u; ++k) {
-            const uint32_t wd = gl * 32u + ((k + gl) & 31u);
-            const uint32_t word = H[(uint32_t)a * 2048u + wd];
+        for (uint32_t k = 0; k < 32u && __any_sync(kFull, rem != 0u); ++k) {
+            if (!rem) continue;
+            const uint32_t word = H[(uint32_t)a * kHA + gl * 33u + k];
             if (!word) continue;
 #pragma unroll
             for (int half = 0; half < 2; ++half) {
                 const uint32_t c = (word >> (16 * half)) & 0xffffu;
                 if (!c) continue;
-                const uint32_t e = wd * 2u + (uint32_t)half;
-                const double g = (double)(e >> 6) + 1.0, l = (double)(e & 63u) + 1.0;
+                rem -= c;
+                const uint32_t li = k * 2u + (uint32_t)half;  // length - 1
+                const double g = (double)gl + 1.0, l = (double)li + 1.0;
                 const double cc = (double)c, g2 = g * g, l2 = l * l;
-                const double rg2 = sm.gl_rcp2[e >> 6], rl2 = sm.gl_rcp2[e & 63u];  // 1/g^2, 1/l^2
+                const double rg2 = sm.gl_rcp2[gl], rl2 = sm.gl_rcp2[li];  // 1/g^2, 1/l^2
                 t[0] += cc * rl2;
                 t[1] += cc * l2;
                 t[2] += cc * rg2;
