@@ -157,6 +157,9 @@ struct CellDiv {
 __device__ __forceinline__ void sred_add(uint32_t* p, uint32_t v) {
     asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
+__device__ __forceinline__ void sred_add(unsigned long long* p, unsigned long long v) {
+    asm volatile("red.shared.add.u64 [%0], %1;" ::"r"(smem_u32(p)), "l"(v) : "memory");
+}
 
 __device__ __forceinline__ uint32_t thash(uint32_t k) {
     k ^= k >> 16;
@@ -633,6 +636,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
     if (cfg.col_glszm >= 0) {
         if (small) glszm_zones<uint16_t>(sm.spar, sm.szsz, lv, w, h, cells);
         else glszm_zones<uint32_t>(S.par, S.zsz, lv, w, h, cells);
+        TT(7);
         auto par_at = [&](uint32_t c) -> uint32_t { return small ? sm.spar[c] : S.par[c]; };
         auto zsz_at = [&](uint32_t c) -> uint32_t { return small ? sm.szsz[c] : S.zsz[c]; };
         double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -685,8 +689,8 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                 }
             if (!cnt) continue;
             const int d = (int)(g + 1) * cnt - sum;  // |(g+1) - sum/cnt| = |d| / cnt
-            atomicAdd(&sm.sng[g], (unsigned long long)((d < 0 ? -d : d) * (840 / cnt)));
-            atomicAdd(&sm.plev[g], 1u);
+            sred_add(&sm.sng[g], (unsigned long long)((d < 0 ? -d : d) * (840 / cnt)));
+            sred_add(&sm.plev[g], 1u);
             ++valid;
         }
         const unsigned long long nvu = tblock_all(valid, sm.u64, TAdd());
@@ -708,11 +712,17 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
             double a_con = 0, a_busy = 0, a_cplx = 0, a_strn = 0;
             // pairs of present levels only (absent levels contribute nothing):
             // compact list in level order with p_i and s_i computed once
-            if (tid == 0) {
+            if (twarp() == 0) {  // ballot compaction, level order
+                const unsigned ln = lane_id();
                 uint32_t k = 0;
-                for (int i = 0; i < ng; ++i)
-                    if (sm.plev[i]) sm.ng_lev[k++] = (uint8_t)i;
-                sm.ng_np = k;
+                for (int i0 = 0; i0 < ng; i0 += 32) {
+                    const int i = i0 + (int)ln;
+                    const bool pr = i < ng && sm.plev[i] != 0u;
+                    const unsigned b = __ballot_sync(kFull, pr);
+                    if (pr) sm.ng_lev[k + __popc(b & lanemask_lt())] = (uint8_t)i;
+                    k += __popc(b);
+                }
+                if (ln == 0) sm.ng_np = k;
             }
             __syncthreads();
             const uint32_t P = sm.ng_np;

@@ -53,10 +53,10 @@ if totb:
     print(f"large-ROI kernel: {totb / nroi:.0f} clocks per ROI (thread 0)")
     for k, nm in enumerate(BNAMES):
         print(f"  {nm:16s} {buf[9 + k] / nroi:10.0f} clk/ROI  {100 * buf[9 + k] / totb:5.1f}%")
-tt = sum(tbuf[:4])  # slots 4-6 split GLRLM (slot 1)
+tt = sum(tbuf[:4]) + tbuf[7]  # slots 4-6 split GLRLM (slot 1), 7 is GLSZM's zones
 if tt:
     names = ["discretize", "GLRLM other", "GLSZM", "NGTDM", "GLRLM runs", "GLRLM features",
-             "GLRLM restore"]
+             "GLRLM restore", "GLSZM zones"]
     print(f"texture kernel: {tt / nroi:.0f} clocks per ROI (thread 0)")
     for k, nm in enumerate(names):
         print(f"  {nm:16s} {tbuf[k] / nroi:10.0f} clk/ROI  {100 * tbuf[k] / tt:5.1f}%")
