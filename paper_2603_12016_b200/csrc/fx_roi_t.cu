@@ -260,18 +260,33 @@ __device__ void extent_features(const double* t8, unsigned long long nr_u, unsig
 }
 
 // union-find with T-bit cell indices (u16 in shared memory for S windows)
+// union-find loads: the u16 parents live in shared memory (S windows)
+__device__ __forceinline__ uint32_t t_ld(const volatile uint16_t* p) {
+    unsigned short r;
+    asm volatile("ld.volatile.shared.u16 %0, [%1];" : "=h"(r) : "r"(smem_u32((const void*)p)) : "memory");
+    return r;
+}
+__device__ __forceinline__ uint32_t t_ld(const volatile uint32_t* p) { return *p; }
 template <typename T>
 __device__ __forceinline__ uint32_t t_root(const volatile T* par, uint32_t x) {
-    uint32_t p = par[x];
+    uint32_t p = t_ld(par + x);
     while (p != x) {
         x = p;
-        p = par[x];
+        p = t_ld(par + x);
     }
     return x;
 }
+// the u16 instantiation only ever lives in shared memory (S windows): explicit
+// shared-space CAS and loads instead of generic ones
 __device__ __forceinline__ uint32_t t_cas(uint16_t* a, uint32_t cmp, uint32_t val) {
-    return atomicCAS(reinterpret_cast<unsigned short*>(a), (unsigned short)cmp, (unsigned short)val);
+    unsigned short r;
+    asm volatile("atom.shared.cas.b16 %0, [%1], %2, %3;"
+                 : "=h"(r)
+                 : "r"(smem_u32(a)), "h"((unsigned short)cmp), "h"((unsigned short)val)
+                 : "memory");
+    return r;
 }
+
 __device__ __forceinline__ uint32_t t_cas(uint32_t* a, uint32_t cmp, uint32_t val) {
     return atomicCAS(a, cmp, val);
 }
@@ -330,7 +345,7 @@ __device__ void glszm_zones(T* par, T* zsz, const uint16_t* lv, int w, int h, ui
                 // 16-bit atomics: add into the containing word
                 const uint32_t r = par[c];
                 uint32_t* word = reinterpret_cast<uint32_t*>(zsz + (r & ~1u));
-                atomicAdd(word, 1u << ((r & 1u) * 16u));
+                sred_add(word, 1u << ((r & 1u) * 16u));
             } else {
                 atomicAdd(reinterpret_cast<uint32_t*>(&zsz[par[c]]), 1u);
             }
@@ -610,7 +625,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                 unit_terms(t, (int)g, len, sm.gl_rcp2);
                 ++runs;
                 emax = max(emax, len);
-                atomicAdd(&sm.plev[g], 1u);
+                sred_add(&sm.plev[g], 1u);
                 table_add(hk, hcn, mask, (g << 24) | len);
                 atomicAdd(&S.ext[len], 1u);
             }
@@ -649,7 +664,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
             unit_terms(t, (int)g, size, sm.gl_rcp2);
             ++zones;
             emax = max(emax, size);
-            atomicAdd(&sm.plev[g], 1u);
+            sred_add(&sm.plev[g], 1u);
             table_add(hk, hcn, mask, (g << 24) | size);
             atomicAdd(&S.ext[size], 1u);
         }
