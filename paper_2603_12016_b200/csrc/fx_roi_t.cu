@@ -118,6 +118,8 @@ struct TShared {
     double red8[kTW + 1][8];
     unsigned long long u64[kTW + 1];
     uint32_t u32[kTW + 1];
+    double redK[kTW + 1][10];      // tblock_fused
+    uint32_t redM[kTW + 1][2];
     uint32_t job;
     // dense GLRLM (S windows, ng <= 64, <= 4 angles)
     uint32_t gl_plev[4 * 64];      // runs per (angle, level)
@@ -183,6 +185,53 @@ __device__ __forceinline__ void table_add(uint32_t* keys, uint32_t* cnts, uint32
 }
 
 
+// One block pass for K fp64 sums (fixed order: lanes, then warps), one u32 max
+// and one u32 min: 3 barriers instead of 3 per reduced value.
+template <int K>
+__device__ __forceinline__ void tblock_fused(double (&v)[K], uint32_t& mx, uint32_t& mn, TShared& sm) {
+    static_assert(K >= 1 && K <= 10, "K");
+    const unsigned lane = lane_id(), w = twarp();
+#pragma unroll
+    for (int k = 0; k < K; ++k) {
+        double x = v[k];
+#pragma unroll
+        for (int o = 16; o; o >>= 1) x += __shfl_xor_sync(kFull, x, o);
+        v[k] = x;
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+        mn = min(mn, __shfl_xor_sync(kFull, mn, o));
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < K; ++k) sm.redK[w][k] = v[k];
+        sm.redM[w][0] = mx;
+        sm.redM[w][1] = mn;
+    }
+    __syncthreads();
+    const unsigned tid = threadIdx.x;
+    if (tid < (unsigned)K) {
+        double t = 0;
+        for (int i = 0; i < kTW; ++i) t += sm.redK[i][tid];
+        sm.redK[kTW][tid] = t;
+    } else if (tid == 32) {
+        uint32_t a = 0, b = 0xffffffffu;
+        for (int i = 0; i < kTW; ++i) {
+            a = max(a, sm.redM[i][0]);
+            b = min(b, sm.redM[i][1]);
+        }
+        sm.redM[kTW][0] = a;
+        sm.redM[kTW][1] = b;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < K; ++k) v[k] = sm.redK[kTW][k];
+    mx = sm.redM[kTW][0];
+    mn = sm.redM[kTW][1];
+    __syncthreads();
+}
+
 // Features of the (level, extent) cells (glrlm_features texture.cpp:282-341,
 // glszm_features :382-441).  t8: block totals of the 8 per-unit sums (sre, lre,
 // lglre, hglre, srlgle, srhgle, lrlgle, lrhgle numerators); nr units, np pixels.
@@ -224,8 +273,8 @@ __device__ void extent_features(const double* t8, unsigned long long nr_u, unsig
         hk[slot] = kEmpty;
         hc[slot] = 0u;
     }
-    cmax = tblock_all(cmax, sm.u32, TMax());
-    tblock_sum<4>(a, sm.red8);
+    uint32_t unused_min = 0xffffffffu;
+    tblock_fused<4>(a, cmax, unused_min, sm);
     const double glnu = a[0], mu_g = a[1] / nr, rlnu = a[2], mu_l = a[3] / nr;
     // pass B: entropy = sum over cells c (log2 nr - log2 c) / nr, variances
     double b[3] = {0, 0, 0};
@@ -561,7 +610,9 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
             hi = max(hi, v);
         }
     }
-    const uint32_t vmin = tblock_all(lo, sm.u32, TMin()), vmax = tblock_all(hi, sm.u32, TMax());
+    double none[1] = {0.0};
+    tblock_fused<1>(none, hi, lo, sm);
+    const uint32_t vmin = lo, vmax = hi;
     const unsigned long long span = (unsigned long long)(vmax - vmin) + 1ull;
     uint16_t* lv = cells <= 4096u ? sm.slev : S.lev;  // shared memory for S-class windows
     for (uint32_t c = tid; c < cells; c += kTT) {
@@ -630,9 +681,12 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                 atomicAdd(&S.ext[len], 1u);
             }
             TT(4);
-            tblock_sum<8>(t, sm.red8);
-            const unsigned long long nr = tblock_all(runs, sm.u64, TAdd());
-            emax = tblock_all(emax, sm.u32, TMax());
+            double t9[9] = {t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], (double)runs};
+            uint32_t unused_min = 0xffffffffu;
+            tblock_fused<9>(t9, emax, unused_min, sm);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) t[k] = t9[k];
+            const unsigned long long nr = (unsigned long long)t9[8];
             const double* tt = t;
             __shared__ double f16[16];
             extent_features(tt, nr, n, ng, S, hk, hcn, mask + 1u, emax, sm, f16);
@@ -668,10 +722,13 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
             table_add(hk, hcn, mask, (g << 24) | size);
             atomicAdd(&S.ext[size], 1u);
         }
-        tblock_sum<8>(t, sm.red8);
+        double t9[9] = {t[0], t[1], t[2], t[3], t[4], t[5], t[6], t[7], (double)zones};
+        uint32_t unused_min = 0xffffffffu;
+        tblock_fused<9>(t9, emax, unused_min, sm);
+#pragma unroll
+        for (int k = 0; k < 8; ++k) t[k] = t9[k];
         const double* tt = t;
-        const unsigned long long nz = tblock_all(zones, sm.u64, TAdd());
-        emax = tblock_all(emax, sm.u32, TMax());
+        const unsigned long long nz = (unsigned long long)t9[8];
         __shared__ double f16z[16];
         extent_features(tt, nz, n, ng, S, hk, hcn, mask + 1u, emax, sm, f16z);
         __syncthreads();
