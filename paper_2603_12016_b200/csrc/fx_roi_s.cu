@@ -374,16 +374,9 @@ __device__ __forceinline__ const uint16_t* radix_sort16(const uint16_t* src, uin
 // sort.  Returns the sorted buffer and vmin / vmax.  cnt: 512 u32.
 __device__ __forceinline__ const uint16_t* bucket_sort16(const uint16_t* src, uint16_t* tmp,
                                                       uint16_t* dst, uint32_t n, uint32_t* cnt,
-                                                      uint32_t& vmin, uint32_t& vmax) {
+                                                      uint32_t lo, uint32_t hi) {
+    // lo / hi: min and max of the keys (the gather computes them)
     const unsigned lane = lane_id();
-    uint32_t lo = 0xffffu, hi = 0;
-    for (uint32_t i = lane; i < n; i += 32) {
-        const uint32_t v = src[i];
-        lo = min(lo, v);
-        hi = max(hi, v);
-    }
-    vmin = lo = warp_min(lo);
-    vmax = hi = warp_max(hi);
     const uint32_t r = hi - lo;
     if (n == 0 || r == 0) return src;  // all keys equal: already sorted
     const int s = max(0, 23 - __clz(r));  // (r >> s) < 512
@@ -423,10 +416,11 @@ __device__ __forceinline__ const uint16_t* bucket_sort16(const uint16_t* src, ui
         const uint32_t v = tmp[i], b = (v - lo) >> s;
         const uint32_t st = b ? cnt[slot(b - 1)] : 0u, en = cnt[slot(b)];
         uint32_t rank = 0;
-        for (uint32_t j = st; j < en; ++j) {
-            const uint32_t u = tmp[j];
-            rank += (u < v) | ((u == v) & (j < i));
-        }
+        if (en - st > 1u)  // singleton buckets (most, at ~n/512 keys per bucket) skip the walk
+            for (uint32_t j = st; j < en; ++j) {
+                const uint32_t u = tmp[j];
+                rank += (u < v) | ((u == v) & (j < i));
+            }
         dst[st + rank] = (uint16_t)v;
     }
     __syncwarp();
@@ -1269,7 +1263,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     __syncwarp();
     // gather member intensities (coalesced within rows), exact integer sums
     unsigned long long sS = 0, sQ = 0, sXI = 0, sYI = 0;
-    uint32_t sLX = 0, sLY = 0;
+    uint32_t sLX = 0, sLY = 0, gmin = 0xffffu, gmax = 0u;
     // moments by k_moments_serial: stage this ROI's pixels when the buffer has room
     uint32_t* mst = nullptr;
     if (cfg.col_mom >= 0 && cfg.mom_px) {
@@ -1308,9 +1302,13 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
                     sYI += (unsigned long long)((uint32_t)v[u] * y);
                     sLX += x;
                     sLY += y;
+                    gmin = min(gmin, (uint32_t)v[u]);
+                    gmax = max(gmax, (uint32_t)v[u]);
                 }
             }
         }
+        gmin = warp_min(gmin);
+        gmax = warp_max(gmax);
         sS = warp_sum(sS);
         sQ = warp_sum(sQ);
         sXI = warp_sum(sXI);
@@ -1418,10 +1416,9 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
                                          (uint16_t*)(base + L.sorted), n,
                                          (uint32_t*)(base + L.cnt));
 #else
-        uint32_t smin, smax;
         const uint16_t* s = bucket_sort16(vals, (uint16_t*)(base + L.tmp),
                                           (uint16_t*)(base + L.sorted), n,
-                                          (uint32_t*)(base + L.cnt), smin, smax);
+                                          (uint32_t*)(base + L.cnt), gmin, gmax);
 #endif
         __syncwarp();
         PT(1);
