@@ -71,10 +71,10 @@ def test_batch_vs_oracle(ctx, oracle):
 
 @pytest.mark.gpu
 def test_batch_more_than_one_launch_set(ctx):
-    """300 images > 128 slots: three sub-batches, staged double-buffered."""
+    """1,100 images > 512 slots: three sub-batches, staged double-buffered."""
     import paper_2603_12016_b200 as fx
     p = fx.resolve_profile("performance")
-    specs = [(48 + (k % 5) * 16, 40 + (k % 7) * 8, 1 + k % 6) for k in range(300)]
+    specs = [(48 + (k % 5) * 16, 40 + (k % 7) * 8, 1 + k % 6) for k in range(1100)]
     pairs = _pairs(specs, seed=21)
     res = ctx.featurize_batch(pairs, GROUPS, p)
     _check_same(ctx, pairs, res, p)
