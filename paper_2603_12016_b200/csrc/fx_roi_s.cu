@@ -2276,6 +2276,9 @@ __device__ void intensity_serial(uint32_t t, const RoiList& rl, Control* ctl, co
         return b < nb32 - 1 ? b : nb32 - 1;
     };
     const double logn = nlog2(dn);
+    // integer thresholds for the integer values: v < mean <=> v < ceil(mean);
+    // p10 <= v <= p90 <=> ceil(p10) <= v <= floor(p90) (exact: v < 2^16)
+    const uint32_t t_mean = (uint32_t)ceil(mean), t_lo = (uint32_t)ceil(p10), t_hi = (uint32_t)floor(p90);
     double a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, ent = 0;
     unsigned long long best = 0, slo = 0, rsum = 0, usq = 0;
     uint32_t clo = 0, rn = 0, run_v = 0, run_b = 0, pv_ = s[0], pb_ = bin_of(s[0]);
@@ -2293,12 +2296,11 @@ __device__ void intensity_serial(uint32_t t, const RoiList& rl, Control* ctl, co
             a4 += d2 * d2;
             a5 += d2 * d2 * d;
             a6 += d2 * d2 * d2;
-            if ((double)v < mean) {
+            if (v < t_mean) {
                 slo += v;
                 ++clo;
             }
-            const double x = (double)v;
-            if (x >= p10 && x <= p90) {
+            if (v >= t_lo && v <= t_hi) {
                 rsum += v;
                 ++rn;
             }
@@ -2336,10 +2338,13 @@ __device__ void intensity_serial(uint32_t t, const RoiList& rl, Control* ctl, co
         const double rmean = (double)rsum / (double)rn;
         unsigned long long rlo = 0;
         uint32_t rcl = 0;
+        // values sorted: the [p10, p90] subset below rmean is one contiguous range
+        const uint32_t t_rm = (uint32_t)ceil(rmean);
         for (uint32_t i = 0; i < n; ++i) {
-            const double x = (double)s[i];
-            if (x >= p10 && x <= p90 && x < rmean) {
-                rlo += s[i];
+            const uint32_t v = s[i];
+            if (v >= t_rm) break;
+            if (v >= t_lo && v <= t_hi) {
+                rlo += v;
                 ++rcl;
             }
         }
