@@ -1204,6 +1204,9 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     PT_DECL
     mbar_wait(mbar, phase);
     phase ^= 1u;
+#ifdef FXG_PT_MBAR
+    PT(4);  // phase-timing probe: the TMA wait alone (slot 4 is idle without GLCM)
+#endif
     // row masks: lane y reads its staged row 8 labels at a time (16 B LDS)
     uint64_t m0 = 0, m1 = 0;  // rows lane, lane + 32
 #pragma unroll 1
