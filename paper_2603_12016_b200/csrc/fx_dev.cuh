@@ -68,6 +68,12 @@ constexpr int kStageW = 72;
 // S0: small windows (w <= 33, h <= 40) staged in a 40-wide tile -> half the slab
 constexpr int kS0W = 33, kS0H = 40, kStageW0 = 40;
 constexpr int kS1N = 1024;  // max ROI pixels for S1
+// max ROI pixels for S0: sizes the per-warp buffers (vals, xy, sort), so it sets how
+// many S0 warps fit an SM; S0-shaped windows with more pixels go to S1
+#ifndef FXG_S0N
+#define FXG_S0N 768
+#endif
+constexpr int kS0N = FXG_S0N;
 constexpr int kS2N = 4096;  // = kSW*kSH
 constexpr int kS1Runs = 512;
 constexpr int kS2Runs = 2176;  // >= worst case (33 free runs x 64 rows + 64)

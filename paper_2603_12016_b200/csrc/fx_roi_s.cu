@@ -109,20 +109,23 @@ __host__ __device__ constexpr SLayout make_slayout(uint32_t TW, uint32_t TH, uin
     return L;
 }
 
-// window-class variants: stage width, max rows, max pixels, run capacity
+// window-class variants: stage width, max rows, max pixels, run capacity, warps/SM
+#ifndef FXG_S0_MINB
+#define FXG_S0_MINB 20
+#endif
 template <int CLS>
 struct SVar;
 template <>
 struct SVar<kClassS0> {
-    static constexpr int TW = kStageW0, TH = kS0H, NMAX = kS1N, RUNMAX = 256;
+    static constexpr int TW = kStageW0, TH = kS0H, NMAX = kS0N, RUNMAX = 256, MINB = FXG_S0_MINB;
 };
 template <>
 struct SVar<kClassS1> {
-    static constexpr int TW = kStageW, TH = kSH, NMAX = kS1N, RUNMAX = 512;
+    static constexpr int TW = kStageW, TH = kSH, NMAX = kS1N, RUNMAX = 512, MINB = 20;
 };
 template <>
 struct SVar<kClassS2> {
-    static constexpr int TW = kStageW, TH = kSH, NMAX = kS2N, RUNMAX = 1024;
+    static constexpr int TW = kStageW, TH = kSH, NMAX = kS2N, RUNMAX = 1024, MINB = 20;
 };
 template <int CLS, int GLCM>
 constexpr SLayout slayout() {
@@ -1936,7 +1939,7 @@ namespace {
 #define FXG_S_PREFETCH 0  // 1: L2 prefetch of the next window (measured slower on C2)
 #endif
 template <int CLS, int GLCM>
-__global__ void __launch_bounds__(32, 20)
+__global__ void __launch_bounds__(32, SVar<CLS>::MINB)
     k_roi_s(const __grid_constant__ CUtensorMap tmapL, const __grid_constant__ CUtensorMap tmapI,
             int use_tma, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg, double* out,
             const DebugOut* dbg) {

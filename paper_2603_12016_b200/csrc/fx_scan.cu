@@ -255,7 +255,7 @@ __global__ void __launch_bounds__(1024) k_compact_count(LabelTable t, Control* c
 
 // class of a window (w x h) with n pixels
 __device__ __forceinline__ int roi_class(uint32_t w, uint32_t h, unsigned long long n) {
-    if (w <= (uint32_t)kS0W && h <= (uint32_t)kS0H && n <= (unsigned long long)kS1N) return kClassS0;
+    if (w <= (uint32_t)kS0W && h <= (uint32_t)kS0H && n <= (unsigned long long)kS0N) return kClassS0;
     if (w <= (uint32_t)kSW && h <= (uint32_t)kSH) return n <= (unsigned long long)kS1N ? kClassS1 : kClassS2;
     return kClassL;
 }
