@@ -2067,13 +2067,17 @@ cudaError_t roi_s_setup(int* occ) {
 // and the origin, eta and Hu; the same formulas as the warp path, scalar and
 // amortised over 32 ROIs per warp.  Binary sums are exact integers (|dx^p dy^q|
 // < 2^32, IMAD.WIDE into int64 on the integer pipe); weighted sums are fp64.
-__device__ void moments_serial(uint32_t t, int grp, const RoiList& rl, Control* ctl,
-                               const FeatCfg& cfg, double* out) {
+// output row of the t-th S-class ROI (S0, then S1, then S2), ~0 past the end
+__device__ __forceinline__ uint32_t s_row_of(uint32_t t, const RoiList& rl, const Control* ctl) {
     const uint32_t n0 = ctl->class_count[kClassS0], n1 = ctl->class_count[kClassS1];
     const uint32_t nt = n0 + n1 + ctl->class_count[kClassS2];
-    if (t >= nt) return;
-    const uint32_t r = t < n0 ? rl.cls_list[kClassS0][t]
-                     : t < n0 + n1 ? rl.cls_list[kClassS1][t - n0] : rl.cls_list[kClassS2][t - n0 - n1];
+    if (t >= nt) return ~0u;
+    return t < n0 ? rl.cls_list[kClassS0][t]
+         : t < n0 + n1 ? rl.cls_list[kClassS1][t - n0] : rl.cls_list[kClassS2][t - n0 - n1];
+}
+
+__device__ void moments_row(uint32_t r, int grp, const RoiList& rl, const FeatCfg& cfg,
+                                         double* out) {
     const unsigned long long off = cfg.mom_off[r];
     if (off == ~0ull) return;  // not staged: the warp path wrote the columns
     const uint32_t n = (uint32_t)rl.n[r];
@@ -2242,13 +2246,8 @@ __device__ uint32_t kth_dev_scan(const uint16_t* s, uint32_t n, uint32_t M2, uin
     return best;
 }
 
-__device__ void intensity_serial(uint32_t t, const RoiList& rl, Control* ctl, const FeatCfg& cfg,
-                                 double* out) {
-    const uint32_t n0 = ctl->class_count[kClassS0], n1 = ctl->class_count[kClassS1];
-    const uint32_t nt = n0 + n1 + ctl->class_count[kClassS2];
-    if (t >= nt) return;
-    const uint32_t r = t < n0 ? rl.cls_list[kClassS0][t]
-                     : t < n0 + n1 ? rl.cls_list[kClassS1][t - n0] : rl.cls_list[kClassS2][t - n0 - n1];
+__device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
+                                           double* out) {
     const unsigned long long off = cfg.int_off[r];
     if (off == ~0ull) return;  // not staged: the warp path wrote the columns
     const uint32_t n = (uint32_t)rl.n[r];
@@ -2388,14 +2387,11 @@ __device__ void intensity_serial(uint32_t t, const RoiList& rl, Control* ctl, co
 __global__ void __launch_bounds__(128, FXG_SERIAL_MINB)
     k_serial_stats(RoiList rl, Control* ctl, FeatCfg cfg, double* out, uint32_t bi, uint32_t bm) {
     const uint32_t b = blockIdx.x;
-#ifdef FXG_SERIAL_ONLY  // register-demand probe of one role (tools only)
-    if (FXG_SERIAL_ONLY == 0) intensity_serial(b * blockDim.x + threadIdx.x, rl, ctl, cfg, out);
-    else moments_serial(b * blockDim.x + threadIdx.x, FXG_SERIAL_ONLY - 1, rl, ctl, cfg, out);
-    return;
-#endif
-    if (b < bi) intensity_serial(b * blockDim.x + threadIdx.x, rl, ctl, cfg, out);
-    else if (b < bi + bm) moments_serial((b - bi) * blockDim.x + threadIdx.x, 0, rl, ctl, cfg, out);
-    else moments_serial((b - bi - bm) * blockDim.x + threadIdx.x, 1, rl, ctl, cfg, out);
+    const uint32_t t = (b < bi ? b : b < bi + bm ? b - bi : b - bi - bm) * blockDim.x + threadIdx.x;
+    const uint32_t r = s_row_of(t, rl, ctl);
+    if (r == ~0u) return;
+    if (b < bi) intensity_row(r, rl, cfg, out);
+    else moments_row(r, b < bi + bm ? 0 : 1, rl, cfg, out);
 }
 
 void launch_serial_stats(int n_s, bool intensity, bool moments, cudaStream_t s, RoiList rl,
