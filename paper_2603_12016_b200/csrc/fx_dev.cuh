@@ -66,7 +66,11 @@ constexpr int kSW = 64, kSH = 64;
 // so the box starts at x0 & ~7 and is 72 wide to cover any 64-wide window.
 constexpr int kStageW = 72;
 // S0: small windows (w <= 33, h <= 40) staged in a 40-wide tile -> half the slab
-constexpr int kS0W = 33, kS0H = 40, kStageW0 = 40;
+// S0 staging tile width (TMA boxes start at x0 & ~7, so windows up to kStageW0 - 7 wide)
+#ifndef FXG_STAGEW0
+#define FXG_STAGEW0 40
+#endif
+constexpr int kStageW0 = FXG_STAGEW0, kS0W = kStageW0 - 7, kS0H = 40;
 constexpr int kS1N = 1024;  // max ROI pixels for S1
 // max ROI pixels for S0: sizes the per-warp buffers (vals, xy, sort), so it sets how
 // many S0 warps fit an SM; S0-shaped windows with more pixels go to S1
