@@ -113,7 +113,7 @@ struct TSlab {
 
 struct TShared {
     uint32_t plev[256];            // runs / zones per level; NGTDM pixels per level
-    unsigned long long sng[256];   // NGTDM 840 * sum |(g+1) - mean| per level
+    unsigned long long* sng;       // [256] NGTDM 840 * sum |(g+1) - mean| per level (dynamic)
     double red[kTW + 1];
     double red8[kTW + 1][8];
     unsigned long long u64[kTW + 1];
@@ -127,19 +127,26 @@ struct TShared {
     double gl_red[kTW][10];        // per-warp cell sums
     double gl_f[4][16];            // features per angle
     double gl_rcp2[256];           // 1 / k^2, k = 1..256
-    // NGTDM: present levels in order, their p_i and s_i
-    uint8_t ng_lev[256];
-    double ng_p[256];
-    double ng_s[256];
+    // NGTDM: present levels in order, their p_i and s_i (dynamic, after GLSZM)
+    uint8_t* ng_lev;
+    double* ng_p;
+    double* ng_s;
     uint32_t ng_np;
-    // dynamic shared memory (kDynBytes), S-class windows:
+    // dynamic shared memory (kDynBytes): the S-window level raster, then one 33 KB
+    // region used by phase: GLSZM (count table of 2048 slots, u16 parents, u16
+    // zone sizes), dense GLRLM counts (4 angles x 64 levels x 33 words), NGTDM
+    // per-level arrays (after GLSZM).  2048 slots hold every distinct (level,
+    // extent) key of a window with n <= 4096 pixels and ng <= 256: taking the
+    // smallest extents, ng k (k + 1) / 2 <= n allows at most ~1,322 keys.
     uint16_t* slev;                // [4096] level raster
-    uint32_t* skey;                // [4096] (level, extent) keys   } distinct keys <=
-    uint32_t* scnt;                // [4096] counts                 } units <= pixels
+    uint32_t* skey;                // [2048] (level, extent) keys   } kept empty
+    uint32_t* scnt;                // [2048] counts                 } between uses
     uint16_t* spar;                // [4096] GLSZM union-find parents (cell index)
     uint16_t* szsz;                // [4096] flatten scratch, then zone sizes
 };
-constexpr size_t kDynBytes = 4096 * 2 + 2 * 4096 * 4 + 2 * 4096 * 2;
+constexpr uint32_t kTSlots = 2048;
+constexpr size_t kRegionBytes = 64 * 33 * 4 * 4;  // dense GLRLM, >= 32 KB of GLSZM arrays
+constexpr size_t kDynBytes = 4096 * 2 + kRegionBytes;
 
 // x, y of cell c of a row-major window of width w without an integer division:
 // m = ceil(2^32 / w) gives floor(c / w) or one more (c < 2^32), fixed by one step
@@ -442,7 +449,7 @@ __device__ void glrlm_dense(const uint16_t* lv, int w, int h, uint32_t cells, un
     // word a * kHA + g * 33 + ((l - 1) >> 1): rows of 32 words padded to 33, so the
     // lanes of the feature scan (lane = level, same word index) hit 32 banks
     constexpr uint32_t kHA = 64u * 33u;
-    uint32_t* H = sm.skey;  // A * kHA words <= skey + scnt + spar (spar is rebuilt per ROI)
+    uint32_t* H = sm.skey;  // A * kHA words <= the dynamic region (GLSZM rebuilds its arrays)
     for (uint32_t i = tid; i < (uint32_t)A * kHA; i += kTT) H[i] = 0u;
     for (uint32_t i = tid; i < 4u * 64u; i += kTT) sm.gl_plev[i] = 0u;
     for (uint32_t i = tid; i < 4u * 65u; i += kTT) sm.gl_ext[i] = 0u;
@@ -574,7 +581,7 @@ __device__ void glrlm_dense(const uint16_t* lv, int w, int h, uint32_t cells, un
     }
     TT(5);
     // the hash table (skey / scnt) is kept empty between uses
-    for (uint32_t i = tid; i < 4096u; i += kTT) {
+    for (uint32_t i = tid; i < kTSlots; i += kTT) {
         sm.skey[i] = kEmpty;
         sm.scnt[i] = 0u;
     }
@@ -633,7 +640,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
     const bool small = cells <= 4096u && n <= 4096ull;
     uint32_t* hk = small ? sm.skey : S.hjk;
     uint32_t* hcn = small ? sm.scnt : S.hjc;
-    const uint32_t mask = small ? 4095u : HC - 1u;
+    const uint32_t mask = small ? kTSlots - 1u : HC - 1u;
     auto lev = [&](int x, int y) -> uint32_t {
         return (x >= 0 && x < w && y >= 0 && y < h) ? lv[(uint32_t)y * (uint32_t)w + (uint32_t)x]
                                                     : (uint32_t)kNoLevel;
@@ -842,17 +849,24 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
 
 // which = 0: the S-class lists (windows <= 64 x 64); 1: the large-ROI list
 #ifndef FXG_T_MINB
-#define FXG_T_MINB 3
+#define FXG_T_MINB 4
 #endif
 __global__ void __launch_bounds__(kTT, FXG_T_MINB) k_roi_t(DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                                                double* out, uint8_t* scratch, TLayout T, int which) {
     __shared__ TShared sm;
     extern __shared__ __align__(16) uint8_t tdyn[];
     sm.slev = reinterpret_cast<uint16_t*>(tdyn);
-    sm.skey = reinterpret_cast<uint32_t*>(tdyn + 4096 * 2);
-    sm.scnt = sm.skey + 4096;
-    sm.spar = reinterpret_cast<uint16_t*>(sm.scnt + 4096);
+    uint8_t* region = tdyn + 4096 * 2;
+    sm.skey = reinterpret_cast<uint32_t*>(region);
+    sm.scnt = sm.skey + kTSlots;
+    sm.spar = reinterpret_cast<uint16_t*>(sm.scnt + kTSlots);
     sm.szsz = sm.spar + 4096;
+    // NGTDM arrays over the GLSZM parents / sizes (dead by then), never over the
+    // count table (kept empty between ROIs)
+    sm.sng = reinterpret_cast<unsigned long long*>(sm.spar);
+    sm.ng_p = reinterpret_cast<double*>(sm.sng + 256);
+    sm.ng_s = sm.ng_p + 256;
+    sm.ng_lev = reinterpret_cast<uint8_t*>(sm.ng_s + 256);
     uint8_t* base = scratch + (size_t)blockIdx.x * T.bytes;
     TSlab S;
     S.lev = (uint16_t*)(base + T.lev);
@@ -864,7 +878,7 @@ __global__ void __launch_bounds__(kTT, FXG_T_MINB) k_roi_t(DevImage img, RoiList
     S.ccnt = (uint32_t*)(base + T.ccnt);
     for (int g = threadIdx.x; g < 256; g += kTT) sm.plev[g] = 0u;
     for (int k = threadIdx.x; k < 256; k += kTT) sm.gl_rcp2[k] = 1.0 / ((double)(k + 1) * (double)(k + 1));
-    for (int i = threadIdx.x; i < 4096; i += kTT) {
+    for (uint32_t i = threadIdx.x; i < kTSlots; i += kTT) {
         sm.skey[i] = kEmpty;
         sm.scnt[i] = 0u;
     }
