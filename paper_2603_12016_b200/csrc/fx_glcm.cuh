@@ -63,18 +63,20 @@ __device__ __forceinline__ void haralick_finish(const uint32_t* px, const uint32
     const double iT = 1.0 / T;
     const double asm2 = (double)s2 / (T * T), acor_ = (double)sa * iT;
     const double ent_ = el * iT, jmax = (double)jm * iT;
-    // marginals -> means, entropies (p log p from integer counts); p = m / T by a
-    // correctly rounded division: a marginal on one level is exactly 1, as in the
-    // reference, so its variance is exactly 0
+    // marginals -> means, entropies (p log p from integer counts); p = m / T as
+    // m * (1 / T) except m == T, which gives exactly 1 as the reference's division
+    // does (a marginal on one level must have variance exactly 0); elsewhere the
+    // two differ by at most one ulp
+    auto pr = [&](uint32_t m) -> double { return (double)m == T ? 1.0 : (double)m * iT; };
     double r8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // mux, muy, sumave, sument, difave, hx, hy
     for (int g = lane; g < ng; g += 32) {  // symmetric: p_y == p_x
         const uint32_t ma = px[g];
-        const double pa = (double)ma / T;
+        const double pa = pr(ma);
         r8[0] += (g + 1) * pa;
         if (ma) r8[5] -= pa * (log2_int(ma) - logT);
         if (!sym) {
             const uint32_t mb = py[g];
-            const double pb = (double)mb / T;
+            const double pb = pr(mb);
             r8[1] += (g + 1) * pb;
             if (mb) r8[6] -= pb * (log2_int(mb) - logT);
         }
@@ -82,31 +84,31 @@ __device__ __forceinline__ void haralick_finish(const uint32_t* px, const uint32
     for (int k = lane; k < 2 * ng - 1; k += 32) {
         const uint32_t m = psum[k];
         if (m) {
-            const double p = (double)m / T;
+            const double p = pr(m);
             r8[2] += (k + 2) * p;
             r8[3] -= p * (log2_int(m) - logT);
         }
     }
     for (int d = lane; d < ng; d += 32) {
         const uint32_t m = pdif[d];
-        if (m) r8[4] += d * ((double)m / T);
+        if (m) r8[4] += d * pr(m);
     }
     warp_sum8(r8);
     const double mux = r8[0], muy = sym ? r8[0] : r8[1], sumave = r8[2], sument = r8[3];
     const double difave = r8[4], hx = r8[5], hy = sym ? r8[5] : r8[6];
     double s8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // vx, vy, sumvar, clut, clus, clup, difent
     for (int g = lane; g < ng; g += 32) {
-        const double a1 = (double)px[g] / T;
+        const double a1 = pr(px[g]);
         s8[0] += (g + 1 - mux) * (g + 1 - mux) * a1;
         if (!sym) {
-            const double b1 = (double)py[g] / T;
+            const double b1 = pr(py[g]);
             s8[1] += (g + 1 - muy) * (g + 1 - muy) * b1;
         }
     }
     for (int k = lane; k < 2 * ng - 1; k += 32) {
         const uint32_t m = psum[k];
         if (m) {
-            const double p = (double)m / T;
+            const double p = pr(m);
             s8[2] += (k + 2 - sumave) * (k + 2 - sumave) * p;
             const double sv = k + 2 - mux - muy;
             s8[3] += sv * sv * p;
@@ -119,7 +121,7 @@ __device__ __forceinline__ void haralick_finish(const uint32_t* px, const uint32
     for (int d = lane; d < ng; d += 32) {
         const uint32_t m = pdif[d];
         if (m) {
-            const double p = (double)m / T, dd = (double)d;
+            const double p = pr(m), dd = (double)d;
             d8[0] -= p * (log2_int(m) - logT);
             d8[1] += dd * dd * p;
             d8[2] += p * __ldg(&g_rcp_tab[0][d]);  // 1 / (1 + d^2)
