@@ -866,6 +866,17 @@ __global__ void __launch_bounds__(128) k_shape_serial(RoiList rl, Control* ctl, 
 // ASM, autocorrelation and max probability from exact integer sums, entropy from
 // one fp64 sum of c*log2(c), marginals by shared atomics; Haralick statistics
 // from the integer marginals (texture.cpp:87-217; hxy1 == hxy2 == hx + hy).
+// shared-memory atomics through explicit shared addresses (the slab pointers a
+// noinline phase receives are generic and would compile to generic ATOM)
+__device__ __forceinline__ uint32_t satom_add(uint32_t* p, uint32_t v) {
+    uint32_t old;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(old) : "r"(smem_u32(p)), "r"(v) : "memory");
+    return old;
+}
+__device__ __forceinline__ void sred_add(uint32_t* p, uint32_t v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
+}
+
 __device__ __noinline__ void glcm_phase_h(uint32_t n, int h, const uint64_t* rowmask,
                                           const uint16_t* xy, const uint16_t* vals,
                                           uint8_t* lmap, uint32_t* hist, uint32_t* marg,
@@ -917,7 +928,7 @@ __device__ __noinline__ void glcm_phase_h(uint32_t n, int h, const uint64_t* row
                     const uint32_t la = lmap[y * 64 + x], lb = lmap[ny * 64 + nx];
                     key = sym ? min(la, lb) * 64u + max(la, lb) : la * 64u + lb;
                     const uint32_t sh = (key & 1u) * 16u;
-                    const uint32_t old = atomicAdd(&hist[key >> 1], 1u << sh);
+                    const uint32_t old = satom_add(&hist[key >> 1], 1u << sh);
                     fresh = ((old >> sh) & 0xffffu) == 0u;
                 }
             }
@@ -925,7 +936,7 @@ __device__ __noinline__ void glcm_phase_h(uint32_t n, int h, const uint64_t* row
             const unsigned fm = __ballot_sync(kFull, fresh);
             if (fm) {
                 uint32_t base = 0;
-                if (lane == 0) base = atomicAdd(&marg[320], (uint32_t)__popc(fm));
+                if (lane == 0) base = satom_add(&marg[320], (uint32_t)__popc(fm));
                 base = __shfl_sync(kFull, base, 0);
                 if (fresh) list[base + __popc(fm & lanemask_lt())] = (uint16_t)key;
             }
@@ -956,11 +967,11 @@ __device__ __noinline__ void glcm_phase_h(uint32_t n, int h, const uint64_t* row
                 sa += (unsigned long long)((ga + 1) * (gb + 1)) * mcc;
                 jm = max(jm, cc);
                 el += (double)mcc * (logT - log2_int(cc));  // exactly 0 for a single cell
-                atomicAdd(&px[ga], cc);
-                if (off) atomicAdd(&px[gb], cc);
-                if (!sym) atomicAdd(&py[gb], cc);
-                atomicAdd(&psum[ga + gb], mcc);
-                atomicAdd(&pdif[ga > gb ? ga - gb : gb - ga], mcc);
+                sred_add(&px[ga], cc);
+                if (off) sred_add(&px[gb], cc);
+                if (!sym) sred_add(&py[gb], cc);
+                sred_add(&psum[ga + gb], mcc);
+                sred_add(&pdif[ga > gb ? ga - gb : gb - ga], mcc);
                 if (dbg && dbg->glcm) {
                     dbg->glcm[((size_t)a * ng + ga) * ng + gb] = cc;
                     if (off) dbg->glcm[((size_t)a * ng + gb) * ng + ga] = cc;
@@ -1946,7 +1957,10 @@ __global__ void __launch_bounds__(32, SVar<CLS>::MINB)
     using V = SVar<CLS>;
     constexpr SLayout L = slayout<CLS, GLCM>();
     extern __shared__ __align__(128) uint8_t smem_raw[];
-    uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 127) & ~(uintptr_t)127);
+    // 128 B aligned slab base by pointer arithmetic on the shared array, so the
+    // inlined phases keep the shared address space (LDS / STS / ATOMS); an
+    // integer round trip through uintptr_t made every access generic
+    uint8_t* base = smem_raw + ((128u - (smem_u32(smem_raw) & 127u)) & 127u);
     uint64_t* mbar = reinterpret_cast<uint64_t*>(base + L.bytes - 128);
     uint16_t* stage = (uint16_t*)(base + L.stage);
     uint16_t* stageI = (uint16_t*)(base + L.stageI);
