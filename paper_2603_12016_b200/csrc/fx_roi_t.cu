@@ -113,7 +113,6 @@ struct TSlab {
 
 struct TShared {
     uint32_t plev[256];            // runs / zones per level; NGTDM pixels per level
-    unsigned long long* sng;       // [256] NGTDM 840 * sum |(g+1) - mean| per level (dynamic)
     double red[kTW + 1];
     double red8[kTW + 1][8];
     unsigned long long u64[kTW + 1];
@@ -127,10 +126,6 @@ struct TShared {
     double gl_red[kTW][10];        // per-warp cell sums
     double gl_f[4][16];            // features per angle
     double gl_rcp2[256];           // 1 / k^2, k = 1..256
-    // NGTDM: present levels in order, their p_i and s_i (dynamic, after GLSZM)
-    uint8_t* ng_lev;
-    double* ng_p;
-    double* ng_s;
     uint32_t ng_np;
     // dynamic shared memory (kDynBytes): the S-window level raster, then one 33 KB
     // region used by phase: GLSZM (count table of 2048 slots, u16 parents, u16
@@ -138,15 +133,27 @@ struct TShared {
     // per-level arrays (after GLSZM).  2048 slots hold every distinct (level,
     // extent) key of a window with n <= 4096 pixels and ng <= 256: taking the
     // smallest extents, ng k (k + 1) / 2 <= n allows at most ~1,322 keys.
-    uint16_t* slev;                // [4096] level raster
-    uint32_t* skey;                // [2048] (level, extent) keys   } kept empty
-    uint32_t* scnt;                // [2048] counts                 } between uses
-    uint16_t* spar;                // [4096] GLSZM union-find parents (cell index)
-    uint16_t* szsz;                // [4096] flatten scratch, then zone sizes
 };
 constexpr uint32_t kTSlots = 2048;
 constexpr size_t kRegionBytes = 64 * 33 * 4 * 4;  // dense GLRLM, >= 32 KB of GLSZM arrays
 constexpr size_t kDynBytes = 4096 * 2 + kRegionBytes;
+
+// The dynamic shared memory and its views, addressed from the shared symbol itself
+// so every use compiles to shared-space instructions (a pointer kept in a struct is
+// generic): level raster [4096] u16, then the region: count table keys / counts
+// [kTSlots] u32 (kept empty between uses), union-find parents and zone sizes [4096]
+// u16; NGTDM's per-level arrays over the parents / sizes (dead by then); the dense
+// GLRLM counts over the whole region.
+extern __shared__ __align__(16) uint8_t tdyn[];
+__device__ __forceinline__ uint16_t* d_slev() { return reinterpret_cast<uint16_t*>(tdyn); }
+__device__ __forceinline__ uint32_t* d_skey() { return reinterpret_cast<uint32_t*>(tdyn + 4096 * 2); }
+__device__ __forceinline__ uint32_t* d_scnt() { return d_skey() + kTSlots; }
+__device__ __forceinline__ uint16_t* d_spar() { return reinterpret_cast<uint16_t*>(d_scnt() + kTSlots); }
+__device__ __forceinline__ uint16_t* d_szsz() { return d_spar() + 4096; }
+__device__ __forceinline__ unsigned long long* d_sng() { return reinterpret_cast<unsigned long long*>(d_spar()); }
+__device__ __forceinline__ double* d_ngp() { return reinterpret_cast<double*>(d_sng() + 256); }
+__device__ __forceinline__ double* d_ngs() { return d_ngp() + 256; }
+__device__ __forceinline__ uint8_t* d_nglev() { return reinterpret_cast<uint8_t*>(d_ngs() + 256); }
 
 // x, y of cell c of a row-major window of width w without an integer division:
 // m = ceil(2^32 / w) gives floor(c / w) or one more (c < 2^32), fixed by one step
@@ -449,7 +456,7 @@ __device__ void glrlm_dense(const uint16_t* lv, int w, int h, uint32_t cells, un
     // word a * kHA + g * 33 + ((l - 1) >> 1): rows of 32 words padded to 33, so the
     // lanes of the feature scan (lane = level, same word index) hit 32 banks
     constexpr uint32_t kHA = 64u * 33u;
-    uint32_t* H = sm.skey;  // A * kHA words <= the dynamic region (GLSZM rebuilds its arrays)
+    uint32_t* H = d_skey();  // A * kHA words <= the dynamic region (GLSZM rebuilds its arrays)
     for (uint32_t i = tid; i < (uint32_t)A * kHA; i += kTT) H[i] = 0u;
     for (uint32_t i = tid; i < 4u * 64u; i += kTT) sm.gl_plev[i] = 0u;
     for (uint32_t i = tid; i < 4u * 65u; i += kTT) sm.gl_ext[i] = 0u;
@@ -582,13 +589,15 @@ __device__ void glrlm_dense(const uint16_t* lv, int w, int h, uint32_t cells, un
     TT(5);
     // the hash table (skey / scnt) is kept empty between uses
     for (uint32_t i = tid; i < kTSlots; i += kTT) {
-        sm.skey[i] = kEmpty;
-        sm.scnt[i] = 0u;
+        d_skey()[i] = kEmpty;
+        d_scnt()[i] = 0u;
     }
     __syncthreads();
     TT(6);
 }
 
+// SM: the window uses the shared-memory path (cells <= 4096; S-class windows always)
+template <bool SM>
 __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Control* ctl,
                           const FeatCfg& cfg, double* __restrict__ out, const TSlab& S, uint32_t HC,
                           uint32_t NMAX, TShared& sm) {
@@ -621,7 +630,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
     tblock_fused<1>(none, hi, lo, sm);
     const uint32_t vmin = lo, vmax = hi;
     const unsigned long long span = (unsigned long long)(vmax - vmin) + 1ull;
-    uint16_t* lv = cells <= 4096u ? sm.slev : S.lev;  // shared memory for S-class windows
+    uint16_t* lv = SM ? d_slev() : S.lev;  // shared memory for S-class windows
     for (uint32_t c = tid; c < cells; c += kTT) {
         uint16_t l = kNoLevel;
         const size_t o = at(c);
@@ -637,9 +646,9 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
     __syncthreads();
     TT(0);
     // (level, extent) count table: shared memory for S-class windows (kept empty)
-    const bool small = cells <= 4096u && n <= 4096ull;
-    uint32_t* hk = small ? sm.skey : S.hjk;
-    uint32_t* hcn = small ? sm.scnt : S.hjc;
+    constexpr bool small = SM;  // cells <= 4096 (so n <= 4096)
+    uint32_t* hk = small ? d_skey() : S.hjk;
+    uint32_t* hcn = small ? d_scnt() : S.hjc;
     const uint32_t mask = small ? kTSlots - 1u : HC - 1u;
     auto lev = [&](int x, int y) -> uint32_t {
         return (x >= 0 && x < w && y >= 0 && y < h) ? lv[(uint32_t)y * (uint32_t)w + (uint32_t)x]
@@ -710,11 +719,17 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
     TT(1);
     // ---- GLSZM (texture.cpp:343-380): 8-connected zones of equal level
     if (cfg.col_glszm >= 0) {
-        if (small) glszm_zones<uint16_t>(sm.spar, sm.szsz, lv, w, h, cells);
+        if constexpr (SM) glszm_zones<uint16_t>(d_spar(), d_szsz(), lv, w, h, cells);
         else glszm_zones<uint32_t>(S.par, S.zsz, lv, w, h, cells);
         TT(7);
-        auto par_at = [&](uint32_t c) -> uint32_t { return small ? sm.spar[c] : S.par[c]; };
-        auto zsz_at = [&](uint32_t c) -> uint32_t { return small ? sm.szsz[c] : S.zsz[c]; };
+        auto par_at = [&](uint32_t c) -> uint32_t {
+            if constexpr (SM) return d_spar()[c];
+            else return S.par[c];
+        };
+        auto zsz_at = [&](uint32_t c) -> uint32_t {
+            if constexpr (SM) return d_szsz()[c];
+            else return S.zsz[c];
+        };
         double t[8] = {0, 0, 0, 0, 0, 0, 0, 0};
         unsigned long long zones = 0;
         uint32_t emax = 0;
@@ -747,7 +762,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
     if (cfg.col_ngtdm >= 0) {
         for (int g = tid; g < ng; g += kTT) {
             sm.plev[g] = 0u;
-            sm.sng[g] = 0ull;
+            d_sng()[g] = 0ull;
         }
         __syncthreads();
         unsigned long long valid = 0;
@@ -768,7 +783,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                 }
             if (!cnt) continue;
             const int d = (int)(g + 1) * cnt - sum;  // |(g+1) - sum/cnt| = |d| / cnt
-            sred_add(&sm.sng[g], (unsigned long long)((d < 0 ? -d : d) * (840 / cnt)));
+            sred_add(&d_sng()[g], (unsigned long long)((d < 0 ? -d : d) * (840 / cnt)));
             sred_add(&sm.plev[g], 1u);
             ++valid;
         }
@@ -779,7 +794,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
             double a_s = 0, a_ps = 0;
             uint32_t a_pres = 0;
             for (int i = tid; i < ng; i += kTT) {
-                const double p = (double)sm.plev[i] / nv, sv = (double)sm.sng[i] / 840.0;
+                const double p = (double)sm.plev[i] / nv, sv = (double)d_sng()[i] / 840.0;
                 a_pres += p > 0;
                 a_s += sv;
                 a_ps += p * sv;
@@ -798,7 +813,7 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                     const int i = i0 + (int)ln;
                     const bool pr = i < ng && sm.plev[i] != 0u;
                     const unsigned b = __ballot_sync(kFull, pr);
-                    if (pr) sm.ng_lev[k + __popc(b & lanemask_lt())] = (uint8_t)i;
+                    if (pr) d_nglev()[k + __popc(b & lanemask_lt())] = (uint8_t)i;
                     k += __popc(b);
                 }
                 if (ln == 0) sm.ng_np = k;
@@ -806,19 +821,19 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
             __syncthreads();
             const uint32_t P = sm.ng_np;
             for (uint32_t k = tid; k < P; k += kTT) {
-                const int i = sm.ng_lev[k];
-                sm.ng_p[k] = (double)sm.plev[i] / nv;
-                sm.ng_s[k] = (double)sm.sng[i] / 840.0;
+                const int i = d_nglev()[k];
+                d_ngp()[k] = (double)sm.plev[i] / nv;
+                d_ngs()[k] = (double)d_sng()[i] / 840.0;
             }
             __syncthreads();
             // every term is symmetric in (i, j) and 0 for i == j: pairs i < j, doubled
             const unsigned lane = lane_id();
             for (uint32_t ki = twarp(); ki < P; ki += kTW) {
-                const int i = sm.ng_lev[ki];
-                const double pi = sm.ng_p[ki], si = sm.ng_s[ki], gi = i + 1;
+                const int i = d_nglev()[ki];
+                const double pi = d_ngp()[ki], si = d_ngs()[ki], gi = i + 1;
                 for (uint32_t kj = ki + 1 + lane; kj < P; kj += 32) {
-                    const int j = sm.ng_lev[kj];
-                    const double pj = sm.ng_p[kj], sj = sm.ng_s[kj], gj = j + 1;
+                    const int j = d_nglev()[kj];
+                    const double pj = d_ngp()[kj], sj = d_ngs()[kj], gj = j + 1;
                     a_con += pi * pj * (i - j) * (i - j);
                     a_busy += fabs(gi * pi - gj * pj);
                     a_cplx += fabs(gi - gj) * (pi * si + pj * sj) / (pi + pj);
@@ -854,19 +869,6 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
 __global__ void __launch_bounds__(kTT, FXG_T_MINB) k_roi_t(DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                                                double* out, uint8_t* scratch, TLayout T, int which) {
     __shared__ TShared sm;
-    extern __shared__ __align__(16) uint8_t tdyn[];
-    sm.slev = reinterpret_cast<uint16_t*>(tdyn);
-    uint8_t* region = tdyn + 4096 * 2;
-    sm.skey = reinterpret_cast<uint32_t*>(region);
-    sm.scnt = sm.skey + kTSlots;
-    sm.spar = reinterpret_cast<uint16_t*>(sm.scnt + kTSlots);
-    sm.szsz = sm.spar + 4096;
-    // NGTDM arrays over the GLSZM parents / sizes (dead by then), never over the
-    // count table (kept empty between ROIs)
-    sm.sng = reinterpret_cast<unsigned long long*>(sm.spar);
-    sm.ng_p = reinterpret_cast<double*>(sm.sng + 256);
-    sm.ng_s = sm.ng_p + 256;
-    sm.ng_lev = reinterpret_cast<uint8_t*>(sm.ng_s + 256);
     uint8_t* base = scratch + (size_t)blockIdx.x * T.bytes;
     TSlab S;
     S.lev = (uint16_t*)(base + T.lev);
@@ -879,8 +881,8 @@ __global__ void __launch_bounds__(kTT, FXG_T_MINB) k_roi_t(DevImage img, RoiList
     for (int g = threadIdx.x; g < 256; g += kTT) sm.plev[g] = 0u;
     for (int k = threadIdx.x; k < 256; k += kTT) sm.gl_rcp2[k] = 1.0 / ((double)(k + 1) * (double)(k + 1));
     for (uint32_t i = threadIdx.x; i < kTSlots; i += kTT) {
-        sm.skey[i] = kEmpty;
-        sm.scnt[i] = 0u;
+        d_skey()[i] = kEmpty;
+        d_scnt()[i] = 0u;
     }
     __syncthreads();
     const uint32_t n0 = ctl->class_count[kClassS0], n1 = ctl->class_count[kClassS1];
@@ -902,7 +904,11 @@ __global__ void __launch_bounds__(kTT, FXG_T_MINB) k_roi_t(DevImage img, RoiList
             if (threadIdx.x == 0) atomicOr(&ctl->error, kErrCapacity);
             continue;
         }
-        process_t(r, img, rl, ctl, cfg, out, S, T.HC, T.NMAX, sm);
+        // shared-memory path for windows of <= 4096 cells (every S-class window)
+        if ((unsigned long long)rl.w[r] * rl.h[r] <= 4096ull)
+            process_t<true>(r, img, rl, ctl, cfg, out, S, T.HC, T.NMAX, sm);
+        else
+            process_t<false>(r, img, rl, ctl, cfg, out, S, T.HC, T.NMAX, sm);
     }
 }
 
