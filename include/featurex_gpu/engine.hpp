@@ -8,8 +8,9 @@
 // the sm_100a kernels through the C ABI (include/fxg.h); there is no CPU path.
 //
 // Differences (documented in INTEGRATION.md):
-//  - ExtractionConfig::threads / parallel / memory_budget / spill_dir are
-//    validated like the reference but do not change the (device) execution.
+//  - ExtractionConfig::threads / parallel size run()'s host workers (PGM decode,
+//    CSV formatting); memory_budget / spill_dir are validated like the reference
+//    but ROI data stays in HBM (no spill).
 //  - all seven groups (intensity, moments, shape, glcm, glrlm, glszm, ngtdm)
 //    run on the device; texture groups with ng > 256 raise ConfigError (the
 //    device kernels bound grey levels at 256; never a silent CPU fallback).
@@ -124,6 +125,11 @@ std::vector<std::string> feature_columns(const std::vector<std::string>& groups,
 std::vector<double> compute_roi_features(const PixelCloud& cloud,
                                          const std::vector<std::string>& groups,
                                          const TextureParams& params);
+// Extension: compute_roi_features for many clouds in one device pass (row k ==
+// compute_roi_features(clouds[k], ...)); amortises the per-call launch cost.
+std::vector<std::vector<double>> compute_roi_features_batch(const std::vector<PixelCloud>& clouds,
+                                                            const std::vector<std::string>& groups,
+                                                            const TextureParams& params);
 RunSummary run(const ExtractionConfig& config);
 size_t write_csv(const std::vector<std::string>& columns, std::vector<FeatureRow> rows,
                  const std::filesystem::path& path);

@@ -187,6 +187,16 @@ int fx_run(const char* intensity_dir, const char* mask_dir, const char* pattern,
            const char* groups_csv, const char* profile, int threads, int parallel, int device,
            const char* output_path, fx_run_summary* out);
 
+/* Many clouds at once (extension; the reference operator takes one cloud per
+ * call): cloud k is pixels [offsets[k], offsets[k+1]) of xs / ys / intensities;
+ * row k of out ([n_clouds x n_cols]) equals fx_roi_features on cloud k.  The
+ * clouds run as one fx_featurize_batch (one bbox image each), so the per-call
+ * launch and synchronisation cost is paid once. */
+int fx_roi_features_batch(fx_ctx* ctx, const uint32_t* xs, const uint32_t* ys,
+                          const uint16_t* intensities, const size_t* offsets, size_t n_clouds,
+                          unsigned groups, const fx_texture_params* params, double* out,
+                          size_t cap_rows);
+
 /* ---- band sharding (C5: a whole slide split into row bands across GPUs) -----
  * 1. every rank: fx_scan_accumulate(own band, reset=1)  -> partial label table in
  *    GLOBAL coordinates (origin_x/origin_y of the band image);

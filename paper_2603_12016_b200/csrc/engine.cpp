@@ -487,6 +487,31 @@ std::vector<double> compute_roi_features(const PixelCloud& cloud,
     return out;
 }
 
+std::vector<std::vector<double>> compute_roi_features_batch(const std::vector<PixelCloud>& clouds,
+                                                            const std::vector<std::string>& groups,
+                                                            const TextureParams& params) {
+    const fx_texture_params t = to_c(params);
+    const unsigned m = group_mask(groups);
+    const size_t ncol = feature_columns(groups, params).size();
+    std::vector<size_t> offsets(clouds.size() + 1, 0);
+    for (size_t k = 0; k < clouds.size(); ++k) offsets[k + 1] = offsets[k] + clouds[k].count();
+    std::vector<uint32_t> xs(offsets.back()), ys(offsets.back());
+    std::vector<uint16_t> vs(offsets.back());
+    for (size_t k = 0; k < clouds.size(); ++k)
+        for (size_t i = 0; i < clouds[k].count(); ++i) {
+            xs[offsets[k] + i] = clouds[k].pixels[i].x;
+            ys[offsets[k] + i] = clouds[k].pixels[i].y;
+            vs[offsets[k] + i] = clouds[k].pixels[i].intensity;
+        }
+    std::vector<double> flat(std::max<size_t>(clouds.size() * ncol, 1));
+    check(fx_roi_features_batch(context(0), xs.data(), ys.data(), vs.data(), offsets.data(),
+                                clouds.size(), m, &t, flat.data(), clouds.size()));
+    std::vector<std::vector<double>> out(clouds.size());
+    for (size_t k = 0; k < clouds.size(); ++k)
+        out[k].assign(flat.begin() + k * ncol, flat.begin() + (k + 1) * ncol);
+    return out;
+}
+
 FeatureTable featurize(const IntensityImage& image, const LabelMask& mask,
                        const std::vector<std::string>& groups, const TextureParams& params,
                        int device) {

@@ -1339,6 +1339,65 @@ int fx_roi_features(fx_ctx* c, const uint32_t* xs, const uint32_t* ys, const uin
     return FX_OK;
 }
 
+int fx_roi_features_batch(fx_ctx* c, const uint32_t* xs, const uint32_t* ys, const uint16_t* is,
+                          const size_t* offsets, size_t n_clouds, unsigned groups,
+                          const fx_texture_params* p, double* out, size_t cap_rows) {
+    if (!c || !p || !offsets || (n_clouds && !out)) return set_error(FX_E_ARG, "null argument");
+    int rc = check_groups(groups);
+    if (rc) return rc;
+    const FeatCfg cfg = make_cfg(groups, *p);
+    if (cap_rows < n_clouds) return set_error(FX_E_CAPACITY, "output rows < clouds");
+    const size_t nc = (size_t)cfg.ncols;
+    // each non-empty cloud becomes its own bbox image (label 1, origin at the bbox
+    // corner), all of them in one fx_featurize_batch call
+    std::vector<size_t> which;  // cloud of each image
+    std::vector<std::vector<uint16_t>> rI, rL;
+    std::vector<fx_image> ims;
+    for (size_t k = 0; k < n_clouds; ++k) {
+        const size_t a = offsets[k], b = offsets[k + 1];
+        if (b < a) return set_error(FX_E_ARG, "offsets not ascending");
+        if (a == b) {  // empty cloud: zeros (engine.cpp:138-209)
+            std::fill(out + k * nc, out + (k + 1) * nc, 0.0);
+            continue;
+        }
+        if (!xs || !ys || !is) return set_error(FX_E_ARG, "null argument");
+        uint32_t x0 = xs[a], x1 = xs[a], y0 = ys[a], y1 = ys[a];
+        for (size_t i = a; i < b; ++i) {
+            x0 = std::min(x0, xs[i]);
+            x1 = std::max(x1, xs[i]);
+            y0 = std::min(y0, ys[i]);
+            y1 = std::max(y1, ys[i]);
+        }
+        const int w = (int)(x1 - x0 + 1), h = (int)(y1 - y0 + 1);
+        rI.emplace_back((size_t)w * h, (uint16_t)0);
+        rL.emplace_back((size_t)w * h, (uint16_t)0);
+        for (size_t i = a; i < b; ++i) {
+            const size_t q = (size_t)(ys[i] - y0) * w + (xs[i] - x0);
+            rI.back()[q] = is[i];
+            rL.back()[q] = 1;
+        }
+        which.push_back(k);
+        ims.push_back(fx_image{nullptr, nullptr, w, h, (size_t)w, (int)x0, (int)y0, FX_MEM_HOST});
+    }
+    if (which.empty()) return FX_OK;
+    for (size_t j = 0; j < ims.size(); ++j) {  // raster storage is stable now
+        ims[j].intensity = rI[j].data();
+        ims[j].labels = rL[j].data();
+    }
+    std::vector<uint32_t> labs(which.size());
+    std::vector<double> vals(which.size() * nc);
+    std::vector<size_t> offs(which.size() + 1);
+    rc = fx_featurize_batch(c, ims.data(), (int)ims.size(), groups, p, labs.data(), vals.data(),
+                            which.size(), offs.data());
+    if (rc) return rc;
+    for (size_t j = 0; j < which.size(); ++j) {
+        if (offs[j + 1] - offs[j] != 1)
+            return set_error(FX_E_INTERNAL, "a rasterized cloud did not yield one ROI");
+        std::copy(vals.begin() + offs[j] * nc, vals.begin() + (offs[j] + 1) * nc, out + which[j] * nc);
+    }
+    return FX_OK;
+}
+
 int fx_roi_table(fx_ctx* c, const fx_image* im, uint32_t* out_labels, uint64_t* out_count,
                  uint32_t* out_bbox, size_t cap, size_t* n_rois) {
     if (!c || !im || !n_rois) return set_error(FX_E_ARG, "null argument");

@@ -300,6 +300,24 @@ class Context:
                                      C.byref(params), _p(out, C.c_double), C.c_size_t(len(out))))
         return out[:ncols]
 
+    def roi_features_batch(self, clouds, groups=("intensity",), params=None):
+        """fx_roi_features_batch: clouds = [(xs, ys, vs), ...]; returns [n, n_cols]."""
+        params = params or resolve_profile("default")
+        mask = groups if isinstance(groups, int) else resolve_groups(list(groups))
+        ncols = len(feature_columns(mask, params))
+        sizes = [len(c[0]) for c in clouds]
+        offs = np.zeros(len(clouds) + 1, dtype=np.uint64)
+        offs[1:] = np.cumsum(sizes)
+        cat = lambda i, t: (np.concatenate([np.asarray(c[i], t) for c in clouds])
+                            if clouds else np.zeros(0, t))
+        xs, ys, vs = cat(0, np.uint32), cat(1, np.uint32), cat(2, np.uint16)
+        out = np.zeros((len(clouds), ncols))
+        _check(lib().fx_roi_features_batch(self.h, _p(xs, C.c_uint32), _p(ys, C.c_uint32),
+                                           _p(vs, C.c_uint16), _p(offs, C.c_size_t),
+                                           C.c_size_t(len(clouds)), C.c_uint(mask), C.byref(params),
+                                           _p(out, C.c_double), C.c_size_t(len(clouds))))
+        return out
+
     def roi_table(self, intensity, labels, origin=(0, 0)):
         intensity = np.ascontiguousarray(intensity, dtype=np.uint16)
         labels = np.ascontiguousarray(labels, dtype=np.uint16)

@@ -278,3 +278,28 @@ def test_large_rois_deterministic(ctx):
     for _ in range(4):
         b = ctx.featurize(I, L, GROUPS)
         assert np.array_equal(a[1], b[1])
+
+
+def test_roi_features_batch_equals_per_cloud(ctx):
+    """fx_roi_features_batch (one device pass for many clouds) == one
+    fx_roi_features call per cloud, bit for bit: small, empty, single-pixel and
+    large-window (L path) clouds, several launch sets."""
+    rng = np.random.default_rng(9)
+    clouds = []
+    for k in range(700):
+        r = 2 + k % 11
+        yy, xx = np.nonzero(np.hypot(*np.mgrid[-r:r + 1, -r:r + 1]) <= r)
+        keep = rng.random(len(xx)) < 0.85
+        xs = (xx[keep] + 50 + 3 * k).astype(np.uint32)
+        ys = (yy[keep] + 20 + k).astype(np.uint32)
+        clouds.append((xs, ys, rng.integers(0, 65536, len(xs)).astype(np.uint16)))
+    clouds[5] = (np.zeros(0, np.uint32), np.zeros(0, np.uint32), np.zeros(0, np.uint16))
+    clouds[6] = (np.array([7], np.uint32), np.array([3], np.uint32), np.array([5], np.uint16))
+    yy, xx = np.nonzero(np.ones((90, 120), bool))
+    clouds[7] = (xx.astype(np.uint32), yy.astype(np.uint32),
+                 rng.integers(0, 4096, len(xx)).astype(np.uint16))
+    for groups in (["intensity", "moments"], ["*ALL*"]):
+        got = ctx.roi_features_batch(clouds, groups)
+        for k in (0, 5, 6, 7, 123, 699):
+            want = ctx.roi_features(*clouds[k], groups)
+            assert np.array_equal(got[k], want, equal_nan=True), (groups, k)
