@@ -265,6 +265,31 @@ static void device_cases() {
         write_csv(feature_columns(c.features, tp), rows, d / "g.csv");
         CHECK(slurp(d / "f.csv") == slurp(d / "g.csv"));
     }
+    {  // batched per-ROI operator (extension) == one compute_roi_features per cloud
+        std::mt19937 g(5);
+        std::vector<PixelCloud> clouds(40);
+        for (size_t k = 0; k < clouds.size(); ++k) {
+            const int r = 2 + static_cast<int>(k % 9);
+            for (int dy = -r; dy <= r; ++dy)
+                for (int dx = -r; dx <= r; ++dx)
+                    if (dx * dx + dy * dy <= r * r && g() % 7)
+                        clouds[k].pixels.push_back({static_cast<uint32_t>(100 + 20 * k + dx),
+                                                    static_cast<uint32_t>(50 + dy),
+                                                    static_cast<uint16_t>(g() % 65536)});
+        }
+        clouds[3].pixels.clear();  // empty cloud: zeros
+        const TextureParams tp = resolve_profile("default");
+        const std::vector<std::string> groups = {"*ALL*"};
+        const auto batch = compute_roi_features_batch(clouds, groups, tp);
+        bool same = batch.size() == clouds.size();
+        for (size_t k = 0; same && k < clouds.size(); ++k) {
+            const auto one = compute_roi_features(clouds[k], groups, tp);
+            same = one.size() == batch[k].size();
+            for (size_t i = 0; same && i < one.size(); ++i)
+                same = one[i] == batch[k][i] || (std::isnan(one[i]) && std::isnan(batch[k][i]));
+        }
+        CHECK(same);
+    }
     {  // pairing errors
         IntensityImage im;
         im.width = 2;
