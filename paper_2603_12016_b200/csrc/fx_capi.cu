@@ -582,17 +582,24 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
     const int tma72 = (!c->no_tma && make_tmap(c, img, img.L, &tmaps[2], kStageW) &&
                        make_tmap(c, img, img.I, &tmaps[3], kStageW)) ? 1 : 0;
     const int glcm = s_glcm_mode(cfg);
+    static const char* names[3] = {"k_roi_s0", "k_roi_s1", "k_roi_s2"};
     {
-        static const char* names[3] = {"k_roi_s0", "k_roi_s1", "k_roi_s2"};
-        for (int cls = kClassS0; cls <= kClassS2; ++cls) {
-            Launch l(c, names[cls]);
-            launch_roi_s(cls, c->sm_count * c->occ_s[cls][glcm], s, tmaps, tma40, tma72, img, rl,
-                         c->d_ctl, cfg, out_dev, dbg_dev);
-        }
+        Launch l(c, names[kClassS0]);
+        launch_roi_s(kClassS0, c->sm_count * c->occ_s[kClassS0][glcm], s, tmaps, tma40, tma72, img, rl,
+                     c->d_ctl, cfg, out_dev, dbg_dev);
     }
     CK(cudaGetLastError());
+    // the class counts arrive while S0 runs; S1 / S2 launch only when they have ROIs
+    // (an empty persistent grid still costs ~7 us)
     CK(cudaEventSynchronize(c->ev_stats));
     const Control hc = *c->h_ctl;
+    for (int cls = kClassS1; cls <= kClassS2; ++cls) {
+        if (hc.class_count[cls] == 0) continue;
+        Launch l(c, names[cls]);
+        launch_roi_s(cls, c->sm_count * c->occ_s[cls][glcm], s, tmaps, tma40, tma72, img, rl,
+                     c->d_ctl, cfg, out_dev, dbg_dev);
+    }
+    CK(cudaGetLastError());
     *n_rois = hc.n_rois;
     if (slot_base) std::memcpy(slot_base, c->h_slot_base, ((size_t)m.nslots + 1) * sizeof(uint32_t));
     if (hc.error & kErrWindow) {
