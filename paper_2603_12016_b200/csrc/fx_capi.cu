@@ -136,6 +136,7 @@ struct fx_ctx {
     int occ_s[3][3] = {{1, 1, 1}, {1, 1, 1}, {1, 1, 1}};
     bool sync_debug = false;
     bool no_tma = false;
+    bool no_stage = false;  // FXG_NO_STAGE=1: in-warp intensity / moments (tests)
 };
 
 namespace {
@@ -540,7 +541,9 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         cfg.shape_rows = c->d_shape_rows;
         cfg.shape_hdr = c->d_shape_hdr;
     }
-    if (cfg.col_int >= 0 && !dbg_dev) {
+    // staged serial passes unless debugging or FXG_NO_STAGE=1 (the in-warp paths,
+    // otherwise taken only when the staging buffers overflow, e.g. huge images)
+    if (cfg.col_int >= 0 && !dbg_dev && !c->no_stage) {
         const int ri = ensure_intensity(c, (size_t)img.w * (size_t)img.h);
         if (ri) return ri;
         cfg.int_vals = c->d_int_vals;
@@ -548,7 +551,7 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         cfg.int_sums = c->d_int_sums;
         cfg.int_cap = c->int_cap;
     }
-    if (cfg.col_mom >= 0 && !dbg_dev) {
+    if (cfg.col_mom >= 0 && !dbg_dev && !c->no_stage) {
         const int rm = ensure_moments(c, (size_t)img.w * (size_t)img.h);
         if (rm) return rm;
         cfg.mom_px = c->d_mom_px;
@@ -856,6 +859,7 @@ int fx_ctx_create(int device, fx_ctx** out) {
     c->sm_count = prop.multiProcessorCount;
     if (const char* e = getenv("FXG_SYNC_DEBUG")) c->sync_debug = atoi(e) != 0;
     if (const char* e = getenv("FXG_NO_TMA")) c->no_tma = atoi(e) != 0;
+    if (const char* e = getenv("FXG_NO_STAGE")) c->no_stage = atoi(e) != 0;
     CKC(cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking));
     CKC(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     c->stream = c->own_stream;

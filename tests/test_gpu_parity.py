@@ -303,3 +303,19 @@ def test_roi_features_batch_equals_per_cloud(ctx):
         for k in (0, 5, 6, 7, 123, 699):
             want = ctx.roi_features(*clouds[k], groups)
             assert np.array_equal(got[k], want, equal_nan=True), (groups, k)
+
+
+def test_unstaged_in_warp_paths(oracle, monkeypatch):
+    """The in-warp intensity statistics and moments (taken when the staging buffers
+    for the serial passes overflow, e.g. on huge images; forced here with
+    FXG_NO_STAGE=1) match the oracle like the staged serial passes."""
+    monkeypatch.setenv("FXG_NO_STAGE", "1")
+    c = fx.Context(0)
+    try:
+        for L, I in [(fx.blob_mask_grid(512, 300, 100, 7), None),
+                     (inputs.random_blobs((96, 130), 40, seed=2), None)]:
+            I = inputs.uniform(L.shape, 3) if I is None else I
+            check(c, oracle, I, L, ["intensity", "moments"])
+            check(c, oracle, I, L, GROUPS)
+    finally:
+        c.close()
