@@ -1194,6 +1194,363 @@ __device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64
 }
 
 // ------------------------------------------------------------------------
+// In-warp intensity statistics (intensity_features.cpp:42-215 without the edge
+// block), the path taken when the sorted values cannot be staged for
+// k_serial_stats: order statistics, moments m2..m6, mad / rmad, mode and histogram
+// runs over the warp-sorted values s, written to oi[0..31].  Out of line so the
+// staged main path of the S kernels is not sized by its registers.
+__device__ __noinline__ void intensity_inwarp(const uint16_t* s, uint32_t n, unsigned long long sS,
+                                              unsigned long long sQ, const FeatCfg& cfg,
+                                              const DebugOut* dbg, double* oi) {
+    const unsigned lane = lane_id();
+    const double dn = (double)n;
+    const uint32_t vmin = s[0], vmax = s[n - 1];
+    const double mean = (double)sS / dn;
+    const double mn = (double)vmin, mxv = (double)vmax, range = mxv - mn;
+    const double median =
+        (n & 1) ? (double)s[n / 2] : 0.5 * ((double)s[n / 2 - 1] + (double)s[n / 2]);
+    // percentiles (lanes 0..5), literal expression (intensity_features.cpp:14-22)
+    double myp = 0;
+    if (lane < 6) {
+        const double pv = lane == 0 ? 1.0 : lane == 1 ? 10.0 : lane == 2 ? 25.0
+                        : lane == 3 ? 75.0 : lane == 4 ? 90.0 : 99.0;
+        myp = percentile_exact(s, n, pv);
+    }
+    const double p10 = __shfl_sync(kFull, myp, 1), p25 = __shfl_sync(kFull, myp, 2);
+    const double p75 = __shfl_sync(kFull, myp, 3), p90 = __shfl_sync(kFull, myp, 4);
+    // median absolute deviation (exact: k-th of the two sorted half-sequences)
+    const uint32_t M2 = (n & 1) ? 2u * s[n / 2] : (uint32_t)s[n / 2 - 1] + s[n / 2];
+    const uint32_t d_hi = kth_dev2_warp(s, n, M2, n / 2);
+    const uint32_t d_lo = (n & 1) ? d_hi : kth_dev2_warp(s, n, M2, n / 2 - 1);
+    const double median_ad = (n & 1) ? 0.5 * (double)d_hi
+                                     : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
+    // one pass over the sorted values: central moments (fp64), exact integer
+    // partial sums for mad and the [p10,p90] subset, value runs (mode) and
+    // histogram-bin runs (entropy = sum c (log2 n - log2 c) / n, uniformity =
+    // sum c^2 / n^2; bins = floor(nb (v - min) / range), exact, A2)
+    const uint32_t nb32 = (uint32_t)cfg.bins;
+    const bool wide = (unsigned long long)nb32 * 65535ull >= (1ull << 32);
+    const uint32_t rng = vmax - vmin;
+    // floor(num / rng) by multiply-high with one correction step (num < 2^32)
+    const uint32_t magic = rng ? (uint32_t)(0xffffffffull / rng) : 0u;
+    auto bin_of = [&](uint32_t v) -> uint32_t {
+        if (rng == 0) return 0u;
+        uint32_t b;
+        if (!wide) {
+            const uint32_t num = nb32 * (v - vmin);
+            b = __umulhi(num, magic);
+            if (num - b * rng >= rng) ++b;
+        } else {
+            b = (uint32_t)((unsigned long long)nb32 * (v - vmin) / rng);
+        }
+        return b < nb32 - 1 ? b : nb32 - 1;
+    };
+    const double logn = nlog2(dn);
+    double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // m2..m6, entropy sum
+    unsigned long long best = 0, slo = 0, rsum = 0, usq = 0;
+    uint32_t clo = 0, rn = 0, carry_v = 0, carry_b = 0;
+    uint32_t prev_v = 0xffffffffu, prev_b = 0xffffffffu;
+#pragma unroll 1
+    for (uint32_t b0 = 0; b0 < n; b0 += 32) {
+        const uint32_t i = b0 + lane;
+        const bool ok = i < n;
+        const uint32_t v = ok ? s[i] : 0xfffffffeu;
+        const uint32_t bin = ok ? bin_of(v) : 0xfffffffeu;
+        const uint32_t nxt = b0 + 32 < n ? s[b0 + 32] : 0xfffffffeu;  // next chunk head
+        uint32_t pv = __shfl_up_sync(kFull, v, 1), pb = __shfl_up_sync(kFull, bin, 1);
+        uint32_t nv = __shfl_down_sync(kFull, v, 1), nbn = __shfl_down_sync(kFull, bin, 1);
+        if (lane == 0) {
+            pv = prev_v;
+            pb = prev_b;
+        }
+        if (lane == 31) {
+            nv = nxt;
+            nbn = b0 + 32 < n ? bin_of(nxt) : 0xfffffffeu;
+        }
+        if (i + 1 == n) {
+            nv = 0xfffffffdu;
+            nbn = 0xfffffffdu;
+        }
+        const bool vstart = ok && pv != v, vend = ok && nv != v;
+        const bool bstart = ok && pb != bin, bend = ok && nbn != bin;
+        const unsigned vs = __ballot_sync(kFull, vstart), bs = __ballot_sync(kFull, bstart);
+        const unsigned le = lanemask_lt() | (1u << lane);
+        if (ok) {
+            const double d = (double)v - mean;
+            const double d2 = d * d;
+            acc[0] += d2;
+            acc[1] += d2 * d;
+            acc[2] += d2 * d2;
+            acc[3] += d2 * d2 * d;
+            acc[4] += d2 * d2 * d2;
+            if ((double)v < mean) {
+                slo += v;
+                ++clo;
+            }
+            const double x = (double)v;
+            if (x >= p10 && x <= p90) {
+                rsum += v;
+                ++rn;
+            }
+            if (vend) {
+                const uint32_t st = (vs & le) ? b0 + 31 - __clz(vs & le) : carry_v;
+                const unsigned long long key =
+                    ((unsigned long long)(i - st + 1) << 16) | (0xffffu - v);
+                best = key > best ? key : best;
+            }
+            if (bend) {
+                const uint32_t st = (bs & le) ? b0 + 31 - __clz(bs & le) : carry_b;
+                const uint32_t c = i - st + 1;
+                acc[5] += (double)c * (logn - log2_int(c));
+                usq += (unsigned long long)c * c;
+                if (dbg && bin < nb32) dbg->hist[bin] = c;
+            }
+        }
+        if (vs) carry_v = b0 + 31 - __clz(vs);
+        if (bs) carry_b = b0 + 31 - __clz(bs);
+        prev_v = __shfl_sync(kFull, v, 31);
+        prev_b = __shfl_sync(kFull, bin, 31);
+    }
+    warp_sum8(acc);
+    best = warp_max(best);
+    slo = warp_sum(slo);
+    clo = warp_sum(clo);
+    rsum = warp_sum(rsum);
+    rn = warp_sum(rn);
+    usq = warp_sum(usq);
+    const double m2 = acc[0] / dn, m3 = acc[1] / dn, m4 = acc[2] / dn, m5 = acc[3] / dn,
+                 m6 = acc[4] / dn;
+    // sum |x - mean| = (S_hi - S_lo) + (c_lo - c_hi) mean, exact integer parts
+    const double mad = ((double)(long long)(sS - 2 * slo) +
+                        (double)((long long)clo - (long long)(n - clo)) * mean) / dn;
+    const double entropy = acc[5] / dn;
+    const double uniformity = (double)usq / (dn * dn);
+    double rmad = 0;
+    if (rn > 0) {
+        const double rmean = (double)rsum / (double)rn;
+        unsigned long long rlo = 0;
+        uint32_t rcl = 0;
+#pragma unroll 1
+        for (uint32_t i = lane; i < n; i += 32) {
+            const double x = (double)s[i];
+            if (x >= p10 && x <= p90 && x < rmean) {
+                rlo += s[i];
+                ++rcl;
+            }
+        }
+        rlo = warp_sum(rlo);
+        rcl = warp_sum(rcl);
+        rmad = ((double)(long long)(rsum - 2 * rlo) +
+                (double)((long long)rcl - (long long)(rn - rcl)) * rmean) / (double)rn;
+    }
+    const double var = n > 1 ? m2 * dn / (dn - 1.0) : 0.0;
+    double skew = 0, kurt = 0, hsk = 0, hfl = 0;
+    if (m2 > 0) {
+        const double r2 = sqrt(m2);
+        skew = m3 / (m2 * r2);
+        kurt = m4 / (m2 * m2);
+        hsk = m5 / (m2 * m2 * r2);
+        hfl = m6 / (m2 * m2 * m2);
+    }
+    const double mode = (double)(0xffffu - (uint32_t)(best & 0xffffu));
+    const double energy = (double)sQ, sdev = sqrt(var);
+    const double iqr = p75 - p25;
+    // lane k writes column k (coalesced row segment); columns 32..38 by lanes 0..6
+    const double pct = __shfl_sync(kFull, myp, (lane - 14) & 31);
+    double o = 0;
+    switch (lane) {
+        case 0: o = mean; break;
+        case 1: o = median; break;
+        case 2: o = mode; break;
+        case 3: o = mn; break;
+        case 4: o = mxv; break;
+        case 5: o = range; break;
+        case 6: o = var; break;
+        case 7: o = m2; break;
+        case 8: o = sdev; break;
+        case 9: o = sqrt(m2); break;
+        case 10: o = mad; break;
+        case 11: o = median_ad; break;
+        case 12: o = rmad; break;
+        case 13: o = iqr; break;
+        case 14: case 15: case 16: case 17: case 18: case 19: o = pct; break;
+        case 20: o = skew; break;
+        case 21: o = kurt; break;
+        case 22: o = m2 > 0 ? kurt - 3.0 : 0.0; break;
+        case 23: o = hsk; break;
+        case 24: o = hfl; break;
+        case 25: o = energy; break;
+        case 26: o = sqrt(energy / dn); break;
+        case 27: o = entropy; break;
+        case 28: o = uniformity; break;
+        case 29: o = (p75 + p25) != 0 ? iqr / (p75 + p25) : 0.0; break;
+        case 30: o = mean != 0 ? sdev / mean : 0.0; break;
+        default: o = (double)sS; break;
+    }
+    oi[lane] = o;
+}
+
+// In-warp moments (moments.cpp:32-92), the path taken when the ROI's pixels cannot
+// be staged for k_serial_stats: separable row sums about the integer anchors (lanes
+// = rows: m0 / m1 and off0 / off1 are this lane's row masks and value offsets),
+// reduce-scatter, two-stage binomial shift, eta and Hu, written to orow.  Out of
+// line so the staged main path of the S kernels is not sized by its registers.
+__device__ __noinline__ void moments_inwarp(uint32_t n, int h, uint64_t m0, uint64_t m1, uint32_t off0,
+                                            uint32_t off1, const uint16_t* vals,
+                                            unsigned long long sS, unsigned long long sXI,
+                                            unsigned long long sYI, uint32_t sLX, uint32_t sLY,
+                                            long long gx0, long long gy0, const FeatCfg& cfg,
+                                            double* orow) {
+    const unsigned lane = lane_id();
+    const double dn = (double)n;
+    const long long nn = (long long)n, W = (long long)sS;
+    const long long axb = (2 * (long long)sLX + nn) / (2 * nn);
+    const long long ayb = (2 * (long long)sLY + nn) / (2 * nn);
+    const long long axw = W > 0 ? (2 * (long long)sXI + W) / (2 * W) : 0;
+    const long long ayw = W > 0 ? (2 * (long long)sYI + W) / (2 * W) : 0;
+    // two passes (unit mass, then intensity) of 16 separable row accumulators
+    // about the integer anchor: A_pq = sum_rows (sum_x w dx^p) dy^q
+    const int nhalf = h > 32 ? 2 : 1;
+    double Nb = 0, Nw = 0;
+#pragma unroll 1
+    for (int g = 0; g < 2; ++g) {
+        const long long ax = g ? axw : axb, ay = g ? ayw : ayb;
+        double acc[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) acc[k] = 0;
+#pragma unroll 1
+        for (int hf = 0; hf < nhalf; ++hf) {
+            const int y = lane + 32 * hf;
+            uint64_t m = hf ? m1 : m0;
+            uint32_t idx = hf ? off1 : off0;
+            double r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+            if (g == 0) {
+                r0 = (double)__popcll(m);
+                while (m) {
+                    const double d = (double)((long long)(__ffsll((long long)m) - 1) - ax);
+                    m &= m - 1;
+                    const double d2 = d * d;
+                    r1 += d;
+                    r2 += d2;
+                    r3 += d2 * d;
+                }
+            } else {
+                while (m) {
+                    const double d = (double)((long long)(__ffsll((long long)m) - 1) - ax);
+                    m &= m - 1;
+                    const double wv = (double)vals[idx++];
+                    const double wd = wv * d, wd2 = wd * d;
+                    r0 += wv;
+                    r1 += wd;
+                    r2 += wd2;
+                    r3 += wd2 * d;
+                }
+            }
+            const double yy = (double)((long long)y - ay);
+            const double q2 = yy * yy;
+            const double rr[4] = {r0, r1, r2, r3}, qq[4] = {1.0, yy, q2, q2 * yy};
+#pragma unroll
+            for (int a = 0; a < 4; ++a)
+#pragma unroll
+                for (int b = 0; b < 4; ++b) acc[a * 4 + b] += rr[a] * qq[b];
+        }
+        // reduce-scatter: after 4 halving steps lane L holds index L >> 1
+#pragma unroll
+        for (int st = 16, half = 8; st >= 2; st >>= 1, half >>= 1) {
+            const bool up = (lane & st) != 0;
+#pragma unroll
+            for (int j = 0; j < half; ++j) {
+                const double send = up ? acc[j] : acc[j + half];
+                const double recv = __shfl_xor_sync(kFull, send, st);
+                acc[j] = (up ? acc[j + half] : acc[j]) + recv;
+            }
+        }
+        double t = acc[0] + __shfl_xor_sync(kFull, acc[0], 1);
+        t = __shfl_sync(kFull, t, 2 * (lane & 15));  // lane L: index L & 15
+        if (g == 0) Nb = t;
+        else Nw = t;
+    }
+    const double N = (lane >> 4) ? Nw : Nb;
+    const int grp = lane >> 4, p = (lane >> 2) & 3, q = lane & 3;
+    const double m00 = grp ? (double)sS : dn;
+    const bool zero_mass = grp && sS == 0;
+    const double dx = grp ? (W > 0 ? (double)((long long)sXI - axw * W) / (double)W : 0.0)
+                          : (double)((long long)sLX - axb * nn) / dn;
+    const double dy = grp ? (W > 0 ? (double)((long long)sYI - ayw * W) / (double)W : 0.0)
+                          : (double)((long long)sLY - ayb * nn) / dn;
+    const double Ax = (double)(gx0 + (grp ? axw : axb)), Ay = (double)(gy0 + (grp ? ayw : ayb));
+    // separable binomial shift in two shuffle stages (no lane-indexed arrays):
+    //   T_pq = sum_j C(q,j) t^(q-j) N_pj,  mu_pq = sum_i C(p,i) s^(p-i) T_iq
+    auto coef = [](int e, int k, double t) -> double {  // C(e,k) t^(e-k), 0 if k > e
+        if (k > e) return 0.0;
+        const int d = e - k;
+        const double c = (k == 0 || k == e) ? 1.0 : (e == 3 ? 3.0 : 2.0);
+        const double t2 = t * t;
+        return c * (d == 0 ? 1.0 : d == 1 ? t : d == 2 ? t2 : t2 * t);
+    };
+    double Tm = 0, Tr = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const double Npj = __shfl_sync(kFull, N, (grp << 4) | (p << 2) | j);
+        Tm += coef(q, j, -dy) * Npj;
+        Tr += coef(q, j, Ay) * Npj;
+    }
+    double mu = 0, raw = 0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int src = (grp << 4) | (i << 2) | q;
+        mu += coef(p, i, -dx) * __shfl_sync(kFull, Tm, src);
+        raw += coef(p, i, Ax) * __shfl_sync(kFull, Tr, src);
+    }
+    if ((p == 1 && q == 0) || (p == 0 && q == 1)) mu = 0.0;
+    if (p == 0 && q == 0) mu = N;
+    // eta = mu / m00^(1 + (p+q)/2)  (moments.cpp:84-89), powers built from m00 and sqrt(m00)
+    double eta = 0;
+    if (p + q >= 2) {
+        const int t = p + q;  // exponent 1 + t/2 in {2, 2.5, 3, 3.5, 4}
+        double den = m00 * m00;
+        if (t >= 4) den *= m00;
+        if (t >= 6) den *= m00;
+        if (t & 1) den *= sqrt(m00);
+        eta = mu / den;
+    }
+    if (zero_mass) raw = mu = eta = 0;
+    const double n20 = __shfl_sync(kFull, eta, (grp << 4) | 8);
+    const double n02 = __shfl_sync(kFull, eta, (grp << 4) | 2);
+    const double n11 = __shfl_sync(kFull, eta, (grp << 4) | 5);
+    const double n30 = __shfl_sync(kFull, eta, (grp << 4) | 12);
+    const double n03 = __shfl_sync(kFull, eta, (grp << 4) | 3);
+    const double n21 = __shfl_sync(kFull, eta, (grp << 4) | 9);
+    const double n12 = __shfl_sync(kFull, eta, (grp << 4) | 6);
+    double* o = orow + cfg.col_mom + grp * 52;
+    const int li = lane & 15;
+    o[li] = raw;
+    o[16 + li] = mu;
+    if (p + q >= 2) o[32 + ((p == 0) ? q - 2 : (p == 1 ? 1 + q : 1 + 4 * (p - 1) + q))] = eta;
+    // Hu invariants: lanes li = 0..6 of each group compute one each
+    if (li < 7) {
+        const double a = n30 + n12, b = n21 + n03;
+        double hu;
+        switch (li) {
+            case 0: hu = n20 + n02; break;
+            case 1: hu = (n20 - n02) * (n20 - n02) + 4.0 * n11 * n11; break;
+            case 2: hu = (n30 - 3.0 * n12) * (n30 - 3.0 * n12) + (3.0 * n21 - n03) * (3.0 * n21 - n03); break;
+            case 3: hu = a * a + b * b; break;
+            case 4:
+                hu = (n30 - 3.0 * n12) * a * (a * a - 3.0 * b * b) +
+                     (3.0 * n21 - n03) * b * (3.0 * a * a - b * b);
+                break;
+            case 5: hu = (n20 - n02) * (a * a - b * b) + 4.0 * n11 * a * b; break;
+            default:
+                hu = (3.0 * n21 - n03) * a * (a * a - 3.0 * b * b) -
+                     (n30 - 3.0 * n12) * b * (3.0 * a * a - b * b);
+                break;
+        }
+        o[45 + li] = zero_mass ? 0.0 : hu;
+    }
+    __syncwarp();
+}
+
 template <int TW, int TH, int NMAX, int RUNMAX, int GLCM>
 __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8_t* base,
                                           const DevImage& img, const FeatCfg& cfg,
@@ -1340,8 +1697,8 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     }
     __syncwarp();
     const double dn = (double)n;
-    uint32_t vmin = 0, vmax = 0;
-    bool have_minmax = false;
+    uint32_t vmin = gmin, vmax = gmax;  // value range (the gather computed it)
+    bool have_minmax = true;
 
     // K (largest 8-connected component, row-major tie-break) and E (4-connected
     // exterior of the window cells outside K) as row masks (lanes = rows); false:
@@ -1529,228 +1886,25 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
             }
             return true;
         };
-        if (staged) {
-            PT(2);
-            if (!edge_stats()) return;
-            double wcx = 0, wcy = 0;
-            if (sS > 0) {
-                wcx = (double)((unsigned long long)gx0 * sS + sXI) / (double)sS;
-                wcy = (double)((unsigned long long)gy0 * sS + sYI) / (double)sS;
-            }
-            if (lane < 7) {
-                const double t[7] = {e_mean, e_min, e_max, e_std, e_int, wcx, wcy};
-                double v = t[0];
-#pragma unroll
-                for (int k = 1; k < 7; ++k)
-                    if ((int)lane == k) v = t[k];
-                orow[cfg.col_int + 32 + lane] = v;
-            }
-            __syncwarp();
-        } else {
-            vmin = s[0];
-            vmax = s[n - 1];
-            have_minmax = true;
-            const double mean = (double)sS / dn;
-            const double mn = (double)vmin, mxv = (double)vmax, range = mxv - mn;
-            const double median =
-                (n & 1) ? (double)s[n / 2] : 0.5 * ((double)s[n / 2 - 1] + (double)s[n / 2]);
-            // percentiles (lanes 0..5), literal expression (intensity_features.cpp:14-22)
-            double myp = 0;
-            if (lane < 6) {
-                const double pv = lane == 0 ? 1.0 : lane == 1 ? 10.0 : lane == 2 ? 25.0
-                                : lane == 3 ? 75.0 : lane == 4 ? 90.0 : 99.0;
-                myp = percentile_exact(s, n, pv);
-            }
-            const double p10 = __shfl_sync(kFull, myp, 1), p25 = __shfl_sync(kFull, myp, 2);
-            const double p75 = __shfl_sync(kFull, myp, 3), p90 = __shfl_sync(kFull, myp, 4);
-            // median absolute deviation (exact: k-th of the two sorted half-sequences)
-            const uint32_t M2 = (n & 1) ? 2u * s[n / 2] : (uint32_t)s[n / 2 - 1] + s[n / 2];
-            const uint32_t d_hi = kth_dev2_warp(s, n, M2, n / 2);
-            const uint32_t d_lo = (n & 1) ? d_hi : kth_dev2_warp(s, n, M2, n / 2 - 1);
-            const double median_ad = (n & 1) ? 0.5 * (double)d_hi
-                                             : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
-            // one pass over the sorted values: central moments (fp64), exact integer
-            // partial sums for mad and the [p10,p90] subset, value runs (mode) and
-            // histogram-bin runs (entropy = sum c (log2 n - log2 c) / n, uniformity =
-            // sum c^2 / n^2; bins = floor(nb (v - min) / range), exact, A2)
-            const uint32_t nb32 = (uint32_t)cfg.bins;
-            const bool wide = (unsigned long long)nb32 * 65535ull >= (1ull << 32);
-            const uint32_t rng = vmax - vmin;
-            // floor(num / rng) by multiply-high with one correction step (num < 2^32)
-            const uint32_t magic = rng ? (uint32_t)(0xffffffffull / rng) : 0u;
-            auto bin_of = [&](uint32_t v) -> uint32_t {
-                if (rng == 0) return 0u;
-                uint32_t b;
-                if (!wide) {
-                    const uint32_t num = nb32 * (v - vmin);
-                    b = __umulhi(num, magic);
-                    if (num - b * rng >= rng) ++b;
-                } else {
-                    b = (uint32_t)((unsigned long long)nb32 * (v - vmin) / rng);
-                }
-                return b < nb32 - 1 ? b : nb32 - 1;
-            };
-            const double logn = nlog2(dn);
-            double acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // m2..m6, entropy sum
-            unsigned long long best = 0, slo = 0, rsum = 0, usq = 0;
-            uint32_t clo = 0, rn = 0, carry_v = 0, carry_b = 0;
-            uint32_t prev_v = 0xffffffffu, prev_b = 0xffffffffu;
-    #pragma unroll 1
-            for (uint32_t b0 = 0; b0 < n; b0 += 32) {
-                const uint32_t i = b0 + lane;
-                const bool ok = i < n;
-                const uint32_t v = ok ? s[i] : 0xfffffffeu;
-                const uint32_t bin = ok ? bin_of(v) : 0xfffffffeu;
-                const uint32_t nxt = b0 + 32 < n ? s[b0 + 32] : 0xfffffffeu;  // next chunk head
-                uint32_t pv = __shfl_up_sync(kFull, v, 1), pb = __shfl_up_sync(kFull, bin, 1);
-                uint32_t nv = __shfl_down_sync(kFull, v, 1), nbn = __shfl_down_sync(kFull, bin, 1);
-                if (lane == 0) {
-                    pv = prev_v;
-                    pb = prev_b;
-                }
-                if (lane == 31) {
-                    nv = nxt;
-                    nbn = b0 + 32 < n ? bin_of(nxt) : 0xfffffffeu;
-                }
-                if (i + 1 == n) {
-                    nv = 0xfffffffdu;
-                    nbn = 0xfffffffdu;
-                }
-                const bool vstart = ok && pv != v, vend = ok && nv != v;
-                const bool bstart = ok && pb != bin, bend = ok && nbn != bin;
-                const unsigned vs = __ballot_sync(kFull, vstart), bs = __ballot_sync(kFull, bstart);
-                const unsigned le = lanemask_lt() | (1u << lane);
-                if (ok) {
-                    const double d = (double)v - mean;
-                    const double d2 = d * d;
-                    acc[0] += d2;
-                    acc[1] += d2 * d;
-                    acc[2] += d2 * d2;
-                    acc[3] += d2 * d2 * d;
-                    acc[4] += d2 * d2 * d2;
-                    if ((double)v < mean) {
-                        slo += v;
-                        ++clo;
-                    }
-                    const double x = (double)v;
-                    if (x >= p10 && x <= p90) {
-                        rsum += v;
-                        ++rn;
-                    }
-                    if (vend) {
-                        const uint32_t st = (vs & le) ? b0 + 31 - __clz(vs & le) : carry_v;
-                        const unsigned long long key =
-                            ((unsigned long long)(i - st + 1) << 16) | (0xffffu - v);
-                        best = key > best ? key : best;
-                    }
-                    if (bend) {
-                        const uint32_t st = (bs & le) ? b0 + 31 - __clz(bs & le) : carry_b;
-                        const uint32_t c = i - st + 1;
-                        acc[5] += (double)c * (logn - log2_int(c));
-                        usq += (unsigned long long)c * c;
-                        if (dbg_on && bin < nb32) dbg->hist[bin] = c;
-                    }
-                }
-                if (vs) carry_v = b0 + 31 - __clz(vs);
-                if (bs) carry_b = b0 + 31 - __clz(bs);
-                prev_v = __shfl_sync(kFull, v, 31);
-                prev_b = __shfl_sync(kFull, bin, 31);
-            }
-            warp_sum8(acc);
-            best = warp_max(best);
-            slo = warp_sum(slo);
-            clo = warp_sum(clo);
-            rsum = warp_sum(rsum);
-            rn = warp_sum(rn);
-            usq = warp_sum(usq);
-            const double m2 = acc[0] / dn, m3 = acc[1] / dn, m4 = acc[2] / dn, m5 = acc[3] / dn,
-                         m6 = acc[4] / dn;
-            // sum |x - mean| = (S_hi - S_lo) + (c_lo - c_hi) mean, exact integer parts
-            const double mad = ((double)(long long)(sS - 2 * slo) +
-                                (double)((long long)clo - (long long)(n - clo)) * mean) / dn;
-            const double entropy = acc[5] / dn;
-            const double uniformity = (double)usq / (dn * dn);
-            double rmad = 0;
-            if (rn > 0) {
-                const double rmean = (double)rsum / (double)rn;
-                unsigned long long rlo = 0;
-                uint32_t rcl = 0;
-    #pragma unroll 1
-                for (uint32_t i = lane; i < n; i += 32) {
-                    const double x = (double)s[i];
-                    if (x >= p10 && x <= p90 && x < rmean) {
-                        rlo += s[i];
-                        ++rcl;
-                    }
-                }
-                rlo = warp_sum(rlo);
-                rcl = warp_sum(rcl);
-                rmad = ((double)(long long)(rsum - 2 * rlo) +
-                        (double)((long long)rcl - (long long)(rn - rcl)) * rmean) / (double)rn;
-            }
-            PT(2);
-            if (!edge_stats()) return;
-            double wcx = 0, wcy = 0;
-            if (sS > 0) {
-                wcx = (double)((unsigned long long)gx0 * sS + sXI) / (double)sS;
-                wcy = (double)((unsigned long long)gy0 * sS + sYI) / (double)sS;
-            }
-            const double var = n > 1 ? m2 * dn / (dn - 1.0) : 0.0;
-            double skew = 0, kurt = 0, hsk = 0, hfl = 0;
-            if (m2 > 0) {
-                const double r2 = sqrt(m2);
-                skew = m3 / (m2 * r2);
-                kurt = m4 / (m2 * m2);
-                hsk = m5 / (m2 * m2 * r2);
-                hfl = m6 / (m2 * m2 * m2);
-            }
-            const double mode = (double)(0xffffu - (uint32_t)(best & 0xffffu));
-            const double energy = (double)sQ, sdev = sqrt(var);
-            const double iqr = p75 - p25;
-            // lane k writes column k (coalesced row segment); columns 32..38 by lanes 0..6
-            const double pct = __shfl_sync(kFull, myp, (lane - 14) & 31);
-            double o = 0;
-            switch (lane) {
-                case 0: o = mean; break;
-                case 1: o = median; break;
-                case 2: o = mode; break;
-                case 3: o = mn; break;
-                case 4: o = mxv; break;
-                case 5: o = range; break;
-                case 6: o = var; break;
-                case 7: o = m2; break;
-                case 8: o = sdev; break;
-                case 9: o = sqrt(m2); break;
-                case 10: o = mad; break;
-                case 11: o = median_ad; break;
-                case 12: o = rmad; break;
-                case 13: o = iqr; break;
-                case 14: case 15: case 16: case 17: case 18: case 19: o = pct; break;
-                case 20: o = skew; break;
-                case 21: o = kurt; break;
-                case 22: o = m2 > 0 ? kurt - 3.0 : 0.0; break;
-                case 23: o = hsk; break;
-                case 24: o = hfl; break;
-                case 25: o = energy; break;
-                case 26: o = sqrt(energy / dn); break;
-                case 27: o = entropy; break;
-                case 28: o = uniformity; break;
-                case 29: o = (p75 + p25) != 0 ? iqr / (p75 + p25) : 0.0; break;
-                case 30: o = mean != 0 ? sdev / mean : 0.0; break;
-                default: o = (double)sS; break;
-            }
-            double* oi = orow + cfg.col_int;
-            oi[lane] = o;
-            if (lane < 7) {
-                const double t[7] = {e_mean, e_min, e_max, e_std, e_int, wcx, wcy};
-                double v = t[0];
-    #pragma unroll
-                for (int k = 1; k < 7; ++k)
-                    if ((int)lane == k) v = t[k];
-                oi[32 + lane] = v;
-            }
-            __syncwarp();
+        // unstaged: the statistics read the sorted values before the edge slow path
+        // reuses their region of the slab
+        if (!staged) intensity_inwarp(s, n, sS, sQ, cfg, dbg_on ? dbg : nullptr, orow + cfg.col_int);
+        PT(2);
+        if (!edge_stats()) return;
+        double wcx = 0, wcy = 0;
+        if (sS > 0) {
+            wcx = (double)((unsigned long long)gx0 * sS + sXI) / (double)sS;
+            wcy = (double)((unsigned long long)gy0 * sS + sYI) / (double)sS;
         }
+        if (lane < 7) {
+            const double t[7] = {e_mean, e_min, e_max, e_std, e_int, wcx, wcy};
+            double v = t[0];
+#pragma unroll
+            for (int k = 1; k < 7; ++k)
+                if ((int)lane == k) v = t[k];
+            orow[cfg.col_int + 32 + lane] = v;
+        }
+        __syncwarp();
     }
 
     // ---------------------------------------------------------------- shape
@@ -1765,154 +1919,8 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
     }
     // ------------------------------------------------------------- moments
     PT(6);
-    if (cfg.col_mom >= 0 && !mst) {  // staged ROIs: k_moments_serial
-        const long long nn = (long long)n, W = (long long)sS;
-        const long long axb = (2 * (long long)sLX + nn) / (2 * nn);
-        const long long ayb = (2 * (long long)sLY + nn) / (2 * nn);
-        const long long axw = W > 0 ? (2 * (long long)sXI + W) / (2 * W) : 0;
-        const long long ayw = W > 0 ? (2 * (long long)sYI + W) / (2 * W) : 0;
-        // two passes (unit mass, then intensity) of 16 separable row accumulators
-        // about the integer anchor: A_pq = sum_rows (sum_x w dx^p) dy^q
-        const int nhalf = h > 32 ? 2 : 1;
-        double Nb = 0, Nw = 0;
-#pragma unroll 1
-        for (int g = 0; g < 2; ++g) {
-            const long long ax = g ? axw : axb, ay = g ? ayw : ayb;
-            double acc[16];
-#pragma unroll
-            for (int k = 0; k < 16; ++k) acc[k] = 0;
-#pragma unroll 1
-            for (int hf = 0; hf < nhalf; ++hf) {
-                const int y = lane + 32 * hf;
-                uint64_t m = hf ? m1 : m0;
-                uint32_t idx = hf ? off1 : off0;
-                double r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-                if (g == 0) {
-                    r0 = (double)__popcll(m);
-                    while (m) {
-                        const double d = (double)((long long)(__ffsll((long long)m) - 1) - ax);
-                        m &= m - 1;
-                        const double d2 = d * d;
-                        r1 += d;
-                        r2 += d2;
-                        r3 += d2 * d;
-                    }
-                } else {
-                    while (m) {
-                        const double d = (double)((long long)(__ffsll((long long)m) - 1) - ax);
-                        m &= m - 1;
-                        const double wv = (double)vals[idx++];
-                        const double wd = wv * d, wd2 = wd * d;
-                        r0 += wv;
-                        r1 += wd;
-                        r2 += wd2;
-                        r3 += wd2 * d;
-                    }
-                }
-                const double yy = (double)((long long)y - ay);
-                const double q2 = yy * yy;
-                const double rr[4] = {r0, r1, r2, r3}, qq[4] = {1.0, yy, q2, q2 * yy};
-#pragma unroll
-                for (int a = 0; a < 4; ++a)
-#pragma unroll
-                    for (int b = 0; b < 4; ++b) acc[a * 4 + b] += rr[a] * qq[b];
-            }
-            // reduce-scatter: after 4 halving steps lane L holds index L >> 1
-#pragma unroll
-            for (int st = 16, half = 8; st >= 2; st >>= 1, half >>= 1) {
-                const bool up = (lane & st) != 0;
-#pragma unroll
-                for (int j = 0; j < half; ++j) {
-                    const double send = up ? acc[j] : acc[j + half];
-                    const double recv = __shfl_xor_sync(kFull, send, st);
-                    acc[j] = (up ? acc[j + half] : acc[j]) + recv;
-                }
-            }
-            double t = acc[0] + __shfl_xor_sync(kFull, acc[0], 1);
-            t = __shfl_sync(kFull, t, 2 * (lane & 15));  // lane L: index L & 15
-            if (g == 0) Nb = t;
-            else Nw = t;
-        }
-        const double N = (lane >> 4) ? Nw : Nb;
-        const int grp = lane >> 4, p = (lane >> 2) & 3, q = lane & 3;
-        const double m00 = grp ? (double)sS : dn;
-        const bool zero_mass = grp && sS == 0;
-        const double dx = grp ? (W > 0 ? (double)((long long)sXI - axw * W) / (double)W : 0.0)
-                              : (double)((long long)sLX - axb * nn) / dn;
-        const double dy = grp ? (W > 0 ? (double)((long long)sYI - ayw * W) / (double)W : 0.0)
-                              : (double)((long long)sLY - ayb * nn) / dn;
-        const double Ax = (double)(gx0 + (grp ? axw : axb)), Ay = (double)(gy0 + (grp ? ayw : ayb));
-        // separable binomial shift in two shuffle stages (no lane-indexed arrays):
-        //   T_pq = sum_j C(q,j) t^(q-j) N_pj,  mu_pq = sum_i C(p,i) s^(p-i) T_iq
-        auto coef = [](int e, int k, double t) -> double {  // C(e,k) t^(e-k), 0 if k > e
-            if (k > e) return 0.0;
-            const int d = e - k;
-            const double c = (k == 0 || k == e) ? 1.0 : (e == 3 ? 3.0 : 2.0);
-            const double t2 = t * t;
-            return c * (d == 0 ? 1.0 : d == 1 ? t : d == 2 ? t2 : t2 * t);
-        };
-        double Tm = 0, Tr = 0;
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-            const double Npj = __shfl_sync(kFull, N, (grp << 4) | (p << 2) | j);
-            Tm += coef(q, j, -dy) * Npj;
-            Tr += coef(q, j, Ay) * Npj;
-        }
-        double mu = 0, raw = 0;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const int src = (grp << 4) | (i << 2) | q;
-            mu += coef(p, i, -dx) * __shfl_sync(kFull, Tm, src);
-            raw += coef(p, i, Ax) * __shfl_sync(kFull, Tr, src);
-        }
-        if ((p == 1 && q == 0) || (p == 0 && q == 1)) mu = 0.0;
-        if (p == 0 && q == 0) mu = N;
-        // eta = mu / m00^(1 + (p+q)/2)  (moments.cpp:84-89), powers built from m00 and sqrt(m00)
-        double eta = 0;
-        if (p + q >= 2) {
-            const int t = p + q;  // exponent 1 + t/2 in {2, 2.5, 3, 3.5, 4}
-            double den = m00 * m00;
-            if (t >= 4) den *= m00;
-            if (t >= 6) den *= m00;
-            if (t & 1) den *= sqrt(m00);
-            eta = mu / den;
-        }
-        if (zero_mass) raw = mu = eta = 0;
-        const double n20 = __shfl_sync(kFull, eta, (grp << 4) | 8);
-        const double n02 = __shfl_sync(kFull, eta, (grp << 4) | 2);
-        const double n11 = __shfl_sync(kFull, eta, (grp << 4) | 5);
-        const double n30 = __shfl_sync(kFull, eta, (grp << 4) | 12);
-        const double n03 = __shfl_sync(kFull, eta, (grp << 4) | 3);
-        const double n21 = __shfl_sync(kFull, eta, (grp << 4) | 9);
-        const double n12 = __shfl_sync(kFull, eta, (grp << 4) | 6);
-        double* o = orow + cfg.col_mom + grp * 52;
-        const int li = lane & 15;
-        o[li] = raw;
-        o[16 + li] = mu;
-        if (p + q >= 2) o[32 + ((p == 0) ? q - 2 : (p == 1 ? 1 + q : 1 + 4 * (p - 1) + q))] = eta;
-        // Hu invariants: lanes li = 0..6 of each group compute one each
-        if (li < 7) {
-            const double a = n30 + n12, b = n21 + n03;
-            double hu;
-            switch (li) {
-                case 0: hu = n20 + n02; break;
-                case 1: hu = (n20 - n02) * (n20 - n02) + 4.0 * n11 * n11; break;
-                case 2: hu = (n30 - 3.0 * n12) * (n30 - 3.0 * n12) + (3.0 * n21 - n03) * (3.0 * n21 - n03); break;
-                case 3: hu = a * a + b * b; break;
-                case 4:
-                    hu = (n30 - 3.0 * n12) * a * (a * a - 3.0 * b * b) +
-                         (3.0 * n21 - n03) * b * (3.0 * a * a - b * b);
-                    break;
-                case 5: hu = (n20 - n02) * (a * a - b * b) + 4.0 * n11 * a * b; break;
-                default:
-                    hu = (3.0 * n21 - n03) * a * (a * a - 3.0 * b * b) -
-                         (n30 - 3.0 * n12) * b * (3.0 * a * a - b * b);
-                    break;
-            }
-            o[45 + li] = zero_mass ? 0.0 : hu;
-        }
-        __syncwarp();
-    }
+    if (cfg.col_mom >= 0 && !mst)  // staged ROIs: k_serial_stats
+        moments_inwarp(n, h, m0, m1, off0, off1, vals, sS, sXI, sYI, sLX, sLY, gx0, gy0, cfg, orow);
 
     // ---------------------------------------------------------------- glcm
     PT(4);
