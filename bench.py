@@ -151,7 +151,9 @@ def run_reference_arm(args, rank, world):
         return
     intensity, labels, roi_size = workload(0)
     n_rois = int(np.count_nonzero(np.bincount(labels.ravel(), minlength=65536)[1:]))
-    steps, warmup = max(1, min(args.steps, 3)), min(args.warmup, 1)
+    # each step is one full C2 image (~1.1 s on 16 threads): the run stays bounded at
+    # <= 3 warm-up + 10 timed steps (~15 s) whatever --steps / --warmup ask for
+    steps, warmup = max(1, min(args.steps, 10)), min(args.warmup, 3)
     times, threads, nr = cpu_reference(intensity, labels, steps, warmup)
     t = float(np.sum(times))
     mp = IMAGE * IMAGE / 1e6
