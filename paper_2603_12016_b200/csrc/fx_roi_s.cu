@@ -2243,16 +2243,27 @@ __device__ void moments_row(uint32_t r, int grp, const RoiList& rl, const FeatCf
 // V-shaped deviations (two-pointer walk from the median split), one sequential
 // scan for the central moments, mad / rmad partial sums, mode and histogram runs.
 // Columns 32..38 (edge statistics, weighted centroid) come from the warp.
-__device__ uint32_t kth_dev_scan(const uint16_t* s, uint32_t n, uint32_t M2, uint32_t k) {
-    uint32_t lo = 0, hi = n;  // m = first index with 2 s[i] >= M2
-    while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (2u * s[mid] >= M2) hi = mid;
-        else lo = mid + 1;
+// Both middle order statistics of the doubled deviations |2 s[i] - M2| in one search:
+// d_hi = the (n/2)-th (0-based), d_lo = the (n/2 - 1)-th (even n; d_lo = d_hi if odd).
+__device__ void kth_dev_pair(const uint16_t* s, uint32_t n, uint32_t M2, uint32_t& d_hi,
+                             uint32_t& d_lo) {
+    // m = first index with 2 s[i] >= M2.  M2 <= 2 s[n/2] (M2 is twice the median),
+    // so m <= n/2, and m == n/2 unless s[n/2 - 1] ties the median: one probe, and a
+    // binary search over [0, n/2 - 1] only for tied medians
+    uint32_t m = n / 2;
+    if (m > 0 && 2u * s[m - 1] >= M2) {
+        uint32_t lo = 0, hi = m - 1;
+        while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (2u * s[mid] >= M2) hi = mid;
+            else lo = mid + 1;
+        }
+        m = lo;
     }
     // A[j] = M2 - 2 s[m-1-j] (j < m) and B[j] = 2 s[m+j] - M2 are ascending; the
-    // k-th (0-based) of their union by a binary search on the count taken from A
-    const uint32_t m = lo, na = m, nb = n - m, kk = k + 1;
+    // kk smallest of their union are A[0, t) and B[0, kk - t) for the t found by a
+    // binary search on the count taken from A (kk = n/2 + 1)
+    const uint32_t na = m, nb = n - m, kk = n / 2 + 1;
     auto A = [&](uint32_t j) { return M2 - 2u * s[m - 1 - j]; };
     auto B = [&](uint32_t j) { return 2u * s[m + j] - M2; };
     uint32_t a = kk > nb ? kk - nb : 0u, b = kk < na ? kk : na;  // t in [a, b]
@@ -2261,11 +2272,18 @@ __device__ uint32_t kth_dev_scan(const uint16_t* s, uint32_t n, uint32_t M2, uin
         if (A(t) < B(kk - 1 - t)) a = t + 1;
         else b = t;
     }
-    const uint32_t t = a;
-    uint32_t best = 0;
-    if (t > 0) best = A(t - 1);
-    if (kk - t > 0) best = max(best, B(kk - t - 1));
-    return best;
+    const uint32_t t = a, tb = kk - t;
+    // the kk-th smallest is the largest of that prefix, the (kk-1)-th its second largest
+    const uint32_t x = t > 0 ? A(t - 1) : 0u, y = tb > 0 ? B(tb - 1) : 0u;
+    d_hi = max(x, y);
+    if (n & 1) {
+        d_lo = d_hi;
+        return;
+    }
+    uint32_t sec = (t > 0 && tb > 0) ? min(x, y) : 0u;
+    if (t >= 2) sec = max(sec, A(t - 2));
+    if (tb >= 2) sec = max(sec, B(tb - 2));
+    d_lo = sec;
 }
 
 __device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
@@ -2310,8 +2328,14 @@ __device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
     unsigned long long best = 0, slo = 0, rsum = 0, usq = 0;
     uint32_t clo = 0, rn = 0, run_v = 0, run_b = 0, pv_ = s[0], pb_ = bin_of(s[0]);
     const uint4* s4 = reinterpret_cast<const uint4*>(s);  // 16 B aligned (staging rounds to 8)
+    uint4 nxt4 = s4[0];  // next 8 values in flight while these 8 are processed
     for (uint32_t q = 0; q * 8u < n; ++q) {
+#ifndef FXG_NO_INT_PREFETCH
+        const uint4 w4 = nxt4;
+        if ((q + 1u) * 8u < n) nxt4 = s4[q + 1];
+#else
         const uint4 w4 = s4[q];
+#endif
         const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
@@ -2354,8 +2378,8 @@ __device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
         ent += (double)run_b * (logn - log2_int(run_b));
         usq += (unsigned long long)run_b * run_b;
     }
-    const uint32_t d_hi = kth_dev_scan(s, n, M2, n / 2);
-    const uint32_t d_lo = (n & 1) ? d_hi : kth_dev_scan(s, n, M2, n / 2 - 1);
+    uint32_t d_hi, d_lo;
+    kth_dev_pair(s, n, M2, d_hi, d_lo);
     const double median_ad = (n & 1) ? 0.5 * (double)d_hi : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
     const double m2 = a2 / dn, m3 = a3 / dn, m4 = a4 / dn, m5 = a5 / dn, m6 = a6 / dn;
     const double mad = ((double)(long long)(sS - 2 * slo) +
@@ -2367,12 +2391,21 @@ __device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
         uint32_t rcl = 0;
         // values sorted: the [p10, p90] subset below rmean is one contiguous range
         const uint32_t t_rm = (uint32_t)ceil(rmean);
-        for (uint32_t i = 0; i < n; ++i) {
-            const uint32_t v = s[i];
-            if (v >= t_rm) break;
-            if (v >= t_lo && v <= t_hi) {
-                rlo += v;
-                ++rcl;
+        bool more = true;
+        for (uint32_t q = 0; more && q * 8u < n; ++q) {  // 8 values per 16 B load
+            const uint4 w4 = s4[q];
+            const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t v = (wv[u >> 1] >> ((u & 1) * 16)) & 0xffffu;
+                if (q * 8u + (uint32_t)u >= n || v >= t_rm) {
+                    more = false;
+                    break;
+                }
+                if (v >= t_lo && v <= t_hi) {
+                    rlo += v;
+                    ++rcl;
+                }
             }
         }
         rmad = ((double)(long long)(rsum - 2 * rlo) +
