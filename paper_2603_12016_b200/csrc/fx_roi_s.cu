@@ -2147,8 +2147,13 @@ __device__ void moments_row(uint32_t r, int grp, const RoiList& rl, const FeatCf
 #pragma unroll
             for (int p = 0; p < 4; ++p)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) M[p * 4 + q] += (long long)X[p] * Y[q];
+                for (int q = 0; q < 4; ++q)
+                    if (p + q >= 2) M[p * 4 + q] += (long long)X[p] * Y[q];
         });
+        // the order-0 / order-1 sums follow from the staged exact sums
+        M[0] = nn;
+        M[1] = SY - ay * nn;
+        M[4] = SX - ax * nn;
 #pragma unroll
         for (int k = 0; k < 16; ++k) N[k] = (double)M[k];
     } else {
@@ -2163,8 +2168,13 @@ __device__ void moments_row(uint32_t r, int grp, const RoiList& rl, const FeatCf
 #pragma unroll
             for (int p = 0; p < 4; ++p)
 #pragma unroll
-                for (int k = 0; k < 4; ++k) N[p * 4 + k] += pw[p] * q[k];
+                for (int k = 0; k < 4; ++k)
+                    if (p + k >= 2) N[p * 4 + k] += pw[p] * q[k];
         });
+        // the order-0 / order-1 sums follow from the staged exact integer sums
+        N[0] = (double)W;
+        N[1] = (double)(SY - ay * W);
+        N[4] = (double)(SX - ax * W);
     }
     const long long gx0 = rl.gx[r], gy0 = rl.gy[r];
     double* o = out + (size_t)r * cfg.ncols + cfg.col_mom + grp * 52;
