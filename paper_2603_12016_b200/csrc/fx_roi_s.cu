@@ -2334,9 +2334,11 @@ __device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
     // integer thresholds for the integer values: v < mean <=> v < ceil(mean);
     // p10 <= v <= p90 <=> ceil(p10) <= v <= floor(p90) (exact: v < 2^16)
     const uint32_t t_mean = (uint32_t)ceil(mean), t_lo = (uint32_t)ceil(p10), t_hi = (uint32_t)floor(p90);
-    double a2 = 0, a3 = 0, a4 = 0, a5 = 0, a6 = 0, ent = 0;
-    unsigned long long best = 0, slo = 0, rsum = 0, usq = 0;
-    uint32_t clo = 0, rn = 0, run_v = 0, run_b = 0, pv_ = s[0], pb_ = bin_of(s[0]);
+    // m2 needs no pass: n^2 m2 = n sQ - sS^2 exactly (both < 2^64 for any n <= 65536);
+    // slo / rsum are 32-bit (an S window holds <= 4096 pixels: sums < 2^28)
+    double a3 = 0, a4 = 0, a5 = 0, a6 = 0, ent = 0;
+    unsigned long long best = 0, usq = 0;
+    uint32_t slo = 0, rsum = 0, clo = 0, rn = 0, run_v = 0, run_b = 0, pv_ = s[0], pb_ = bin_of(s[0]);
     const uint4* s4 = reinterpret_cast<const uint4*>(s);  // 16 B aligned (staging rounds to 8)
     uint4 nxt4 = s4[0];  // next 8 values in flight while these 8 are processed
     for (uint32_t q = 0; q * 8u < n; ++q) {
@@ -2352,7 +2354,6 @@ __device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
             if (q * 8u + (uint32_t)u >= n) break;
             const uint32_t v = (wv[u >> 1] >> ((u & 1) * 16)) & 0xffffu;
             const double d = (double)v - mean, d2 = d * d;
-            a2 += d2;
             a3 += d2 * d;
             a4 += d2 * d2;
             a5 += d2 * d2 * d;
@@ -2391,8 +2392,9 @@ __device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
     uint32_t d_hi, d_lo;
     kth_dev_pair(s, n, M2, d_hi, d_lo);
     const double median_ad = (n & 1) ? 0.5 * (double)d_hi : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
-    const double m2 = a2 / dn, m3 = a3 / dn, m4 = a4 / dn, m5 = a5 / dn, m6 = a6 / dn;
-    const double mad = ((double)(long long)(sS - 2 * slo) +
+    const double m2 = (double)((unsigned long long)n * sQ - sS * sS) / (dn * dn);
+    const double m3 = a3 / dn, m4 = a4 / dn, m5 = a5 / dn, m6 = a6 / dn;
+    const double mad = ((double)(long long)(sS - 2ull * slo) +
                         (double)((long long)clo - (long long)(n - clo)) * mean) / dn;
     double rmad = 0;
     if (rn > 0) {
