@@ -2448,10 +2448,13 @@ __device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
 // intensity statistics, [bi, bi + bm) the binary moments, the rest the weighted
 // moments, so the sparse waves overlap (and binary moments use the integer pipe
 // while the other two use fp64)
-#ifndef FXG_SERIAL_MINB
-#define FXG_SERIAL_MINB 5
+#ifndef FXG_SERIAL_TPB
+#define FXG_SERIAL_TPB 128
 #endif
-__global__ void __launch_bounds__(128, FXG_SERIAL_MINB)
+#ifndef FXG_SERIAL_MINB
+#define FXG_SERIAL_MINB (5 * 128 / FXG_SERIAL_TPB)
+#endif
+__global__ void __launch_bounds__(FXG_SERIAL_TPB, FXG_SERIAL_MINB)
     k_serial_stats(RoiList rl, Control* ctl, FeatCfg cfg, double* out, uint32_t bi, uint32_t bm) {
     const uint32_t b = blockIdx.x;
     const uint32_t t = (b < bi ? b : b < bi + bm ? b - bi : b - bi - bm) * blockDim.x + threadIdx.x;
@@ -2464,9 +2467,9 @@ __global__ void __launch_bounds__(128, FXG_SERIAL_MINB)
 void launch_serial_stats(int n_s, bool intensity, bool moments, cudaStream_t s, RoiList rl,
                          Control* ctl, FeatCfg cfg, double* out) {
     if (n_s <= 0 || (!intensity && !moments)) return;
-    const uint32_t nb = (uint32_t)((n_s + 127) / 128);
+    const uint32_t nb = (uint32_t)((n_s + FXG_SERIAL_TPB - 1) / FXG_SERIAL_TPB);
     const uint32_t bi = intensity ? nb : 0u, bm = moments ? nb : 0u;
-    k_serial_stats<<<bi + 2 * bm, 128, 0, s>>>(rl, ctl, cfg, out, bi, bm);
+    k_serial_stats<<<bi + 2 * bm, FXG_SERIAL_TPB, 0, s>>>(rl, ctl, cfg, out, bi, bm);
 }
 
 void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, FeatCfg cfg,
