@@ -319,3 +319,23 @@ def test_unstaged_in_warp_paths(oracle, monkeypatch):
             check(c, oracle, I, L, GROUPS)
     finally:
         c.close()
+
+
+@pytest.mark.parametrize("spread", [1, 3, 40])
+def test_tied_values_small_rois(ctx, oracle, spread):
+    """Heavy ties around the median (the median split of the median absolute
+    deviation, intensity_features.cpp:96-101) on ROIs of 1..16 pixels of both
+    parities, plus blob ROIs of a few hundred pixels over a handful of levels."""
+    rng = np.random.default_rng(spread)
+    L = np.zeros((96, 96), np.uint16)
+    lab = 1
+    for y in range(0, 96, 4):
+        for x in range(0, 96, 4):
+            keep = rng.random((4, 4)) < 0.45
+            L[y:y + 4, x:x + 4][keep] = lab
+            lab += 1
+    I = rng.integers(1000, 1000 + spread, size=L.shape, dtype=np.uint16)
+    check(ctx, oracle, I, L, ["intensity", "moments"])
+    Lb = fx.blob_mask_grid(512, 300, 100, 5)
+    Ib = rng.integers(7, 7 + spread, size=Lb.shape, dtype=np.uint16)
+    check(ctx, oracle, Ib, Lb, ["intensity", "moments"])
