@@ -18,8 +18,15 @@ CXX_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CXX_SRCS))
 HDRS     := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.hpp) $(wildcard include/*.h) \
             $(wildcard include/featurex_gpu/*.hpp)
 
-.PHONY: all lib oracle ref clean
-all: lib oracle
+.PHONY: all lib oracle ref synth clean
+all: lib oracle synth
+
+# bench / test tooling (synthetic inputs), not linked into libfxg.so
+SYNTH := tools/synth/_build/libfxsynth.so
+synth: $(SYNTH)
+$(SYNTH): tools/synth/fx_synth.cpp
+	@mkdir -p $(dir $@)
+	g++ -O2 -std=c++20 -fPIC -shared -Wall -Wextra -o $@ $<
 
 lib: $(LIB)
 
@@ -42,4 +49,4 @@ ref:
 	$(MAKE) -C oracle ref
 
 clean:
-	rm -rf $(OBJ) $(LIBDIR)
+	rm -rf $(OBJ) $(LIBDIR) tools/synth/_build

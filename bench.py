@@ -43,9 +43,9 @@ UNIT = "MP/s"
 
 
 def workload(seed_intensity: int):
-    import paper_2603_12016_b200 as fx
-    labels, roi_size = fx.packed_blob_mask_grid(IMAGE, ROI_SIZE0, ROI_COUNT, 1)
-    intensity = fx.uniform_u16(labels.shape, seed_intensity)
+    from tools import synth  # bench tooling (tools/synth), not the product library
+    labels, roi_size = synth.packed_blob_mask_grid(IMAGE, ROI_SIZE0, ROI_COUNT, 1)
+    intensity = synth.uniform_u16(labels.shape, seed_intensity)
     return intensity, labels, roi_size
 
 
@@ -127,6 +127,25 @@ def profiled_traffic(kernel):
     return norm.get(kernel)
 
 
+def roi_classes(labels):
+    """Per present label: pixel count and window class, by the rule the compaction
+    applies on the device (fx_scan.cu roi_class: S0 w<=33, h<=40, n<=768; S1/S2
+    w, h <= 64 split at n = 1024; else L).  Host-side, outside any timed region."""
+    ys, xs = np.nonzero(labels)
+    lab = labels[ys, xs].astype(np.int64)
+    n = np.bincount(lab, minlength=65536)
+    big = np.iinfo(np.int64).max
+    x0 = np.full(65536, big); x1 = np.full(65536, -1)
+    y0 = np.full(65536, big); y1 = np.full(65536, -1)
+    np.minimum.at(x0, lab, xs); np.maximum.at(x1, lab, xs)
+    np.minimum.at(y0, lab, ys); np.maximum.at(y1, lab, ys)
+    present = np.nonzero(n[1:])[0] + 1
+    n, w, h = n[present], (x1 - x0 + 1)[present], (y1 - y0 + 1)[present]
+    cls = np.where((w <= 33) & (h <= 40) & (n <= 768), 0,
+                   np.where((w <= 64) & (h <= 64), np.where(n <= 1024, 1, 2), 3))
+    return n, cls
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -149,7 +168,22 @@ def cpu_reference(intensity, labels, steps, warmup, threads=None):
         dt = time.perf_counter() - t0
         if i >= warmup:
             times.append(dt)
-    return times, threads, len(rl)
+    return times, threads, rl, rv
+
+
+def reference_sample(intensity, labels, steps, warmup, budget_s=60.0, full_step_s=1.2):
+    """Bounded per-step sample of the C2 image for the reference arm: the full
+    image when (steps + warmup) full steps fit the budget (~1.1 s each on 16
+    threads), else a band of whole rows sized to it (>= 512 rows).  Returns
+    (intensity, labels, description)."""
+    total = max(1, steps + warmup)
+    frac = min(1.0, budget_s / (total * full_step_s))
+    if frac >= 1.0:
+        return intensity, labels, "full C2 image per step"
+    rows = max(512, int(IMAGE * frac) // 256 * 256)
+    return (np.ascontiguousarray(intensity[:rows]), np.ascontiguousarray(labels[:rows]),
+            f"rows 0..{rows} of the C2 image per step ({rows}x{IMAGE}, labels cut at the band "
+            f"edge); MP/s on the band's pixels")
 
 
 def run_reference_arm(args, rank, world):
@@ -157,12 +191,12 @@ def run_reference_arm(args, rank, world):
         return
     intensity, labels, roi_size = workload(0)
     n_rois = int(np.count_nonzero(np.bincount(labels.ravel(), minlength=65536)[1:]))
-    # each step is one full C2 image (~1.1 s on 16 threads): the run stays bounded at
-    # <= 3 warm-up + 10 timed steps (~15 s) whatever --steps / --warmup ask for
-    steps, warmup = max(1, min(args.steps, 10)), min(args.warmup, 3)
-    times, threads, nr = cpu_reference(intensity, labels, steps, warmup)
+    steps, warmup = max(1, args.steps), args.warmup
+    I_s, L_s, sample = reference_sample(intensity, labels, steps, warmup)
+    times, threads, rl, _ = cpu_reference(I_s, L_s, steps, warmup)
+    nr = len(rl)
     t = float(np.sum(times))
-    mp = IMAGE * IMAGE / 1e6
+    mp = L_s.shape[0] * L_s.shape[1] / 1e6
     value = mp * len(times) / t
     line = {"impl": "reference", "metric": METRIC, "value": round(value, 3), "unit": UNIT,
             "n_gpus": world, "steps": len(times), "warmup": warmup,
@@ -172,11 +206,27 @@ def run_reference_arm(args, rank, world):
             "rois_per_s": round(nr * len(times) / t, 1),
             "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": threads,
                              "kind": "reference",
-                             "sample": f"full C2 image per step ({len(times)} steps, "
-                                       f"OpenMP over ROIs, {threads} threads)"},
+                             "sample": f"{sample} ({len(times)} steps, accumulate + OpenMP "
+                                       f"compute_roi_features over ROIs, {threads} threads)"},
             "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def spot_check(intensity, labels, gl, gv, rl, rv, cols, sample=2000, seed=0):
+    """tests/parity.py's comparator (bit-exact classes + tolerances with floors) on
+    a random sample of ROIs of the benchmarked image; labels compared in full."""
+    sys.path.insert(0, os.path.join(ROOT, "tests"))
+    from parity import compare, floors
+    if not np.array_equal(gl, rl):
+        return {"ok": False, "rois": int(len(rl)), "violations": ["label list differs"]}
+    pick = np.sort(np.random.default_rng(seed).choice(len(rl), min(sample, len(rl)),
+                                                      replace=False))
+    lab_pick = np.where(np.isin(labels, rl[pick]), labels, 0).astype(np.uint16)
+    s = floors(cols, rv[pick], intensity, lab_pick, rl[pick])
+    bad = compare(cols, gv[pick], rv[pick], s)
+    return {"ok": not bad, "rois_compared": int(len(pick)), "rois": int(len(rl)),
+            "violations": [f"{c} x{r:.3g} ({n} rows)" for c, r, n in bad[:8]]}
 
 
 def main():
@@ -304,24 +354,32 @@ def main():
     value = world * mp_step * args.steps / t_dev
     e2e_value = world * mp_step * e2e_steps / t_e2e
 
-    # roofline of the dominant kernel (largest share of device time)
+    # roofline of the dominant kernel (largest share of device time).  Algorithmic
+    # bytes are SURVEY.md 8(d)'s per-unit figures, independent of internal passes
+    # (DESIGN.md section 5): the label scan reads the label raster once (W*H*2); a
+    # per-ROI kernel reads its ROIs' member labels + intensities (n*4) and writes
+    # their feature rows (n_cols*8).  The internal passes (compaction, the serial
+    # passes over staged values) move no compulsory bytes and get no fraction.
     hbm, peak_src = peaks()
     dom_ms, dom_cnt = ktimes[dom_name]
     fg = int(np.count_nonzero(labels))
-    # per launch, SURVEY.md 8(d) per-unit figures split by kernel:
-    # the S kernels read each ROI pixel's label + intensity (4 B), stage 6 B per pixel
-    # (packed x,y,v for the moments pass, sorted value for the intensity pass) and
-    # write 7 intensity columns; the serial passes read their staged bytes and write
-    # their columns (32 intensity + 104 moments, one launch: k_serial_stats)
-    s_bytes = fg * 4 + fg * 6 + n_rois * 7 * 8
-    algo_bytes = {
-        "k_label_scan": h * w * 2,                      # label raster read once
-        "k_roi_s0": s_bytes, "k_roi_s1": s_bytes, "k_roi_s2": s_bytes,
-        "k_serial_stats": fg * 6 + n_rois * (32 + 104) * 8,
-    }
+    n_px, cls = roi_classes(labels)
+    per_roi = lambda c: int((n_px[cls == c] * 4).sum() + (cls == c).sum() * ncols * 8)
+    algo_bytes = {"k_label_scan": h * w * 2, "k_roi_s0": per_roi(0), "k_roi_s1": per_roi(1),
+                  "k_roi_s2": per_roi(2), "k_roi_b": per_roi(3)}
     per_launch_s = dom_ms / 1e3 / max(1, dom_cnt)
-    achieved = algo_bytes.get(dom_name, h * w * 4 + n_rois * ncols * 8) / per_launch_s / 1e9
+    achieved = algo_bytes.get(dom_name, 0) / per_launch_s / 1e9
     call_bytes = h * w * 4 + n_rois * ncols * 8
+    call_gbs = call_bytes / (t_dev / args.steps) / 1e9
+    kernels = {}
+    for k, (ms, cnt) in sorted(kall.items(), key=lambda kv: -kv[1][0]):
+        per = ms / 1e3 / max(1, cnt)
+        ab = algo_bytes.get(k)
+        kernels[k] = {"ms_per_step": round(ms / bd_steps, 4),
+                      "share": round(ms / max(1e-12, sum(v[0] for v in kall.values())), 4),
+                      "algorithmic_bytes": ab,
+                      "gbs": round(ab / per / 1e9, 1) if ab else None,
+                      "frac": round(ab / per / 1e9 / hbm, 4) if ab else None}
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
@@ -329,27 +387,36 @@ def main():
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": config_dict(roi_size, n_rois, fg / (h * w), world),
         "rois_per_s": round(world * n_rois * args.steps / t_dev, 1),
-        "featurize_hbm_gbs": round(call_bytes / (t_dev / args.steps) / 1e9, 1),
+        "featurize_hbm_gbs": round(call_gbs, 1),
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT,
                 "h2d_bytes_per_step": int(2 * h * w * 2),
                 "d2h_bytes_per_step": int(n_rois * ncols * 8 + n_rois * 4),
                 "steps": e2e_steps},
         "gpu_launches": int(launches),
-        "kernels_ms_per_step": {k: round(v[0] / bd_steps, 4) for k, v in kall.items()},
+        "kernels": kernels,
         "kernels_note": f"per-kernel split from a separate {bd_steps}-step pass with every "
                         f"kernel event-timed; the timed region times only {dom_name}",
         "roofline": {"kernel": dom_name, "bound": "hbm", "achieved": round(achieved, 1),
                      "peak": hbm, "unit": "GB/s", "frac": round(achieved / hbm, 4),
                      "traffic": profiled_traffic(dom_name), "peak_source": peak_src,
-                     "algorithmic_bytes_per_launch": int(algo_bytes.get(dom_name, call_bytes))},
+                     "algorithmic_bytes_per_launch": int(algo_bytes.get(dom_name, 0)),
+                     "call": {"achieved": round(call_gbs, 1), "frac": round(call_gbs / hbm, 4),
+                              "bytes": int(call_bytes),
+                              "note": "whole fx_featurize call: W*H*4 + n_rois*n_cols*8 over "
+                                      "ms_per_step"}},
         "clocks": clk.summary(),
     }
     if not args.no_cpu_baseline and world == 1:
-        times, threads, _ = cpu_reference(intensity, labels, 1, 0)
+        times, threads, rl, rv = cpu_reference(intensity, labels, 1, 0)
         line["cpu_baseline"] = {"value": round(mp_step / times[0], 3), "unit": UNIT,
                                 "cores": threads, "kind": "reference",
                                 "sample": "one full C2 image (in-memory accumulate + OpenMP "
                                           "compute_roi_features, oracle/_ref)"}
+        # parity spot check of the benchmarked output (outside every timed region):
+        # the device table of the last device step against the reference's table
+        line["parity_spot_check"] = spot_check(
+            intensity, labels, d_ol.cpu().numpy().view(np.uint32), d_out.cpu().numpy(),
+            rl, rv, fx.feature_columns(gmask, params))
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()

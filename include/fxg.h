@@ -242,16 +242,6 @@ int fx_debug_phase_clocks(unsigned long long* out, int n, int reset);
  * 1 GLRLM (other), 2 GLSZM, 3 NGTDM, 4 GLRLM run counting, 5 GLRLM features. */
 int fx_debug_texture_clocks(unsigned long long* out, int n, int reset);
 
-/* ---- synthetic inputs (the reference's synth.hpp generators) --------------- */
-
-/* blob_mask_grid (synth.hpp:22-26): disk-with-ears blobs on a grid, labels
- * 1..roi_count; FX_E_CONFIG (PackingError) when it cannot pack. */
-int fx_synth_blob_mask_grid(int image_size, int roi_size, int roi_count, uint64_t seed,
-                            uint16_t* out);
-/* siemens_star (synth.hpp:18-20) */
-int fx_synth_siemens_star(int size, int spokes, uint16_t* out);
-/* uniform uint16: std::mt19937_64(seed)() & 0xffff in row-major order */
-int fx_synth_uniform_u16(uint64_t seed, size_t n, uint16_t* out);
 
 #ifdef __cplusplus
 }

@@ -10,6 +10,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstddef>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -172,10 +173,11 @@ LabelTable label_table(fx_ctx* c) {
     return t;
 }
 
-CompactArgs compact_args(fx_ctx* c, uint32_t own_y0, uint32_t own_y1) {
+CompactArgs compact_args(fx_ctx* c, uint32_t own_y0, uint32_t own_y1, size_t cap_rows = ~size_t(0)) {
     const size_t nb = (size_t)c->tab_slots * kBlocksPerSlot;
     uint32_t* b = c->d_csum;
-    return CompactArgs{own_y0,     own_y1,     b, b + nb, b + 3 * nb, b + 2 * nb,
+    const uint32_t cap = (uint32_t)std::min<size_t>(cap_rows, 0xffffffffu);
+    return CompactArgs{own_y0,     own_y1,     cap, b, b + nb, b + 3 * nb, b + 2 * nb,
                        b + 3 * nb + c->tab_slots + 1};
 }
 
@@ -443,7 +445,8 @@ int ensure_moments(fx_ctx* c, size_t img_pixels) {
         c->d_mom_off = nullptr;
         c->d_mom_sums = nullptr;
         c->mom_cap = c->mom_off_cap = 0;
-        CK(cudaMalloc(&c->d_mom_px, want * sizeof(uint32_t)));
+        // +4 elements: the serial pass reads staged pixels in 16 B vectors
+        CK(cudaMalloc(&c->d_mom_px, (want + 4) * sizeof(uint32_t)));
         CK(cudaMalloc(&c->d_mom_off, c->roi_cap * sizeof(unsigned long long)));
         CK(cudaMalloc(&c->d_mom_sums, c->roi_cap * 5 * sizeof(unsigned long long)));
         c->mom_cap = want;
@@ -463,7 +466,8 @@ int ensure_intensity(fx_ctx* c, size_t img_pixels) {
         c->d_int_off = nullptr;
         c->d_int_sums = nullptr;
         c->int_cap = c->int_off_cap = 0;
-        CK(cudaMalloc(&c->d_int_vals, want * sizeof(uint16_t)));
+        // +8 elements: the serial pass reads staged values in 16 B vectors
+        CK(cudaMalloc(&c->d_int_vals, (want + 8) * sizeof(uint16_t)));
         CK(cudaMalloc(&c->d_int_off, c->roi_cap * sizeof(unsigned long long)));
         CK(cudaMalloc(&c->d_int_sums, c->roi_cap * 2 * sizeof(unsigned long long)));
         c->int_cap = want;
@@ -506,15 +510,18 @@ int scan_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, bool reset) {
     return FX_OK;
 }
 
-// compaction of the table (slots of m) into the ROI list; consumes the table
-int compact_stage(fx_ctx* c, const SlotMap& m, uint32_t own_y0, uint32_t own_y1) {
+// compaction of the table (slots of m) into the ROI list; consumes the table.
+// More ROIs than cap_rows: none is queued for the per-ROI kernels (kErrOutCap).
+// first: the first stage of an API call also clears the sticky error word.
+int compact_stage(fx_ctx* c, const SlotMap& m, uint32_t own_y0, uint32_t own_y1, size_t cap_rows,
+                  bool first) {
     LabelTable t = label_table(c);
     RoiList rl = roi_list(c);
-    const CompactArgs ca = compact_args(c, own_y0, own_y1);
+    const CompactArgs ca = compact_args(c, own_y0, own_y1, cap_rows);
     cudaStream_t s = c->stream;
     const int nb = m.nslots * kBlocksPerSlot;
     const int grid = std::min(nb, 2 * c->sm_count);
-    CK(cudaMemsetAsync(c->d_ctl, 0, sizeof(Control), s));
+    CK(cudaMemsetAsync(c->d_ctl, 0, first ? sizeof(Control) : offsetof(Control, error), s));
     {
         Launch l(c, "k_compact_count");
         k_compact_count<<<grid, 1024, m.nslots * sizeof(uint32_t), s>>>(t, c->d_ctl, ca, m.nslots);
@@ -533,7 +540,7 @@ int compact_stage(fx_ctx* c, const SlotMap& m, uint32_t own_y0, uint32_t own_y1)
 int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t own_y0,
                     uint32_t own_y1, unsigned groups, const fx_texture_params& p, double* out_dev,
                     size_t cap_rois, size_t* n_rois, const DebugOut* dbg_dev,
-                    uint32_t* slot_base = nullptr) {
+                    uint32_t* slot_base = nullptr, bool first = true) {
     FeatCfg cfg = make_cfg(groups, p);
     if (cfg.col_shape >= 0) {
         const int rs = ensure_shape(c);
@@ -562,7 +569,7 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
     const int vrc = validate_texture(groups, p);
     RoiList rl = roi_list(c);
     cudaStream_t s = c->stream;
-    int rc0 = compact_stage(c, m, own_y0, own_y1);
+    int rc0 = compact_stage(c, m, own_y0, own_y1, cap_rois, first);
     if (rc0) return rc0;
     CK(cudaEventRecord(c->ev_compact, s));
     CK(cudaStreamWaitEvent(c->side, c->ev_compact, 0));
@@ -593,7 +600,8 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
     }
     CK(cudaGetLastError());
     // the class counts arrive while S0 runs; S1 / S2 launch only when they have ROIs
-    // (an empty persistent grid still costs ~7 us)
+    // (an empty persistent grid still costs ~7 us).  With more ROIs than cap_rois the
+    // compaction queued none, so S0 found no work and wrote no row.
     CK(cudaEventSynchronize(c->ev_stats));
     const Control hc = *c->h_ctl;
     for (int cls = kClassS1; cls <= kClassS2; ++cls) {
@@ -716,6 +724,8 @@ int finish(fx_ctx* c) {
         return set_error(FX_E_CAPACITY, "a large ROI exceeded the L-path slab");
     if (c->h_ctl->error & kErrRuns)
         return set_error(FX_E_CAPACITY, "a large ROI exceeded the run-list capacity");
+    if (c->h_ctl->error & kErrOutCap)
+        return set_error(FX_E_CAPACITY, "more ROIs than output rows");
     return FX_OK;
 }
 
@@ -1280,7 +1290,8 @@ int fx_featurize_batch(fx_ctx* c, const fx_image* ims, int n, unsigned groups,
         rc = scan_stage(c, d, m, true);
         if (!rc)
             rc = featurize_stage(c, d, m, 0u, 0xffffffffu, groups, *p, out_dev + base * cfg.ncols,
-                                 cap_rois >= base ? cap_rois - base : 0, &nr, nullptr, sb.data());
+                                 cap_rois >= base ? cap_rois - base : 0, &nr, nullptr, sb.data(),
+                                 k == 0);
         if (rc) {
             if (rc == FX_E_CAPACITY) row_offsets[n] = base + nr;  // rows needed so far
             break;
@@ -1420,7 +1431,7 @@ int fx_roi_table(fx_ctx* c, const fx_image* im, uint32_t* out_labels, uint64_t* 
     cudaStream_t s = c->stream;
     const SlotMap m = single_map(d);
     rc = scan_stage(c, d, m, true);
-    if (!rc) rc = compact_stage(c, m, 0u, 0xffffffffu);
+    if (!rc) rc = compact_stage(c, m, 0u, 0xffffffffu, ~size_t(0), true);
     if (rc) return rc;
     CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
     CK(cudaStreamSynchronize(s));

@@ -89,7 +89,6 @@ struct Control {
     uint32_t class_next[kNumClasses];
     uint32_t overflow_count;  // S ROIs re-queued to the L path (run capacity)
     uint32_t overflow_next;
-    uint32_t error;           // bit flags, see kErr*
     uint32_t l_max_h;         // max window height among L ROIs
     uint32_t l_max_wpr;       // max 64-bit words per row among L ROIs
     unsigned long long l_max_n;      // max pixel count among L ROIs
@@ -97,6 +96,10 @@ struct Control {
     uint32_t t_next[2];              // GLRLM/GLSZM/NGTDM work counters (S lists, L list)
     unsigned long long mom_alloc;    // moments: pixels staged so far (bump allocator)
     unsigned long long int_alloc;    // intensity: sorted values staged so far
+    // sticky across the sub-batches of one API call: compact_stage clears only the
+    // fields above (offsetof(Control, error) bytes); the call's first stage clears all
+    uint32_t error;                  // bit flags, see kErr*
+    uint32_t pad_;
 };
 
 // compaction scratch: per (slot, 1024-label block) counts and exclusive bases
@@ -106,11 +109,13 @@ constexpr uint32_t kBlockLive = 0x80000000u;  // block_sum flag: block <= maxlab
 constexpr uint32_t kErrCapacity = 1u;  // L slab too small for a ROI
 constexpr uint32_t kErrRuns = 2u;      // L run capacity exceeded
 constexpr uint32_t kErrWindow = 4u;    // an owned ROI window is not inside the image
+constexpr uint32_t kErrOutCap = 8u;    // more ROIs than output rows: no per-ROI kernel ran
 
 // compaction parameters: owned row range (band sharding; [0, ~0) = all), in
 // global coordinates, and the scratch arrays
 struct CompactArgs {
     uint32_t own_y0, own_y1;
+    uint32_t cap_rows;     // output rows available; above it no ROI is queued (kErrOutCap)
     uint32_t* block_sum;   // [nslots*64]
     uint32_t* block_base;  // [nslots*64]
     uint32_t* slot_base;   // [nslots+1] first output row of each slot, + total

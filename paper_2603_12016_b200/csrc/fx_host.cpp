@@ -1,5 +1,5 @@
 // Pure host parts of the C ABI: profiles, group resolution, column names,
-// error state and the synthetic-input generators.  No device code here.
+// error state.  No device code here.
 #include <algorithm>
 #include <cmath>
 #include <cstring>
@@ -111,50 +111,6 @@ std::vector<std::string> column_names(unsigned groups, const fx_texture_params& 
     return cols;
 }
 
-// ---- synthetic inputs: the reference generators (synth.cpp), re-derived ----
-
-namespace {
-
-// Disk of radius r with two triangular ears (apex ~1.8 r), rotated by phi.
-int paint_blob(uint16_t* lab, int size, double cx, double cy, double r, double phi,
-               uint16_t label) {
-    const int reach = static_cast<int>(std::ceil(r * 1.9)) + 1;
-    const double c = std::cos(phi), s = std::sin(phi);
-    int painted = 0;
-    const int ylo = std::max(0, static_cast<int>(cy) - reach);
-    const int yhi = std::min(size - 1, static_cast<int>(cy) + reach);
-    const int xlo = std::max(0, static_cast<int>(cx) - reach);
-    const int xhi = std::min(size - 1, static_cast<int>(cx) + reach);
-    for (int y = ylo; y <= yhi; ++y) {
-        for (int x = xlo; x <= xhi; ++x) {
-            const double dx = x - cx, dy = y - cy;
-            const double u = dx * c + dy * s;
-            const double v = -dx * s + dy * c;
-            bool in = u * u + v * v <= r * r;
-            for (int sg = -1; !in && sg <= 1; sg += 2) {
-                const double du = u - sg * r * 0.62, dv = v - (-r * 0.62);
-                const double along = (sg * du - dv) / std::numbers::sqrt2;
-                const double across = std::abs((sg * du + dv) / std::numbers::sqrt2);
-                const double height = r * 0.95;
-                in = along >= 0 && along <= height && across <= 0.55 * r * (1.0 - along / height);
-            }
-            if (in) {
-                lab[static_cast<size_t>(y) * size + x] = label;
-                ++painted;
-            }
-        }
-    }
-    return painted;
-}
-
-int blob_area(double r, double phi) {
-    const int size = static_cast<int>(std::ceil(r * 4)) + 8;
-    std::vector<uint16_t> probe(static_cast<size_t>(size) * size, 0);
-    return paint_blob(probe.data(), size, size / 2.0, size / 2.0, r, phi, 1);
-}
-
-}  // namespace
-
 }  // namespace fxg
 
 using namespace fxg;
@@ -232,58 +188,6 @@ int fx_columns(unsigned groups, const fx_texture_params* params, char* buf, size
         if (cap < joined.size() + 1) return set_error(FX_E_CAPACITY, "column buffer too small");
         std::memcpy(buf, joined.c_str(), joined.size() + 1);
     }
-    return FX_OK;
-}
-
-int fx_synth_blob_mask_grid(int image_size, int roi_size, int roi_count, uint64_t seed,
-                            uint16_t* out) {
-    if (!out) return set_error(FX_E_ARG, "null argument");
-    if (image_size < 16) return set_error(FX_E_CONFIG, "image size must be >= 16");
-    if (roi_count < 1 || roi_size < 1) return set_error(FX_E_CONFIG, "empty synth spec");
-    if (roi_count > 65535) return set_error(FX_E_CONFIG, "too many ROIs for 16-bit labels");
-    if (static_cast<double>(roi_count) * roi_size > 0.9 * static_cast<double>(image_size) * image_size)
-        return set_error(FX_E_CONFIG, "roi_count * roi_size exceeds image capacity");
-    double lo = 0.5, hi = std::sqrt(static_cast<double>(roi_size));
-    while (blob_area(hi, 0.0) < roi_size) hi *= 1.5;
-    for (int it = 0; it < 40; ++it) {
-        const double mid = (lo + hi) / 2.0;
-        if (blob_area(mid, 0.0) < roi_size) lo = mid;
-        else hi = mid;
-    }
-    const double r = (lo + hi) / 2.0;
-    const int cell = static_cast<int>(std::ceil(2.0 * 1.9 * r)) + 4;
-    const int gd = static_cast<int>(std::ceil(std::sqrt(static_cast<double>(roi_count))));
-    if (gd * cell > image_size) return set_error(FX_E_CONFIG, "blob grid does not fit the image");
-    std::memset(out, 0, static_cast<size_t>(image_size) * image_size * sizeof(uint16_t));
-    std::mt19937_64 rng(seed);
-    std::uniform_real_distribution<double> rot(0.0, 2.0 * std::numbers::pi);
-    for (int i = 0; i < roi_count; ++i) {
-        const double cx = (i % gd) * cell + cell / 2.0;
-        const double cy = (i / gd) * cell + cell / 2.0;
-        paint_blob(out, image_size, cx, cy, r, rot(rng), static_cast<uint16_t>(i + 1));
-    }
-    return FX_OK;
-}
-
-int fx_synth_siemens_star(int size, int spokes, uint16_t* out) {
-    if (!out) return set_error(FX_E_ARG, "null argument");
-    if (size < 1) return set_error(FX_E_CONFIG, "star size must be >= 1");
-    if (spokes < 2 || spokes % 2) return set_error(FX_E_CONFIG, "spoke count must be even and >= 2");
-    const double c = (size - 1) / 2.0, two_pi = 2.0 * std::numbers::pi;
-    for (int y = 0; y < size; ++y)
-        for (int x = 0; x < size; ++x) {
-            double th = std::atan2(static_cast<double>(y) - c, static_cast<double>(x) - c);
-            if (th < 0) th += two_pi;
-            const int sector = static_cast<int>(spokes * th / two_pi);
-            out[static_cast<size_t>(y) * size + x] = (sector % 2 == 0) ? 65535 : 0;
-        }
-    return FX_OK;
-}
-
-int fx_synth_uniform_u16(uint64_t seed, size_t n, uint16_t* out) {
-    if (!out && n) return set_error(FX_E_ARG, "null argument");
-    std::mt19937_64 rng(seed);
-    for (size_t i = 0; i < n; ++i) out[i] = static_cast<uint16_t>(rng() & 0xffffu);
     return FX_OK;
 }
 

@@ -30,13 +30,16 @@ struct CacheEnt {
     uint32_t label, cnt, x0, x1, y0, y1;
 };
 
-__device__ __noinline__ void global_fold(const LabelTable& t, const CacheEnt& e) {
-    if (!e.label) return;
-    atomicAdd(&t.cnt[e.label], (unsigned long long)e.cnt);
-    atomicMin(&t.xmin[e.label], e.x0);
-    atomicMax(&t.xmax[e.label], e.x1);
-    atomicMin(&t.ymin[e.label], e.y0);
-    atomicMax(&t.ymax[e.label], e.y1);
+// Everything below is inlined and takes the cache by value-in-registers: an
+// earlier version passed the cache by reference into __noinline__ helpers, which
+// made it address-taken (120 B of stack, LDL/STL on every nonzero chunk).
+__device__ __forceinline__ void global_fold(const LabelTable& t, uint32_t l, uint32_t cnt,
+                                            uint32_t x0, uint32_t x1, uint32_t y0, uint32_t y1) {
+    atomicAdd(&t.cnt[l], (unsigned long long)cnt);
+    atomicMin(&t.xmin[l], x0);
+    atomicMax(&t.xmax[l], x1);
+    atomicMin(&t.ymin[l], y0);
+    atomicMax(&t.ymax[l], y1);
 }
 
 // fold a run summary (label, count, first x, last x) of row y into the cache
@@ -54,18 +57,23 @@ __device__ __forceinline__ void cache_put(CacheEnt& c0, CacheEnt& c1, const Labe
         c1.x1 = max(c1.x1, xb);
         c1.y1 = y;
     } else {
-        global_fold(t, c1);
+        if (c1.label) global_fold(t, c1.label, c1.cnt, c1.x0, c1.x1, c1.y0, c1.y1);
         c1 = c0;
         c0 = CacheEnt{l, cnt, xa, xb, y, y};
     }
 }
 
-// several distinct labels inside one 8-px chunk: per pixel
-__device__ __noinline__ void chunk_slow(uint4 v, uint32_t x, uint32_t y, uint32_t sb,
-                                        CacheEnt& c0, CacheEnt& c1, const LabelTable& t) {
-    const uint32_t wv[4] = {v.x, v.y, v.z, v.w};
-    for (int k = 0; k < 8; ++k) {
-        const uint32_t l = (wv[k >> 1] >> (16 * (k & 1))) & 0xffffu;
+// several distinct labels inside one 8-px chunk: per pixel, the chunk shifted
+// through a register pair (no runtime-indexed array)
+__device__ __forceinline__ void chunk_slow(uint4 v, uint32_t x, uint32_t y, uint32_t sb,
+                                           CacheEnt& c0, CacheEnt& c1, const LabelTable& t) {
+    unsigned long long q0 = v.x | ((unsigned long long)v.y << 32);
+    unsigned long long q1 = v.z | ((unsigned long long)v.w << 32);
+#pragma unroll 1
+    for (uint32_t k = 0; k < 8; ++k) {
+        const uint32_t l = (uint32_t)q0 & 0xffffu;
+        q0 = (q0 >> 16) | (q1 << 48);
+        q1 >>= 16;
         if (l) cache_put(c0, c1, t, sb | l, 1u, x + k, x + k, y);
     }
 }
@@ -119,7 +127,7 @@ __device__ __forceinline__ void warp_flush(const CacheEnt& e, const LabelTable& 
         const uint32_t x1 = __reduce_max_sync(kFull, mine ? e.x1 : 0u);
         const uint32_t y0 = __reduce_min_sync(kFull, mine ? e.y0 : 0xffffffffu);
         const uint32_t y1 = __reduce_max_sync(kFull, mine ? e.y1 : 0u);
-        if ((int)lane == leader) global_fold(t, CacheEnt{L, cnt, x0, x1, y0, y1});
+        if ((int)lane == leader) global_fold(t, L, cnt, x0, x1, y0, y1);
     }
 }
 
@@ -265,6 +273,10 @@ __global__ void __launch_bounds__(1024) k_compact_emit(LabelTable t, Control* ct
     __shared__ uint32_t warp_cnt[32];
     const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint32_t n_live = a.done[1];
+    // more ROIs than output rows: the table is still consumed and the ROI list
+    // written, but no ROI is queued, so no per-ROI kernel writes a row
+    const bool fits = ctl->n_rois <= a.cap_rows;
+    if (!fits && blockIdx.x == 0 && tid == 0) atomicOr(&ctl->error, kErrOutCap);
     for (uint32_t i = blockIdx.x; i < n_live; i += gridDim.x) {
         const uint32_t pair = a.live[i];
         const uint32_t slot = pair / kBlocksPerSlot, blk = pair % kBlocksPerSlot;
@@ -307,6 +319,7 @@ __global__ void __launch_bounds__(1024) k_compact_emit(LabelTable t, Control* ct
         r.w[rank] = w;
         r.h[rank] = h;
         r.n[rank] = n;
+        if (!fits) continue;
         const int c = roi_class(w, h, n);
         // one atomic per (warp, class): the class lists are consumed in any order
         const unsigned peers = __match_any_sync(__activemask(), c);
@@ -315,7 +328,11 @@ __global__ void __launch_bounds__(1024) k_compact_emit(LabelTable t, Control* ct
         if ((int)lane == leader) base = atomicAdd(&ctl->class_count[c], (uint32_t)__popc(peers));
         base = __shfl_sync(peers, base, leader);
         const uint32_t pos = base + __popc(peers & lanemask_lt());
-        r.cls_list[c][pos] = rank;
+        // select, not a runtime index into the kernel-parameter array (a local copy)
+        uint32_t* lst = c == kClassS0 ? r.cls_list[kClassS0]
+                        : c == kClassS1 ? r.cls_list[kClassS1]
+                        : c == kClassS2 ? r.cls_list[kClassS2] : r.cls_list[kClassL];
+        lst[pos] = rank;
         if (c == kClassL) {
             atomicMax(&ctl->l_max_h, h);
             atomicMax(&ctl->l_max_wpr, (w + 63) / 64);

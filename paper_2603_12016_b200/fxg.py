@@ -21,7 +21,6 @@ ERRORS = {1: "ConfigError", 2: "UnknownProfile", 3: "PairingError", 4: "IoError"
 MEM_HOST, MEM_DEVICE = 0, 1
 GROUP_BITS = {"intensity": 1, "shape": 2, "moments": 4, "glcm": 8, "glrlm": 16, "glszm": 32,
               "ngtdm": 64}
-DEVICE_GROUPS = ("intensity", "moments", "glcm")
 
 
 class FxError(RuntimeError):
@@ -353,36 +352,3 @@ class Context:
                                   _p(hist, C.c_uint64), _p(edge, C.c_int32), C.c_size_t(cap_edge),
                                   C.byref(ne), _p(glcm, C.c_uint32), _p(pairs, C.c_uint64)))
         return hist, edge[: 2 * ne.value].reshape(-1, 2), glcm.reshape(A, ng, ng), pairs
-
-
-# ---- synthetic inputs (synth.hpp generators) ---------------------------------
-
-def blob_mask_grid(image_size: int, roi_size: int, roi_count: int, seed: int = 1) -> np.ndarray:
-    out = np.zeros((image_size, image_size), np.uint16)
-    _check(lib().fx_synth_blob_mask_grid(image_size, roi_size, roi_count, C.c_uint64(seed),
-                                         _p(out, C.c_uint16)))
-    return out
-
-
-def packed_blob_mask_grid(image_size: int, roi_size: int, roi_count: int, seed: int = 1):
-    """blob_mask_grid, shrinking roi_size by 10% until it packs."""
-    rs = roi_size
-    while True:
-        try:
-            return blob_mask_grid(image_size, rs, roi_count, seed), rs
-        except FxError:
-            rs = int(rs * 0.9)
-            if rs < 1:
-                raise
-
-
-def siemens_star(size: int, spokes: int = 8) -> np.ndarray:
-    out = np.zeros((size, size), np.uint16)
-    _check(lib().fx_synth_siemens_star(size, spokes, _p(out, C.c_uint16)))
-    return out
-
-
-def uniform_u16(shape, seed: int = 0) -> np.ndarray:
-    out = np.zeros(shape, np.uint16)
-    _check(lib().fx_synth_uniform_u16(C.c_uint64(seed), C.c_size_t(out.size), _p(out, C.c_uint16)))
-    return out

@@ -47,30 +47,43 @@ HARALICK_UNIT = ("clushade", "corr", "infomeas1")
 def _moment_scales(intensity, labels, roi_labels, reference_frame=True):
     """Per ROI, binary and weighted: s_pq = sum w (lx+lcx)^p (ly+lcy)^q (the
     reference's binomial-shift scale) or, with reference_frame=False, the
-    natural scale sum w |x-cx|^p |y-cy|^q."""
+    natural scale sum w |x-cx|^p |y-cy|^q.  Vectorised over all ROIs (bincount),
+    so full-size images (C2: 50k ROIs, 14M pixels) take seconds."""
+    roi_labels = np.asarray(roi_labels)
+    out = np.zeros((len(roi_labels), 2, 4, 4))
+    if len(roi_labels) == 0:
+        return out
     ys, xs = np.nonzero(labels)
     lab = labels[ys, xs]
+    keep = np.isin(lab, roi_labels)
+    ys, xs, lab = ys[keep], xs[keep], lab[keep]
+    k = np.searchsorted(roi_labels, lab)
+    n = len(roi_labels)
+    x, y = xs.astype(np.float64), ys.astype(np.float64)
     val = intensity[ys, xs].astype(np.float64)
-    order = np.argsort(lab, kind="stable")
-    lab, xs, ys, val = lab[order], xs[order].astype(np.float64), ys[order].astype(np.float64), val[order]
-    bounds = np.searchsorted(lab, roi_labels), np.searchsorted(lab, roi_labels, side="right")
-    out = np.zeros((len(roi_labels), 2, 4, 4))
-    for k, (a, b) in enumerate(zip(*bounds)):
-        x, y, v = xs[a:b], ys[a:b], val[a:b]
-        for g, w in enumerate((np.ones_like(v), v)):
-            m = w.sum()
-            if m <= 0:
-                continue
+    xmin = np.full(n, np.inf)
+    ymin = np.full(n, np.inf)
+    np.minimum.at(xmin, k, x)
+    np.minimum.at(ymin, k, y)
+    for g, w in enumerate((np.ones_like(val), val)):
+        m = np.bincount(k, w, minlength=n)
+        with np.errstate(divide="ignore", invalid="ignore"):
             if reference_frame:
-                lx, ly = x - x.min(), y - y.min()
-                ax = lx + (w * lx).sum() / m
-                ay = ly + (w * ly).sum() / m
+                lx, ly = x - xmin[k], y - ymin[k]
+                ax = lx + (np.bincount(k, w * lx, minlength=n) / m)[k]
+                ay = ly + (np.bincount(k, w * ly, minlength=n) / m)[k]
             else:
-                ax = np.abs(x - (w * x).sum() / m)
-                ay = np.abs(y - (w * y).sum() / m)
-            for p in range(4):
-                for q in range(4):
-                    out[k, g, p, q] = (w * ax ** p * ay ** q).sum()
+                ax = np.abs(x - (np.bincount(k, w * x, minlength=n) / m)[k])
+                ay = np.abs(y - (np.bincount(k, w * y, minlength=n) / m)[k])
+        ok = (m > 0)[k]
+        ax, ay, ww = ax[ok], ay[ok], w[ok]
+        kk = k[ok]
+        px = [np.ones_like(ax), ax, ax * ax, ax * ax * ax]
+        py = [np.ones_like(ay), ay, ay * ay, ay * ay * ay]
+        for p in range(4):
+            wp = ww * px[p]
+            for q in range(4):
+                out[:, g, p, q] = np.bincount(kk, wp * py[q], minlength=n)
     return out
 
 

@@ -11,6 +11,7 @@ import inputs
 from parity import assert_parity
 
 import paper_2603_12016_b200 as fx
+from tools import synth
 from oracle import make_params as oparams
 
 pytestmark = pytest.mark.gpu
@@ -33,21 +34,21 @@ def check(ctx, oracle, I, L, groups, profile="default", **over):
 
 @pytest.mark.parametrize("profile", ["default", "performance", "ibsi-like"])
 def test_c1_blob_grid_all_groups(ctx, oracle, profile):
-    L = fx.blob_mask_grid(1024, 421, 500, 1)
-    I = fx.uniform_u16(L.shape, 0)
+    L = synth.blob_mask_grid(1024, 421, 500, 1)
+    I = synth.uniform_u16(L.shape, 0)
     gl, _ = check(ctx, oracle, I, L, GROUPS, profile)
     assert len(gl) == 500
 
 
 @pytest.mark.parametrize("groups", [["intensity"], ["moments"], ["glcm"], ["intensity", "glcm"]])
 def test_group_subsets(ctx, oracle, groups):
-    L = fx.blob_mask_grid(512, 300, 100, 7)
-    I = fx.siemens_star(512)
+    L = synth.blob_mask_grid(512, 300, 100, 7)
+    I = synth.siemens_star(512)
     check(ctx, oracle, I, L, groups)
 
 
 def test_tertiary_intensities(ctx, oracle):
-    L, _ = fx.packed_blob_mask_grid(768, 600, 250, 3)
+    L, _ = synth.packed_blob_mask_grid(768, 600, 250, 3)
     I = inputs.per_roi_levels(L, 5)
     check(ctx, oracle, I, L, GROUPS)
 
@@ -77,7 +78,7 @@ def _value_distributions(shape):
 
 @pytest.mark.parametrize("law", ["narrow", "twelve_bit", "bimodal", "outliers"])
 def test_value_sort_branches(ctx, oracle, law):
-    L, _ = fx.packed_blob_mask_grid(1024, 700, 300, 5)
+    L, _ = synth.packed_blob_mask_grid(1024, 700, 300, 5)
     I = _value_distributions(L.shape)[law]
     check(ctx, oracle, I, L, ["intensity", "moments"])
     check(ctx, oracle, I, L, GROUPS)
@@ -108,13 +109,13 @@ def test_large_roi_l_path(ctx, oracle):
 
 
 def test_odd_width_no_tma(ctx, oracle):
-    L = fx.blob_mask_grid(331, 200, 40, 2)[:, :329].copy()
+    L = synth.blob_mask_grid(331, 200, 40, 2)[:, :329].copy()
     I = inputs.uniform(L.shape, 4)
     check(ctx, oracle, I, L, GROUPS)
 
 
 def test_histogram_bins_and_offsets(ctx, oracle):
-    L = fx.blob_mask_grid(256, 220, 25, 5)
+    L = synth.blob_mask_grid(256, 220, 25, 5)
     I = inputs.uniform(L.shape, 6)
     for over in [dict(histogram_bins=2), dict(histogram_bins=1000), dict(offset=2),
                  dict(ng=2), dict(ng=7, symmetric=False, angles=(135, 0, 45)),
@@ -130,7 +131,7 @@ def test_empty_mask(ctx):
 
 
 def test_label_scan_bit_exact(ctx, oracle):
-    for L in [fx.blob_mask_grid(1024, 421, 500, 1), inputs.random_labels((77, 1003), 300, 3),
+    for L in [synth.blob_mask_grid(1024, 421, 500, 1), inputs.random_labels((77, 1003), 300, 3),
               inputs.random_blobs((257, 513), 200, seed=4,
                                   label_values=np.array([1, 2, 65535, 40000, 17]))]:
         gl, gc, gb = ctx.roi_table(np.zeros_like(L), L)
@@ -140,7 +141,7 @@ def test_label_scan_bit_exact(ctx, oracle):
 
 def test_debug_histogram_edges_glcm_bit_exact(ctx, oracle):
     masks = inputs.adversarial_masks()
-    masks["blobs"] = fx.blob_mask_grid(256, 220, 25, 5)
+    masks["blobs"] = synth.blob_mask_grid(256, 220, 25, 5)
     p = fx.make_params("default", histogram_bins=16)
     for name, L in masks.items():
         I = inputs.uniform(L.shape, 3)
@@ -174,8 +175,8 @@ def test_per_roi_operator(ctx, oracle):
 
 
 def test_vs_compiled_reference(ctx, reference):
-    L = fx.blob_mask_grid(512, 300, 100, 7)
-    I = fx.uniform_u16(L.shape, 0)
+    L = synth.blob_mask_grid(512, 300, 100, 7)
+    I = synth.uniform_u16(L.shape, 0)
     gp, op = both_params("default")
     cols = fx.feature_columns(GROUPS, gp)
     gl, gv = ctx.featurize(I, L, GROUPS, gp)
@@ -312,7 +313,7 @@ def test_unstaged_in_warp_paths(oracle, monkeypatch):
     monkeypatch.setenv("FXG_NO_STAGE", "1")
     c = fx.Context(0)
     try:
-        for L, I in [(fx.blob_mask_grid(512, 300, 100, 7), None),
+        for L, I in [(synth.blob_mask_grid(512, 300, 100, 7), None),
                      (inputs.random_blobs((96, 130), 40, seed=2), None)]:
             I = inputs.uniform(L.shape, 3) if I is None else I
             check(c, oracle, I, L, ["intensity", "moments"])
@@ -336,6 +337,6 @@ def test_tied_values_small_rois(ctx, oracle, spread):
             lab += 1
     I = rng.integers(1000, 1000 + spread, size=L.shape, dtype=np.uint16)
     check(ctx, oracle, I, L, ["intensity", "moments"])
-    Lb = fx.blob_mask_grid(512, 300, 100, 5)
+    Lb = synth.blob_mask_grid(512, 300, 100, 5)
     Ib = rng.integers(7, 7 + spread, size=Lb.shape, dtype=np.uint16)
     check(ctx, oracle, Ib, Lb, ["intensity", "moments"])

@@ -16,6 +16,7 @@ import inputs
 from parity import assert_parity
 
 import paper_2603_12016_b200 as fx
+from tools import synth
 
 pytestmark = pytest.mark.gpu
 
@@ -23,16 +24,16 @@ pytestmark = pytest.mark.gpu
 def _pairs():
     rng = np.random.default_rng(5)
     out = {}
-    L = fx.blob_mask_grid(256, 200, 40, 2)
-    out["a_blobs.pgm"] = (fx.uniform_u16(L.shape, 3), L, 65535, 65535)
-    S = fx.siemens_star(128)
-    Ls = fx.blob_mask_grid(128, 200, 9, 4)
+    L = synth.blob_mask_grid(256, 200, 40, 2)
+    out["a_blobs.pgm"] = (synth.uniform_u16(L.shape, 3), L, 65535, 65535)
+    S = synth.siemens_star(128)
+    Ls = synth.blob_mask_grid(128, 200, 9, 4)
     out["b_star.pgm"] = (S, Ls, 65535, 65535)
-    Lt, _ = fx.packed_blob_mask_grid(192, 250, 30, 6)
+    Lt, _ = synth.packed_blob_mask_grid(192, 250, 30, 6)
     out["c_tertiary.pgm"] = (inputs.per_roi_levels(Lt, 7), Lt, 65535, 255)
     Lr = inputs.random_blobs((90, 140), 25, seed=8)
     out["d_random.pgm"] = (rng.integers(0, 4096, Lr.shape).astype(np.uint16), Lr, 4095, 255)
-    L8 = fx.blob_mask_grid(64, 80, 6, 9)
+    L8 = synth.blob_mask_grid(64, 80, 6, 9)
     out["e_8bit.pgm"] = (rng.integers(0, 256, L8.shape).astype(np.uint16), L8, 255, 255)
     Lw = np.zeros((300, 280), np.uint16)
     Lw[20:260, 30:250] = 3  # a window wider and taller than 64 (large-ROI path)

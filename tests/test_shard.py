@@ -135,14 +135,15 @@ def test_halo_plan():
 def test_device_band_sharding_bitwise(ctx, nbands):
     import ctypes as C
     import paper_2603_12016_b200 as fx
+    from tools import synth
     from paper_2603_12016_b200 import fxg, shard
     I, L = straddling_image(200, 160, seed=9)
-    big, _ = fx.packed_blob_mask_grid(256, 900, 40, 2)
+    big, _ = synth.packed_blob_mask_grid(256, 900, 40, 2)
     L = np.zeros((456, 256), np.uint16)
     L[:256] = big
     L[256:456, :160] = np.where(straddling_image(200, 160, seed=9)[1] > 0,
                                 straddling_image(200, 160, seed=9)[1] + 100, 0)
-    I = fx.uniform_u16(L.shape, 4)
+    I = synth.uniform_u16(L.shape, 4)
     p = fx.resolve_profile("default")
     gl, gv = ctx.featurize(I, L, GROUPS, p)
     H, W = L.shape

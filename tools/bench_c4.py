@@ -34,9 +34,10 @@ ROI_SIZE0 = 1000
 
 def label_tiles(distinct):
     import paper_2603_12016_b200 as fx
+    from tools import synth
     tiles, sizes = [], []
     for s in range(distinct):
-        L, rs = fx.packed_blob_mask_grid(TILE, ROI_SIZE0, ROIS, s)
+        L, rs = synth.packed_blob_mask_grid(TILE, ROI_SIZE0, ROIS, s)
         tiles.append(L)
         sizes.append(rs)
     return np.stack(tiles), sizes

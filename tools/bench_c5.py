@@ -64,6 +64,7 @@ def main():
     import torch.distributed as dist
 
     import paper_2603_12016_b200 as fx
+    from tools import synth
     from paper_2603_12016_b200 import shard
     rank, world = int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1))
     local = int(os.environ.get("LOCAL_RANK", 0))
@@ -77,7 +78,7 @@ def main():
     ncols = len(fx.feature_columns(mask, p))
     S, T = args.size, args.tile
     t0 = time.time()
-    tile, rs = fx.packed_blob_mask_grid(T, 200000, 144, 1)
+    tile, rs = synth.packed_blob_mask_grid(T, 200000, 144, 1)
     per = int(tile.max())
     tile_lab = torch.from_numpy(tile.astype(np.int64)).to(dev)
     bands = shard.band_plan(S, world) if args.sharded else [(0, S)]

@@ -34,7 +34,8 @@ TILE, ROIS, ROI_SIZE0, DISTINCT = 512, 100, 1000, 16
 
 def write_tiles(d, n, first=0):
     import paper_2603_12016_b200 as fx
-    labs = [fx.packed_blob_mask_grid(TILE, ROI_SIZE0, ROIS, s)[0] for s in range(DISTINCT)]
+    from tools import synth
+    labs = [synth.packed_blob_mask_grid(TILE, ROI_SIZE0, ROIS, s)[0] for s in range(DISTINCT)]
     for sub in ("int", "seg"):
         os.makedirs(os.path.join(d, sub), exist_ok=True)
     for t in range(first, first + n):

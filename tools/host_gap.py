@@ -11,10 +11,11 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2603_12016_b200 as fx  # noqa: E402
+from tools import synth  # noqa: E402
 
 steps = int(sys.argv[1]) if len(sys.argv) > 1 else 50
-L, _ = fx.packed_blob_mask_grid(8192, 400, 50000, 1)
-I = fx.uniform_u16(L.shape, 0)
+L, _ = synth.packed_blob_mask_grid(8192, 400, 50000, 1)
+I = synth.uniform_u16(L.shape, 0)
 p = fx.resolve_profile("default")
 mask = fx.resolve_groups(["intensity", "moments"])
 ncols = len(fx.feature_columns(mask, p))

@@ -9,24 +9,25 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2603_12016_b200 as fx  # noqa: E402
+from tools import synth  # noqa: E402
 
 which = sys.argv[1] if len(sys.argv) > 1 else "c2"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 10
 if which == "c2":
-    L, _ = fx.packed_blob_mask_grid(8192, 400, 50000, 1)
+    L, _ = synth.packed_blob_mask_grid(8192, 400, 50000, 1)
     groups = os.environ.get("FX_GROUPS", "intensity,moments").split(",")
     prof = "default"
 elif which.startswith("c5"):  # C5 regime at reduced size: 16384^2, ~2e5-px blobs
     size = int(os.environ.get("C5_SIZE", "16384"))
     n = (size // 680) ** 2
-    L, _ = fx.packed_blob_mask_grid(size, 200000, n, 1)
+    L, _ = synth.packed_blob_mask_grid(size, 200000, n, 1)
     groups = ["intensity", "moments", "glcm"]
     prof = "default"
 else:  # c3: 4096^2, 10k ROIs, GLCM 4 angles ng=256
-    L, _ = fx.packed_blob_mask_grid(4096, 400, 10000, 1)
+    L, _ = synth.packed_blob_mask_grid(4096, 400, 10000, 1)
     groups = ["glcm"]
     prof = "ibsi-like"
-I = fx.uniform_u16(L.shape, 0)
+I = synth.uniform_u16(L.shape, 0)
 law = os.environ.get("FX_LAW", "uniform")  # intensity law: uniform u16 | twelve (0..4095) | narrow
 if law == "twelve":
     I = I & np.uint16(4095)

@@ -8,6 +8,7 @@ import numpy as np
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_12016_b200 as fx  # noqa: E402
+from tools import synth  # noqa: E402
 from paper_2603_12016_b200 import fxg  # noqa: E402
 
 NAMES = ["load+gather", "int sort", "int stats", "edge", "moments", "glcm keys", "glcm sort",
@@ -19,22 +20,22 @@ ctx = fx.Context(0)
 lib = fxg.lib()
 buf = (C.c_ulonglong * 16)()
 if which == "c2":
-    L, _ = fx.packed_blob_mask_grid(8192, 400, 50000, 1)
-    I = fx.uniform_u16(L.shape, 0)
+    L, _ = synth.packed_blob_mask_grid(8192, 400, 50000, 1)
+    I = synth.uniform_u16(L.shape, 0)
     run = lambda: ctx.featurize(I, L, ["intensity", "moments"], fx.resolve_profile("default"))
     nroi = 50000
 elif which == "c4":
     T = int(sys.argv[2]) if len(sys.argv) > 2 else 256
     pairs = []
     for t in range(T):
-        Lt, _ = fx.packed_blob_mask_grid(512, 1000, 100, t % 16)
-        pairs.append((fx.uniform_u16(Lt.shape, t), Lt))
+        Lt, _ = synth.packed_blob_mask_grid(512, 1000, 100, t % 16)
+        pairs.append((synth.uniform_u16(Lt.shape, t), Lt))
     groups = os.environ.get("FX_GROUPS", "intensity,moments,glcm").split(",")
     run = lambda: ctx.featurize_batch(pairs, groups, fx.resolve_profile("default"))
     nroi = sum(int(np.count_nonzero(np.bincount(p[1].ravel(), minlength=65536)[1:])) for p in pairs)
 if which == "c5":
-    L, _ = fx.packed_blob_mask_grid(16384, 200000, 576, 1)
-    I = fx.uniform_u16(L.shape, 0)
+    L, _ = synth.packed_blob_mask_grid(16384, 200000, 576, 1)
+    I = synth.uniform_u16(L.shape, 0)
     run = lambda: ctx.featurize(I, L, ["intensity", "moments", "glcm"], fx.resolve_profile("default"))
     nroi = int(L.max())
 tbuf = (C.c_ulonglong * 8)()

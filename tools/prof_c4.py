@@ -6,12 +6,13 @@ import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2603_12016_b200 as fx  # noqa: E402
+from tools import synth  # noqa: E402
 
 T = int(sys.argv[1]) if len(sys.argv) > 1 else 256
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 groups = os.environ.get("FX_GROUPS", "*ALL*").split(",")
-labs = [fx.packed_blob_mask_grid(512, 1000, 100, s)[0] for s in range(16)]
-pairs = [(fx.uniform_u16((512, 512), t), labs[t % 16]) for t in range(T)]
+labs = [synth.packed_blob_mask_grid(512, 1000, 100, s)[0] for s in range(16)]
+pairs = [(synth.uniform_u16((512, 512), t), labs[t % 16]) for t in range(T)]
 ctx = fx.Context(0)
 out = ctx.featurize_batch(pairs, groups, fx.resolve_profile("default"))
 if reps > 1:
