@@ -112,6 +112,11 @@ int fx_ctx_create(int device, fx_ctx** out);
 int fx_ctx_destroy(fx_ctx* ctx);
 /* Launch on a caller-owned cudaStream_t (NULL restores the ctx's own stream). */
 int fx_ctx_set_stream(fx_ctx* ctx, void* cuda_stream);
+/* Host rasters of fx_featurize move in row bands of this many rows (multiple of
+ * 64), overlapping H2D, kernels and D2H; 0 = automatic (~8 bands for images of
+ * >= 2048 rows and >= 8 Mpx, else unbanded), < 0 = never banded.  Results are
+ * identical either way. */
+int fx_ctx_set_band_rows(fx_ctx* ctx, int rows);
 /* Kernel launches issued by this ctx since creation (evidence counter). */
 uint64_t fx_ctx_launch_count(const fx_ctx* ctx);
 /* Optional per-kernel CUDA-event timing on the launching stream. */

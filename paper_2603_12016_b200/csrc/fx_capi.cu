@@ -69,6 +69,13 @@ struct fx_ctx {
     int sm_count = 0;
     cudaStream_t own_stream = nullptr, stream = nullptr, side = nullptr;
     cudaStream_t copy = nullptr;  // batch staging (H2D of the next sub-batch)
+    cudaStream_t d2h = nullptr;   // banded host path: feature rows back while bands compute
+    // banded host path (featurize_banded): per-band events and pinned host staging
+    std::vector<cudaEvent_t> ev_band;  // 3 per band: labels in, intensities in, rows done
+    uint32_t* h_band = nullptr;        // pinned: per-band class lists (n_rois entries)
+    size_t h_band_cap = 0;
+    Control* h_band_ctl = nullptr;     // pinned: one control block per band
+    int h_band_ctl_cap = 0;
     cudaEvent_t ev_compact = nullptr, ev_stats = nullptr;
     cudaEvent_t ev_staged[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
     // label table: tab_slots slices of 65536 entries, left reset by each compaction
@@ -138,6 +145,7 @@ struct fx_ctx {
     bool sync_debug = false;
     bool no_tma = false;
     bool no_stage = false;  // FXG_NO_STAGE=1: in-warp intensity / moments (tests)
+    int band_rows = 0;      // FXG_BAND_ROWS: banded host path band height (0 auto, <0 off)
 };
 
 namespace {
@@ -534,13 +542,11 @@ int compact_stage(fx_ctx* c, const SlotMap& m, uint32_t own_y0, uint32_t own_y1,
     return FX_OK;
 }
 
-// Compaction (owned rows [own_y0, own_y1)) + per-ROI kernels over the ctx's label
-// table, reading pixels of img.  out_dev: [cap_rois x ncols] device.
-// With slot_base (host, [m.nslots+1]) the first output row of every slot is returned.
-int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t own_y0,
-                    uint32_t own_y1, unsigned groups, const fx_texture_params& p, double* out_dev,
-                    size_t cap_rois, size_t* n_rois, const DebugOut* dbg_dev,
-                    uint32_t* slot_base = nullptr, bool first = true) {
+// Staging buffers of the serial passes for one call (intensity / moments / shape),
+// unless debugging or FXG_NO_STAGE=1 (the in-warp paths, otherwise taken only when
+// the staging buffers overflow, e.g. huge images).
+int prepare_cfg(fx_ctx* c, const DevImage& img, unsigned groups, const fx_texture_params& p,
+                const DebugOut* dbg_dev, FeatCfg* out) {
     FeatCfg cfg = make_cfg(groups, p);
     if (cfg.col_shape >= 0) {
         const int rs = ensure_shape(c);
@@ -548,8 +554,6 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         cfg.shape_rows = c->d_shape_rows;
         cfg.shape_hdr = c->d_shape_hdr;
     }
-    // staged serial passes unless debugging or FXG_NO_STAGE=1 (the in-warp paths,
-    // otherwise taken only when the staging buffers overflow, e.g. huge images)
     if (cfg.col_int >= 0 && !dbg_dev && !c->no_stage) {
         const int ri = ensure_intensity(c, (size_t)img.w * (size_t)img.h);
         if (ri) return ri;
@@ -566,87 +570,51 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         cfg.mom_sums = c->d_mom_sums;
         cfg.mom_cap = c->mom_cap;
     }
-    const int vrc = validate_texture(groups, p);
-    RoiList rl = roi_list(c);
-    cudaStream_t s = c->stream;
-    int rc0 = compact_stage(c, m, own_y0, own_y1, cap_rois, first);
-    if (rc0) return rc0;
-    CK(cudaEventRecord(c->ev_compact, s));
-    CK(cudaStreamWaitEvent(c->side, c->ev_compact, 0));
-    CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, c->side));
-    if (slot_base)
-        CK(cudaMemcpyAsync(c->h_slot_base, compact_args(c, 0, 0).slot_base,
-                           ((size_t)m.nslots + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                           c->side));
-    CK(cudaEventRecord(c->ev_stats, c->side));
+    *out = cfg;
+    return FX_OK;
+}
 
-    if (vrc != FX_OK) {  // texture parameters are only an error when a ROI exists
-        CK(cudaEventSynchronize(c->ev_stats));
-        *n_rois = c->h_ctl->n_rois;
-        return c->h_ctl->n_rois ? vrc : FX_OK;
-    }
-    CUtensorMap tmaps[4];  // labels / intensities, 40- and 72-wide boxes
-    std::memset(tmaps, 0, sizeof tmaps);
-    const int tma40 = (!c->no_tma && make_tmap(c, img, img.L, &tmaps[0], kStageW0) &&
-                       make_tmap(c, img, img.I, &tmaps[1], kStageW0)) ? 1 : 0;
-    const int tma72 = (!c->no_tma && make_tmap(c, img, img.L, &tmaps[2], kStageW) &&
-                       make_tmap(c, img, img.I, &tmaps[3], kStageW)) ? 1 : 0;
+// TMA descriptors of img's label / intensity rasters (40- and 72-wide boxes)
+struct TmaSet {
+    CUtensorMap m[4];
+    int tma40 = 0, tma72 = 0;
+};
+void make_tmaps(fx_ctx* c, const DevImage& img, TmaSet* t) {
+    std::memset(t->m, 0, sizeof t->m);
+    t->tma40 = (!c->no_tma && make_tmap(c, img, img.L, &t->m[0], kStageW0) &&
+                make_tmap(c, img, img.I, &t->m[1], kStageW0)) ? 1 : 0;
+    t->tma72 = (!c->no_tma && make_tmap(c, img, img.L, &t->m[2], kStageW) &&
+                make_tmap(c, img, img.I, &t->m[3], kStageW)) ? 1 : 0;
+}
+
+const char* const kSName[3] = {"k_roi_s0", "k_roi_s1", "k_roi_s2"};
+
+// Per-ROI kernels over the ROIs queued in the device control block, whose class
+// counts the host knows (hc): S classes from cls_first on, GLRLM/GLSZM/NGTDM, the
+// serial passes over the staged S ROIs, then the large-ROI kernel (L ROIs + S
+// overflow).
+int roi_work(fx_ctx* c, const DevImage& img, const FeatCfg& cfg, const Control& hc,
+             const TmaSet& tm, double* out_dev, const DebugOut* dbg_dev, int cls_first) {
+    cudaStream_t s = c->stream;
     const int glcm = s_glcm_mode(cfg);
-    static const char* names[3] = {"k_roi_s0", "k_roi_s1", "k_roi_s2"};
-    {
-        Launch l(c, names[kClassS0]);
-        launch_roi_s(kClassS0, c->sm_count * c->occ_s[kClassS0][glcm], s, tmaps, tma40, tma72, img, rl,
-                     c->d_ctl, cfg, out_dev, dbg_dev);
-    }
-    CK(cudaGetLastError());
-    // the class counts arrive while S0 runs; S1 / S2 launch only when they have ROIs
-    // (an empty persistent grid still costs ~7 us).  With more ROIs than cap_rois the
-    // compaction queued none, so S0 found no work and wrote no row.
-    CK(cudaEventSynchronize(c->ev_stats));
-    const Control hc = *c->h_ctl;
-    for (int cls = kClassS1; cls <= kClassS2; ++cls) {
+    for (int cls = cls_first; cls <= kClassS2; ++cls) {
         if (hc.class_count[cls] == 0) continue;
-        Launch l(c, names[cls]);
-        launch_roi_s(cls, c->sm_count * c->occ_s[cls][glcm], s, tmaps, tma40, tma72, img, rl,
-                     c->d_ctl, cfg, out_dev, dbg_dev);
+        Launch l(c, kSName[cls]);
+        launch_roi_s(cls, c->sm_count * c->occ_s[cls][glcm], s, tm.m, tm.tma40, tm.tma72, img,
+                     roi_list(c), c->d_ctl, cfg, out_dev, dbg_dev);
     }
     CK(cudaGetLastError());
-    *n_rois = hc.n_rois;
-    if (slot_base) std::memcpy(slot_base, c->h_slot_base, ((size_t)m.nslots + 1) * sizeof(uint32_t));
-    if (hc.error & kErrWindow) {
-        cudaStreamSynchronize(s);
-        return set_error(FX_E_ARG, "an owned ROI window extends beyond the image (halo too small)");
-    }
-    if (hc.n_rois > cap_rois) {
-        cudaStreamSynchronize(s);
-        return set_error(FX_E_CAPACITY, "output capacity " + std::to_string(cap_rois) +
-                                            " < " + std::to_string(hc.n_rois) + " ROIs");
-    }
+    RoiList rl = roi_list(c);
     const bool texture = cfg.col_glrlm >= 0 || cfg.col_glszm >= 0 || cfg.col_ngtdm >= 0;
     const uint64_t n_s_rois = (uint64_t)hc.class_count[kClassS0] + hc.class_count[kClassS1] +
                               hc.class_count[kClassS2];
-    auto serial_passes = [&](cudaStream_t on) {
-        // (fusing these into the S kernels, one lane per finished ROI, measured 30%
-        // slower: the S slabs leave the serial loads almost no L1)
-        if (cfg.int_vals || cfg.mom_px) {
-            Launch l(c, "k_serial_stats", on);
-            launch_serial_stats((int)n_s_rois, cfg.int_vals != nullptr, cfg.mom_px != nullptr, on, rl,
-                                c->d_ctl, cfg, out_dev);
-        }
-        if (cfg.col_shape >= 0) {
-            Launch l(c, "k_shape_serial", on);
-            launch_shape_serial((int)n_s_rois, on, rl, c->d_ctl, cfg, out_dev);
-        }
-    };
-    // (running them on a second stream next to k_roi_t measured slower: its
-    // persistent CTAs leave no room, and 512-image batches fill the GPU anyway)
+    const uint64_t n_l = hc.class_count[kClassL];
+    // (running the serial passes on a second stream next to k_roi_t measured slower:
+    // its persistent CTAs leave no room, and 512-image batches fill the GPU anyway)
     if (texture) {
         // GLRLM/GLSZM/NGTDM: S-class windows, then large windows (own slabs)
-        const uint64_t n_s = (uint64_t)hc.class_count[kClassS0] + hc.class_count[kClassS1] +
-                             hc.class_count[kClassS2];
-        const uint64_t n_l = hc.class_count[kClassL];
         for (int which = 0; which < 2; ++which) {
-            const uint64_t nw = which ? n_l : n_s;
+            const uint64_t nw = which ? n_l : n_s_rois;
             if (!nw) continue;
             const TLayout T = which ? make_tlayout(std::max<unsigned long long>(hc.l_max_cells, 4096ull),
                                                    (uint32_t)std::max<unsigned long long>(hc.l_max_n, 4096ull))
@@ -675,18 +643,28 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         }
     }
     // intensity statistics, moments and serial shape columns of the staged S ROIs,
-    // before k_roi_b (which rewrites the rows of overflowed S ROIs)
-    if (n_s_rois > 0) serial_passes(s);
+    // before k_roi_b (which rewrites the rows of overflowed S ROIs).  (Fusing these
+    // into the S kernels, one lane per finished ROI, measured 30% slower: the S slabs
+    // leave the serial loads almost no L1.)
+    if (n_s_rois > 0) {
+        if (cfg.int_vals || cfg.mom_px) {
+            Launch l(c, "k_serial_stats");
+            launch_serial_stats((int)n_s_rois, cfg.int_vals != nullptr, cfg.mom_px != nullptr, s, rl,
+                                c->d_ctl, cfg, out_dev);
+        }
+        if (cfg.col_shape >= 0) {
+            Launch l(c, "k_shape_serial");
+            launch_shape_serial((int)n_s_rois, s, rl, c->d_ctl, cfg, out_dev);
+        }
+    }
+    if (n_l == 0 && n_s_rois == 0) return FX_OK;
     {
         // large ROIs + S overflow: one CTA per ROI; the slabs' histograms are kept
         // zero by the kernel, so they are cleared only when the layout changes
         const BLayout B = b_layout(hc, cfg.bins);
-        const uint32_t nl = hc.class_count[kClassL];
-        const uint64_t s_rois = (uint64_t)hc.class_count[kClassS0] + hc.class_count[kClassS1] +
-                                hc.class_count[kClassS2];
         uint64_t grid = std::min<uint64_t>((uint64_t)c->sm_count * 2,
-                                           std::max<uint64_t>(std::max<uint64_t>(nl, 1),
-                                                              s_rois > 0 ? 16 : 1));
+                                           std::max<uint64_t>(std::max<uint64_t>(n_l, 1),
+                                                              n_s_rois > 0 ? 16 : 1));
         const uint64_t budget = 8ull << 30;  // scratch cap: fewer CTAs for huge windows
         grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, budget / std::max<size_t>(B.bytes, 1)));
         int rc = ensure_lscratch(c, (size_t)B.bytes * grid);
@@ -703,6 +681,66 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         launch_roi_b((int)grid, s, img, rl, c->d_ctl, cfg, out_dev, dbg_dev, c->d_lscratch, B);
     }
     CK(cudaGetLastError());
+    return FX_OK;
+}
+
+// Compaction (owned rows [own_y0, own_y1)) + per-ROI kernels over the ctx's label
+// table, reading pixels of img.  out_dev: [cap_rois x ncols] device.
+// With slot_base (host, [m.nslots+1]) the first output row of every slot is returned.
+int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t own_y0,
+                    uint32_t own_y1, unsigned groups, const fx_texture_params& p, double* out_dev,
+                    size_t cap_rois, size_t* n_rois, const DebugOut* dbg_dev,
+                    uint32_t* slot_base = nullptr, bool first = true) {
+    FeatCfg cfg;
+    int rc = prepare_cfg(c, img, groups, p, dbg_dev, &cfg);
+    if (rc) return rc;
+    const int vrc = validate_texture(groups, p);
+    cudaStream_t s = c->stream;
+    rc = compact_stage(c, m, own_y0, own_y1, cap_rois, first);
+    if (rc) return rc;
+    CK(cudaEventRecord(c->ev_compact, s));
+    CK(cudaStreamWaitEvent(c->side, c->ev_compact, 0));
+    CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, c->side));
+    if (slot_base)
+        CK(cudaMemcpyAsync(c->h_slot_base, compact_args(c, 0, 0).slot_base,
+                           ((size_t)m.nslots + 1) * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                           c->side));
+    CK(cudaEventRecord(c->ev_stats, c->side));
+
+    if (vrc != FX_OK) {  // texture parameters are only an error when a ROI exists
+        CK(cudaEventSynchronize(c->ev_stats));
+        *n_rois = c->h_ctl->n_rois;
+        return c->h_ctl->n_rois ? vrc : FX_OK;
+    }
+    TmaSet tm;
+    make_tmaps(c, img, &tm);
+    const int glcm = s_glcm_mode(cfg);
+    {
+        // S0 before the class counts are known (its persistent grid finds its list
+        // empty when there is none), overlapping the counters' readback
+        Launch l(c, kSName[kClassS0]);
+        launch_roi_s(kClassS0, c->sm_count * c->occ_s[kClassS0][glcm], s, tm.m, tm.tma40, tm.tma72,
+                     img, roi_list(c), c->d_ctl, cfg, out_dev, dbg_dev);
+    }
+    CK(cudaGetLastError());
+    // the class counts arrive while S0 runs; S1 / S2 launch only when they have ROIs
+    // (an empty persistent grid still costs ~7 us).  With more ROIs than cap_rois the
+    // compaction queued none, so S0 found no work and wrote no row.
+    CK(cudaEventSynchronize(c->ev_stats));
+    const Control hc = *c->h_ctl;
+    *n_rois = hc.n_rois;
+    if (slot_base) std::memcpy(slot_base, c->h_slot_base, ((size_t)m.nslots + 1) * sizeof(uint32_t));
+    if (hc.error & kErrWindow) {
+        cudaStreamSynchronize(s);
+        return set_error(FX_E_ARG, "an owned ROI window extends beyond the image (halo too small)");
+    }
+    if (hc.n_rois > cap_rois) {
+        cudaStreamSynchronize(s);
+        return set_error(FX_E_CAPACITY, "output capacity " + std::to_string(cap_rois) +
+                                            " < " + std::to_string(hc.n_rois) + " ROIs");
+    }
+    rc = roi_work(c, img, cfg, hc, tm, out_dev, dbg_dev, kClassS1);
+    if (rc) return rc;
     CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
     return FX_OK;
 }
@@ -836,6 +874,205 @@ int ensure_blab(fx_ctx* c, size_t n) {
     return FX_OK;
 }
 
+// ---- host rasters in row bands (the end-to-end path of fx_featurize) ----------
+//
+// PCIe moves ~55 GB/s: a C2 image (268 MB of rasters) takes ~4.9 ms to arrive and
+// its 57 MB table ~1 ms to leave, against ~0.6 ms of kernels.  Instead of copy ->
+// compute -> copy back, the rasters move in row bands on the copy stream (all
+// labels first, then the intensities):
+//   - the label scan runs band by band as the labels arrive;
+//   - the compaction runs once over the whole table (a ROI's bbox is only final when
+//     every row has been scanned); the host reads the ROI windows back and sorts
+//     each class list by the band holding the window's last row;
+//   - band b's ROIs are featurized as soon as band b's intensities are in (the
+//     unchanged per-ROI kernels over a control block holding that band's lists);
+//   - output rows [r_(b-1), r_b) leave on the d2h stream as soon as every ROI of
+//     rank < r_b is final (blob grids: about one band's rows per band), so the D2H
+//     overlaps the remaining H2D (PCIe is full duplex).
+// Results are identical to the unbanded path: the same kernels on the same ROIs.
+
+int ensure_band_host(fx_ctx* c, size_t entries, int bands) {
+    if (entries > c->h_band_cap) {
+        if (c->h_band) cudaFreeHost(c->h_band);
+        c->h_band = nullptr;
+        c->h_band_cap = 0;
+        CK(cudaMallocHost(&c->h_band, std::max<size_t>(entries, 1) * sizeof(uint32_t)));
+        c->h_band_cap = entries;
+    }
+    if (bands > c->h_band_ctl_cap) {
+        if (c->h_band_ctl) cudaFreeHost(c->h_band_ctl);
+        c->h_band_ctl = nullptr;
+        c->h_band_ctl_cap = 0;
+        CK(cudaMallocHost(&c->h_band_ctl, (size_t)bands * sizeof(Control)));
+        c->h_band_ctl_cap = bands;
+    }
+    while ((int)c->ev_band.size() < 3 * bands) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_band.push_back(e);
+    }
+    return FX_OK;
+}
+
+// band height for a host image (0: unbanded); FXG_BAND_ROWS overrides (<0: off)
+int band_rows_for(const fx_ctx* c, int w, int h) {
+    if (c->band_rows < 0) return 0;
+    if (c->band_rows > 0) return (c->band_rows + 63) / 64 * 64;
+    if (h < 2048 || (size_t)w * (size_t)h < (8u << 20)) return 0;  // not worth it
+    return std::max(256, (h / 8 + 63) / 64 * 64);                   // ~8 bands
+}
+
+int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned groups,
+                     const fx_texture_params& p, uint32_t* out_labels, double* out_values,
+                     size_t cap_rois, size_t* n_rois) {
+    const int W = im->width, H = im->height;
+    const int nb = (H + band_rows - 1) / band_rows;
+    int rc = ensure_img(c, W, H);
+    if (!rc) rc = ensure_band_host(c, 0, nb);
+    if (rc) return rc;
+    cudaStream_t s = c->stream;
+    const size_t P = c->img_pitch, sp = (im->pitch ? im->pitch : (size_t)W) * 2;
+    DevImage d;
+    d.I = c->d_img;
+    d.L = c->d_img + P * c->img_rows_cap;
+    d.w = W;
+    d.h = H;
+    d.pitch = P;
+    d.ox = im->origin_x;
+    d.oy = im->origin_y;
+    cudaEvent_t* ev = c->ev_band.data();  // [b]: labels in, [nb+b]: intensities in, [2nb+b]: rows
+    // the copy stream starts after this stream's earlier work (staging buffer reuse)
+    CK(cudaEventRecord(c->ev_compact, s));
+    CK(cudaStreamWaitEvent(c->copy, c->ev_compact, 0));
+    auto rows_of = [&](int b) { return std::min(band_rows, H - b * band_rows); };
+    for (int pass = 0; pass < 2; ++pass)  // all labels, then all intensities
+        for (int b = 0; b < nb; ++b) {
+            const size_t y0 = (size_t)b * band_rows;
+            const uint16_t* src = (pass ? im->intensity : im->labels) + y0 * (sp / 2);
+            uint16_t* dst = const_cast<uint16_t*>(pass ? d.I : d.L) + y0 * P;
+            CK(cudaMemcpy2DAsync(dst, P * 2, src, sp, (size_t)W * 2, (size_t)rows_of(b),
+                                 cudaMemcpyHostToDevice, c->copy));
+            CK(cudaEventRecord(ev[pass * nb + b], c->copy));
+        }
+    // label scan band by band, in global coordinates
+    for (int b = 0; b < nb; ++b) {
+        CK(cudaStreamWaitEvent(s, ev[b], 0));
+        DevImage band = d;
+        band.L = d.L + (size_t)b * band_rows * P;
+        band.I = band.L;
+        band.h = rows_of(b);
+        band.oy = d.oy + b * band_rows;
+        rc = scan_stage(c, band, single_map(band), b == 0);
+        if (rc) return rc;
+    }
+    FeatCfg cfg;
+    rc = prepare_cfg(c, d, groups, p, nullptr, &cfg);
+    if (rc) return rc;
+    const int vrc = validate_texture(groups, p);
+    rc = compact_stage(c, single_map(d), 0u, 0xffffffffu, cap_rois, true);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));  // the intensities keep arriving meanwhile
+    const Control hc = *c->h_ctl;
+    const size_t n = hc.n_rois;
+    *n_rois = n;
+    if (vrc != FX_OK) return n ? vrc : FX_OK;
+    if (hc.error & kErrWindow)
+        return set_error(FX_E_ARG, "an owned ROI window extends beyond the image (halo too small)");
+    if (n > cap_rois)
+        return set_error(FX_E_CAPACITY, "output capacity " + std::to_string(cap_rois) + " < " +
+                                            std::to_string(n) + " ROIs");
+    if (n == 0) {
+        CK(cudaStreamSynchronize(c->copy));
+        return FX_OK;
+    }
+    // ROI windows and class lists to the host; band of a ROI = band of its last row
+    RoiList rl = roi_list(c);
+    rc = ensure_band_host(c, n, nb);
+    if (rc) return rc;
+    std::vector<uint32_t> y0(n), hh(n), lists(n);
+    CK(cudaMemcpyAsync(y0.data(), rl.y0, n * 4, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(hh.data(), rl.h, n * 4, cudaMemcpyDeviceToHost, s));
+    size_t cls_off[kNumClasses + 1] = {0};
+    for (int k = 0; k < kNumClasses; ++k) {
+        cls_off[k + 1] = cls_off[k] + hc.class_count[k];
+        if (hc.class_count[k])
+            CK(cudaMemcpyAsync(lists.data() + cls_off[k], rl.cls_list[k],
+                               (size_t)hc.class_count[k] * 4, cudaMemcpyDeviceToHost, s));
+    }
+    CK(cudaEventRecord(c->ev_stats, s));
+    if (out_labels) {
+        CK(cudaStreamWaitEvent(c->d2h, c->ev_stats, 0));
+        CK(cudaMemcpyAsync(out_labels, rl.label, n * 4, cudaMemcpyDeviceToHost, c->d2h));
+    }
+    CK(cudaStreamSynchronize(s));
+    auto band_of = [&](uint32_t r) {
+        return std::min<int>(nb - 1, (int)((y0[r] + hh[r] - 1) / (uint32_t)band_rows));
+    };
+    // counting sort of every class list by band: h_band = [band][class] segments
+    std::vector<uint32_t> cnt((size_t)nb * kNumClasses, 0), first_rank(nb, (uint32_t)n);
+    for (int k = 0; k < kNumClasses; ++k)
+        for (size_t i = cls_off[k]; i < cls_off[k + 1]; ++i) {
+            const int b = band_of(lists[i]);
+            cnt[(size_t)b * kNumClasses + k]++;
+            first_rank[b] = std::min(first_rank[b], lists[i]);
+        }
+    std::vector<size_t> seg((size_t)nb * kNumClasses + 1, 0);
+    for (size_t i = 0; i < cnt.size(); ++i) seg[i + 1] = seg[i] + cnt[i];
+    {
+        std::vector<size_t> fill(seg.begin(), seg.end() - 1);
+        for (int k = 0; k < kNumClasses; ++k)
+            for (size_t i = cls_off[k]; i < cls_off[k + 1]; ++i)
+                c->h_band[fill[(size_t)band_of(lists[i]) * kNumClasses + k]++] = lists[i];
+    }
+    // rows final after band b: every rank below the first rank of any later band
+    std::vector<uint32_t> final_after(nb);
+    uint32_t later = (uint32_t)n;
+    for (int b = nb - 1; b >= 0; --b) {
+        final_after[b] = later;
+        later = std::min(later, first_rank[b]);
+    }
+    const size_t ncols = (size_t)cfg.ncols;
+    TmaSet tm;
+    make_tmaps(c, d, &tm);
+    size_t rows_out = 0;
+    for (int b = 0; b < nb; ++b) {
+        Control& bc = c->h_band_ctl[b];
+        bc = hc;
+        uint64_t band_rois = 0;
+        for (int k = 0; k < kNumClasses; ++k) {
+            const size_t a = seg[(size_t)b * kNumClasses + k];
+            bc.class_count[k] = cnt[(size_t)b * kNumClasses + k];
+            bc.class_next[k] = 0;
+            band_rois += bc.class_count[k];
+            if (bc.class_count[k])
+                CK(cudaMemcpyAsync(rl.cls_list[k], c->h_band + a, (size_t)bc.class_count[k] * 4,
+                                   cudaMemcpyHostToDevice, s));
+        }
+        bc.overflow_count = bc.overflow_next = 0;
+        bc.t_next[0] = bc.t_next[1] = 0;
+        bc.mom_alloc = bc.int_alloc = 0;
+        CK(cudaStreamWaitEvent(s, ev[nb + b], 0));
+        if (band_rois) {
+            CK(cudaMemcpyAsync(c->d_ctl, &bc, offsetof(Control, error), cudaMemcpyHostToDevice, s));
+            rc = roi_work(c, d, cfg, bc, tm, c->d_out, nullptr, kClassS0);
+            if (rc) return rc;
+        }
+        const size_t upto = std::max<size_t>(rows_out, b == nb - 1 ? n : final_after[b]);
+        if (upto > rows_out) {
+            CK(cudaEventRecord(ev[2 * nb + b], s));
+            CK(cudaStreamWaitEvent(c->d2h, ev[2 * nb + b], 0));
+            CK(cudaMemcpyAsync(out_values + rows_out * ncols, c->d_out + rows_out * ncols,
+                               (upto - rows_out) * ncols * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->d2h));
+            rows_out = upto;
+        }
+    }
+    CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(c->d2h));
+    return FX_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -876,6 +1113,8 @@ int fx_ctx_create(int device, fx_ctx** out) {
     CKC(cudaEventCreateWithFlags(&c->ev_compact, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
     CKC(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    if (const char* e = getenv("FXG_BAND_ROWS")) c->band_rows = atoi(e);
     for (int b = 0; b < 2; ++b) {
         CKC(cudaEventCreateWithFlags(&c->ev_staged[b], cudaEventDisableTiming));
         CKC(cudaEventCreateWithFlags(&c->ev_free[b], cudaEventDisableTiming));
@@ -909,6 +1148,7 @@ int fx_ctx_destroy(fx_ctx* c) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->copy) cudaStreamSynchronize(c->copy);
+    if (c->d2h) cudaStreamSynchronize(c->d2h);
     collect_times(c);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     c->ev_pool.clear();
@@ -954,6 +1194,10 @@ int fx_ctx_destroy(fx_ctx* c) {
     if (c->ev_stats) cudaEventDestroy(c->ev_stats);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->copy) cudaStreamDestroy(c->copy);
+    if (c->d2h) cudaStreamDestroy(c->d2h);
+    for (cudaEvent_t e : c->ev_band) cudaEventDestroy(e);
+    if (c->h_band) cudaFreeHost(c->h_band);
+    if (c->h_band_ctl) cudaFreeHost(c->h_band_ctl);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;
     return FX_OK;
@@ -982,6 +1226,12 @@ int fx_host_free(void* p) {
 int fx_ctx_set_stream(fx_ctx* c, void* stream) {
     if (!c) return set_error(FX_E_ARG, "null ctx");
     c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own_stream;
+    return FX_OK;
+}
+
+int fx_ctx_set_band_rows(fx_ctx* c, int rows) {
+    if (!c) return set_error(FX_E_ARG, "null ctx");
+    c->band_rows = rows;
     return FX_OK;
 }
 
@@ -1039,10 +1289,24 @@ int fx_featurize(fx_ctx* c, const fx_image* im, unsigned groups, const fx_textur
     int rc = check_groups(groups);
     if (rc) return rc;
     CK(cudaSetDevice(c->device));
+    const FeatCfg cfg = make_cfg(groups, *p);
+    if (im->mem_kind == FX_MEM_HOST) {
+        const int br = band_rows_for(c, im->width, im->height);
+        if (br > 0) {
+            rc = ensure_out(c, std::max<size_t>(1, cap_rois) * (size_t)cfg.ncols);
+            if (!rc) rc = featurize_banded(c, im, br, groups, *p, out_labels, out_values, cap_rois, n_rois);
+            if (rc) {
+                cudaStreamSynchronize(c->copy);
+                cudaStreamSynchronize(c->d2h);
+                cudaStreamSynchronize(c->stream);
+                return rc;
+            }
+            return finish(c);
+        }
+    }
     DevImage d;
     rc = stage_image(c, im, &d);
     if (rc) return rc;
-    const FeatCfg cfg = make_cfg(groups, *p);
     double* out_dev = out_values;
     if (im->mem_kind == FX_MEM_HOST) {
         rc = ensure_out(c, std::max<size_t>(1, cap_rois) * (size_t)cfg.ncols);

@@ -2098,6 +2098,83 @@ __device__ __forceinline__ uint32_t s_row_of(uint32_t t, const RoiList& rl, cons
          : t < n0 + n1 ? rl.cls_list[kClassS1][t - n0] : rl.cls_list[kClassS2][t - n0 - n1];
 }
 
+// Moments epilogue of one ROI and group from its 16 sums N[p*4+q] of w dx^p dy^q
+// about the integer anchor (ax, ay): binomial shifts to the image origin (raw) and
+// to the centroid (central), eta, Hu (moments.cpp:32-92); writes the 52 columns at o.
+__device__ __forceinline__ void moments_epilogue_serial(const double (&N)[16], int grp, uint32_t n,
+                                                     long long W, long long SX, long long SY,
+                                                     long long ax, long long ay, long long gx0,
+                                                     long long gy0, double* o) {
+    const long long nn = (long long)n;
+    const bool zero_mass = grp && W == 0;
+    const double m00 = grp ? (double)W : (double)n;
+    const double dx = grp ? (W > 0 ? (double)(SX - ax * W) / (double)W : 0.0) : (double)(SX - ax * nn) / (double)nn;
+    const double dy = grp ? (W > 0 ? (double)(SY - ay * W) / (double)W : 0.0) : (double)(SY - ay * nn) / (double)nn;
+    const double Ax = (double)(gx0 + ax), Ay = (double)(gy0 + ay);
+    // binomial shifts, separable: T[i][q] = sum_j C(q,j) s_y^(q-j) N[i][j], then
+    // out[p][q] = sum_i C(p,i) s_x^(p-i) T[i][q] (one 4x4 tile live at a time);
+    // s = -d for the central moments, the anchor's origin A for the raw ones
+    auto shift = [&](double sx, double sy, double* R) {
+        const double y1 = sy, y2 = sy * sy, y3 = y2 * sy;
+        const double x1 = sx, x2 = sx * sx, x3 = x2 * sx;
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const double a0 = N[i * 4], a1 = N[i * 4 + 1], a2 = N[i * 4 + 2], a3 = N[i * 4 + 3];
+            R[i * 4] = a0;
+            R[i * 4 + 1] = a1 + y1 * a0;
+            R[i * 4 + 2] = a2 + 2.0 * y1 * a1 + y2 * a0;
+            R[i * 4 + 3] = a3 + 3.0 * y1 * a2 + 3.0 * y2 * a1 + y3 * a0;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double a0 = R[q], a1 = R[4 + q], a2 = R[8 + q], a3 = R[12 + q];
+            R[4 + q] = a1 + x1 * a0;
+            R[8 + q] = a2 + 2.0 * x1 * a1 + x2 * a0;
+            R[12 + q] = a3 + 3.0 * x1 * a2 + 3.0 * x2 * a1 + x3 * a0;
+        }
+    };
+    double R[16];
+    shift(Ax, Ay, R);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) o[k] = zero_mass ? 0.0 : R[k];
+    shift(-dx, -dy, R);
+    R[1] = R[4] = 0.0;  // moments.cpp:80-81
+    R[0] = N[0];
+    double eta[4][4];
+#pragma unroll
+    for (int p = 0; p < 4; ++p)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const double mu = R[p * 4 + q];
+            double et = 0;
+            if (p + q >= 2) {  // eta = mu / m00^(1 + (p+q)/2)
+                double den = m00 * m00;
+                if (p + q >= 4) den *= m00;
+                if (p + q >= 6) den *= m00;
+                if ((p + q) & 1) den *= sqrt(m00);
+                et = mu / den;
+            }
+            if (zero_mass) et = 0;
+            eta[p][q] = et;
+            o[16 + p * 4 + q] = zero_mass ? 0.0 : mu;
+            if (p + q >= 2) o[32 + ((p == 0) ? q - 2 : (p == 1 ? 1 + q : 1 + 4 * (p - 1) + q))] = et;
+        }
+    const double n20 = eta[2][0], n02 = eta[0][2], n11 = eta[1][1], n30 = eta[3][0],
+                 n03 = eta[0][3], n21 = eta[2][1], n12 = eta[1][2];
+    const double a = n30 + n12, b = n21 + n03;
+    const double hu[7] = {n20 + n02,
+                          (n20 - n02) * (n20 - n02) + 4.0 * n11 * n11,
+                          (n30 - 3.0 * n12) * (n30 - 3.0 * n12) + (3.0 * n21 - n03) * (3.0 * n21 - n03),
+                          a * a + b * b,
+                          (n30 - 3.0 * n12) * a * (a * a - 3.0 * b * b) +
+                              (3.0 * n21 - n03) * b * (3.0 * a * a - b * b),
+                          (n20 - n02) * (a * a - b * b) + 4.0 * n11 * a * b,
+                          (3.0 * n21 - n03) * a * (a * a - 3.0 * b * b) -
+                              (n30 - 3.0 * n12) * b * (3.0 * a * a - b * b)};
+#pragma unroll
+    for (int k = 0; k < 7; ++k) o[45 + k] = zero_mass ? 0.0 : hu[k];
+}
+
 __device__ void moments_row(uint32_t r, int grp, const RoiList& rl, const FeatCfg& cfg,
                                          double* out) {
     const unsigned long long off = cfg.mom_off[r];
@@ -2176,75 +2253,8 @@ __device__ void moments_row(uint32_t r, int grp, const RoiList& rl, const FeatCf
         N[1] = (double)(SY - ay * W);
         N[4] = (double)(SX - ax * W);
     }
-    const long long gx0 = rl.gx[r], gy0 = rl.gy[r];
-    double* o = out + (size_t)r * cfg.ncols + cfg.col_mom + grp * 52;
-    const bool zero_mass = grp && W == 0;
-    const double m00 = grp ? (double)W : (double)n;
-    const double dx = grp ? (W > 0 ? (double)(SX - ax * W) / (double)W : 0.0) : (double)(SX - ax * nn) / (double)nn;
-    const double dy = grp ? (W > 0 ? (double)(SY - ay * W) / (double)W : 0.0) : (double)(SY - ay * nn) / (double)nn;
-    const double Ax = (double)(gx0 + ax), Ay = (double)(gy0 + ay);
-    // binomial shifts, separable: T[i][q] = sum_j C(q,j) s_y^(q-j) N[i][j], then
-    // out[p][q] = sum_i C(p,i) s_x^(p-i) T[i][q] (one 4x4 tile live at a time);
-    // s = -d for the central moments, the anchor's origin A for the raw ones
-    auto shift = [&](double sx, double sy, double* R) {
-        const double y1 = sy, y2 = sy * sy, y3 = y2 * sy;
-        const double x1 = sx, x2 = sx * sx, x3 = x2 * sx;
-#pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            const double a0 = N[i * 4], a1 = N[i * 4 + 1], a2 = N[i * 4 + 2], a3 = N[i * 4 + 3];
-            R[i * 4] = a0;
-            R[i * 4 + 1] = a1 + y1 * a0;
-            R[i * 4 + 2] = a2 + 2.0 * y1 * a1 + y2 * a0;
-            R[i * 4 + 3] = a3 + 3.0 * y1 * a2 + 3.0 * y2 * a1 + y3 * a0;
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const double a0 = R[q], a1 = R[4 + q], a2 = R[8 + q], a3 = R[12 + q];
-            R[4 + q] = a1 + x1 * a0;
-            R[8 + q] = a2 + 2.0 * x1 * a1 + x2 * a0;
-            R[12 + q] = a3 + 3.0 * x1 * a2 + 3.0 * x2 * a1 + x3 * a0;
-        }
-    };
-    double R[16];
-    shift(Ax, Ay, R);
-#pragma unroll
-    for (int k = 0; k < 16; ++k) o[k] = zero_mass ? 0.0 : R[k];
-    shift(-dx, -dy, R);
-    R[1] = R[4] = 0.0;  // moments.cpp:80-81
-    R[0] = N[0];
-    double eta[4][4];
-#pragma unroll
-    for (int p = 0; p < 4; ++p)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const double mu = R[p * 4 + q];
-            double et = 0;
-            if (p + q >= 2) {  // eta = mu / m00^(1 + (p+q)/2)
-                double den = m00 * m00;
-                if (p + q >= 4) den *= m00;
-                if (p + q >= 6) den *= m00;
-                if ((p + q) & 1) den *= sqrt(m00);
-                et = mu / den;
-            }
-            if (zero_mass) et = 0;
-            eta[p][q] = et;
-            o[16 + p * 4 + q] = zero_mass ? 0.0 : mu;
-            if (p + q >= 2) o[32 + ((p == 0) ? q - 2 : (p == 1 ? 1 + q : 1 + 4 * (p - 1) + q))] = et;
-        }
-    const double n20 = eta[2][0], n02 = eta[0][2], n11 = eta[1][1], n30 = eta[3][0],
-                 n03 = eta[0][3], n21 = eta[2][1], n12 = eta[1][2];
-    const double a = n30 + n12, b = n21 + n03;
-    const double hu[7] = {n20 + n02,
-                          (n20 - n02) * (n20 - n02) + 4.0 * n11 * n11,
-                          (n30 - 3.0 * n12) * (n30 - 3.0 * n12) + (3.0 * n21 - n03) * (3.0 * n21 - n03),
-                          a * a + b * b,
-                          (n30 - 3.0 * n12) * a * (a * a - 3.0 * b * b) +
-                              (3.0 * n21 - n03) * b * (3.0 * a * a - b * b),
-                          (n20 - n02) * (a * a - b * b) + 4.0 * n11 * a * b,
-                          (3.0 * n21 - n03) * a * (a * a - 3.0 * b * b) -
-                              (n30 - 3.0 * n12) * b * (3.0 * a * a - b * b)};
-#pragma unroll
-    for (int k = 0; k < 7; ++k) o[45 + k] = zero_mass ? 0.0 : hu[k];
+    moments_epilogue_serial(N, grp, n, W, SX, SY, ax, ay, rl.gx[r], rl.gy[r],
+                            out + (size_t)r * cfg.ncols + cfg.col_mom + grp * 52);
 }
 
 // Intensity statistics of the staged S ROIs (intensity_features.cpp:42-215), one
@@ -2444,6 +2454,344 @@ __device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
     for (int k = 0; k < 32; ++k) oi[k] = o32[k];
 }
 
+// ---- the serial passes with G lanes per ROI -----------------------------------
+//
+// Thread-per-ROI left the pass in one partial wave (C2: 50k ROIs -> ~10 warps per
+// SM, latency-bound on the dependent fp64 chains).  Here G consecutive lanes share
+// a ROI: lane g takes the g-th chunk of the sorted values (or of the staged
+// pixels), partial sums combine by a fixed butterfly (deterministic), and the runs
+// that cross chunk borders (mode, histogram bins) are stitched in lane order by
+// the group's first lane, which then writes the row.
+#ifndef FXG_SERIAL_G
+#define FXG_SERIAL_G 8
+#endif
+constexpr int kSerialG = FXG_SERIAL_G;
+
+template <typename T>
+__device__ __forceinline__ T group_sum(T v, unsigned gm) {
+#pragma unroll
+    for (int o = kSerialG / 2; o >= 1; o >>= 1) v += __shfl_xor_sync(gm, v, o, kSerialG);
+    return v;
+}
+
+// One chunk's runs: the first run (may continue the previous chunk), the last run
+// (may continue into the next), and whether the chunk is one single run.
+struct ChunkRuns {
+    uint32_t fv, fl, lv, ll;
+    bool single;
+};
+
+// stitch the chunk runs of the G lanes in lane order (called by every lane; the
+// result is meaningful on the group's first lane).  done(v, len) is called for
+// every run completed across a border, and for the final run.
+template <typename Done>
+__device__ __forceinline__ void stitch_runs(const ChunkRuns& c, bool nonempty, unsigned gm,
+                                            Done&& done) {
+    uint32_t cv = 0, cl = 0;
+    bool have = false;
+#pragma unroll 1
+    for (int k = 0; k < kSerialG; ++k) {
+        const bool ne = __shfl_sync(gm, (int)nonempty, k, kSerialG) != 0;
+        const uint32_t fv = __shfl_sync(gm, c.fv, k, kSerialG), fl = __shfl_sync(gm, c.fl, k, kSerialG);
+        const uint32_t lv = __shfl_sync(gm, c.lv, k, kSerialG), ll = __shfl_sync(gm, c.ll, k, kSerialG);
+        const bool single = __shfl_sync(gm, (int)c.single, k, kSerialG) != 0;
+        if (!ne) continue;
+        if (have && fv == cv) {
+            cl += fl;
+        } else {
+            if (have) done(cv, cl);
+            cv = fv;
+            cl = fl;
+            have = true;
+        }
+        if (!single) {
+            done(cv, cl);  // the first run ended inside chunk k
+            cv = lv;
+            cl = ll;
+        }
+    }
+    if (have) done(cv, cl);
+}
+
+__device__ void intensity_group(uint32_t r, uint32_t g, unsigned gm, const RoiList& rl,
+                                const FeatCfg& cfg, double* out) {
+    const unsigned long long off = cfg.int_off[r];
+    if (off == ~0ull) return;  // not staged: the warp path wrote the columns (group-uniform)
+    const uint32_t n = (uint32_t)rl.n[r];
+    const uint16_t* s = cfg.int_vals + off;
+    const unsigned long long sS = cfg.int_sums[(size_t)r * 2], sQ = cfg.int_sums[(size_t)r * 2 + 1];
+    const double dn = (double)n, mean = (double)sS / dn;
+    const uint32_t vmin = s[0], vmax = s[n - 1];
+    const double p10 = percentile_exact(s, n, 10.0), p90 = percentile_exact(s, n, 90.0);
+    const uint32_t nb32 = (uint32_t)cfg.bins, rng = vmax - vmin;
+    const bool wide = (unsigned long long)nb32 * 65535ull >= (1ull << 32);
+    const uint32_t magic = rng ? (uint32_t)(0xffffffffull / rng) : 0u;
+    auto bin_of = [&](uint32_t v) -> uint32_t {  // floor(nb (v - min) / range), exact
+        if (rng == 0) return 0u;
+        uint32_t b;
+        if (!wide) {
+            const uint32_t num = nb32 * (v - vmin);
+            b = __umulhi(num, magic);
+            if (num - b * rng >= rng) ++b;
+        } else {
+            b = (uint32_t)((unsigned long long)nb32 * (v - vmin) / rng);
+        }
+        return b < nb32 - 1 ? b : nb32 - 1;
+    };
+    const double logn = nlog2(dn);
+    // integer thresholds for the integer values: v < mean <=> v < ceil(mean);
+    // p10 <= v <= p90 <=> ceil(p10) <= v <= floor(p90) (exact: v < 2^16)
+    const uint32_t t_mean = (uint32_t)ceil(mean), t_lo = (uint32_t)ceil(p10), t_hi = (uint32_t)floor(p90);
+    // this lane's chunk: [a, e), a multiple of 8 (16 B aligned loads)
+    const uint32_t C = ((n + kSerialG - 1) / kSerialG + 7u) & ~7u;
+    const uint32_t a = min(n, g * C), e = min(n, a + C);
+    const bool nonempty = a < e;
+    double a3 = 0, a4 = 0, a5 = 0, a6 = 0, ent = 0;
+    unsigned long long best = 0, usq = 0;
+    uint32_t slo = 0, rsum = 0, clo = 0, rn = 0;
+    ChunkRuns vr{0, 0, 0, 0, true}, br{0, 0, 0, 0, true};
+    if (nonempty) {
+        uint32_t pv_ = s[a], pb_ = bin_of(s[a]), run_v = 0, run_b = 0;
+        bool vfirst = true, bfirst = true;
+        vr.fv = pv_;
+        br.fv = pb_;
+        const uint4* s4 = reinterpret_cast<const uint4*>(s + a);
+        for (uint32_t q = 0; a + q * 8u < e; ++q) {
+            const uint4 w4 = s4[q];
+            const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (a + q * 8u + (uint32_t)u >= e) break;
+                const uint32_t v = (wv[u >> 1] >> ((u & 1) * 16)) & 0xffffu;
+                const double d = (double)v - mean, d2 = d * d;
+                a3 += d2 * d;
+                a4 += d2 * d2;
+                a5 += d2 * d2 * d;
+                a6 += d2 * d2 * d2;
+                if (v < t_mean) {
+                    slo += v;
+                    ++clo;
+                }
+                if (v >= t_lo && v <= t_hi) {
+                    rsum += v;
+                    ++rn;
+                }
+                if (v != pv_) {  // a value run ended
+                    if (vfirst) {
+                        vr.fl = run_v;
+                        vfirst = false;
+                    } else {
+                        const unsigned long long key = ((unsigned long long)run_v << 16) | (0xffffu - pv_);
+                        best = key > best ? key : best;
+                    }
+                    pv_ = v;
+                    run_v = 0;
+                }
+                ++run_v;
+                const uint32_t b = bin_of(v);
+                if (b != pb_) {  // a bin run ended
+                    if (bfirst) {
+                        br.fl = run_b;
+                        bfirst = false;
+                    } else {
+                        ent += (double)run_b * (logn - log2_int(run_b));
+                        usq += (unsigned long long)run_b * run_b;
+                    }
+                    pb_ = b;
+                    run_b = 0;
+                }
+                ++run_b;
+            }
+        }
+        vr.lv = pv_;
+        vr.ll = run_v;
+        vr.single = vfirst;
+        if (vfirst) vr.fl = run_v;
+        br.lv = pb_;
+        br.ll = run_b;
+        br.single = bfirst;
+        if (bfirst) br.fl = run_b;
+    }
+    // fixed-order combination (butterfly: identical on every lane)
+    a3 = group_sum(a3, gm);
+    a4 = group_sum(a4, gm);
+    a5 = group_sum(a5, gm);
+    a6 = group_sum(a6, gm);
+    ent = group_sum(ent, gm);
+    usq = group_sum(usq, gm);
+    slo = group_sum(slo, gm);
+    clo = group_sum(clo, gm);
+    rsum = group_sum(rsum, gm);
+    rn = group_sum(rn, gm);
+#pragma unroll
+    for (int o = kSerialG / 2; o >= 1; o >>= 1) {
+        const unsigned long long ob = __shfl_xor_sync(gm, best, o, kSerialG);
+        best = ob > best ? ob : best;
+    }
+    stitch_runs(vr, nonempty, gm, [&](uint32_t v, uint32_t len) {
+        const unsigned long long key = ((unsigned long long)len << 16) | (0xffffu - v);
+        best = key > best ? key : best;
+    });
+    stitch_runs(br, nonempty, gm, [&](uint32_t, uint32_t len) {
+        ent += (double)len * (logn - log2_int(len));
+        usq += (unsigned long long)len * len;
+    });
+    // rmad: the [p10, p90] subset below its mean is one contiguous range of the
+    // sorted values; each lane sums its part of it
+    double rmean = 0;
+    unsigned long long rlo = 0;
+    uint32_t rcl = 0;
+    if (rn > 0) {
+        rmean = (double)rsum / (double)rn;
+        const uint32_t t_rm = (uint32_t)ceil(rmean);
+        if (nonempty && s[a] < t_rm) {
+            const uint4* s4 = reinterpret_cast<const uint4*>(s + a);
+            bool more = true;
+            for (uint32_t q = 0; more && a + q * 8u < e; ++q) {
+                const uint4 w4 = s4[q];
+                const uint32_t wv[4] = {w4.x, w4.y, w4.z, w4.w};
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t v = (wv[u >> 1] >> ((u & 1) * 16)) & 0xffffu;
+                    if (a + q * 8u + (uint32_t)u >= e || v >= t_rm) {
+                        more = false;
+                        break;
+                    }
+                    if (v >= t_lo && v <= t_hi) {
+                        rlo += v;
+                        ++rcl;
+                    }
+                }
+            }
+        }
+        rlo = group_sum(rlo, gm);
+        rcl = group_sum(rcl, gm);
+    }
+    if (g != 0) return;
+    const double mn = (double)vmin, mxv = (double)vmax;
+    const double median = (n & 1) ? (double)s[n / 2] : 0.5 * ((double)s[n / 2 - 1] + (double)s[n / 2]);
+    const double p1 = percentile_exact(s, n, 1.0), p25 = percentile_exact(s, n, 25.0),
+                 p75 = percentile_exact(s, n, 75.0), p99 = percentile_exact(s, n, 99.0);
+    const uint32_t M2 = (n & 1) ? 2u * s[n / 2] : (uint32_t)s[n / 2 - 1] + s[n / 2];
+    uint32_t d_hi, d_lo;
+    kth_dev_pair(s, n, M2, d_hi, d_lo);
+    const double median_ad = (n & 1) ? 0.5 * (double)d_hi : 0.5 * (0.5 * (double)d_lo + 0.5 * (double)d_hi);
+    // m2 needs no pass: n^2 m2 = n sQ - sS^2 exactly (both < 2^64 for any n <= 65536)
+    const double m2 = (double)((unsigned long long)n * sQ - sS * sS) / (dn * dn);
+    const double m3 = a3 / dn, m4 = a4 / dn, m5 = a5 / dn, m6 = a6 / dn;
+    const double mad = ((double)(long long)(sS - 2ull * slo) +
+                        (double)((long long)clo - (long long)(n - clo)) * mean) / dn;
+    const double rmad = rn > 0 ? ((double)(long long)(rsum - 2 * rlo) +
+                                  (double)((long long)rcl - (long long)(rn - rcl)) * rmean) / (double)rn
+                               : 0.0;
+    const double var = n > 1 ? m2 * dn / (dn - 1.0) : 0.0;
+    double skew = 0, kurt = 0, hsk = 0, hfl = 0;
+    if (m2 > 0) {
+        const double r2 = sqrt(m2);
+        skew = m3 / (m2 * r2);
+        kurt = m4 / (m2 * m2);
+        hsk = m5 / (m2 * m2 * r2);
+        hfl = m6 / (m2 * m2 * m2);
+    }
+    const double energy = (double)sQ, sdev = sqrt(var), iqr = p75 - p25;
+    const double o32[32] = {mean, median, (double)(0xffffu - (uint32_t)(best & 0xffffu)), mn, mxv,
+                            mxv - mn, var, m2, sdev, sqrt(m2), mad, median_ad, rmad, iqr,
+                            p1, p10, p25, p75, p90, p99, skew, kurt,
+                            m2 > 0 ? kurt - 3.0 : 0.0, hsk, hfl, energy, sqrt(energy / dn), ent / dn,
+                            (double)usq / (dn * dn), (p75 + p25) != 0 ? iqr / (p75 + p25) : 0.0,
+                            mean != 0 ? sdev / mean : 0.0, (double)sS};
+    double* oi = out + (size_t)r * cfg.ncols + cfg.col_int;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) oi[k] = o32[k];
+}
+
+// Moments with G lanes per ROI: lane g sums its chunk of staged pixel quads, the
+// 16 sums combine by butterfly, the group's first lane runs the epilogue.
+__device__ void moments_group(uint32_t r, int grp, uint32_t g, unsigned gm, const RoiList& rl,
+                              const FeatCfg& cfg, double* out) {
+    const unsigned long long off = cfg.mom_off[r];
+    if (off == ~0ull) return;  // not staged: the warp path wrote the columns (group-uniform)
+    const uint32_t n = (uint32_t)rl.n[r];
+    const unsigned long long* sums = cfg.mom_sums + (size_t)r * 5;
+    const long long nn = (long long)n;
+    double N[16];
+    long long W = 0, ax, ay, SX, SY;
+    if (grp == 0) {
+        SX = (long long)sums[3];
+        SY = (long long)sums[4];
+        ax = (2 * SX + nn) / (2 * nn);
+        ay = (2 * SY + nn) / (2 * nn);
+    } else {
+        W = (long long)sums[0];
+        SX = (long long)sums[1];
+        SY = (long long)sums[2];
+        ax = W > 0 ? (2 * SX + W) / (2 * W) : 0;
+        ay = W > 0 ? (2 * SY + W) / (2 * W) : 0;
+    }
+    const uint4* px4 = reinterpret_cast<const uint4*>(cfg.mom_px + off);  // 16 B aligned
+    const uint32_t nq = (n + 3u) >> 2, cq = (nq + kSerialG - 1) / kSerialG;
+    const uint32_t q0 = min(nq, g * cq), q1 = min(nq, q0 + cq);
+    auto stream = [&](auto&& pixel) {
+        for (uint32_t q4 = q0; q4 < q1; ++q4) {
+            const uint4 cur = px4[q4];
+            const uint32_t base = q4 * 4u;
+            pixel(cur.x);
+            if (base + 1 < n) pixel(cur.y);
+            if (base + 2 < n) pixel(cur.z);
+            if (base + 3 < n) pixel(cur.w);
+        }
+    };
+    if (grp == 0) {
+        long long M[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) M[k] = 0;
+        stream([&](uint32_t e) {
+            const int dx = (int)(e & 0xffu) - (int)ax, dy = (int)((e >> 8) & 0xffu) - (int)ay;
+            const int X[4] = {1, dx, dx * dx, dx * dx * dx};
+            const int Y[4] = {1, dy, dy * dy, dy * dy * dy};
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (p + q >= 2) M[p * 4 + q] += (long long)X[p] * Y[q];
+        });
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k != 0 && k != 1 && k != 4) M[k] = group_sum(M[k], gm);
+        // the order-0 / order-1 sums follow from the staged exact sums
+        M[0] = nn;
+        M[1] = SY - ay * nn;
+        M[4] = SX - ax * nn;
+#pragma unroll
+        for (int k = 0; k < 16; ++k) N[k] = (double)M[k];
+    } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) N[k] = 0;
+        stream([&](uint32_t e) {
+            const double dx = (double)((long long)(e & 0xffu) - ax);
+            const double dy = (double)((long long)((e >> 8) & 0xffu) - ay);
+            const double wv = (double)(e >> 16);
+            const double pw[4] = {wv, wv * dx, wv * dx * dx, wv * dx * dx * dx};
+            const double q[4] = {1.0, dy, dy * dy, dy * dy * dy};
+#pragma unroll
+            for (int p = 0; p < 4; ++p)
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (p + k >= 2) N[p * 4 + k] += pw[p] * q[k];
+        });
+#pragma unroll
+        for (int k = 0; k < 16; ++k)
+            if (k != 0 && k != 1 && k != 4) N[k] = group_sum(N[k], gm);
+        // the order-0 / order-1 sums follow from the staged exact integer sums
+        N[0] = (double)W;
+        N[1] = (double)(SY - ay * W);
+        N[4] = (double)(SX - ax * W);
+    }
+    if (g != 0) return;
+    moments_epilogue_serial(N, grp, n, W, SX, SY, ax, ay, rl.gx[r], rl.gy[r],
+                            out + (size_t)r * cfg.ncols + cfg.col_mom + grp * 52);
+}
+
 // the per-ROI serial passes of the S ROIs in one launch: blocks [0, bi) run the
 // intensity statistics, [bi, bi + bm) the binary moments, the rest the weighted
 // moments, so the sparse waves overlap (and binary moments use the integer pipe
@@ -2458,16 +2806,26 @@ __global__ void __launch_bounds__(FXG_SERIAL_TPB, FXG_SERIAL_MINB)
     k_serial_stats(RoiList rl, Control* ctl, FeatCfg cfg, double* out, uint32_t bi, uint32_t bm) {
     const uint32_t b = blockIdx.x;
     const uint32_t t = (b < bi ? b : b < bi + bm ? b - bi : b - bi - bm) * blockDim.x + threadIdx.x;
+#if FXG_SERIAL_G > 1
+    // G lanes per ROI (group-uniform exits keep the group's shuffles converged)
+    const uint32_t g = t % kSerialG, lane = threadIdx.x & 31;
+    const unsigned gm = (kSerialG == 32 ? kFull : ((1u << kSerialG) - 1u)) << (lane & ~(uint32_t)(kSerialG - 1));
+    const uint32_t r = s_row_of(t / kSerialG, rl, ctl);
+    if (r == ~0u) return;
+    if (b < bi) intensity_group(r, g, gm, rl, cfg, out);
+    else moments_group(r, b < bi + bm ? 0 : 1, g, gm, rl, cfg, out);
+#else
     const uint32_t r = s_row_of(t, rl, ctl);
     if (r == ~0u) return;
     if (b < bi) intensity_row(r, rl, cfg, out);
     else moments_row(r, b < bi + bm ? 0 : 1, rl, cfg, out);
+#endif
 }
 
 void launch_serial_stats(int n_s, bool intensity, bool moments, cudaStream_t s, RoiList rl,
                          Control* ctl, FeatCfg cfg, double* out) {
     if (n_s <= 0 || (!intensity && !moments)) return;
-    const uint32_t nb = (uint32_t)((n_s + FXG_SERIAL_TPB - 1) / FXG_SERIAL_TPB);
+    const uint32_t nb = (uint32_t)(((size_t)n_s * kSerialG + FXG_SERIAL_TPB - 1) / FXG_SERIAL_TPB);
     const uint32_t bi = intensity ? nb : 0u, bm = moments ? nb : 0u;
     k_serial_stats<<<bi + 2 * bm, FXG_SERIAL_TPB, 0, s>>>(rl, ctl, cfg, out, bi, bm);
 }

@@ -164,6 +164,11 @@ class Context:
     def set_stream(self, stream_handle: int | None):
         _check(lib().fx_ctx_set_stream(self.h, C.c_void_p(stream_handle or 0)))
 
+    def set_band_rows(self, rows: int):
+        """Row-band height of the host-raster path (0 auto, < 0 off); results are
+        identical either way (fx_ctx_set_band_rows)."""
+        _check(lib().fx_ctx_set_band_rows(self.h, int(rows)))
+
     def launch_count(self) -> int:
         return int(lib().fx_ctx_launch_count(self.h))
 

@@ -147,3 +147,55 @@ def test_batch_device_rasters(ctx, stacked):
         sl, sv = ctx.featurize(I, L, GROUPS, p)
         assert np.array_equal(bl[offs[k]:offs[k + 1]], sl), k
         assert np.array_equal(bv[offs[k]:offs[k + 1]], sv), k
+
+
+# ---- banded host path (fx_featurize with host rasters: H2D / kernels / D2H
+# overlapped in row bands) must give exactly the unbanded rows ---------------
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("rows", [64, 128, 512])
+def test_banded_host_path_bitwise(ctx, rows):
+    import paper_2603_12016_b200 as fx
+    p = fx.resolve_profile("default")
+    # multi-component ROIs spanning many bands, holes, border contact, big windows
+    L = inputs.random_blobs((700, 300), 90, seed=7, max_r=40,
+                            label_values=np.array([1, 2, 3, 65535, 40000, 17, 900]))
+    L[650:700, 0:300:7] = 5  # one ROI spread over a wide strip of the bottom band
+    I = inputs.uniform(L.shape, 3)
+    try:
+        ctx.set_band_rows(-1)
+        rl, rv = ctx.featurize(I, L, GROUPS, p)
+        ctx.set_band_rows(rows)
+        bl, bv = ctx.featurize(I, L, GROUPS, p)
+    finally:
+        ctx.set_band_rows(0)
+    assert np.array_equal(rl, bl)
+    assert np.array_equal(rv, bv)
+
+
+@pytest.mark.gpu
+def test_banded_host_path_c2_bitwise(ctx):
+    """bench.py's e2e call (host rasters, automatic bands) == the device-resident call"""
+    import torch
+    import bench
+    import paper_2603_12016_b200 as fx
+    I, L, _ = bench.workload(0)
+    p = fx.resolve_profile(bench.PROFILE)
+    mask = fx.resolve_groups(bench.GROUPS)
+    ncols = len(fx.feature_columns(mask, p))
+    h, w = L.shape
+    n = bench.ROI_COUNT
+    dI = torch.from_numpy(I.view(np.int16)).cuda()
+    dL = torch.from_numpy(L.view(np.int16)).cuda()
+    ol = torch.empty(n, dtype=torch.int32, device="cuda")
+    ov = torch.empty((n, ncols), dtype=torch.float64, device="cuda")
+    assert ctx.featurize_device(dI.data_ptr(), dL.data_ptr(), w, h, w, mask, p, ol.data_ptr(),
+                                ov.data_ptr(), n) == n
+    hI = torch.from_numpy(I.view(np.int16)).pin_memory()
+    hL = torch.from_numpy(L.view(np.int16)).pin_memory()
+    hv = torch.empty((n, ncols), dtype=torch.float64).pin_memory()
+    hl = torch.empty(n, dtype=torch.int32).pin_memory()
+    assert ctx.featurize_host_ptrs(hI.data_ptr(), hL.data_ptr(), w, h, mask, p, hl.data_ptr(),
+                                   hv.data_ptr(), n) == n
+    assert torch.equal(hl, ol.cpu())
+    assert torch.equal(hv, ov.cpu())

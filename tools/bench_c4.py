@@ -99,11 +99,13 @@ def main():
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     l0 = ctx.launch_count()
     torch.cuda.synchronize()
-    ev0.record(stream)
-    for _ in range(args.steps):
-        offs = ctx.featurize_batch_raw(ims, T, mask, p, out_l.data_ptr(), out_v.data_ptr(), cap)
-    ev1.record(stream)
-    torch.cuda.synchronize()
+    from bench import ClockSampler
+    with ClockSampler(0) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            offs = ctx.featurize_batch_raw(ims, T, mask, p, out_l.data_ptr(), out_v.data_ptr(), cap)
+        ev1.record(stream)
+        torch.cuda.synchronize()
     ms = ev0.elapsed_time(ev1) / args.steps
     launches = (ctx.launch_count() - l0) // args.steps
     kt = ctx.kernel_times()
@@ -150,6 +152,7 @@ def main():
                 "d2h_bytes_per_step": int(offs[Te]) * (ncols * 8 + 4),
                 "matches_device_table": same},
         "setup_s": gen_s,
+        "clocks": clk.summary(),
     }
     print(json.dumps(line))
     ctx.close()

@@ -107,12 +107,14 @@ def main():
     ctx.enable_timing(True)
     ctx.reset_kernel_times()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
+    from bench import ClockSampler
     n_own = 0
-    for _ in range(args.steps):
-        n_own = run()
-    e1.record(stream)
-    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            n_own = run()
+        e1.record(stream)
+        torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     kt = ctx.kernel_times()
     n_all = n_own
@@ -138,7 +140,7 @@ def main():
             "roofline": {"bound": "hbm", "algorithmic_bytes": alg,
                          "achieved_gbs": alg / (ms / 1e3) / 1e9},
             "kernels_ms_per_step_rank0": {k_: v[0] / args.steps for k_, v in sorted(kt.items())},
-            "setup_s": gen_s}))
+            "setup_s": gen_s, "clocks": clk.summary()}))
     ctx.close()
     if args.sharded:
         dist.destroy_process_group()
