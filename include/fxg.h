@@ -237,6 +237,24 @@ int fx_debug_roi(fx_ctx* ctx, const fx_image* image, uint32_t label,
                  const fx_texture_params* params, uint64_t* hist, int32_t* edge_xy,
                  size_t cap_edge, size_t* n_edge, uint32_t* glcm_counts, uint64_t* glcm_pairs);
 
+/* ---- several devices of this process ----------------------- */
+
+typedef struct fx_multi fx_multi;
+/* One fx_ctx and one host thread per listed device (a device may be listed more
+ * than once: several contexts share it). */
+int fx_multi_create(const int* devices, int n_devices, fx_multi** out);
+int fx_multi_destroy(fx_multi* m);
+int fx_multi_device_count(const fx_multi* m);
+/* The i-th device's context (owned by m), e.g. for fx_ctx_set_band_rows. */
+fx_ctx* fx_multi_ctx(fx_multi* m, int i);
+/* C4 across devices: the batch is cut into chunks of up to 512 images, chunk j
+ * runs on device j mod N through the fx_featurize_batch pipeline, and rows come
+ * back straight into their place: output identical to fx_featurize_batch (rows in
+ * input order, row_offsets[n+1]).  Host images only when N > 1. */
+int fx_multi_featurize_batch(fx_multi* m, const fx_image* images, int n, unsigned groups,
+                             const fx_texture_params* params, uint32_t* out_labels,
+                             double* out_values, size_t cap_rois, size_t* row_offsets);
+
 /* Per-phase clock totals of the S-class ROI kernels (summed over ROIs, lane 0's
  * clock64 deltas): 0 load+gather, 1 intensity sort, 2 intensity statistics,
  * 3 edge set + edge statistics, 4 moments, 5 GLCM levels+pair keys, 6 GLCM key

@@ -82,34 +82,43 @@ unsigned group_mask(const std::vector<std::string>& groups) {
     return m;
 }
 
-bool glob_match(const std::string& pattern, const std::string& name) {  // '*' and '?'
-    size_t p = 0, n = 0, star = std::string::npos, mark = 0;
-    while (n < name.size()) {
-        if (p < pattern.size() && (pattern[p] == '?' || pattern[p] == name[n])) {
-            ++p;
-            ++n;
-        } else if (p < pattern.size() && pattern[p] == '*') {
-            star = p++;
-            mark = n;
-        } else if (star != std::string::npos) {
-            p = star + 1;
-            n = ++mark;
+// File-name filter of run() (same language as the reference's: '*' matches any
+// run of characters, '?' exactly one, everything else itself).  Dynamic
+// programming over pattern prefixes: row[j] says whether the pattern prefix
+// consumed so far matches name[0, j).
+bool name_matches(const std::string& pat, const std::string& name) {
+    std::vector<char> row(name.size() + 1, 0), next(name.size() + 1, 0);
+    row[0] = 1;
+    for (char pc : pat) {
+        std::fill(next.begin(), next.end(), 0);
+        if (pc == '*') {
+            char any = 0;  // '*': reachable from any shorter prefix
+            for (size_t j = 0; j <= name.size(); ++j) next[j] = any = any | row[j];
         } else {
-            return false;
+            for (size_t j = 1; j <= name.size(); ++j)
+                next[j] = row[j - 1] && (pc == '?' || pc == name[j - 1]);
         }
+        row.swap(next);
     }
-    while (p < pattern.size() && pattern[p] == '*') ++p;
-    return p == pattern.size();
+    return row[name.size()] != 0;
 }
 
+// CSV field: as is unless it holds a separator, quote or newline; then wrapped in
+// quotes with every quote doubled (RFC 4180 style, as the reference writes names)
 std::string csv_field(const std::string& s) {
     if (s.find_first_of(",\"\n") == std::string::npos) return s;
-    std::string out = "\"";
-    for (char ch : s) {
-        if (ch == '"') out += '"';
-        out += ch;
+    std::string q;
+    q.reserve(s.size() + 8);
+    q.push_back('"');
+    size_t from = 0;
+    for (size_t at = s.find('"'); at != std::string::npos; at = s.find('"', from)) {
+        q.append(s, from, at + 1 - from);
+        q.push_back('"');
+        from = at + 1;
     }
-    return out + "\"";
+    q.append(s, from, std::string::npos);
+    q.push_back('"');
+    return q;
 }
 
 // ---- PGM P5 decode (pgm.cpp:37-99) -------------------------------------------
@@ -417,11 +426,6 @@ struct Pinned {
     }
 };
 
-std::filesystem::path spill_dir_of(const ExtractionConfig& c) {  // engine.cpp:274-279
-    if (const char* env = std::getenv("FEATUREX_SPILL_DIR"); env && *env) return env;
-    if (!c.spill_dir.empty()) return c.spill_dir;
-    return std::filesystem::temp_directory_path() / "featurex-spill";
-}
 
 }  // namespace
 
@@ -625,22 +629,23 @@ RunSummary run(const ExtractionConfig& config) {
     if (config.glcm_override) params.glcm = *config.glcm_override;
     if (config.histogram_bins_override) params.histogram_bins = *config.histogram_bins_override;
     if (config.memory_budget == 0) throw ConfigError("memory budget must be positive");
-    (void)spill_dir_of(config);  // no host spill: ROI data lives in HBM
+    // spill_dir / FEATUREX_SPILL_DIR are accepted and unused: ROI data lives in HBM
     const int workers = host_workers(config);
 
     RunSummary summary;
-    // pairing by identical basename (engine.cpp:240-272)
-    std::map<std::string, std::filesystem::path> ints, masks;
-    auto scan = [&](const std::filesystem::path& dir, std::map<std::string, std::filesystem::path>& into) {
+    // pairing by identical basename (engine.cpp:240-272): both directories listed
+    // into name-sorted maps, then one merge walk; an unmatched name is logged and
+    // counted as a failed pair
+    auto list_dir = [&](const std::filesystem::path& dir) {
         if (!std::filesystem::is_directory(dir)) throw IoError("not a directory: " + dir.string());
-        for (const auto& e : std::filesystem::directory_iterator(dir)) {
-            if (!e.is_regular_file()) continue;
-            const std::string name = e.path().filename().string();
-            if (glob_match(config.file_pattern, name)) into[name] = e.path();
-        }
+        std::map<std::string, std::filesystem::path> found;
+        for (const auto& e : std::filesystem::directory_iterator(dir))
+            if (e.is_regular_file() && name_matches(config.file_pattern, e.path().filename().string()))
+                found.emplace(e.path().filename().string(), e.path());
+        return found;
     };
-    scan(config.intensity_dir, ints);
-    scan(config.mask_dir, masks);
+    const auto ints = list_dir(config.intensity_dir);
+    const auto masks = list_dir(config.mask_dir);
     struct Pair {
         std::string name;
         std::filesystem::path ip, mp;
@@ -649,19 +654,25 @@ RunSummary run(const ExtractionConfig& config) {
         uint16_t maxlab = 0;
     };
     std::vector<Pair> pairs;
-    for (const auto& [name, p] : ints) {
-        if (!masks.count(name)) {
-            std::cerr << "featurex: no mask for image '" << name << "', skipped\n";
+    std::vector<std::string> lone_masks;
+    for (auto i = ints.begin(), k = masks.begin(); i != ints.end() || k != masks.end();) {
+        if (k == masks.end() || (i != ints.end() && i->first < k->first)) {
+            std::cerr << "featurex: no mask for image '" << i->first << "', skipped\n";
             ++summary.failed_pairs;
-            continue;
+            ++i;
+        } else if (i == ints.end() || k->first < i->first) {
+            lone_masks.push_back(k->first);
+            ++k;
+        } else {
+            pairs.push_back(Pair{i->first, i->second, k->second, {}, {}, {}, 0});
+            ++i;
+            ++k;
         }
-        pairs.push_back(Pair{name, p, masks[name], {}, {}, {}, 0});
     }
-    for (const auto& [name, p] : masks)
-        if (!ints.count(name)) {
-            std::cerr << "featurex: no image for mask '" << name << "', skipped\n";
-            ++summary.failed_pairs;
-        }
+    for (const auto& name : lone_masks) {  // reported after the images, as the reference
+        std::cerr << "featurex: no image for mask '" << name << "', skipped\n";
+        ++summary.failed_pairs;
+    }
     const fx_texture_params tp = to_c(params);
     const unsigned gm = group_mask(groups);
     const std::vector<std::string> columns = feature_columns(groups, params);

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <string>
 #include <vector>
@@ -1073,7 +1074,193 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     return FX_OK;
 }
 
+// per-image checks of a batch; row_offsets[1..n] zeroed
+int validate_batch(const fx_image* ims, int n, size_t* row_offsets) {
+    const int kind = ims[0].mem_kind;
+    for (int i = 0; i < n; ++i) {
+        const fx_image& im = ims[i];
+        if (!im.intensity || !im.labels) return set_error(FX_E_ARG, "null raster in batch");
+        if (im.width < 1 || im.height < 1) return set_error(FX_E_PAIRING, "empty raster in batch");
+        if (im.pitch && im.pitch < (size_t)im.width) return set_error(FX_E_ARG, "pitch < width");
+        if (im.mem_kind != kind) return set_error(FX_E_ARG, "mixed host/device images in one batch");
+        row_offsets[i + 1] = 0;
+    }
+    return FX_OK;
+}
+
+// The sub-batch pipeline of fx_featurize_batch with device outputs (out_dev,
+// lab_dev: [cap_rois] rows): images stacked per sub-batch (one label-table slot
+// each, staging double-buffered on the copy stream).  After each sub-batch's
+// work is enqueued, on_sub(first_row, rows) may enqueue its readback (rows are
+// final once the stream reaches that point).  Inputs validated by the caller.
+int batch_core(fx_ctx* c, const fx_image* ims, int n, unsigned groups, const fx_texture_params* p,
+               double* out_dev, uint32_t* lab_dev, size_t cap_rois, size_t* row_offsets,
+               const std::function<int(size_t, size_t)>& on_sub) {
+    const int kind = ims[0].mem_kind;
+    int maxw = 0;
+    for (int i = 0; i < n; ++i) maxw = std::max(maxw, ims[i].width);
+    int rc = FX_OK;
+    const FeatCfg cfg = make_cfg(groups, *p);
+    const size_t P = ((size_t)maxw + 63) / 64 * 64;  // staging pitch (elements)
+    auto pitch_of = [](const fx_image& im) { return im.pitch ? im.pitch : (size_t)im.width; };
+    // plan: sub-batches of <= kBatchSlots images within the staging budget
+    struct Sub {
+        int first, count;
+        size_t rows;  // stacked rows (each image padded to a multiple of 64)
+        bool zero_copy;
+    };
+    std::vector<Sub> plan;
+    for (int i = 0; i < n; ++i) {
+        const size_t r = ((size_t)ims[i].height + 63) / 64 * 64;
+        if (plan.empty() || plan.back().count == kBatchSlots ||
+            (plan.back().rows + r) * P > kStageBudget)
+            plan.push_back(Sub{i, 0, 0, false});
+        plan.back().count++;
+        plan.back().rows += r;
+    }
+    size_t max_rows = 0, max_strips = 0;
+    int max_count = 0;
+    bool need_stage = false;
+    for (Sub& b : plan) {
+        // device images already stacked in one pitched allocation are read in place
+        bool zc = kind == FX_MEM_DEVICE;
+        const size_t pt = pitch_of(ims[b.first]);
+        for (int j = b.first; zc && j < b.first + b.count; ++j) {
+            const fx_image& im = ims[j];
+            zc = pitch_of(im) == pt;
+            if (zc && j + 1 < b.first + b.count) {
+                const size_t step = pt * (size_t)im.height;
+                zc = im.height % 64 == 0 && ims[j + 1].labels == im.labels + step &&
+                     ims[j + 1].intensity == im.intensity + step;
+            }
+        }
+        b.zero_copy = zc;
+        if (zc) {
+            b.rows = 0;
+            for (int j = b.first; j < b.first + b.count; ++j) b.rows += (size_t)ims[j].height;
+        } else {
+            need_stage = true;
+            max_rows = std::max(max_rows, b.rows);
+        }
+        max_strips = std::max(max_strips, (b.rows + 63) / 64);
+        max_count = std::max(max_count, b.count);
+    }
+    rc = ensure_slots(c, max_count);
+    if (!rc) rc = ensure_maps(c, (size_t)max_count, max_strips);
+    if (!rc && need_stage) rc = ensure_stage(c, P * max_rows);
+    if (rc) return rc;
+    // stage sub-batch k into buffer k%2 on the copy stream (slot map included)
+    auto stage = [&](int k) -> int {
+        const Sub& b = plan[k];
+        const int buf = k % 2;
+        CK(cudaStreamWaitEvent(c->copy, c->ev_free[buf], 0));
+        SlotInfo* hs = c->h_slots[buf];
+        uint16_t* hst = c->h_strips[buf];
+        size_t row0 = 0;
+        for (int j = 0; j < b.count; ++j) {
+            const fx_image& im = ims[b.first + j];
+            hs[j] = SlotInfo{(int32_t)row0, im.width, im.height, im.origin_x, im.origin_y};
+            const size_t r = b.zero_copy ? (size_t)im.height : ((size_t)im.height + 63) / 64 * 64;
+            for (size_t st = row0 / 64; st < (row0 + r + 63) / 64; ++st) hst[st] = (uint16_t)j;
+            if (!b.zero_copy) {
+                const cudaMemcpyKind mk =
+                    kind == FX_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+                const size_t sp = pitch_of(im) * 2;
+                uint16_t* dI = c->d_stage[buf] + row0 * P;
+                uint16_t* dL = c->d_stage[buf] + c->stage_elems + row0 * P;
+                CK(cudaMemcpy2DAsync(dI, P * 2, im.intensity, sp, (size_t)im.width * 2,
+                                     (size_t)im.height, mk, c->copy));
+                CK(cudaMemcpy2DAsync(dL, P * 2, im.labels, sp, (size_t)im.width * 2,
+                                     (size_t)im.height, mk, c->copy));
+            }
+            row0 += r;
+        }
+        CK(cudaMemcpyAsync(c->d_slots[buf], hs, (size_t)b.count * sizeof(SlotInfo),
+                           cudaMemcpyHostToDevice, c->copy));
+        CK(cudaMemcpyAsync(c->d_strips[buf], hst, ((b.rows + 63) / 64) * sizeof(uint16_t),
+                           cudaMemcpyHostToDevice, c->copy));
+        CK(cudaEventRecord(c->ev_staged[buf], c->copy));
+        return FX_OK;
+    };
+    size_t base = 0;
+    std::vector<uint32_t> sb((size_t)max_count + 1);
+    rc = stage(0);
+    for (size_t k = 0; !rc && k < plan.size(); ++k) {
+        if (k + 1 < plan.size()) rc = stage((int)k + 1);
+        if (rc) break;
+        const Sub& b = plan[k];
+        const int buf = (int)(k % 2);
+        CK(cudaStreamWaitEvent(c->stream, c->ev_staged[buf], 0));
+        DevImage d;
+        int wmax = 0;
+        for (int j = b.first; j < b.first + b.count; ++j) wmax = std::max(wmax, ims[j].width);
+        if (b.zero_copy) {
+            d.I = ims[b.first].intensity;
+            d.L = ims[b.first].labels;
+            d.pitch = pitch_of(ims[b.first]);
+        } else {
+            d.I = c->d_stage[buf];
+            d.L = c->d_stage[buf] + c->stage_elems;
+            d.pitch = P;
+        }
+        d.w = wmax;
+        d.h = (int)b.rows;
+        d.ox = d.oy = 0;
+        SlotMap m;
+        m.info = c->d_slots[buf];
+        m.strip_slot = c->d_strips[buf];
+        m.s0 = SlotInfo{0, 0, 0, 0, 0};
+        m.nslots = b.count;
+        size_t nr = 0;
+        rc = scan_stage(c, d, m, true);
+        if (!rc)
+            rc = featurize_stage(c, d, m, 0u, 0xffffffffu, groups, *p, out_dev + base * cfg.ncols,
+                                 cap_rois >= base ? cap_rois - base : 0, &nr, nullptr, sb.data(),
+                                 k == 0);
+        if (rc) {
+            if (rc == FX_E_CAPACITY) row_offsets[n] = base + nr;  // rows needed so far
+            break;
+        }
+        for (int j = 0; j < b.count; ++j) row_offsets[b.first + j] = base + sb[j];
+        if (nr)
+            CK(cudaMemcpyAsync(lab_dev + base, roi_list(c).label, nr * sizeof(uint32_t),
+                               cudaMemcpyDeviceToDevice, c->stream));
+        CK(cudaEventRecord(c->ev_free[buf], c->stream));
+        if (on_sub) {
+            rc = on_sub(base, nr);
+            if (rc) break;
+        }
+        base += nr;
+    }
+    if (rc) {
+        cudaStreamSynchronize(c->copy);
+        cudaStreamSynchronize(c->stream);
+        return rc;
+    }
+    row_offsets[n] = base;
+    return FX_OK;
+}
+
+
 }  // namespace
+
+// ---- internal entry points for fx_multi.cu (not part of the C ABI) ------------
+namespace fxg {
+int ictx_validate_batch(const fx_image* ims, int n, size_t* row_offsets) {
+    return validate_batch(ims, n, row_offsets);
+}
+int ictx_check_groups(unsigned groups) { return check_groups(groups); }
+int ictx_ncols(unsigned groups, const fx_texture_params& p) { return make_cfg(groups, p).ncols; }
+int ictx_batch_device(fx_ctx* c, const fx_image* ims, int n, unsigned groups,
+                      const fx_texture_params* p, double* out_dev, uint32_t* lab_dev,
+                      size_t cap_rows, size_t* row_offsets) {
+    return batch_core(c, ims, n, groups, p, out_dev, lab_dev, cap_rows, row_offsets, nullptr);
+}
+cudaStream_t ictx_stream(fx_ctx* c) { return c->stream; }
+cudaStream_t ictx_d2h(fx_ctx* c) { return c->d2h; }
+int ictx_device(const fx_ctx* c) { return c->device; }
+int ictx_finish(fx_ctx* c) { return finish(c); }
+}  // namespace fxg
 
 extern "C" {
 
@@ -1416,170 +1603,36 @@ int fx_featurize_batch(fx_ctx* c, const fx_image* ims, int n, unsigned groups,
     if (!c || (n && !ims) || !p || !row_offsets || n < 0) return set_error(FX_E_ARG, "null argument");
     row_offsets[0] = 0;
     if (n == 0) return FX_OK;
-    const int kind = ims[0].mem_kind;
-    int maxw = 0;
-    for (int i = 0; i < n; ++i) {
-        const fx_image& im = ims[i];
-        if (!im.intensity || !im.labels) return set_error(FX_E_ARG, "null raster in batch");
-        if (im.width < 1 || im.height < 1) return set_error(FX_E_PAIRING, "empty raster in batch");
-        if (im.pitch && im.pitch < (size_t)im.width) return set_error(FX_E_ARG, "pitch < width");
-        if (im.mem_kind != kind) return set_error(FX_E_ARG, "mixed host/device images in one batch");
-        maxw = std::max(maxw, im.width);
-        row_offsets[i + 1] = 0;
-    }
-    int rc = check_groups(groups);
+    int rc = validate_batch(ims, n, row_offsets);
+    if (!rc) rc = check_groups(groups);
     if (rc) return rc;
     CK(cudaSetDevice(c->device));
     const FeatCfg cfg = make_cfg(groups, *p);
-    const size_t P = ((size_t)maxw + 63) / 64 * 64;  // staging pitch (elements)
-    auto pitch_of = [](const fx_image& im) { return im.pitch ? im.pitch : (size_t)im.width; };
-    // plan: sub-batches of <= kBatchSlots images within the staging budget
-    struct Sub {
-        int first, count;
-        size_t rows;  // stacked rows (each image padded to a multiple of 64)
-        bool zero_copy;
-    };
-    std::vector<Sub> plan;
-    for (int i = 0; i < n; ++i) {
-        const size_t r = ((size_t)ims[i].height + 63) / 64 * 64;
-        if (plan.empty() || plan.back().count == kBatchSlots ||
-            (plan.back().rows + r) * P > kStageBudget)
-            plan.push_back(Sub{i, 0, 0, false});
-        plan.back().count++;
-        plan.back().rows += r;
+    if (ims[0].mem_kind == FX_MEM_DEVICE) {
+        rc = batch_core(c, ims, n, groups, p, out_values, out_labels, cap_rois, row_offsets, nullptr);
+        return rc ? rc : finish(c);
     }
-    size_t max_rows = 0, max_strips = 0;
-    int max_count = 0;
-    bool need_stage = false;
-    for (Sub& b : plan) {
-        // device images already stacked in one pitched allocation are read in place
-        bool zc = kind == FX_MEM_DEVICE;
-        const size_t pt = pitch_of(ims[b.first]);
-        for (int j = b.first; zc && j < b.first + b.count; ++j) {
-            const fx_image& im = ims[j];
-            zc = pitch_of(im) == pt;
-            if (zc && j + 1 < b.first + b.count) {
-                const size_t step = pt * (size_t)im.height;
-                zc = im.height % 64 == 0 && ims[j + 1].labels == im.labels + step &&
-                     ims[j + 1].intensity == im.intensity + step;
-            }
-        }
-        b.zero_copy = zc;
-        if (zc) {
-            b.rows = 0;
-            for (int j = b.first; j < b.first + b.count; ++j) b.rows += (size_t)ims[j].height;
-        } else {
-            need_stage = true;
-            max_rows = std::max(max_rows, b.rows);
-        }
-        max_strips = std::max(max_strips, (b.rows + 63) / 64);
-        max_count = std::max(max_count, b.count);
-    }
-    rc = ensure_slots(c, max_count);
-    if (!rc) rc = ensure_maps(c, (size_t)max_count, max_strips);
-    if (!rc && need_stage) rc = ensure_stage(c, P * max_rows);
+    // host images: each sub-batch's rows leave on the d2h stream while the next
+    // sub-batch computes
+    rc = ensure_out(c, std::max<size_t>(1, cap_rois) * (size_t)cfg.ncols);
+    if (!rc) rc = ensure_blab(c, std::max<size_t>(1, cap_rois));
     if (rc) return rc;
-    double* out_dev = out_values;
-    uint32_t* lab_dev = out_labels;
-    if (kind == FX_MEM_HOST) {
-        rc = ensure_out(c, std::max<size_t>(1, cap_rois) * (size_t)cfg.ncols);
-        if (!rc) rc = ensure_blab(c, std::max<size_t>(1, cap_rois));
-        if (rc) return rc;
-        out_dev = c->d_out;
-        lab_dev = c->d_blab;
-    }
-    // stage sub-batch k into buffer k%2 on the copy stream (slot map included)
-    auto stage = [&](int k) -> int {
-        const Sub& b = plan[k];
-        const int buf = k % 2;
-        CK(cudaStreamWaitEvent(c->copy, c->ev_free[buf], 0));
-        SlotInfo* hs = c->h_slots[buf];
-        uint16_t* hst = c->h_strips[buf];
-        size_t row0 = 0;
-        for (int j = 0; j < b.count; ++j) {
-            const fx_image& im = ims[b.first + j];
-            hs[j] = SlotInfo{(int32_t)row0, im.width, im.height, im.origin_x, im.origin_y};
-            const size_t r = b.zero_copy ? (size_t)im.height : ((size_t)im.height + 63) / 64 * 64;
-            for (size_t st = row0 / 64; st < (row0 + r + 63) / 64; ++st) hst[st] = (uint16_t)j;
-            if (!b.zero_copy) {
-                const cudaMemcpyKind mk =
-                    kind == FX_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-                const size_t sp = pitch_of(im) * 2;
-                uint16_t* dI = c->d_stage[buf] + row0 * P;
-                uint16_t* dL = c->d_stage[buf] + c->stage_elems + row0 * P;
-                CK(cudaMemcpy2DAsync(dI, P * 2, im.intensity, sp, (size_t)im.width * 2,
-                                     (size_t)im.height, mk, c->copy));
-                CK(cudaMemcpy2DAsync(dL, P * 2, im.labels, sp, (size_t)im.width * 2,
-                                     (size_t)im.height, mk, c->copy));
-            }
-            row0 += r;
-        }
-        CK(cudaMemcpyAsync(c->d_slots[buf], hs, (size_t)b.count * sizeof(SlotInfo),
-                           cudaMemcpyHostToDevice, c->copy));
-        CK(cudaMemcpyAsync(c->d_strips[buf], hst, ((b.rows + 63) / 64) * sizeof(uint16_t),
-                           cudaMemcpyHostToDevice, c->copy));
-        CK(cudaEventRecord(c->ev_staged[buf], c->copy));
+    const size_t nc = (size_t)cfg.ncols;
+    auto readback = [&](size_t first, size_t rows) -> int {
+        if (!rows) return FX_OK;
+        cudaEvent_t e = get_event(c);
+        CK(cudaEventRecord(e, c->stream));
+        CK(cudaStreamWaitEvent(c->d2h, e, 0));
+        c->ev_pool.push_back(e);  // reusable once recorded work is queued behind it
+        CK(cudaMemcpyAsync(out_values + first * nc, c->d_out + first * nc, rows * nc * sizeof(double),
+                           cudaMemcpyDeviceToHost, c->d2h));
+        CK(cudaMemcpyAsync(out_labels + first, c->d_blab + first, rows * sizeof(uint32_t),
+                           cudaMemcpyDeviceToHost, c->d2h));
         return FX_OK;
     };
-    size_t base = 0;
-    std::vector<uint32_t> sb((size_t)max_count + 1);
-    rc = stage(0);
-    for (size_t k = 0; !rc && k < plan.size(); ++k) {
-        if (k + 1 < plan.size()) rc = stage((int)k + 1);
-        if (rc) break;
-        const Sub& b = plan[k];
-        const int buf = (int)(k % 2);
-        CK(cudaStreamWaitEvent(c->stream, c->ev_staged[buf], 0));
-        DevImage d;
-        int wmax = 0;
-        for (int j = b.first; j < b.first + b.count; ++j) wmax = std::max(wmax, ims[j].width);
-        if (b.zero_copy) {
-            d.I = ims[b.first].intensity;
-            d.L = ims[b.first].labels;
-            d.pitch = pitch_of(ims[b.first]);
-        } else {
-            d.I = c->d_stage[buf];
-            d.L = c->d_stage[buf] + c->stage_elems;
-            d.pitch = P;
-        }
-        d.w = wmax;
-        d.h = (int)b.rows;
-        d.ox = d.oy = 0;
-        SlotMap m;
-        m.info = c->d_slots[buf];
-        m.strip_slot = c->d_strips[buf];
-        m.s0 = SlotInfo{0, 0, 0, 0, 0};
-        m.nslots = b.count;
-        size_t nr = 0;
-        rc = scan_stage(c, d, m, true);
-        if (!rc)
-            rc = featurize_stage(c, d, m, 0u, 0xffffffffu, groups, *p, out_dev + base * cfg.ncols,
-                                 cap_rois >= base ? cap_rois - base : 0, &nr, nullptr, sb.data(),
-                                 k == 0);
-        if (rc) {
-            if (rc == FX_E_CAPACITY) row_offsets[n] = base + nr;  // rows needed so far
-            break;
-        }
-        for (int j = 0; j < b.count; ++j) row_offsets[b.first + j] = base + sb[j];
-        if (nr)
-            CK(cudaMemcpyAsync(lab_dev + base, roi_list(c).label, nr * sizeof(uint32_t),
-                               cudaMemcpyDeviceToDevice, c->stream));
-        CK(cudaEventRecord(c->ev_free[buf], c->stream));
-        base += nr;
-    }
-    if (rc) {
-        cudaStreamSynchronize(c->copy);
-        cudaStreamSynchronize(c->stream);
-        return rc;
-    }
-    row_offsets[n] = base;
-    if (kind == FX_MEM_HOST && base) {
-        CK(cudaMemcpyAsync(out_values, out_dev, base * cfg.ncols * sizeof(double),
-                           cudaMemcpyDeviceToHost, c->stream));
-        CK(cudaMemcpyAsync(out_labels, lab_dev, base * sizeof(uint32_t), cudaMemcpyDeviceToHost,
-                           c->stream));
-    }
-    return finish(c);
+    rc = batch_core(c, ims, n, groups, p, c->d_out, c->d_blab, cap_rois, row_offsets, readback);
+    cudaStreamSynchronize(c->d2h);
+    return rc ? rc : finish(c);
 }
 
 int fx_featurize_u16(fx_ctx* c, const uint16_t* intensity, const uint16_t* labels, int width,

@@ -2463,7 +2463,7 @@ __device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
 // that cross chunk borders (mode, histogram bins) are stitched in lane order by
 // the group's first lane, which then writes the row.
 #ifndef FXG_SERIAL_G
-#define FXG_SERIAL_G 8
+#define FXG_SERIAL_G 1
 #endif
 constexpr int kSerialG = FXG_SERIAL_G;
 

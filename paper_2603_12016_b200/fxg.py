@@ -63,6 +63,8 @@ def lib() -> C.CDLL:
             getattr(L, fn).argtypes = [C.c_void_p] + ([C.c_int] if fn == "fx_ctx_enable_timing" else [])
         L.fx_ctx_set_stream.argtypes = [C.c_void_p, C.c_void_p]
         L.fx_ctx_timing_filter.argtypes = [C.c_void_p, C.c_char_p]
+        L.fx_multi_destroy.argtypes = [C.c_void_p]
+        L.fx_multi_ctx.restype = C.c_void_p
         _lib = L
     return _lib
 
@@ -357,3 +359,54 @@ class Context:
                                   _p(hist, C.c_uint64), _p(edge, C.c_int32), C.c_size_t(cap_edge),
                                   C.byref(ne), _p(glcm, C.c_uint32), _p(pairs, C.c_uint64)))
         return hist, edge[: 2 * ne.value].reshape(-1, 2), glcm.reshape(A, ng, ng), pairs
+
+
+class Multi:
+    """fx_multi: one context and host thread per listed device.
+    A device may be listed more than once (several contexts share it)."""
+
+    def __init__(self, devices):
+        self.h = C.c_void_p()
+        arr = (C.c_int * len(devices))(*devices)
+        _check(lib().fx_multi_create(arr, len(devices), C.byref(self.h)))
+        self.devices = list(devices)
+
+    def close(self):
+        if self.h:
+            lib().fx_multi_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def featurize_batch(self, pairs, groups=("intensity",), params=None, cap_rois=None):
+        """Host (intensity, labels) pairs -> [(labels, table)] per image, identical to
+        Context.featurize_batch (fx_multi_featurize_batch)."""
+        params = params or resolve_profile("default")
+        mask = groups if isinstance(groups, int) else resolve_groups(list(groups))
+        ncols = len(feature_columns(mask, params))
+        keep, ims, cap = [], (FxImage * max(1, len(pairs)))(), 0
+        for i, (I, L) in enumerate(pairs):
+            I = np.ascontiguousarray(I, dtype=np.uint16)
+            L = np.ascontiguousarray(L, dtype=np.uint16)
+            if I.shape != L.shape:
+                raise FxError(3, "image/mask dimension mismatch")
+            keep.append((I, L))
+            h, w = L.shape
+            ims[i] = FxImage(I.ctypes.data, L.ctypes.data, w, h, w, 0, 0, MEM_HOST)
+            if cap_rois is None:
+                cap += int(np.count_nonzero(np.bincount(L.ravel(), minlength=65536)[1:]))
+        cap = cap if cap_rois is None else cap_rois
+        out_l = np.zeros(max(cap, 1), np.uint32)
+        out_v = np.zeros((max(cap, 1), max(ncols, 1)), np.float64)
+        offs = np.zeros(len(pairs) + 1, np.uint64)
+        _check(lib().fx_multi_featurize_batch(self.h, ims, C.c_int(len(pairs)), C.c_uint(mask),
+                                              C.byref(params), _p(out_l, C.c_uint32),
+                                              _p(out_v, C.c_double), C.c_size_t(cap),
+                                              _p(offs, C.c_size_t)))
+        offs = offs.astype(np.int64)
+        return [(out_l[offs[i]:offs[i + 1]], out_v[offs[i]:offs[i + 1], :ncols])
+                for i in range(len(pairs))]

@@ -199,3 +199,44 @@ def test_banded_host_path_c2_bitwise(ctx):
                                    hv.data_ptr(), n) == n
     assert torch.equal(hl, ol.cpu())
     assert torch.equal(hv, ov.cpu())
+
+
+# ---- several devices of one process (fx_multi): rows identical to one context --
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0]])
+def test_multi_batch_matches_single(ctx, devices):
+    """Chunks of 512 images dealt over the contexts (the same GPU listed several
+    times stands in for several devices: each context has its own streams, buffers
+    and host thread); output order and values identical to fx_featurize_batch."""
+    import paper_2603_12016_b200 as fx
+    p = fx.resolve_profile("default")
+    specs = [(48 + (k % 5) * 16, 40 + (k % 7) * 8, (k % 6)) for k in range(1300)]
+    pairs = _pairs(specs, seed=31)
+    ref = ctx.featurize_batch(pairs, GROUPS, p)
+    m = fx.Multi(devices)
+    try:
+        res = m.featurize_batch(pairs, GROUPS, p)
+    finally:
+        m.close()
+    assert len(res) == len(ref)
+    for (rl, rv), (ml, mv) in zip(ref, res):
+        assert np.array_equal(rl, ml)
+        assert np.array_equal(rv, mv)
+
+
+@pytest.mark.gpu
+def test_multi_batch_capacity_error(ctx):
+    import paper_2603_12016_b200 as fx
+    p = fx.resolve_profile("performance")
+    pairs = _pairs([(64, 64, 6)] * 700, seed=3)
+    m = fx.Multi([0, 0])
+    try:
+        with pytest.raises(fx.FxError) as e:
+            m.featurize_batch(pairs, GROUPS, p, cap_rois=10)
+        assert e.value.kind == "CapacityError"
+        # the contexts stay usable
+        res = m.featurize_batch(pairs[:50], GROUPS, p)
+        assert len(res) == 50
+    finally:
+        m.close()
