@@ -30,6 +30,17 @@ __global__ void k_label_scan(const uint16_t* L, int W, int H, size_t pitch, int 
                              LabelTable t);
 __global__ void k_compact_count(LabelTable t, Control* ctl, CompactArgs a, int nslots);
 __global__ void k_compact_emit(LabelTable t, Control* ctl, RoiList r, CompactArgs a, SlotMap m);
+__global__ void k_table_merge(TablePeers tp, uint32_t lmax, unsigned long long* out_cnt,
+                              uint32_t* out_bb, size_t out_pitch);
+__global__ void k_halo_gather(const HaloRect* rects, int n_rects, const uint16_t* const* srcL,
+                              const uint16_t* const* srcI, const size_t* src_pitch,
+                              const int* src_y0, uint16_t* dstL, uint16_t* dstI, size_t dst_pitch,
+                              int dst_y0);
+__global__ void k_band_count(RoiList rl, const Control* ctl, uint32_t band_rows, uint32_t nb,
+                             uint32_t* cnt, uint32_t* first);
+__global__ void k_band_scatter(RoiList rl, const Control* ctl, uint32_t band_rows, uint32_t nb,
+                               const uint32_t* cnt, uint32_t* cursor, uint32_t* seg,
+                               Control* band_ctl);
 cudaError_t roi_s_setup(int* occ /* [3][3]: class x GlcmMode */);
 void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap* tmaps, int tma40, int tma72,
                   DevImage img, RoiList rl, Control* ctl, FeatCfg cfg, double* out,
@@ -73,10 +84,19 @@ struct fx_ctx {
     cudaStream_t d2h = nullptr;   // banded host path: feature rows back while bands compute
     // banded host path (featurize_banded): per-band events and pinned host staging
     std::vector<cudaEvent_t> ev_band;  // 3 per band: labels in, intensities in, rows done
-    uint32_t* h_band = nullptr;        // pinned: per-band class lists (n_rois entries)
-    size_t h_band_cap = 0;
-    Control* h_band_ctl = nullptr;     // pinned: one control block per band
-    int h_band_ctl_cap = 0;
+    uint32_t* d_band = nullptr;        // [cnt kMaxBands*4][cursor kMaxBands*4][first kMaxBands]
+    uint32_t* h_band = nullptr;        // pinned mirror of d_band
+    Control* d_band_ctl = nullptr;     // one control block per band
+    Control* h_band_ctl = nullptr;     // pinned mirror (error flags)
+    uint32_t* d_band_seg = nullptr;    // band-major class lists [roi_cap]
+    size_t band_seg_cap = 0;
+    // whole slide over several devices (fx_multi_featurize_slide)
+    unsigned long long* d_mcnt = nullptr;  // merged table scratch (slot-0 layout)
+    uint32_t* d_mbb = nullptr;
+    uint8_t* d_slide = nullptr;            // halo rects + peer pointer arrays
+    size_t slide_bytes = 0;
+    uint16_t* d_work = nullptr;            // band + halo raster when the reserve is too small
+    size_t work_elems = 0;
     cudaEvent_t ev_compact = nullptr, ev_stats = nullptr;
     cudaEvent_t ev_staged[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
     // label table: tab_slots slices of 65536 entries, left reset by each compaction
@@ -595,17 +615,17 @@ const char* const kSName[3] = {"k_roi_s0", "k_roi_s1", "k_roi_s2"};
 // serial passes over the staged S ROIs, then the large-ROI kernel (L ROIs + S
 // overflow).
 int roi_work(fx_ctx* c, const DevImage& img, const FeatCfg& cfg, const Control& hc,
-             const TmaSet& tm, double* out_dev, const DebugOut* dbg_dev, int cls_first) {
+             const TmaSet& tm, double* out_dev, const DebugOut* dbg_dev, int cls_first,
+             Control* ctl, const RoiList& rl) {
     cudaStream_t s = c->stream;
     const int glcm = s_glcm_mode(cfg);
     for (int cls = cls_first; cls <= kClassS2; ++cls) {
         if (hc.class_count[cls] == 0) continue;
         Launch l(c, kSName[cls]);
         launch_roi_s(cls, c->sm_count * c->occ_s[cls][glcm], s, tm.m, tm.tma40, tm.tma72, img,
-                     roi_list(c), c->d_ctl, cfg, out_dev, dbg_dev);
+                     rl, ctl, cfg, out_dev, dbg_dev);
     }
     CK(cudaGetLastError());
-    RoiList rl = roi_list(c);
     const bool texture = cfg.col_glrlm >= 0 || cfg.col_glszm >= 0 || cfg.col_ngtdm >= 0;
     const uint64_t n_s_rois = (uint64_t)hc.class_count[kClassS0] + hc.class_count[kClassS1] +
                               hc.class_count[kClassS2];
@@ -635,7 +655,7 @@ int roi_work(fx_ctx* c, const DevImage& img, const FeatCfg& cfg, const Control& 
             const bool same = c->tlay_grid[which] >= (int)grid && T.bytes == c->tlay_prev[which].bytes &&
                               T.HC == c->tlay_prev[which].HC && T.hjk == c->tlay_prev[which].hjk;
             Launch l(c, which ? "k_roi_t_large" : "k_roi_t");
-            launch_roi_t((int)grid, s, img, rl, c->d_ctl, cfg, out_dev, c->d_tscratch[which], T,
+            launch_roi_t((int)grid, s, img, rl, ctl, cfg, out_dev, c->d_tscratch[which], T,
                          which, !same);
             if (!same) {
                 c->tlay_prev[which] = T;
@@ -651,11 +671,11 @@ int roi_work(fx_ctx* c, const DevImage& img, const FeatCfg& cfg, const Control& 
         if (cfg.int_vals || cfg.mom_px) {
             Launch l(c, "k_serial_stats");
             launch_serial_stats((int)n_s_rois, cfg.int_vals != nullptr, cfg.mom_px != nullptr, s, rl,
-                                c->d_ctl, cfg, out_dev);
+                                ctl, cfg, out_dev);
         }
         if (cfg.col_shape >= 0) {
             Launch l(c, "k_shape_serial");
-            launch_shape_serial((int)n_s_rois, s, rl, c->d_ctl, cfg, out_dev);
+            launch_shape_serial((int)n_s_rois, s, rl, ctl, cfg, out_dev);
         }
     }
     if (n_l == 0 && n_s_rois == 0) return FX_OK;
@@ -679,7 +699,7 @@ int roi_work(fx_ctx* c, const DevImage& img, const FeatCfg& cfg, const Control& 
             c->lay_grid = (int)grid;
         }
         Launch l(c, "k_roi_b");
-        launch_roi_b((int)grid, s, img, rl, c->d_ctl, cfg, out_dev, dbg_dev, c->d_lscratch, B);
+        launch_roi_b((int)grid, s, img, rl, ctl, cfg, out_dev, dbg_dev, c->d_lscratch, B);
     }
     CK(cudaGetLastError());
     return FX_OK;
@@ -740,7 +760,7 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         return set_error(FX_E_CAPACITY, "output capacity " + std::to_string(cap_rois) +
                                             " < " + std::to_string(hc.n_rois) + " ROIs");
     }
-    rc = roi_work(c, img, cfg, hc, tm, out_dev, dbg_dev, kClassS1);
+    rc = roi_work(c, img, cfg, hc, tm, out_dev, dbg_dev, kClassS1, c->d_ctl, roi_list(c));
     if (rc) return rc;
     CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
     return FX_OK;
@@ -892,20 +912,19 @@ int ensure_blab(fx_ctx* c, size_t n) {
 //     overlaps the remaining H2D (PCIe is full duplex).
 // Results are identical to the unbanded path: the same kernels on the same ROIs.
 
-int ensure_band_host(fx_ctx* c, size_t entries, int bands) {
-    if (entries > c->h_band_cap) {
-        if (c->h_band) cudaFreeHost(c->h_band);
-        c->h_band = nullptr;
-        c->h_band_cap = 0;
-        CK(cudaMallocHost(&c->h_band, std::max<size_t>(entries, 1) * sizeof(uint32_t)));
-        c->h_band_cap = entries;
+int ensure_band(fx_ctx* c, int bands) {
+    if (!c->d_band) {
+        CK(cudaMalloc(&c->d_band, (size_t)kMaxBands * (2 * kNumClasses + 1) * sizeof(uint32_t)));
+        CK(cudaMallocHost(&c->h_band, (size_t)kMaxBands * (2 * kNumClasses + 1) * sizeof(uint32_t)));
+        CK(cudaMalloc(&c->d_band_ctl, (size_t)kMaxBands * sizeof(Control)));
+        CK(cudaMallocHost(&c->h_band_ctl, (size_t)kMaxBands * sizeof(Control)));
     }
-    if (bands > c->h_band_ctl_cap) {
-        if (c->h_band_ctl) cudaFreeHost(c->h_band_ctl);
-        c->h_band_ctl = nullptr;
-        c->h_band_ctl_cap = 0;
-        CK(cudaMallocHost(&c->h_band_ctl, (size_t)bands * sizeof(Control)));
-        c->h_band_ctl_cap = bands;
+    if (c->roi_cap > c->band_seg_cap) {
+        cudaFree(c->d_band_seg);
+        c->d_band_seg = nullptr;
+        c->band_seg_cap = 0;
+        CK(cudaMalloc(&c->d_band_seg, c->roi_cap * sizeof(uint32_t)));
+        c->band_seg_cap = c->roi_cap;
     }
     while ((int)c->ev_band.size() < 3 * bands) {
         cudaEvent_t e;
@@ -923,13 +942,19 @@ int band_rows_for(const fx_ctx* c, int w, int h) {
     return std::max(256, (h / 8 + 63) / 64 * 64);                   // ~8 bands
 }
 
+int band_rows_clamped(int band_rows, int h) {  // at most kMaxBands bands
+    const int min_rows = ((h + kMaxBands - 1) / kMaxBands + 63) / 64 * 64;
+    return std::max(band_rows, min_rows);
+}
+
 int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned groups,
                      const fx_texture_params& p, uint32_t* out_labels, double* out_values,
                      size_t cap_rois, size_t* n_rois) {
     const int W = im->width, H = im->height;
+    band_rows = band_rows_clamped(band_rows, H);
     const int nb = (H + band_rows - 1) / band_rows;
     int rc = ensure_img(c, W, H);
-    if (!rc) rc = ensure_band_host(c, 0, nb);
+    if (!rc) rc = ensure_band(c, nb);
     if (rc) return rc;
     cudaStream_t s = c->stream;
     const size_t P = c->img_pitch, sp = (im->pitch ? im->pitch : (size_t)W) * 2;
@@ -972,8 +997,30 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     const int vrc = validate_texture(groups, p);
     rc = compact_stage(c, single_map(d), 0u, 0xffffffffu, cap_rois, true);
     if (rc) return rc;
+    // bucket the queued ROIs by band on the device (nothing queued when the ROIs
+    // exceed cap_rois); the host reads back the control block, the per-(band,
+    // class) counts and first ranks in one round trip, while the intensities keep
+    // arriving; no host-to-device copy competes with them
+    RoiList rl = roi_list(c);
+    uint32_t* cnt = c->d_band;
+    uint32_t* cursor = cnt + kMaxBands * kNumClasses;
+    uint32_t* first = cursor + kMaxBands * kNumClasses;
+    CK(cudaMemsetAsync(cnt, 0, 2 * kMaxBands * kNumClasses * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(first, 0xff, kMaxBands * sizeof(uint32_t), s));
+    {
+        const int grid = 2 * c->sm_count;
+        Launch l(c, "k_band_count");
+        k_band_count<<<grid, 256, 0, s>>>(rl, c->d_ctl, (uint32_t)band_rows, (uint32_t)nb, cnt, first);
+        Launch l2(c, "k_band_scatter");
+        k_band_scatter<<<grid, 256, 0, s>>>(rl, c->d_ctl, (uint32_t)band_rows, (uint32_t)nb, cnt, cursor,
+                                            c->d_band_seg, c->d_band_ctl);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->h_band, c->d_band, (size_t)kMaxBands * (2 * kNumClasses + 1) * sizeof(uint32_t),
+                       cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));  // the intensities keep arriving meanwhile
+    CK(cudaEventRecord(c->ev_stats, s));
+    CK(cudaStreamSynchronize(s));
     const Control hc = *c->h_ctl;
     const size_t n = hc.n_rois;
     *n_rois = n;
@@ -987,76 +1034,36 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
         CK(cudaStreamSynchronize(c->copy));
         return FX_OK;
     }
-    // ROI windows and class lists to the host; band of a ROI = band of its last row
-    RoiList rl = roi_list(c);
-    rc = ensure_band_host(c, n, nb);
-    if (rc) return rc;
-    std::vector<uint32_t> y0(n), hh(n), lists(n);
-    CK(cudaMemcpyAsync(y0.data(), rl.y0, n * 4, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(hh.data(), rl.h, n * 4, cudaMemcpyDeviceToHost, s));
-    size_t cls_off[kNumClasses + 1] = {0};
-    for (int k = 0; k < kNumClasses; ++k) {
-        cls_off[k + 1] = cls_off[k] + hc.class_count[k];
-        if (hc.class_count[k])
-            CK(cudaMemcpyAsync(lists.data() + cls_off[k], rl.cls_list[k],
-                               (size_t)hc.class_count[k] * 4, cudaMemcpyDeviceToHost, s));
-    }
-    CK(cudaEventRecord(c->ev_stats, s));
     if (out_labels) {
         CK(cudaStreamWaitEvent(c->d2h, c->ev_stats, 0));
         CK(cudaMemcpyAsync(out_labels, rl.label, n * 4, cudaMemcpyDeviceToHost, c->d2h));
     }
-    CK(cudaStreamSynchronize(s));
-    auto band_of = [&](uint32_t r) {
-        return std::min<int>(nb - 1, (int)((y0[r] + hh[r] - 1) / (uint32_t)band_rows));
-    };
-    // counting sort of every class list by band: h_band = [band][class] segments
-    std::vector<uint32_t> cnt((size_t)nb * kNumClasses, 0), first_rank(nb, (uint32_t)n);
-    for (int k = 0; k < kNumClasses; ++k)
-        for (size_t i = cls_off[k]; i < cls_off[k + 1]; ++i) {
-            const int b = band_of(lists[i]);
-            cnt[(size_t)b * kNumClasses + k]++;
-            first_rank[b] = std::min(first_rank[b], lists[i]);
-        }
-    std::vector<size_t> seg((size_t)nb * kNumClasses + 1, 0);
-    for (size_t i = 0; i < cnt.size(); ++i) seg[i + 1] = seg[i] + cnt[i];
-    {
-        std::vector<size_t> fill(seg.begin(), seg.end() - 1);
-        for (int k = 0; k < kNumClasses; ++k)
-            for (size_t i = cls_off[k]; i < cls_off[k + 1]; ++i)
-                c->h_band[fill[(size_t)band_of(lists[i]) * kNumClasses + k]++] = lists[i];
-    }
+    const uint32_t* h_cnt = c->h_band;
+    const uint32_t* h_first = c->h_band + 2 * kMaxBands * kNumClasses;
     // rows final after band b: every rank below the first rank of any later band
     std::vector<uint32_t> final_after(nb);
     uint32_t later = (uint32_t)n;
     for (int b = nb - 1; b >= 0; --b) {
         final_after[b] = later;
-        later = std::min(later, first_rank[b]);
+        later = std::min(later, h_first[b]);
     }
     const size_t ncols = (size_t)cfg.ncols;
     TmaSet tm;
     make_tmaps(c, d, &tm);
-    size_t rows_out = 0;
+    size_t rows_out = 0, seg_at = 0;
     for (int b = 0; b < nb; ++b) {
-        Control& bc = c->h_band_ctl[b];
-        bc = hc;
+        Control bc = hc;  // host copy of the band's counts (launch decisions)
+        RoiList rb = rl;  // the band's lists: segments of d_band_seg
         uint64_t band_rois = 0;
         for (int k = 0; k < kNumClasses; ++k) {
-            const size_t a = seg[(size_t)b * kNumClasses + k];
-            bc.class_count[k] = cnt[(size_t)b * kNumClasses + k];
-            bc.class_next[k] = 0;
+            bc.class_count[k] = h_cnt[b * kNumClasses + k];
+            rb.cls_list[k] = c->d_band_seg + seg_at;
+            seg_at += bc.class_count[k];
             band_rois += bc.class_count[k];
-            if (bc.class_count[k])
-                CK(cudaMemcpyAsync(rl.cls_list[k], c->h_band + a, (size_t)bc.class_count[k] * 4,
-                                   cudaMemcpyHostToDevice, s));
         }
-        bc.overflow_count = bc.overflow_next = 0;
-        bc.t_next[0] = bc.t_next[1] = 0;
-        bc.mom_alloc = bc.int_alloc = 0;
         CK(cudaStreamWaitEvent(s, ev[nb + b], 0));
         if (band_rois) {
-            CK(cudaMemcpyAsync(c->d_ctl, &bc, offsetof(Control, error), cudaMemcpyHostToDevice, s));
-            rc = roi_work(c, d, cfg, bc, tm, c->d_out, nullptr, kClassS0);
+            rc = roi_work(c, d, cfg, bc, tm, c->d_out, nullptr, kClassS0, c->d_band_ctl + b, rb);
             if (rc) return rc;
         }
         const size_t upto = std::max<size_t>(rows_out, b == nb - 1 ? n : final_after[b]);
@@ -1069,7 +1076,12 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
             rows_out = upto;
         }
     }
+    // the bands' error flags into the call's control block
+    CK(cudaMemcpyAsync(c->h_band_ctl, c->d_band_ctl, (size_t)nb * sizeof(Control),
+                       cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int b = 0; b < nb; ++b) c->h_ctl->error |= c->h_band_ctl[b].error;
     CK(cudaStreamSynchronize(c->d2h));
     return FX_OK;
 }
@@ -1256,6 +1268,177 @@ int ictx_batch_device(fx_ctx* c, const fx_image* ims, int n, unsigned groups,
                       size_t cap_rows, size_t* row_offsets) {
     return batch_core(c, ims, n, groups, p, out_dev, lab_dev, cap_rows, row_offsets, nullptr);
 }
+// ---- whole slide over several devices: one row band per context ---------------
+// (driven by fx_multi_featurize_slide, fx_multi.cu; every step is enqueued on the
+// context's stream, the order across devices is kept by events)
+
+// H2D of rows [y0, y1) of the host slide into this context's raster (with
+// `reserve` spare rows below for the halo), then the label scan of the band into
+// a fresh table (global rows).  *lmax: the band's largest label.
+int islide_load_scan(fx_ctx* c, const fx_image* im, int y0, int y1, int reserve,
+                     cudaEvent_t loaded, cudaEvent_t scanned, uint32_t* lmax) {
+    CK(cudaSetDevice(c->device));
+    const int rows = y1 - y0, W = im->width;
+    int rc = ensure_img(c, W, rows + reserve);
+    if (rc) return rc;
+    cudaStream_t s = c->stream;
+    const size_t P = c->img_pitch, sp = (im->pitch ? im->pitch : (size_t)W) * 2;
+    uint16_t* dI = c->d_img;
+    uint16_t* dL = c->d_img + P * c->img_rows_cap;
+    CK(cudaMemcpy2DAsync(dL, P * 2, im->labels + (size_t)y0 * (sp / 2), sp, (size_t)W * 2, rows,
+                         cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpy2DAsync(dI, P * 2, im->intensity + (size_t)y0 * (sp / 2), sp, (size_t)W * 2, rows,
+                         cudaMemcpyHostToDevice, s));
+    CK(cudaEventRecord(loaded, s));
+    DevImage band{dI, dL, W, rows, P, im->origin_x, im->origin_y + y0};
+    rc = scan_stage(c, band, single_map(band), true);
+    if (rc) return rc;
+    CK(cudaEventRecord(scanned, s));
+    CK(cudaMemcpyAsync(c->h_slot_base, c->d_maxlab, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *lmax = c->h_slot_base[0];
+    return FX_OK;
+}
+
+// this context's band raster and label table, for its peers
+void islide_band(fx_ctx* c, const uint16_t** L, const uint16_t** I, size_t* pitch,
+                 const unsigned long long** cnt, const uint32_t** bb, size_t* bb_pitch) {
+    *I = c->d_img;
+    *L = c->d_img + c->img_pitch * c->img_rows_cap;
+    *pitch = c->img_pitch;
+    *cnt = c->d_cnt;
+    *bb = c->d_bb;
+    *bb_pitch = (size_t)c->tab_slots * kMaxLabels;
+}
+
+// the table of labels [0, lmax] merged from every band's table (peer reads, after
+// every band's scan) into this context's scratch
+int islide_merge(fx_ctx* c, const TablePeers& tp, uint32_t lmax, const cudaEvent_t* scanned,
+                 cudaEvent_t merged) {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    if (!c->d_mcnt) {
+        CK(cudaMalloc(&c->d_mcnt, (size_t)kMaxLabels * sizeof(unsigned long long)));
+        CK(cudaMalloc(&c->d_mbb, 4 * (size_t)kMaxLabels * sizeof(uint32_t)));
+    }
+    for (int e = 0; e < tp.n; ++e) CK(cudaStreamWaitEvent(s, scanned[e], 0));
+    {
+        Launch l(c, "k_table_merge");
+        const int grid = std::max(1, std::min<int>((int)(lmax / 256) + 1, 4 * c->sm_count));
+        k_table_merge<<<grid, 256, 0, s>>>(tp, lmax, c->d_mcnt, c->d_mbb, kMaxLabels);
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(merged, s));
+    return FX_OK;
+}
+
+// after every context merged (its peers stop reading this table): the merged
+// table becomes this context's table, and is read back (host cnt [lmax+1],
+// bbox [4][lmax+1]) for the ownership and halo plan
+int islide_commit(fx_ctx* c, uint32_t lmax, const cudaEvent_t* merged, int n_peers,
+                  uint64_t* h_cnt, uint32_t* h_bb) {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    for (int e = 0; e < n_peers; ++e) CK(cudaStreamWaitEvent(s, merged[e], 0));
+    const size_t n = (size_t)lmax + 1, bp = (size_t)c->tab_slots * kMaxLabels;
+    CK(cudaMemcpyAsync(c->d_cnt, c->d_mcnt, n * sizeof(unsigned long long), cudaMemcpyDeviceToDevice, s));
+    CK(cudaMemcpy2DAsync(c->d_bb, bp * 4, c->d_mbb, (size_t)kMaxLabels * 4, n * 4, 4,
+                         cudaMemcpyDeviceToDevice, s));
+    c->h_slot_base[0] = lmax;  // the compaction walks labels up to the table's max label
+    CK(cudaMemcpyAsync(c->d_maxlab, c->h_slot_base, sizeof(uint32_t), cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(h_cnt, c->d_mcnt, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpy2DAsync(h_bb, n * 4, c->d_mbb, (size_t)kMaxLabels * 4, n * 4, 4,
+                         cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    c->table_clean = false;
+    return FX_OK;
+}
+
+// Halo of the owned straddling windows: `need` rows below the band with zeroed
+// labels, the windows' rectangles gathered from the peers' band rasters (peer
+// reads after their loads), then the owned ROIs featurized on band + halo.  Rows
+// (labels ascending) and labels are read back into host buffers.
+int islide_featurize(fx_ctx* c, const fx_image* im, int y0, int y1, int need,
+                     const std::vector<HaloRect>& rects, const std::vector<const uint16_t*>& pL,
+                     const std::vector<const uint16_t*>& pI, const std::vector<size_t>& pp,
+                     const std::vector<int>& py0, const cudaEvent_t* loaded, unsigned groups,
+                     const fx_texture_params& p, size_t cap, uint32_t* h_labels, double* h_values,
+                     size_t* n_rois) {
+    CK(cudaSetDevice(c->device));
+    cudaStream_t s = c->stream;
+    const int W = im->width, rows = y1 - y0, total = rows + need;
+    const size_t P = c->img_pitch;
+    uint16_t* bandI = c->d_img;
+    uint16_t* bandL = c->d_img + P * c->img_rows_cap;
+    uint16_t *wI = bandI, *wL = bandL;
+    if ((size_t)total > c->img_rows_cap) {
+        // too few reserve rows: a separate band + halo raster (the band buffer stays
+        // in place: the peers may be reading it)
+        const size_t elems = P * (size_t)total * 2;
+        if (elems > c->work_elems) {
+            cudaStreamSynchronize(s);
+            cudaFree(c->d_work);
+            c->d_work = nullptr;
+            c->work_elems = 0;
+            CK(cudaMalloc(&c->d_work, elems * sizeof(uint16_t)));
+            c->work_elems = elems;
+        }
+        wI = c->d_work;
+        wL = c->d_work + P * (size_t)total;
+        CK(cudaMemcpy2DAsync(wI, P * 2, bandI, P * 2, (size_t)W * 2, rows, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpy2DAsync(wL, P * 2, bandL, P * 2, (size_t)W * 2, rows, cudaMemcpyDeviceToDevice, s));
+    }
+    if (need > 0) {
+        CK(cudaMemset2DAsync(wL + (size_t)rows * P, P * 2, 0, (size_t)W * 2, need, s));
+        const int nr = (int)rects.size(), np = (int)pL.size();
+        std::vector<uint8_t> h;
+        auto put = [&](const void* src, size_t n) {
+            const size_t at = (h.size() + 15) / 16 * 16;
+            h.resize(at + n);
+            std::memcpy(h.data() + at, src, n);
+            return at;
+        };
+        const size_t oR = put(rects.data(), nr * sizeof(HaloRect));
+        const size_t oL = put(pL.data(), np * sizeof(void*)), oI = put(pI.data(), np * sizeof(void*));
+        const size_t oP = put(pp.data(), np * sizeof(size_t)), oY = put(py0.data(), np * sizeof(int));
+        if (h.size() > c->slide_bytes) {
+            cudaStreamSynchronize(s);
+            cudaFree(c->d_slide);
+            c->d_slide = nullptr;
+            c->slide_bytes = 0;
+            CK(cudaMalloc(&c->d_slide, h.size()));
+            c->slide_bytes = h.size();
+        }
+        CK(cudaMemcpyAsync(c->d_slide, h.data(), h.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // h is a pageable local
+        for (int e = 0; e < np; ++e) CK(cudaStreamWaitEvent(s, loaded[e], 0));
+        if (nr) {
+            const uint8_t* b = c->d_slide;
+            Launch l(c, "k_halo_gather");
+            k_halo_gather<<<dim3(64, std::min(nr, 1024)), 256, 0, s>>>(
+                (const HaloRect*)(b + oR), nr, (const uint16_t* const*)(b + oL),
+                (const uint16_t* const*)(b + oI), (const size_t*)(b + oP), (const int*)(b + oY), wL, wI,
+                P, y0);
+        }
+        CK(cudaGetLastError());
+    }
+    const FeatCfg cfg = make_cfg(groups, p);
+    int rc = ensure_out(c, std::max<size_t>(1, cap) * (size_t)cfg.ncols);
+    if (rc) return rc;
+    DevImage d{wI, wL, W, total, P, im->origin_x, im->origin_y + y0};
+    rc = featurize_stage(c, d, single_map(d), (uint32_t)(im->origin_y + y0),
+                         (uint32_t)(im->origin_y + y1), groups, p, c->d_out, cap, n_rois, nullptr);
+    if (rc) {
+        cudaStreamSynchronize(s);
+        return rc;
+    }
+    if (*n_rois) {
+        CK(cudaMemcpyAsync(h_values, c->d_out, *n_rois * cfg.ncols * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(h_labels, roi_list(c).label, *n_rois * sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+    }
+    return finish(c);
+}
+
 cudaStream_t ictx_stream(fx_ctx* c) { return c->stream; }
 cudaStream_t ictx_d2h(fx_ctx* c) { return c->d2h; }
 int ictx_device(const fx_ctx* c) { return c->device; }
@@ -1383,6 +1566,13 @@ int fx_ctx_destroy(fx_ctx* c) {
     if (c->copy) cudaStreamDestroy(c->copy);
     if (c->d2h) cudaStreamDestroy(c->d2h);
     for (cudaEvent_t e : c->ev_band) cudaEventDestroy(e);
+    cudaFree(c->d_band);
+    cudaFree(c->d_band_ctl);
+    cudaFree(c->d_band_seg);
+    cudaFree(c->d_mcnt);
+    cudaFree(c->d_mbb);
+    cudaFree(c->d_slide);
+    cudaFree(c->d_work);
     if (c->h_band) cudaFreeHost(c->h_band);
     if (c->h_band_ctl) cudaFreeHost(c->h_band_ctl);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);

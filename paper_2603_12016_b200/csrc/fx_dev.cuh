@@ -102,6 +102,22 @@ struct Control {
     uint32_t pad_;
 };
 
+// whole slide over several devices: the label tables of the bands (peer pointers)
+constexpr int kMaxPeers = 16;
+struct TablePeers {
+    const unsigned long long* cnt[kMaxPeers];
+    const uint32_t* bb[kMaxPeers];  // xmin | ymin | xmax | ymax rows, pitch[e] apart
+    size_t pitch[kMaxPeers];
+    int n;
+};
+// one rectangle of a straddling window to fetch from band src
+struct HaloRect {
+    int src, y_lo, y_hi, x_lo, x_hi;
+};
+
+// banded host path: at most this many row bands per call
+constexpr int kMaxBands = 64;
+
 // compaction scratch: per (slot, 1024-label block) counts and exclusive bases
 constexpr int kBlocksPerSlot = kMaxLabels / 1024;
 constexpr uint32_t kBlockLive = 0x80000000u;  // block_sum flag: block <= maxlab

@@ -380,4 +380,139 @@ __global__ void __launch_bounds__(1024) k_compact_emit(LabelTable t, Control* ct
     }
 }
 
+
+// --- banded host path (fx_capi.cu featurize_banded) --------------------------
+//
+// After the one compaction of a banded call, every queued ROI is bucketed by the
+// band holding its window's last row (its pixels are all on the device once that
+// band's intensities have arrived): per (band, class) counts and the smallest
+// rank per band, then the band-major lists and one control block per band, so the
+// host issues the per-band kernels without copying anything to the device.
+
+__device__ __forceinline__ bool band_item(const RoiList& rl, const Control* ctl, uint32_t i,
+                                          uint32_t band_rows, uint32_t nb, uint32_t& r, uint32_t& b,
+                                          uint32_t& k) {
+    uint32_t base = 0;
+    for (k = 0; k < (uint32_t)kNumClasses; ++k) {
+        const uint32_t n = ctl->class_count[k];
+        if (i < base + n) break;
+        base += n;
+    }
+    if (k == (uint32_t)kNumClasses) return false;
+    const uint32_t* lst = k == kClassS0 ? rl.cls_list[kClassS0]
+                          : k == kClassS1 ? rl.cls_list[kClassS1]
+                          : k == kClassS2 ? rl.cls_list[kClassS2] : rl.cls_list[kClassL];
+    r = lst[i - base];
+    b = min(nb - 1, (rl.y0[r] + rl.h[r] - 1) / band_rows);
+    return true;
+}
+
+__global__ void k_band_count(RoiList rl, const Control* ctl, uint32_t band_rows, uint32_t nb,
+                             uint32_t* cnt, uint32_t* first) {
+    const uint32_t total = ctl->class_count[0] + ctl->class_count[1] + ctl->class_count[2] +
+                           ctl->class_count[3];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        uint32_t r, b, k;
+        if (!band_item(rl, ctl, i, band_rows, nb, r, b, k)) continue;
+        atomicAdd(&cnt[b * kNumClasses + k], 1u);
+        atomicMin(&first[b], r);
+    }
+}
+
+__global__ void k_band_scatter(RoiList rl, const Control* ctl, uint32_t band_rows, uint32_t nb,
+                               const uint32_t* cnt, uint32_t* cursor, uint32_t* seg,
+                               Control* band_ctl) {
+    __shared__ uint32_t off[kMaxBands * kNumClasses];
+    if (threadIdx.x == 0) {  // band-major, class-minor exclusive offsets (<= 256 entries)
+        uint32_t acc = 0;
+        for (uint32_t j = 0; j < nb * kNumClasses; ++j) {
+            off[j] = acc;
+            acc += cnt[j];
+        }
+    }
+    __syncthreads();
+    const uint32_t total = ctl->class_count[0] + ctl->class_count[1] + ctl->class_count[2] +
+                           ctl->class_count[3];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        uint32_t r, b, k;
+        if (!band_item(rl, ctl, i, band_rows, nb, r, b, k)) continue;
+        const uint32_t j = b * kNumClasses + k;
+        seg[off[j] + atomicAdd(&cursor[j], 1u)] = r;
+    }
+    if (blockIdx.x == 0 && threadIdx.x < nb) {  // control block of each band
+        Control c = *ctl;
+        const uint32_t b = threadIdx.x;
+        for (int k = 0; k < kNumClasses; ++k) {
+            c.class_count[k] = cnt[b * kNumClasses + k];
+            c.class_next[k] = 0;
+        }
+        c.overflow_count = c.overflow_next = 0;
+        c.t_next[0] = c.t_next[1] = 0;
+        c.mom_alloc = c.int_alloc = 0;
+        c.error = 0;
+        band_ctl[b] = c;
+    }
+}
+
+
+// --- whole slide over several devices (fx_multi_featurize_slide) ---------------
+//
+// Each device scans its own row band into its own label table.  The tables are
+// merged by peer reads over NVLink (a device listed twice reads its own memory):
+// every device sums the counts and takes the min / max of the boxes of all bands
+// for labels [0, lmax] into a scratch table (the peers' tables are only read, so
+// no device sees a half-merged table), then commits it.  Integer sums and min /
+// max are order-free, so every device ends with the table a whole-slide scan
+// would give, bit for bit.
+
+__global__ void k_table_merge(TablePeers tp, uint32_t lmax, unsigned long long* out_cnt,
+                              uint32_t* out_bb, size_t out_pitch) {
+    for (uint32_t l = blockIdx.x * blockDim.x + threadIdx.x; l <= lmax; l += gridDim.x * blockDim.x) {
+        unsigned long long c = 0;
+        uint32_t x0 = 0xffffffffu, y0 = 0xffffffffu, x1 = 0u, y1 = 0u;
+        for (int e = 0; e < tp.n; ++e) {
+            const unsigned long long ce = tp.cnt[e][l];
+            if (!ce) continue;
+            c += ce;
+            const uint32_t* b = tp.bb[e];
+            const size_t pp = tp.pitch[e];
+            x0 = min(x0, b[l]);
+            y0 = min(y0, b[pp + l]);
+            x1 = max(x1, b[2 * pp + l]);
+            y1 = max(y1, b[3 * pp + l]);
+        }
+        out_cnt[l] = c;
+        out_bb[l] = x0;
+        out_bb[out_pitch + l] = y0;
+        out_bb[2 * out_pitch + l] = x1;
+        out_bb[3 * out_pitch + l] = y1;
+    }
+}
+
+// Straddling windows: rectangle k covers slide rows [y_lo, y_hi) and columns
+// [x_lo, x_hi) of the owner's window below its band; the rows come from the band
+// of device src (peer pointers), into the owner's raster at row (y - y_own).
+// One block per (rectangle, row chunk), 16 B copies where the columns allow.
+__global__ void k_halo_gather(const HaloRect* rects, int n_rects, const uint16_t* const* srcL,
+                              const uint16_t* const* srcI, const size_t* src_pitch,
+                              const int* src_y0, uint16_t* dstL, uint16_t* dstI, size_t dst_pitch,
+                              int dst_y0) {
+    for (int k = blockIdx.y; k < n_rects; k += gridDim.y) {
+        const HaloRect r = rects[k];
+        const uint16_t* sL = srcL[r.src];
+        const uint16_t* sI = srcI[r.src];
+        const size_t sp = src_pitch[r.src];
+        const int sy0 = src_y0[r.src];
+        const int w = r.x_hi - r.x_lo;
+        for (int y = r.y_lo + blockIdx.x; y < r.y_hi; y += gridDim.x) {
+            const size_t so = (size_t)(y - sy0) * sp + r.x_lo;
+            const size_t dof = (size_t)(y - dst_y0) * dst_pitch + r.x_lo;
+            for (int x = threadIdx.x; x < w; x += blockDim.x) {
+                dstL[dof + x] = sL[so + x];
+                dstI[dof + x] = sI[so + x];
+            }
+        }
+    }
+}
+
 }  // namespace fxg
