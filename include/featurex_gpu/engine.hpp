@@ -20,6 +20,7 @@
 #include <filesystem>
 #include <limits>
 #include <optional>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -34,6 +35,13 @@ struct SpillIoError : std::runtime_error { using std::runtime_error::runtime_err
 struct ZeroMassError : std::runtime_error { using std::runtime_error::runtime_error; };
 struct UnknownProfile : std::runtime_error { using std::runtime_error::runtime_error; };
 struct ConfigError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ShapeError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct PackingError : std::runtime_error { using std::runtime_error::runtime_error; };
+// the tuner's errors (out of scope here, declared so callers compile unchanged)
+struct ClassCountError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct GridError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct InsufficientClassItems : std::runtime_error { using std::runtime_error::runtime_error; };
+struct NoFeasiblePoint : std::runtime_error { using std::runtime_error::runtime_error; };
 // device-side failures (no reference counterpart)
 struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
 
@@ -53,6 +61,20 @@ struct LabelMask {  // image.hpp:20-27
     uint16_t at(int x, int y) const { return labels[static_cast<size_t>(y) * width + x]; }
 };
 
+// Read-only view of a horizontal band of a matched image/mask pair (image.hpp:30-37)
+struct RowTile {
+    int y0 = 0;
+    int rows = 0;
+    int width = 0;
+    std::span<const uint16_t> intensity;  // rows*width values
+    std::span<const uint16_t> labels;
+};
+
+// Contiguous tiles of at most rows_per_tile rows; PairingError on a dimension
+// mismatch or rows_per_tile < 1 (image.hpp:41-42, image.cpp:7-26).
+std::vector<RowTile> iter_row_tiles(const IntensityImage& image, const LabelMask& mask,
+                                    int rows_per_tile = 256);
+
 struct Pixel {  // roi.hpp:13-17
     uint32_t x = 0;
     uint32_t y = 0;
@@ -70,6 +92,42 @@ struct PixelCloud {  // roi.hpp:28-34
     std::vector<Pixel> pixels;
     BoundingBox bbox;
     size_t count() const { return pixels.size(); }
+};
+
+struct MemoryBudget {  // roi.hpp:36-39 (accepted; clouds are built on the device, no spill)
+    size_t max_resident_bytes = std::numeric_limits<size_t>::max();
+    std::filesystem::path spill_dir;
+};
+
+// Per-label pixel clouds of one image (roi.hpp:45-88).  accumulate() runs the
+// label scan and the cloud gather on the GPU (fx_roi_clouds): labels ascending,
+// each cloud in mask scan order with its tight inclusive bbox -- the reference's
+// contents.  The clouds then live in host memory; nothing is spilled, so
+// peak_resident_bytes() is the total and cleanup() has nothing to remove.
+class RoiRegistry {
+public:
+    RoiRegistry() = default;
+    RoiRegistry(RoiRegistry&&) = default;
+    RoiRegistry& operator=(RoiRegistry&&) = default;
+    RoiRegistry(const RoiRegistry&) = delete;
+    RoiRegistry& operator=(const RoiRegistry&) = delete;
+    ~RoiRegistry() = default;
+
+    static RoiRegistry accumulate(const std::vector<RowTile>& tiles, const MemoryBudget& budget);
+
+    std::vector<uint32_t> labels() const { return labels_; }  // ascending
+    size_t roi_count() const { return labels_.size(); }
+    bool contains(uint32_t label) const;
+    // std::out_of_range for an unknown label (roi.cpp:124); safe for concurrent readers
+    PixelCloud cloud(uint32_t label) const;
+    size_t peak_resident_bytes() const { return pixels_.size() * sizeof(Pixel); }
+    void cleanup() {}
+
+private:
+    std::vector<uint32_t> labels_;
+    std::vector<uint64_t> offsets_;     // [roi_count + 1] into pixels_
+    std::vector<BoundingBox> bboxes_;
+    std::vector<Pixel> pixels_;
 };
 
 struct GlcmParams {  // texture.hpp:30-35

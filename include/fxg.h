@@ -225,6 +225,15 @@ int fx_featurize_owned(fx_ctx* ctx, const fx_image* image, int own_y0, int own_y
 int fx_roi_table(fx_ctx* ctx, const fx_image* image, uint32_t* out_labels, uint64_t* out_count,
                  uint32_t* out_bbox, size_t cap, size_t* n_rois);
 
+/* RoiRegistry::accumulate + cloud (roi.cpp:76-148) on the device: every ROI's
+ * pixel cloud, clouds in label order (ascending), each in mask scan order, (x, y)
+ * with the image origin added.  offsets[n_rois + 1] index xs / ys / vs; bbox
+ * [n_rois][4] = x_min, y_min, x_max, y_max.  With any output pointer NULL only
+ * *n_rois / *n_px are returned (size query); FX_E_CAPACITY if a buffer is short. */
+int fx_roi_clouds(fx_ctx* ctx, const fx_image* image, uint32_t* out_labels, uint64_t* offsets,
+                  uint32_t* bbox, size_t cap_rois, uint32_t* xs, uint32_t* ys, uint16_t* vs,
+                  size_t cap_px, size_t* n_rois, size_t* n_px);
+
 /* Introspection of one ROI's integer intermediates, for the bit-exact tests:
  *  hist      : intensity histogram counts over max(2,bins) bins
  *              (intensity_features.cpp:156-167)                 [nb]
@@ -254,6 +263,16 @@ fx_ctx* fx_multi_ctx(fx_multi* m, int i);
 int fx_multi_featurize_batch(fx_multi* m, const fx_image* images, int n, unsigned groups,
                              const fx_texture_params* params, uint32_t* out_labels,
                              double* out_values, size_t cap_rois, size_t* row_offsets);
+/* C5 across devices: one host image in row bands, one band per device.  Each
+ * device scans its band; the label tables are merged by peer reads (NVLink);
+ * a ROI belongs to the band of its first row, and an owner gathers only its
+ * straddling windows' rectangles from the other bands (peer reads) before
+ * featurizing its ROIs.  Output identical to fx_featurize on the whole image
+ * (labels ascending).  Replaces the per-pair body of run() (engine.cpp:300-336)
+ * for one image too large for one device's pass. */
+int fx_multi_featurize_slide(fx_multi* m, const fx_image* image, unsigned groups,
+                             const fx_texture_params* params, uint32_t* out_labels,
+                             double* out_values, size_t cap_rois, size_t* n_rois);
 
 /* Per-phase clock totals of the S-class ROI kernels (summed over ROIs, lane 0's
  * clock64 deltas): 0 load+gather, 1 intensity sort, 2 intensity statistics,

@@ -516,6 +516,86 @@ std::vector<std::vector<double>> compute_roi_features_batch(const std::vector<Pi
     return out;
 }
 
+std::vector<RowTile> iter_row_tiles(const IntensityImage& image, const LabelMask& mask,
+                                    int rows_per_tile) {
+    if (image.width != mask.width || image.height != mask.height)
+        throw PairingError("image/mask dimension mismatch");
+    if (rows_per_tile < 1) throw PairingError("rows_per_tile must be >= 1");
+    std::vector<RowTile> tiles;
+    const size_t w = static_cast<size_t>(image.width);
+    for (int y = 0; y < image.height; y += rows_per_tile) {
+        const int rows = std::min(rows_per_tile, image.height - y);
+        const size_t at = static_cast<size_t>(y) * w, len = static_cast<size_t>(rows) * w;
+        tiles.push_back(RowTile{y, rows, image.width,
+                                std::span<const uint16_t>(image.pixels.data() + at, len),
+                                std::span<const uint16_t>(mask.labels.data() + at, len)});
+    }
+    return tiles;
+}
+
+RoiRegistry RoiRegistry::accumulate(const std::vector<RowTile>& tiles, const MemoryBudget&) {
+    RoiRegistry reg;
+    if (tiles.empty()) return reg;
+    // the tiles' rows as one raster: in place when they are consecutive views of
+    // one image (iter_row_tiles), else gathered into a contiguous copy
+    const int W = tiles.front().width;
+    int H = 0;
+    bool contiguous = true;
+    for (size_t k = 0; k < tiles.size(); ++k) {
+        const RowTile& t = tiles[k];
+        if (t.width != W) throw PairingError("tiles of different widths");
+        if (t.y0 != H) throw PairingError("tiles are not consecutive row bands");
+        if (k && (t.labels.data() != tiles[k - 1].labels.data() + tiles[k - 1].labels.size() ||
+                  t.intensity.data() != tiles[k - 1].intensity.data() + tiles[k - 1].intensity.size()))
+            contiguous = false;
+        H += t.rows;
+    }
+    if (H == 0 || W == 0) return reg;
+    std::vector<uint16_t> I, L;
+    const uint16_t *pi = tiles.front().intensity.data(), *pl = tiles.front().labels.data();
+    if (!contiguous) {
+        for (const RowTile& t : tiles) {
+            I.insert(I.end(), t.intensity.begin(), t.intensity.end());
+            L.insert(L.end(), t.labels.begin(), t.labels.end());
+        }
+        pi = I.data();
+        pl = L.data();
+    }
+    fx_image im{pi, pl, W, H, static_cast<size_t>(W), 0, 0, FX_MEM_HOST};
+    fx_ctx* c = context(0);
+    size_t nr = 0, np = 0;
+    check(fx_roi_clouds(c, &im, nullptr, nullptr, nullptr, 0, nullptr, nullptr, nullptr, 0, &nr, &np));
+    std::vector<uint32_t> xs(std::max<size_t>(np, 1)), ys(std::max<size_t>(np, 1)), bb(4 * std::max<size_t>(nr, 1));
+    std::vector<uint16_t> vs(std::max<size_t>(np, 1));
+    reg.labels_.resize(std::max<size_t>(nr, 1));
+    reg.offsets_.resize(nr + 1);
+    check(fx_roi_clouds(c, &im, reg.labels_.data(), reg.offsets_.data(), bb.data(), nr, xs.data(), ys.data(),
+                        vs.data(), np, &nr, &np));
+    reg.labels_.resize(nr);
+    reg.bboxes_.resize(nr);
+    for (size_t i = 0; i < nr; ++i) reg.bboxes_[i] = BoundingBox{bb[4 * i], bb[4 * i + 1], bb[4 * i + 2], bb[4 * i + 3]};
+    reg.pixels_.resize(np);
+    for (size_t k = 0; k < np; ++k) reg.pixels_[k] = Pixel{xs[k], ys[k], vs[k]};
+    return reg;
+}
+
+bool RoiRegistry::contains(uint32_t label) const {
+    return std::binary_search(labels_.begin(), labels_.end(), label);
+}
+
+PixelCloud RoiRegistry::cloud(uint32_t label) const {
+    const auto it = std::lower_bound(labels_.begin(), labels_.end(), label);
+    if (it == labels_.end() || *it != label)
+        throw std::out_of_range("unknown ROI label " + std::to_string(label));
+    const size_t i = static_cast<size_t>(it - labels_.begin());
+    PixelCloud c;
+    c.label = label;
+    c.bbox = bboxes_[i];
+    c.pixels.assign(pixels_.begin() + static_cast<std::ptrdiff_t>(offsets_[i]),
+                    pixels_.begin() + static_cast<std::ptrdiff_t>(offsets_[i + 1]));
+    return c;
+}
+
 FeatureTable featurize(const IntensityImage& image, const LabelMask& mask,
                        const std::vector<std::string>& groups, const TextureParams& params,
                        int device) {

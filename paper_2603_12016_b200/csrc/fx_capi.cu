@@ -36,6 +36,9 @@ __global__ void k_halo_gather(const HaloRect* rects, int n_rects, const uint16_t
                               const uint16_t* const* srcI, const size_t* src_pitch,
                               const int* src_y0, uint16_t* dstL, uint16_t* dstI, size_t dst_pitch,
                               int dst_y0);
+__global__ void k_cloud_gather(DevImage img, RoiList rl, const Control* ctl,
+                               const unsigned long long* offsets, uint32_t* xs, uint32_t* ys,
+                               uint16_t* vs);
 __global__ void k_band_count(RoiList rl, const Control* ctl, uint32_t band_rows, uint32_t nb,
                              uint32_t* cnt, uint32_t* first);
 __global__ void k_band_scatter(RoiList rl, const Control* ctl, uint32_t band_rows, uint32_t nb,
@@ -1961,6 +1964,75 @@ int fx_roi_table(fx_ctx* c, const fx_image* im, uint32_t* out_labels, uint64_t* 
         out_bbox[4 * i + 1] = (uint32_t)y0[i];
         out_bbox[4 * i + 2] = (uint32_t)x0[i] + w[i] - 1;
         out_bbox[4 * i + 3] = (uint32_t)y0[i] + h[i] - 1;
+    }
+    return finish(c);
+}
+
+int fx_roi_clouds(fx_ctx* c, const fx_image* im, uint32_t* out_labels, uint64_t* out_offsets,
+                  uint32_t* out_bbox, size_t cap_rois, uint32_t* xs, uint32_t* ys, uint16_t* vs,
+                  size_t cap_px, size_t* n_rois, size_t* n_px) {
+    if (!c || !im || !n_rois || !n_px) return set_error(FX_E_ARG, "null argument");
+    if (!im->intensity || !im->labels) return set_error(FX_E_ARG, "null raster");
+    if (im->width < 1 || im->height < 1) return set_error(FX_E_PAIRING, "empty raster");
+    *n_rois = *n_px = 0;
+    CK(cudaSetDevice(c->device));
+    DevImage d;
+    int rc = stage_image(c, im, &d);
+    if (rc) return rc;
+    const SlotMap m = single_map(d);
+    rc = scan_stage(c, d, m, true);
+    if (!rc) rc = compact_stage(c, m, 0u, 0xffffffffu, ~size_t(0), true);
+    if (rc) return rc;
+    cudaStream_t s = c->stream;
+    CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    const size_t nr = c->h_ctl->n_rois;
+    RoiList rl = roi_list(c);
+    std::vector<unsigned long long> cnt(nr), off(nr + 1, 0);
+    if (nr) CK(cudaMemcpy(cnt.data(), rl.n, nr * 8, cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < nr; ++i) off[i + 1] = off[i] + cnt[i];
+    *n_rois = nr;
+    *n_px = off[nr];
+    if (!xs || !ys || !vs || !out_labels || !out_offsets || !out_bbox) return finish(c);  // size query
+    if (nr > cap_rois || off[nr] > cap_px) return set_error(FX_E_CAPACITY, "cloud buffers too small");
+    if (nr) {
+        std::vector<int32_t> gx(nr), gy(nr);
+        std::vector<uint32_t> w(nr), h(nr);
+        CK(cudaMemcpy(out_labels, rl.label, nr * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(gx.data(), rl.gx, nr * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(gy.data(), rl.gy, nr * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(w.data(), rl.w, nr * 4, cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(h.data(), rl.h, nr * 4, cudaMemcpyDeviceToHost));
+        for (size_t i = 0; i < nr; ++i) {
+            out_offsets[i] = off[i];
+            out_bbox[4 * i + 0] = (uint32_t)gx[i];
+            out_bbox[4 * i + 1] = (uint32_t)gy[i];
+            out_bbox[4 * i + 2] = (uint32_t)gx[i] + w[i] - 1;
+            out_bbox[4 * i + 3] = (uint32_t)gy[i] + h[i] - 1;
+        }
+        out_offsets[nr] = off[nr];
+        const size_t np = off[nr];
+        void* buf = nullptr;  // offsets | xs | ys | vs, device
+        const size_t bytes = (nr + 1) * 8 + np * 10 + 64;
+        CK(cudaMalloc(&buf, bytes));
+        uint8_t* b = (uint8_t*)buf;
+        unsigned long long* d_off = (unsigned long long*)b;
+        uint32_t* d_x = (uint32_t*)(b + (nr + 1) * 8);
+        uint32_t* d_y = d_x + np;
+        uint16_t* d_v = (uint16_t*)(d_y + np);
+        cudaError_t e = cudaMemcpyAsync(d_off, off.data(), (nr + 1) * 8, cudaMemcpyHostToDevice, s);
+        if (e == cudaSuccess) {
+            Launch l(c, "k_cloud_gather");
+            k_cloud_gather<<<std::max<int>(1, std::min<int>((int)((nr + 7) / 8), 8 * c->sm_count)), 256, 0, s>>>(
+                d, rl, c->d_ctl, d_off, d_x, d_y, d_v);
+            e = cudaGetLastError();
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(xs, d_x, np * 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(ys, d_y, np * 4, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(vs, d_v, np * 2, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        cudaFree(buf);
+        if (e != cudaSuccess) return set_error(FX_E_CUDA, std::string("fx_roi_clouds: ") + cudaGetErrorString(e));
     }
     return finish(c);
 }

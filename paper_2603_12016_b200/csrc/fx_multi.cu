@@ -16,11 +16,13 @@
 
 #include <algorithm>
 #include <condition_variable>
+#include <cstring>
 #include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
 
+#include "fx_dev.cuh"
 #include "fx_host.hpp"
 #include "fxg.h"
 
@@ -35,6 +37,20 @@ cudaStream_t ictx_stream(fx_ctx* c);
 cudaStream_t ictx_d2h(fx_ctx* c);
 int ictx_device(const fx_ctx* c);
 int ictx_finish(fx_ctx* c);
+int islide_load_scan(fx_ctx* c, const fx_image* im, int y0, int y1, int reserve,
+                     cudaEvent_t loaded, cudaEvent_t scanned, uint32_t* lmax);
+void islide_band(fx_ctx* c, const uint16_t** L, const uint16_t** I, size_t* pitch,
+                 const unsigned long long** cnt, const uint32_t** bb, size_t* bb_pitch);
+int islide_merge(fx_ctx* c, const TablePeers& tp, uint32_t lmax, const cudaEvent_t* scanned,
+                 cudaEvent_t merged);
+int islide_commit(fx_ctx* c, uint32_t lmax, const cudaEvent_t* merged, int n_peers,
+                  uint64_t* h_cnt, uint32_t* h_bb);
+int islide_featurize(fx_ctx* c, const fx_image* im, int y0, int y1, int need,
+                     const std::vector<HaloRect>& rects, const std::vector<const uint16_t*>& pL,
+                     const std::vector<const uint16_t*>& pI, const std::vector<size_t>& pp,
+                     const std::vector<int>& py0, const cudaEvent_t* loaded, unsigned groups,
+                     const fx_texture_params& p, size_t cap, uint32_t* h_labels, double* h_values,
+                     size_t* n_rois);
 }  // namespace fxg
 
 using namespace fxg;
@@ -57,6 +73,8 @@ struct fx_multi {
     std::vector<int> devices;
     std::vector<fx_ctx*> ctx;
     std::vector<DevBufs> bufs;
+    // slide: per device, events on its own device: band loaded, scanned, table merged
+    std::vector<cudaEvent_t> ev_loaded, ev_scanned, ev_merged;
 };
 
 namespace {
@@ -138,7 +156,36 @@ int fx_multi_create(const int* devices, int n_devices, fx_multi** out) {
                 fx_multi_destroy(m);
                 return set_error(FX_E_CUDA, "cudaEventCreate failed");
             }
+        cudaEvent_t e[3];
+        for (cudaEvent_t& x : e)
+            if (cudaEventCreateWithFlags(&x, cudaEventDisableTiming) != cudaSuccess) {
+                fx_multi_destroy(m);
+                return set_error(FX_E_CUDA, "cudaEventCreate failed");
+            }
+        m->ev_loaded.push_back(e[0]);
+        m->ev_scanned.push_back(e[1]);
+        m->ev_merged.push_back(e[2]);
     }
+    // peer access between distinct devices (the slide's table merge and halo
+    // gather read the other bands' memory over NVLink)
+    for (int i = 0; i < n_devices; ++i)
+        for (int j = 0; j < n_devices; ++j) {
+            if (devices[i] == devices[j]) continue;
+            int ok = 0;
+            cudaDeviceCanAccessPeer(&ok, devices[i], devices[j]);
+            if (!ok) {
+                fx_multi_destroy(m);
+                return set_error(FX_E_CUDA, "no peer access between devices " +
+                                                std::to_string(devices[i]) + " and " + std::to_string(devices[j]));
+            }
+            cudaSetDevice(devices[i]);
+            const cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+            if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+                fx_multi_destroy(m);
+                return set_error(FX_E_CUDA, std::string("peer access: ") + cudaGetErrorString(e));
+            }
+            cudaGetLastError();
+        }
     *out = m;
     return FX_OK;
 }
@@ -155,6 +202,8 @@ int fx_multi_destroy(fx_multi* m) {
             if (b.drained[k]) cudaEventDestroy(b.drained[k]);
         }
     }
+    for (auto* v : {&m->ev_loaded, &m->ev_scanned, &m->ev_merged})
+        for (cudaEvent_t e : *v) cudaEventDestroy(e);
     delete m;
     return FX_OK;
 }
@@ -266,6 +315,151 @@ int fx_multi_featurize_batch(fx_multi* m, const fx_image* ims, int n, unsigned g
     size_t total = 0;
     for (size_t j = 0; j < n_chunks; ++j) total += (size_t)ledger.rows[j];
     row_offsets[n] = total;
+    return FX_OK;
+}
+
+
+// C5 across devices: one host slide in row bands, one band per device.
+//   1. every device loads its band (H2D) and scans it into its own label table;
+//   2. every device merges the tables of all bands by peer reads (k_table_merge:
+//      counts summed, boxes min / max, labels [0, lmax]) and commits the result:
+//      each ends with the table of the whole slide, bit for bit;
+//   3. a ROI belongs to the band holding its first row; an owner whose ROIs run
+//      below its band gathers just those windows' rectangles from the bands that
+//      hold them (k_halo_gather, peer reads) -- only straddling ROIs move, not
+//      whole rows -- and featurizes its ROIs on band + halo;
+//   4. the bands' rows (labels ascending each) are merged by label.
+// Every statistic is computed by one device over the ROI's complete window, so
+// the table equals fx_featurize on the whole slide for any number of devices.
+int fx_multi_featurize_slide(fx_multi* m, const fx_image* im, unsigned groups,
+                             const fx_texture_params* p, uint32_t* out_labels, double* out_values,
+                             size_t cap_rois, size_t* n_rois) {
+    if (!m || !im || !p || !n_rois) return set_error(FX_E_ARG, "null argument");
+    *n_rois = 0;
+    if (!im->intensity || !im->labels) return set_error(FX_E_ARG, "null raster");
+    if (im->width < 1 || im->height < 1) return set_error(FX_E_PAIRING, "empty raster");
+    if (im->pitch && im->pitch < (size_t)im->width) return set_error(FX_E_ARG, "pitch < width");
+    if (im->mem_kind != FX_MEM_HOST) return set_error(FX_E_ARG, "the slide is read from host memory");
+    int rc = ictx_check_groups(groups);
+    if (rc) return rc;
+    const int N = (int)m->ctx.size();
+    if (N > kMaxPeers) return set_error(FX_E_ARG, "at most 16 devices per slide");
+    const int H = im->height, W = im->width;
+    const int nc = ictx_ncols(groups, *p);
+    // bands of whole 64-row strips (the last one takes the remainder)
+    std::vector<int> y0(N), y1(N);
+    for (int d = 0; d < N; ++d) {
+        y0[d] = (int)((long long)H * d / N) / 64 * 64;
+        y1[d] = d == N - 1 ? H : (int)((long long)H * (d + 1) / N) / 64 * 64;
+    }
+    for (int d = 0; d < N; ++d)
+        if (y1[d] <= y0[d]) return set_error(FX_E_ARG, "slide too short for this many devices");
+    std::vector<int> status(N, FX_OK);
+    std::vector<std::string> errs(N);
+    auto parallel = [&](auto&& fn) {  // fn(d) on one host thread per device
+        std::vector<std::thread> th;
+        for (int d = 0; d < N; ++d)
+            th.emplace_back([&, d] {
+                cudaSetDevice(m->devices[d]);
+                const int r = fn(d);
+                if (r && !status[d]) {
+                    status[d] = r;
+                    errs[d] = fx_last_error();
+                }
+            });
+        for (auto& t : th) t.join();
+        for (int d = 0; d < N; ++d)
+            if (status[d]) return set_error(status[d], errs[d]);
+        return (int)FX_OK;
+    };
+    // 1. load + scan
+    std::vector<uint32_t> lmax(N, 0);
+    rc = parallel([&](int d) {
+        const int reserve = std::min(H - y1[d], std::max(256, (y1[d] - y0[d]) / 4));
+        return islide_load_scan(m->ctx[d], im, y0[d], y1[d], reserve, m->ev_loaded[d], m->ev_scanned[d],
+                                &lmax[d]);
+    });
+    if (rc) return rc;
+    const uint32_t L = *std::max_element(lmax.begin(), lmax.end());
+    if (L == 0) return FX_OK;  // no labelled pixel
+    // 2. merge by peer reads, commit
+    TablePeers tp{};
+    tp.n = N;
+    std::vector<const uint16_t*> pL(N), pI(N);
+    std::vector<size_t> pp(N);
+    for (int d = 0; d < N; ++d)
+        islide_band(m->ctx[d], &pL[d], &pI[d], &pp[d], &tp.cnt[d], &tp.bb[d], &tp.pitch[d]);
+    std::vector<uint64_t> cnt((size_t)L + 1);
+    std::vector<uint32_t> bb(4 * ((size_t)L + 1));
+    rc = parallel([&](int d) {
+        int r = islide_merge(m->ctx[d], tp, L, m->ev_scanned.data(), m->ev_merged[d]);
+        return r;
+    });
+    if (rc) return rc;
+    rc = parallel([&](int d) {
+        std::vector<uint64_t> c2;
+        std::vector<uint32_t> b2;
+        if (d) {  // every device commits; device 0's copy feeds the plan
+            c2.resize(cnt.size());
+            b2.resize(bb.size());
+        }
+        return islide_commit(m->ctx[d], L, m->ev_merged.data(), N, d ? c2.data() : cnt.data(),
+                             d ? b2.data() : bb.data());
+    });
+    if (rc) return rc;
+    // 3. ownership (first row) and the straddling rectangles per owner
+    const size_t nl = (size_t)L + 1;
+    const long long oy = im->origin_y, ox = im->origin_x;
+    std::vector<int> need(N, 0);
+    std::vector<size_t> owned(N, 0);
+    std::vector<std::vector<HaloRect>> rects(N);
+    size_t total = 0;
+    for (size_t l = 1; l < nl; ++l) {
+        if (!cnt[l]) continue;
+        ++total;
+        const long long ymin = (long long)bb[nl + l] - oy, ymax = (long long)bb[3 * nl + l] - oy;
+        const int xlo = (int)((long long)bb[l] - ox), xhi = (int)((long long)bb[2 * nl + l] - ox) + 1;
+        int d = 0;
+        while (d + 1 < N && ymin >= y0[d + 1]) ++d;
+        ++owned[d];
+        if (ymax < y1[d]) continue;
+        need[d] = std::max(need[d], (int)(ymax + 1 - y1[d]));
+        for (int e = d + 1; e < N && y0[e] <= ymax; ++e) {
+            const int a = std::max(y1[d], y0[e]), b = (int)std::min<long long>(y1[e], ymax + 1);
+            if (a < b) rects[d].push_back(HaloRect{e, a, b, xlo, xhi});
+        }
+    }
+    if (total > cap_rois)
+        return set_error(FX_E_CAPACITY, "output capacity " + std::to_string(cap_rois) + " < " +
+                                            std::to_string(total) + " ROIs");
+    std::vector<int> py0(y0.begin(), y0.end());
+    std::vector<std::vector<uint32_t>> labs(N);
+    std::vector<std::vector<double>> vals(N);
+    std::vector<size_t> got(N, 0);
+    rc = parallel([&](int d) {
+        labs[d].resize(std::max<size_t>(owned[d], 1));
+        vals[d].resize(std::max<size_t>(owned[d], 1) * (size_t)std::max(nc, 1));
+        return islide_featurize(m->ctx[d], im, y0[d], y1[d], need[d], rects[d], pL, pI, pp, py0,
+                                m->ev_loaded.data(), groups, *p, owned[d], labs[d].data(),
+                                vals[d].data(), &got[d]);
+    });
+    if (rc) return rc;
+    // 4. merge the bands' rows by label
+    std::vector<size_t> at(N, 0);
+    size_t k = 0;
+    while (k < total) {
+        int best = -1;
+        for (int d = 0; d < N; ++d)
+            if (at[d] < got[d] && (best < 0 || labs[d][at[d]] < labs[best][at[best]])) best = d;
+        if (best < 0) break;
+        out_labels[k] = labs[best][at[best]];
+        std::memcpy(out_values + k * nc, vals[best].data() + at[best] * nc, (size_t)nc * sizeof(double));
+        ++at[best];
+        ++k;
+    }
+    if (k != total) return set_error(FX_E_INTERNAL, "bands returned " + std::to_string(k) + " of " +
+                                                      std::to_string(total) + " ROIs");
+    *n_rois = total;
     return FX_OK;
 }
 

@@ -515,4 +515,36 @@ __global__ void k_halo_gather(const HaloRect* rects, int n_rects, const uint16_t
     }
 }
 
+
+// --- pixel clouds (RoiRegistry::cloud, roi.cpp:76-148) --------------------------
+//
+// One warp per ROI walks its window row by row, 32 columns at a time; member
+// pixels are ballot-compacted, so each cloud comes out in mask scan order (the
+// reference's order) at its offset in label order: (x, y) global, intensity.
+__global__ void k_cloud_gather(DevImage img, RoiList rl, const Control* ctl,
+                               const unsigned long long* offsets, uint32_t* xs, uint32_t* ys,
+                               uint16_t* vs) {
+    const uint32_t lane = threadIdx.x & 31;
+    const uint32_t warps = gridDim.x * (blockDim.x >> 5);
+    const uint32_t n = ctl->n_rois;
+    for (uint32_t r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+        const uint32_t L = rl.label[r], x0 = rl.x0[r], y0 = rl.y0[r], w = rl.w[r], h = rl.h[r];
+        unsigned long long at = offsets[r];
+        for (uint32_t y = 0; y < h; ++y) {
+            const size_t row = (size_t)(y0 + y) * img.pitch + x0;
+            for (uint32_t x = 0; x < w; x += 32) {
+                const bool in = x + lane < w && img.L[row + x + lane] == L;
+                const unsigned m = __ballot_sync(kFull, in);
+                if (in) {
+                    const unsigned long long k = at + __popc(m & lanemask_lt());
+                    xs[k] = (uint32_t)rl.gx[r] + x + lane;
+                    ys[k] = (uint32_t)rl.gy[r] + y;
+                    vs[k] = img.I[row + x + lane];
+                }
+                at += __popc(m);
+            }
+        }
+    }
+}
+
 }  // namespace fxg

@@ -410,3 +410,28 @@ class Multi:
         offs = offs.astype(np.int64)
         return [(out_l[offs[i]:offs[i + 1]], out_v[offs[i]:offs[i + 1], :ncols])
                 for i in range(len(pairs))]
+
+    def featurize_slide(self, intensity, labels, groups=("intensity",), params=None,
+                        cap_rois=None, origin=(0, 0)):
+        """One host image in row bands over the devices (fx_multi_featurize_slide);
+        identical to Context.featurize on the whole image."""
+        intensity = np.ascontiguousarray(intensity, dtype=np.uint16)
+        labels = np.ascontiguousarray(labels, dtype=np.uint16)
+        if intensity.shape != labels.shape:
+            raise FxError(3, "image/mask dimension mismatch")
+        h, w = labels.shape
+        params = params or resolve_profile("default")
+        mask = groups if isinstance(groups, int) else resolve_groups(list(groups))
+        ncols = len(feature_columns(mask, params))
+        if cap_rois is None:
+            cap_rois = int(np.count_nonzero(np.bincount(labels.ravel(), minlength=65536)[1:]))
+        out_l = np.zeros(max(cap_rois, 1), np.uint32)
+        out_v = np.zeros((max(cap_rois, 1), max(ncols, 1)), np.float64)
+        im = FxImage(intensity.ctypes.data, labels.ctypes.data, w, h, w, int(origin[0]),
+                     int(origin[1]), MEM_HOST)
+        n = C.c_size_t()
+        _check(lib().fx_multi_featurize_slide(self.h, C.byref(im), C.c_uint(mask), C.byref(params),
+                                              _p(out_l, C.c_uint32), _p(out_v, C.c_double),
+                                              C.c_size_t(cap_rois), C.byref(n)))
+        return out_l[:n.value], out_v[:n.value, :ncols]
+

@@ -95,15 +95,18 @@ def featurize_band(backend, dist, rank, world, band_intensity, band_labels, y0, 
     ext_I[: y1 - y0] = band_intensity
     ext_L[: y1 - y0] = band_labels
     ops = []
+    # rows travel as bytes: NCCL has no 16-bit integer type (torch's NCCL type map
+    # lacks int16), so the uint16 rasters are viewed as uint8 on both sides
+    as_bytes = lambda t: t.contiguous().view(torch.uint8)
     for src, dst, a, b in plan:
         if src == dst:
             continue
         if src == rank:  # send my rows [a, b)
-            ops.append(dist.P2POp(dist.isend, band_intensity[a - y0:b - y0].contiguous(), dst))
-            ops.append(dist.P2POp(dist.isend, band_labels[a - y0:b - y0].contiguous(), dst))
-        if dst == rank:
-            ops.append(dist.P2POp(dist.irecv, ext_I[a - y0:b - y0], src))
-            ops.append(dist.P2POp(dist.irecv, ext_L[a - y0:b - y0], src))
+            ops.append(dist.P2POp(dist.isend, as_bytes(band_intensity[a - y0:b - y0]), dst))
+            ops.append(dist.P2POp(dist.isend, as_bytes(band_labels[a - y0:b - y0]), dst))
+        if dst == rank:  # row slices of the contiguous extended rasters: byte views alias them
+            ops.append(dist.P2POp(dist.irecv, ext_I[a - y0:b - y0].view(torch.uint8), src))
+            ops.append(dist.P2POp(dist.irecv, ext_L[a - y0:b - y0].view(torch.uint8), src))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()

@@ -126,6 +126,58 @@ static void host_cases() {
     }
 }
 
+static void registry_cases() {
+    // RoiRegistry on the device (roi.hpp:45-88): the 2x2 read-off of
+    // test_roistore.cpp:34-58 -- mask [0,1,1,2], I [9,8,7,6]
+    IntensityImage im;
+    im.width = im.height = 2;
+    im.pixels = {9, 8, 7, 6};
+    LabelMask mk;
+    mk.width = mk.height = 2;
+    mk.labels = {0, 1, 1, 2};
+    const RoiRegistry reg = RoiRegistry::accumulate(iter_row_tiles(im, mk, 1), {});
+    CHECK((reg.labels() == std::vector<uint32_t>{1, 2}));
+    CHECK(reg.roi_count() == 2 && reg.contains(1) && !reg.contains(3));
+    const PixelCloud c1 = reg.cloud(1);
+    CHECK(c1.count() == 2 && c1.pixels[0].x == 1 && c1.pixels[0].y == 0 && c1.pixels[0].intensity == 8);
+    CHECK(c1.pixels[1].x == 0 && c1.pixels[1].y == 1 && c1.pixels[1].intensity == 7);
+    CHECK(c1.bbox.x_min == 0 && c1.bbox.y_min == 0 && c1.bbox.x_max == 1 && c1.bbox.y_max == 1);
+    const PixelCloud c2 = reg.cloud(2);
+    CHECK(c2.count() == 1 && c2.pixels[0].x == 1 && c2.pixels[0].y == 1 && c2.pixels[0].intensity == 6);
+    CHECK_THROWS_AS(reg.cloud(5), std::out_of_range);
+    // all background: an empty registry (:60-64)
+    mk.labels = {0, 0, 0, 0};
+    CHECK(RoiRegistry::accumulate(iter_row_tiles(im, mk), {}).roi_count() == 0);
+    CHECK_THROWS_AS(iter_row_tiles(im, mk, 0), PairingError);
+    // accumulate -> cloud -> compute_roi_features == featurize (the run_tune call
+    // pattern, featurex_main.cpp:104-109), on a 97x83 image of random blobs
+    IntensityImage I;
+    LabelMask L;
+    I.width = L.width = 97;
+    I.height = L.height = 83;
+    I.pixels.resize(97 * 83);
+    L.labels.assign(97 * 83, 0);
+    uint32_t st = 12345;
+    auto rnd = [&] { st = st * 1664525u + 1013904223u; return st >> 8; };
+    for (auto& v : I.pixels) v = (uint16_t)(rnd() & 0xffff);
+    for (int k = 0; k < 30; ++k) {
+        const int cx = rnd() % 97, cy = rnd() % 83, r = 2 + rnd() % 9;
+        const uint16_t lab = (uint16_t)(1 + rnd() % 20);
+        for (int y = std::max(0, cy - r); y < std::min(83, cy + r + 1); ++y)
+            for (int x = std::max(0, cx - r); x < std::min(97, cx + r + 1); ++x)
+                if ((x - cx) * (x - cx) + (y - cy) * (y - cy) <= r * r) L.labels[y * 97 + x] = lab;
+    }
+    const std::vector<std::string> g = {"intensity", "moments", "glcm"};
+    const TextureParams tp = resolve_profile("default");
+    const FeatureTable t = featurize(I, L, g, tp);
+    const RoiRegistry r2 = RoiRegistry::accumulate(iter_row_tiles(I, L, 16), {});
+    CHECK(r2.labels() == t.labels);
+    for (size_t i = 0; i < t.labels.size(); ++i) {
+        const std::vector<double> v = compute_roi_features(r2.cloud(t.labels[i]), g, tp);
+        CHECK(std::equal(v.begin(), v.end(), t.values.begin() + i * t.columns.size()));
+    }
+}
+
 static void device_cases() {
     {  // one row per ROI (:77-97)
         const auto d = fresh_dir("fxg_engine_simple");
@@ -310,7 +362,10 @@ int main(int argc, char** argv) {
     const bool host_only = argc > 1 && std::strcmp(argv[1], "--host") == 0;
     try {
         host_cases();
-        if (!host_only) device_cases();
+        if (!host_only) {
+            device_cases();
+            registry_cases();
+        }
     } catch (const std::exception& e) {
         std::fprintf(stderr, "unexpected exception: %s\n", e.what());
         return 2;

@@ -191,3 +191,164 @@ def test_device_band_sharding_bitwise(ctx, nbands):
     assert np.array_equal(values[order], gv)
     for c in ctxs:
         c.close()
+
+
+# ---- the library's own slide path over several devices (fx_multi_featurize_slide:
+# table merge and straddling windows by peer reads) -------------------------
+
+def _slide_image():
+    """600 x 300: blob grid + seam straddlers + a ROI spanning every band (its
+    halo exceeds the reserve rows: the separate band + halo raster path) + a
+    two-component ROI split across the slide."""
+    from tools import synth
+    sys.path.insert(0, HERE)
+    import inputs
+    L = np.zeros((600, 300), np.uint16)
+    g, _ = synth.packed_blob_mask_grid(300, 600, 64, 3)
+    L[:300] = g
+    L[300:600] = np.where(inputs.random_blobs((300, 300), 40, seed=5, max_r=30) > 0,
+                          inputs.random_blobs((300, 300), 40, seed=5, max_r=30) + 200, 0)
+    L[5:595, 140:143] = 900           # spans every band
+    L[60:70, 10:20] = 901             # two components far apart
+    L[520:530, 280:290] = 901
+    L[140:170, 200:260] = 902         # straddles row 150
+    I = synth.uniform_u16(L.shape, 8)
+    return I, L
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("devices", [[0], [0, 0], [0, 0, 0], [0, 0, 0, 0]])
+def test_multi_slide_matches_single(ctx, devices):
+    import paper_2603_12016_b200 as fx
+    I, L = _slide_image()
+    p = fx.resolve_profile("default")
+    gl, gv = ctx.featurize(I, L, GROUPS, p)
+    m = fx.Multi(devices)
+    try:
+        ml, mv = m.featurize_slide(I, L, GROUPS, p, origin=(0, 0))
+        # twice: the contexts' tables and buffers are left reusable
+        ml2, mv2 = m.featurize_slide(I, L, GROUPS, p)
+    finally:
+        m.close()
+    assert np.array_equal(gl, ml) and np.array_equal(gv, mv)
+    assert np.array_equal(ml, ml2) and np.array_equal(mv, mv2)
+
+
+@pytest.mark.gpu
+def test_multi_slide_c5_shape(ctx):
+    """C5-like 16384^2 slide of ~2e5-px ROIs over 4 contexts == one featurize."""
+    import paper_2603_12016_b200 as fx
+    from tools import synth
+    L, _ = synth.packed_blob_mask_grid(16384, 200000, 576, 1)
+    L = np.roll(L, 340, axis=0)
+    I = synth.uniform_u16(L.shape, 5)
+    groups = ["intensity", "moments", "glcm"]
+    p = fx.resolve_profile("default")
+    gl, gv = ctx.featurize(I, L, groups, p)
+    m = fx.Multi([0, 0, 0, 0])
+    try:
+        ml, mv = m.featurize_slide(I, L, groups, p)
+    finally:
+        m.close()
+    assert np.array_equal(gl, ml) and np.array_equal(gv, mv)
+
+
+# ---- the device backend itself with 2 ranks: two processes on one GPU, the
+# collectives staged through host memory over gloo (the ranks' kernels never
+# wait on each other) ----------------------------------------------------------
+
+class StagedDist:
+    """torch.distributed over gloo for CUDA tensors: every collective / p2p op
+    copies through host memory.  Exposes the subset shard.featurize_band uses."""
+    ReduceOp = dist.ReduceOp
+
+    class P2POp:
+        def __init__(self, op, tensor, peer):
+            self.op, self.tensor, self.peer = op, tensor, peer
+
+    isend, irecv = "isend", "irecv"
+
+    @staticmethod
+    def all_reduce(t, op=dist.ReduceOp.SUM):
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        t.copy_(c)
+
+    @staticmethod
+    def all_gather(outs, t):
+        cs = [torch.empty_like(o, device="cpu") for o in outs]
+        dist.all_gather(cs, t.cpu())
+        for o, c in zip(outs, cs):
+            o.copy_(c)
+
+    @staticmethod
+    def batch_isend_irecv(ops):
+        reqs, backs = [], []
+        for o in ops:
+            if o.op == "isend":
+                reqs.append(dist.isend(o.tensor.cpu(), o.peer))
+            else:
+                buf = torch.empty_like(o.tensor, device="cpu")
+                reqs.append(dist.irecv(buf, o.peer))
+                backs.append((o.tensor, buf))
+
+        class Done:
+            def wait(self_):
+                for r in reqs:
+                    r.wait()
+                for t, b in backs:
+                    t.copy_(b)
+        return [Done()]
+
+
+def _device_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    sys.path.insert(0, HERE)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2603_12016_b200 as fx
+    from paper_2603_12016_b200 import shard
+    I, L = _slide_image()
+    H, W = L.shape
+    y0, y1 = shard.band_plan(H, world)[rank]
+    ctx = fx.Context(0)
+    be = shard.DeviceBackend(ctx, GROUPS, fx.resolve_profile("default"))
+    bI = torch.from_numpy(I[y0:y1].view(np.int16).copy()).cuda()
+    bL = torch.from_numpy(L[y0:y1].view(np.int16).copy()).cuda()
+    labels, values = shard.featurize_band(be, StagedDist, rank, world, bI, bL, y0, H, W)
+    q.put((rank, labels.cpu().numpy(), values.cpu().numpy()))
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_device_backend_multi_rank(ctx, world):
+    import paper_2603_12016_b200 as fx
+    mpc = mp.get_context("spawn")
+    q = mpc.Queue()
+    port = 29700 + world * 11 + os.getpid() % 1000
+    procs = [mpc.Process(target=_device_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted([q.get(timeout=600) for _ in range(world)], key=lambda t: t[0])
+    for p in procs:
+        p.join(120)
+        assert p.exitcode == 0
+    labels = np.concatenate([r[1] for r in res]).astype(np.uint32)
+    values = np.concatenate([r[2] for r in res])
+    order = np.argsort(labels)
+    I, L = _slide_image()
+    gl, gv = ctx.featurize(I, L, GROUPS, fx.resolve_profile("default"))
+    assert np.array_equal(labels[order], gl)
+    assert np.array_equal(values[order], gv)
+
+
+def test_halo_rows_travel_as_bytes():
+    """NCCL has no int16: the halo rows are exchanged as uint8 views."""
+    import inspect
+    from paper_2603_12016_b200 import shard
+    src = inspect.getsource(shard.featurize_band)
+    assert "view(torch.uint8)" in src
