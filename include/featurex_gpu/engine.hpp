@@ -159,6 +159,9 @@ struct ExtractionConfig {  // engine.hpp:24-38
     int rows_per_tile = 256;
     bool parallel = true;
     int device = 0;  // extension: CUDA device used by run()
+    // extension: several devices (one context and host thread each, pairs dealt in
+    // chunks, rows identical to one device); empty = {device}
+    std::vector<int> devices;
 };
 
 struct FeatureRow {  // engine.hpp:41-46

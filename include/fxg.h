@@ -256,7 +256,8 @@ int fx_multi_destroy(fx_multi* m);
 int fx_multi_device_count(const fx_multi* m);
 /* The i-th device's context (owned by m), e.g. for fx_ctx_set_band_rows. */
 fx_ctx* fx_multi_ctx(fx_multi* m, int i);
-/* C4 across devices: the batch is cut into chunks of up to 512 images, chunk j
+/* C4 across devices: the batch is cut into chunks (up to 512 images, at least
+ * one chunk per device when the batch allows), chunk j
  * runs on device j mod N through the fx_featurize_batch pipeline, and rows come
  * back straight into their place: output identical to fx_featurize_batch (rows in
  * input order, row_offsets[n+1]).  Host images only when N > 1. */

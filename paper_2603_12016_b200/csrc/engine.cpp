@@ -62,6 +62,23 @@ fx_ctx* context(int device) {
     return c;
 }
 
+// one fx_multi per (host thread, device list)
+fx_multi* multi_context(const std::vector<int>& devices) {
+    struct MultiCache {
+        std::map<std::vector<int>, fx_multi*> m;
+        ~MultiCache() {
+            for (auto& kv : m) fx_multi_destroy(kv.second);
+        }
+    };
+    thread_local MultiCache cache;
+    auto it = cache.m.find(devices);
+    if (it != cache.m.end()) return it->second;
+    fx_multi* m = nullptr;
+    check(fx_multi_create(devices.data(), static_cast<int>(devices.size()), &m));
+    cache.m[devices] = m;
+    return m;
+}
+
 fx_texture_params to_c(const TextureParams& p) {
     if (p.glcm.angles.size() > 8) throw ConfigError("at most 8 GLCM angles are supported");
     fx_texture_params t{};
@@ -782,7 +799,11 @@ RunSummary run(const ExtractionConfig& config) {
     }
 
     // 2. batch plan
-    constexpr size_t kBatchPairs = 128, kBatchBytes = size_t(256) << 20;
+    // several devices (ExtractionConfig::devices): batches N times larger, dealt
+    // over the devices in chunks by fx_multi_featurize_batch
+    const std::vector<int> devs = config.devices.empty() ? std::vector<int>{config.device} : config.devices;
+    const size_t scale = devs.size();
+    const size_t kBatchPairs = 128 * scale, kBatchBytes = (size_t(256) << 20) * scale;
     std::vector<std::pair<size_t, size_t>> plan;  // [begin, end) into good
     {
         size_t b = 0, bytes = 0;
@@ -858,13 +879,15 @@ RunSummary run(const ExtractionConfig& config) {
         }
         bt.offsets.assign(ims.size() + 1, 0);
         if (ims.empty()) return;
-        fx_ctx* ctx = context(config.device);
+        fx_ctx* ctx = context(devs.front());
+        fx_multi* multi = devs.size() > 1 ? multi_context(devs) : nullptr;
         auto call = [&](const fx_image* im, int n, size_t* offs, size_t cap_hint) -> int {
             size_t cap = std::max<size_t>(cap_hint, 1);
             for (;;) {
                 uint32_t* lab = sl.lab.get<uint32_t>(cap);
                 double* val = sl.val.get<double>(cap * std::max<size_t>(nc, 1));
-                const int rc = fx_featurize_batch(ctx, im, n, gm, &tp, lab, val, cap, offs);
+                const int rc = multi && n > 1 ? fx_multi_featurize_batch(multi, im, n, gm, &tp, lab, val, cap, offs)
+                                              : fx_featurize_batch(ctx, im, n, gm, &tp, lab, val, cap, offs);
                 if (rc != FX_E_CAPACITY) return rc;
                 cap = std::max(cap * 2, offs[n]);
             }

@@ -229,8 +229,10 @@ int fx_multi_featurize_batch(fx_multi* m, const fx_image* ims, int n, unsigned g
     if (kind == FX_MEM_DEVICE && m->ctx.size() > 1)
         return set_error(FX_E_ARG, "device-resident batches live on one device: use fx_featurize_batch");
     const int nc = ictx_ncols(groups, *p);
-    const size_t n_chunks = ((size_t)n + kChunkImages - 1) / kChunkImages;
     const int N = (int)m->ctx.size();
+    // chunks of up to one launch set, at least one per device when the batch allows
+    const int chunk = std::max(1, std::min(kChunkImages, (n + N - 1) / N));
+    const size_t n_chunks = ((size_t)n + chunk - 1) / chunk;
     Ledger ledger(n_chunks);
     double total_px = 0;
     for (int i = 0; i < n; ++i) total_px += (double)ims[i].width * ims[i].height;
@@ -244,7 +246,7 @@ int fx_multi_featurize_batch(fx_multi* m, const fx_image* ims, int n, unsigned g
         bool ran = false;  // finish() reads this call's control block: only after work
         for (size_t j = (size_t)d; j < n_chunks; j += N, use ^= 1) {
             ran = true;
-            const int first = (int)(j * kChunkImages), cnt = std::min(kChunkImages, n - first);
+            const int first = (int)(j * chunk), cnt = std::min(chunk, n - first);
             // rows of this chunk: guess from its pixel share of cap_rois, grow on overflow
             double px = 0;
             for (int i = first; i < first + cnt; ++i) px += (double)ims[i].width * ims[i].height;

@@ -369,6 +369,80 @@ __device__ __forceinline__ const uint16_t* radix_sort16(const uint16_t* src, uin
     return dst;
 }
 
+// Bitonic sort of up to 32 * NPL u16 keys held by one warp in registers: lane l
+// holds elements [l NPL, (l + 1) NPL), two per 32-bit register, compared two at a
+// time with the paired-halfword min / max (VIMNMX.U16x2).  Strides >= NPL swap
+// whole registers with the partner lane (shuffles), strides 2..NPL/2 pair
+// registers of one lane, stride 1 pairs the two halves of a register.  No shared
+// memory traffic and no atomics: the bucket sort's dependent shared-atomic
+// round trips were the S0 kernel's largest phase (36% of its clocks on C2).
+// Keys past n are 0xFFFF and sort to the end.
+template <int NPL>
+__device__ __forceinline__ void bitonic_warp_u16(uint32_t (&r)[NPL / 2]) {
+    const unsigned lane = lane_id();
+    constexpr int LL = NPL == 8 ? 3 : NPL == 16 ? 4 : 5;  // log2(NPL)
+    constexpr int LOGN = LL + 5;
+#pragma unroll
+    for (int k = 1; k <= LOGN; ++k) {
+#pragma unroll
+        for (int st = k - 1; st >= 0; --st) {
+            if (st >= LL) {  // partner lane
+                const int lm = 1 << (st - LL);
+                const bool up = k == LOGN || !((lane >> (k - LL)) & 1u);
+                const bool keep_min = ((lane & lm) == 0) == up;
+#pragma unroll
+                for (int q = 0; q < NPL / 2; ++q) {
+                    const uint32_t y = __shfl_xor_sync(kFull, r[q], lm);
+                    r[q] = keep_min ? __vminu2(r[q], y) : __vmaxu2(r[q], y);
+                }
+            } else if (st >= 1) {  // registers q, q + 2^(st-1) of this lane
+                const int rs = 1 << (st - 1);
+#pragma unroll
+                for (int q = 0; q < NPL / 2; ++q) {
+                    if (q & rs) continue;
+                    // direction: bit k of e = l NPL + 2 q + h
+                    const bool up = k == LOGN ||
+                                    (k >= LL ? !((lane >> (k - LL)) & 1u) : !((q >> (k - 1)) & 1));
+                    const uint32_t a = r[q], b = r[q + rs];
+                    const uint32_t lo = __vminu2(a, b), hi = __vmaxu2(a, b);
+                    r[q] = up ? lo : hi;
+                    r[q + rs] = up ? hi : lo;
+                }
+            } else {  // the two halves of each register
+#pragma unroll
+                for (int q = 0; q < NPL / 2; ++q) {
+                    const bool up = k == LOGN ||
+                                    (k >= LL ? !((lane >> (k - LL)) & 1u) : !((q >> (k - 1)) & 1));
+                    const uint32_t x = r[q], sw = __byte_perm(x, 0u, 0x1032);
+                    const uint32_t mn = __vminu2(x, sw), mxv = __vmaxu2(x, sw);
+                    r[q] = up ? __byte_perm(mn, mxv, 0x7610) : __byte_perm(mxv, mn, 0x7610);
+                }
+            }
+        }
+    }
+}
+
+// src[0, n) sorted into dst by bitonic_warp_u16 (n <= 32 NPL); src 4 B aligned
+template <int NPL>
+__device__ __forceinline__ void bitonic_sort16(const uint16_t* src, uint16_t* dst, uint32_t n) {
+    const unsigned lane = lane_id();
+    uint32_t r[NPL / 2];
+    const uint32_t e0 = lane * NPL;
+#pragma unroll
+    for (int q = 0; q < NPL / 2; ++q) {
+        const uint32_t e = e0 + 2 * q;
+        const uint32_t a = e < n ? src[e] : 0xffffu, b = e + 1 < n ? src[e + 1] : 0xffffu;
+        r[q] = a | (b << 16);
+    }
+    bitonic_warp_u16<NPL>(r);
+#pragma unroll
+    for (int q = 0; q < NPL / 2; ++q) {
+        const uint32_t e = e0 + 2 * q;
+        if (e < n) dst[e] = (uint16_t)(r[q] & 0xffffu);
+        if (e + 1 < n) dst[e + 1] = (uint16_t)(r[q] >> 16);
+    }
+}
+
 // Sort of plain u16 keys by one warp (no payload, so equal keys need no stable
 // order): bucket b = (v - vmin) >> s with s the least shift giving <= 512 buckets,
 // shared-atomic histogram and scatter, then each key ranks itself inside its
@@ -1069,8 +1143,18 @@ __device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64
             PT(6);
             const double T = sym ? 2.0 * (double)np : (double)np;
             const double logT = nlog2(T);
-            double asm_ = 0, ent = 0, acor = 0, jmax = 0;
-            uint32_t carry = 0;
+            // cells in key order: exact integer sums (ASM numerator, autocorrelation),
+            // the largest cell, and the entropy terms from the log2 table of counts;
+            // integer marginals by shared atomics (order-free) -- then the Haralick
+            // statistics from the marginals (haralick_finish, shared with the
+            // histogram path and the large-ROI kernel)
+            unsigned long long s2 = 0, sa = 0;
+            uint32_t jm = 0, carry = 0;
+            double el = 0;
+            uint32_t* px = marg;
+            uint32_t* py = marg + 256;
+            uint32_t* psum = marg + 512;
+            uint32_t* pdif = marg + 1024;
             for (uint32_t b0 = 0; b0 < np; b0 += 32) {
                 const uint32_t i = b0 + lane;
                 const bool ok = i < np;
@@ -1083,22 +1167,18 @@ __device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64
                 if (en_) {
                     const uint32_t c = i - s0 + 1;
                     const uint32_t ga = k / (uint32_t)ng, gb = k % (uint32_t)ng;
-                    const double gi = ga + 1.0, gj = gb + 1.0;
                     const bool off = sym && ga != gb;
                     const uint32_t cc = (sym && !off) ? 2u * c : c;
-                    const double p = (double)cc / T, mult = off ? 2.0 : 1.0;
-                    asm_ += mult * p * p;
-                    ent += mult * p * (logT - log2_int(cc));
-                    acor += mult * gi * gj * p;
-                    jmax = fmax(jmax, p);
-                    atomicAdd(&marg[ga], cc);
-                    atomicAdd(&marg[256 + gb], cc);
-                    atomicAdd(&marg[512 + ga + gb], off ? 2u * cc : cc);
-                    atomicAdd(&marg[1024 + (ga > gb ? ga - gb : gb - ga)], off ? 2u * cc : cc);
-                    if (off) {
-                        atomicAdd(&marg[gb], cc);
-                        atomicAdd(&marg[256 + ga], cc);
-                    }
+                    const uint32_t mcc = off ? 2u * cc : cc;
+                    s2 += (unsigned long long)mcc * cc;
+                    sa += (unsigned long long)((ga + 1) * (gb + 1)) * mcc;
+                    jm = max(jm, cc);
+                    el += (double)mcc * (logT - log2_int(cc));
+                    sred_add(&px[ga], cc);
+                    if (off) sred_add(&px[gb], cc);
+                    if (!sym) sred_add(&py[gb], cc);
+                    sred_add(&psum[ga + gb], mcc);
+                    sred_add(&pdif[ga > gb ? ga - gb : gb - ga], mcc);
                     if (dbg && dbg->glcm) {
                         dbg->glcm[((size_t)a * ng + ga) * ng + gb] = cc;
                         if (off) dbg->glcm[((size_t)a * ng + gb) * ng + ga] = cc;
@@ -1106,77 +1186,13 @@ __device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64
                 }
                 if (sb) carry = b0 + 31 - __clz(sb);
             }
+            s2 = warp_sum(s2);
+            sa = warp_sum(sa);
+            jm = warp_max(jm);
+            el = warp_sum(el);
             __syncwarp();
             PT(7);
-            double r8[8] = {asm_, ent, acor, 0, 0, 0, 0, 0};
-            jmax = warp_max(jmax);
-            // marginals px, py -> means (texture.cpp:127-131)
-            const double iT = 1.0 / T;
-            for (int g = lane; g < ng; g += 32) {
-                r8[3] += (g + 1) * ((double)marg[g] * iT);
-                r8[4] += (g + 1) * ((double)marg[256 + g] * iT);
-            }
-            // p_{x+y}: sum average and entropy; p_{x-y}: difference average/entropy
-            for (int k = lane; k < 2 * ng - 1; k += 32) {
-                const double p = (double)marg[512 + k] * iT;
-                if (p > 0) {
-                    r8[5] += (k + 2) * p;
-                    r8[6] -= p * nlog2(p);
-                }
-            }
-            for (int d = lane; d < ng; d += 32) {
-                const double p = (double)marg[1024 + d] * iT;
-                if (p > 0) r8[7] += d * p;
-            }
-            warp_sum8(r8);
-            const double mux = r8[3], muy = r8[4], sumave = r8[5], sument = r8[6], difave = r8[7];
-            double s8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // vx, vy, hx, hy, sumvar, clut, clus, clup
-            for (int g = lane; g < ng; g += 32) {
-                const double a1 = (double)marg[g] * iT, b1 = (double)marg[256 + g] * iT;
-                s8[0] += (g + 1 - mux) * (g + 1 - mux) * a1;
-                s8[1] += (g + 1 - muy) * (g + 1 - muy) * b1;
-                if (a1 > 0) s8[2] -= a1 * nlog2(a1);
-                if (b1 > 0) s8[3] -= b1 * nlog2(b1);
-            }
-            for (int k = lane; k < 2 * ng - 1; k += 32) {
-                const double p = (double)marg[512 + k] * iT;
-                if (p > 0) {
-                    s8[4] += (k + 2 - sumave) * (k + 2 - sumave) * p;
-                    const double s = k + 2 - mux - muy;
-                    s8[5] += s * s * p;
-                    s8[6] += s * s * s * p;
-                    s8[7] += s * s * s * s * p;
-                }
-            }
-            warp_sum8(s8);
-            double d8[8] = {0, 0, 0, 0, 0, 0, 0, 0};  // difent, contrast, idm, id, idn, idmn, iv, difvar
-            const double dng = (double)ng;
-            for (int d = lane; d < ng; d += 32) {
-                const double p = (double)marg[1024 + d] * iT;
-                if (p > 0) {
-                    const double dd = (double)d;
-                    d8[0] -= p * nlog2(p);
-                    d8[1] += dd * dd * p;
-                    d8[2] += p / (1.0 + dd * dd);
-                    d8[3] += p / (1.0 + dd);
-                    d8[4] += p / (1.0 + dd / dng);
-                    d8[5] += p / (1.0 + dd * dd / (dng * dng));
-                    if (d > 0) d8[6] += p / (dd * dd);
-                    d8[7] += (dd - difave) * (dd - difave) * p;
-                }
-            }
-            warp_sum8(d8);
-            const double vx = s8[0], vy = s8[1], hx = s8[2], hy = s8[3];
-            const double ent_ = r8[1], asm2 = r8[0], acor_ = r8[2];
-            const double corr = (vx > 0 && vy > 0) ? (acor_ - mux * muy) / sqrt(vx * vy) : 0.0;
-            const double hxy = hx + hy, hmax = fmax(hx, hy);
-            const double v29[29] = {asm2, acor_, s8[7], s8[6], s8[5], d8[1], corr, difave, d8[0],
-                                    d8[7], difave, sqrt(asm2), ent_, d8[3], d8[2], d8[3], d8[4],
-                                    d8[2], d8[5], hmax > 0 ? (ent_ - hxy) / hmax : 0.0,
-                                    sqrt(fmax(0.0, 1.0 - exp(-2.0 * (hxy - ent_)))), d8[6], mux,
-                                    ent_, jmax, vx, sumave, sument, s8[4]};
-#pragma unroll
-            for (int k = 0; k < 29; ++k) st[k] = v29[k];
+            haralick_finish(px, sym ? px : py, psum, pdif, ng, sym, T, logT, s2, sa, jm, el, st);
             PT(8);
         }
         double mine = 0;
@@ -1790,9 +1806,14 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
                                          (uint16_t*)(base + L.sorted), n,
                                          (uint32_t*)(base + L.cnt));
 #else
-        const uint16_t* s = bucket_sort16(vals, (uint16_t*)(base + L.tmp),
-                                          (uint16_t*)(base + L.sorted), n,
-                                          (uint32_t*)(base + L.cnt), gmin, gmax);
+        // registers bitonic networks up to 1024 keys (every S0 ROI), the bucket sort
+        // above that
+        uint16_t* sorted = (uint16_t*)(base + L.sorted);
+        const uint16_t* s = sorted;
+        if (n <= 256) bitonic_sort16<8>(vals, sorted, n);
+        else if (n <= 512) bitonic_sort16<16>(vals, sorted, n);
+        else if (n <= 1024) bitonic_sort16<32>(vals, sorted, n);
+        else s = bucket_sort16(vals, (uint16_t*)(base + L.tmp), sorted, n, (uint32_t*)(base + L.cnt), gmin, gmax);
 #endif
         __syncwarp();
         PT(1);

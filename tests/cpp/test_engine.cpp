@@ -316,6 +316,16 @@ static void device_cases() {
         CHECK(s.rows == rows.size() && s.rows > 299 * 5);
         write_csv(feature_columns(c.features, tp), rows, d / "g.csv");
         CHECK(slurp(d / "f.csv") == slurp(d / "g.csv"));
+        // several devices (ExtractionConfig::devices; here contexts sharing GPU 0):
+        // the same CSV, byte for byte, failure counted once
+        for (const std::vector<int>& devs : {std::vector<int>{0, 0}, std::vector<int>{0, 0, 0}}) {
+            ExtractionConfig cm = c;
+            cm.devices = devs;
+            cm.output_path = d / "m.csv";
+            const RunSummary sm = run(cm);
+            CHECK(sm.images == 299 && sm.failed_pairs == 1 && sm.rows == s.rows);
+            CHECK(slurp(d / "m.csv") == slurp(d / "f.csv"));
+        }
     }
     {  // batched per-ROI operator (extension) == one compute_roi_features per cloud
         std::mt19937 g(5);

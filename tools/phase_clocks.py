@@ -1,5 +1,5 @@
 """Per-phase clock shares of the S-class ROI kernels (phase-timing build).
-usage: FXG_LIB=.../libfxg_pt.so python tools/phase_clocks.py c2|c4 [tiles]"""
+usage: FXG_LIB=.../libfxg_pt.so python tools/phase_clocks.py c2|c3|c4|c5 [tiles]"""
 import ctypes as C
 import os
 import sys
@@ -33,6 +33,11 @@ elif which == "c4":
     groups = os.environ.get("FX_GROUPS", "intensity,moments,glcm").split(",")
     run = lambda: ctx.featurize_batch(pairs, groups, fx.resolve_profile("default"))
     nroi = sum(int(np.count_nonzero(np.bincount(p[1].ravel(), minlength=65536)[1:])) for p in pairs)
+if which == "c3":
+    L, _ = synth.packed_blob_mask_grid(4096, 400, 10000, 1)
+    I = synth.uniform_u16(L.shape, 0)
+    run = lambda: ctx.featurize(I, L, ["glcm"], fx.resolve_profile("ibsi-like"))
+    nroi = 10000
 if which == "c5":
     L, _ = synth.packed_blob_mask_grid(16384, 200000, 576, 1)
     I = synth.uniform_u16(L.shape, 0)
