@@ -374,9 +374,8 @@ __device__ __forceinline__ const uint16_t* radix_sort16(const uint16_t* src, uin
 // time with the paired-halfword min / max (VIMNMX.U16x2).  Strides >= NPL swap
 // whole registers with the partner lane (shuffles), strides 2..NPL/2 pair
 // registers of one lane, stride 1 pairs the two halves of a register.  No shared
-// memory traffic and no atomics: the bucket sort's dependent shared-atomic
-// round trips were the S0 kernel's largest phase (36% of its clocks on C2).
-// Keys past n are 0xFFFF and sort to the end.
+// memory traffic and no atomics (the radix sort's dependent shared-memory round
+// trips).  Used for the GLCM pair keys; keys past n are 0xFFFF and sort to the end.
 template <int NPL>
 __device__ __forceinline__ void bitonic_warp_u16(uint32_t (&r)[NPL / 2]) {
     const unsigned lane = lane_id();
@@ -1138,7 +1137,12 @@ __device__ __noinline__ void glcm_phase_s(uint32_t n, int h, int w, const uint64
         for (int k = 0; k < 29; ++k) st[k] = 0;
         if (dbg && dbg->pairs && lane == 0) dbg->pairs[a] = np;
         if (np > 0) {
-            const uint16_t* sk = radix_sort16(keys, keys2, keys, np, gcnt);
+            // register bitonic network up to 1024 pairs, the radix sort above that
+            const uint16_t* sk = keys;
+            if (np <= 256) bitonic_sort16<8>(keys, keys, np);
+            else if (np <= 512) bitonic_sort16<16>(keys, keys, np);
+            else if (np <= 1024) bitonic_sort16<32>(keys, keys, np);
+            else sk = radix_sort16(keys, keys2, keys, np, gcnt);
             __syncwarp();
             PT(6);
             const double T = sym ? 2.0 * (double)np : (double)np;
@@ -1806,14 +1810,11 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
                                          (uint16_t*)(base + L.sorted), n,
                                          (uint32_t*)(base + L.cnt));
 #else
-        // registers bitonic networks up to 1024 keys (every S0 ROI), the bucket sort
-        // above that
-        uint16_t* sorted = (uint16_t*)(base + L.sorted);
-        const uint16_t* s = sorted;
-        if (n <= 256) bitonic_sort16<8>(vals, sorted, n);
-        else if (n <= 512) bitonic_sort16<16>(vals, sorted, n);
-        else if (n <= 1024) bitonic_sort16<32>(vals, sorted, n);
-        else s = bucket_sort16(vals, (uint16_t*)(base + L.tmp), sorted, n, (uint32_t*)(base + L.cnt), gmin, gmax);
+        // (a register bitonic network here measured slower on C2, 0.320 -> 0.348 ms:
+        // its unrolled code pushed the other phases out of the instruction cache)
+        const uint16_t* s = bucket_sort16(vals, (uint16_t*)(base + L.tmp),
+                                          (uint16_t*)(base + L.sorted), n,
+                                          (uint32_t*)(base + L.cnt), gmin, gmax);
 #endif
         __syncwarp();
         PT(1);
