@@ -39,11 +39,10 @@ __global__ void k_halo_gather(const HaloRect* rects, int n_rects, const uint16_t
 __global__ void k_cloud_gather(DevImage img, RoiList rl, const Control* ctl,
                                const unsigned long long* offsets, uint32_t* xs, uint32_t* ys,
                                uint16_t* vs);
-__global__ void k_band_count(RoiList rl, const Control* ctl, uint32_t band_rows, uint32_t nb,
-                             uint32_t* cnt, uint32_t* first);
-__global__ void k_band_scatter(RoiList rl, const Control* ctl, uint32_t band_rows, uint32_t nb,
-                               const uint32_t* cnt, uint32_t* cursor, uint32_t* seg,
-                               Control* band_ctl);
+__global__ void k_band_count(RoiList rl, const Control* ctl, BandPlan bp, uint32_t* cnt,
+                             uint32_t* first);
+__global__ void k_band_scatter(RoiList rl, const Control* ctl, BandPlan bp, const uint32_t* cnt,
+                               uint32_t* cursor, uint32_t* seg, Control* band_ctl);
 cudaError_t roi_s_setup(int* occ /* [3][3]: class x GlcmMode */);
 void launch_roi_s(int cls, int grid, cudaStream_t s, const CUtensorMap* tmaps, int tma40, int tma72,
                   DevImage img, RoiList rl, Control* ctl, FeatCfg cfg, double* out,
@@ -945,17 +944,27 @@ int band_rows_for(const fx_ctx* c, int w, int h) {
     return std::max(256, (h / 8 + 63) / 64 * 64);                   // ~8 bands
 }
 
-int band_rows_clamped(int band_rows, int h) {  // at most kMaxBands bands
-    const int min_rows = ((h + kMaxBands - 1) / kMaxBands + 63) / 64 * 64;
-    return std::max(band_rows, min_rows);
+// band plan of an image of h rows: bands of band_rows (at least h / kMaxBands), the
+// last one cut into quarters (>= 64 rows each) so little work follows the last copy
+BandPlan band_plan(int band_rows, int h) {
+    const int min_rows = ((h + kMaxBands - 4 - 1) / (kMaxBands - 4) + 63) / 64 * 64;
+    const uint32_t R = (uint32_t)std::max(band_rows, min_rows);
+    BandPlan bp{};
+    bp.rows = R;
+    const uint32_t nb0 = ((uint32_t)h + R - 1) / R;
+    bp.nb1 = nb0 - 1;
+    bp.split_y = bp.nb1 * R;
+    bp.rows2 = std::max<uint32_t>(64, (R / 4 + 63) / 64 * 64);
+    bp.nb = bp.nb1 + ((uint32_t)h - bp.split_y + bp.rows2 - 1) / bp.rows2;
+    return bp;
 }
 
 int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned groups,
                      const fx_texture_params& p, uint32_t* out_labels, double* out_values,
                      size_t cap_rois, size_t* n_rois) {
     const int W = im->width, H = im->height;
-    band_rows = band_rows_clamped(band_rows, H);
-    const int nb = (H + band_rows - 1) / band_rows;
+    const BandPlan bp = band_plan(band_rows, H);
+    const int nb = (int)bp.nb;
     int rc = ensure_img(c, W, H);
     if (!rc) rc = ensure_band(c, nb);
     if (rc) return rc;
@@ -973,10 +982,13 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     // the copy stream starts after this stream's earlier work (staging buffer reuse)
     CK(cudaEventRecord(c->ev_compact, s));
     CK(cudaStreamWaitEvent(c->copy, c->ev_compact, 0));
-    auto rows_of = [&](int b) { return std::min(band_rows, H - b * band_rows); };
+    auto rows_of = [&](int b) {
+        const int y0 = (int)bp.y0_of((uint32_t)b);
+        return (b + 1 < nb ? (int)bp.y0_of((uint32_t)b + 1) : H) - y0;
+    };
     for (int pass = 0; pass < 2; ++pass)  // all labels, then all intensities
         for (int b = 0; b < nb; ++b) {
-            const size_t y0 = (size_t)b * band_rows;
+            const size_t y0 = bp.y0_of((uint32_t)b);
             const uint16_t* src = (pass ? im->intensity : im->labels) + y0 * (sp / 2);
             uint16_t* dst = const_cast<uint16_t*>(pass ? d.I : d.L) + y0 * P;
             CK(cudaMemcpy2DAsync(dst, P * 2, src, sp, (size_t)W * 2, (size_t)rows_of(b),
@@ -987,10 +999,10 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     for (int b = 0; b < nb; ++b) {
         CK(cudaStreamWaitEvent(s, ev[b], 0));
         DevImage band = d;
-        band.L = d.L + (size_t)b * band_rows * P;
+        band.L = d.L + (size_t)bp.y0_of((uint32_t)b) * P;
         band.I = band.L;
         band.h = rows_of(b);
-        band.oy = d.oy + b * band_rows;
+        band.oy = d.oy + (int)bp.y0_of((uint32_t)b);
         rc = scan_stage(c, band, single_map(band), b == 0);
         if (rc) return rc;
     }
@@ -1013,10 +1025,9 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     {
         const int grid = 2 * c->sm_count;
         Launch l(c, "k_band_count");
-        k_band_count<<<grid, 256, 0, s>>>(rl, c->d_ctl, (uint32_t)band_rows, (uint32_t)nb, cnt, first);
+        k_band_count<<<grid, 256, 0, s>>>(rl, c->d_ctl, bp, cnt, first);
         Launch l2(c, "k_band_scatter");
-        k_band_scatter<<<grid, 256, 0, s>>>(rl, c->d_ctl, (uint32_t)band_rows, (uint32_t)nb, cnt, cursor,
-                                            c->d_band_seg, c->d_band_ctl);
+        k_band_scatter<<<grid, 256, 0, s>>>(rl, c->d_ctl, bp, cnt, cursor, c->d_band_seg, c->d_band_ctl);
     }
     CK(cudaGetLastError());
     CK(cudaMemcpyAsync(c->h_band, c->d_band, (size_t)kMaxBands * (2 * kNumClasses + 1) * sizeof(uint32_t),

@@ -117,6 +117,19 @@ struct HaloRect {
 
 // banded host path: at most this many row bands per call
 constexpr int kMaxBands = 64;
+// Row bands of a banded call: nb1 bands of `rows` rows from row 0, then the rest
+// (from split_y) in bands of `rows2` (the last band is cut finer, so the work left
+// after the last copy is small).
+struct BandPlan {
+    uint32_t rows, rows2, split_y, nb1, nb;
+    __host__ __device__ uint32_t band_of(uint32_t y) const {
+        const uint32_t b = y < split_y ? y / rows : nb1 + (y - split_y) / rows2;
+        return b < nb ? b : nb - 1;
+    }
+    __host__ __device__ uint32_t y0_of(uint32_t b) const {
+        return b < nb1 ? b * rows : split_y + (b - nb1) * rows2;
+    }
+};
 
 // compaction scratch: per (slot, 1024-label block) counts and exclusive bases
 constexpr int kBlocksPerSlot = kMaxLabels / 1024;

@@ -390,7 +390,7 @@ __global__ void __launch_bounds__(1024) k_compact_emit(LabelTable t, Control* ct
 // host issues the per-band kernels without copying anything to the device.
 
 __device__ __forceinline__ bool band_item(const RoiList& rl, const Control* ctl, uint32_t i,
-                                          uint32_t band_rows, uint32_t nb, uint32_t& r, uint32_t& b,
+                                          const BandPlan& bp, uint32_t& r, uint32_t& b,
                                           uint32_t& k) {
     uint32_t base = 0;
     for (k = 0; k < (uint32_t)kNumClasses; ++k) {
@@ -403,25 +403,25 @@ __device__ __forceinline__ bool band_item(const RoiList& rl, const Control* ctl,
                           : k == kClassS1 ? rl.cls_list[kClassS1]
                           : k == kClassS2 ? rl.cls_list[kClassS2] : rl.cls_list[kClassL];
     r = lst[i - base];
-    b = min(nb - 1, (rl.y0[r] + rl.h[r] - 1) / band_rows);
+    b = bp.band_of(rl.y0[r] + rl.h[r] - 1);
     return true;
 }
 
-__global__ void k_band_count(RoiList rl, const Control* ctl, uint32_t band_rows, uint32_t nb,
-                             uint32_t* cnt, uint32_t* first) {
+__global__ void k_band_count(RoiList rl, const Control* ctl, BandPlan bp, uint32_t* cnt,
+                             uint32_t* first) {
     const uint32_t total = ctl->class_count[0] + ctl->class_count[1] + ctl->class_count[2] +
                            ctl->class_count[3];
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         uint32_t r, b, k;
-        if (!band_item(rl, ctl, i, band_rows, nb, r, b, k)) continue;
+        if (!band_item(rl, ctl, i, bp, r, b, k)) continue;
         atomicAdd(&cnt[b * kNumClasses + k], 1u);
         atomicMin(&first[b], r);
     }
 }
 
-__global__ void k_band_scatter(RoiList rl, const Control* ctl, uint32_t band_rows, uint32_t nb,
-                               const uint32_t* cnt, uint32_t* cursor, uint32_t* seg,
-                               Control* band_ctl) {
+__global__ void k_band_scatter(RoiList rl, const Control* ctl, BandPlan bp, const uint32_t* cnt,
+                               uint32_t* cursor, uint32_t* seg, Control* band_ctl) {
+    const uint32_t nb = bp.nb;
     __shared__ uint32_t off[kMaxBands * kNumClasses];
     if (threadIdx.x == 0) {  // band-major, class-minor exclusive offsets (<= 256 entries)
         uint32_t acc = 0;
@@ -435,7 +435,7 @@ __global__ void k_band_scatter(RoiList rl, const Control* ctl, uint32_t band_row
                            ctl->class_count[3];
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         uint32_t r, b, k;
-        if (!band_item(rl, ctl, i, band_rows, nb, r, b, k)) continue;
+        if (!band_item(rl, ctl, i, bp, r, b, k)) continue;
         const uint32_t j = b * kNumClasses + k;
         seg[off[j] + atomicAdd(&cursor[j], 1u)] = r;
     }
