@@ -12,8 +12,9 @@
 //    CSV formatting); memory_budget / spill_dir are validated like the reference
 //    but ROI data stays in HBM (no spill).
 //  - all seven groups (intensity, moments, shape, glcm, glrlm, glszm, ngtdm)
-//    run on the device; texture groups with ng > 256 raise ConfigError (the
-//    device kernels bound grey levels at 256; never a silent CPU fallback).
+//    run on the device for any grey-level count up to 32768 (the reference's
+//    int16 level grid); larger counts raise ConfigError (never a CPU fallback).
+//  - ExtractionConfig::devices (extension) spreads run() over several GPUs.
 #pragma once
 
 #include <cstdint>

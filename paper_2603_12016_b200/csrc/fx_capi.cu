@@ -60,6 +60,10 @@ BLayout make_blayout(uint32_t H, uint32_t WPR, uint32_t NMAX, uint32_t RUNMAX, u
                      unsigned long long CELLS);
 void launch_roi_b(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                   double* out, const DebugOut* dbg, uint8_t* scratch, const BLayout& B);
+WLayout make_wlayout(unsigned long long cells, unsigned long long nmax, int ng);
+cudaError_t wide_setup();
+void launch_texture_wide(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
+                         double* out, uint8_t* scratch, const WLayout& L);
 }  // namespace fxg
 
 using namespace fxg;
@@ -99,6 +103,8 @@ struct fx_ctx {
     size_t slide_bytes = 0;
     uint16_t* d_work = nullptr;            // band + halo raster when the reserve is too small
     size_t work_elems = 0;
+    uint8_t* d_wscratch = nullptr;         // wide texture kernel slabs (ng > 256)
+    size_t wscratch_bytes = 0;
     cudaEvent_t ev_compact = nullptr, ev_stats = nullptr;
     cudaEvent_t ev_staged[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
     // label table: tab_slots slices of 65536 entries, left reset by each compaction
@@ -320,12 +326,23 @@ void collect_times(fx_ctx* c) {
     c->pending.clear();
 }
 
+// texture groups with more than 256 grey levels run on the wide kernel (fx_wide.cu)
+constexpr int kWideNg = 256, kWideMaxNg = 32768;
+bool wide_texture(const FeatCfg& f) {
+    return f.ng > kWideNg && (f.col_glcm >= 0 || f.col_glrlm >= 0 || f.col_glszm >= 0 || f.col_ngtdm >= 0);
+}
+// the same configuration without the texture groups (their columns stay reserved)
+FeatCfg core_cfg(FeatCfg f) {
+    f.col_glcm = f.col_glrlm = f.col_glszm = f.col_ngtdm = -1;
+    return f;
+}
+
 int validate_texture(unsigned groups, const fx_texture_params& p) {
     if (!(groups & (FX_GROUP_GLCM | FX_GROUP_GLRLM | FX_GROUP_GLSZM | FX_GROUP_NGTDM)))
         return FX_OK;
     if (p.ng < 2) return set_error(FX_E_CONFIG, "grey level count must be >= 2");
-    if (p.ng > 256)
-        return set_error(FX_E_CONFIG, "device texture groups support ng <= 256 in this build");
+    if (p.ng > kWideMaxNg)  // the reference's level grid is int16 (texture.hpp:15-28)
+        return set_error(FX_E_CONFIG, "grey level count above 32768");
     if (p.n_angles < 1 || p.n_angles > 8) return set_error(FX_E_CONFIG, "1..8 angles supported");
     for (int i = 0; i < p.n_angles; ++i) {
         const int a = p.angles[i];
@@ -618,7 +635,7 @@ const char* const kSName[3] = {"k_roi_s0", "k_roi_s1", "k_roi_s2"};
 // overflow).
 int roi_work(fx_ctx* c, const DevImage& img, const FeatCfg& cfg, const Control& hc,
              const TmaSet& tm, double* out_dev, const DebugOut* dbg_dev, int cls_first,
-             Control* ctl, const RoiList& rl) {
+             Control* ctl, const RoiList& rl, const FeatCfg* wide = nullptr) {
     cudaStream_t s = c->stream;
     const int glcm = s_glcm_mode(cfg);
     for (int cls = cls_first; cls <= kClassS2; ++cls) {
@@ -704,6 +721,26 @@ int roi_work(fx_ctx* c, const DevImage& img, const FeatCfg& cfg, const Control& 
         launch_roi_b((int)grid, s, img, rl, ctl, cfg, out_dev, dbg_dev, c->d_lscratch, B);
     }
     CK(cudaGetLastError());
+    if (wide) {
+        // texture groups above 256 grey levels: every queued ROI's texture columns
+        const uint64_t total = n_s_rois + n_l;
+        const WLayout W = make_wlayout(std::max<unsigned long long>(hc.l_max_cells, (unsigned long long)kSW * kSH),
+                                       std::max<unsigned long long>(hc.l_max_n, (unsigned long long)kS2N), wide->ng);
+        uint64_t grid = std::min<uint64_t>((uint64_t)c->sm_count * 2, total);
+        grid = std::max<uint64_t>(1, std::min<uint64_t>(grid, (4ull << 30) / std::max<size_t>(W.bytes, 1)));
+        const size_t need = W.bytes * grid;
+        if (need > c->wscratch_bytes) {
+            cudaStreamSynchronize(s);
+            cudaFree(c->d_wscratch);
+            c->d_wscratch = nullptr;
+            c->wscratch_bytes = 0;
+            CK(cudaMalloc(&c->d_wscratch, need));
+            c->wscratch_bytes = need;
+        }
+        Launch l(c, "k_texture_wide");
+        launch_texture_wide((int)grid, s, img, rl, ctl, *wide, out_dev, c->d_wscratch, W);
+        CK(cudaGetLastError());
+    }
     return FX_OK;
 }
 
@@ -718,6 +755,9 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
     int rc = prepare_cfg(c, img, groups, p, dbg_dev, &cfg);
     if (rc) return rc;
     const int vrc = validate_texture(groups, p);
+    const FeatCfg wcfg = cfg;
+    const bool wide = vrc == FX_OK && wide_texture(cfg);
+    if (wide) cfg = core_cfg(cfg);
     cudaStream_t s = c->stream;
     rc = compact_stage(c, m, own_y0, own_y1, cap_rois, first);
     if (rc) return rc;
@@ -762,7 +802,8 @@ int featurize_stage(fx_ctx* c, const DevImage& img, const SlotMap& m, uint32_t o
         return set_error(FX_E_CAPACITY, "output capacity " + std::to_string(cap_rois) +
                                             " < " + std::to_string(hc.n_rois) + " ROIs");
     }
-    rc = roi_work(c, img, cfg, hc, tm, out_dev, dbg_dev, kClassS1, c->d_ctl, roi_list(c));
+    rc = roi_work(c, img, cfg, hc, tm, out_dev, dbg_dev, kClassS1, c->d_ctl, roi_list(c),
+                  wide ? &wcfg : nullptr);
     if (rc) return rc;
     CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
     return FX_OK;
@@ -1010,6 +1051,9 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     rc = prepare_cfg(c, d, groups, p, nullptr, &cfg);
     if (rc) return rc;
     const int vrc = validate_texture(groups, p);
+    const FeatCfg wcfg = cfg;
+    const bool wide = vrc == FX_OK && wide_texture(cfg);
+    if (wide) cfg = core_cfg(cfg);
     rc = compact_stage(c, single_map(d), 0u, 0xffffffffu, cap_rois, true);
     if (rc) return rc;
     // bucket the queued ROIs by band on the device (nothing queued when the ROIs
@@ -1077,7 +1121,8 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
         }
         CK(cudaStreamWaitEvent(s, ev[nb + b], 0));
         if (band_rois) {
-            rc = roi_work(c, d, cfg, bc, tm, c->d_out, nullptr, kClassS0, c->d_band_ctl + b, rb);
+            rc = roi_work(c, d, cfg, bc, tm, c->d_out, nullptr, kClassS0, c->d_band_ctl + b, rb,
+                          wide ? &wcfg : nullptr);
             if (rc) return rc;
         }
         const size_t upto = std::max<size_t>(rows_out, b == nb - 1 ? n : final_after[b]);
@@ -1514,6 +1559,7 @@ int fx_ctx_create(int device, fx_ctx** out) {
     CKC(roi_s_setup(&c->occ_s[0][0]));
     CKC(roi_b_setup());
     CKC(roi_t_setup());
+    CKC(wide_setup());
     for (auto& row : c->occ_s)
         for (int& o : row) o = std::max(1, o);
     void* fn = nullptr;
@@ -1587,6 +1633,7 @@ int fx_ctx_destroy(fx_ctx* c) {
     cudaFree(c->d_mbb);
     cudaFree(c->d_slide);
     cudaFree(c->d_work);
+    cudaFree(c->d_wscratch);
     if (c->h_band) cudaFreeHost(c->h_band);
     if (c->h_band_ctl) cudaFreeHost(c->h_band_ctl);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
@@ -2057,6 +2104,7 @@ int fx_debug_roi(fx_ctx* c, const fx_image* im, uint32_t label, const fx_texture
     const FeatCfg cfg = make_cfg(groups, *p);
     int rc = validate_texture(groups, *p);
     if (rc) return rc;
+    if (p->ng > kWideNg) return set_error(FX_E_CONFIG, "fx_debug_roi captures GLCM counts for ng <= 256");
     DevImage d;
     rc = stage_image(c, im, &d);
     if (rc) return rc;

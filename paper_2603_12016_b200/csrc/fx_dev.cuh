@@ -96,6 +96,8 @@ struct Control {
     uint32_t t_next[2];              // GLRLM/GLSZM/NGTDM work counters (S lists, L list)
     unsigned long long mom_alloc;    // moments: pixels staged so far (bump allocator)
     unsigned long long int_alloc;    // intensity: sorted values staged so far
+    uint32_t w_next;                 // wide texture kernel (ng > 256) work counter
+    uint32_t pad0_;
     // sticky across the sub-batches of one API call: compact_stage clears only the
     // fields above (offsetof(Control, error) bytes); the call's first stage clears all
     uint32_t error;                  // bit flags, see kErr*

@@ -124,11 +124,12 @@ __device__ __forceinline__ void haralick_finish(const uint32_t* px, const uint32
             const double p = pr(m), dd = (double)d;
             d8[0] -= p * (log2_int(m) - logT);
             d8[1] += dd * dd * p;
-            d8[2] += p * __ldg(&g_rcp_tab[0][d]);  // 1 / (1 + d^2)
-            d8[3] += p * __ldg(&g_rcp_tab[1][d]);  // 1 / (1 + d)
+            const bool tab = d < 256;  // the tables cover d < 256 (ng <= 256 always)
+            d8[2] += p * (tab ? __ldg(&g_rcp_tab[0][d]) : 1.0 / (1.0 + dd * dd));
+            d8[3] += p * (tab ? __ldg(&g_rcp_tab[1][d]) : 1.0 / (1.0 + dd));
             d8[4] += p * dng / (dng + dd);
             d8[5] += p * (dng * dng) / (dng * dng + dd * dd);
-            if (d > 0) d8[6] += p * __ldg(&g_rcp_tab[2][d]);  // 1 / d^2
+            if (d > 0) d8[6] += p * (tab ? __ldg(&g_rcp_tab[2][d]) : 1.0 / (dd * dd));
             d8[7] += (dd - difave) * (dd - difave) * p;
         }
     }

@@ -222,4 +222,12 @@ struct TLayout {
     uint32_t NMAX, HC;         // max ROI pixels; count-table capacity (power of 2)
 };
 
+// Byte offsets of one CTA's slab in the wide texture kernel (fx_wide.cu, ng > 256).
+struct WLayout {
+    size_t lev, par, keys, px, pext, sv, plist;
+    size_t bytes;
+    unsigned long long CELLS, NMAX;  // max window cells / ROI pixels of the launch
+    uint32_t NG;
+};
+
 }  // namespace fxg

@@ -234,15 +234,23 @@ static void device_cases() {
         c.mask_dir = d / "seg";
         c.output_path = d / "f.csv";
         c.features = {"glrlm"};
+        // more than 256 grey levels run on the device (the wide texture kernel); above
+        // the reference's int16 level grid: ConfigError, the pair logged and skipped
         GlcmParams gp = resolve_profile("default").glcm;
         gp.ng = 300;
         c.glcm_override = gp;
-        const RunSummary s = run(c);
+        RunSummary s = run(c);
+        CHECK(s.images == 1 && s.failed_pairs == 0 && s.rows == 2);
+        gp.ng = 40000;
+        c.glcm_override = gp;
+        s = run(c);
         CHECK(s.images == 0 && s.failed_pairs == 1);
         PixelCloud pc;
         pc.pixels = {{1, 1, 5}, {2, 1, 6}};
         TextureParams tp = resolve_profile("default");
         tp.glcm.ng = 300;
+        CHECK(compute_roi_features(pc, {"glszm"}, tp).size() == 16);
+        tp.glcm.ng = 40000;
         CHECK_THROWS_AS(compute_roi_features(pc, {"glszm"}, tp), ConfigError);
     }
     {  // the shape group runs on the device: a 1-pixel cloud reports the conventions

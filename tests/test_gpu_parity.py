@@ -340,3 +340,49 @@ def test_tied_values_small_rois(ctx, oracle, spread):
     Lb = synth.blob_mask_grid(512, 300, 100, 5)
     Ib = rng.integers(7, 7 + spread, size=Lb.shape, dtype=np.uint16)
     check(ctx, oracle, Ib, Lb, ["intensity", "moments"])
+
+
+# ---- texture groups with more than 256 grey levels (the wide kernel) ----------
+
+TEXTURE = ["glcm", "glrlm", "glszm", "ngtdm"]
+
+
+@pytest.mark.parametrize("over", [dict(ng=512), dict(ng=300, symmetric=False, angles=(135, 0, 45)),
+                                  dict(ng=2000, angles=(90, 90)), dict(ng=257, offset=2),
+                                  dict(ng=4096)])
+def test_wide_grey_levels(ctx, oracle, over):
+    """ng > 256 (the reference accepts any ng >= 2, its level grid is int16): every
+    texture group against the oracle, with the other groups alongside."""
+    L = inputs.random_blobs((120, 150), 30, seed=3, max_r=14)
+    I = inputs.uniform(L.shape, 7)
+    check(ctx, oracle, I, L, GROUPS, **over)
+    check(ctx, oracle, I, L, TEXTURE, **over)
+
+
+def test_wide_grey_levels_tiles_and_large_rois(ctx, oracle):
+    """ng = 512 on blob tiles (S windows) and on windows beyond 64 x 64 (L windows)"""
+    L, _ = synth.packed_blob_mask_grid(512, 1000, 100, 3)
+    I = synth.uniform_u16(L.shape, 2)
+    check(ctx, oracle, I, L, GROUPS, ng=512)
+    yy, xx = np.mgrid[0:300, 0:260]
+    L = np.zeros((300, 260), np.uint16)
+    L[(xx - 130) ** 2 / 110.0 ** 2 + (yy - 150) ** 2 / 140.0 ** 2 <= 1] = 3
+    L[20:40, 10:200] = 9
+    I = inputs.per_roi_levels(L, 4, noise=900)
+    check(ctx, oracle, I, L, TEXTURE, ng=1024)
+
+
+def test_wide_grey_levels_int16_limit(ctx, oracle):
+    """ng = 32768, the largest level count of the reference's int16 grid (run-length
+    and zone groups: the oracle's GLCM / NGTDM are O(ng^2) there)"""
+    L = inputs.random_blobs((60, 70), 12, seed=8, max_r=10)
+    I = inputs.uniform(L.shape, 9)
+    check(ctx, oracle, I, L, ["intensity", "glrlm", "glszm"], ng=32768)
+
+
+def test_wide_grey_levels_above_int16_is_config_error(ctx):
+    L = inputs.random_blobs((40, 40), 5, seed=1)
+    I = inputs.uniform(L.shape, 1)
+    with pytest.raises(fx.FxError) as e:
+        ctx.featurize(I, L, ["glcm"], fx.make_params("default", ng=40000))
+    assert e.value.kind == "ConfigError"
