@@ -866,10 +866,15 @@ int stage_image(fx_ctx* c, const fx_image* im, DevImage* d) {
     uint16_t* dI = c->d_img;
     uint16_t* dL = c->d_img + c->img_pitch * c->img_rows_cap;
     const size_t sp = (im->pitch ? im->pitch : (size_t)im->width) * 2;
-    CK(cudaMemcpy2DAsync(dI, c->img_pitch * 2, im->intensity, sp, (size_t)im->width * 2,
-                         (size_t)im->height, cudaMemcpyHostToDevice, c->stream));
-    CK(cudaMemcpy2DAsync(dL, c->img_pitch * 2, im->labels, sp, (size_t)im->width * 2,
-                         (size_t)im->height, cudaMemcpyHostToDevice, c->stream));
+    if (sp == c->img_pitch * 2 && (size_t)im->width == c->img_pitch) {  // linear copies
+        CK(cudaMemcpyAsync(dI, im->intensity, sp * (size_t)im->height, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpyAsync(dL, im->labels, sp * (size_t)im->height, cudaMemcpyHostToDevice, c->stream));
+    } else {
+        CK(cudaMemcpy2DAsync(dI, c->img_pitch * 2, im->intensity, sp, (size_t)im->width * 2,
+                             (size_t)im->height, cudaMemcpyHostToDevice, c->stream));
+        CK(cudaMemcpy2DAsync(dL, c->img_pitch * 2, im->labels, sp, (size_t)im->width * 2,
+                             (size_t)im->height, cudaMemcpyHostToDevice, c->stream));
+    }
     d->I = dI;
     d->L = dL;
     d->pitch = c->img_pitch;
@@ -1032,8 +1037,11 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
             const size_t y0 = bp.y0_of((uint32_t)b);
             const uint16_t* src = (pass ? im->intensity : im->labels) + y0 * (sp / 2);
             uint16_t* dst = const_cast<uint16_t*>(pass ? d.I : d.L) + y0 * P;
-            CK(cudaMemcpy2DAsync(dst, P * 2, src, sp, (size_t)W * 2, (size_t)rows_of(b),
-                                 cudaMemcpyHostToDevice, c->copy));
+            if (sp == P * 2 && (size_t)W == P)  // rows contiguous on both sides: one linear copy
+                CK(cudaMemcpyAsync(dst, src, sp * (size_t)rows_of(b), cudaMemcpyHostToDevice, c->copy));
+            else
+                CK(cudaMemcpy2DAsync(dst, P * 2, src, sp, (size_t)W * 2, (size_t)rows_of(b),
+                                     cudaMemcpyHostToDevice, c->copy));
             CK(cudaEventRecord(ev[pass * nb + b], c->copy));
         }
     // label scan band by band, in global coordinates
