@@ -52,7 +52,8 @@ void launch_shape_serial(int n_s, cudaStream_t s, RoiList rl, Control* ctl, Feat
                          double* out);
 cudaError_t roi_t_setup();
 void launch_serial_stats(int n_s, bool intensity, bool moments, cudaStream_t s, RoiList rl,
-                         Control* ctl, FeatCfg cfg, double* out);
+                         Control* ctl, FeatCfg cfg, double* out, cudaStream_t s2, cudaEvent_t fork,
+                         cudaEvent_t join);
 TLayout make_tlayout(unsigned long long CELLS, uint32_t NMAX);
 void launch_roi_t(int grid, cudaStream_t s, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg,
                   double* out, uint8_t* scratch, const TLayout& T, int which, bool init);
@@ -106,6 +107,7 @@ struct fx_ctx {
     uint8_t* d_wscratch = nullptr;         // wide texture kernel slabs (ng > 256)
     size_t wscratch_bytes = 0;
     cudaEvent_t ev_compact = nullptr, ev_stats = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;  // the serial passes on two streams
     cudaEvent_t ev_staged[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
     // label table: tab_slots slices of 65536 entries, left reset by each compaction
     int tab_slots = 0;
@@ -690,7 +692,7 @@ int roi_work(fx_ctx* c, const DevImage& img, const FeatCfg& cfg, const Control& 
         if (cfg.int_vals || cfg.mom_px) {
             Launch l(c, "k_serial_stats");
             launch_serial_stats((int)n_s_rois, cfg.int_vals != nullptr, cfg.mom_px != nullptr, s, rl,
-                                ctl, cfg, out_dev);
+                                ctl, cfg, out_dev, c->side, c->ev_fork, c->ev_join);
         }
         if (cfg.col_shape >= 0) {
             Launch l(c, "k_shape_serial");
@@ -1549,6 +1551,8 @@ int fx_ctx_create(int device, fx_ctx** out) {
     c->stream = c->own_stream;
     CKC(cudaEventCreateWithFlags(&c->ev_compact, cudaEventDisableTiming));
     CKC(cudaEventCreateWithFlags(&c->ev_stats, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    CKC(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CKC(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
     CKC(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
     if (const char* e = getenv("FXG_BAND_ROWS")) c->band_rows = atoi(e);
@@ -1630,6 +1634,8 @@ int fx_ctx_destroy(fx_ctx* c) {
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     if (c->ev_compact) cudaEventDestroy(c->ev_compact);
     if (c->ev_stats) cudaEventDestroy(c->ev_stats);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->copy) cudaStreamDestroy(c->copy);
     if (c->d2h) cudaStreamDestroy(c->d2h);

@@ -2487,6 +2487,9 @@ __device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
 #ifndef FXG_SERIAL_G
 #define FXG_SERIAL_G 1
 #endif
+#ifndef FXG_SERIAL_SPLIT
+#define FXG_SERIAL_SPLIT 0
+#endif
 constexpr int kSerialG = FXG_SERIAL_G;
 
 template <typename T>
@@ -2844,10 +2847,40 @@ __global__ void __launch_bounds__(FXG_SERIAL_TPB, FXG_SERIAL_MINB)
 #endif
 }
 
+// The two moments roles as their own kernel (fewer registers than the intensity
+// role needs, so more warps per SM), on a second stream next to the intensity role.
+#ifndef FXG_SERIAL_MOM_MINB
+#define FXG_SERIAL_MOM_MINB 8
+#endif
+__global__ void __launch_bounds__(FXG_SERIAL_TPB, FXG_SERIAL_MOM_MINB)
+    k_serial_moments(RoiList rl, Control* ctl, FeatCfg cfg, double* out, uint32_t bm) {
+    const uint32_t b = blockIdx.x, grp = b < bm ? 0u : 1u;
+    const uint32_t t = (b - grp * bm) * blockDim.x + threadIdx.x;
+    const uint32_t r = s_row_of(t, rl, ctl);
+    if (r == ~0u) return;
+    moments_row(r, (int)grp, rl, cfg, out);
+}
+
 void launch_serial_stats(int n_s, bool intensity, bool moments, cudaStream_t s, RoiList rl,
-                         Control* ctl, FeatCfg cfg, double* out) {
+                         Control* ctl, FeatCfg cfg, double* out, cudaStream_t s2, cudaEvent_t fork,
+                         cudaEvent_t join) {
     if (n_s <= 0 || (!intensity && !moments)) return;
     const uint32_t nb = (uint32_t)(((size_t)n_s * kSerialG + FXG_SERIAL_TPB - 1) / FXG_SERIAL_TPB);
+#if FXG_SERIAL_SPLIT
+    if (s2 && intensity && moments && kSerialG == 1) {
+        cudaEventRecord(fork, s);
+        cudaStreamWaitEvent(s2, fork, 0);
+        k_serial_moments<<<2 * nb, FXG_SERIAL_TPB, 0, s2>>>(rl, ctl, cfg, out, nb);
+        cudaEventRecord(join, s2);
+        k_serial_stats<<<nb, FXG_SERIAL_TPB, 0, s>>>(rl, ctl, cfg, out, nb, 0u);
+        cudaStreamWaitEvent(s, join, 0);
+        return;
+    }
+#else
+    (void)s2;
+    (void)fork;
+    (void)join;
+#endif
     const uint32_t bi = intensity ? nb : 0u, bm = moments ? nb : 0u;
     k_serial_stats<<<bi + 2 * bm, FXG_SERIAL_TPB, 0, s>>>(rl, ctl, cfg, out, bi, bm);
 }
