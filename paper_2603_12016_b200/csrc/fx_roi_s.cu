@@ -2488,7 +2488,7 @@ __device__ void intensity_row(uint32_t r, const RoiList& rl, const FeatCfg& cfg,
 #define FXG_SERIAL_G 1
 #endif
 #ifndef FXG_SERIAL_SPLIT
-#define FXG_SERIAL_SPLIT 0
+#define FXG_SERIAL_SPLIT 1
 #endif
 constexpr int kSerialG = FXG_SERIAL_G;
 
