@@ -1238,24 +1238,52 @@ int batch_core(fx_ctx* c, const fx_image* ims, int n, unsigned groups, const fx_
         SlotInfo* hs = c->h_slots[buf];
         uint16_t* hst = c->h_strips[buf];
         size_t row0 = 0;
+        const cudaMemcpyKind mk = kind == FX_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+        // images that sit back to back in the caller's memory with the staging pitch
+        // and whole 64-row strips (e.g. a [T, H, W] stack) go in one linear copy per
+        // raster: one call per run instead of two per image (host enqueue time
+        // bounded the C4 end-to-end path)
+        const uint16_t *runI = nullptr, *runL = nullptr;
+        size_t run_row0 = 0, run_rows = 0;
+        auto flush = [&]() -> int {
+            if (run_rows) {
+                CK(cudaMemcpyAsync(c->d_stage[buf] + run_row0 * P, runI, run_rows * P * 2, mk, c->copy));
+                CK(cudaMemcpyAsync(c->d_stage[buf] + c->stage_elems + run_row0 * P, runL, run_rows * P * 2,
+                                   mk, c->copy));
+            }
+            run_rows = 0;
+            return FX_OK;
+        };
         for (int j = 0; j < b.count; ++j) {
             const fx_image& im = ims[b.first + j];
             hs[j] = SlotInfo{(int32_t)row0, im.width, im.height, im.origin_x, im.origin_y};
             const size_t r = b.zero_copy ? (size_t)im.height : ((size_t)im.height + 63) / 64 * 64;
             for (size_t st = row0 / 64; st < (row0 + r + 63) / 64; ++st) hst[st] = (uint16_t)j;
             if (!b.zero_copy) {
-                const cudaMemcpyKind mk =
-                    kind == FX_MEM_HOST ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-                const size_t sp = pitch_of(im) * 2;
-                uint16_t* dI = c->d_stage[buf] + row0 * P;
-                uint16_t* dL = c->d_stage[buf] + c->stage_elems + row0 * P;
-                CK(cudaMemcpy2DAsync(dI, P * 2, im.intensity, sp, (size_t)im.width * 2,
-                                     (size_t)im.height, mk, c->copy));
-                CK(cudaMemcpy2DAsync(dL, P * 2, im.labels, sp, (size_t)im.width * 2,
-                                     (size_t)im.height, mk, c->copy));
+                const bool linear = pitch_of(im) == P && (size_t)im.height == r;
+                if (linear && run_rows && im.intensity == runI + run_rows * P && im.labels == runL + run_rows * P) {
+                    run_rows += r;  // extends the current run
+                } else {
+                    if (flush()) return FX_E_CUDA;
+                    if (linear) {
+                        runI = im.intensity;
+                        runL = im.labels;
+                        run_row0 = row0;
+                        run_rows = r;
+                    } else {
+                        const size_t sp = pitch_of(im) * 2;
+                        uint16_t* dI = c->d_stage[buf] + row0 * P;
+                        uint16_t* dL = c->d_stage[buf] + c->stage_elems + row0 * P;
+                        CK(cudaMemcpy2DAsync(dI, P * 2, im.intensity, sp, (size_t)im.width * 2,
+                                             (size_t)im.height, mk, c->copy));
+                        CK(cudaMemcpy2DAsync(dL, P * 2, im.labels, sp, (size_t)im.width * 2,
+                                             (size_t)im.height, mk, c->copy));
+                    }
+                }
             }
             row0 += r;
         }
+        if (flush()) return FX_E_CUDA;
         CK(cudaMemcpyAsync(c->d_slots[buf], hs, (size_t)b.count * sizeof(SlotInfo),
                            cudaMemcpyHostToDevice, c->copy));
         CK(cudaMemcpyAsync(c->d_strips[buf], hst, ((b.rows + 63) / 64) * sizeof(uint16_t),
