@@ -12,7 +12,7 @@ namespace fxg {
 // (tools/kbench.py): 8 rows x 1 block/SM 130 us, 2 rows x 8 blocks/SM 86 us --
 // the sweep is latency-bound, occupancy (bytes in flight) is the lever.
 #ifndef FXG_SCAN_BATCH
-#define FXG_SCAN_BATCH 4
+#define FXG_SCAN_BATCH 2
 #endif
 #ifndef FXG_SCAN_MINB
 #define FXG_SCAN_MINB 8

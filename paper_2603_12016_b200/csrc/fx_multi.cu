@@ -242,6 +242,15 @@ int fx_multi_featurize_batch(fx_multi* m, const fx_image* ims, int n, unsigned g
         fx_ctx* c = m->ctx[d];
         DevBufs& B = m->bufs[d];
         cudaSetDevice(m->devices[d]);
+        // whatever path leaves the worker, no copy into the caller's buffers is
+        // still in flight when the call returns
+        struct Drain {
+            fx_ctx* c;
+            ~Drain() {
+                cudaStreamSynchronize(ictx_d2h(c));
+                cudaStreamSynchronize(ictx_stream(c));
+            }
+        } drain{c};
         int use = 0;
         bool ran = false;  // finish() reads this call's control block: only after work
         for (size_t j = (size_t)d; j < n_chunks; j += N, use ^= 1) {
@@ -346,7 +355,7 @@ int fx_multi_featurize_slide(fx_multi* m, const fx_image* im, unsigned groups,
     if (rc) return rc;
     const int N = (int)m->ctx.size();
     if (N > kMaxPeers) return set_error(FX_E_ARG, "at most 16 devices per slide");
-    const int H = im->height, W = im->width;
+    const int H = im->height;
     const int nc = ictx_ncols(groups, *p);
     // bands of whole 64-row strips (the last one takes the remainder)
     std::vector<int> y0(N), y1(N);
@@ -371,7 +380,14 @@ int fx_multi_featurize_slide(fx_multi* m, const fx_image* im, unsigned groups,
             });
         for (auto& t : th) t.join();
         for (int d = 0; d < N; ++d)
-            if (status[d]) return set_error(status[d], errs[d]);
+            if (status[d]) {
+                // the other devices may still read the caller's slide (H2D): drain them
+                for (int e = 0; e < N; ++e) {
+                    cudaSetDevice(m->devices[e]);
+                    cudaStreamSynchronize(ictx_stream(m->ctx[e]));
+                }
+                return set_error(status[d], errs[d]);
+            }
         return (int)FX_OK;
     };
     // 1. load + scan

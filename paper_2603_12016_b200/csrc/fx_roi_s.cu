@@ -1716,7 +1716,6 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
         }
     }
     __syncwarp();
-    const double dn = (double)n;
     uint32_t vmin = gmin, vmax = gmax;  // value range (the gather computed it)
     bool have_minmax = true;
 

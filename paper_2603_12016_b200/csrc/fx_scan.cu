@@ -100,22 +100,24 @@ __device__ __forceinline__ void chunk_slow(uint4 v, uint32_t x, uint32_t y, uint
 __device__ __forceinline__ void chunk(uint4 v, uint32_t x, uint32_t y, uint32_t sb, CacheEnt& c0,
                                       CacheEnt& c1, const LabelTable& t) {
     if ((v.x | v.y | v.z | v.w) == 0u) return;
-    // nonzero halfwords and the largest label in the chunk (SIMD-in-word)
-    const uint32_t n0 = __vcmpne2(v.x, 0u), n1 = __vcmpne2(v.y, 0u), n2 = __vcmpne2(v.z, 0u),
-                   n3 = __vcmpne2(v.w, 0u);
+    // the largest label of the chunk (paired-halfword max, VIMNMX.U16x2)
     const uint32_t mx2 = __vmaxu2(__vmaxu2(v.x, v.y), __vmaxu2(v.z, v.w));
     const uint32_t L = max(mx2 & 0xffffu, mx2 >> 16);
     const uint32_t LL = L | (L << 16);
-    // every nonzero halfword equal to L ?
-    const uint32_t bad = (n0 & ~__vcmpeq2(v.x, LL)) | (n1 & ~__vcmpeq2(v.y, LL)) |
-                         (n2 & ~__vcmpeq2(v.z, LL)) | (n3 & ~__vcmpeq2(v.w, LL));
+    // a halfword h is 0 or L  <=>  min(h, h ^ L) == 0: one XOR and one paired min
+    // per word instead of the emulated SIMD compares
+    const uint32_t bad = __vminu2(v.x, v.x ^ LL) | __vminu2(v.y, v.y ^ LL) |
+                         __vminu2(v.z, v.z ^ LL) | __vminu2(v.w, v.w ^ LL);
     if (bad) {
         chunk_slow(v, x, y, sb, c0, c1, t);
         return;
     }
-    // one byte per pixel (0xFF if nonzero): bytes 0 and 2 of each halfword mask
-    const uint32_t olo = __byte_perm(n0, n1, 0x6420), ohi = __byte_perm(n2, n3, 0x6420);
-    cache_put(c0, c1, t, x, sb | L, (uint32_t)(__popc(olo) + __popc(ohi)) >> 3, olo, ohi, y);
+    // nonzero halfwords (SWAR: bit 15 of each half set iff the half is nonzero), then
+    // one byte per pixel carrying that bit (PRMT of the high bytes)
+    auto nz = [](uint32_t q) { return ((q & 0x7fff7fffu) + 0x7fff7fffu) | q; };
+    const uint32_t olo = __byte_perm(nz(v.x), nz(v.y), 0x7531) & 0x80808080u;
+    const uint32_t ohi = __byte_perm(nz(v.z), nz(v.w), 0x7531) & 0x80808080u;
+    cache_put(c0, c1, t, x, sb | L, (uint32_t)(__popc(olo) + __popc(ohi)), olo, ohi, y);
 }
 
 __device__ __forceinline__ uint4 load_chunk(const uint16_t* __restrict__ L, size_t pitch, int W,
