@@ -12,7 +12,7 @@ namespace fxg {
 // (tools/kbench.py): 8 rows x 1 block/SM 130 us, 2 rows x 8 blocks/SM 86 us --
 // the sweep is latency-bound, occupancy (bytes in flight) is the lever.
 #ifndef FXG_SCAN_BATCH
-#define FXG_SCAN_BATCH 2
+#define FXG_SCAN_BATCH 4
 #endif
 #ifndef FXG_SCAN_MINB
 #define FXG_SCAN_MINB 8
@@ -24,7 +24,7 @@ namespace fxg {
 #define FXG_B_MINB 2  // large-ROI kernel: min CTAs per SM (register cap; 2: 7.1 -> 5.2 ms on C5-regime)
 #endif
 #ifndef FXG_SCAN_ROWS
-#define FXG_SCAN_ROWS 32
+#define FXG_SCAN_ROWS 64
 #endif
 
 constexpr int kMaxLabels = 65536;  // uint16 labels (reference image.hpp:24)

@@ -190,23 +190,12 @@ __global__ void __launch_bounds__(kScanThreads, FXG_SCAN_MINB)
                 gy += kBatch;
             }
         } else {
-            // edge tile: bounds-checked loads, software pipeline of kBatch rows
-            uint4 v[kBatch], nx[kBatch];
-#pragma unroll
-            for (int r = 0; r < kBatch; ++r) v[r] = load_chunk(L, pitch, sw, send, x, y0 + r, vec_ok);
+            // edge tile (image borders, batch slots): bounds-checked loads, one row at
+            // a time (rare; kept simple so the interior loop keeps its registers)
 #pragma unroll 1
-            for (int r0 = 0; r0 < kStripRows; r0 += kBatch) {
-                if (r0 + kBatch < kStripRows) {
-#pragma unroll
-                    for (int r = 0; r < kBatch; ++r)
-                        nx[r] = load_chunk(L, pitch, sw, send, x, y0 + r0 + kBatch + r, vec_ok);
-                }
-#pragma unroll
-                for (int r = 0; r < kBatch; ++r)
-                    chunk(v[r], gx, (uint32_t)(y0 + r0 + r) + gyo, sb, c0, c1, t);
-#pragma unroll
-                for (int r = 0; r < kBatch; ++r) v[r] = nx[r];
-            }
+            for (int r = 0; r < kStripRows; ++r)
+                chunk(load_chunk(L, pitch, sw, send, x, y0 + r, vec_ok), gx, (uint32_t)(y0 + r) + gyo, sb,
+                      c0, c1, t);
         }
         warp_flush(c0, gx, t);
         warp_flush(c1, gx, t);
