@@ -180,6 +180,23 @@ __device__ __forceinline__ uint64_t run_fill(uint64_t f, uint64_t s) {
     return g;
 }
 
+// the same on 32-bit rows (windows up to 32 wide: most S0 ROIs), half the work
+__device__ __forceinline__ uint32_t run_fill32(uint32_t f, uint32_t s) {
+    uint32_t g = s & f, p = f;
+    g |= p & (g << 1); p &= p << 1;
+    g |= p & (g << 2); p &= p << 2;
+    g |= p & (g << 4); p &= p << 4;
+    g |= p & (g << 8); p &= p << 8;
+    g |= p & (g << 16);
+    p = f;
+    g |= p & (g >> 1); p &= p >> 1;
+    g |= p & (g >> 2); p &= p >> 2;
+    g |= p & (g >> 4); p &= p >> 4;
+    g |= p & (g >> 8); p &= p >> 8;
+    g |= p & (g >> 16);
+    return g;
+}
+
 struct SJob {
     uint32_t label, x0, y0, w, h, row;
 };
@@ -1734,6 +1751,27 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
             const uint64_t f0 = ((int)lane < h) ? (~m0 & wm) : 0ull;
             const uint64_t f1 = ((int)lane + 32 < h) ? (~m1 & wm) : 0ull;
             const uint64_t side = 1ull | (1ull << (w - 1));
+            if (w <= 32) {
+                // 32-bit rows: the same flood with 32-bit fills and shuffles
+                const uint32_t g0 = (uint32_t)f0, g1 = (uint32_t)f1, sd = (uint32_t)side;
+                uint32_t x0 = run_fill32(g0, (lane == 0 || (int)lane == h - 1) ? g0 : (g0 & sd));
+                uint32_t x1 = run_fill32(g1, ((int)lane + 32 == h - 1) ? g1 : (g1 & sd));
+                for (int it = 0; it < 64 * TH; ++it) {
+                    const uint32_t up0 = __shfl_up_sync(kFull, x0, 1), dn0 = __shfl_down_sync(kFull, x0, 1);
+                    const uint32_t up1 = __shfl_up_sync(kFull, x1, 1), dn1 = __shfl_down_sync(kFull, x1, 1);
+                    const uint32_t l31 = __shfl_sync(kFull, x0, 31), f32 = __shfl_sync(kFull, x1, 0);
+                    const uint32_t a0 = (lane == 0 ? 0u : up0) | (lane == 31 ? f32 : dn0);
+                    const uint32_t a1 = (lane == 0 ? l31 : up1) | (lane == 31 ? 0u : dn1);
+                    const uint32_t n0 = run_fill32(g0, x0 | (a0 & g0));
+                    const uint32_t n1 = run_fill32(g1, x1 | (a1 & g1));
+                    const bool ch = (n0 != x0) || (n1 != x1);
+                    x0 = n0;
+                    x1 = n1;
+                    if (!__any_sync(kFull, ch)) break;
+                }
+                e0 = x0;
+                e1 = x1;
+            } else {
             e0 = run_fill(f0, (lane == 0 || (int)lane == h - 1) ? f0 : (f0 & side));
             e1 = run_fill(f1, ((int)lane + 32 == h - 1) ? f1 : (f1 & side));
             for (int it = 0; it < 64 * TH; ++it) {
@@ -1750,6 +1788,7 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
                 e0 = n0;
                 e1 = n1;
                 if (!__any_sync(kFull, ch)) break;
+            }
             }
             // holes: free cells not reached
             const bool hole = ((f0 & ~e0) | (f1 & ~e1)) != 0ull;
