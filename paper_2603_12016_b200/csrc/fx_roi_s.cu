@@ -1627,11 +1627,18 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
 #pragma unroll 1
             for (int c = 0; c < c_end; ++c) {
                 const uint4 q = row[c];
-                const uint32_t wv[4] = {q.x, q.y, q.z, q.w};
-                uint32_t bits = 0;
-#pragma unroll
-                for (int k = 0; k < 8; ++k)
-                    bits |= (uint32_t)(((wv[k >> 1] >> (16 * (k & 1))) & 0xffffu) == label) << k;
+                // 8 label compares per 16 B: XOR with the label in both halves, a SWAR
+                // nonzero test per halfword (bit 15 of each half), the halves' high
+                // bytes gathered by PRMT, then a multiply packs bit 7 of 4 bytes into
+                // a nibble (movemask)
+                const uint32_t LL = label | (label << 16);
+                auto nz = [&](uint32_t w) {
+                    const uint32_t x = w ^ LL;
+                    return ((x & 0x7fff7fffu) + 0x7fff7fffu) | x;  // bit 15 / 31: half != label
+                };
+                const uint32_t lo = ~__byte_perm(nz(q.x), nz(q.y), 0x7531) & 0x80808080u;
+                const uint32_t hi = ~__byte_perm(nz(q.z), nz(q.w), 0x7531) & 0x80808080u;
+                const uint32_t bits = ((lo * 0x00204081u) >> 28) | (((hi * 0x00204081u) >> 28) << 4);
                 const int sh = c * 8 - (int)xo;  // pixel index of this chunk's bit 0
                 m |= sh >= 0 ? ((uint64_t)bits << sh) : ((uint64_t)bits >> (-sh));
             }
