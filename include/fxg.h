@@ -269,8 +269,10 @@ int fx_multi_featurize_batch(fx_multi* m, const fx_image* images, int n, unsigne
  * a ROI belongs to the band of its first row, and an owner gathers only its
  * straddling windows' rectangles from the other bands (peer reads) before
  * featurizing its ROIs.  Output identical to fx_featurize on the whole image
- * (labels ascending).  Replaces the per-pair body of run() (engine.cpp:300-336)
- * for one image too large for one device's pass. */
+ * (labels ascending).  Bands are whole 64-row strips: an image of fewer strips
+ * than devices uses its first max(1, height / 64) devices.  Replaces the
+ * per-pair body of run() (engine.cpp:300-336) for one image too large for one
+ * device's pass. */
 int fx_multi_featurize_slide(fx_multi* m, const fx_image* image, unsigned groups,
                              const fx_texture_params* params, uint32_t* out_labels,
                              double* out_values, size_t cap_rois, size_t* n_rois);

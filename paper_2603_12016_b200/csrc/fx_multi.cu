@@ -353,18 +353,19 @@ int fx_multi_featurize_slide(fx_multi* m, const fx_image* im, unsigned groups,
     if (im->mem_kind != FX_MEM_HOST) return set_error(FX_E_ARG, "the slide is read from host memory");
     int rc = ictx_check_groups(groups);
     if (rc) return rc;
-    const int N = (int)m->ctx.size();
-    if (N > kMaxPeers) return set_error(FX_E_ARG, "at most 16 devices per slide");
+    if ((int)m->ctx.size() > kMaxPeers) return set_error(FX_E_ARG, "at most 16 devices per slide");
     const int H = im->height;
+    // bands of whole 64-row strips (the last one takes the remainder); a slide of
+    // fewer strips than devices runs on its first H / 64 devices (at least one)
+    const int N = std::min((int)m->ctx.size(), std::max(1, H / 64));
     const int nc = ictx_ncols(groups, *p);
-    // bands of whole 64-row strips (the last one takes the remainder)
     std::vector<int> y0(N), y1(N);
     for (int d = 0; d < N; ++d) {
         y0[d] = (int)((long long)H * d / N) / 64 * 64;
         y1[d] = d == N - 1 ? H : (int)((long long)H * (d + 1) / N) / 64 * 64;
     }
     for (int d = 0; d < N; ++d)
-        if (y1[d] <= y0[d]) return set_error(FX_E_ARG, "slide too short for this many devices");
+        if (y1[d] <= y0[d]) return set_error(FX_E_INTERNAL, "empty slide band");
     std::vector<int> status(N, FX_OK);
     std::vector<std::string> errs(N);
     auto parallel = [&](auto&& fn) {  // fn(d) on one host thread per device

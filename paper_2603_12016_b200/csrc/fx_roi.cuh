@@ -22,6 +22,27 @@ namespace fxg {
 __host__ __device__ constexpr uint32_t al(uint32_t v, uint32_t a) { return (v + a - 1) / a * a; }
 __host__ __device__ constexpr uint32_t mx(uint32_t a, uint32_t b) { return a > b ? a : b; }
 
+// Ellipse orientation 0.5 atan2(2b, a - c) wrapped into (-pi/2, pi/2]
+// (shape_features.cpp:176-197).  The wrap is a discontinuity: an ROI whose
+// rounded b is a tiny negative with a < c sits at atan2 = -pi + |2b / (a - c)|,
+// which rounds to -pi (wraps to +pi/2) or to the next double (stays near -pi/2)
+// by half an ulp.  CUDA's atan2 is accurate to 2 ulp, glibc's to the rounding,
+// so near +-pi the angle is rebuilt as (pi_lo - atan|y/x|) + pi_hi with one
+// final rounding, which lands on the side the reference lands on.
+__device__ __forceinline__ double ellipse_orientation(double bb, double amc) {
+    const double y = 2.0 * bb;
+    double t;
+    if (amc < 0.0 && fabs(y) < -1e-8 * amc) {
+        const double r = atan(fabs(y) / -amc);
+        t = copysign(__dadd_rn(__dsub_rn(1.2246467991473532e-16, r), 3.141592653589793), y);
+    } else {
+        t = atan2(y, amc);
+    }
+    double th = 0.5 * t;
+    if (th <= -3.141592653589793 / 2.0) th += 3.141592653589793;
+    return th;
+}
+
 // --------------------------------------------------------- debug capture --
 
 struct DebugOut {

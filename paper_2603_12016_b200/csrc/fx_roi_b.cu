@@ -641,9 +641,7 @@ __device__ void shape_b(int h, int w, int wpr, uint32_t nw, uint32_t n, long lon
                     else if (lane == 16) v = l1 > 0 ? sqrt(fmax(0.0, 1.0 - l2 / l1)) : 0.0;
                     else if (lane == 17) v = mnr > 0 ? maj / mnr : 0.0;
                     else {
-                        double th = 0.5 * atan2(2.0 * bb, amc);
-                        if (th <= -PI / 2.0) th += PI;
-                        v = th;
+                        v = ellipse_orientation(bb, amc);
                     }
                 }
             }

@@ -941,9 +941,7 @@ __global__ void __launch_bounds__(128) k_shape_serial(RoiList rl, Control* ctl, 
         o[15] = mnr;
         o[16] = l1 > 0 ? sqrt(fmax(0.0, 1.0 - l2 / l1)) : 0.0;
         o[17] = mnr > 0 ? maj / mnr : 0.0;
-        double th = 0.5 * atan2(2.0 * bb, amc);
-        if (th <= -PI / 2.0) th += PI;
-        o[18] = th;
+        o[18] = ellipse_orientation(bb, amc);
     }
     o[20] = fmx;
     o[21] = fmn;

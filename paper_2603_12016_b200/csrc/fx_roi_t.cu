@@ -494,7 +494,10 @@ __device__ void glrlm_dense(const uint16_t* lv, int w, int h, uint32_t cells, un
         const int a = (int)(wp >> 1);
         const uint32_t gl = (wp & 1u) * 32u + lane;
         uint32_t rem = gl < 64u ? sm.gl_plev[a * 64 + gl] : 0u;
-        double t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};  // t8, sum c, sum c log2 c
+        // t8, sum c, sum c log2 c (RE = (nr log2 nr - sum c log2 c) / nr: exactly 0 for
+        // a single cell, where c log2 c and nr log2 nr are the same rounded product;
+        // __dmul_rn keeps the subtraction from contracting into an FMA)
+        double t[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
         for (uint32_t k = 0; k < 32u && __any_sync(kFull, rem != 0u); ++k) {
             if (!rem) continue;
             const uint32_t word = H[(uint32_t)a * kHA + gl * 33u + k];
@@ -569,7 +572,7 @@ __device__ void glrlm_dense(const uint16_t* lv, int w, int h, uint32_t cells, un
 #pragma unroll
                 for (int o = 16; o; o >>= 1) v2[k] += __shfl_xor_sync(kFull, v2[k], o);
             const double v[16] = {t[0] / nr, t[1] / nr, s[0] / nr, s[0] / (nr * nr), s[2] / nr,
-                                  s[2] / (nr * nr), nr / np, v2[0], v2[1], logn - t[9] / nr,
+                                  s[2] / (nr * nr), nr / np, v2[0], v2[1], (__dmul_rn(nr, logn) - t[9]) / nr,
                                   t[2] / nr, t[3] / nr, t[4] / nr, t[5] / nr, t[6] / nr, t[7] / nr};
 #pragma unroll
             for (int k = 0; k < 16; ++k)

@@ -55,8 +55,14 @@ __device__ __forceinline__ uint32_t occ_last(const CacheEnt& e) {
     return e.occ_hi ? 7u - ((uint32_t)__clz(e.occ_hi) >> 3) : 3u - ((uint32_t)__clz(e.occ_lo) >> 3);
 }
 
+// an entry evicted mid-strip is not in the end-of-strip caches the warp reduces
+// for maxlab, so its label raises the slot's maxlab here (compaction skips
+// 1024-label blocks above it)
 __device__ __forceinline__ void evict(const LabelTable& t, const CacheEnt& e, uint32_t x) {
-    if (e.label) global_fold(t, e.label, e.cnt, x + occ_first(e), x + occ_last(e), e.y0, e.y1);
+    if (e.label) {
+        global_fold(t, e.label, e.cnt, x + occ_first(e), x + occ_last(e), e.y0, e.y1);
+        atomicMax(&t.maxlab[e.label >> 16], e.label & 0xffffu);
+    }
 }
 
 // fold a row's pixels of label l (pixel bytes olo/ohi, cnt of them) into the cache

@@ -16,6 +16,9 @@
     - eta_pq: s_mu / m00^(1+(p+q)/2);  Hu: s2, s2^2, s3^2, s3^2, s3^4, s2*s3^2, s3^4
       with s2 = e20+e02+2e11, s3 = e30+3e12+3e21+e03 over e = |eta| + s_eta
     - skewness / hyperskewness, and Haralick clushade / corr / infomeas1: s = 1
+    - Haralick clutend / cluprom: s = d^k / tol, d = c u (|sumave| + 1), the
+      rounding noise of mu_x + mu_y raised to the moment's power (their truth is
+      0 when every pair sums to the same level)
     - Haralick infomeas2 = sqrt(1 - exp(-2 (HXY2 - HXY))): a rounding error d of
       order c u (HXY + 1) in the entropy difference moves it by d / imc2 (by
       sqrt(d) near 0), so s = d / (tol max(imc2, sqrt(d))), c = 4096; this only
@@ -90,19 +93,31 @@ def _moment_scales(intensity, labels, roi_labels, reference_frame=True):
 def floors(columns, ref_table, intensity=None, labels=None, roi_labels=None):
     """Per-cell floor s (same shape as the table)."""
     s = np.full(ref_table.shape, 1e-300)
+    # names repeat when an angle is listed twice: walk every index, look partners
+    # up by name (a repeated angle's columns hold identical values)
     col = {c: i for i, c in enumerate(columns)}
-    for c, i in col.items():
+    for i, c in enumerate(columns):
         if c in UNIT_FLOOR:
             s[:, i] = 1.0
         if c.startswith("glcm_") and any(c.startswith("glcm_" + h + "_") for h in HARALICK_UNIT):
             s[:, i] = 1.0
-    for c, i in col.items():
+    for i, c in enumerate(columns):
         if c.startswith("glcm_infomeas2_"):
             h = col.get("glcm_entropy_" + c[len("glcm_infomeas2_"):])
             if h is None:
                 continue
             d = 4096 * 2.2e-16 * (np.abs(ref_table[:, h]) + 1.0)
             s[:, i] = d / (1e-6 * np.maximum(np.abs(ref_table[:, i]), np.sqrt(d)))
+        for k, name in ((2, "clutend"), (4, "cluprom")):
+            # sum p (i + j - mu_x - mu_y)^k: when all mass sits on one anti-diagonal
+            # the truth is 0 and both sides return the rounding noise of mu_x + mu_y
+            # (d, as for infomeas2) to the k-th power; either may be exactly 0
+            if c.startswith(f"glcm_{name}_"):
+                h = col.get("glcm_sumave_" + c[len(f"glcm_{name}_"):])
+                if h is None:
+                    continue
+                d = 4096 * 2.2e-16 * (np.abs(ref_table[:, h]) + 1.0)
+                s[:, i] = np.maximum(s[:, i], d ** k / 1e-6)
     # GLRLM/GLSZM variances sum p (x - mu)^2: the reference's rounding noise scales
     # with E[x^2] (its own lre / hglre / lae / hglze columns), not with the variance.
     # Scale columns are found by position (feature-major blocks, names may repeat

@@ -139,6 +139,41 @@ def test_label_scan_bit_exact(ctx, oracle):
         assert np.array_equal(gl, ol) and np.array_equal(gc, oc) and np.array_equal(gb, ob)
 
 
+def test_label_scan_evicted_largest_label(ctx, oracle):
+    """The largest label of a strip leaves a lane's 2-entry cache before the strip
+    ends (three labels down one 8-px column): it must still raise the slot's max
+    label, or compaction skips its 1024-label block, drops the ROI and leaves its
+    table entry to leak into the next call."""
+    for big in (1024, 40000, 65535):
+        L = np.zeros((70, 40), np.uint16)
+        L[0:3, 0:5] = big
+        L[3:5, 0:8] = 1
+        L[5:9, 0:8] = 2
+        L[20:22, 9:20] = big - 1
+        L[22, 9:20] = 3
+        L[23, 9:20] = 4
+        for _ in range(2):  # twice: a leaked entry would double the second count
+            gl, gc, gb = ctx.roi_table(np.zeros_like(L), L)
+            ol, oc, ob = oracle.roi_table(L)
+            assert np.array_equal(gl, ol) and np.array_equal(gc, oc) and np.array_equal(gb, ob)
+        check(ctx, oracle, inputs.uniform(L.shape, 1), L, GROUPS)
+
+
+@pytest.mark.parametrize("hw", [(7, 5), (3, 30), (40, 60), (90, 20), (150, 150)])
+def test_single_run_cell_entropy_is_zero(ctx, oracle, hw):
+    """Constant-intensity rectangles: at 0 and 90 degrees every run falls in one
+    (level, length) cell, so run entropy is exactly 0 in the reference; the device
+    sums must cancel exactly too (a 1-ulp residue is an infinite relative error)."""
+    h, w = hw
+    L = np.zeros((h + 4, w + 4), np.uint16)
+    L[2:2 + h, 2:2 + w] = 7
+    I = np.full(L.shape, 1234, np.uint16)
+    gl, gv = check(ctx, oracle, I, L, ["glrlm"], angles=(0, 90))
+    cols = fx.feature_columns(["glrlm"], fx.make_params("default", angles=(0, 90)))
+    for c in ("glrlm_re_0", "glrlm_re_90"):
+        assert gv[0, cols.index(c)] == 0.0
+
+
 def test_debug_histogram_edges_glcm_bit_exact(ctx, oracle):
     masks = inputs.adversarial_masks()
     masks["blobs"] = synth.blob_mask_grid(256, 220, 25, 5)

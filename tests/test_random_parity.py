@@ -1,0 +1,106 @@
+"""Randomised parity sweep: many small seeded cases, each a random mix of mask
+layout, intensity law and texture parameters, every group, device vs the oracle
+(itself pinned bit for bit to the reference).  Complements the named-shape tests
+with combinations nobody picked by hand: odd sizes, ng from 2 to 2000 (both
+texture paths and the wide kernel), asymmetric GLCMs, 1-4 angles with
+duplicates, offsets 1-3, histogram bins 1-1000.  The same cases also go
+through the batch call (8 images per call), the banded host-raster path (64-row
+bands) and the multi-context slide path (bands dealt over 3 contexts).
+"""
+import numpy as np
+import pytest
+
+import inputs
+from parity import assert_parity
+
+import paper_2603_12016_b200 as fx
+from oracle import make_params as oparams
+
+pytestmark = pytest.mark.gpu
+
+ALL = ["intensity", "shape", "moments", "glcm", "glrlm", "glszm", "ngtdm"]
+
+
+def _case(seed):
+    rng = np.random.default_rng(1000 + seed)
+    h, w = int(rng.integers(8, 160)), int(rng.integers(8, 160))
+    kind = seed % 4
+    if kind == 0:
+        L = inputs.random_blobs((h, w), int(rng.integers(1, 25)), seed=seed,
+                                max_r=int(rng.integers(2, 20)))
+    elif kind == 1:
+        L = inputs.random_labels((h, w), int(rng.integers(1, 12)), seed=seed,
+                                 p_bg=float(rng.uniform(0.1, 0.9)))
+    elif kind == 2:  # stripes and single pixels
+        L = np.zeros((h, w), np.uint16)
+        for k in range(int(rng.integers(1, 8))):
+            y = int(rng.integers(0, h))
+            L[y, : int(rng.integers(1, w + 1))] = k + 1
+        L[rng.random((h, w)) < 0.01] = 60000
+    else:  # blobs with scattered label values up to 65535
+        vals = rng.choice(np.arange(1, 65536), size=6, replace=False)
+        L = inputs.random_blobs((h, w), 12, seed=seed, max_r=15, label_values=vals)
+    law = (seed // 4) % 5
+    if law == 0:
+        I = inputs.uniform((h, w), seed)
+    elif law == 1:
+        I = np.full((h, w), int(rng.integers(0, 65536)), np.uint16)
+    elif law == 2:
+        I = rng.integers(0, int(rng.integers(2, 12)), (h, w)).astype(np.uint16)
+    elif law == 3:
+        I = inputs.per_roi_levels(L, seed, noise=int(rng.integers(0, 200)))
+    else:
+        I = np.where(rng.random((h, w)) < 0.5, 0, 65535).astype(np.uint16)
+    angles = tuple(int(a) for a in rng.choice([0, 45, 90, 135], size=int(rng.integers(1, 5))))
+    over = dict(ng=int(rng.choice([2, 3, 16, 32, 64, 65, 100, 256, 257, 500, 2000])),
+                offset=int(rng.integers(1, 4)), angles=angles,
+                symmetric=bool(rng.integers(0, 2)),
+                histogram_bins=int(rng.choice([1, 2, 7, 256, 1000])))
+    return I, L, over
+
+
+def _check(oracle, I, L, over, gl, gv):
+    gp, op = fx.make_params("default", **over), oparams("default", **over)
+    ol, ov = oracle.featurize(I, L, ALL, op)
+    assert_parity(fx.feature_columns(ALL, gp), gl, gv, ol, ov, I, L)
+
+
+@pytest.mark.parametrize("seed", range(200))
+def test_random_case(ctx, oracle, seed):
+    I, L, over = _case(seed)
+    gl, gv = ctx.featurize(I, L, ALL, fx.make_params("default", **over))
+    _check(oracle, I, L, over, gl, gv)
+
+
+@pytest.mark.parametrize("k", range(20))
+def test_random_batch(ctx, oracle, k):
+    cases = [_case(8 * k + j) for j in range(8)]
+    over = cases[0][2]
+    res = ctx.featurize_batch([(I, L) for I, L, _ in cases], ALL, fx.make_params("default", **over))
+    for (I, L, _), (gl, gv) in zip(cases, res):
+        _check(oracle, I, L, over, gl, gv)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_banded(ctx, oracle, seed):
+    I, L, over = _case(seed)
+    try:
+        ctx.set_band_rows(64)
+        gl, gv = ctx.featurize(I, L, ALL, fx.make_params("default", **over))
+    finally:
+        ctx.set_band_rows(0)
+    _check(oracle, I, L, over, gl, gv)
+
+
+@pytest.fixture(scope="module")
+def multi():
+    m = fx.Multi([0, 0, 0])
+    yield m
+    m.close()
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_slide(multi, oracle, seed):
+    I, L, over = _case(seed)
+    gl, gv = multi.featurize_slide(I, L, ALL, fx.make_params("default", **over))
+    _check(oracle, I, L, over, gl, gv)
