@@ -15,6 +15,7 @@ from parity import assert_parity
 
 import paper_2603_12016_b200 as fx
 from oracle import make_params as oparams
+from tools import synth
 
 pytestmark = pytest.mark.gpu
 
@@ -104,3 +105,52 @@ def test_random_slide(multi, oracle, seed):
     I, L, over = _case(seed)
     gl, gv = multi.featurize_slide(I, L, ALL, fx.make_params("default", **over))
     _check(oracle, I, L, over, gl, gv)
+
+
+def _large_case(seed):
+    """Bigger rasters (200-1100 px a side, up to a few hundred ROIs): every window
+    class (S0/S1/S2, the CTA path, the texture kernel), many labels per warp tile
+    of the scan, random profile and group subset."""
+    rng = np.random.default_rng(5000 + seed)
+    h, w = (int(v) for v in rng.integers(200, 1100, 2))
+    kind = seed % 3
+    if kind == 0:
+        size = int(min(h, w))
+        roi = int(rng.integers(20, 2500))
+        pitch = int(np.ceil(3.8 * 1.1 * np.sqrt(roi / np.pi))) + 5  # the generator's grid pitch
+        per_row = max(1, size // pitch)
+        L = synth.blob_mask_grid(size, roi, int(rng.integers(1, per_row * per_row + 1)),
+                                 int(rng.integers(1, 99)))
+    elif kind == 1:
+        vals = None
+        if rng.random() < 0.5:
+            vals = rng.choice(np.arange(1, 65536), size=int(rng.integers(2, 400)), replace=False)
+        L = inputs.random_blobs((h, w), int(rng.integers(20, 400)), seed=seed,
+                                max_r=int(rng.integers(3, 60)), label_values=vals)
+    else:
+        L = inputs.random_labels((h, w), int(rng.integers(2, 40)), seed=seed,
+                                 p_bg=float(rng.uniform(0.3, 0.97)))
+    law = int(rng.integers(0, 3))
+    if law == 0:
+        I = inputs.uniform(L.shape, seed)
+    elif law == 1:
+        I = inputs.per_roi_levels(L, seed, noise=int(rng.integers(0, 3000)))
+    else:
+        I = rng.integers(0, int(rng.integers(2, 70000)), L.shape).clip(0, 65535).astype(np.uint16)
+    profile = str(rng.choice(["default", "performance", "ibsi-like"]))
+    groups = [g for g in ALL if rng.random() < 0.6] or ["intensity"]
+    angles = tuple(int(a) for a in rng.choice([0, 45, 90, 135], size=int(rng.integers(1, 5))))
+    over = dict(ng=int(rng.choice([2, 8, 16, 32, 64, 100, 256, 300])),
+                offset=int(rng.integers(1, 4)), angles=angles,
+                symmetric=bool(rng.integers(0, 2)),
+                histogram_bins=int(rng.choice([1, 16, 256, 1000])))
+    return I, L, profile, groups, over
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_random_large(ctx, oracle, seed):
+    I, L, profile, groups, over = _large_case(seed)
+    gp, op = fx.make_params(profile, **over), oparams(profile, **over)
+    gl, gv = ctx.featurize(I, L, groups, gp)
+    ol, ov = oracle.featurize(I, L, groups, op)
+    assert_parity(fx.feature_columns(groups, gp), gl, gv, ol, ov, I, L)
