@@ -463,8 +463,12 @@ BLayout b_layout(const Control& h, int bins) {
     const uint32_t WPR = std::max<uint32_t>(h.l_max_wpr, 1);
     const uint32_t NMAX = (uint32_t)std::max<unsigned long long>(h.l_max_n, kS2N);
     const unsigned long long cells = std::max<unsigned long long>(h.l_max_cells, (unsigned long long)kSW * kSH);
-    const uint32_t RUNMAX =
-        (uint32_t)std::min<unsigned long long>(cells / 2 + H + 64, 64ull << 20);
+    // runs of the member mask: <= n and <= cells / 2 + H; runs of the window cells
+    // outside K: <= (runs of K) + 1 per row <= n + H.  Bounding by n as well keeps a
+    // tall, sparse window (a two-component ROI spanning a slide) from sizing every
+    // CTA's slab by its cell count (C5: 13M -> 0.2M runs, 26 -> 296 CTAs)
+    const uint32_t RUNMAX = (uint32_t)std::min<unsigned long long>(
+        std::min<unsigned long long>(cells / 2 + H + 64, (unsigned long long)NMAX + H + 64), 64ull << 20);
     return make_blayout(H, WPR, NMAX, RUNMAX, (uint32_t)std::max(bins, 2), cells);
 }
 

@@ -82,6 +82,11 @@ constexpr int kS2N = 4096;  // = kSW*kSH
 constexpr int kS1Runs = 512;
 constexpr int kS2Runs = 2176;  // >= worst case (33 free runs x 64 rows + 64)
 
+// k_roi_b takes the windows above this many cells first (one sweep of the L list),
+// then the rest: a few slide-tall windows picked up last would otherwise run alone
+// at the end of the launch
+constexpr unsigned long long kBigCells = 1ull << 20;
+
 // Device-side control block, zeroed per featurize call.
 struct Control {
     uint32_t n_rois;
@@ -97,7 +102,7 @@ struct Control {
     unsigned long long mom_alloc;    // moments: pixels staged so far (bump allocator)
     unsigned long long int_alloc;    // intensity: sorted values staged so far
     uint32_t w_next;                 // wide texture kernel (ng > 256) work counter
-    uint32_t pad0_;
+    uint32_t b_next_big;             // k_roi_b: first sweep, windows of > kBigCells cells
     // sticky across the sub-batches of one API call: compact_stage clears only the
     // fields above (offsetof(Control, error) bytes); the call's first stage clears all
     uint32_t error;                  // bit flags, see kErr*

@@ -696,17 +696,34 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
     const bool want_shape = cfg.col_shape >= 0;
 
     BT_DECL
-    // ---- membership words (warp per 64-column word) and popcounts
-    for (uint32_t wi = wid; wi < nw; wi += kBW) {
-        const int y = (int)(wi / wpr), k = (int)(wi % wpr);
-        const uint16_t* row = img.L + (size_t)(y0 + y) * img.pitch + x0;
-        const int xa = k * 64 + (int)lane, xb = xa + 32;
-        const unsigned lo = __ballot_sync(kFull, xa < w && row[xa] == label);
-        const unsigned hi = __ballot_sync(kFull, xb < w && row[xb] == label);
-        if (lane == 0) {
-            const uint64_t m = (uint64_t)lo | ((uint64_t)hi << 32);
-            S.rowmask[wi] = m;
-            S.wordoff[wi] = __popcll(m);
+    // ---- membership words (warp per 64-column word) and popcounts; a warp takes
+    // kBU consecutive words per step and issues all their loads before the ballots
+    // (one word per step left the loop latency-bound: a slide-tall window's 0.5M
+    // words took ~20 ms on one CTA)
+    constexpr uint32_t kBU = 8;
+    for (uint32_t wb = wid * kBU; wb < nw; wb += kBW * kBU) {
+        uint32_t va[kBU], vb[kBU];
+#pragma unroll
+        for (uint32_t u = 0; u < kBU; ++u) {
+            const uint32_t wi = wb + u;
+            va[u] = vb[u] = 0u;  // never equal to a label (labels are >= 1)
+            if (wi < nw) {
+                const int y = (int)(wi / wpr), k = (int)(wi % wpr);
+                const uint16_t* row = img.L + (size_t)(y0 + y) * img.pitch + x0;
+                const int xa = k * 64 + (int)lane, xb = xa + 32;
+                if (xa < w) va[u] = row[xa];
+                if (xb < w) vb[u] = row[xb];
+            }
+        }
+#pragma unroll
+        for (uint32_t u = 0; u < kBU; ++u) {
+            const unsigned lo = __ballot_sync(kFull, va[u] == label);
+            const unsigned hi = __ballot_sync(kFull, vb[u] == label);
+            if (lane == 0 && wb + u < nw) {
+                const uint64_t m = (uint64_t)lo | ((uint64_t)hi << 32);
+                S.rowmask[wb + u] = m;
+                S.wordoff[wb + u] = __popcll(m);
+            }
         }
     }
     for (int i = tid; i < 256; i += kBT) sm.coarse[i] = 0u;
@@ -718,19 +735,34 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
     // ---- pixel list (row-major), intensities, exact integer sums, value histogram
     unsigned long long sS = 0, sQ = 0, sX = 0, sY = 0, sXI = 0, sYI = 0;
     uint32_t vlo = 0xffffu, vhi = 0u;
-    for (uint32_t wi = wid; wi < nw; wi += kBW) {
-        const uint64_t m = S.rowmask[wi];
+    // (kBP words per warp step, their intensity loads issued together)
+    constexpr uint32_t kBP = 4;
+    for (uint32_t wb = wid * kBP; wb < nw; wb += kBW * kBP) {
+      uint64_t mw[kBP];
+      uint32_t vv[kBP][2];
+#pragma unroll
+      for (uint32_t u = 0; u < kBP; ++u) {
+        const uint32_t wi = wb + u;
+        mw[u] = wi < nw ? S.rowmask[wi] : 0ull;
+        const uint16_t* Irow = img.I + (size_t)(y0 + wi / wpr) * img.pitch + x0 + (wi % wpr) * 64;
+#pragma unroll
+        for (int hf = 0; hf < 2; ++hf)
+            vv[u][hf] = ((mw[u] >> ((int)lane + 32 * hf)) & 1ull) ? Irow[(int)lane + 32 * hf] : 0u;
+      }
+#pragma unroll
+      for (uint32_t u = 0; u < kBP; ++u) {
+        const uint64_t m = mw[u];
         if (!m) continue;
+        const uint32_t wi = wb + u;
         const uint32_t base = S.wordoff[wi];
         const uint32_t y = wi / wpr, k = wi % wpr;
-        const uint16_t* Irow = img.I + (size_t)(y0 + y) * img.pitch + x0;
 #pragma unroll
         for (int hf = 0; hf < 2; ++hf) {
             const int bit = (int)lane + 32 * hf;
             if (!((m >> bit) & 1ull)) continue;
             const uint32_t pos = base + __popcll(m & ((1ull << bit) - 1ull));
             const uint32_t x = k * 64 + bit;
-            const uint32_t v = Irow[x];
+            const uint32_t v = vv[u][hf];
             S.xy[pos] = x | (y << 16);
             S.vals[pos] = (uint16_t)v;
             sS += v;
@@ -746,6 +778,7 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
                 atomicAdd(&sm.coarse[v >> 8], 1u);
             }
         }
+      }
     }
     sS = block_all(sS, sm.u64s, OpAdd());
     sQ = block_all(sQ, sm.u64s, OpAdd());
@@ -1290,14 +1323,21 @@ __global__ void __launch_bounds__(kBT, FXG_B_MINB) k_roi_b(DevImage img, RoiList
     const BSlab S = bslab(scratch + (size_t)blockIdx.x * B.bytes, B);
     const uint32_t nl = ctl->class_count[kClassL];
     const uint32_t total = nl + ctl->overflow_count;  // S kernels have finished
-    for (;;) {
-        if (threadIdx.x == 0) sm.job = atomicAdd(&ctl->class_next[kClassL], 1u);
+    // sweep 0 claims the L list for windows of > kBigCells cells only; sweep 1 takes
+    // every other job (longest jobs first, so none starts at the end of the launch)
+    for (int sweep = 0; sweep < 2;) {
+        if (threadIdx.x == 0) sm.job = atomicAdd(sweep ? &ctl->class_next[kClassL] : &ctl->b_next_big, 1u);
         __syncthreads();
         const uint32_t idx = sm.job;
         __syncthreads();
-        if (idx >= total) break;
+        if (idx >= (sweep ? total : nl)) {
+            ++sweep;
+            continue;
+        }
         const uint32_t r = idx < nl ? rl.cls_list[kClassL][idx] : rl.overflow[idx - nl];
         const uint32_t w = rl.w[r], h = rl.h[r];
+        const bool big = idx < nl && (unsigned long long)w * h > kBigCells;
+        if (big != (sweep == 0)) continue;
         if (h > B.H || (w + 63) / 64 > B.WPR || rl.n[r] > (unsigned long long)B.NMAX) {
             if (threadIdx.x == 0) atomicOr(&ctl->error, kErrCapacity);
             continue;

@@ -446,7 +446,7 @@ __global__ void k_band_scatter(RoiList rl, const Control* ctl, BandPlan bp, cons
         c.overflow_count = c.overflow_next = 0;
         c.t_next[0] = c.t_next[1] = 0;
         c.mom_alloc = c.int_alloc = 0;
-        c.w_next = 0;
+        c.w_next = c.b_next_big = 0;
         c.error = 0;
         band_ctl[b] = c;
     }

@@ -28,7 +28,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
 
-def band_rasters(torch, dev, tile_lab, per, S, T, y0, y1, chunk=1024):
+def band_rasters(torch, dev, tile_lab, per, S, T, y0, y1, chunk=1024, roll=None):
     """Rows [y0, y1) of the rolled composition: labels and hashed intensities
     (built in row chunks to bound the int64 temporaries)."""
     k = S // T
@@ -39,7 +39,7 @@ def band_rasters(torch, dev, tile_lab, per, S, T, y0, y1, chunk=1024):
     for c0 in range(y0, y1, chunk):
         c1 = min(y1, c0 + chunk)
         rows = torch.arange(c0, c1, device=dev, dtype=torch.int64)
-        src = (rows - T // 2) % S                  # row of the unrolled composition
+        src = (rows - (T // 2 if roll is None else roll)) % S  # row of the unrolled composition
         by, ty = src // T, src % T                 # tile block row, row inside the tile
         lab = tile_lab[ty][:, tx]
         off = (by[:, None] * k + bx[None, :]) * per
@@ -59,6 +59,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=1)
     ap.add_argument("--groups", default="intensity,moments,glcm")
     ap.add_argument("--sharded", action="store_true")
+    ap.add_argument("--roll", type=int, default=None, help="rows to roll (default tile/2)")
+    ap.add_argument("--phase", action="store_true", help="print k_roi_b phase clocks "
+                    "(FXG_LIB pointing at a -DFXG_PHASE_TIMING build)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -83,7 +86,7 @@ def main():
     tile_lab = torch.from_numpy(tile.astype(np.int64)).to(dev)
     bands = shard.band_plan(S, world) if args.sharded else [(0, S)]
     y0, y1 = bands[rank]
-    I, L = band_rasters(torch, dev, tile_lab, per, S, T, y0, y1)
+    I, L = band_rasters(torch, dev, tile_lab, per, S, T, y0, y1, roll=args.roll)
     del tile_lab
     torch.cuda.synchronize()
     gen_s = time.time() - t0
@@ -117,6 +120,16 @@ def main():
         torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / args.steps
     kt = ctx.kernel_times()
+    if args.phase:
+        import ctypes as C
+        from paper_2603_12016_b200 import fxg
+        buf = (C.c_ulonglong * 16)()
+        assert fxg.lib().fx_debug_phase_clocks(buf, 16, 1) == 0, "not a phase-timing build"
+        names = ["words+scan", "pixels", "int hist/order", "edge+int out", "moments",
+                 "glcm levels", "glcm angles"]
+        tot = sum(buf[9:16])
+        print("k_roi_b phases (thread 0, all steps):", ", ".join(
+            f"{nm} {100 * buf[9 + k] / max(tot, 1):.1f}%" for k, nm in enumerate(names)), file=sys.stderr)
     n_all = n_own
     if args.sharded:
         t = torch.tensor([ms], device=dev, dtype=torch.float64)
