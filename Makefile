@@ -12,7 +12,7 @@ NVFLAGS  := -O3 -std=c++17 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -I$(SRC)
 CXXFLAGS := -O3 -std=c++20 -fPIC -Wall -Wextra -Iinclude -I$(SRC) -I/usr/local/cuda/include
 
 CU_SRCS  := $(SRC)/fx_scan.cu $(SRC)/fx_roi_s.cu $(SRC)/fx_roi_b.cu $(SRC)/fx_roi_t.cu $(SRC)/fx_capi.cu $(SRC)/fx_multi.cu $(SRC)/fx_wide.cu
-CXX_SRCS := $(SRC)/fx_host.cpp $(SRC)/engine.cpp
+CXX_SRCS := $(SRC)/fx_host.cpp $(SRC)/engine.cpp $(SRC)/fx_pack.cpp
 CU_OBJS  := $(patsubst $(SRC)/%.cu,$(OBJ)/%.o,$(CU_SRCS))
 CXX_OBJS := $(patsubst $(SRC)/%.cpp,$(OBJ)/%.o,$(CXX_SRCS))
 HDRS     := $(wildcard $(SRC)/*.cuh) $(wildcard $(SRC)/*.hpp) $(wildcard include/*.h) \

@@ -344,6 +344,19 @@ def main():
     barrier()
     t_e2e = max_over_ranks(e0.elapsed_time(e1) / 1e3)
     assert int(h_ol[0]) >= 1
+    h2d_b, d2h_b = ctx.last_transfer()
+    # the same call with raw rows over PCIe (no host packing), for reference
+    ctx.set_packing(False)
+    step_e2e()
+    raw_h2d, _ = ctx.last_transfer()
+    barrier()
+    e0.record(stream)
+    for _ in range(e2e_steps):
+        step_e2e()
+    e1.record(stream)
+    barrier()
+    t_e2e_raw = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    ctx.set_packing(True)
 
     if rank != 0:
         if dist is not None:
@@ -389,9 +402,13 @@ def main():
         "rois_per_s": round(world * n_rois * args.steps / t_dev, 1),
         "featurize_hbm_gbs": round(call_gbs, 1),
         "e2e": {"value": round(e2e_value, 2), "unit": UNIT,
-                "h2d_bytes_per_step": int(2 * h * w * 2),
-                "d2h_bytes_per_step": int(n_rois * ncols * 8 + n_rois * 4),
-                "steps": e2e_steps},
+                "h2d_bytes_per_step": int(h2d_b), "d2h_bytes_per_step": int(d2h_b),
+                "steps": e2e_steps,
+                "path": "host rasters packed by host threads (label change points + "
+                        "labelled intensities), unpacked on the device"
+                        if h2d_b < 2 * h * w * 2 else "raw row bands",
+                "raw_rows": {"value": round(world * mp_step * e2e_steps / t_e2e_raw, 2),
+                             "h2d_bytes_per_step": int(raw_h2d)}},
         "gpu_launches": int(launches),
         "kernels": kernels,
         "kernels_note": f"per-kernel split from a separate {bd_steps}-step pass with every "

@@ -117,6 +117,15 @@ int fx_ctx_set_stream(fx_ctx* ctx, void* cuda_stream);
  * >= 2048 rows and >= 8 Mpx, else unbanded), < 0 = never banded.  Results are
  * identical either way. */
 int fx_ctx_set_band_rows(fx_ctx* ctx, int rows);
+/* Banded host rasters cross PCIe packed (default on when the host has AVX-512
+ * VBMI2 and width <= 65536): per row the label change points and only the
+ * intensities of labelled pixels, packed by a pool of host threads and unpacked
+ * on the device (the features never read an unlabelled pixel's intensity).
+ * 0 sends raw rows.  Results are identical either way. */
+int fx_ctx_set_packing(fx_ctx* ctx, int on);
+/* Bytes the last fx_featurize call on host rasters moved host-to-device and
+ * device-to-host (0 for device-resident calls). */
+int fx_ctx_last_transfer(const fx_ctx* ctx, uint64_t* h2d_bytes, uint64_t* d2h_bytes);
 /* Kernel launches issued by this ctx since creation (evidence counter). */
 uint64_t fx_ctx_launch_count(const fx_ctx* ctx);
 /* Optional per-kernel CUDA-event timing on the launching stream. */

@@ -17,11 +17,13 @@
 #include <cstring>
 #include <functional>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
 #include "fx_dev.cuh"
 #include "fx_host.hpp"
+#include "fx_pack.hpp"
 #include "fx_roi.cuh"
 #include "fxg.h"
 
@@ -41,6 +43,9 @@ __global__ void k_cloud_gather(DevImage img, RoiList rl, const Control* ctl,
                                uint16_t* vs);
 __global__ void k_band_count(RoiList rl, const Control* ctl, BandPlan bp, uint32_t* cnt,
                              uint32_t* first);
+__global__ void k_unpack_labels(const uint8_t* region, int rows, int W, uint16_t* L, size_t P);
+__global__ void k_unpack_intensity(const uint8_t* region, int rows, int W, const uint16_t* L,
+                                   uint16_t* I, size_t P);
 __global__ void k_band_scatter(RoiList rl, const Control* ctl, BandPlan bp, const uint32_t* cnt,
                                uint32_t* cursor, uint32_t* seg, Control* band_ctl);
 cudaError_t roi_s_setup(int* occ /* [3][3]: class x GlcmMode */);
@@ -89,6 +94,7 @@ struct fx_ctx {
     cudaStream_t own_stream = nullptr, stream = nullptr, side = nullptr;
     cudaStream_t copy = nullptr;  // batch staging (H2D of the next sub-batch)
     cudaStream_t d2h = nullptr;   // banded host path: feature rows back while bands compute
+    cudaStream_t copy2 = nullptr; // packed host path: packed blocks next to the raw ones
     // banded host path (featurize_banded): per-band events and pinned host staging
     std::vector<cudaEvent_t> ev_band;  // 3 per band: labels in, intensities in, rows done
     uint32_t* d_band = nullptr;        // [cnt kMaxBands*4][cursor kMaxBands*4][first kMaxBands]
@@ -177,6 +183,17 @@ struct fx_ctx {
     bool no_tma = false;
     bool no_stage = false;  // FXG_NO_STAGE=1: in-warp intensity / moments (tests)
     int band_rows = 0;      // FXG_BAND_ROWS: banded host path band height (0 auto, <0 off)
+    // packed host rows (fx_pack.hpp): worker pool, pinned + device block staging,
+    // the host's nonzero masks; FXG_PACK=0 / fx_ctx_set_packing(0) sends raw rows
+    bool packing = true;
+    int pack_raw_pct = 20;  // FXG_PACK_RAW: % of row blocks sent raw (DMA next to the packers)
+    std::unique_ptr<PackPool> pool;
+    uint8_t* h_pack = nullptr;
+    uint8_t* d_pack = nullptr;
+    size_t pack_bytes = 0;
+    std::vector<uint32_t> pack_mask;
+    // bytes moved by the last call (host paths)
+    uint64_t h2d_bytes = 0, d2h_bytes = 0;
 };
 
 namespace {
@@ -1011,6 +1028,323 @@ BandPlan band_plan(int band_rows, int h) {
     return bp;
 }
 
+// Row blocks of the packed host path: each band cut into pieces of at most
+// kPackRows rows (a block never straddles a band, so a band's intensities are
+// complete once its last block has been unpacked).
+constexpr int kPackRows = 256;
+struct PackBlock {
+    int y0, rows, band;
+    bool raw;  // sent raw by DMA (both rasters) while the workers pack the others
+    size_t lab_off, int_off;  // region offsets in the staging buffers
+    size_t lab_cap_seg;
+};
+
+bool packing_usable(const fx_ctx* c, const fx_image* im) {
+    return c->packing && pack_isa() == 2 && im->width <= 65536;
+}
+
+// Host rasters as packed row blocks (fx_pack.hpp): the pool's workers pack every
+// block's labels (change points + nonzero masks), then every block's labelled
+// intensities; this thread ships each block as soon as it is packed, unpacks it
+// on the device, scans the whole label raster after the last label block,
+// compacts, and runs each band's ROIs once that band's intensities are unpacked
+// (the per-band ROI work and row readback of featurize_banded).  A block whose
+// labels do not pack into half their raw size goes raw (both rasters).
+int featurize_packed(fx_ctx* c, const fx_image* im, int band_rows, unsigned groups,
+                     const fx_texture_params& p, uint32_t* out_labels, double* out_values,
+                     size_t cap_rois, size_t* n_rois) {
+    const int W = im->width, H = im->height;
+    const BandPlan bp = band_plan(band_rows, H);
+    const int nb = (int)bp.nb;
+    int rc = ensure_img(c, W, H);
+    if (!rc) rc = ensure_band(c, nb);
+    if (rc) return rc;
+    cudaStream_t s = c->stream;
+    const size_t P = c->img_pitch, spe = im->pitch ? im->pitch : (size_t)W, sp = spe * 2;
+    DevImage d;
+    d.I = c->d_img;
+    d.L = c->d_img + P * c->img_rows_cap;
+    d.w = W;
+    d.h = H;
+    d.pitch = P;
+    d.ox = im->origin_x;
+    d.oy = im->origin_y;
+    // blocks and their staging regions
+    std::vector<PackBlock> blk;
+    size_t bytes = 0;
+    for (int b = 0; b < nb; ++b) {
+        const int ya = (int)bp.y0_of((uint32_t)b), yb = b + 1 < nb ? (int)bp.y0_of((uint32_t)b + 1) : H;
+        for (int y = ya; y < yb; y += kPackRows) {
+            PackBlock k;
+            k.y0 = y;
+            k.rows = std::min(kPackRows, yb - y);
+            k.band = b;
+            k.raw = false;
+            k.lab_cap_seg = (size_t)k.rows * (size_t)W / 4;  // half the raw label bytes
+            k.lab_off = bytes;
+            bytes += pk_align16(pk_lab_bytes(k.rows, W, k.lab_cap_seg));
+            k.int_off = bytes;
+            bytes += pk_align16(pk_int_bytes(k.rows, W, (size_t)k.rows * (size_t)W));
+            blk.push_back(k);
+        }
+    }
+    const int NB = (int)blk.size();
+    // The host's memory bandwidth bounds the packers (~2.6 B read per pixel) and
+    // PCIe the raw DMA (4 B per pixel): a share of the blocks goes raw so both run
+    // from the start (spread evenly: block j raw when floor((j+1) r) > floor(j r)).
+    for (int q = 0; q < NB; ++q)
+        blk[q].raw = (q + 1) * c->pack_raw_pct / 100 > q * c->pack_raw_pct / 100;
+    if (bytes > c->pack_bytes) {
+        cudaFreeHost(c->h_pack);
+        cudaFree(c->d_pack);
+        c->h_pack = nullptr;
+        c->d_pack = nullptr;
+        c->pack_bytes = 0;
+        CK(cudaMallocHost(&c->h_pack, bytes));
+        CK(cudaMalloc(&c->d_pack, bytes));
+        c->pack_bytes = bytes;
+    }
+    const size_t mp = ((size_t)W + 31) / 32;  // mask words per row
+    if (c->pack_mask.size() < mp * (size_t)H) c->pack_mask.resize(mp * (size_t)H);
+    if (!c->pool) {
+        const int hw = (int)std::thread::hardware_concurrency();
+        c->pool = std::make_unique<PackPool>(std::max(1, std::min(hw - 1, 15)));
+    }
+    std::vector<size_t> lab_bytes(NB, 0), int_bytes(NB, 0);
+    // FXG_PACK_TRACE=1: host timeline of the call on stderr (tools)
+    static const bool trace = getenv("FXG_PACK_TRACE") && atoi(getenv("FXG_PACK_TRACE"));
+    const auto t_start = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what, int k) {
+        if (trace)
+            fprintf(stderr, "pack-trace %8.3f ms %s %d\n",
+                    std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(),
+                    what, k);
+    };
+    uint8_t* hp = c->h_pack;
+    uint32_t* mask = c->pack_mask.data();
+    PackPool* pool = c->pool.get();
+    // the previous call's copies out of the staging buffers are complete (its
+    // finish() synchronised every stream)
+    pool->start(2 * NB, [&, pool](int t) {
+        const PackBlock& k = blk[t < NB ? t : t - NB];
+        uint32_t* m = mask + (size_t)k.y0 * mp;
+        if (k.raw) return;
+        if (t < NB) {
+            lab_bytes[t] = pack_labels(im->labels, spe, W, k.y0, k.y0 + k.rows, hp + k.lab_off,
+                                       k.lab_cap_seg, m, mp);
+        } else {
+            const int j = t - NB;
+            while (!pool->done(j)) std::this_thread::yield();  // claimed earlier, running
+            if (lab_bytes[j])
+                int_bytes[j] = pack_intensity(im->intensity, spe, W, k.y0, k.y0 + k.rows, m, mp,
+                                              hp + k.int_off);
+        }
+    });
+    // the workers read the caller's rasters and write the staging buffers: every
+    // return waits for them
+    struct Join {
+        PackPool* p;
+        ~Join() { p->wait(); }
+    } join{pool};
+    auto spin = [&](int t) {
+        while (!pool->done(t)) std::this_thread::yield();
+    };
+    // events: [nb+b] band b's rows final (as featurize_banded), [2nb+j] label block
+    // j shipped, [2nb+NB+j] intensity block j shipped
+    while (c->ev_band.size() < (size_t)(2 * nb + 2 * NB)) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_band.push_back(e);
+    }
+    cudaEvent_t* ev = c->ev_band.data();
+    CK(cudaEventRecord(c->ev_compact, s));
+    CK(cudaStreamWaitEvent(c->copy, c->ev_compact, 0));
+    c->h2d_bytes = c->d2h_bytes = 0;
+    // trace: device timeline (timing events on s / d2h, read at the end)
+    std::vector<std::pair<std::string, cudaEvent_t>> tev;
+    auto dmark = [&](const std::string& what, cudaStream_t st) {
+        if (!trace) return;
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        cudaEventRecord(e, st);
+        tev.emplace_back(what, e);
+    };
+    dmark("start", s);
+    auto raw_rows = [&](const uint16_t* src, uint16_t* dst, const PackBlock& k) -> int {
+        CK(cudaMemcpy2DAsync(dst + (size_t)k.y0 * P, P * 2, src + (size_t)k.y0 * spe, sp, (size_t)W * 2,
+                             (size_t)k.rows, cudaMemcpyHostToDevice, c->copy));
+        c->h2d_bytes += (size_t)W * 2 * (size_t)k.rows;
+        return FX_OK;
+    };
+    // 0. the raw blocks' labels, then their intensities, on the copy stream at once
+    CK(cudaStreamWaitEvent(c->copy2, c->ev_compact, 0));
+    for (int pass = 0; pass < 2; ++pass)
+        for (int j = 0; j < NB; ++j) {
+            if (!blk[j].raw) continue;
+            if ((rc = raw_rows(pass ? im->intensity : im->labels, const_cast<uint16_t*>(pass ? d.I : d.L),
+                               blk[j])))
+                return rc;
+            CK(cudaEventRecord(ev[2 * nb + pass * NB + j], c->copy));
+        }
+    // 1. label blocks: ship the packed ones as they are done (copy2), unpack
+    for (int j = 0; j < NB; ++j) {
+        const PackBlock& k = blk[j];
+        cudaEvent_t e = ev[2 * nb + j];
+        if (!k.raw) {
+            spin(j);
+            mark("labels packed", j);
+            if (lab_bytes[j]) {
+                CK(cudaMemcpyAsync(c->d_pack + k.lab_off, hp + k.lab_off, lab_bytes[j],
+                                   cudaMemcpyHostToDevice, c->copy2));
+                c->h2d_bytes += lab_bytes[j];
+                CK(cudaEventRecord(e, c->copy2));
+            } else {  // did not pack: raw after all (copy stream, behind the raw blocks)
+                if ((rc = raw_rows(im->labels, const_cast<uint16_t*>(d.L), k))) return rc;
+                CK(cudaEventRecord(e, c->copy));
+            }
+        }
+        CK(cudaStreamWaitEvent(s, e, 0));
+        if (lab_bytes[j]) {
+            Launch l(c, "k_unpack_labels");
+            k_unpack_labels<<<dim3(pk_tiles(W), k.rows), 256, 0, s>>>(c->d_pack + k.lab_off, k.rows, W,
+                                                           const_cast<uint16_t*>(d.L) + (size_t)k.y0 * P, P);
+        }
+    }
+    CK(cudaGetLastError());
+    dmark("labels unpacked", s);
+    rc = scan_stage(c, d, single_map(d), true);
+    if (rc) return rc;
+    FeatCfg cfg;
+    rc = prepare_cfg(c, d, groups, p, nullptr, &cfg);
+    if (rc) return rc;
+    const int vrc = validate_texture(groups, p);
+    const FeatCfg wcfg = cfg;
+    const bool wide = vrc == FX_OK && wide_texture(cfg);
+    if (wide) cfg = core_cfg(cfg);
+    rc = compact_stage(c, single_map(d), 0u, 0xffffffffu, cap_rois, true);
+    if (rc) return rc;
+    RoiList rl = roi_list(c);
+    uint32_t* cnt = c->d_band;
+    uint32_t* cursor = cnt + kMaxBands * kNumClasses;
+    uint32_t* first = cursor + kMaxBands * kNumClasses;
+    CK(cudaMemsetAsync(cnt, 0, 2 * kMaxBands * kNumClasses * sizeof(uint32_t), s));
+    CK(cudaMemsetAsync(first, 0xff, kMaxBands * sizeof(uint32_t), s));
+    {
+        const int grid = 2 * c->sm_count;
+        Launch l(c, "k_band_count");
+        k_band_count<<<grid, 256, 0, s>>>(rl, c->d_ctl, bp, cnt, first);
+        Launch l2(c, "k_band_scatter");
+        k_band_scatter<<<grid, 256, 0, s>>>(rl, c->d_ctl, bp, cnt, cursor, c->d_band_seg, c->d_band_ctl);
+    }
+    CK(cudaGetLastError());
+    CK(cudaMemcpyAsync(c->h_band, c->d_band, (size_t)kMaxBands * (2 * kNumClasses + 1) * sizeof(uint32_t),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+    CK(cudaEventRecord(c->ev_stats, s));
+    mark("compaction queued", 0);
+    CK(cudaStreamSynchronize(s));
+    mark("compaction done", 0);
+    const Control hc = *c->h_ctl;
+    const size_t n = hc.n_rois;
+    *n_rois = n;
+    if (vrc != FX_OK) return n ? vrc : FX_OK;
+    if (hc.error & kErrWindow)
+        return set_error(FX_E_ARG, "an owned ROI window extends beyond the image (halo too small)");
+    if (n > cap_rois)
+        return set_error(FX_E_CAPACITY, "output capacity " + std::to_string(cap_rois) + " < " +
+                                            std::to_string(n) + " ROIs");
+    if (n == 0) return FX_OK;
+    if (out_labels) {
+        CK(cudaStreamWaitEvent(c->d2h, c->ev_stats, 0));
+        CK(cudaMemcpyAsync(out_labels, rl.label, n * 4, cudaMemcpyDeviceToHost, c->d2h));
+        c->d2h_bytes += n * 4;
+    }
+    const uint32_t* h_cnt = c->h_band;
+    const uint32_t* h_first = c->h_band + 2 * kMaxBands * kNumClasses;
+    std::vector<uint32_t> final_after(nb);
+    uint32_t later = (uint32_t)n;
+    for (int b = nb - 1; b >= 0; --b) {
+        final_after[b] = later;
+        later = std::min(later, h_first[b]);
+    }
+    const size_t ncols = (size_t)cfg.ncols;
+    TmaSet tm;
+    make_tmaps(c, d, &tm);
+    size_t rows_out = 0, seg_at = 0;
+    int j = 0;
+    for (int b = 0; b < nb; ++b) {
+        // 2. this band's intensity blocks: ship, unpack
+        for (; j < NB && blk[j].band == b; ++j) {
+            const PackBlock& k = blk[j];
+            cudaEvent_t e = ev[2 * nb + NB + j];
+            if (!k.raw) {
+                spin(NB + j);
+                mark("intensity packed", j);
+                if (int_bytes[j]) {
+                    CK(cudaMemcpyAsync(c->d_pack + k.int_off, hp + k.int_off, int_bytes[j],
+                                       cudaMemcpyHostToDevice, c->copy2));
+                    c->h2d_bytes += int_bytes[j];
+                    CK(cudaEventRecord(e, c->copy2));
+                } else {
+                    if ((rc = raw_rows(im->intensity, const_cast<uint16_t*>(d.I), k))) return rc;
+                    CK(cudaEventRecord(e, c->copy));
+                }
+            }
+            CK(cudaStreamWaitEvent(s, e, 0));
+            if (int_bytes[j]) {
+                Launch l(c, "k_unpack_intensity");
+                k_unpack_intensity<<<dim3(pk_tiles(W), k.rows), 256, 0, s>>>(
+                    c->d_pack + k.int_off, k.rows, W, d.L + (size_t)k.y0 * P,
+                    const_cast<uint16_t*>(d.I) + (size_t)k.y0 * P, P);
+            }
+        }
+        CK(cudaGetLastError());
+        dmark("band " + std::to_string(b) + " intensities unpacked", s);
+        Control bc = hc;
+        RoiList rb = rl;
+        uint64_t band_rois = 0;
+        for (int q = 0; q < kNumClasses; ++q) {
+            bc.class_count[q] = h_cnt[b * kNumClasses + q];
+            rb.cls_list[q] = c->d_band_seg + seg_at;
+            seg_at += bc.class_count[q];
+            band_rois += bc.class_count[q];
+        }
+        if (band_rois) {
+            rc = roi_work(c, d, cfg, bc, tm, c->d_out, nullptr, kClassS0, c->d_band_ctl + b, rb,
+                          wide ? &wcfg : nullptr, false);
+            if (rc) return rc;
+        }
+        const size_t upto = std::max<size_t>(rows_out, b == nb - 1 ? n : final_after[b]);
+        if (upto > rows_out) {
+            CK(cudaEventRecord(ev[nb + b], s));
+            CK(cudaStreamWaitEvent(c->d2h, ev[nb + b], 0));
+            CK(cudaMemcpyAsync(out_values + rows_out * ncols, c->d_out + rows_out * ncols,
+                               (upto - rows_out) * ncols * sizeof(double), cudaMemcpyDeviceToHost,
+                               c->d2h));
+            c->d2h_bytes += (upto - rows_out) * ncols * sizeof(double);
+            rows_out = upto;
+            dmark("band " + std::to_string(b) + " rows back", c->d2h);
+        }
+    }
+    CK(cudaMemcpyAsync(c->h_band_ctl, c->d_band_ctl, (size_t)nb * sizeof(Control),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    mark("compute done", 0);
+    for (int b = 0; b < nb; ++b) c->h_ctl->error |= c->h_band_ctl[b].error;
+    CK(cudaStreamSynchronize(c->d2h));
+    mark("d2h done", 0);
+    if (trace) {
+        for (auto& te : tev) {
+            float ms = 0;
+            cudaEventElapsedTime(&ms, tev[0].second, te.second);
+            fprintf(stderr, "pack-trace device %8.3f ms %s\n", ms, te.first.c_str());
+        }
+        for (auto& te : tev) cudaEventDestroy(te.second);
+    }
+    return FX_OK;
+}
+
 int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned groups,
                      const fx_texture_params& p, uint32_t* out_labels, double* out_values,
                      size_t cap_rois, size_t* n_rois) {
@@ -1034,6 +1368,7 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     // the copy stream starts after this stream's earlier work (staging buffer reuse)
     CK(cudaEventRecord(c->ev_compact, s));
     CK(cudaStreamWaitEvent(c->copy, c->ev_compact, 0));
+    c->h2d_bytes = c->d2h_bytes = 0;
     auto rows_of = [&](int b) {
         const int y0 = (int)bp.y0_of((uint32_t)b);
         return (b + 1 < nb ? (int)bp.y0_of((uint32_t)b + 1) : H) - y0;
@@ -1048,6 +1383,7 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
             else
                 CK(cudaMemcpy2DAsync(dst, P * 2, src, sp, (size_t)W * 2, (size_t)rows_of(b),
                                      cudaMemcpyHostToDevice, c->copy));
+            c->h2d_bytes += (size_t)W * 2 * (size_t)rows_of(b);
             CK(cudaEventRecord(ev[pass * nb + b], c->copy));
         }
     // label scan band by band, in global coordinates
@@ -1109,6 +1445,7 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     if (out_labels) {
         CK(cudaStreamWaitEvent(c->d2h, c->ev_stats, 0));
         CK(cudaMemcpyAsync(out_labels, rl.label, n * 4, cudaMemcpyDeviceToHost, c->d2h));
+        c->d2h_bytes += n * 4;
     }
     const uint32_t* h_cnt = c->h_band;
     const uint32_t* h_first = c->h_band + 2 * kMaxBands * kNumClasses;
@@ -1148,6 +1485,7 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
             CK(cudaMemcpyAsync(out_values + rows_out * ncols, c->d_out + rows_out * ncols,
                                (upto - rows_out) * ncols * sizeof(double), cudaMemcpyDeviceToHost,
                                c->d2h));
+            c->d2h_bytes += (upto - rows_out) * ncols * sizeof(double);
             rows_out = upto;
         }
     }
@@ -1589,7 +1927,10 @@ int fx_ctx_create(int device, fx_ctx** out) {
     CKC(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     CKC(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
     CKC(cudaStreamCreateWithFlags(&c->d2h, cudaStreamNonBlocking));
+    CKC(cudaStreamCreateWithFlags(&c->copy2, cudaStreamNonBlocking));
     if (const char* e = getenv("FXG_BAND_ROWS")) c->band_rows = atoi(e);
+    if (const char* e = getenv("FXG_PACK")) c->packing = atoi(e) != 0;
+    if (const char* e = getenv("FXG_PACK_RAW")) c->pack_raw_pct = std::max(0, std::min(100, atoi(e)));
     for (int b = 0; b < 2; ++b) {
         CKC(cudaEventCreateWithFlags(&c->ev_staged[b], cudaEventDisableTiming));
         CKC(cudaEventCreateWithFlags(&c->ev_free[b], cudaEventDisableTiming));
@@ -1628,6 +1969,9 @@ int fx_ctx_destroy(fx_ctx* c) {
     collect_times(c);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     c->ev_pool.clear();
+    c->pool.reset();  // joins the packing workers
+    cudaFreeHost(c->h_pack);
+    cudaFree(c->d_pack);
     cudaFree(c->d_cnt);
     cudaFree(c->d_bb);
     cudaFree(c->d_maxlab);
@@ -1673,6 +2017,7 @@ int fx_ctx_destroy(fx_ctx* c) {
     if (c->side) cudaStreamDestroy(c->side);
     if (c->copy) cudaStreamDestroy(c->copy);
     if (c->d2h) cudaStreamDestroy(c->d2h);
+    if (c->copy2) cudaStreamDestroy(c->copy2);
     for (cudaEvent_t e : c->ev_band) cudaEventDestroy(e);
     cudaFree(c->d_band);
     cudaFree(c->d_band_ctl);
@@ -1718,6 +2063,19 @@ int fx_ctx_set_stream(fx_ctx* c, void* stream) {
 int fx_ctx_set_band_rows(fx_ctx* c, int rows) {
     if (!c) return set_error(FX_E_ARG, "null ctx");
     c->band_rows = rows;
+    return FX_OK;
+}
+
+int fx_ctx_set_packing(fx_ctx* c, int on) {
+    if (!c) return set_error(FX_E_ARG, "null ctx");
+    c->packing = on != 0;
+    return FX_OK;
+}
+
+int fx_ctx_last_transfer(const fx_ctx* c, uint64_t* h2d, uint64_t* d2h) {
+    if (!c || !h2d || !d2h) return set_error(FX_E_ARG, "null argument");
+    *h2d = c->h2d_bytes;
+    *d2h = c->d2h_bytes;
     return FX_OK;
 }
 
@@ -1780,7 +2138,13 @@ int fx_featurize(fx_ctx* c, const fx_image* im, unsigned groups, const fx_textur
         const int br = band_rows_for(c, im->width, im->height);
         if (br > 0) {
             rc = ensure_out(c, std::max<size_t>(1, cap_rois) * (size_t)cfg.ncols);
-            if (!rc) rc = featurize_banded(c, im, br, groups, *p, out_labels, out_values, cap_rois, n_rois);
+            if (!rc)
+                rc = packing_usable(c, im)
+                         ? featurize_packed(c, im, br, groups, *p, out_labels, out_values, cap_rois, n_rois)
+                         : featurize_banded(c, im, br, groups, *p, out_labels, out_values, cap_rois, n_rois);
+            // no copy may still read the caller's rasters once the call returns
+            cudaStreamSynchronize(c->copy);
+            cudaStreamSynchronize(c->copy2);
             if (rc) {
                 cudaStreamSynchronize(c->copy);
                 cudaStreamSynchronize(c->d2h);

@@ -816,6 +816,15 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
         double acc[5] = {0, 0, 0, 0, 0};
         unsigned long long slo = 0, best = 0;
         uint32_t clo = 0;
+        // mode key and entropy bins: per distinct value from the value histogram
+        // (coalesced over [vmin, vmax]) when that range is small next to n, else per
+        // pixel (a gather from the histogram and a 64-bit division each)
+        const bool by_value = rng < 2u * n;
+        auto bin_of = [&](uint32_t v) -> uint32_t {
+            if (!rng) return 0u;
+            const unsigned long long q = (unsigned long long)nb32 * (v - vmin) / rng;
+            return q < nb32 - 1 ? (uint32_t)q : nb32 - 1;
+        };
         for (uint32_t i = tid; i < n; i += kBT) {
             const uint32_t v = S.vals[i];
             const double d = (double)v - mean, d2 = d * d;
@@ -828,14 +837,20 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
                 slo += v;
                 ++clo;
             }
-            const unsigned long long key = ((unsigned long long)S.vhist[v] << 16) | (0xffffu - v);
-            best = key > best ? key : best;
-            uint32_t bin = 0;
-            if (rng) {
-                const unsigned long long q = (unsigned long long)nb32 * (v - vmin) / rng;
-                bin = q < nb32 - 1 ? (uint32_t)q : nb32 - 1;
+            if (!by_value) {
+                const unsigned long long key = ((unsigned long long)S.vhist[v] << 16) | (0xffffu - v);
+                best = key > best ? key : best;
+                atomicAdd(&S.bins[bin_of(v)], 1u);
             }
-            atomicAdd(&S.bins[bin], 1u);
+        }
+        if (by_value) {
+            for (uint32_t v = vmin + tid; v <= vmax; v += kBT) {
+                const uint32_t c = S.vhist[v];
+                if (!c) continue;
+                const unsigned long long key = ((unsigned long long)c << 16) | (0xffffu - v);
+                best = key > best ? key : best;
+                atomicAdd(&S.bins[bin_of(v)], c);
+            }
         }
 #pragma unroll
         for (int k = 0; k < 5; ++k) acc[k] = block_all(acc[k], sm.f64s, OpAdd());
@@ -924,8 +939,11 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
             rmad = ((double)(long long)(rsum - 2 * rlo) +
                     (double)((long long)rcl - (long long)(rn - rcl)) * rmean) / (double)rn;
         }
-        // value histogram back to zero
-        for (uint32_t i = tid; i < n; i += kBT) S.vhist[S.vals[i]] = 0u;
+        // value histogram back to zero (the value range, or the pixels' values)
+        if (by_value)
+            for (uint32_t v = vmin + tid; v <= vmax; v += kBT) S.vhist[v] = 0u;
+        else
+            for (uint32_t i = tid; i < n; i += kBT) S.vhist[S.vals[i]] = 0u;
         BT(2);
 
         // ---- edge set: K = largest 8-connected component, E = 4-connected exterior
@@ -1163,9 +1181,21 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
             const unsigned long long q = (unsigned long long)ng * (v - vmin) / span;
             return q < (unsigned long long)(ng - 1) ? (uint32_t)q : (uint32_t)(ng - 1);
         };
+        // window cells c = tid + k kBT walked as (x, y) with one division per ROI
+        const uint32_t uw = (uint32_t)w, step_y = (uint32_t)kBT / uw, step_x = (uint32_t)kBT % uw;
+        auto advance = [&](uint32_t& x, uint32_t& y) {
+            x += step_x;
+            y += step_y;
+            if (x >= uw) {
+                x -= uw;
+                ++y;
+            }
+        };
         if (dense) {
+            uint32_t xc = tid % uw, yc = tid / uw;
             for (uint32_t c = tid; c < cells; c += kBT) {
-                const uint32_t y = c / (uint32_t)w, x = c - y * (uint32_t)w;
+                const uint32_t y = yc, x = xc;
+                advance(xc, yc);
                 uint16_t lv = kNoLevel;
                 if ((S.rowmask[y * wpr + (x >> 6)] >> (x & 63)) & 1ull)
                     lv = (uint16_t)level(img.I[(size_t)(y0 + y) * img.pitch + x0 + x]);
@@ -1183,10 +1213,12 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
         uint32_t npa0 = 0, npa1 = 0, npa2 = 0, npa3 = 0;
         if (fused) {
             const uint32_t ngu = (uint32_t)ng;
+            uint32_t xc = tid % uw, yc = tid / uw;
             for (uint32_t c = tid; c < cells; c += kBT) {
+                const int y = (int)yc, x = (int)xc;
+                advance(xc, yc);
                 const uint32_t la = S.lraster[c];
                 if (la == kNoLevel) continue;
-                const int y = (int)(c / (uint32_t)w), x = (int)(c - (uint32_t)y * (uint32_t)w);
 #pragma unroll
                 for (int a = 0; a < 4; ++a) {
                     if (a >= A) break;

@@ -13,6 +13,7 @@
 // k_compact_count / k_compact_emit: ascending list of present labels (rank =
 // output row), bbox -> window, window-size class lists for the per-ROI kernels.
 #include "fx_dev.cuh"
+#include "fx_pack.hpp"
 
 namespace fxg {
 
@@ -542,6 +543,94 @@ __global__ void k_cloud_gather(DevImage img, RoiList rl, const Control* ctl,
                 at += __popc(m);
             }
         }
+    }
+}
+
+
+// --- packed host rows (fx_pack.hpp) -------------------------------------------
+//
+// One 256-thread CTA per (row, 2048-pixel tile) of a packed block, 8 pixels per
+// thread (16 B stores).  Labels: a binary search from the tile's first segment
+// for the one covering the thread's first pixel, then a walk over the (rarely
+// more than one or two) change points inside its 8 pixels.  Intensities: the
+// labelled pixels' values follow in row order, so a thread's first value sits at
+// the tile's count plus the labelled pixels before it in the tile (block scan).
+__global__ void __launch_bounds__(256) k_unpack_labels(const uint8_t* __restrict__ region, int rows,
+                                                       int W, uint16_t* __restrict__ L, size_t P) {
+    const int tiles = pk_tiles(W), t = (int)blockIdx.x, row = (int)blockIdx.y;
+    const uint32_t* tile_seg = reinterpret_cast<const uint32_t*>(region);
+    const uint32_t* seg = reinterpret_cast<const uint32_t*>(region + pk_index_bytes(rows, W));
+    const size_t ti = (size_t)row * tiles + t;
+    const uint32_t rs = tile_seg[(size_t)row * tiles], re = tile_seg[(size_t)(row + 1) * tiles];
+    const int x0 = t * kPackTile + (int)threadIdx.x * 8;
+    if (x0 >= W) return;
+    auto x_of = [&](uint32_t k) -> uint32_t { return k < re ? (seg[k] & 0xffffu) : 0x10000u; };
+    // the segment covering the tile's first pixel is the tile's first or the one before
+    uint32_t lo = max(rs, tile_seg[ti] ? tile_seg[ti] - 1u : 0u), hi = re - 1;
+    while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (x_of(mid) <= (uint32_t)x0) lo = mid;
+        else hi = mid - 1;
+    }
+    uint32_t k = lo, nx = x_of(k + 1), lab = seg[k] >> 16;
+    uint32_t v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        while ((uint32_t)(x0 + j) >= nx) {
+            ++k;
+            lab = seg[k] >> 16;
+            nx = x_of(k + 1);
+        }
+        v[j] = lab;
+    }
+    uint16_t* out = L + (size_t)row * P;
+    if (x0 + 8 <= W) {
+        *reinterpret_cast<uint4*>(out + x0) =
+            make_uint4(v[0] | v[1] << 16, v[2] | v[3] << 16, v[4] | v[5] << 16, v[6] | v[7] << 16);
+    } else {
+        for (int j = 0; j < 8 && x0 + j < W; ++j) out[x0 + j] = (uint16_t)v[j];
+    }
+}
+
+__global__ void __launch_bounds__(256) k_unpack_intensity(const uint8_t* __restrict__ region, int rows,
+                                                          int W, const uint16_t* __restrict__ L,
+                                                          uint16_t* __restrict__ I, size_t P) {
+    __shared__ uint32_t warp_tot[8];
+    const int tiles = pk_tiles(W), t = (int)blockIdx.x, row = (int)blockIdx.y;
+    const uint32_t* tile_pix = reinterpret_cast<const uint32_t*>(region);
+    const uint16_t* pix = reinterpret_cast<const uint16_t*>(region + pk_index_bytes(rows, W));
+    const int x0 = t * kPackTile + (int)threadIdx.x * 8;
+    const unsigned lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const uint16_t* lrow = L + (size_t)row * P;
+    uint32_t lab[8];
+    if (x0 + 8 <= W) {
+        const uint4 q = *reinterpret_cast<const uint4*>(lrow + x0);
+        const uint32_t w4[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) lab[j] = (w4[j >> 1] >> (16 * (j & 1))) & 0xffffu;
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) lab[j] = x0 + j < W ? lrow[x0 + j] : 0u;
+    }
+    uint32_t cnt = 0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) cnt += lab[j] != 0u;
+    const uint32_t incl = warp_incl_scan(cnt);
+    if (lane == 31) warp_tot[wid] = incl;
+    __syncthreads();
+    uint32_t before = 0;
+    for (unsigned q = 0; q < wid; ++q) before += warp_tot[q];
+    if (x0 >= W) return;
+    uint32_t at = tile_pix[(size_t)row * tiles + t] + before + incl - cnt;
+    uint32_t v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = lab[j] ? pix[at++] : 0u;
+    uint16_t* out = I + (size_t)row * P;
+    if (x0 + 8 <= W) {
+        *reinterpret_cast<uint4*>(out + x0) =
+            make_uint4(v[0] | v[1] << 16, v[2] | v[3] << 16, v[4] | v[5] << 16, v[6] | v[7] << 16);
+    } else {
+        for (int j = 0; j < 8 && x0 + j < W; ++j) out[x0 + j] = (uint16_t)v[j];
     }
 }
 

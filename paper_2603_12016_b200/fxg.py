@@ -171,6 +171,17 @@ class Context:
         identical either way (fx_ctx_set_band_rows)."""
         _check(lib().fx_ctx_set_band_rows(self.h, int(rows)))
 
+    def set_packing(self, on: bool):
+        """Banded host rasters cross PCIe packed (label change points + labelled
+        intensities) or raw; results are identical either way (fx_ctx_set_packing)."""
+        _check(lib().fx_ctx_set_packing(self.h, 1 if on else 0))
+
+    def last_transfer(self):
+        """(h2d_bytes, d2h_bytes) of the last host-raster call (fx_ctx_last_transfer)."""
+        a, b = C.c_uint64(), C.c_uint64()
+        _check(lib().fx_ctx_last_transfer(self.h, C.byref(a), C.byref(b)))
+        return a.value, b.value
+
     def launch_count(self) -> int:
         return int(lib().fx_ctx_launch_count(self.h))
 

@@ -173,6 +173,60 @@ def test_banded_host_path_bitwise(ctx, rows):
     assert np.array_equal(rv, bv)
 
 
+def _packed_case(name):
+    rng = np.random.default_rng(5)
+    if name == "blobs":
+        L = inputs.random_blobs((700, 300), 90, seed=7, max_r=40,
+                                label_values=np.array([1, 2, 3, 65535, 40000, 17, 900]))
+    elif name == "noise_rows":  # some blocks do not pack into half their size: sent raw
+        L = inputs.random_blobs((900, 256), 60, seed=3, max_r=30)
+        L[300:700] = rng.integers(0, 65536, (400, 256)).astype(np.uint16)
+    elif name == "odd_width":  # width not a multiple of 8 / 32; labels on the last column
+        L = inputs.random_blobs((520, 333), 50, seed=9, max_r=25)
+        L[:, 332] = 7
+        L[100:110, :] = 11
+    elif name == "full_rows":  # labelled everywhere: every intensity crosses
+        L = inputs.random_labels((400, 192), 20, seed=4, p_bg=0.0)
+    else:  # empty
+        L = np.zeros((300, 130), np.uint16)
+    return inputs.uniform(L.shape, 11), L
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["blobs", "noise_rows", "odd_width", "full_rows", "empty"])
+def test_packed_host_path_bitwise(ctx, oracle, name):
+    """Banded host rasters crossing PCIe packed (label change points + labelled
+    intensities, host threads) == raw bands == the unbanded call, bit for bit, and
+    the oracle; raw fallback per block where the labels do not pack."""
+    import paper_2603_12016_b200 as fx
+    from oracle import make_params as oparams
+    p = fx.resolve_profile("default")
+    I, L = _packed_case(name)
+    try:
+        ctx.set_band_rows(-1)
+        rl, rv = ctx.featurize(I, L, GROUPS, p)
+        ctx.set_band_rows(128)
+        ctx.set_packing(False)
+        bl, bv = ctx.featurize(I, L, GROUPS, p)
+        raw_h2d, _ = ctx.last_transfer()
+        ctx.set_packing(True)
+        pl, pv = ctx.featurize(I, L, GROUPS, p)
+        pk_h2d, _ = ctx.last_transfer()
+        pl2, pv2 = ctx.featurize(I, L, GROUPS, p)  # staging buffers reused
+    finally:
+        ctx.set_band_rows(0)
+        ctx.set_packing(True)
+    assert raw_h2d == 2 * L.size * 2
+    if name in ("blobs", "odd_width", "empty"):  # a share of the blocks always goes raw
+        assert pk_h2d < 0.75 * raw_h2d, (pk_h2d, raw_h2d)
+    for a, b in ((rl, bl), (rl, pl), (rl, pl2)):
+        assert np.array_equal(a, b)
+    for a, b in ((rv, bv), (rv, pv), (rv, pv2)):
+        assert np.array_equal(a, b)
+    ol, ov = oracle.featurize(I, L, GROUPS, oparams("default"))
+    assert_parity(fx.feature_columns(GROUPS, p), pl, pv, ol, ov, I, L)
+
+
 @pytest.mark.gpu
 def test_banded_host_path_c2_bitwise(ctx):
     """bench.py's e2e call (host rasters, automatic bands) == the device-resident call"""

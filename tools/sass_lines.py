@@ -14,19 +14,23 @@ if True:
     dis = dis[:j] if j > 0 else dis
 cur = None
 addr2 = {}
+chain, fresh = [], True
 for line in dis.splitlines():
     if "//## File" in line:
-        chain = re.findall(r'File "([^"]+)", line (\d+)', line)
-        chain = [(f.split("/")[-1], int(l)) for f, l in chain]
+        # nvdisasm prints one marker line per inline level, innermost first
+        if fresh:
+            chain, fresh = [], False
+        chain += [(f.split("/")[-1], int(l)) for f, l in re.findall(r'"([^"]+)", line (\d+)', line)[:1]]
         cur = chain[0]
         if PHASE_FILE:
             inside = [c for c in chain if c[0] == PHASE_FILE and PHASE_LO <= c[1] <= PHASE_HI]
             if inside:
-                cur = inside[-1]
+                cur = inside[0]
         continue
     m = re.match(r'\s+/\*([0-9a-f]{4,})\*/', line)
     if m and cur:
         addr2[int(m.group(1), 16)] = cur
+        fresh = True
 rows = list(csv.reader(open(csvf)))
 hdr = rows[1]
 ia, ie, isamp = hdr.index("Address"), hdr.index("Instructions Executed"), hdr.index("Warp Stall Sampling (All Samples)")
