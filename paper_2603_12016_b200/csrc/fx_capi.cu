@@ -18,6 +18,7 @@
 #include <functional>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -187,7 +188,6 @@ struct fx_ctx {
     // the host's nonzero masks; FXG_PACK=0 / fx_ctx_set_packing(0) sends raw rows
     bool packing = true;
     int pack_raw_pct = 20;  // FXG_PACK_RAW: % of row blocks sent raw (DMA next to the packers)
-    std::unique_ptr<PackPool> pool;
     uint8_t* h_pack = nullptr;
     uint8_t* d_pack = nullptr;
     size_t pack_bytes = 0;
@@ -1106,10 +1106,14 @@ int featurize_packed(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     }
     const size_t mp = ((size_t)W + 31) / 32;  // mask words per row
     if (c->pack_mask.size() < mp * (size_t)H) c->pack_mask.resize(mp * (size_t)H);
-    if (!c->pool) {
+    // one pool per process (the packers are bound by the host's memory bandwidth,
+    // which every context shares): one packed call at a time holds it
+    static std::mutex pool_mu;
+    std::unique_lock<std::mutex> pool_lock(pool_mu);
+    static PackPool* const shared_pool = [] {
         const int hw = (int)std::thread::hardware_concurrency();
-        c->pool = std::make_unique<PackPool>(std::max(1, std::min(hw - 1, 15)));
-    }
+        return new PackPool(std::max(1, std::min(hw - 1, 15)));  // lives for the process
+    }();
     std::vector<size_t> lab_bytes(NB, 0), int_bytes(NB, 0);
     // FXG_PACK_TRACE=1: host timeline of the call on stderr (tools)
     static const bool trace = getenv("FXG_PACK_TRACE") && atoi(getenv("FXG_PACK_TRACE"));
@@ -1122,7 +1126,7 @@ int featurize_packed(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     };
     uint8_t* hp = c->h_pack;
     uint32_t* mask = c->pack_mask.data();
-    PackPool* pool = c->pool.get();
+    PackPool* pool = shared_pool;
     // the previous call's copies out of the staging buffers are complete (its
     // finish() synchronised every stream)
     pool->start(2 * NB, [&, pool](int t) {
@@ -1144,8 +1148,15 @@ int featurize_packed(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     // return waits for them
     struct Join {
         PackPool* p;
-        ~Join() { p->wait(); }
-    } join{pool};
+        std::unique_lock<std::mutex>* lk;
+        void release() {
+            if (!lk) return;
+            p->wait();
+            lk->unlock();
+            lk = nullptr;
+        }
+        ~Join() { release(); }
+    } join{pool, &pool_lock};
     auto spin = [&](int t) {
         while (!pool->done(t)) std::this_thread::yield();
     };
@@ -1326,6 +1337,7 @@ int featurize_packed(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
             dmark("band " + std::to_string(b) + " rows back", c->d2h);
         }
     }
+    join.release();  // every block packed and shipped: the pool is free for other contexts
     CK(cudaMemcpyAsync(c->h_band_ctl, c->d_band_ctl, (size_t)nb * sizeof(Control),
                        cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(c->h_ctl, c->d_ctl, sizeof(Control), cudaMemcpyDeviceToHost, s));
@@ -1969,7 +1981,6 @@ int fx_ctx_destroy(fx_ctx* c) {
     collect_times(c);
     for (cudaEvent_t e : c->ev_pool) cudaEventDestroy(e);
     c->ev_pool.clear();
-    c->pool.reset();  // joins the packing workers
     cudaFreeHost(c->h_pack);
     cudaFree(c->d_pack);
     cudaFree(c->d_cnt);

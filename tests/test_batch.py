@@ -228,6 +228,46 @@ def test_packed_host_path_bitwise(ctx, oracle, name):
 
 
 @pytest.mark.gpu
+def test_packed_host_path_concurrent_contexts(ctx):
+    """Two contexts packing at once from two host threads (one process-wide packer
+    pool, taken in turn): each gets the unbanded rows."""
+    import threading
+    import paper_2603_12016_b200 as fx
+    p = fx.resolve_profile("default")
+    cases = [_packed_case("blobs"), _packed_case("odd_width")]
+    ctx.set_band_rows(-1)
+    try:
+        want = [ctx.featurize(I, L, GROUPS, p) for I, L in cases]
+    finally:
+        ctx.set_band_rows(0)
+    ctxs = [fx.Context(0), fx.Context(0)]
+    got = [[None] * 4, [None] * 4]
+    errs = []
+
+    def run(t):
+        try:
+            ctxs[t].set_band_rows(128)
+            for k in range(4):
+                got[t][k] = ctxs[t].featurize(*cases[(t + k) % 2], GROUPS, p)
+        except Exception as e:  # surfaced below
+            errs.append(e)
+
+    th = [threading.Thread(target=run, args=(t,)) for t in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join()
+    for c in ctxs:
+        c.close()
+    assert not errs, errs
+    for t in range(2):
+        for k in range(4):
+            wl, wv = want[(t + k) % 2]
+            gl, gv = got[t][k]
+            assert np.array_equal(wl, gl) and np.array_equal(wv, gv), (t, k)
+
+
+@pytest.mark.gpu
 def test_banded_host_path_c2_bitwise(ctx):
     """bench.py's e2e call (host rasters, automatic bands) == the device-resident call"""
     import torch
