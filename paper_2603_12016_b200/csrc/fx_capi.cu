@@ -189,6 +189,12 @@ struct fx_ctx {
     bool packing = true;
     int pack_raw_pct = 20;  // FXG_PACK_RAW: % of row blocks sent raw (DMA next to the packers)
     uint8_t* h_pack = nullptr;
+    // batch path: packed staging in two halves (by staging buffer); events: a half's
+    // host-to-device copies done, its unpack kernels done; one per shipped block
+    size_t pack_half = 0;
+    cudaEvent_t ev_pack_free[2] = {nullptr, nullptr}, ev_unpacked[2] = {nullptr, nullptr};
+    std::vector<cudaEvent_t> ev_blocks;
+    std::vector<uint32_t> pack_mask_b[2];
     uint8_t* d_pack = nullptr;
     size_t pack_bytes = 0;
     std::vector<uint32_t> pack_mask;
@@ -1036,8 +1042,40 @@ struct PackBlock {
     int y0, rows, band;
     bool raw;  // sent raw by DMA (both rasters) while the workers pack the others
     size_t lab_off, int_off;  // region offsets in the staging buffers
-    size_t lab_cap_seg;
+    size_t lab_cap_seg, int_cap_pix;
 };
+
+// One packer pool per process (the packers are bound by the host's memory
+// bandwidth, which every context shares); one packing call at a time holds it.
+std::mutex& packer_mutex() {
+    static std::mutex m;
+    return m;
+}
+PackPool* packer_pool() {
+    static PackPool* const pool = [] {
+        const int hw = (int)std::thread::hardware_concurrency();
+        return new PackPool(std::max(1, std::min(hw - 1, 15)));  // lives for the process
+    }();
+    return pool;
+}
+
+// pinned + device staging for packed blocks (both paths)
+int ensure_pack(fx_ctx* c, size_t bytes) {
+    if (bytes <= c->pack_bytes) return FX_OK;
+    cudaStreamSynchronize(c->copy);
+    cudaStreamSynchronize(c->copy2);
+    cudaStreamSynchronize(c->stream);
+    cudaFreeHost(c->h_pack);
+    cudaFree(c->d_pack);
+    c->h_pack = nullptr;
+    c->d_pack = nullptr;
+    c->pack_bytes = 0;
+    CK(cudaMallocHost(&c->h_pack, bytes));
+    CK(cudaMalloc(&c->d_pack, bytes));
+    c->pack_bytes = bytes;
+    c->pack_half = 0;  // the caller re-lays its halves
+    return FX_OK;
+}
 
 bool packing_usable(const fx_ctx* c, const fx_image* im) {
     return c->packing && pack_isa() == 2 && im->width <= 65536;
@@ -1084,7 +1122,8 @@ int featurize_packed(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
             k.lab_off = bytes;
             bytes += pk_align16(pk_lab_bytes(k.rows, W, k.lab_cap_seg));
             k.int_off = bytes;
-            bytes += pk_align16(pk_int_bytes(k.rows, W, (size_t)k.rows * (size_t)W));
+            k.int_cap_pix = (size_t)k.rows * (size_t)W / 2;  // half the raw intensity bytes
+            bytes += pk_align16(pk_int_bytes(k.rows, W, k.int_cap_pix));
             blk.push_back(k);
         }
     }
@@ -1094,26 +1133,12 @@ int featurize_packed(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     // from the start (spread evenly: block j raw when floor((j+1) r) > floor(j r)).
     for (int q = 0; q < NB; ++q)
         blk[q].raw = (q + 1) * c->pack_raw_pct / 100 > q * c->pack_raw_pct / 100;
-    if (bytes > c->pack_bytes) {
-        cudaFreeHost(c->h_pack);
-        cudaFree(c->d_pack);
-        c->h_pack = nullptr;
-        c->d_pack = nullptr;
-        c->pack_bytes = 0;
-        CK(cudaMallocHost(&c->h_pack, bytes));
-        CK(cudaMalloc(&c->d_pack, bytes));
-        c->pack_bytes = bytes;
-    }
+    rc = ensure_pack(c, bytes);
+    if (rc) return rc;
     const size_t mp = ((size_t)W + 31) / 32;  // mask words per row
     if (c->pack_mask.size() < mp * (size_t)H) c->pack_mask.resize(mp * (size_t)H);
-    // one pool per process (the packers are bound by the host's memory bandwidth,
-    // which every context shares): one packed call at a time holds it
-    static std::mutex pool_mu;
-    std::unique_lock<std::mutex> pool_lock(pool_mu);
-    static PackPool* const shared_pool = [] {
-        const int hw = (int)std::thread::hardware_concurrency();
-        return new PackPool(std::max(1, std::min(hw - 1, 15)));  // lives for the process
-    }();
+    std::unique_lock<std::mutex> pool_lock(packer_mutex());
+    PackPool* const shared_pool = packer_pool();
     std::vector<size_t> lab_bytes(NB, 0), int_bytes(NB, 0);
     // FXG_PACK_TRACE=1: host timeline of the call on stderr (tools)
     static const bool trace = getenv("FXG_PACK_TRACE") && atoi(getenv("FXG_PACK_TRACE"));
@@ -1141,7 +1166,7 @@ int featurize_packed(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
             while (!pool->done(j)) std::this_thread::yield();  // claimed earlier, running
             if (lab_bytes[j])
                 int_bytes[j] = pack_intensity(im->intensity, spe, W, k.y0, k.y0 + k.rows, m, mp,
-                                              hp + k.int_off);
+                                              hp + k.int_off, k.int_cap_pix);
         }
     });
     // the workers read the caller's rasters and write the staging buffers: every
@@ -1525,6 +1550,133 @@ int validate_batch(const fx_image* ims, int n, size_t* row_offsets) {
     return FX_OK;
 }
 
+// Host image runs of a batch sub-batch (images back to back with the staging
+// pitch, whole 64-row strips) staged packed: blocks of up to kBatchPackRows rows
+// packed by the shared pool into half `buf` of the packed staging while this
+// thread ships finished blocks (copy2: never waits for compute) and unpacks them
+// on the copy stream (which waits until compute has released staging buffer buf);
+// a share of the blocks goes raw by DMA meanwhile (as featurize_packed).  Packing
+// into a half waits only for that half's previous copies (ev_pack_free), and its
+// device half is rewritten only after its previous unpacks (ev_unpacked).
+struct PackRun {
+    const uint16_t *I, *L;
+    size_t row0, rows;
+};
+constexpr int kBatchPackRows = 4096;
+int stage_packed_runs(fx_ctx* c, const std::vector<PackRun>& runs, int P, int buf) {
+    struct Blk {
+        const uint16_t *I, *L;
+        size_t row0;
+        int rows;
+        bool raw;
+        size_t lab_off, int_off, cap_seg, cap_pix, mask_row;
+    };
+    std::vector<Blk> blk;
+    size_t bytes = 0, mask_rows = 0;
+    for (const PackRun& r : runs)
+        for (size_t y = 0; y < r.rows; y += kBatchPackRows) {
+            Blk b;
+            b.rows = (int)std::min<size_t>(kBatchPackRows, r.rows - y);
+            b.I = r.I + y * (size_t)P;
+            b.L = r.L + y * (size_t)P;
+            b.row0 = r.row0 + y;
+            b.cap_seg = (size_t)b.rows * (size_t)P / 4;  // half the raw label bytes
+            b.cap_pix = (size_t)b.rows * (size_t)P / 2;  // half the raw intensity bytes
+            b.lab_off = bytes;
+            bytes += pk_align16(pk_lab_bytes(b.rows, P, b.cap_seg));
+            b.int_off = bytes;
+            bytes += pk_align16(pk_int_bytes(b.rows, P, b.cap_pix));
+            b.mask_row = mask_rows;
+            mask_rows += (size_t)b.rows;
+            b.raw = false;
+            blk.push_back(b);
+        }
+    const int NB = (int)blk.size();
+    for (int q = 0; q < NB; ++q) blk[q].raw = (q + 1) * c->pack_raw_pct / 100 > q * c->pack_raw_pct / 100;
+    // staging halves sized for the largest sub-batch seen
+    const size_t half = std::max(c->pack_half, pk_align16(bytes));
+    int rc = FX_OK;
+    if (half > c->pack_half) {  // re-lay the halves: nothing may still use the old ones
+        CK(cudaStreamSynchronize(c->copy));
+        CK(cudaStreamSynchronize(c->copy2));
+        rc = ensure_pack(c, 2 * half);
+        if (rc) return rc;
+        c->pack_half = half;
+    }
+    for (int h = 0; h < 2; ++h) {
+        if (!c->ev_pack_free[h]) CK(cudaEventCreateWithFlags(&c->ev_pack_free[h], cudaEventDisableTiming));
+        if (!c->ev_unpacked[h]) CK(cudaEventCreateWithFlags(&c->ev_unpacked[h], cudaEventDisableTiming));
+    }
+    while ((int)c->ev_blocks.size() < NB) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        c->ev_blocks.push_back(e);
+    }
+    CK(cudaEventSynchronize(c->ev_pack_free[buf]));  // this half's previous copies are done
+    uint8_t* hp = c->h_pack + (size_t)buf * c->pack_half;
+    uint8_t* dp = c->d_pack + (size_t)buf * c->pack_half;
+    const size_t mp = (size_t)P / 32;
+    std::vector<uint32_t>& maskv = c->pack_mask_b[buf];
+    if (maskv.size() < mp * mask_rows) maskv.resize(mp * mask_rows);
+    uint32_t* mask = maskv.data();
+    std::vector<size_t> lab_bytes(NB, 0), int_bytes(NB, 0);
+    std::unique_lock<std::mutex> lock(packer_mutex());
+    PackPool* pool = packer_pool();
+    pool->start(NB, [&](int t) {
+        const Blk& b = blk[t];
+        if (b.raw) return;
+        uint32_t* m = mask + b.mask_row * mp;
+        lab_bytes[t] = pack_labels(b.L, (size_t)P, P, 0, b.rows, hp + b.lab_off, b.cap_seg, m, mp);
+        if (lab_bytes[t])
+            int_bytes[t] = pack_intensity(b.I, (size_t)P, P, 0, b.rows, m, mp, hp + b.int_off, b.cap_pix);
+    });
+    struct Join {
+        PackPool* p;
+        ~Join() { p->wait(); }
+    } join{pool};
+    uint16_t* sI = c->d_stage[buf];
+    uint16_t* sL = c->d_stage[buf] + c->stage_elems;
+    auto raw = [&](const uint16_t* src, uint16_t* dst, const Blk& b) -> int {
+        const size_t n = (size_t)b.rows * (size_t)P * 2;
+        CK(cudaMemcpyAsync(dst + b.row0 * P, src, n, cudaMemcpyHostToDevice, c->copy));
+        c->h2d_bytes += n;
+        return FX_OK;
+    };
+    for (const Blk& b : blk)
+        if (b.raw && ((rc = raw(b.L, sL, b)) || (rc = raw(b.I, sI, b)))) return rc;
+    CK(cudaStreamWaitEvent(c->copy2, c->ev_unpacked[buf], 0));  // device half free
+    for (int t = 0; t < NB; ++t) {
+        const Blk& b = blk[t];
+        if (b.raw) continue;
+        while (!pool->done(t)) std::this_thread::yield();
+        if (!lab_bytes[t]) {
+            if ((rc = raw(b.L, sL, b)) || (rc = raw(b.I, sI, b))) return rc;
+            continue;
+        }
+        CK(cudaMemcpyAsync(dp + b.lab_off, hp + b.lab_off, lab_bytes[t], cudaMemcpyHostToDevice, c->copy2));
+        if (int_bytes[t])
+            CK(cudaMemcpyAsync(dp + b.int_off, hp + b.int_off, int_bytes[t], cudaMemcpyHostToDevice,
+                               c->copy2));
+        c->h2d_bytes += lab_bytes[t] + int_bytes[t];
+        CK(cudaEventRecord(c->ev_blocks[t], c->copy2));
+        CK(cudaStreamWaitEvent(c->copy, c->ev_blocks[t], 0));
+        const dim3 grid(pk_tiles(P), b.rows);
+        Launch l(c, "k_unpack_labels");
+        k_unpack_labels<<<grid, 256, 0, c->copy>>>(dp + b.lab_off, b.rows, P, sL + b.row0 * P, P);
+        if (int_bytes[t]) {
+            Launch l2(c, "k_unpack_intensity");
+            k_unpack_intensity<<<grid, 256, 0, c->copy>>>(dp + b.int_off, b.rows, P, sL + b.row0 * P,
+                                                          sI + b.row0 * P, P);
+        } else if ((rc = raw(b.I, sI, b))) {
+            return rc;
+        }
+    }
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(c->ev_pack_free[buf], c->copy2));
+    CK(cudaEventRecord(c->ev_unpacked[buf], c->copy));
+    return FX_OK;
+}
+
 // The sub-batch pipeline of fx_featurize_batch with device outputs (out_dev,
 // lab_dev: [cap_rois] rows): images stacked per sub-batch (one label-table slot
 // each, staging double-buffered on the copy stream).  After each sub-batch's
@@ -1601,11 +1753,20 @@ int batch_core(fx_ctx* c, const fx_image* ims, int n, unsigned groups, const fx_
         // bounded the C4 end-to-end path)
         const uint16_t *runI = nullptr, *runL = nullptr;
         size_t run_row0 = 0, run_rows = 0;
+        // host runs are packed (label change points + labelled intensities) where the
+        // host can (fx_pack.hpp), else copied raw
+        const bool pack = kind == FX_MEM_HOST && c->packing && pack_isa() == 2 && P <= 65536;
+        std::vector<PackRun> runs;
         auto flush = [&]() -> int {
             if (run_rows) {
-                CK(cudaMemcpyAsync(c->d_stage[buf] + run_row0 * P, runI, run_rows * P * 2, mk, c->copy));
-                CK(cudaMemcpyAsync(c->d_stage[buf] + c->stage_elems + run_row0 * P, runL, run_rows * P * 2,
-                                   mk, c->copy));
+                if (pack) {
+                    runs.push_back(PackRun{runI, runL, run_row0, run_rows});
+                } else {
+                    CK(cudaMemcpyAsync(c->d_stage[buf] + run_row0 * P, runI, run_rows * P * 2, mk, c->copy));
+                    CK(cudaMemcpyAsync(c->d_stage[buf] + c->stage_elems + run_row0 * P, runL,
+                                       run_rows * P * 2, mk, c->copy));
+                    c->h2d_bytes += run_rows * P * 4;
+                }
             }
             run_rows = 0;
             return FX_OK;
@@ -1634,12 +1795,17 @@ int batch_core(fx_ctx* c, const fx_image* ims, int n, unsigned groups, const fx_
                                              (size_t)im.height, mk, c->copy));
                         CK(cudaMemcpy2DAsync(dL, P * 2, im.labels, sp, (size_t)im.width * 2,
                                              (size_t)im.height, mk, c->copy));
+                        if (kind == FX_MEM_HOST) c->h2d_bytes += (size_t)im.width * im.height * 4;
                     }
                 }
             }
             row0 += r;
         }
         if (flush()) return FX_E_CUDA;
+        if (!runs.empty()) {
+            const int prc = stage_packed_runs(c, runs, (int)P, buf);
+            if (prc) return prc;
+        }
         CK(cudaMemcpyAsync(c->d_slots[buf], hs, (size_t)b.count * sizeof(SlotInfo),
                            cudaMemcpyHostToDevice, c->copy));
         CK(cudaMemcpyAsync(c->d_strips[buf], hst, ((b.rows + 63) / 64) * sizeof(uint16_t),
@@ -1983,6 +2149,11 @@ int fx_ctx_destroy(fx_ctx* c) {
     c->ev_pool.clear();
     cudaFreeHost(c->h_pack);
     cudaFree(c->d_pack);
+    for (int h = 0; h < 2; ++h) {
+        if (c->ev_pack_free[h]) cudaEventDestroy(c->ev_pack_free[h]);
+        if (c->ev_unpacked[h]) cudaEventDestroy(c->ev_unpacked[h]);
+    }
+    for (cudaEvent_t e : c->ev_blocks) cudaEventDestroy(e);
     cudaFree(c->d_cnt);
     cudaFree(c->d_bb);
     cudaFree(c->d_maxlab);
@@ -2288,6 +2459,7 @@ int fx_featurize_batch(fx_ctx* c, const fx_image* ims, int n, unsigned groups,
     }
     // host images: each sub-batch's rows leave on the d2h stream while the next
     // sub-batch computes
+    c->h2d_bytes = c->d2h_bytes = 0;
     rc = ensure_out(c, std::max<size_t>(1, cap_rois) * (size_t)cfg.ncols);
     if (!rc) rc = ensure_blab(c, std::max<size_t>(1, cap_rois));
     if (rc) return rc;
@@ -2302,10 +2474,12 @@ int fx_featurize_batch(fx_ctx* c, const fx_image* ims, int n, unsigned groups,
                            cudaMemcpyDeviceToHost, c->d2h));
         CK(cudaMemcpyAsync(out_labels + first, c->d_blab + first, rows * sizeof(uint32_t),
                            cudaMemcpyDeviceToHost, c->d2h));
+        c->d2h_bytes += rows * (nc * sizeof(double) + sizeof(uint32_t));
         return FX_OK;
     };
     rc = batch_core(c, ims, n, groups, p, c->d_out, c->d_blab, cap_rois, row_offsets, readback);
     cudaStreamSynchronize(c->d2h);
+    cudaStreamSynchronize(c->copy);  // no copy may still read the caller's rasters
     return rc ? rc : finish(c);
 }
 

@@ -62,12 +62,14 @@ FXP_TARGET size_t pack_labels_vbmi2(const uint16_t* labels, size_t pitch, uint32
 }
 
 FXP_TARGET size_t pack_intensity_vbmi2(const uint16_t* intensity, size_t pitch, uint32_t w, int y0,
-                                       int y1, const uint32_t* mask, size_t mp, uint8_t* region) {
+                                       int y1, const uint32_t* mask, size_t mp, uint8_t* region,
+                                       size_t cap_pix) {
     const int rows = y1 - y0, tiles = pk_tiles((int)w);
     uint32_t* tile_pix = reinterpret_cast<uint32_t*>(region);
     uint16_t* pix = reinterpret_cast<uint16_t*>(region + pk_index_bytes(rows, (int)w));
     size_t np = 0;
     for (int y = y0; y < y1; ++y) {
+        if (np + w > cap_pix) return 0;
         const uint16_t* iv = intensity + (size_t)y * pitch;
         const uint32_t* mrow = mask + (size_t)(y - y0) * mp;
         uint32_t* tp = tile_pix + (size_t)(y - y0) * tiles;
@@ -98,8 +100,9 @@ size_t pack_labels(const uint16_t* labels, size_t pitch, int width, int y0, int 
 }
 
 size_t pack_intensity(const uint16_t* intensity, size_t pitch, int width, int y0, int y1,
-                      const uint32_t* mask, size_t mask_pitch, uint8_t* region) {
-    return pack_intensity_vbmi2(intensity, pitch, (uint32_t)width, y0, y1, mask, mask_pitch, region);
+                      const uint32_t* mask, size_t mask_pitch, uint8_t* region, size_t cap_pix) {
+    return pack_intensity_vbmi2(intensity, pitch, (uint32_t)width, y0, y1, mask, mask_pitch, region,
+                                cap_pix);
 }
 
 // ---------------------------------------------------------------- pool ----

@@ -61,9 +61,10 @@ inline size_t pk_int_bytes(int rows, int width, size_t cap_pix) {
 size_t pack_labels(const uint16_t* labels, size_t pitch, int width, int y0, int y1, uint8_t* region,
                    size_t cap_seg, uint32_t* mask, size_t mask_pitch);
 // Intensities of the labelled pixels of rows [y0, y1) (mask from pack_labels)
-// into an intensity region (capacity: every pixel).  Returns the region bytes.
+// into an intensity region of capacity cap_pix pixels.  Returns the region bytes,
+// or 0 when a row might not fit (send the block's intensities raw).
 size_t pack_intensity(const uint16_t* intensity, size_t pitch, int width, int y0, int y1,
-                      const uint32_t* mask, size_t mask_pitch, uint8_t* region);
+                      const uint32_t* mask, size_t mask_pitch, uint8_t* region, size_t cap_pix);
 
 // 2: AVX-512 VBMI2 packers; 0: none on this host (the banded path sends raw rows)
 int pack_isa();

@@ -134,6 +134,18 @@ def main():
     e2e_s = (time.perf_counter() - t1) / e_steps
     # spot check: the e2e table equals the device table for the same tiles
     same = bool(torch.equal(ho_v[:int(offs[Te])], out_v[:int(offs[Te])].cpu()))
+    h2d_b, d2h_b = ctx.last_transfer()
+    # the same calls with raw rows over PCIe (no host packing)
+    ctx.set_packing(False)
+    ctx.featurize_batch_raw(ims_h, Te, mask, p, ho_l.data_ptr(), ho_v.data_ptr(), cap_e)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    for _ in range(e_steps):
+        ctx.featurize_batch_raw(ims_h, Te, mask, p, ho_l.data_ptr(), ho_v.data_ptr(), cap_e)
+    torch.cuda.synchronize()
+    e2e_raw_s = (time.perf_counter() - t1) / e_steps
+    raw_h2d, _ = ctx.last_transfer()
+    ctx.set_packing(True)
 
     line = {
         "metric": "megapixels/s", "unit": "MP/s", "value": mp / (ms / 1e3),
@@ -148,9 +160,9 @@ def main():
         "gpu_launches_per_step": int(launches),
         "kernels_ms_per_step": {k: v[0] / args.steps for k, v in sorted(kt.items())},
         "e2e": {"value": Te * TILE * TILE / 1e6 / e2e_s, "unit": "MP/s", "tiles": Te,
-                "h2d_bytes_per_step": Te * TILE * TILE * 4,
-                "d2h_bytes_per_step": int(offs[Te]) * (ncols * 8 + 4),
-                "matches_device_table": same},
+                "h2d_bytes_per_step": int(h2d_b), "d2h_bytes_per_step": int(d2h_b),
+                "matches_device_table": same,
+                "raw_rows": {"value": Te * TILE * TILE / 1e6 / e2e_raw_s, "h2d_bytes_per_step": int(raw_h2d)}},
         "setup_s": gen_s,
         "clocks": clk.summary(),
     }
