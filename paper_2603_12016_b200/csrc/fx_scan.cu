@@ -57,17 +57,18 @@ __device__ __forceinline__ uint32_t occ_last(const CacheEnt& e) {
 }
 
 // an entry evicted mid-strip is not in the end-of-strip caches the warp reduces
-// for maxlab, so its label raises the slot's maxlab here (compaction skips
-// 1024-label blocks above it)
-__device__ __forceinline__ void evict(const LabelTable& t, const CacheEnt& e, uint32_t x) {
+// for maxlab, so its label raises the lane's running maximum lmax (compaction
+// skips 1024-label blocks above the slot's maxlab; a global atomic per eviction
+// cost the C2 scan 23 us of contention on one address)
+__device__ __forceinline__ void evict(const LabelTable& t, const CacheEnt& e, uint32_t x, uint32_t& lmax) {
     if (e.label) {
         global_fold(t, e.label, e.cnt, x + occ_first(e), x + occ_last(e), e.y0, e.y1);
-        atomicMax(&t.maxlab[e.label >> 16], e.label & 0xffffu);
+        lmax = max(lmax, e.label & 0xffffu);
     }
 }
 
 // fold a row's pixels of label l (pixel bytes olo/ohi, cnt of them) into the cache
-__device__ __forceinline__ void cache_put(CacheEnt& c0, CacheEnt& c1, const LabelTable& t,
+__device__ __forceinline__ void cache_put(CacheEnt& c0, CacheEnt& c1, uint32_t& lmax, const LabelTable& t,
                                           uint32_t x, uint32_t l, uint32_t cnt, uint32_t olo,
                                           uint32_t ohi, uint32_t y) {
     if (l == c0.label) {
@@ -81,7 +82,7 @@ __device__ __forceinline__ void cache_put(CacheEnt& c0, CacheEnt& c1, const Labe
         c1.occ_hi |= ohi;
         c1.y1 = y;
     } else {
-        evict(t, c1, x);
+        evict(t, c1, x, lmax);
         c1 = c0;
         c0 = CacheEnt{l, cnt, olo, ohi, y, y};
     }
@@ -90,7 +91,8 @@ __device__ __forceinline__ void cache_put(CacheEnt& c0, CacheEnt& c1, const Labe
 // several distinct labels inside one 8-px chunk: per pixel, the chunk shifted
 // through a register pair (no runtime-indexed array)
 __device__ __forceinline__ void chunk_slow(uint4 v, uint32_t x, uint32_t y, uint32_t sb,
-                                           CacheEnt& c0, CacheEnt& c1, const LabelTable& t) {
+                                           CacheEnt& c0, CacheEnt& c1, uint32_t& lmax,
+                                           const LabelTable& t) {
     unsigned long long q0 = v.x | ((unsigned long long)v.y << 32);
     unsigned long long q1 = v.z | ((unsigned long long)v.w << 32);
 #pragma unroll 1
@@ -99,13 +101,13 @@ __device__ __forceinline__ void chunk_slow(uint4 v, uint32_t x, uint32_t y, uint
         q0 = (q0 >> 16) | (q1 << 48);
         q1 >>= 16;
         const uint32_t byte = 0xffu << (8 * (k & 3));
-        if (l) cache_put(c0, c1, t, x, sb | l, 1u, k < 4 ? byte : 0u, k < 4 ? 0u : byte, y);
+        if (l) cache_put(c0, c1, lmax, t, x, sb | l, 1u, k < 4 ? byte : 0u, k < 4 ? 0u : byte, y);
     }
 }
 
 // sb = slot << 16: cache keys and table indices are slot * 65536 + label
 __device__ __forceinline__ void chunk(uint4 v, uint32_t x, uint32_t y, uint32_t sb, CacheEnt& c0,
-                                      CacheEnt& c1, const LabelTable& t) {
+                                      CacheEnt& c1, uint32_t& lmax, const LabelTable& t) {
     if ((v.x | v.y | v.z | v.w) == 0u) return;
     // the largest label of the chunk (paired-halfword max, VIMNMX.U16x2)
     const uint32_t mx2 = __vmaxu2(__vmaxu2(v.x, v.y), __vmaxu2(v.z, v.w));
@@ -116,7 +118,7 @@ __device__ __forceinline__ void chunk(uint4 v, uint32_t x, uint32_t y, uint32_t 
     const uint32_t bad = __vminu2(v.x, v.x ^ LL) | __vminu2(v.y, v.y ^ LL) |
                          __vminu2(v.z, v.z ^ LL) | __vminu2(v.w, v.w ^ LL);
     if (bad) {
-        chunk_slow(v, x, y, sb, c0, c1, t);
+        chunk_slow(v, x, y, sb, c0, c1, lmax, t);
         return;
     }
     // nonzero halfwords (SWAR: bit 15 of each half set iff the half is nonzero), then
@@ -124,7 +126,7 @@ __device__ __forceinline__ void chunk(uint4 v, uint32_t x, uint32_t y, uint32_t 
     auto nz = [](uint32_t q) { return ((q & 0x7fff7fffu) + 0x7fff7fffu) | q; };
     const uint32_t olo = __byte_perm(nz(v.x), nz(v.y), 0x7531) & 0x80808080u;
     const uint32_t ohi = __byte_perm(nz(v.z), nz(v.w), 0x7531) & 0x80808080u;
-    cache_put(c0, c1, t, x, sb | L, (uint32_t)(__popc(olo) + __popc(ohi)), olo, ohi, y);
+    cache_put(c0, c1, lmax, t, x, sb | L, (uint32_t)(__popc(olo) + __popc(ohi)), olo, ohi, y);
 }
 
 __device__ __forceinline__ uint4 load_chunk(const uint16_t* __restrict__ L, size_t pitch, int W,
@@ -181,6 +183,7 @@ __global__ void __launch_bounds__(kScanThreads, FXG_SCAN_MINB)
         const int y0 = strip * kStripRows;
         const uint32_t gx = (uint32_t)x + gxo;
         CacheEnt c0{0, 0, 0, 0, 0, 0}, c1{0, 0, 0, 0, 0, 0};
+        uint32_t lmax = 0;  // largest label this lane evicted in the tile
         if (vec_ok && tx0 + 256 <= sw && y0 + kStripRows <= send) {
             // interior tile: plain pointer walk, kBatch rows of 16 B in flight per lane
             const uint4* p = reinterpret_cast<const uint4*>(L + (size_t)y0 * pitch + x);
@@ -193,7 +196,7 @@ __global__ void __launch_bounds__(kScanThreads, FXG_SCAN_MINB)
                 for (int r = 0; r < kBatch; ++r) v[r] = __ldg(p + (size_t)r * step);
                 p += (size_t)kBatch * step;
 #pragma unroll
-                for (int r = 0; r < kBatch; ++r) chunk(v[r], gx, gy + r, sb, c0, c1, t);
+                for (int r = 0; r < kBatch; ++r) chunk(v[r], gx, gy + r, sb, c0, c1, lmax, t);
                 gy += kBatch;
             }
         } else {
@@ -202,11 +205,11 @@ __global__ void __launch_bounds__(kScanThreads, FXG_SCAN_MINB)
 #pragma unroll 1
             for (int r = 0; r < kStripRows; ++r)
                 chunk(load_chunk(L, pitch, sw, send, x, y0 + r, vec_ok), gx, (uint32_t)(y0 + r) + gyo, sb,
-                      c0, c1, t);
+                      c0, c1, lmax, t);
         }
         warp_flush(c0, gx, t);
         warp_flush(c1, gx, t);
-        const uint32_t mx = warp_max(max(c0.label & 0xffffu, c1.label & 0xffffu));
+        const uint32_t mx = warp_max(max(lmax, max(c0.label & 0xffffu, c1.label & 0xffffu)));
         if (lane == 0 && mx) atomicMax(&t.maxlab[slot], mx);
     }
 }

@@ -11,5 +11,5 @@ for f in paper_2603_12016_b200/csrc/*.cu; do
   nvcc $FL $defs -c $f -o $out/$(basename $f .cu).o &
 done
 wait
-nvcc $ARCH -shared -cudart static -o $out/libfxg.so $out/*.o paper_2603_12016_b200/build/fx_host.o paper_2603_12016_b200/build/engine.o -lpthread -ldl -lrt
+nvcc $ARCH -shared -cudart static -o $out/libfxg.so $out/*.o paper_2603_12016_b200/build/fx_host.o paper_2603_12016_b200/build/engine.o paper_2603_12016_b200/build/fx_pack.o -lpthread -ldl -lrt
 echo $out/libfxg.so
