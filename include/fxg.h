@@ -292,6 +292,15 @@ int fx_multi_featurize_slide(fx_multi* m, const fx_image* image, unsigned groups
  * sort, 7 GLCM run-length counts, 8 Haralick.  Only in builds with
  * -DFXG_PHASE_TIMING (tools/); others return FX_E_CONFIG. */
 int fx_debug_phase_clocks(unsigned long long* out, int n, int reset);
+/* Host packer of the packed host rows (fx_ctx_set_packing), for tests: packs
+ * `rows` rows of width `width` (pitch in elements) into a label region of
+ * lab_cap bytes and an intensity region of int_cap bytes, in the layout the
+ * device unpacks (csrc/fx_pack.hpp).  *lab_bytes / *int_bytes receive the bytes
+ * used (0: does not fit, the block goes raw).  FX_E_CONFIG when this host has no
+ * AVX-512 VBMI2 (packing is then off). */
+int fx_debug_pack_rows(const uint16_t* labels, const uint16_t* intensity, size_t pitch, int width,
+                       int rows, uint8_t* lab_region, size_t lab_cap, uint8_t* int_region,
+                       size_t int_cap, size_t* lab_bytes, size_t* int_bytes);
 /* Same for the GLRLM/GLSZM/NGTDM kernel (thread 0 per ROI): 0 discretize,
  * 1 GLRLM (other), 2 GLSZM, 3 NGTDM, 4 GLRLM run counting, 5 GLRLM features. */
 int fx_debug_texture_clocks(unsigned long long* out, int n, int reset);

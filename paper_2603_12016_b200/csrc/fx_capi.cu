@@ -2248,6 +2248,25 @@ int fx_ctx_set_band_rows(fx_ctx* c, int rows) {
     return FX_OK;
 }
 
+int fx_debug_pack_rows(const uint16_t* labels, const uint16_t* intensity, size_t pitch, int width,
+                       int rows, uint8_t* lab_region, size_t lab_cap, uint8_t* int_region,
+                       size_t int_cap, size_t* lab_bytes, size_t* int_bytes) {
+    if (!labels || !intensity || !lab_region || !int_region || !lab_bytes || !int_bytes || width < 1 ||
+        rows < 1 || pitch < (size_t)width)
+        return set_error(FX_E_ARG, "bad argument");
+    if (pack_isa() != 2) return set_error(FX_E_CONFIG, "this host has no AVX-512 VBMI2 packer");
+    const size_t idx = pk_index_bytes(rows, width);
+    if (lab_cap < idx + 128 || int_cap < idx + 64) return set_error(FX_E_ARG, "region too small");
+    const size_t cap_seg = (lab_cap - idx - 128) / 4, cap_pix = (int_cap - idx - 64) / 2;
+    const size_t mp = ((size_t)width + 31) / 32;
+    std::vector<uint32_t> mask(mp * (size_t)rows);
+    *lab_bytes = pack_labels(labels, pitch, width, 0, rows, lab_region, cap_seg, mask.data(), mp);
+    *int_bytes = *lab_bytes ? pack_intensity(intensity, pitch, width, 0, rows, mask.data(), mp, int_region,
+                                             cap_pix)
+                            : 0;
+    return FX_OK;
+}
+
 int fx_ctx_set_packing(fx_ctx* c, int on) {
     if (!c) return set_error(FX_E_ARG, "null ctx");
     c->packing = on != 0;
