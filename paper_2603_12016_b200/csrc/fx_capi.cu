@@ -1661,10 +1661,10 @@ int stage_packed_runs(fx_ctx* c, const std::vector<PackRun>& runs, int P, int bu
         CK(cudaEventRecord(c->ev_blocks[t], c->copy2));
         CK(cudaStreamWaitEvent(c->copy, c->ev_blocks[t], 0));
         const dim3 grid(pk_tiles(P), b.rows);
-        Launch l(c, "k_unpack_labels");
+        Launch l(c, "k_unpack_labels", c->copy);
         k_unpack_labels<<<grid, 256, 0, c->copy>>>(dp + b.lab_off, b.rows, P, sL + b.row0 * P, P);
         if (int_bytes[t]) {
-            Launch l2(c, "k_unpack_intensity");
+            Launch l2(c, "k_unpack_intensity", c->copy);
             k_unpack_intensity<<<grid, 256, 0, c->copy>>>(dp + b.int_off, b.rows, P, sL + b.row0 * P,
                                                           sI + b.row0 * P, P);
         } else if ((rc = raw(b.I, sI, b))) {
