@@ -1051,10 +1051,19 @@ std::mutex& packer_mutex() {
     static std::mutex m;
     return m;
 }
+// Threads: FXG_PACK_THREADS, else the host's cores shared among the processes of
+// a torchrun job on this node (LOCAL_WORLD_SIZE), less one for the caller, <= 15.
 PackPool* packer_pool() {
     static PackPool* const pool = [] {
-        const int hw = (int)std::thread::hardware_concurrency();
-        return new PackPool(std::max(1, std::min(hw - 1, 15)));  // lives for the process
+        int n = 0;
+        if (const char* e = getenv("FXG_PACK_THREADS")) n = atoi(e);
+        if (n <= 0) {
+            const int hw = std::max(1, (int)std::thread::hardware_concurrency());
+            const char* lw = getenv("LOCAL_WORLD_SIZE");
+            const int procs = lw ? std::max(1, atoi(lw)) : 1;
+            n = std::min(hw / procs - 1, 15);
+        }
+        return new PackPool(std::max(1, n));  // lives for the process
     }();
     return pool;
 }
