@@ -110,22 +110,33 @@ __host__ __device__ constexpr SLayout make_slayout(uint32_t TW, uint32_t TH, uin
 }
 
 // window-class variants: stage width, max rows, max pixels, run capacity, warps/SM
+// (MINB: without GLCM; MINB_G: with a GLCM mode, whose longer code runs faster with
+// more registers per warp than the occupancy it gives up)
 #ifndef FXG_S0_MINB
 #define FXG_S0_MINB 20
+#endif
+#ifndef FXG_S0_MINB_G
+#define FXG_S0_MINB_G 16
+#endif
+#ifndef FXG_S12_MINB_G
+#define FXG_S12_MINB_G 16
 #endif
 template <int CLS>
 struct SVar;
 template <>
 struct SVar<kClassS0> {
-    static constexpr int TW = kStageW0, TH = kS0H, NMAX = kS0N, RUNMAX = 256, MINB = FXG_S0_MINB;
+    static constexpr int TW = kStageW0, TH = kS0H, NMAX = kS0N, RUNMAX = 256, MINB = FXG_S0_MINB,
+                         MINB_G = FXG_S0_MINB_G;
 };
 template <>
 struct SVar<kClassS1> {
-    static constexpr int TW = kStageW, TH = kSH, NMAX = kS1N, RUNMAX = 512, MINB = 20;
+    static constexpr int TW = kStageW, TH = kSH, NMAX = kS1N, RUNMAX = 512, MINB = 20,
+                         MINB_G = FXG_S12_MINB_G;
 };
 template <>
 struct SVar<kClassS2> {
-    static constexpr int TW = kStageW, TH = kSH, NMAX = kS2N, RUNMAX = 1024, MINB = 20;
+    static constexpr int TW = kStageW, TH = kSH, NMAX = kS2N, RUNMAX = 1024, MINB = 20,
+                         MINB_G = FXG_S12_MINB_G;
 };
 template <int CLS, int GLCM>
 constexpr SLayout slayout() {
@@ -2023,7 +2034,7 @@ namespace {
 #define FXG_S_PREFETCH 0  // 1: L2 prefetch of the next window (measured slower on C2)
 #endif
 template <int CLS, int GLCM>
-__global__ void __launch_bounds__(32, SVar<CLS>::MINB)
+__global__ void __launch_bounds__(32, GLCM ? SVar<CLS>::MINB_G : SVar<CLS>::MINB)
     k_roi_s(const __grid_constant__ CUtensorMap tmapL, const __grid_constant__ CUtensorMap tmapI,
             int use_tma, DevImage img, RoiList rl, Control* ctl, FeatCfg cfg, double* out,
             const DebugOut* dbg) {
