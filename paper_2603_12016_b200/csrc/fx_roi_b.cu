@@ -1168,7 +1168,7 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
     if (want_glcm) {
         const int ng = cfg.ng, A = cfg.n_angles;
         const bool sym = cfg.symmetric != 0;
-        const unsigned long long span = (unsigned long long)(vmax - vmin) + 1ull;
+        const uint32_t span = vmax - vmin + 1u, mdiv = 0xffffffffu / span;
         // dense windows (cells <= raster capacity, ~4 n): a level raster of the window
         // (u16, kNoLevel outside the ROI) lets pair counting walk window cells
         // coalesced with one load per neighbour; sparse windows (multi-component ROIs
@@ -1176,10 +1176,12 @@ __device__ void process_b(uint32_t r, const DevImage& img, const RoiList& rl, Co
         constexpr uint16_t kNoLevel = 0xffffu;
         const uint32_t cells = (uint32_t)w * (uint32_t)h;
         const bool dense = (unsigned long long)w * h <= B.RCAP;
-        auto level = [&](uint32_t v) -> uint32_t {
+        auto level = [&](uint32_t v) -> uint32_t {  // floor(ng (v - vmin) / span), ng <= 256
             if (vmax <= vmin) return 0u;
-            const unsigned long long q = (unsigned long long)ng * (v - vmin) / span;
-            return q < (unsigned long long)(ng - 1) ? (uint32_t)q : (uint32_t)(ng - 1);
+            const uint32_t num = (uint32_t)ng * (v - vmin);
+            uint32_t q = __umulhi(num, mdiv);
+            if (num - q * span >= span) ++q;
+            return min((uint32_t)(ng - 1), q);
         };
         // window cells c = tid + k kBT walked as (x, y) with one division per ROI
         const uint32_t uw = (uint32_t)w, step_y = (uint32_t)kBT / uw, step_x = (uint32_t)kBT % uw;

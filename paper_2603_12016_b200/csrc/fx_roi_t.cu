@@ -632,7 +632,9 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
     double none[1] = {0.0};
     tblock_fused<1>(none, hi, lo, sm);
     const uint32_t vmin = lo, vmax = hi;
-    const unsigned long long span = (unsigned long long)(vmax - vmin) + 1ull;
+    // floor(ng (v - vmin) / span) by multiply-high and one fix-up (ng <= 256, so the
+    // numerator fits 32 bits): a 64-bit division per cell was ~10 % of the kernel
+    const uint32_t span = vmax - vmin + 1u, mdiv = 0xffffffffu / span;
     uint16_t* lv = SM ? d_slev() : S.lev;  // shared memory for S-class windows
     for (uint32_t c = tid; c < cells; c += kTT) {
         uint16_t l = kNoLevel;
@@ -640,8 +642,10 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
         if (img.L[o] == label) {
             l = 0;
             if (vmax > vmin) {
-                const unsigned long long q = (unsigned long long)ng * (img.I[o] - vmin) / span;
-                l = (uint16_t)(q < (unsigned long long)(ng - 1) ? q : (unsigned long long)(ng - 1));
+                const uint32_t num = (uint32_t)ng * (img.I[o] - vmin);
+                uint32_t q = __umulhi(num, mdiv);
+                if (num - q * span >= span) ++q;
+                l = (uint16_t)min((uint32_t)(ng - 1), q);
             }
         }
         lv[c] = l;
