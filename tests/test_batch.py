@@ -149,6 +149,43 @@ def test_batch_device_rasters(ctx, stacked):
         assert np.array_equal(bv[offs[k]:offs[k + 1]], sv), k
 
 
+@pytest.mark.gpu
+def test_batch_host_stack_packed(ctx):
+    """A host [T, H, W] stack is one run of back-to-back images: it is
+    packed in 4096-row blocks (a block boundary falls inside an image), noise tiles
+    fall back to raw rows, and every image's rows equal its device-resident call."""
+    import paper_2603_12016_b200 as fx
+    from paper_2603_12016_b200 import fxg
+    p = fx.resolve_profile("default")
+    mask = fx.resolve_groups(GROUPS)
+    T, H, W = 44, 128, 192
+    pairs = _pairs([(H, W, 6 + k % 9) for k in range(T)], seed=17)
+    rng = np.random.default_rng(3)
+    for k in (5, 6, 40):  # label noise: these rows do not pack
+        pairs[k] = (pairs[k][0], rng.integers(0, 65536, (H, W)).astype(np.uint16))
+    sI = np.ascontiguousarray(np.stack([a for a, _ in pairs]))
+    sL = np.ascontiguousarray(np.stack([b for _, b in pairs]))
+    ims = (fxg.FxImage * T)()
+    for k in range(T):
+        ims[k] = fxg.FxImage(sI[k].ctypes.data, sL[k].ctypes.data, W, H, W, 0, 0, fxg.MEM_HOST)
+    cap = int(sum(np.count_nonzero(np.bincount(L.ravel(), minlength=65536)[1:]) for _, L in pairs))
+    try:
+        ctx.set_packing(True)
+        bl, bv, offs = ctx.featurize_batch_raw(ims, T, mask, p, None, None, cap)
+        pk, _ = ctx.last_transfer()
+        ctx.set_packing(False)
+        rl, rv, roffs = ctx.featurize_batch_raw(ims, T, mask, p, None, None, cap)
+        raw, _ = ctx.last_transfer()
+    finally:
+        ctx.set_packing(True)
+    assert raw == T * H * W * 4 and pk < 0.8 * raw, (pk, raw)
+    assert np.array_equal(offs, roffs) and np.array_equal(bl, rl) and np.array_equal(bv, rv)
+    for k in (0, 5, 31, 32, 40, 43):  # 32: straddles the 4096-row block boundary
+        sl, sv = ctx.featurize(sI[k], sL[k], GROUPS, p)
+        assert np.array_equal(bl[offs[k]:offs[k + 1]], sl), k
+        assert np.array_equal(bv[offs[k]:offs[k + 1]], sv), k
+
+
 # ---- banded host path (fx_featurize with host rasters: H2D / kernels / D2H
 # overlapped in row bands) must give exactly the unbanded rows ---------------
 
@@ -187,13 +224,17 @@ def _packed_case(name):
         L[100:110, :] = 11
     elif name == "full_rows":  # labelled everywhere: every intensity crosses
         L = inputs.random_labels((400, 192), 20, seed=4, p_bg=0.0)
+    elif name == "wide_odd":  # three 2048-px unpack tiles, the last partial; runs across tiles
+        L = inputs.random_blobs((260, 4100), 120, seed=12, max_r=35)
+        L[:, 2040:2060] = 3
+        L[50:60, 4090:] = 4
     else:  # empty
         L = np.zeros((300, 130), np.uint16)
     return inputs.uniform(L.shape, 11), L
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["blobs", "noise_rows", "odd_width", "full_rows", "empty"])
+@pytest.mark.parametrize("name", ["blobs", "noise_rows", "odd_width", "full_rows", "wide_odd", "empty"])
 def test_packed_host_path_bitwise(ctx, oracle, name):
     """Banded host rasters crossing PCIe packed (label change points + labelled
     intensities, host threads) == raw bands == the unbanded call, bit for bit, and
@@ -217,7 +258,7 @@ def test_packed_host_path_bitwise(ctx, oracle, name):
         ctx.set_band_rows(0)
         ctx.set_packing(True)
     assert raw_h2d == 2 * L.size * 2
-    if name in ("blobs", "odd_width", "empty"):  # a share of the blocks always goes raw
+    if name in ("blobs", "odd_width", "wide_odd", "empty"):  # a share of the blocks always goes raw
         assert pk_h2d < 0.75 * raw_h2d, (pk_h2d, raw_h2d)
     for a, b in ((rl, bl), (rl, pl), (rl, pl2)):
         assert np.array_equal(a, b)
