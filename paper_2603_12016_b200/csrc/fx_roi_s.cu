@@ -1825,6 +1825,9 @@ __device__ __forceinline__ void process_s(const SJob& J, const SLayout& L, uint8
                 if ((int)lane <= h) q += quads(lane == 0 ? 0ull : pm0, (int)lane < h ? m0 : 0ull);
                 if ((int)lane + 32 <= h)
                     q += quads(lane == 0 ? l31 : pm1, (int)lane + 32 < h ? m1 : 0ull);
+                // a 64-row window's bottom pair (row 63, empty row 64) has no lane of its
+                // own: without it a ROI on the last row counted as one fewer component
+                if (h == 64 && lane == 31) q += quads(m1, 0ull);
                 q = warp_sum(q);
             }
             fast = !__any_sync(kFull, hole) && q == 4;  // one component, no holes

@@ -842,7 +842,9 @@ __device__ void process_t(uint32_t r, const DevImage& img, const RoiList& rl, Co
                     const int j = d_nglev()[kj];
                     const double pj = d_ngp()[kj], sj = d_ngs()[kj], gj = j + 1;
                     a_con += pi * pj * (i - j) * (i - j);
-                    a_busy += fabs(gi * pi - gj * pj);
+                    // unfused products: busyness divides by this sum, and equal products
+                    // must cancel to exactly 0 as in the reference (an FMA leaves 1 ulp)
+                    a_busy += fabs(__dsub_rn(__dmul_rn(gi, pi), __dmul_rn(gj, pj)));
                     a_cplx += fabs(gi - gj) * (pi * si + pj * sj) / (pi + pj);
                     a_strn += (pi + pj) * (gi - gj) * (gi - gj);
                 }

@@ -510,7 +510,7 @@ __device__ void process_wide(uint32_t r, const DevImage& img, const RoiList& rl,
                     const double pj = (double)S.plev[j] / nv, sj = (double)S.sv[j] / 840.0, gj = j + 1.0;
                     const double di = (double)i - (double)j;
                     a4[0] += pi * pj * di * di;
-                    a4[1] += fabs(gi * pi - gj * pj);
+                    a4[1] += fabs(__dsub_rn(__dmul_rn(gi, pi), __dmul_rn(gj, pj)));  // unfused (fx_roi_t.cu)
                     a4[2] += fabs(gi - gj) * (pi * si + pj * sj) / (pi + pj);
                     a4[3] += (pi + pj) * (gi - gj) * (gi - gj);
                 }

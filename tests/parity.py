@@ -18,7 +18,12 @@
     - skewness / hyperskewness, and Haralick clushade / corr / infomeas1: s = 1
     - Haralick clutend / cluprom: s = d^k / tol, d = c u (|sumave| + 1), the
       rounding noise of mu_x + mu_y raised to the moment's power (their truth is
-      0 when every pair sums to the same level)
+      0 when every pair sums to the same level); difvar / sumvar likewise with
+      difave / sumave;
+      clushade: c u sqrt(clutend cluprom) / tol (its terms cancel between signs);
+      entropies (entropy, je, sument, difentro): c u (H + 16) / tol (a one-cell
+      distribution is exactly 0 from integer counts, ~u from summed p)
+    - an _ave column inherits the mean of its angle columns' bounds
     - Haralick infomeas2 = sqrt(1 - exp(-2 (HXY2 - HXY))): a rounding error d of
       order c u (HXY + 1) in the entropy difference moves it by d / imc2 (by
       sqrt(d) near 0), so s = d / (tol max(imc2, sqrt(d))), c = 4096; this only
@@ -108,6 +113,27 @@ def floors(columns, ref_table, intensity=None, labels=None, roi_labels=None):
                 continue
             d = 4096 * 2.2e-16 * (np.abs(ref_table[:, h]) + 1.0)
             s[:, i] = d / (1e-6 * np.maximum(np.abs(ref_table[:, i]), np.sqrt(d)))
+        # entropies -sum p log2 p: when the reference's p sum to 1 only within rounding,
+        # a one-cell distribution gives ~u instead of 0 (and the device's integer p give
+        # exactly 0); noise c u (H + 16)
+        if any(c.startswith(f"glcm_{e}_") for e in ("difentro", "sument", "entropy", "je")):
+            s[:, i] = np.maximum(s[:, i], 4096 * 2.2e-16 * (np.abs(ref_table[:, i]) + 16.0) / 1e-6)
+        # difvar = sum p (d - difave)^2, sumvar = sum p (k - sumave)^2: rounding noise
+        # of the mean, squared (as clutend)
+        for v_, m_ in (("difvar", "difave"), ("sumvar", "sumave")):
+            if c.startswith(f"glcm_{v_}_"):
+                h = col.get(f"glcm_{m_}_" + c[len(f"glcm_{v_}_"):])
+                if h is not None:
+                    d = 4096 * 2.2e-16 * (np.abs(ref_table[:, h]) + 1.0)
+                    s[:, i] = np.maximum(s[:, i], d * d / 1e-6)
+        # clushade = sum p s^3 cancels between signs: the noise is u times the terms'
+        # magnitude, sum p |s|^3 <= sqrt(clutend cluprom) (Cauchy-Schwarz)
+        if c.startswith("glcm_clushade_"):
+            sfx = c[len("glcm_clushade_"):]
+            ht, hp = col.get("glcm_clutend_" + sfx), col.get("glcm_cluprom_" + sfx)
+            if ht is not None and hp is not None:
+                mag = np.sqrt(np.abs(ref_table[:, ht]) * np.abs(ref_table[:, hp]))
+                s[:, i] = np.maximum(s[:, i], 4096 * 2.2e-16 * mag / 1e-6)
         for k, name in ((2, "clutend"), (4, "cluprom")):
             # sum p (i + j - mu_x - mu_y)^k: when all mass sits on one anti-diagonal
             # the truth is 0 and both sides return the rounding noise of mu_x + mu_y
@@ -118,6 +144,20 @@ def floors(columns, ref_table, intensity=None, labels=None, roi_labels=None):
                     continue
                 d = 4096 * 2.2e-16 * (np.abs(ref_table[:, h]) + 1.0)
                 s[:, i] = np.maximum(s[:, i], d ** k / 1e-6)
+    # an _ave column is the mean of its angle columns: it inherits their noise, so its
+    # bound covers the mean of theirs (e.g. infomeas2 with one angle at ~0, where the
+    # noise is sqrt(d), averaged into a larger _ave)
+    for i, c in enumerate(columns):
+        if not c.endswith("_ave"):
+            continue
+        pre = c[:-len("ave")]
+        j = i - 1
+        while j >= 0 and columns[j].startswith(pre) and columns[j][len(pre):].isdigit():
+            j -= 1
+        ang = list(range(j + 1, i))
+        if ang:
+            inherited = np.mean([np.abs(ref_table[:, a]) + s[:, a] for a in ang], axis=0) - np.abs(ref_table[:, i])
+            s[:, i] = np.maximum(s[:, i], inherited)
     # GLRLM/GLSZM variances sum p (x - mu)^2: the reference's rounding noise scales
     # with E[x^2] (its own lre / hglre / lae / hglze columns), not with the variance.
     # Scale columns are found by position (feature-major blocks, names may repeat

@@ -159,6 +159,23 @@ def test_label_scan_evicted_largest_label(ctx, oracle):
         check(ctx, oracle, inputs.uniform(L.shape, 1), L, GROUPS)
 
 
+@pytest.mark.parametrize("rows", [32, 63, 64])
+def test_two_components_touching_last_window_row(ctx, oracle, rows):
+    """A two-component ROI whose window is `rows` tall, the components at the top and
+    on the last row (found by the randomized sweep: a 64-row window lost its bottom
+    Euler quads, took the one-component fast path and merged both edge sets)."""
+    L = np.zeros((rows + 6, 60), np.uint16)
+    L[3:3 + 12, 40:53] = 9                 # top component
+    L[3 + rows - 8:3 + rows, 2:27] = 9     # bottom component, on the window's last row
+    L[3 + rows - 1, 12:17] = 0             # a notch: two runs on that row
+    L[3 + rows - 3, 5:9] = 0
+    I = inputs.uniform(L.shape, 2)
+    check(ctx, oracle, I, L, GROUPS)
+    ys, xs = np.nonzero(L == 9)
+    _, edge, _, _ = ctx.debug_roi(I, L, 9, fx.make_params("default"))
+    assert set(map(tuple, edge.tolist())) == set(map(tuple, oracle.trace_contour(xs, ys).tolist()))
+
+
 @pytest.mark.parametrize("hw", [(7, 5), (3, 30), (40, 60), (90, 20), (150, 150)])
 def test_single_run_cell_entropy_is_zero(ctx, oracle, hw):
     """Constant-intensity rectangles: at 0 and 90 degrees every run falls in one

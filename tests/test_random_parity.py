@@ -7,6 +7,8 @@ duplicates, offsets 1-3, histogram bins 1-1000.  The same cases also go
 through the batch call (8 images per call), the banded host-raster path (64-row
 bands) and the multi-context slide path (bands dealt over 3 contexts).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -66,7 +68,8 @@ def _check(oracle, I, L, over, gl, gv):
     assert_parity(fx.feature_columns(ALL, gp), gl, gv, ol, ov, I, L)
 
 
-@pytest.mark.parametrize("seed", range(200))
+# FX_RANDOM_CASES widens the sweep (e.g. 2000 for a bug hunt; 200 by default)
+@pytest.mark.parametrize("seed", range(int(os.environ.get("FX_RANDOM_CASES", "200"))))
 def test_random_case(ctx, oracle, seed):
     I, L, over = _case(seed)
     gl, gv = ctx.featurize(I, L, ALL, fx.make_params("default", **over))
@@ -147,7 +150,7 @@ def _large_case(seed):
     return I, L, profile, groups, over
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("FX_RANDOM_LARGE", "40"))))
 def test_random_large(ctx, oracle, seed):
     I, L, profile, groups, over = _large_case(seed)
     gp, op = fx.make_params(profile, **over), oparams(profile, **over)
