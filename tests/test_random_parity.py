@@ -76,7 +76,7 @@ def test_random_case(ctx, oracle, seed):
     _check(oracle, I, L, over, gl, gv)
 
 
-@pytest.mark.parametrize("k", range(20))
+@pytest.mark.parametrize("k", range(int(os.environ.get("FX_RANDOM_BATCHES", "20"))))
 def test_random_batch(ctx, oracle, k):
     cases = [_case(8 * k + j) for j in range(8)]
     over = cases[0][2]
@@ -85,7 +85,7 @@ def test_random_batch(ctx, oracle, k):
         _check(oracle, I, L, over, gl, gv)
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("FX_RANDOM_BANDED", "40"))))
 def test_random_banded(ctx, oracle, seed):
     I, L, over = _case(seed)
     try:
@@ -103,7 +103,7 @@ def multi():
     m.close()
 
 
-@pytest.mark.parametrize("seed", range(40))
+@pytest.mark.parametrize("seed", range(int(os.environ.get("FX_RANDOM_SLIDE", "40"))))
 def test_random_slide(multi, oracle, seed):
     I, L, over = _case(seed)
     gl, gv = multi.featurize_slide(I, L, ALL, fx.make_params("default", **over))
