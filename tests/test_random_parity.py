@@ -157,3 +157,36 @@ def test_random_large(ctx, oracle, seed):
     gl, gv = ctx.featurize(I, L, groups, gp)
     ol, ov = oracle.featurize(I, L, groups, op)
     assert_parity(fx.feature_columns(groups, gp), gl, gv, ol, ov, I, L)
+
+
+# window sizes at the class boundaries: S0 (<= 33 x 40 with the 40-wide stage),
+# S1/S2 (<= 64 x 64), the 62-column fast-path limit, 64-row windows, L beyond
+BOUNDARY_WINDOWS = [(33, 40), (34, 40), (33, 41), (62, 64), (63, 64), (64, 64), (64, 63), (64, 62),
+                    (65, 64), (64, 65), (32, 64), (64, 32), (1, 64), (64, 1), (2, 2)]
+
+
+@pytest.mark.parametrize("wh", BOUNDARY_WINDOWS, ids=[f"{w}x{h}" for w, h in BOUNDARY_WINDOWS])
+@pytest.mark.parametrize("seed", range(int(os.environ.get("FX_RANDOM_BOUNDARY", "6"))))
+def test_random_boundary_windows(ctx, oracle, wh, seed):
+    """ROIs whose bounding box is exactly w x h: random fill (several components,
+    holes) with pixels forced on all four box edges, placed at a random offset
+    next to a second ROI; every group against the oracle."""
+    w, h = wh
+    rng = np.random.default_rng(7000 + 97 * seed + w * 131 + h)
+    H, W = h + int(rng.integers(2, 20)), w + int(rng.integers(2, 20))
+    L = np.zeros((H, W), np.uint16)
+    y0, x0 = int(rng.integers(0, H - h + 1)), int(rng.integers(0, W - w + 1))
+    box = rng.random((h, w)) < float(rng.uniform(0.2, 0.95))
+    box[0, int(rng.integers(0, w))] = box[-1, int(rng.integers(0, w))] = True
+    box[int(rng.integers(0, h)), 0] = box[int(rng.integers(0, h)), -1] = True
+    lab = int(rng.choice([1, 77, 65535]))
+    L[y0:y0 + h, x0:x0 + w] = np.where(box, lab, 0)
+    free = L == 0
+    L[free & (rng.random((H, W)) < 0.05)] = 3 if lab != 3 else 4  # a scattered second ROI
+    I = rng.integers(0, int(rng.choice([4, 300, 65536])), (H, W)).astype(np.uint16)
+    over = dict(ng=int(rng.choice([8, 64, 256, 300])), angles=(0, 45, 90, 135),
+                symmetric=bool(rng.integers(0, 2)), offset=int(rng.integers(1, 3)))
+    gp, op = fx.make_params("default", **over), oparams("default", **over)
+    gl, gv = ctx.featurize(I, L, ALL, gp)
+    ol, ov = oracle.featurize(I, L, ALL, op)
+    assert_parity(fx.feature_columns(ALL, gp), gl, gv, ol, ov, I, L)
