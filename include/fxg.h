@@ -178,9 +178,10 @@ int fx_featurize_u16(fx_ctx* ctx, const uint16_t* intensity, const uint16_t* lab
                      double* out_values, size_t cap_rois, size_t* n_rois);
 
 /* The per-ROI operator compute_roi_features(PixelCloud, groups, params)
- * (engine.hpp:68-70): host arrays of pixel x, y, intensity (no duplicates).
- * The cloud is rasterized into its bbox window and run through the same
- * device kernels (a batch of one).  out receives n_cols values. */
+ * (engine.hpp:68-70): host arrays of pixel x, y, intensity, each pixel once
+ * (FX_E_ARG on a repeated pixel or a bounding box above 2^31 cells).  The cloud
+ * is rasterized into its bbox window and run through the same device kernels (a
+ * batch of one).  out receives n_cols values. */
 int fx_roi_features(fx_ctx* ctx, const uint32_t* xs, const uint32_t* ys,
                     const uint16_t* intensities, size_t n, unsigned groups,
                     const fx_texture_params* params, double* out, size_t cap);

@@ -2538,10 +2538,15 @@ int fx_roi_features(fx_ctx* c, const uint32_t* xs, const uint32_t* ys, const uin
         y0 = std::min(y0, ys[i]);
         y1 = std::max(y1, ys[i]);
     }
+    if ((uint64_t)(x1 - x0 + 1) * (uint64_t)(y1 - y0 + 1) > (1ull << 31))
+        return set_error(FX_E_ARG, "cloud bounding box above 2^31 cells");
     const int w = (int)(x1 - x0 + 1), h = (int)(y1 - y0 + 1);
     std::vector<uint16_t> I((size_t)w * h, 0), L((size_t)w * h, 0);
     for (size_t i = 0; i < n; ++i) {
         const size_t k = (size_t)(ys[i] - y0) * w + (xs[i] - x0);
+        if (L[k])  // each pixel once (fx_roi_features_batch)
+            return set_error(FX_E_ARG, "duplicate pixel (" + std::to_string(xs[i]) + ", " +
+                                           std::to_string(ys[i]) + ") in cloud");
         I[k] = is[i];
         L[k] = 1;
     }
@@ -2583,11 +2588,18 @@ int fx_roi_features_batch(fx_ctx* c, const uint32_t* xs, const uint32_t* ys, con
             y0 = std::min(y0, ys[i]);
             y1 = std::max(y1, ys[i]);
         }
+        if ((uint64_t)(x1 - x0 + 1) * (uint64_t)(y1 - y0 + 1) > (1ull << 31))
+            return set_error(FX_E_ARG, "cloud " + std::to_string(k) + ": bounding box above 2^31 cells");
         const int w = (int)(x1 - x0 + 1), h = (int)(y1 - y0 + 1);
         rI.emplace_back((size_t)w * h, (uint16_t)0);
         rL.emplace_back((size_t)w * h, (uint16_t)0);
         for (size_t i = a; i < b; ++i) {
             const size_t q = (size_t)(ys[i] - y0) * w + (xs[i] - x0);
+            // a PixelCloud holds each pixel once (roi.cpp:76-117 builds it from a mask);
+            // a repeated pixel would be counted once here and twice by the reference
+            if (rL.back()[q])
+                return set_error(FX_E_ARG, "cloud " + std::to_string(k) + ": duplicate pixel (" +
+                                               std::to_string(xs[i]) + ", " + std::to_string(ys[i]) + ")");
             rI.back()[q] = is[i];
             rL.back()[q] = 1;
         }

@@ -226,6 +226,21 @@ def test_per_roi_operator(ctx, oracle):
         assert_parity(fx.feature_columns(GROUPS, gp), [1], g[None], [1], o[None])
 
 
+def test_per_roi_operator_rejects_repeated_pixels(ctx):
+    """A PixelCloud holds each pixel once; a repeated one is an argument error, not
+    a silently different table (the rasterized cloud would count it once)."""
+    xs = np.array([3, 4, 5, 4], np.uint32)
+    ys = np.array([7, 7, 7, 7], np.uint32)
+    vs = np.array([10, 20, 30, 40], np.uint16)
+    with pytest.raises(fx.FxError) as e:
+        ctx.roi_features(xs, ys, vs, GROUPS)
+    assert e.value.kind == "ArgumentError" and "duplicate" in str(e.value)
+    with pytest.raises(fx.FxError) as e:
+        ctx.roi_features_batch([(xs[:3], ys[:3], vs[:3]), (xs, ys, vs)], GROUPS)
+    assert e.value.kind == "ArgumentError" and "cloud 1" in str(e.value)
+    ctx.roi_features(xs[:3], ys[:3], vs[:3], GROUPS)  # the context stays usable
+
+
 def test_vs_compiled_reference(ctx, reference):
     L = synth.blob_mask_grid(512, 300, 100, 7)
     I = synth.uniform_u16(L.shape, 0)
