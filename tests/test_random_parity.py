@@ -190,3 +190,29 @@ def test_random_boundary_windows(ctx, oracle, wh, seed):
     gl, gv = ctx.featurize(I, L, ALL, gp)
     ol, ov = oracle.featurize(I, L, ALL, op)
     assert_parity(fx.feature_columns(ALL, gp), gl, gv, ol, ov, I, L)
+
+
+def test_random_small_masks_edge_sets(ctx, oracle):
+    """SURVEY A1 at scale: random one-label masks of 3..12 x 3..12 pixels (fill
+    0.3-0.9: several components, holes, border contact), batched; every group of
+    every mask against the oracle (the edge set drives the edge statistics and
+    the perimeter)."""
+    n = int(os.environ.get("FX_RANDOM_SMALL", "2000"))
+    rng = np.random.default_rng(4242)
+    pairs = []
+    for _ in range(n):
+        h, w = (int(v) for v in rng.integers(3, 13, 2))
+        m = rng.random((h, w)) < float(rng.uniform(0.3, 0.9))
+        if not m.any():
+            m[h // 2, w // 2] = True
+        pad = int(rng.integers(0, 3))
+        L = np.zeros((h + 2 * pad, w + 2 * pad), np.uint16)
+        L[pad:pad + h, pad:pad + w] = m.astype(np.uint16) * int(rng.integers(1, 65536))
+        I = rng.integers(0, 65536, L.shape).astype(np.uint16)
+        pairs.append((I, L))
+    p, op = fx.make_params("default"), oparams("default")
+    cols = fx.feature_columns(ALL, p)
+    res = ctx.featurize_batch(pairs, ALL, p)
+    for (I, L), (gl, gv) in zip(pairs, res):
+        ol, ov = oracle.featurize(I, L, ALL, op)
+        assert_parity(cols, gl, gv, ol, ov, I, L)
