@@ -101,6 +101,7 @@ size_t pack_labels(const uint16_t* labels, size_t pitch, int width, int y0, int 
 
 size_t pack_intensity(const uint16_t* intensity, size_t pitch, int width, int y0, int y1,
                       const uint32_t* mask, size_t mask_pitch, uint8_t* region, size_t cap_pix) {
+    if (pack_isa() != 2 || width > 65536) return 0;
     return pack_intensity_vbmi2(intensity, pitch, (uint32_t)width, y0, y1, mask, mask_pitch, region,
                                 cap_pix);
 }
