@@ -1037,7 +1037,10 @@ BandPlan band_plan(int band_rows, int h) {
 // Row blocks of the packed host path: each band cut into pieces of at most
 // kPackRows rows (a block never straddles a band, so a band's intensities are
 // complete once its last block has been unpacked).
-constexpr int kPackRows = 256;
+#ifndef FXG_PACK_ROWS
+#define FXG_PACK_ROWS 256
+#endif
+constexpr int kPackRows = FXG_PACK_ROWS;
 struct PackBlock {
     int y0, rows, band;
     bool raw;  // sent raw by DMA (both rasters) while the workers pack the others
