@@ -68,15 +68,19 @@ def _check(oracle, I, L, over, gl, gv):
     assert_parity(fx.feature_columns(ALL, gp), gl, gv, ol, ov, I, L)
 
 
-# FX_RANDOM_CASES widens the sweep (e.g. 2000 for a bug hunt; 200 by default)
-@pytest.mark.parametrize("seed", range(int(os.environ.get("FX_RANDOM_CASES", "200"))))
+# FX_RANDOM_CASES widens the sweep (e.g. 2000 for a bug hunt; 200 by default);
+# FX_RANDOM_OFFSET starts every sweep at another seed
+_OFF = int(os.environ.get("FX_RANDOM_OFFSET", "0"))
+
+
+@pytest.mark.parametrize("seed", range(_OFF, _OFF + int(os.environ.get("FX_RANDOM_CASES", "200"))))
 def test_random_case(ctx, oracle, seed):
     I, L, over = _case(seed)
     gl, gv = ctx.featurize(I, L, ALL, fx.make_params("default", **over))
     _check(oracle, I, L, over, gl, gv)
 
 
-@pytest.mark.parametrize("k", range(int(os.environ.get("FX_RANDOM_BATCHES", "20"))))
+@pytest.mark.parametrize("k", range(_OFF, _OFF + int(os.environ.get("FX_RANDOM_BATCHES", "20"))))
 def test_random_batch(ctx, oracle, k):
     cases = [_case(8 * k + j) for j in range(8)]
     over = cases[0][2]
@@ -85,7 +89,7 @@ def test_random_batch(ctx, oracle, k):
         _check(oracle, I, L, over, gl, gv)
 
 
-@pytest.mark.parametrize("seed", range(int(os.environ.get("FX_RANDOM_BANDED", "40"))))
+@pytest.mark.parametrize("seed", range(_OFF, _OFF + int(os.environ.get("FX_RANDOM_BANDED", "40"))))
 def test_random_banded(ctx, oracle, seed):
     I, L, over = _case(seed)
     try:
@@ -103,7 +107,7 @@ def multi():
     m.close()
 
 
-@pytest.mark.parametrize("seed", range(int(os.environ.get("FX_RANDOM_SLIDE", "40"))))
+@pytest.mark.parametrize("seed", range(_OFF, _OFF + int(os.environ.get("FX_RANDOM_SLIDE", "40"))))
 def test_random_slide(multi, oracle, seed):
     I, L, over = _case(seed)
     gl, gv = multi.featurize_slide(I, L, ALL, fx.make_params("default", **over))
@@ -150,7 +154,7 @@ def _large_case(seed):
     return I, L, profile, groups, over
 
 
-@pytest.mark.parametrize("seed", range(int(os.environ.get("FX_RANDOM_LARGE", "40"))))
+@pytest.mark.parametrize("seed", range(_OFF, _OFF + int(os.environ.get("FX_RANDOM_LARGE", "40"))))
 def test_random_large(ctx, oracle, seed):
     I, L, profile, groups, over = _large_case(seed)
     gp, op = fx.make_params(profile, **over), oparams(profile, **over)
@@ -166,7 +170,7 @@ BOUNDARY_WINDOWS = [(33, 40), (34, 40), (33, 41), (62, 64), (63, 64), (64, 64), 
 
 
 @pytest.mark.parametrize("wh", BOUNDARY_WINDOWS, ids=[f"{w}x{h}" for w, h in BOUNDARY_WINDOWS])
-@pytest.mark.parametrize("seed", range(int(os.environ.get("FX_RANDOM_BOUNDARY", "6"))))
+@pytest.mark.parametrize("seed", range(_OFF, _OFF + int(os.environ.get("FX_RANDOM_BOUNDARY", "6"))))
 def test_random_boundary_windows(ctx, oracle, wh, seed):
     """ROIs whose bounding box is exactly w x h: random fill (several components,
     holes) with pixels forced on all four box edges, placed at a random offset
@@ -198,7 +202,7 @@ def test_random_small_masks_edge_sets(ctx, oracle):
     every mask against the oracle (the edge set drives the edge statistics and
     the perimeter)."""
     n = int(os.environ.get("FX_RANDOM_SMALL", "2000"))
-    rng = np.random.default_rng(4242)
+    rng = np.random.default_rng(4242 + _OFF)
     pairs = []
     for _ in range(n):
         h, w = (int(v) for v in rng.integers(3, 13, 2))
