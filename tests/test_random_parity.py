@@ -220,3 +220,36 @@ def test_random_small_masks_edge_sets(ctx, oracle):
     for (I, L), (gl, gv) in zip(pairs, res):
         ol, ov = oracle.featurize(I, L, ALL, op)
         assert_parity(cols, gl, gv, ol, ov, I, L)
+
+
+@pytest.mark.parametrize("seed", range(_OFF, _OFF + int(os.environ.get("FX_RANDOM_ORIGIN", "30"))))
+def test_random_device_pitch_origin(ctx, oracle, seed):
+    """Device-resident rasters with a row pitch above the width and a tile origin:
+    the table equals the reference's on the tile placed at that origin of a larger
+    zero image (every coordinate column is global)."""
+    import torch
+    I, L, over = _case(seed)
+    rng = np.random.default_rng(9000 + seed)
+    h, w = L.shape
+    ox, oy = int(rng.integers(0, 200)), int(rng.integers(0, 200))
+    pitch = w + int(rng.integers(0, 40))
+    gp, op = fx.make_params("default", **over), oparams("default", **over)
+    cols = fx.feature_columns(ALL, gp)
+    dI = torch.zeros((h, pitch), dtype=torch.int16, device="cuda")
+    dL = torch.zeros((h, pitch), dtype=torch.int16, device="cuda")
+    dI[:, :w] = torch.from_numpy(I.view(np.int16)).cuda()
+    dL[:, :w] = torch.from_numpy(L.view(np.int16)).cuda()
+    dL[:, w:] = 5  # garbage past the width: never read
+    cap = int(np.count_nonzero(np.bincount(L.ravel(), minlength=65536)[1:])) + 1
+    ol_ = torch.empty(cap, dtype=torch.int32, device="cuda")
+    ov_ = torch.empty((cap, len(cols)), dtype=torch.float64, device="cuda")
+    n = ctx.featurize_device(dI.data_ptr(), dL.data_ptr(), w, h, pitch, fx.resolve_groups(ALL), gp,
+                             ol_.data_ptr(), ov_.data_ptr(), cap, origin=(ox, oy))
+    torch.cuda.synchronize()
+    gl = ol_[:n].cpu().numpy().view(np.uint32)
+    gv = ov_[:n].cpu().numpy()
+    Ib = np.zeros((h + oy, w + ox), np.uint16)
+    Lb = np.zeros((h + oy, w + ox), np.uint16)
+    Ib[oy:, ox:], Lb[oy:, ox:] = I, L
+    rl, rv = oracle.featurize(Ib, Lb, ALL, op)
+    assert_parity(cols, gl, gv, rl, rv, Ib, Lb)
