@@ -102,7 +102,7 @@ struct fx_ctx {
     uint32_t* h_band = nullptr;        // pinned mirror of d_band
     Control* d_band_ctl = nullptr;     // one control block per band
     Control* h_band_ctl = nullptr;     // pinned mirror (error flags)
-    uint32_t* d_band_seg = nullptr;    // band-major class lists [roi_cap]
+    uint32_t* d_band_seg = nullptr;    // class-major band lists [roi_cap] (band_range_lists)
     size_t band_seg_cap = 0;
     // whole slide over several devices (fx_multi_featurize_slide)
     unsigned long long* d_mcnt = nullptr;  // merged table scratch (slot-0 layout)
@@ -1034,6 +1034,31 @@ BandPlan band_plan(int band_rows, int h) {
     return bp;
 }
 
+// The ROI lists of bands [b0, b1] after k_band_scatter (class-major segments of
+// d_band_seg: class k's lists of bands 0..nb-1 are consecutive, so a run of bands
+// is one range per class); bc: the host copy of the counts for launch decisions.
+uint64_t band_range_lists(const fx_ctx* c, const uint32_t* h_cnt, int nb, int b0, int b1,
+                          const Control& hc, const RoiList& rl, Control& bc, RoiList& rb) {
+    bc = hc;
+    rb = rl;
+    size_t base = 0;
+    uint64_t total = 0;
+    for (int k = 0; k < kNumClasses; ++k) {
+        size_t before = 0, in = 0, all = 0;
+        for (int b = 0; b < nb; ++b) {
+            const uint32_t v = h_cnt[b * kNumClasses + k];
+            all += v;
+            if (b < b0) before += v;
+            else if (b <= b1) in += v;
+        }
+        rb.cls_list[k] = c->d_band_seg + base + before;
+        bc.class_count[k] = (uint32_t)in;
+        base += all;
+        total += in;
+    }
+    return total;
+}
+
 // Row blocks of the packed host path: each band cut into pieces of at most
 // kPackRows rows (a block never straddles a band, so a band's intensities are
 // complete once its last block has been unpacked).
@@ -1318,51 +1343,81 @@ int featurize_packed(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     const size_t ncols = (size_t)cfg.ncols;
     TmaSet tm;
     make_tmaps(c, d, &tm);
-    size_t rows_out = 0, seg_at = 0;
+    size_t rows_out = 0;
     int j = 0;
-    for (int b = 0; b < nb; ++b) {
-        // 2. this band's intensity blocks: ship, unpack
-        for (; j < NB && blk[j].band == b; ++j) {
-            const PackBlock& k = blk[j];
-            cudaEvent_t e = ev[2 * nb + NB + j];
-            if (!k.raw) {
-                spin(NB + j);
-                mark("intensity packed", j);
-                if (int_bytes[j]) {
-                    CK(cudaMemcpyAsync(c->d_pack + k.int_off, hp + k.int_off, int_bytes[j],
-                                       cudaMemcpyHostToDevice, c->copy2));
-                    c->h2d_bytes += int_bytes[j];
-                    CK(cudaEventRecord(e, c->copy2));
-                } else {
-                    if ((rc = raw_rows(im->intensity, const_cast<uint16_t*>(d.I), k))) return rc;
-                    CK(cudaEventRecord(e, c->copy));
-                }
+    // 2. ship and unpack one intensity block (waiting for its packing if needed)
+    auto ship_int = [&](int q) -> int {
+        const PackBlock& k = blk[q];
+        cudaEvent_t e = ev[2 * nb + NB + q];
+        if (!k.raw) {
+            spin(NB + q);
+            mark("intensity packed", q);
+            if (int_bytes[q]) {
+                CK(cudaMemcpyAsync(c->d_pack + k.int_off, hp + k.int_off, int_bytes[q],
+                                   cudaMemcpyHostToDevice, c->copy2));
+                c->h2d_bytes += int_bytes[q];
+                CK(cudaEventRecord(e, c->copy2));
+            } else {
+                int r2 = raw_rows(im->intensity, const_cast<uint16_t*>(d.I), k);
+                if (r2) return r2;
+                CK(cudaEventRecord(e, c->copy));
             }
-            CK(cudaStreamWaitEvent(s, e, 0));
-            if (int_bytes[j]) {
-                Launch l(c, "k_unpack_intensity");
-                k_unpack_intensity<<<dim3(pk_tiles(W), k.rows), 256, 0, s>>>(
-                    c->d_pack + k.int_off, k.rows, W, d.L + (size_t)k.y0 * P,
-                    const_cast<uint16_t*>(d.I) + (size_t)k.y0 * P, P);
-            }
+        }
+        CK(cudaStreamWaitEvent(s, e, 0));
+        if (int_bytes[q]) {
+            Launch l(c, "k_unpack_intensity");
+            k_unpack_intensity<<<dim3(pk_tiles(W), k.rows), 256, 0, s>>>(
+                c->d_pack + k.int_off, k.rows, W, d.L + (size_t)k.y0 * P,
+                const_cast<uint16_t*>(d.I) + (size_t)k.y0 * P, P);
+        }
+        return FX_OK;
+    };
+    // a band is ready when every one of its intensity blocks is packed (raw ones are
+    // queued from the start)
+    auto band_ready = [&](int bb, int from) -> bool {
+        for (int q = from; q < NB && blk[q].band == bb; ++q)
+            if (!blk[q].raw && !pool->done(NB + q)) return false;
+        return true;
+    };
+    for (int b = 0; b < nb;) {
+        // this band's blocks (waiting for them), then every following band whose blocks
+        // are already packed: one set of ROI launches for the run of bands (each band's
+        // launches have a fixed latency, and the packers often finish several at once)
+        for (; j < NB && blk[j].band == b; ++j)
+            if ((rc = ship_int(j))) return rc;
+        int b2 = b;
+        static const bool merge = !getenv("FXG_PACK_MERGE") || atoi(getenv("FXG_PACK_MERGE"));
+        while (merge && b2 + 1 < nb && band_ready(b2 + 1, j)) {
+            ++b2;
+            for (; j < NB && blk[j].band == b2; ++j)
+                if ((rc = ship_int(j))) return rc;
         }
         CK(cudaGetLastError());
-        dmark("band " + std::to_string(b) + " intensities unpacked", s);
-        Control bc = hc;
-        RoiList rb = rl;
-        uint64_t band_rois = 0;
-        for (int q = 0; q < kNumClasses; ++q) {
-            bc.class_count[q] = h_cnt[b * kNumClasses + q];
-            rb.cls_list[q] = c->d_band_seg + seg_at;
-            seg_at += bc.class_count[q];
-            band_rois += bc.class_count[q];
-        }
+        dmark("bands " + std::to_string(b) + "-" + std::to_string(b2) + " intensities unpacked", s);
+        Control bc;
+        RoiList rb;
+        const uint64_t band_rois = band_range_lists(c, h_cnt, nb, b, b2, hc, rl, bc, rb);
         if (band_rois) {
-            rc = roi_work(c, d, cfg, bc, tm, c->d_out, nullptr, kClassS0, c->d_band_ctl + b, rb,
+            Control* dctl = c->d_band_ctl + b;
+            if (b2 > b) {  // the run's own control block (as k_band_scatter builds a band's)
+                Control cb = hc;
+                for (int q = 0; q < kNumClasses; ++q) {
+                    cb.class_count[q] = bc.class_count[q];
+                    cb.class_next[q] = 0;
+                }
+                cb.overflow_count = cb.overflow_next = 0;
+                cb.t_next[0] = cb.t_next[1] = 0;
+                cb.mom_alloc = cb.int_alloc = 0;
+                cb.w_next = cb.b_next_big = 0;
+                cb.error = 0;
+                c->h_band_ctl[b] = cb;
+                CK(cudaMemcpyAsync(dctl, c->h_band_ctl + b, sizeof(Control), cudaMemcpyHostToDevice, s));
+            }
+            rc = roi_work(c, d, cfg, bc, tm, c->d_out, nullptr, kClassS0, dctl, rb,
                           wide ? &wcfg : nullptr, false);
             if (rc) return rc;
         }
-        const size_t upto = std::max<size_t>(rows_out, b == nb - 1 ? n : final_after[b]);
+        const size_t upto = std::max<size_t>(rows_out, b2 == nb - 1 ? n : final_after[b2]);
         if (upto > rows_out) {
             CK(cudaEventRecord(ev[nb + b], s));
             CK(cudaStreamWaitEvent(c->d2h, ev[nb + b], 0));
@@ -1371,8 +1426,9 @@ int featurize_packed(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
                                c->d2h));
             c->d2h_bytes += (upto - rows_out) * ncols * sizeof(double);
             rows_out = upto;
-            dmark("band " + std::to_string(b) + " rows back", c->d2h);
+            dmark("bands " + std::to_string(b) + "-" + std::to_string(b2) + " rows back", c->d2h);
         }
+        b = b2 + 1;
     }
     join.release();  // every block packed and shipped: the pool is free for other contexts
     CK(cudaMemcpyAsync(c->h_band_ctl, c->d_band_ctl, (size_t)nb * sizeof(Control),
@@ -1508,17 +1564,11 @@ int featurize_banded(fx_ctx* c, const fx_image* im, int band_rows, unsigned grou
     const size_t ncols = (size_t)cfg.ncols;
     TmaSet tm;
     make_tmaps(c, d, &tm);
-    size_t rows_out = 0, seg_at = 0;
+    size_t rows_out = 0;
     for (int b = 0; b < nb; ++b) {
-        Control bc = hc;  // host copy of the band's counts (launch decisions)
-        RoiList rb = rl;  // the band's lists: segments of d_band_seg
-        uint64_t band_rois = 0;
-        for (int k = 0; k < kNumClasses; ++k) {
-            bc.class_count[k] = h_cnt[b * kNumClasses + k];
-            rb.cls_list[k] = c->d_band_seg + seg_at;
-            seg_at += bc.class_count[k];
-            band_rois += bc.class_count[k];
-        }
+        Control bc;  // host copy of the band's counts (launch decisions)
+        RoiList rb;  // the band's lists: segments of d_band_seg
+        const uint64_t band_rois = band_range_lists(c, h_cnt, nb, b, b, hc, rl, bc, rb);
         CK(cudaStreamWaitEvent(s, ev[nb + b], 0));
         if (band_rois) {
             // (one stream per band: the serial passes' second stream only added

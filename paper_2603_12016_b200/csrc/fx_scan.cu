@@ -424,12 +424,13 @@ __global__ void k_band_scatter(RoiList rl, const Control* ctl, BandPlan bp, cons
                                uint32_t* cursor, uint32_t* seg, Control* band_ctl) {
     const uint32_t nb = bp.nb;
     __shared__ uint32_t off[kMaxBands * kNumClasses];
-    if (threadIdx.x == 0) {  // band-major, class-minor exclusive offsets (<= 256 entries)
-        uint32_t acc = 0;
-        for (uint32_t j = 0; j < nb * kNumClasses; ++j) {
-            off[j] = acc;
-            acc += cnt[j];
-        }
+    if (threadIdx.x == 0) {  // class-major exclusive offsets: off[k nb + b] (<= 256 entries),
+        uint32_t acc = 0;      // so a run of consecutive bands is one range per class
+        for (uint32_t k = 0; k < (uint32_t)kNumClasses; ++k)
+            for (uint32_t b = 0; b < nb; ++b) {
+                off[k * nb + b] = acc;
+                acc += cnt[b * kNumClasses + k];
+            }
     }
     __syncthreads();
     const uint32_t total = ctl->class_count[0] + ctl->class_count[1] + ctl->class_count[2] +
@@ -437,8 +438,7 @@ __global__ void k_band_scatter(RoiList rl, const Control* ctl, BandPlan bp, cons
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         uint32_t r, b, k;
         if (!band_item(rl, ctl, i, bp, r, b, k)) continue;
-        const uint32_t j = b * kNumClasses + k;
-        seg[off[j] + atomicAdd(&cursor[j], 1u)] = r;
+        seg[off[k * nb + b] + atomicAdd(&cursor[b * kNumClasses + k], 1u)] = r;
     }
     if (blockIdx.x == 0 && threadIdx.x < nb) {  // control block of each band
         Control c = *ctl;
