@@ -187,7 +187,7 @@ struct fx_ctx {
     // packed host rows (fx_pack.hpp): worker pool, pinned + device block staging,
     // the host's nonzero masks; FXG_PACK=0 / fx_ctx_set_packing(0) sends raw rows
     bool packing = true;
-    int pack_raw_pct = 20;  // FXG_PACK_RAW: % of row blocks sent raw (DMA next to the packers)
+    int pack_raw_pct = 25;  // FXG_PACK_RAW: % of row blocks sent raw (DMA next to the packers)
     uint8_t* h_pack = nullptr;
     // batch path: packed staging in two halves (by staging buffer); events: a half's
     // host-to-device copies done, its unpack kernels done; one per shipped block
