@@ -8,9 +8,11 @@ all through torch.distributed (NCCL on GPUs, gloo in the CPU tests):
    xmin/ymin = MIN, xmax/ymax = MAX  -- one all-reduce per array, 1.5 MB total,
    integer-exact, so the merged table is bit-identical to a whole-image scan;
 3. ownership: a ROI belongs to the band that holds its first row (ymin);
-4. halo: each rank needs the rows below its band up to the last row of its owned
-   ROIs; the rows are sent by the ranks that own them (send/recv of label and
-   intensity rows) -- only ROIs straddling a seam make a halo non-empty;
+4. halo: an owner needs, for each owned ROI that runs below its band, that ROI's
+   window columns in the rows below the band (halo_rects, the same plan on every
+   rank from the merged table); the ranks holding those rows send the rectangles,
+   one packed message per (source, owner) and raster -- only straddling windows
+   move, never whole rows, so a tall or slide-spanning ROI costs its own columns;
 5. each rank featurizes its owned ROIs on band + halo.  Non-mergeable statistics
    (order statistics, the contour edge set) need no merge: the owner holds the
    whole window.  Rows are therefore identical to a single-GPU featurize of the
@@ -56,6 +58,25 @@ def halo_transfers(bands, needs):
     return out
 
 
+def halo_rects(cnt, bbox, bands):
+    """(dst, src, row_lo, row_hi, x_lo, x_hi) for every owned ROI that runs below its
+    owner's band: its window columns in the rows below, split by the bands holding
+    them.  Ordered by owner, label, source: every rank derives the same list."""
+    cnt, bbox = np.asarray(cnt), np.asarray(bbox)
+    xmin, ymin, xmax, ymax = (bbox[i].astype(np.int64) for i in range(4))
+    present = cnt > 0
+    out = []
+    for dst, (b0, b1) in enumerate(bands):
+        own = np.nonzero(present & (ymin >= b0) & (ymin < b1) & (ymax >= b1))[0]
+        for lab in own:
+            lo, hi = b1, int(ymax[lab]) + 1
+            for src, (s0, s1) in enumerate(bands):
+                a, b = max(lo, s0), min(hi, s1)
+                if a < b:
+                    out.append((dst, src, a, b, int(xmin[lab]), int(xmax[lab]) + 1))
+    return out
+
+
 def merge_tables(dist, cnt, bbox):
     """All-reduce of the partial label tables (torch tensors, int64):
     cnt [65536] SUM; bbox [4, 65536] = xmin, ymin (MIN), xmax, ymax (MAX)."""
@@ -81,35 +102,46 @@ def featurize_band(backend, dist, rank, world, band_intensity, band_labels, y0, 
     cnt, bbox = backend.scan(band_intensity, band_labels, y0)
     cnt, bbox = merge_tables(dist, cnt, bbox)
     backend.set_table(cnt, bbox)
-    # 3-4: halo plan from the merged table (needs on the host: 1.5 MB)
+    # 3-4: halo plan from the merged table (on the host: 1.5 MB), identical on every rank
     hc, hb = cnt.cpu().numpy(), bbox.cpu().numpy()
-    need = owned_need(hc, hb, y0, y1)
-    needs_t = backend.tensor([need])
-    gathered = [backend.tensor([0]) for _ in range(world)]
-    dist.all_gather(gathered, needs_t)
-    needs = [int(t.item()) for t in gathered]
-    plan = halo_transfers(bands, needs)
-    ext_rows = (y1 - y0) + needs[rank]
+    rects = halo_rects(hc, hb, bands)
+    need = max([r[3] - y1 for r in rects if r[0] == rank], default=0)
+    ext_rows = (y1 - y0) + need
     ext_I = backend.empty_rows(ext_rows, width)
     ext_L = backend.empty_rows(ext_rows, width)
     ext_I[: y1 - y0] = band_intensity
     ext_L[: y1 - y0] = band_labels
-    ops = []
+    ext_I[y1 - y0:] = 0  # outside the rectangles: no pixel of any owned ROI
+    ext_L[y1 - y0:] = 0
+    ops, recvs = [], []
     # rows travel as bytes: NCCL has no 16-bit integer type (torch's NCCL type map
     # lacks int16), so the uint16 rasters are viewed as uint8 on both sides
     as_bytes = lambda t: t.contiguous().view(torch.uint8)
-    for src, dst, a, b in plan:
-        if src == dst:
+    for other in range(world):
+        if other == rank:
             continue
-        if src == rank:  # send my rows [a, b)
-            ops.append(dist.P2POp(dist.isend, as_bytes(band_intensity[a - y0:b - y0]), dst))
-            ops.append(dist.P2POp(dist.isend, as_bytes(band_labels[a - y0:b - y0]), dst))
-        if dst == rank:  # row slices of the contiguous extended rasters: byte views alias them
-            ops.append(dist.P2POp(dist.irecv, ext_I[a - y0:b - y0].view(torch.uint8), src))
-            ops.append(dist.P2POp(dist.irecv, ext_L[a - y0:b - y0].view(torch.uint8), src))
+        out_r = [r for r in rects if r[1] == rank and r[0] == other]
+        if out_r:  # my rows of the owner's straddling windows, one message per raster
+            for band in (band_intensity, band_labels):
+                parts = [band[a - y0:b - y0, xl:xh].reshape(-1) for _, _, a, b, xl, xh in out_r]
+                ops.append(dist.P2POp(dist.isend, as_bytes(torch.cat(parts)), other))
+        in_r = [r for r in rects if r[0] == rank and r[1] == other]
+        if in_r:
+            total = sum((b - a) * (xh - xl) for _, _, a, b, xl, xh in in_r)
+            bufs = [backend.empty_flat(total), backend.empty_flat(total)]
+            for buf in bufs:
+                ops.append(dist.P2POp(dist.irecv, buf.view(torch.uint8), other))
+            recvs.append((in_r, bufs))
     if ops:
         for req in dist.batch_isend_irecv(ops):
             req.wait()
+    for in_r, (bI, bL) in recvs:  # the rectangles into the extended rasters
+        at = 0
+        for _, _, a, b, xl, xh in in_r:
+            k = (b - a) * (xh - xl)
+            ext_I[a - y0:b - y0, xl:xh] = bI[at:at + k].view(b - a, xh - xl)
+            ext_L[a - y0:b - y0, xl:xh] = bL[at:at + k].view(b - a, xh - xl)
+            at += k
     # 5: featurize owned ROIs on band + halo
     return backend.featurize_owned(ext_I, ext_L, y0, y0, y1)
 
@@ -131,6 +163,9 @@ class DeviceBackend:
 
     def empty_rows(self, rows, width):
         return self.torch.empty((rows, width), dtype=self.torch.int16, device="cuda")
+
+    def empty_flat(self, n):
+        return self.torch.empty(n, dtype=self.torch.int16, device="cuda")
 
     def _image(self, I, L, oy):
         h, w = L.shape

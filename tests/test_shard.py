@@ -49,6 +49,9 @@ class OracleBackend:
     def empty_rows(self, rows, width):
         return torch.zeros((rows, width), dtype=torch.int16)
 
+    def empty_flat(self, n):
+        return torch.zeros(n, dtype=torch.int16)
+
     def scan(self, I, L, oy):
         lab = L.numpy().view(np.uint16)
         cnt = np.zeros(65536, np.int64)
@@ -74,6 +77,21 @@ class OracleBackend:
             assert len(ys) == self.cnt[l], "halo must hold the whole owned ROI"
             rows.append(self.o.roi_features(xs, ys + oy, img[ys, xs], GROUPS, self.params))
         return torch.tensor(own, dtype=torch.int64), torch.tensor(np.array(rows).reshape(len(own), -1))
+
+
+def test_halo_rects_only_straddling_columns():
+    """A tall ROI owned by band 0 moves only its own columns of bands 1-2; an ROI
+    inside its band moves nothing (no full-width halo rows)."""
+    from paper_2603_12016_b200 import shard
+    bands = shard.band_plan(100, 4)
+    cnt = np.zeros(65536, np.int64)
+    bbox = np.zeros((4, 65536), np.int64)
+    bbox[:2] = 0xFFFFFFFF
+    for lab, (x0, y0, x1, y1) in {7: (10, 3, 19, 70), 9: (40, 30, 60, 45), 11: (0, 60, 99, 80)}.items():
+        cnt[lab] = 5
+        bbox[:, lab] = (x0, y0, x1, y1)
+    rects = shard.halo_rects(cnt, bbox, bands)
+    assert rects == [(0, 1, 25, 50, 10, 20), (0, 2, 50, 71, 10, 20), (2, 3, 75, 81, 0, 100)]
 
 
 def _worker(rank, world, port, q):
