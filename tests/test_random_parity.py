@@ -253,3 +253,20 @@ def test_random_device_pitch_origin(ctx, oracle, seed):
     Ib[oy:, ox:], Lb[oy:, ox:] = I, L
     rl, rv = oracle.featurize(Ib, Lb, ALL, op)
     assert_parity(cols, gl, gv, rl, rv, Ib, Lb)
+
+
+@pytest.mark.parametrize("offset", [0, 1, 4, 5, 7, 8, 9, 15, 16, 17, 31, 32, 33, 40, 63, 64, 65, 100, 300])
+def test_glcm_offsets_up_to_beyond_windows(ctx, oracle, offset):
+    """GLCM offsets from 1 to beyond every window (no pair at all for most ROIs),
+    small and large windows, symmetric and not, all angles."""
+    rng = np.random.default_rng(offset)
+    L = inputs.random_blobs((150, 170), 30, seed=offset, max_r=int(rng.integers(4, 40)))
+    L[140:, :] = np.where(L[140:, :] > 0, L[140:, :], 0)
+    I = rng.integers(0, int(rng.choice([5, 70, 65536])), L.shape).astype(np.uint16)
+    for sym in (True, False):
+        over = dict(ng=int(rng.choice([8, 64, 256, 300])), offset=offset, angles=(0, 45, 90, 135),
+                    symmetric=sym)
+        gp, op = fx.make_params("default", **over), oparams("default", **over)
+        gl, gv = ctx.featurize(I, L, ["glcm"], gp)
+        ol, ov = oracle.featurize(I, L, ["glcm"], op)
+        assert_parity(fx.feature_columns(["glcm"], gp), gl, gv, ol, ov, I, L)
