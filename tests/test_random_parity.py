@@ -270,3 +270,24 @@ def test_glcm_offsets_up_to_beyond_windows(ctx, oracle, offset):
         gl, gv = ctx.featurize(I, L, ["glcm"], gp)
         ol, ov = oracle.featurize(I, L, ["glcm"], op)
         assert_parity(fx.feature_columns(["glcm"], gp), gl, gv, ol, ov, I, L)
+
+
+def test_every_label_value_present(ctx, oracle):
+    """(Nearly) all 65,535 label values in one image: the label table's full range,
+    ROIs of 1-4 pixels, labels in random order; every group against the oracle."""
+    rng = np.random.default_rng(65535)
+    # 2 x 2 cells of a 256 x 256 grid, labels in random order, one cell empty; some
+    # cells lose pixels (ROIs of 1-4 pixels, diagonal-only contacts)
+    grid = np.zeros(65536, np.uint16)
+    grid[rng.permutation(65536)[:65535]] = np.arange(1, 65536, dtype=np.uint16)
+    L = np.kron(grid.reshape(256, 256), np.ones((2, 2), np.uint16)).astype(np.uint16)
+    L[rng.random(L.shape) < 0.2] = 0
+    for lab in (1, 65535, 40000):  # keep a few labels present for the count check
+        ys, xs = np.nonzero(np.kron(grid.reshape(256, 256) == lab, np.ones((2, 2), bool)))
+        L[ys[0], xs[0]] = lab
+    I = rng.integers(0, 65536, L.shape).astype(np.uint16)
+    p, op = fx.make_params("default"), oparams("default")
+    gl, gv = ctx.featurize(I, L, ALL, p)
+    ol, ov = oracle.featurize(I, L, ALL, op)
+    assert len(gl) == len(np.unique(L)) - 1 > 60000
+    assert_parity(fx.feature_columns(ALL, p), gl, gv, ol, ov, I, L)
