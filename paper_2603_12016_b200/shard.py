@@ -5,8 +5,9 @@ all through torch.distributed (NCCL on GPUs, gloo in the CPU tests):
 
 1. local label scan of the own band into a label table in global coordinates;
 2. merge of the partial tables (the mergeable accumulators): count = SUM,
-   xmin/ymin = MIN, xmax/ymax = MAX  -- one all-reduce per array, 1.5 MB total,
-   integer-exact, so the merged table is bit-identical to a whole-image scan;
+   xmin/ymin = MIN, xmax/ymax = MAX -- the present labels' records all-gathered
+   when the bands hold few labels, else a dense all-reduce per array; integer-
+   exact, so the merged table is bit-identical to a whole-image scan;
 3. ownership: a ROI belongs to the band that holds its first row (ymin);
 4. halo: an owner needs, for each owned ROI that runs below its band, that ROI's
    window columns in the rows below the band (halo_rects, the same plan on every
@@ -58,6 +59,10 @@ def halo_transfers(bands, needs):
     return out
 
 
+def len_world(dist):
+    return dist.get_world_size()
+
+
 def halo_rects(cnt, bbox, bands):
     """(dst, src, row_lo, row_hi, x_lo, x_hi) for every owned ROI that runs below its
     owner's band: its window columns in the rows below, split by the bands holding
@@ -78,8 +83,34 @@ def halo_rects(cnt, bbox, bands):
 
 
 def merge_tables(dist, cnt, bbox):
-    """All-reduce of the partial label tables (torch tensors, int64):
-    cnt [65536] SUM; bbox [4, 65536] = xmin, ymin (MIN), xmax, ymax (MAX)."""
+    """Merge of the partial label tables (torch tensors, int64): cnt [65536] SUM;
+    bbox [4, 65536] = xmin, ymin (MIN), xmax, ymax (MAX).  A band holding few
+    labels sends only its present labels' records (label, count, box: 48 B each,
+    all-gathered); a band holding many all-reduces the dense arrays (2.5 MB).
+    Integer-exact either way: the merged table is identical."""
+    import torch
+    k = int((cnt > 0).sum().item())
+    ks = [torch.zeros(1, dtype=torch.int64, device=cnt.device) for _ in range(len_world(dist))]
+    dist.all_gather(ks, torch.tensor([k], dtype=torch.int64, device=cnt.device))
+    kmax = max(int(t.item()) for t in ks)
+    if kmax * 6 * 8 * len(ks) < 3 * NL * 8:  # sparse records beat the dense all-reduce
+        labs = torch.nonzero(cnt > 0).squeeze(1)
+        rec = torch.full((kmax, 6), -1, dtype=torch.int64, device=cnt.device)
+        rec[:k, 0] = labs
+        rec[:k, 1] = cnt[labs]
+        rec[:k, 2:] = bbox[:, labs].t()
+        recs = [torch.empty_like(rec) for _ in ks]
+        dist.all_gather(recs, rec)
+        allr = torch.cat(recs)
+        allr = allr[allr[:, 0] >= 0]
+        lab = allr[:, 0]
+        cnt = torch.zeros(NL, dtype=torch.int64, device=cnt.device).index_add_(0, lab, allr[:, 1])
+        mins = torch.full((2, NL), SENT, dtype=torch.int64, device=cnt.device)
+        maxs = torch.zeros((2, NL), dtype=torch.int64, device=cnt.device)
+        for r in range(2):
+            mins[r].scatter_reduce_(0, lab, allr[:, 2 + r], reduce="amin", include_self=True)
+            maxs[r].scatter_reduce_(0, lab, allr[:, 4 + r], reduce="amax", include_self=True)
+        return cnt, torch.cat([mins, maxs])
     dist.all_reduce(cnt, op=dist.ReduceOp.SUM)
     mins, maxs = bbox[:2].contiguous(), bbox[2:].contiguous()
     dist.all_reduce(mins, op=dist.ReduceOp.MIN)

@@ -136,6 +136,51 @@ def test_gloo_band_sharding_matches_whole_image(oracle, world):
     assert np.array_equal(values[order], ov)
 
 
+def _merge_worker(rank, world, port, q):
+    sys.path.insert(0, ROOT)
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2603_12016_b200 import shard
+    out = []
+    for n_labels in (50, 30000):  # sparse records, then the dense all-reduce
+        rng = np.random.default_rng(1000 * rank + n_labels)
+        cnt = np.zeros(65536, np.int64)
+        bbox = np.zeros((4, 65536), np.int64)
+        bbox[:2] = 0xFFFFFFFF
+        labs = rng.choice(np.arange(1, 65536), n_labels, replace=False)
+        cnt[labs] = rng.integers(1, 1000, n_labels)
+        lo = rng.integers(0, 5000, (2, n_labels))
+        bbox[:2, labs] = lo
+        bbox[2:, labs] = lo + rng.integers(0, 100, (2, n_labels))
+        c, b = shard.merge_tables(dist, torch.from_numpy(cnt.copy()), torch.from_numpy(bbox.copy()))
+        rc, rb = torch.from_numpy(cnt.copy()), torch.from_numpy(bbox.copy())
+        dist.all_reduce(rc, op=dist.ReduceOp.SUM)
+        mins, maxs = rb[:2].contiguous(), rb[2:].contiguous()
+        dist.all_reduce(mins, op=dist.ReduceOp.MIN)
+        dist.all_reduce(maxs, op=dist.ReduceOp.MAX)
+        out.append(bool(torch.equal(c, rc)) and bool(torch.equal(b, torch.cat([mins, maxs]))))
+    q.put((rank, out))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_merge_tables_sparse_and_dense_agree():
+    """The label-table merge: present-label records (few labels) and the dense
+    all-reduce (many) give the identical merged table on every rank."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 29700 + os.getpid() % 1000
+    procs = [ctx.Process(target=_merge_worker, args=(r, 3, port, q)) for r in range(3)]
+    for p in procs:
+        p.start()
+    res = [q.get(timeout=300) for _ in range(3)]
+    for p in procs:
+        p.join(60)
+        assert p.exitcode == 0
+    assert all(all(r[1]) for r in res), res
+
+
 def test_halo_plan():
     from paper_2603_12016_b200 import shard
     bands = shard.band_plan(100, 4)
@@ -285,6 +330,10 @@ class StagedDist:
             self.op, self.tensor, self.peer = op, tensor, peer
 
     isend, irecv = "isend", "irecv"
+
+    @staticmethod
+    def get_world_size():
+        return dist.get_world_size()
 
     @staticmethod
     def all_reduce(t, op=dist.ReduceOp.SUM):
